@@ -1,0 +1,313 @@
+"""Oracle solvers — TEST INFRASTRUCTURE ONLY.
+
+numpy/scipy restatement of the reference's solver path (file:line in each
+docstring refers to /root/reference/pkg/src/rbws).  Used by tests as the
+checker and by bench.py as the timed CPU baseline; never by the product.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from typing import Callable, Sequence
+
+import numpy as np
+import scipy.linalg as sla
+import scipy.sparse as sp
+
+JACOBI_OMEGA = 0.7   # multigrid.py:367
+
+
+class OperatorError(Exception):
+    pass
+
+
+class DegenerateBasisError(Exception):
+    pass
+
+
+# ----------------------------------------------------------------- grid / MG
+
+def galerkin(A_fine, P) -> sp.csr_matrix:
+    """P^T A P (grid.py:201-209)."""
+    A_fine = sp.csr_matrix(A_fine)
+    P = sp.csr_matrix(P)
+    if A_fine.shape[1] != P.shape[0]:
+        raise ValueError("incompatible shapes for coarsening")
+    return (P.T @ (A_fine @ P)).tocsr()
+
+
+def jacobi_sweep(A, diag, x, b, omega=JACOBI_OMEGA):
+    """One damped Jacobi sweep x + omega (b - A x)/diag (kernels.py:98-115)."""
+    return x + omega * (b - A @ x) / diag
+
+
+@dataclass
+class OracleMgContext:
+    """Per-parameter V-cycle data (multigrid.py:455-468, 493-507)."""
+
+    operators: list
+    prolongations: list
+    diags: list
+    nu: int
+    coarse_factor: tuple
+    omega: float = JACOBI_OMEGA
+
+    @property
+    def levels(self):
+        return len(self.operators)
+
+
+def mg_context_for(problem, mu, nu: int = 1, omega: float = JACOBI_OMEGA) -> OracleMgContext:
+    """Operators per level from the affine terms + Cholesky of level 0 (multigrid.py:530-541)."""
+    if nu < 0:
+        raise ValueError("smoothing count must be non-negative")
+    ops = [problem.operator(mu, level=i) for i in range(problem.levels)]
+    try:
+        cf = sla.cho_factor(ops[0].toarray())
+    except sla.LinAlgError as exc:
+        raise OperatorError(f"coarsest operator not SPD: {exc}") from exc
+    diags = [A.diagonal().copy() for A in ops]
+    for d in diags[1:]:
+        if np.any(d == 0.0):
+            raise ValueError("zero diagonal entry; point smoothing undefined")
+    return OracleMgContext(ops, list(problem.prolongations), diags, nu, cf, omega)
+
+
+def mg_vcycle(b, ctx: OracleMgContext, level=None) -> np.ndarray:
+    """One V-cycle from zero (multigrid.py:544-561) with Jacobi pre/post sweeps."""
+    if level is None:
+        level = ctx.levels - 1
+    b = np.asarray(b, dtype=np.float64)
+    if level == 0:
+        return sla.cho_solve(ctx.coarse_factor, b)
+    A, d = ctx.operators[level], ctx.diags[level]
+    P = ctx.prolongations[level - 1]
+    u = np.zeros_like(b)
+    for _ in range(ctx.nu):
+        u = jacobi_sweep(A, d, u, b, ctx.omega)
+    r = b - A @ u
+    e = mg_vcycle(P.T @ r, ctx, level - 1)
+    u = u + P @ e
+    for _ in range(ctx.nu):
+        u = jacobi_sweep(A, d, u, b, ctx.omega)
+    return u
+
+
+# ---------------------------------------------------------------------- PCG
+
+@dataclass
+class SolveReport:
+    """Convergence record (krylov.py:250-264)."""
+
+    method: str
+    iterations: int
+    history: list
+    converged: bool
+    true_residual: float
+    wall_time: float
+    delta: float
+    l_max: int
+    mu: np.ndarray | None = None
+    absolute_norms: bool = False
+    config: dict = field(default_factory=dict)
+
+
+def pcg_solve(A, f, x0, precond=None, delta=1e-16, l_max=40, method="pcg", mu=None):
+    """Preconditioned CG, recurrence residual drives the loop (krylov.py:267-334)."""
+    if delta <= 0:
+        raise ValueError("tolerance must be positive")
+    if l_max < 0:
+        raise ValueError("l_max must be non-negative")
+    t0 = time.perf_counter()
+    f = np.asarray(f, dtype=np.float64)
+    x = np.array(x0, dtype=np.float64, copy=True)
+    fn = np.linalg.norm(f)
+    absolute = fn == 0.0
+    scale = 1.0 if absolute else fn
+    prec = (lambda r, k: r.copy()) if precond is None else precond
+    r = f - A @ x
+    hist = [float(np.linalg.norm(r) / scale)]
+    k = 0
+    if hist[0] > delta and l_max > 0:
+        s = prec(r, 0)
+        p = s.copy()
+        rs = float(r @ s)
+        while k < l_max:
+            q = A @ p
+            pq = float(p @ q)
+            if pq <= 0.0:
+                raise OperatorError(f"non-positive curvature p.A.p = {pq:g}; operator not SPD")
+            alpha = rs / pq
+            x += alpha * p
+            r -= alpha * q
+            k += 1
+            rel = float(np.linalg.norm(r) / scale)
+            hist.append(rel)
+            if rel <= delta:
+                break
+            s = prec(r, k)
+            rs_new = float(r @ s)
+            beta = rs_new / rs
+            p = s + beta * p
+            rs = rs_new
+    tr = float(np.linalg.norm(f - A @ x) / scale)
+    return x, SolveReport(method, k, hist, tr <= delta, tr, time.perf_counter() - t0,
+                          delta, l_max, None if mu is None else np.asarray(mu, float), absolute)
+
+
+def mgcg_solve(A, f, x0, ctx, delta=1e-16, l_max=40, mu=None, method="mgcg"):
+    """PCG with one V-cycle per application (multigrid.py:564-571)."""
+    return pcg_solve(A, f, x0, lambda r, k: mg_vcycle(r, ctx), delta, l_max, method, mu)
+
+
+# ------------------------------------------------------------------- L1ROC
+
+def deim_extend(W, X, v, exclude=None):
+    """Interpolatory basis extension (rb.py:96-126).
+
+    Returns (column, index, coeffs, pivot).
+    """
+    v = np.asarray(v, dtype=np.float64)
+    W = np.zeros((len(v), 0)) if W is None else np.asarray(W)
+    X = list(X)
+    if W.shape[1] != len(X):
+        raise ValueError("basis width and point count differ")
+    if W.shape[1] == 0:
+        c = np.zeros(0)
+        rho = v.copy()
+    else:
+        c = np.linalg.solve(W[X, :], v[X])
+        rho = v - W @ c
+    if np.max(np.abs(rho)) <= 1e-14 * max(np.max(np.abs(v)), 1e-300):
+        raise DegenerateBasisError("snapshot numerically inside the current basis")
+    mag = np.abs(rho)
+    if exclude:
+        mag = mag.copy()
+        mag[list(exclude)] = -1.0
+    idx = int(np.argmax(mag))
+    piv = rho[idx]
+    if piv == 0.0:
+        raise DegenerateBasisError("residual vanishes at all admissible points")
+    return rho / piv, idx, c, piv
+
+
+def l1_indicator(c) -> float:
+    """||c||_1 (rb.py:129-131)."""
+    return float(np.sum(np.abs(np.asarray(c))))
+
+
+def _lstsq(B, b):
+    """Least squares with rank check (rb.py:182-187)."""
+    a, _, rank, _ = np.linalg.lstsq(B, b, rcond=None)
+    if rank < B.shape[1]:
+        raise DegenerateBasisError("sub-sampled reduced system is rank deficient")
+    return a
+
+
+@dataclass(frozen=True)
+class OracleL1rocModel:
+    """Trained over-collocation model (rb.py:134-175)."""
+
+    basis: np.ndarray
+    transform: np.ndarray
+    collocation: np.ndarray
+    solution_points: np.ndarray
+    residual_points: np.ndarray
+    chosen: np.ndarray          # indices into the training list
+    indicator_history: np.ndarray
+    saturated: bool = False
+
+    @property
+    def dim(self):
+        return self.basis.shape[1]
+
+    def prefix(self, N):
+        if not 1 <= N <= self.dim:
+            raise ValueError("prefix dimension outside model")
+        return OracleL1rocModel(self.basis[:, :N], self.transform[:N, :N],
+                                self.collocation[:2 * N - 1], self.solution_points[:N],
+                                self.residual_points[:N - 1], self.chosen[:N],
+                                self.indicator_history[:N], self.saturated)
+
+
+def l1roc_online(model: OracleL1rocModel, A, b):
+    """Sub-sampled least-squares reduced solve (rb.py:190-205)."""
+    if model.dim == 0:
+        raise ValueError("empty model")
+    rows = model.collocation
+    R = A(rows) if callable(A) else A[rows, :]
+    B = np.asarray(R @ model.basis)
+    a = _lstsq(B, np.asarray(b, dtype=np.float64)[rows])
+    return model.basis @ a, sla.solve_triangular(model.transform, a, lower=False), a
+
+
+def l1roc_offline(mus, N, hf_solve, operator, operator_rows, rhs, seed=0):
+    """Greedy over-collocation training (rb.py:208-293)."""
+    mus = [np.asarray(m, dtype=np.float64) for m in mus]
+    if not 1 <= N <= len(mus):
+        raise ValueError("need 1 <= N <= number of training parameters")
+    first = int(np.random.default_rng(seed).integers(len(mus)))
+    rhss = [rhs(m) for m in mus]
+    n_h = len(rhss[0])
+    col, idx, _, piv = deim_extend(None, [], hf_solve(mus[first]))
+    W = col[:, None]
+    T = np.array([[piv]])
+    xs, xr, xi = [idx], [], [idx]
+    chosen = [first]
+    R = np.zeros((n_h, 0))
+    hist = [1.0]
+    saturated = False
+    sampled = [operator_rows(m, xi) for m in mus]
+    for _n in range(2, N + 1):
+        taken = set(xs) | set(xr)
+        ind = np.empty(len(mus))
+        coeffs = []
+        for j in range(len(mus)):
+            a = _lstsq(np.asarray(sampled[j] @ W), rhss[j][xi])
+            coeffs.append(a)
+            ind[j] = l1_indicator(sla.solve_triangular(T, a, lower=False))
+        pick = int(np.argmax(ind))
+        hist.append(float(ind[pick]))
+        if pick in chosen:
+            saturated = True
+            break
+        chosen.append(pick)
+        col, idx, c, piv = deim_extend(W, xs, hf_solve(mus[pick]), exclude=taken)
+        taken.add(idx)
+        T = np.block([[T, c[:, None]], [np.zeros((1, T.shape[1])), np.array([[piv]])]])
+        W = np.column_stack([W, col])
+        xs.append(idx)
+        r = rhss[pick] - operator(mus[pick]) @ (W[:, :-1] @ coeffs[pick])
+        rcol, ridx, _, _ = deim_extend(R, xr, r, exclude=taken)
+        R = np.column_stack([R, rcol])
+        xr.append(ridx)
+        xi.extend([idx, ridx])
+        for j, m in enumerate(mus):
+            sampled[j] = sp.vstack([sampled[j], operator_rows(m, xi[-2:])]).tocsr()
+    return OracleL1rocModel(W, T, np.asarray(xi, np.int64), np.asarray(xs, np.int64),
+                            np.asarray(xr, np.int64), np.asarray(chosen, np.int64),
+                            np.asarray(hist), saturated)
+
+
+def rbi_mgcg_solve(problem, mu, model, delta=1e-10, l_max=40, nu=1):
+    """RBI-MGCG: L1ROC warm start then MGCG (warmstart.py:364-410, experiment.py:149-157)."""
+    A, f = problem.operator(mu), problem.rhs(mu)
+    ctx = mg_context_for(problem, mu, nu=nu)
+    u0 = np.zeros_like(f) if model is None else l1roc_online(model, A, f)[0]
+    return mgcg_solve(A, f, u0, ctx, delta, l_max, mu,
+                      "mgcg" if model is None else "rbi-mgcg")
+
+
+def lhs_sample(p, n, bounds, seed=0):
+    """Seeded Latin hypercube (sampling.py:478-497)."""
+    if n < 1:
+        raise ValueError("need at least one sample")
+    bounds = np.asarray(bounds, dtype=np.float64)
+    lo, hi = bounds[:, 0], bounds[:, 1]
+    if np.any(hi <= lo):
+        raise ValueError("degenerate bounds")
+    rng = np.random.default_rng(seed)
+    u = (rng.random((n, p)) + np.stack([rng.permutation(n) for _ in range(p)], axis=1)) / n
+    pts = lo + u * (hi - lo)
+    return [pts[i].copy() for i in range(n)]

@@ -1,0 +1,201 @@
+"""Generate golden vectors by running the REAL reference package.
+
+Run in the build container (needs /root/reference; never on the GPU box):
+
+    python tests/golden/make_golden.py
+
+The reference (``/root/reference/pkg``) is copied to /tmp and its Cython
+smoother extension built in place (reference setup.py), so the reference's
+default compiled backend is the one exercised.  The BASELINE problems are
+finite-volume operators the reference cannot assemble itself; they are fed
+through the reference's own ``ProblemSpec``/``ParametricProblem`` API by
+substituting its two assembly hooks (``grid.assemble_stiffness_kernel`` and
+``grid.assemble_load``) with the oracle's FV term matrices.  Everything after
+assembly — free-DoF slicing, prolongations, Galerkin coarsening
+(grid.py:231-262), ``mg_context_for``/``mg_vcycle``/``mgcg_solve``
+(multigrid.py), ``pcg_solve`` (krylov.py), ``l1roc_offline``/``l1roc_online``
+(rb.py), ``HighFidelitySolver`` (hf.py) — is the unmodified reference code.
+
+Outputs ``tests/golden/golden_fd.npz`` (small cases only).
+"""
+
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parents[2]
+REF = Path("/root/reference/pkg")
+BUILD = Path("/tmp/rbws_ref_golden")
+
+
+def _import_reference():
+    if not (BUILD / "src/rbws").exists():
+        shutil.copytree(REF, BUILD)
+    if not list((BUILD / "src/rbws").glob("_smoothers*.so")):
+        subprocess.run([sys.executable, "setup.py", "build_ext", "--inplace"],
+                       cwd=BUILD, check=True, capture_output=True)
+    sys.path.insert(0, str(BUILD / "src"))
+    os.environ.pop("RBWS_KERNELS", None)
+    import rbws
+    assert rbws.BACKEND == "cython", rbws.BACKEND
+    return rbws
+
+
+class _FDKernel:
+    """Marker standing in for a coefficient callable; carries (spec, q)."""
+
+    def __init__(self, spec, q):
+        self.spec, self.q = spec, q
+
+    def __call__(self, x, y, z):  # pragma: no cover - never evaluated
+        raise RuntimeError("FD terms are injected, not quadrature-assembled")
+
+
+def reference_problem(rbws, fdspec, n, m0=4):
+    """Build the reference ParametricProblem for an FD spec via its own API."""
+    sys.path.insert(0, str(REPO))
+    from oracle import problems as op
+    import rbws.grid as rg
+    from rbws.problems import DiffusionTerm, ProblemSpec
+
+    terms = []
+    for q in range(fdspec.n_terms):
+        if fdspec.kind == "thermal-block":
+            theta = (lambda mu, q=q: mu[q])
+        else:
+            theta = (lambda mu, q=q: 1.0 if q == 0 else mu[q - 1])
+        terms.append(DiffusionTerm(theta=theta, kernel=_FDKernel(fdspec, q)))
+    spec = ProblemSpec(pid=fdspec.pid, p=fdspec.p, bounds=np.asarray(fdspec.bounds),
+                       diffusion_terms=tuple(terms),
+                       source=lambda x, y, z, mu: np.zeros(np.broadcast(x, y, z).shape),
+                       dirichlet=lambda x, y, z, mu: np.zeros(np.broadcast(x, y, z).shape),
+                       source_mu_dependent=False)
+
+    orig_k, orig_l = rg.assemble_stiffness_kernel, rg.assemble_load
+
+    def fd_stiffness(nn, kernel, aniso=(1.0, 1.0, 1.0)):
+        return op.assemble_term_full(kernel.spec, nn, kernel.q)
+
+    def fd_load(nn, source, mu):
+        return op.rhs_full(fdspec, nn)
+
+    rg.assemble_stiffness_kernel, rg.assemble_load = fd_stiffness, fd_load
+    try:
+        levels = int(np.log2(n // m0)) + 1
+        prob = rg.ParametricProblem(spec, levels=levels, m0=m0)
+        prob.rhs(np.asarray([b[0] for b in fdspec.bounds]))  # populate cached load
+    finally:
+        rg.assemble_stiffness_kernel, rg.assemble_load = orig_k, orig_l
+    return prob
+
+
+def main():
+    rbws = _import_reference()
+    sys.path.insert(0, str(REPO))
+    from oracle import problems as op
+    from rbws.hf import HighFidelitySolver
+    from rbws.multigrid import mg_context_for, mg_vcycle, mgcg_solve
+    from rbws.rb import l1roc_offline
+    from rbws.warmstart import MethodConfig, rbi_pcg_solve
+
+    out = {}
+
+    # 1. operators on every level (thermal block 2x1x1, n=8, m0=2 -> 3 levels)
+    tb = op.thermal_block((2, 1, 1))
+    prob = reference_problem(rbws, tb, 8, m0=2)
+    mu = np.array([0.37, 4.2])
+    for lvl in range(prob.mesh.levels):
+        A = prob.operator(mu, level=lvl).toarray()
+        out[f"ops_tb211_n8_l{lvl}"] = A
+    out["ops_tb211_n8_mu"] = mu
+    out["ops_tb211_n8_rhs"] = prob.rhs(mu)
+
+    # 2. single V-cycle application on a seeded vector (thermal 2x2x1, n=16)
+    tb4 = op.thermal_block((2, 2, 1))
+    prob16 = reference_problem(rbws, tb4, 16, m0=4)
+    mu = np.array([0.2, 3.0, 7.5, 0.9])
+    ctx = mg_context_for(prob16, mu)
+    v = np.random.default_rng(5).standard_normal(prob16.n_free)
+    out["vcycle_tb221_n16_mu"] = mu
+    out["vcycle_tb221_n16_in"] = v
+    out["vcycle_tb221_n16_out"] = mg_vcycle(v, ctx)
+
+    # 3. zero-init MGCG solves
+    cases = [("tb211", tb, 16, 3, 1e-10), ("tb221", tb4, 32, 2, 1e-10),
+             ("tb222", op.thermal_block((2, 2, 2)), 16, 2, 1e-12),
+             ("smooth6", op.smooth_affine(6), 16, 2, 1e-12)]
+    for tag, spec, n, cnt, delta in cases:
+        p = reference_problem(rbws, spec, n, m0=4)
+        mus = op.sample_mus(spec, cnt, seed=100 + n)
+        xs, hists, its = [], [], []
+        for m in mus:
+            A, f = p.operator(m), p.rhs(m)
+            c = mg_context_for(p, m)
+            x, rep = mgcg_solve(A, f, np.zeros_like(f), c, delta=delta, l_max=60, mu=m)
+            xs.append(x)
+            hists.append(np.pad(rep.history, (0, 61 - len(rep.history)), constant_values=np.nan))
+            its.append(rep.iterations)
+        out[f"mgcg_{tag}_n{n}_mus"] = mus
+        out[f"mgcg_{tag}_n{n}_x"] = np.array(xs)
+        out[f"mgcg_{tag}_n{n}_hist"] = np.array(hists)
+        out[f"mgcg_{tag}_n{n}_iters"] = np.array(its)
+        out[f"mgcg_{tag}_n{n}_delta"] = np.array(delta)
+
+    # 4. L1ROC offline (LU high fidelity, reference default) + online + RBI-MGCG
+    p = reference_problem(rbws, tb4, 16, m0=4)
+    train = op.sample_mus(tb4, 64, seed=1)
+    test = op.sample_mus(tb4, 4, seed=8)
+    hf = HighFidelitySolver(p, method="lu")
+    model = l1roc_offline(list(train), 6, hf, p.operator, p.operator_rows, p.rhs, seed=3)
+    out["l1roc_tb221_n16_train"] = train
+    out["l1roc_tb221_n16_test"] = test
+    out["l1roc_tb221_n16_W"] = model.basis
+    out["l1roc_tb221_n16_T"] = model.transform
+    out["l1roc_tb221_n16_colloc"] = model.collocation
+    out["l1roc_tb221_n16_xs"] = model.solution_points
+    out["l1roc_tb221_n16_xr"] = model.residual_points
+    out["l1roc_tb221_n16_chosen_mus"] = model.chosen_mus
+    out["l1roc_tb221_n16_hist"] = model.indicator_history
+    out["l1roc_tb221_n16_saturated"] = np.array(model.saturated)
+    # a saturating greedy (duplicate pick terminates early, rb.py:258-260)
+    tb2 = op.thermal_block((2, 1, 1))
+    p2 = reference_problem(rbws, tb2, 16, m0=4)
+    tr2 = op.sample_mus(tb2, 32, seed=1)
+    m2 = l1roc_offline(list(tr2), 8, HighFidelitySolver(p2, method="lu"), p2.operator,
+                       p2.operator_rows, p2.rhs, seed=0)
+    out["l1roc_tb211_n16_train"] = tr2
+    out["l1roc_tb211_n16_W"] = m2.basis
+    out["l1roc_tb211_n16_colloc"] = m2.collocation
+    out["l1roc_tb211_n16_hist"] = m2.indicator_history
+    out["l1roc_tb211_n16_saturated"] = np.array(m2.saturated)
+    from rbws.rb import l1roc_online
+    u0s, cs, xs, its, hists = [], [], [], [], []
+    for m in test:
+        A, f = p.operator(m), p.rhs(m)
+        u0, c = l1roc_online(model, A, f)
+        u0s.append(u0)
+        cs.append(c)
+        cfg = MethodConfig("rbi-mgcg", delta=1e-10, l_max=60, N=model.dim)
+        x, rep = rbi_pcg_solve(A, f, cfg, mg_ctx=mg_context_for(p, m), l1roc_model=model, mu=m)
+        xs.append(x)
+        its.append(rep.iterations)
+        hists.append(np.pad(rep.history, (0, 61 - len(rep.history)), constant_values=np.nan))
+    out["l1roc_tb221_n16_u0"] = np.array(u0s)
+    out["l1roc_tb221_n16_c"] = np.array(cs)
+    out["rbi_tb221_n16_x"] = np.array(xs)
+    out["rbi_tb221_n16_iters"] = np.array(its)
+    out["rbi_tb221_n16_hist"] = np.array(hists)
+
+    dest = REPO / "tests/golden/golden_fd.npz"
+    np.savez_compressed(dest, **out)
+    print(f"wrote {dest} ({dest.stat().st_size/1e6:.2f} MB, {len(out)} arrays)")
+
+
+if __name__ == "__main__":
+    main()
