@@ -1,0 +1,438 @@
+"""Benchmark: warm-started (RBI-)MGCG solves/s to 1e-10 on the BASELINE workload.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config C]
+
+One step = the online stage for one batch of test parameters, resident in
+HBM: batched mg_context_for (per-mu coarse operators + coarsest Cholesky),
+the batched L1ROC online solve (affine reduced assembly + least squares +
+warm-start expansion) and the batched MGCG refinement to the tolerance —
+the reference's t_on protocol (experiment.py:31-33) for a whole batch.
+Offline greedy training runs once before timing.  Multi-GPU: one process
+per GPU, parameters sharded by rank (weak scaling, no data-path collective).
+
+--impl reference times the CPU restatement of the reference algorithm
+(oracle/, the reference package is Python and cannot travel to the box) on
+all host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+METRIC = "warm-started MGCG solves/s to 1e-10 rel. residual; stencil HBM GB/s vs peak"
+
+# BASELINE.json configs (index = position in "configs")
+CONFIGS = {
+    0: dict(workload="thermal-block 2x1x1, 32^3 cells, r=10 from 256 train, batch 64, tol 1e-10",
+            kind="tb", blocks=(2, 1, 1), n=32, m0=4, r=10, n_train=256, batch=64, delta=1e-10),
+    1: dict(workload="thermal-block 2x2x1, 64^3 cells, r=20 from 1024 train, batch 1024, tol 1e-10",
+            kind="tb", blocks=(2, 2, 1), n=64, m0=4, r=20, n_train=1024, batch=1024, delta=1e-10),
+    2: dict(workload="thermal-block 2x2x2, 128^3 cells, r=30 from 4096 train, batch 512, tol 1e-12",
+            kind="tb", blocks=(2, 2, 2), n=128, m0=4, r=30, n_train=4096, batch=512, delta=1e-12),
+    3: dict(workload="smooth affine (6 modes), 256^3 cells, r=40 from 2048 train, batch 128, tol 1e-12",
+            kind="smooth", blocks=None, n=256, m0=4, r=40, n_train=2048, batch=128, delta=1e-12),
+}
+L_MAX = 60
+
+# algorithmic bytes per interior node and instance for each profiled kernel class
+CLASS_NAMES = ["fine_apply_dot", "fine_cg_update", "fine_pre_residual", "fine_restrict",
+               "fine_prolong", "fine_post_smooth", "fine_p_update", "coarse_levels", "scalars"]
+CLASS_BYTES = {0: 8.0, 1: 40.0, 2: 24.0, 3: 9.0, 4: 25.0, 5: 24.0, 6: 24.0}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        smax = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for nm, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def make_spec(cfg, pkg):
+    if cfg["kind"] == "tb":
+        return pkg.thermal_block(cfg["blocks"])
+    return pkg.smooth_affine(6)
+
+
+def make_ospec(cfg):
+    from oracle import problems as op
+    if cfg["kind"] == "tb":
+        return op.thermal_block(cfg["blocks"])
+    return op.smooth_affine(6)
+
+
+# ---------------------------------------------------------------- b200 arm
+
+def run_b200(args, rank, world, dist):
+    import torch
+
+    import build as _build
+    if rank == 0:
+        _build.build(verbose=False)
+    if dist is not None:
+        dist.barrier()
+    import paper_2311_13862_b200 as rb
+    from paper_2311_13862_b200 import _native
+
+    cfg = CONFIGS[args.config]
+    n, m0 = cfg["n"], cfg["m0"]
+    batch = args.batch or cfg["batch"]
+    delta = cfg["delta"]
+    spec = make_spec(cfg, rb)
+    levels = rb.problems.levels_for(n, m0)
+    prob = rb.ParametricProblem(spec, levels=levels, m0=m0)
+    train = rb.sample_mus(spec, cfg["n_train"], seed=1000)
+    test = rb.sample_mus(spec, batch, seed=2000 + rank)
+
+    t0 = time.perf_counter()
+    hf = rb.HighFidelitySolver(prob, delta=1e-14, l_max=100)
+    model = rb.l1roc_offline(train, cfg["r"], hf, prob, seed=0)
+    torch.cuda.synchronize()
+    t_off = time.perf_counter() - t0
+    log(f"[rank {rank}] offline greedy: N={model.dim} saturated={model.saturated} "
+        f"in {t_off:.2f}s")
+
+    ctx = rb.MgContext(prob, batch)
+    f = prob.rhs()
+    method = rb.MethodConfig("rbi-mgcg", delta=delta, l_max=L_MAX, N=model.dim)
+    xbuf = torch.empty(rb.padded_len(n, batch), dtype=torch.float64, device="cuda")
+    state = {}
+
+    def step():
+        rb.mg_context_for(prob, test, ctx=ctx)
+        x, reps = rb.rbi_pcg_solve(rb.BatchOperator(ctx), f, method, mg_ctx=ctx,
+                                   l1roc_model=model, x0_out=xbuf)
+        state["reps"], state["x"] = reps, x
+        return x
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # zero-initialised MGCG on the same batch for reference (outside the timed region)
+    _, zreps = rb.mgcg_solve(None, f, None, ctx, delta=delta, l_max=L_MAX)
+    zero_iters = float(np.mean([r.iterations for r in zreps]))
+
+    # ---- timed region (device-resident inputs)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    _native.call("rbws_batch_profile", ctx.handle, 1)
+    lc0 = _native.launch_count()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = _native.launch_count() - lc0
+    ms = ev0.elapsed_time(ev1)
+    NC = len(CLASS_NAMES)
+    pms = np.zeros(NC)
+    pcalls = np.zeros(NC, dtype=np.int64)
+    punits = np.zeros(NC, dtype=np.int64)
+    _native.call("rbws_batch_profile_read", ctx.handle, pms.ctypes.data, pcalls.ctypes.data,
+                 punits.ctypes.data, NC)
+    _native.call("rbws_batch_profile", ctx.handle, 0)
+    if dist is not None:
+        dist.barrier()
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    ms_step = ms_max / args.steps
+    value = world * batch * args.steps / (ms_max / 1e3)
+    reps = state["reps"]
+    iters = [r.iterations for r in reps]
+    worst_res = max(r.true_residual for r in reps)
+    converged = all(r.converged for r in reps)
+
+    # ---- end to end through the public API with host buffers
+    hbuf = torch.empty(xbuf.numel(), dtype=torch.float64, pin_memory=True)
+    mus_host = np.ascontiguousarray(test)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        rb.mg_context_for(prob, mus_host, ctx=ctx)  # theta(mu) host -> device
+        x, reps_e = rb.rbi_pcg_solve(rb.BatchOperator(ctx), f, method, mg_ctx=ctx,
+                                     l1roc_model=model, x0_out=xbuf)
+        hbuf.copy_(x, non_blocking=True)          # solutions device -> host
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = world * batch * args.steps / (float(e2e_ms.item()) / 1e3)
+    h2d = batch * spec.n_terms * 8
+    d2h = xbuf.numel() * 8 + batch * (L_MAX + 1) * 8 + batch * (4 + 8 + 4)
+
+    # ---- roofline of the dominant fine-level kernel class
+    peak, peak_kind = peaks()
+    nodes = (n - 1) ** 3
+    table = {}
+    for k in range(NC):
+        if pcalls[k] == 0:
+            continue
+        row = {"ms_total": round(float(pms[k]), 3), "launches": int(pcalls[k]),
+               "ms_per_launch": round(float(pms[k]) / pcalls[k], 4),
+               "share": round(float(pms[k]) / ms, 4)}
+        if k in CLASS_BYTES:
+            gbs = CLASS_BYTES[k] * nodes * punits[k] / (pms[k] / 1e3) / 1e9
+            row["achieved_gbs"] = round(gbs, 1)
+        table[CLASS_NAMES[k]] = row
+    dom = max((k for k in CLASS_BYTES if pcalls[k]), key=lambda k: pms[k])
+    dom_bytes = CLASS_BYTES[dom] * nodes * punits[dom] / pcalls[dom]
+    dom_s = pms[dom] / pcalls[dom] / 1e3
+    achieved = dom_bytes / dom_s / 1e9
+    roofline = {"bound": "hbm", "kernel": CLASS_NAMES[dom], "achieved": round(achieved, 1),
+                "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                "traffic": None, "peak_source": peak_kind,
+                "bytes_per_launch": int(dom_bytes),
+                "bytes_per_node": CLASS_BYTES[dom]}
+
+    # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(cfg, model, test, iters, budget_s=args.cpu_budget)
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "solves/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded log-uniform parameters; no dataset)",
+        "config": {"workload": cfg["workload"], "batch_per_gpu": batch, "grid_cells": n,
+                   "levels": levels, "rb_dim": model.dim, "n_train": cfg["n_train"],
+                   "tolerance": delta, "smoother": "jacobi(0.7), nu=1",
+                   "parallelism": f"parameter-sharded x{world}",
+                   "l2": "inputs larger than L2 (working set >> 126 MB)",
+                   "mean_iterations_warm": round(float(np.mean(iters)), 3),
+                   "max_iterations_warm": int(max(iters)),
+                   "mean_iterations_zero_init": round(zero_iters, 3),
+                   "all_converged": converged, "max_true_residual": worst_res,
+                   "t_offline_s": round(t_off, 3)},
+        "e2e": {"value": round(e2e_value, 2), "unit": "solves/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "roofline": roofline,
+        "kernels": table,
+        "clocks": clocks.summary(),
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg, model, test, gpu_iters, budget_s=15.0):
+    """Oracle RBI-MGCG per parameter (single core) on a bounded sample."""
+    from oracle import problems as op
+    from oracle import solvers as so
+    ospec = make_ospec(cfg)
+    t0 = time.perf_counter()
+    oprob = op.OracleProblem(ospec, cfg["n"], cfg["m0"])
+    t_build = time.perf_counter() - t0
+    omodel = so.OracleL1rocModel(model.basis_numpy(), model.transform, model.collocation,
+                                 model.solution_points, model.residual_points,
+                                 np.asarray(model.chosen if model.chosen is not None else []),
+                                 model.indicator_history, model.saturated)
+    done, match, t_solve = 0, 0, 0.0
+    for m, mu in enumerate(test):
+        t1 = time.perf_counter()
+        _, rep = so.rbi_mgcg_solve(oprob, mu, omodel, delta=cfg["delta"], l_max=L_MAX)
+        t_solve += time.perf_counter() - t1
+        done += 1
+        match += int(abs(rep.iterations - gpu_iters[m]) <= 1)
+        if t_solve > budget_s:
+            break
+    return {"value": round(done / t_solve, 4), "unit": "solves/s", "cores": 1, "kind": "port",
+            "sample": f"{done} of the step's test parameters, oracle RBI-MGCG (mg_context_for + "
+                      f"l1roc_online + MGCG to tol) single-threaded; operator assembly "
+                      f"{t_build:.1f}s excluded; iteration counts within +-1 of the GPU: "
+                      f"{match}/{done}"}
+
+
+# ---------------------------------------------------------------- reference arm
+
+_W = {}
+
+
+def _ref_worker_init(cfg, model_state):
+    from oracle import problems as op
+    from oracle import solvers as so
+    _W["oprob"] = op.OracleProblem(make_ospec(cfg), cfg["n"], cfg["m0"])
+    _W["model"] = so.OracleL1rocModel(*model_state)
+    _W["cfg"] = cfg
+
+
+def _ref_solve(mu):
+    from oracle import solvers as so
+    _, rep = so.rbi_mgcg_solve(_W["oprob"], mu, _W["model"], delta=_W["cfg"]["delta"],
+                               l_max=L_MAX)
+    return rep.iterations
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import multiprocessing as mp
+    from oracle import problems as op
+    from oracle import solvers as so
+    cfg = CONFIGS[args.config]
+    ospec = make_ospec(cfg)
+    n, m0 = cfg["n"], cfg["m0"]
+    cores = os.cpu_count() or 1
+    oprob = op.OracleProblem(ospec, n, m0)
+    train = op.sample_mus(ospec, cfg["n_train"], seed=1000)
+    test = op.sample_mus(ospec, args.batch or cfg["batch"], seed=2000)
+
+    def hf(mu):  # reference HighFidelitySolver(method="mgcg") (hf.py:453-467)
+        A, f = oprob.operator(mu), oprob.rhs()
+        x, _ = so.mgcg_solve(A, f, np.zeros_like(f), so.mg_context_for(oprob, mu), 1e-14, 100)
+        return x
+
+    t0 = time.perf_counter()
+    model = so.l1roc_offline(list(train), cfg["r"], hf, oprob.operator, oprob.operator_rows,
+                             oprob.rhs, seed=0)
+    t_off = time.perf_counter() - t0
+    log(f"[reference] offline greedy N={model.dim} in {t_off:.1f}s")
+    state = (model.basis, model.transform, model.collocation, model.solution_points,
+             model.residual_points, model.chosen, model.indicator_history, model.saturated)
+    sample = cores * max(1, args.ref_per_core)
+    ctxm = mp.get_context("fork")
+    with ctxm.Pool(cores, initializer=_ref_worker_init, initargs=(cfg, state)) as pool:
+        k = 0
+        for _ in range(args.warmup):
+            pool.map(_ref_solve, [test[(k + i) % len(test)] for i in range(cores)])
+            k += cores
+        t1 = time.perf_counter()
+        iters = []
+        for _ in range(args.steps):
+            iters += pool.map(_ref_solve, [test[(k + i) % len(test)] for i in range(sample)])
+            k += sample
+        el = time.perf_counter() - t1
+    value = args.steps * sample / el
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": "solves/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(el / args.steps * 1e3, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded log-uniform parameters; no dataset)", "impl": "reference",
+        "config": {"workload": cfg["workload"], "rb_dim": model.dim,
+                   "mean_iterations_warm": round(float(np.mean(iters)), 3),
+                   "t_offline_s": round(t_off, 1)},
+        "cpu_baseline": {"value": round(value, 4), "unit": "solves/s", "cores": cores,
+                         "kind": "port",
+                         "sample": f"{sample} test parameters per step ({args.ref_per_core} per "
+                                   f"core), oracle restatement of the reference RBI-MGCG "
+                                   f"(scipy.sparse), process pool over all host cores"},
+        "e2e": {"value": round(value, 4), "unit": "solves/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-per-core", type=int, default=1)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        log("note: fewer than 3 warm-up steps requested")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    run_b200(args, rank, world, dist)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,147 @@
+/* rbws_b200.h — C ABI of the B200-native RBWS hot path.
+ *
+ * The reference (rbws, Python) binds its compiled hot loops through the
+ * Cython module rbws._smoothers (csr_gauss_seidel / csr_jacobi,
+ * reference _smoothers.pyx:14-45) and otherwise runs scipy.sparse / numpy.
+ * This library replaces the whole data-parallel path those calls sit on —
+ * operator application, smoothing sweeps, grid transfers, V-cycle, PCG and
+ * the L1ROC online/offline kernels — batched over parameter instances.
+ *
+ * Conventions
+ *  - All functions return 0 on success, non-zero on error;
+ *    rbws_last_error() describes the last failure of the calling thread.
+ *  - Array arguments marked (dev) are device pointers, (host) host pointers.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
+ *  - Grid vectors use the padded batch layout: instance `mu` of a level with
+ *    n cells occupies doubles [mu*n^3, (mu+1)*n^3) indexed i + n*(j + n*k);
+ *    interior (free) DoFs are i,j,k in [1, n-1], all other entries are 0.
+ *    A buffer for `count` instances holds count*n^3 + n^2 doubles.
+ *    Interior ordering inside the padded block equals the reference's free-DoF
+ *    ordering (lexicographic, x fastest; reference grid.py:29-34,
+ *    problems.py:409-421).
+ *  - Separable operator tables of an n-cell finest grid with Q affine terms:
+ *      face[(q*3+d)*n + i]           d-face factor between nodes i and i+1
+ *      node[((q*3+d)*3+a)*(n+1)+j]   factor along axis a != d at node j
+ *    The weight of the d-face between X and X+e_d is
+ *      sum_q theta_q(mu) * face[q][d][X_d] * prod_{a != d} node[q][d][a][X_a].
+ */
+#ifndef RBWS_B200_H
+#define RBWS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rbws_hierarchy rbws_hierarchy;
+typedef struct rbws_batch rbws_batch;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int rbws_version(void);
+/* Last error message of the calling thread ("" if none). */
+const char* rbws_last_error(void);
+/* Kernel launches issued by this library so far (process-wide counter). */
+int64_t rbws_launch_count(void);
+
+/* ---- hierarchy: mu-independent part of ParametricProblem -------------------
+ * Replaces ParametricProblem.__init__ hierarchy/coarsening
+ * (reference grid.py:231-262) and build_hierarchy (grid.py:191-198): nested
+ * grids m0*2^i cells, trilinear prolongation, termwise Galerkin coarsening
+ * (carried out on the 1D Kronecker factors of every affine term).
+ * face/node: (host) separable tables of the finest grid (see above). */
+int rbws_hierarchy_create(rbws_hierarchy** out, int n, int m0, int nterms,
+                          const double* face, const double* node);
+int rbws_hierarchy_destroy(rbws_hierarchy* h);
+int rbws_hierarchy_levels(const rbws_hierarchy* h);
+int rbws_hierarchy_cells(const rbws_hierarchy* h, int level);
+/* (host) copy of the 1D factors of `level`: Q*3*3*2*(cells+1) doubles */
+int rbws_hierarchy_factors(const rbws_hierarchy* h, int level, double* out, int64_t capacity);
+
+/* Host-only variant (no device needed): the 1D factors of `level` computed
+ * from the separable tables, same layout as rbws_hierarchy_factors. */
+int rbws_kron_factors(int n, int m0, int nterms, const double* face, const double* node,
+                      int level, double* out, int64_t capacity);
+
+/* ---- batch: mg_context_for for a batch of parameters -----------------------
+ * Replaces mg_context_for / _finish_context (multigrid.py:493-541): per-mu
+ * operators on every level, Jacobi diagonals, Cholesky of the coarsest level.
+ * nu: sweeps per side (>= 1), omega: Jacobi damping (reference 0.7,
+ * multigrid.py:367). */
+int rbws_batch_create(rbws_batch** out, rbws_hierarchy* h, int capacity, int nu, double omega);
+int rbws_batch_destroy(rbws_batch* b);
+/* theta: (dev) [count][Q] affine weights theta_q(mu). Returns the number of
+ * instances whose coarsest operator failed to factor in *n_bad (host). */
+int rbws_batch_setup(rbws_batch* b, const double* theta, int count, int* n_bad, void* stream);
+
+/* y = A^level(mu) x for every instance (ParametricProblem.operator(mu, level) @ x,
+ * grid.py:274-283).  x, y: (dev) padded vectors of that level. */
+int rbws_apply(rbws_batch* b, int level, const double* x, double* y, void* stream);
+/* One damped-Jacobi sweep y = x + omega (rhs - A x)/diag on `level`
+ * (replaces _smoothers.pyx:31 csr_jacobi via Smoother._jacobi, kernels.py:98-115). */
+int rbws_jacobi_sweep(rbws_batch* b, int level, const double* x, const double* rhs, double* y,
+                      void* stream);
+/* bc = P^T rf (multigrid.py:559 `P.T @ r`); nf = fine cells. (dev) */
+int rbws_restrict(int nf, int count, const double* rf, double* bc, void* stream);
+/* u += P ec (multigrid.py:560 `u + P @ e`). (dev) */
+int rbws_prolong_add(int nf, int count, const double* ec, double* u, void* stream);
+/* One V-cycle from zero on the finest level (mg_vcycle, multigrid.py:544-561). (dev) */
+int rbws_vcycle(rbws_batch* b, const double* rhs, double* out, void* stream);
+
+/* Batched MGCG (pcg_solve with the V-cycle preconditioner, krylov.py:267-334,
+ * multigrid.py:564-571).
+ * f: (dev) rhs, per instance stride f_stride doubles (0 = shared by all).
+ * x: (dev) in: initial guesses, out: solutions.
+ * iters [count], hist [count][l_max+1] (NaN padded), true_res [count],
+ * status [count]: (host) outputs; status bit0 = breakdown (non-SPD),
+ * bit1 = not converged, bit2 = ||f|| = 0 (absolute norms). */
+int rbws_mgcg_solve(rbws_batch* b, const double* f, int64_t f_stride, double* x, double delta,
+                    int l_max, int* iters, double* hist, double* true_res, int* status,
+                    void* stream);
+
+/* Optional per-kernel-class timing with CUDA events on the launch stream
+ * (enable resets the counters).  Classes (9): fine apply+dot, fine CG update,
+ * fine pre-smooth+residual, fine restriction, fine prolongation, fine
+ * post-smooth, p-update, all coarse levels, per-instance scalar kernels.
+ * ms/calls: (host) arrays of nclass entries. */
+int rbws_batch_profile(rbws_batch* b, int enable);
+int rbws_batch_profile_read(rbws_batch* b, double* ms, int64_t* calls, int64_t* units,
+                            int nclass);
+
+/* ---- L1ROC reduced model (reference rb.py) -------------------------------- */
+/* Term-wise sampled projections Bq[q][m][c] = (A_q W)[rows[m], c]
+ * (the affine pieces of rb.py:200-201 `A[rows,:] @ basis`).
+ * W: (dev) N padded finest-level vectors (stride Wstride doubles);
+ * rows: (dev) padded node indices [M]; Bq: (dev) [Q][M][N]. */
+int rbws_l1roc_project(rbws_hierarchy* h, const double* W, int64_t Wstride, int N,
+                       const int64_t* rows, int M, double* Bq, void* stream);
+/* Batched online stage (rb.py:182-205, 129-131): B(mu) = sum_q theta_q Bq,
+ * least squares min ||B a - b_s||, snapshot coordinates c = T^{-1} a and
+ * indicator ||c||_1.  theta (dev) [count][Q]; bs (dev) [M] per instance with
+ * stride bs_stride (0 = shared); T (dev) [N][N] row-major upper triangular
+ * (may be NULL: no indicator).  Outputs (dev): a [count][N], c [count][N],
+ * ind [count], status [count] (1 = rank deficient). */
+int rbws_l1roc_online(int count, int Q, int M, int N, const double* theta, const double* Bq,
+                      const double* bs, int64_t bs_stride, const double* T, double* a,
+                      double* c, double* ind, int* status, void* stream);
+/* x[mu] = W a[mu] (rb.py:205 `model.basis @ a`), (dev) padded output. */
+int rbws_expand(int n, int count, const double* W, int64_t Wstride, int N, const double* a,
+                double* x, void* stream);
+/* DEIM residual step (rb.py:113-126): rho = v - W c, then the first index of
+ * max |rho| over interior nodes not flagged in `excluded` (dev uint8, padded
+ * layout, may be NULL), written with the pivot rho[idx] and max|v| to
+ * out_idx (dev int64) / out_vals (dev double[2]); column = rho / pivot is
+ * written to `col` (dev padded). */
+int rbws_deim_step(int n, const double* W, int64_t Wstride, int N, const double* c,
+                   const double* v, const uint8_t* excluded, double* col, int64_t* out_idx,
+                   double* out_vals, void* stream);
+/* Small dense solve A x = b (partial pivoting) on the device, A (dev) [m][m]
+ * row-major, b/x (dev) [m] (np.linalg.solve in rb.py:113). */
+int rbws_dense_solve(int m, const double* A, const double* b, double* x, int* status,
+                     void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RBWS_B200_H */

@@ -1,0 +1,103 @@
+"""ctypes binding of the C ABI in include/rbws_b200.h.
+
+The shared library ``_rbws_b200.so`` is built in-tree by ``build.py`` (nvcc,
+sm_100a).  There is no fallback: if the library is missing or no CUDA device
+is present, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+LIB_NAME = "_rbws_b200.so"
+LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
+
+_c_int, _c_int64, _c_double, _vp = ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
+_pp = ctypes.POINTER(ctypes.c_void_p)
+_ip = ctypes.POINTER(ctypes.c_int)
+_dp = ctypes.POINTER(ctypes.c_double)
+
+# name -> argtypes (every function returns int unless listed in _RESTYPES)
+SIGNATURES = {
+    "rbws_version": [],
+    "rbws_last_error": [],
+    "rbws_launch_count": [],
+    "rbws_hierarchy_create": [_pp, _c_int, _c_int, _c_int, _vp, _vp],
+    "rbws_hierarchy_destroy": [_vp],
+    "rbws_hierarchy_levels": [_vp],
+    "rbws_hierarchy_cells": [_vp, _c_int],
+    "rbws_hierarchy_factors": [_vp, _c_int, _vp, _c_int64],
+    "rbws_kron_factors": [_c_int, _c_int, _c_int, _vp, _vp, _c_int, _vp, _c_int64],
+    "rbws_batch_create": [_pp, _vp, _c_int, _c_int, _c_double],
+    "rbws_batch_destroy": [_vp],
+    "rbws_batch_setup": [_vp, _vp, _c_int, _ip, _vp],
+    "rbws_apply": [_vp, _c_int, _vp, _vp, _vp],
+    "rbws_jacobi_sweep": [_vp, _c_int, _vp, _vp, _vp, _vp],
+    "rbws_restrict": [_c_int, _c_int, _vp, _vp, _vp],
+    "rbws_prolong_add": [_c_int, _c_int, _vp, _vp, _vp],
+    "rbws_vcycle": [_vp, _vp, _vp, _vp],
+    "rbws_mgcg_solve": [_vp, _vp, _c_int64, _vp, _c_double, _c_int, _vp, _vp, _vp, _vp, _vp],
+    "rbws_batch_profile": [_vp, _c_int],
+    "rbws_batch_profile_read": [_vp, _vp, _vp, _vp, _c_int],
+    "rbws_l1roc_project": [_vp, _vp, _c_int64, _c_int, _vp, _c_int, _vp, _vp],
+    "rbws_l1roc_online": [_c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _c_int64, _vp, _vp,
+                          _vp, _vp, _vp, _vp],
+    "rbws_expand": [_c_int, _c_int, _vp, _c_int64, _c_int, _vp, _vp, _vp],
+    "rbws_deim_step": [_c_int, _vp, _c_int64, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "rbws_dense_solve": [_c_int, _vp, _vp, _vp, _vp, _vp],
+}
+_RESTYPES = {"rbws_last_error": ctypes.c_char_p, "rbws_launch_count": ctypes.c_int64}
+
+
+def launch_count() -> int:
+    return int(load().rbws_launch_count())
+
+_lib = None
+
+
+class NativeError(RuntimeError):
+    """A C-ABI call failed (message from rbws_last_error)."""
+
+
+def load(path: str | os.PathLike | None = None):
+    """Load (once) and return the ctypes library; raises if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise NativeError(
+            f"native library {p} not built; run `python build.py` (nvcc, sm_100a). "
+            "There is no CPU fallback.")
+    lib = ctypes.CDLL(str(p))
+    for name, argtypes in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = argtypes
+        fn.restype = _RESTYPES.get(name, ctypes.c_int)
+    _lib = lib
+    return lib
+
+
+def call(name: str, *args) -> int:
+    """Invoke an entry point; non-zero status raises NativeError."""
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        msg = lib.rbws_last_error().decode(errors="replace")
+        raise NativeError(f"{name} failed: {msg}")
+    return rc
+
+
+def require_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        raise NativeError("no CUDA device: the RBWS B200 path has no CPU fallback")
+    load()
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)

@@ -1,0 +1,227 @@
+// extern "C" boundary (include/rbws_b200.h).
+#include "../../include/rbws_b200.h"
+#include "l1roc.cuh"
+#include "solver.cuh"
+
+const char* rbws_get_error();
+
+#define RBWS_FAIL(msg) return rbws_set_error(msg, __FILE__, __LINE__)
+#define RBWS_CHECK(expr)                                                          \
+  do {                                                                            \
+    cudaError_t _e = (expr);                                                      \
+    if (_e != cudaSuccess) return rbws_set_error(cudaGetErrorString(_e), __FILE__, __LINE__); \
+  } while (0)
+
+using rbws::Batch;
+using rbws::Hierarchy;
+
+static inline Hierarchy* H(rbws_hierarchy* h) { return reinterpret_cast<Hierarchy*>(h); }
+static inline const Hierarchy* H(const rbws_hierarchy* h) { return reinterpret_cast<const Hierarchy*>(h); }
+static inline Batch* B(rbws_batch* b) { return reinterpret_cast<Batch*>(b); }
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+int rbws_version(void) { return 100; }
+
+const char* rbws_last_error(void) { return rbws_get_error(); }
+
+int64_t rbws_launch_count(void) { return rbws::launch_count(); }
+
+int rbws_hierarchy_create(rbws_hierarchy** out, int n, int m0, int nterms, const double* face,
+                          const double* node) {
+  if (!out || !face || !node) RBWS_FAIL("null argument");
+  Hierarchy* h = nullptr;
+  if (rbws::hierarchy_create(&h, n, m0, nterms, face, node)) return 1;
+  *out = reinterpret_cast<rbws_hierarchy*>(h);
+  return 0;
+}
+
+int rbws_hierarchy_destroy(rbws_hierarchy* h) {
+  delete H(h);
+  return 0;
+}
+
+int rbws_hierarchy_levels(const rbws_hierarchy* h) { return H(h)->levels; }
+
+int rbws_hierarchy_cells(const rbws_hierarchy* h, int level) {
+  if (level < 0 || level >= H(h)->levels) return -1;
+  return H(h)->cells[level];
+}
+
+int rbws_hierarchy_factors(const rbws_hierarchy* h, int level, double* out, int64_t capacity) {
+  const Hierarchy* hh = H(h);
+  if (level < 0 || level >= hh->levels) RBWS_FAIL("level outside hierarchy");
+  const auto& f = hh->h_fac[level];
+  if ((int64_t)f.size() > capacity) RBWS_FAIL("output buffer too small");
+  for (size_t i = 0; i < f.size(); ++i) out[i] = f[i];
+  return 0;
+}
+
+int rbws_kron_factors(int n, int m0, int nterms, const double* face, const double* node,
+                      int level, double* out, int64_t capacity) {
+  std::vector<int> cells;
+  std::vector<std::vector<double>> fac;
+  if (rbws::kron_factors(n, m0, nterms, face, node, cells, fac)) return 1;
+  if (level < 0 || level >= (int)cells.size()) RBWS_FAIL("level outside hierarchy");
+  if ((int64_t)fac[level].size() > capacity) RBWS_FAIL("output buffer too small");
+  for (size_t i = 0; i < fac[level].size(); ++i) out[i] = fac[level][i];
+  return 0;
+}
+
+int rbws_batch_create(rbws_batch** out, rbws_hierarchy* h, int capacity, int nu, double omega) {
+  if (!out || !h) RBWS_FAIL("null argument");
+  Batch* b = nullptr;
+  if (rbws::batch_create(&b, H(h), capacity, nu, omega)) return 1;
+  *out = reinterpret_cast<rbws_batch*>(b);
+  return 0;
+}
+
+int rbws_batch_destroy(rbws_batch* b) {
+  delete B(b);
+  return 0;
+}
+
+int rbws_batch_setup(rbws_batch* b, const double* theta, int count, int* n_bad, void* stream) {
+  Batch* bb = B(b);
+  if (rbws::batch_setup(bb, theta, count, S(stream))) return 1;
+  if (n_bad) {
+    std::vector<int> st(count);
+    RBWS_CHECK(cudaMemcpyAsync(st.data(), bb->d_status, sizeof(int) * count,
+                               cudaMemcpyDeviceToHost, S(stream)));
+    RBWS_CHECK(cudaStreamSynchronize(S(stream)));
+    int bad = 0;
+    for (int v : st) bad += v ? 1 : 0;
+    *n_bad = bad;
+  }
+  return 0;
+}
+
+int rbws_apply(rbws_batch* b, int level, const double* x, double* y, void* stream) {
+  Batch* bb = B(b);
+  Hierarchy* h = bb->h;
+  if (level < 0 || level >= h->levels) RBWS_FAIL("level outside hierarchy");
+  if (bb->count < 1) RBWS_FAIL("batch_setup must be called first");
+  rbws::LaunchCtx lc{S(stream), nullptr};
+  if (level == h->levels - 1) {
+    RBWS_CHECK(rbws::sep7_launch(bb->fine_op(), bb->count, rbws::MODE_APPLY, rbws::DOT_NONE, x,
+                                 nullptr, nullptr, y, nullptr, 0.0, lc));
+  } else {
+    rbws::St27 op{h->cells[level], bb->lv[level].coef};
+    RBWS_CHECK(rbws::st27_launch(op, bb->count, rbws::MODE_APPLY, x, nullptr, nullptr, y, 0.0, lc));
+  }
+  return 0;
+}
+
+int rbws_jacobi_sweep(rbws_batch* b, int level, const double* x, const double* rhs, double* y,
+                      void* stream) {
+  Batch* bb = B(b);
+  Hierarchy* h = bb->h;
+  if (level < 1 || level >= h->levels) RBWS_FAIL("smoothing level must be in [1, levels)");
+  if (bb->count < 1) RBWS_FAIL("batch_setup must be called first");
+  rbws::LaunchCtx lc{S(stream), nullptr};
+  if (level == h->levels - 1) {
+    RBWS_CHECK(rbws::sep7_launch(bb->fine_op(), bb->count, rbws::MODE_JACOBI, rbws::DOT_NONE, x,
+                                 rhs, nullptr, y, nullptr, bb->omega, lc));
+  } else {
+    rbws::St27 op{h->cells[level], bb->lv[level].coef};
+    RBWS_CHECK(rbws::st27_launch(op, bb->count, rbws::MODE_JACOBI, x, rhs, bb->lv[level].dinv, y,
+                                 bb->omega, lc));
+  }
+  return 0;
+}
+
+int rbws_restrict(int nf, int count, const double* rf, double* bc, void* stream) {
+  if (nf < 4 || (nf & 1)) RBWS_FAIL("fine grid must have an even number of cells >= 4");
+  rbws::LaunchCtx lc{S(stream), nullptr};
+  RBWS_CHECK(rbws::restrict_launch(nf, count, rf, bc, lc));
+  return 0;
+}
+
+int rbws_prolong_add(int nf, int count, const double* ec, double* u, void* stream) {
+  if (nf < 4 || (nf & 1)) RBWS_FAIL("fine grid must have an even number of cells >= 4");
+  rbws::LaunchCtx lc{S(stream), nullptr};
+  RBWS_CHECK(rbws::prolong_launch(nf, count, 0, ec, u, nullptr, nullptr, 0.0, lc));
+  return 0;
+}
+
+int rbws_vcycle(rbws_batch* b, const double* rhs, double* out, void* stream) {
+  Batch* bb = B(b);
+  if (bb->count < 1) RBWS_FAIL("batch_setup must be called first");
+  rbws::LaunchCtx lc{S(stream), nullptr};
+  return bb->vcycle(bb->h->levels - 1, rhs, out, nullptr, lc);
+}
+
+int rbws_mgcg_solve(rbws_batch* b, const double* f, int64_t f_stride, double* x, double delta,
+                    int l_max, int* iters, double* hist, double* true_res, int* status,
+                    void* stream) {
+  rbws::PcgOut o{iters, hist, true_res, status};
+  return rbws::pcg_solve(B(b), f, f_stride, x, delta, l_max, o, S(stream));
+}
+
+int rbws_batch_profile(rbws_batch* b, int enable) {
+  Batch* bb = B(b);
+  bb->prof_on = enable != 0;
+  for (int k = 0; k < rbws::PROF_NCLASS; ++k) {
+    bb->prof_ms[k] = 0.0;
+    bb->prof_calls[k] = 0;
+    bb->prof_units[k] = 0;
+  }
+  return 0;
+}
+
+int rbws_batch_profile_read(rbws_batch* b, double* ms, int64_t* calls, int64_t* units,
+                            int nclass) {
+  Batch* bb = B(b);
+  for (int k = 0; k < nclass && k < rbws::PROF_NCLASS; ++k) {
+    ms[k] = bb->prof_ms[k];
+    calls[k] = bb->prof_calls[k];
+    units[k] = bb->prof_units[k];
+  }
+  return 0;
+}
+
+int rbws_l1roc_project(rbws_hierarchy* h, const double* W, int64_t Wstride, int N,
+                       const int64_t* rows, int M, double* Bq, void* stream) {
+  Hierarchy* hh = H(h);
+  RBWS_CHECK(rbws::l1roc_project(hh->n, hh->Q, hh->d_face, hh->d_node, W, Wstride, N, rows, M, Bq,
+                                 S(stream)));
+  return 0;
+}
+
+int rbws_l1roc_online(int count, int Q, int M, int N, const double* theta, const double* Bq,
+                      const double* bs, int64_t bs_stride, const double* T, double* a, double* c,
+                      double* ind, int* status, void* stream) {
+  if (count < 1 || N < 1 || M < N) RBWS_FAIL("need count >= 1 and M >= N >= 1");
+  RBWS_CHECK(rbws::l1roc_online(count, Q, M, N, theta, Bq, bs, bs_stride, T, a, c, ind, status,
+                                S(stream)));
+  return 0;
+}
+
+int rbws_expand(int n, int count, const double* W, int64_t Wstride, int N, const double* a,
+                double* x, void* stream) {
+  if (N < 1) RBWS_FAIL("empty basis");
+  RBWS_CHECK(rbws::expand(n, count, W, Wstride, N, a, x, S(stream)));
+  return 0;
+}
+
+int rbws_deim_step(int n, const double* W, int64_t Wstride, int N, const double* c,
+                   const double* v, const uint8_t* excluded, double* col, int64_t* out_idx,
+                   double* out_vals, void* stream) {
+  void* scratch = nullptr;
+  RBWS_CHECK(cudaMallocAsync(&scratch, rbws::deim_scratch_bytes(n), S(stream)));
+  cudaError_t e = rbws::deim_step(n, W, Wstride, N, c, v, excluded, col, out_idx, out_vals,
+                                  scratch, S(stream));
+  cudaFreeAsync(scratch, S(stream));
+  RBWS_CHECK(e);
+  return 0;
+}
+
+int rbws_dense_solve(int m, const double* A, const double* b, double* x, int* status,
+                     void* stream) {
+  if (m < 1) RBWS_FAIL("empty system");
+  RBWS_CHECK(rbws::dense_solve(m, A, b, x, status, S(stream)));
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,85 @@
+// Shared definitions for the RBWS B200 kernels.
+//
+// Vector layout ("padded batch layout"): a level with n cells
+// per axis stores each parameter instance as an n^3 block of doubles indexed
+// i + n*(j + n*k), i,j,k in [0,n).  Interior (free) nodes are i,j,k in
+// [1,n-1]; every entry with a zero coordinate is a Dirichlet ghost that stays
+// 0.0.  Neighbour addresses of interior nodes that step onto the far
+// boundary (coordinate n) wrap onto the next row/plane/instance's ghost
+// entries, so stencils need no bounds checks.  A batch of B instances is
+// B*n^3 + n^2 doubles (one trailing ghost plane).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define RBWS_HD __host__ __device__ __forceinline__
+
+namespace rbws {
+
+constexpr int kMaxTerms = 8;
+
+// process-wide count of kernel launches issued by this library
+void count_launch();
+int64_t launch_count();
+
+RBWS_HD int64_t vec_doubles(int n, int batch) {
+  return (int64_t)batch * n * n * n + (int64_t)n * n;
+}
+
+// Separable 7-point operator of the finest level.
+// face[(q*3+d)*n + i]            : factor of the d-face between nodes i, i+1 along d
+// node[((q*3+d)*3+a)*(n+1) + j]  : factor along axis a != d at node j
+// theta[mu*Q + q]                : affine weight of term q for instance mu
+struct Sep7 {
+  int n;
+  int Q;
+  const double* face;
+  const double* node;
+  const double* theta;
+};
+
+// Per-instance symmetric 27-point stencil of a coarse level.
+// coef[(mu*14 + o)*n^3 + X]: o=0 diagonal, o=1..13 forward offsets; the
+// backward coefficient for -o at X is coef[o] at X - o.
+struct St27 {
+  int n;
+  const double* coef;
+};
+
+// forward offsets (dx,dy,dz) with (dz,dy,dx) lexicographically positive
+__host__ __device__ inline void fwd_offset(int o, int& dx, int& dy, int& dz) {
+  // o in 1..13
+  int t = o - 1;
+  if (t < 9) { dz = 1; dy = t / 3 - 1; dx = t % 3 - 1; }
+  else if (t < 12) { dz = 0; dy = 1; dx = t - 10; }
+  else { dz = 0; dy = 0; dx = 1; }
+}
+
+// Deterministic reduction of one double per thread over a (possibly 2D)
+// block.  Result valid in thread 0.  smem must hold >= 32 doubles.
+__device__ __forceinline__ double block_reduce_sum(double v, double* smem) {
+  const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+  const int nthreads = blockDim.x * blockDim.y * blockDim.z;
+  for (int s = 16; s > 0; s >>= 1) v += __shfl_down_sync(0xffffffffu, v, s);
+  const int lane = tid & 31, wid = tid >> 5;
+  const int nwarps = (nthreads + 31) >> 5;
+  __syncthreads();
+  if (lane == 0) smem[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (tid == 0) {
+    for (int w = 0; w < nwarps; ++w) r += smem[w];
+  }
+  return r;
+}
+
+}  // namespace rbws
+
+#define RBWS_CUDA_CHECK(expr)                                              \
+  do {                                                                     \
+    cudaError_t _e = (expr);                                               \
+    if (_e != cudaSuccess) return rbws_set_error(cudaGetErrorString(_e), __FILE__, __LINE__); \
+  } while (0)
+
+int rbws_set_error(const char* msg, const char* file, int line);

@@ -1,0 +1,384 @@
+// L1ROC reduced-model kernels (reference rb.py): sampled term projections,
+// batched online least squares with the L1 indicator, warm-start expansion,
+// DEIM residual/argmax and a small dense solver.
+#include <cfloat>
+
+#include "l1roc.cuh"
+
+namespace rbws {
+
+// ---------------------------------------------------------------- projections
+// Bq[q][m][c] = (A_q w_c)(rows[m]) with the separable term-q 7-point stencil
+__global__ void l1roc_project_kernel(int n, int Q, const double* __restrict__ face,
+                                     const double* __restrict__ node,
+                                     const double* __restrict__ W, int64_t Wstride, int N,
+                                     const int64_t* __restrict__ rows, int M,
+                                     double* __restrict__ Bq) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)Q * M * N) return;
+  const int c = t % N, m = (t / N) % M, q = t / ((int64_t)N * M);
+  const int64_t X = rows[m];
+  const int i = X % n, j = (X / n) % n, k = X / ((int64_t)n * n);
+  const int n1 = n + 1;
+  const double* w = W + (int64_t)c * Wstride;
+  const double* F = face + (size_t)q * 3 * n;
+  const double* Nd = node + (size_t)q * 9 * n1;
+  const int xyz[3] = {i, j, k};
+  const int64_t stride[3] = {1, n, (int64_t)n * n};
+  const double wc = w[X];
+  double acc = 0.0;
+  for (int d = 0; d < 3; ++d) {
+    double lat = 1.0;
+    for (int a = 0; a < 3; ++a)
+      if (a != d) lat *= Nd[((d * 3) + a) * n1 + xyz[a]];
+    const double wp = F[d * n + xyz[d]] * lat, wm = F[d * n + xyz[d] - 1] * lat;
+    acc += wp * (wc - w[X + stride[d]]) + wm * (wc - w[X - stride[d]]);
+  }
+  Bq[t] = acc;
+}
+
+cudaError_t l1roc_project(int n, int Q, const double* face, const double* node, const double* W,
+                          int64_t Wstride, int N, const int64_t* rows, int M, double* Bq,
+                          cudaStream_t stream) {
+  const int64_t tot = (int64_t)Q * M * N;
+  if (tot == 0) return cudaSuccess;
+  count_launch();
+  l1roc_project_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, stream>>>(n, Q, face, node, W,
+                                                                          Wstride, N, rows, M, Bq);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- online LS
+// one block per instance; Householder QR of the M x N sampled matrix in smem
+__global__ void __launch_bounds__(128) l1roc_online_kernel(int M, int N, int Q,
+                                                           const double* __restrict__ theta,
+                                                           const double* __restrict__ Bq,
+                                                           const double* __restrict__ bs,
+                                                           int64_t bs_stride,
+                                                           const double* __restrict__ T,
+                                                           double* __restrict__ a_out,
+                                                           double* __restrict__ c_out,
+                                                           double* __restrict__ ind,
+                                                           int* __restrict__ status) {
+  extern __shared__ double sm[];
+  double* B = sm;               // column-major [N][M]
+  double* rhs = B + M * N;      // [M]
+  double* red = rhs + M;        // [32]
+  double* sol = red + 32;       // [N]
+  const int mu = blockIdx.x;
+  const int tid = threadIdx.x;
+  const double* th = theta + (int64_t)mu * Q;
+  for (int t = tid; t < M * N; t += blockDim.x) {
+    const int m = t / N, c = t % N;
+    double v = 0.0;
+    for (int q = 0; q < Q; ++q) v = fma(th[q], Bq[((int64_t)q * M + m) * N + c], v);
+    B[c * M + m] = v;
+  }
+  for (int m = tid; m < M; m += blockDim.x) rhs[m] = bs[mu * bs_stride + m];
+  __syncthreads();
+  double rmax = 0.0;
+  int bad = 0;
+  for (int j = 0; j < N; ++j) {
+    double* col = B + j * M;
+    double part = 0.0;
+    for (int m = j + tid; m < M; m += blockDim.x) part = fma(col[m], col[m], part);
+    const double nrm2 = block_reduce_sum(part, red);
+    __syncthreads();
+    if (tid == 0) red[0] = nrm2;
+    __syncthreads();
+    const double nrm = sqrt(red[0]);
+    const double x0 = col[j];
+    const double alpha = (x0 >= 0.0) ? -nrm : nrm;  // R_jj
+    // v = x - alpha e_j (stored in col[j..]), tau = 1/(alpha (alpha - x0)) * ... use v^T v
+    __syncthreads();
+    if (nrm == 0.0) {
+      if (tid == 0) col[j] = 0.0;
+      __syncthreads();
+      continue;
+    }
+    if (tid == 0) col[j] = x0 - alpha;
+    __syncthreads();
+    const double vtv = 2.0 * nrm * (nrm + fabs(x0));  // ||x - alpha e_j||^2
+    // apply H = I - 2 v v^T / vtv to remaining columns and rhs
+    for (int c = j + 1; c <= N; ++c) {
+      double* y = (c < N) ? B + c * M : rhs;
+      double pd = 0.0;
+      for (int m = j + tid; m < M; m += blockDim.x) pd = fma(col[m], y[m], pd);
+      const double s = block_reduce_sum(pd, red);
+      __syncthreads();
+      if (tid == 0) red[0] = s;
+      __syncthreads();
+      const double f = 2.0 * red[0] / vtv;
+      for (int m = j + tid; m < M; m += blockDim.x) y[m] = fma(-f, col[m], y[m]);
+      __syncthreads();
+    }
+    if (tid == 0) col[j] = alpha;  // R_jj (below-diagonal part of v no longer needed)
+    __syncthreads();
+  }
+  if (tid == 0) {
+    for (int j = 0; j < N; ++j) rmax = fmax(rmax, fabs(B[j * M + j]));
+    const double tol = rmax * DBL_EPSILON * (double)(M > N ? M : N);
+    for (int j = 0; j < N; ++j)
+      if (!(fabs(B[j * M + j]) > tol)) bad = 1;
+    // back substitution R a = (Q^T b)[0:N]
+    for (int j = N - 1; j >= 0; --j) {
+      double s = rhs[j];
+      for (int c = j + 1; c < N; ++c) s -= B[c * M + j] * sol[c];
+      sol[j] = bad ? 0.0 : s / B[j * M + j];
+    }
+    double* ao = a_out + (int64_t)mu * N;
+    for (int j = 0; j < N; ++j) ao[j] = sol[j];
+    if (T) {
+      // snapshot coordinates c = T^{-1} a (T upper triangular, row-major)
+      double l1 = 0.0;
+      double* co = c_out + (int64_t)mu * N;
+      for (int j = N - 1; j >= 0; --j) {
+        double s = sol[j];
+        for (int c = j + 1; c < N; ++c) s -= T[j * N + c] * co[c];
+        co[j] = s / T[j * N + j];
+      }
+      for (int j = 0; j < N; ++j) l1 += fabs(co[j]);
+      ind[mu] = l1;
+    }
+    status[mu] = bad;
+  }
+}
+
+cudaError_t l1roc_online(int count, int Q, int M, int N, const double* theta, const double* Bq,
+                         const double* bs, int64_t bs_stride, const double* T, double* a,
+                         double* c, double* ind, int* status, cudaStream_t stream) {
+  const size_t smem = sizeof(double) * ((size_t)M * N + M + 32 + N);
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(l1roc_online_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  count_launch();
+  l1roc_online_kernel<<<count, 128, smem, stream>>>(M, N, Q, theta, Bq, bs, bs_stride, T, a, c,
+                                                     ind, status);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- expansion
+// x[mu] = W a[mu]; a block holds a 256-node tile of W in smem and sweeps a
+// chunk of instances, so W is read count/kChunk times in total.
+constexpr int kExpandChunk = 128;
+
+__global__ void __launch_bounds__(256) expand_kernel(int64_t n3, const double* __restrict__ W,
+                                                     int64_t Wstride, int N,
+                                                     const double* __restrict__ a, int count,
+                                                     double* __restrict__ x) {
+  extern __shared__ double wt[];  // [N][256]
+  const int64_t X = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  for (int c = 0; c < N; ++c) wt[c * 256 + threadIdx.x] = (X < n3) ? W[c * Wstride + X] : 0.0;
+  __syncthreads();
+  if (X >= n3) return;
+  const int m0 = blockIdx.y * kExpandChunk;
+  const int m1 = min(count, m0 + kExpandChunk);
+  for (int mu = m0; mu < m1; ++mu) {
+    const double* am = a + (int64_t)mu * N;
+    double s = 0.0;
+    for (int c = 0; c < N; ++c) s = fma(wt[c * 256 + threadIdx.x], __ldg(am + c), s);
+    x[(int64_t)mu * n3 + X] = s;
+  }
+}
+
+cudaError_t expand(int n, int count, const double* W, int64_t Wstride, int N, const double* a,
+                   double* x, cudaStream_t stream) {
+  const int64_t n3 = (int64_t)n * n * n;
+  const size_t smem = sizeof(double) * 256 * (size_t)N;
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(expand_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grd((unsigned)((n3 + 255) / 256), (count + kExpandChunk - 1) / kExpandChunk);
+  count_launch();
+  expand_kernel<<<grd, 256, smem, stream>>>(n3, W, Wstride, N, a, count, x);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- DEIM step
+struct ArgMax {
+  double v;
+  int64_t i;
+};
+
+__device__ __forceinline__ ArgMax better(ArgMax a, ArgMax b) {
+  // larger value wins; ties -> smaller index (np.argmax first occurrence)
+  if (b.v > a.v || (b.v == a.v && b.i < a.i)) return b;
+  return a;
+}
+
+__global__ void __launch_bounds__(256) deim_rho_kernel(int n, const double* __restrict__ W,
+                                                       int64_t Wstride, int N,
+                                                       const double* __restrict__ c,
+                                                       const double* __restrict__ v,
+                                                       const uint8_t* __restrict__ excl,
+                                                       double* __restrict__ rho,
+                                                       ArgMax* __restrict__ part_arg,
+                                                       double* __restrict__ part_max) {
+  __shared__ ArgMax sa[256];
+  __shared__ double sv[256], sr[256];
+  const int64_t n3 = (int64_t)n * n * n;
+  const int64_t X = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  ArgMax best{-1.0, INT64_MAX};
+  double mv = 0.0, mr = 0.0;
+  if (X < n3) {
+    const int i = X % n, j = (X / n) % n, k = X / ((int64_t)n * n);
+    double r = v[X];
+    for (int q = 0; q < N; ++q) r -= W[q * Wstride + X] * c[q];
+    const bool interior = i && j && k;
+    if (!interior) r = 0.0;
+    rho[X] = r;
+    if (interior) {
+      mv = fabs(v[X]);
+      mr = fabs(r);
+      if (!(excl && excl[X])) best = ArgMax{fabs(r), X};
+    }
+  }
+  sa[threadIdx.x] = best;
+  sv[threadIdx.x] = mv;
+  sr[threadIdx.x] = mr;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      sa[threadIdx.x] = better(sa[threadIdx.x], sa[threadIdx.x + s]);
+      sv[threadIdx.x] = fmax(sv[threadIdx.x], sv[threadIdx.x + s]);
+      sr[threadIdx.x] = fmax(sr[threadIdx.x], sr[threadIdx.x + s]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part_arg[blockIdx.x] = sa[0];
+    part_max[2 * blockIdx.x] = sv[0];
+    part_max[2 * blockIdx.x + 1] = sr[0];
+  }
+}
+
+__global__ void deim_final_kernel(int nblocks, const ArgMax* __restrict__ part_arg,
+                                  const double* __restrict__ part_max,
+                                  const double* __restrict__ rho, int64_t* out_idx,
+                                  double* out_vals) {
+  __shared__ ArgMax sa[256];
+  __shared__ double sv[256], sr[256];
+  ArgMax best{-1.0, INT64_MAX};
+  double mv = 0.0, mr = 0.0;
+  for (int b = threadIdx.x; b < nblocks; b += 256) {
+    best = better(best, part_arg[b]);
+    mv = fmax(mv, part_max[2 * b]);
+    mr = fmax(mr, part_max[2 * b + 1]);
+  }
+  sa[threadIdx.x] = best;
+  sv[threadIdx.x] = mv;
+  sr[threadIdx.x] = mr;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      sa[threadIdx.x] = better(sa[threadIdx.x], sa[threadIdx.x + s]);
+      sv[threadIdx.x] = fmax(sv[threadIdx.x], sv[threadIdx.x + s]);
+      sr[threadIdx.x] = fmax(sr[threadIdx.x], sr[threadIdx.x + s]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const int64_t idx = sa[0].i;
+    out_idx[0] = (sa[0].v >= 0.0) ? idx : -1;
+    out_vals[0] = (sa[0].v >= 0.0) ? rho[idx] : 0.0;  // pivot
+    out_vals[1] = sv[0];                              // max |v|
+    out_vals[2] = sr[0];                              // max |rho|
+  }
+}
+
+__global__ void __launch_bounds__(256) scale_kernel(int64_t n3, double* __restrict__ col,
+                                                    const double* __restrict__ vals) {
+  const int64_t X = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const double piv = vals[0];
+  if (X < n3 && piv != 0.0) col[X] = col[X] / piv;
+}
+
+cudaError_t deim_step(int n, const double* W, int64_t Wstride, int N, const double* c,
+                      const double* v, const uint8_t* excl, double* col, int64_t* out_idx,
+                      double* out_vals, void* scratch, cudaStream_t stream) {
+  const int64_t n3 = (int64_t)n * n * n;
+  const int nb = (int)((n3 + 255) / 256);
+  ArgMax* pa = (ArgMax*)scratch;
+  double* pm = (double*)(pa + nb);
+  count_launch();
+  deim_rho_kernel<<<nb, 256, 0, stream>>>(n, W, Wstride, N, c, v, excl, col, pa, pm);
+  count_launch();
+  deim_final_kernel<<<1, 256, 0, stream>>>(nb, pa, pm, col, out_idx, out_vals);
+  count_launch();
+  scale_kernel<<<nb, 256, 0, stream>>>(n3, col, out_vals);
+  return cudaGetLastError();
+}
+
+size_t deim_scratch_bytes(int n) {
+  const int64_t n3 = (int64_t)n * n * n;
+  const int64_t nb = (n3 + 255) / 256;
+  return nb * (sizeof(ArgMax) + 2 * sizeof(double)) + 64;
+}
+
+// ---------------------------------------------------------------- dense solve
+__global__ void dense_solve_kernel(int m, const double* __restrict__ Ain,
+                                   const double* __restrict__ bin, double* __restrict__ x,
+                                   int* status) {
+  extern __shared__ double A[];  // [m][m+1]
+  const int w = m + 1;
+  for (int t = threadIdx.x; t < m * m; t += blockDim.x) A[(t / m) * w + t % m] = Ain[t];
+  for (int t = threadIdx.x; t < m; t += blockDim.x) A[t * w + m] = bin[t];
+  __shared__ int piv;
+  __shared__ int sing;
+  if (threadIdx.x == 0) sing = 0;
+  __syncthreads();
+  for (int c = 0; c < m; ++c) {
+    if (threadIdx.x == 0) {
+      int p = c;
+      double best = fabs(A[c * w + c]);
+      for (int r = c + 1; r < m; ++r)
+        if (fabs(A[r * w + c]) > best) { best = fabs(A[r * w + c]); p = r; }
+      piv = p;
+      if (best == 0.0) sing = 1;
+    }
+    __syncthreads();
+    if (piv != c)
+      for (int t = threadIdx.x; t <= m; t += blockDim.x) {
+        const double tmp = A[c * w + t];
+        A[c * w + t] = A[piv * w + t];
+        A[piv * w + t] = tmp;
+      }
+    __syncthreads();
+    const double d = A[c * w + c];
+    for (int r = c + 1 + threadIdx.x; r < m; r += blockDim.x) {
+      const double f = (d != 0.0) ? A[r * w + c] / d : 0.0;
+      for (int t = c; t <= m; ++t) A[r * w + t] -= f * A[c * w + t];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    for (int r = m - 1; r >= 0; --r) {
+      double s = A[r * w + m];
+      for (int t = r + 1; t < m; ++t) s -= A[r * w + t] * x[t];
+      x[r] = (A[r * w + r] != 0.0) ? s / A[r * w + r] : 0.0;
+    }
+    if (status) status[0] = sing;
+  }
+}
+
+cudaError_t dense_solve(int m, const double* A, const double* b, double* x, int* status,
+                        cudaStream_t stream) {
+  const size_t smem = sizeof(double) * (size_t)m * (m + 1);
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(dense_solve_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  count_launch();
+  dense_solve_kernel<<<1, 128, smem, stream>>>(m, A, b, x, status);
+  return cudaGetLastError();
+}
+
+}  // namespace rbws

@@ -1,0 +1,571 @@
+// Batched MGCG runtime (host C++ orchestrating the sm_100a kernels).
+//
+// Restates, batched over parameter instances:
+//   ParametricProblem hierarchy + termwise Galerkin coarsening  (reference grid.py:231-262)
+//   mg_context_for: per-mu operators on every level + Cholesky   (multigrid.py:530-541, 493-507)
+//   mg_vcycle with damped-Jacobi pre/post sweeps                  (multigrid.py:544-561, kernels.py:98-115)
+//   pcg_solve                                                      (krylov.py:267-334)
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "solver.cuh"
+
+static thread_local std::string g_err;
+
+int rbws_set_error(const char* msg, const char* file, int line) {
+  char buf[512];
+  snprintf(buf, sizeof(buf), "%s (%s:%d)", msg, file, line);
+  g_err = buf;
+  return 1;
+}
+
+const char* rbws_get_error() { return g_err.c_str(); }
+
+#define RBWS_FAIL(msg) return rbws_set_error(msg, __FILE__, __LINE__)
+
+namespace rbws {
+
+static std::atomic<int64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+template <class T>
+static cudaError_t dalloc(T** p, size_t count) {
+  return cudaMalloc((void**)p, count * sizeof(T) + 16);
+}
+
+// ------------------------------------------------------------ hierarchy
+
+Hierarchy::~Hierarchy() {
+  cudaFree(d_face);
+  cudaFree(d_node);
+  for (double* p : d_fac) cudaFree(p);
+}
+
+// 1D Galerkin product P^T T P of a tridiagonal interior operator
+// (diag[i], upper[i] = T(i,i+1)) with linear interpolation nc -> 2nc.
+static void galerkin_1d(const double* df, const double* uf, int nf, double* dc, double* uc) {
+  const int nc = nf / 2;
+  auto T = [&](int i, int j) -> double {
+    if (i < 1 || j < 1 || i > nf - 1 || j > nf - 1) return 0.0;
+    if (i == j) return df[i];
+    if (j == i + 1) return uf[i];
+    if (i == j + 1) return uf[j];
+    return 0.0;
+  };
+  auto P = [&](int i, int I) -> double {
+    if (i == 2 * I) return 1.0;
+    if (i == 2 * I - 1 || i == 2 * I + 1) return 0.5;
+    return 0.0;
+  };
+  for (int I = 0; I <= nc; ++I) { dc[I] = 0.0; uc[I] = 0.0; }
+  for (int I = 1; I <= nc - 1; ++I) {
+    for (int J = I; J <= I + 1 && J <= nc - 1; ++J) {
+      double acc = 0.0;
+      for (int i = 2 * I - 1; i <= 2 * I + 1; ++i)
+        for (int j = 2 * J - 1; j <= 2 * J + 1; ++j) {
+          const double t = T(i, j);
+          if (t != 0.0) acc += P(i, I) * t * P(j, J);
+        }
+      if (J == I) dc[I] = acc; else uc[I] = acc;
+    }
+  }
+}
+
+int kron_factors(int n, int m0, int Q, const double* face, const double* node,
+                 std::vector<int>& cells, std::vector<std::vector<double>>& fac) {
+  if (Q < 1 || Q > kMaxTerms) RBWS_FAIL("number of affine terms must be in [1, 8]");
+  if (m0 < 2) RBWS_FAIL("base grid needs at least 2 cells per dimension");
+  if (n % m0) RBWS_FAIL("n must be m0 * 2^J");
+  int r = n / m0;
+  if (r & (r - 1)) RBWS_FAIL("n must be m0 * 2^J");
+  if (r < 2) RBWS_FAIL("need at least 2 levels for coarse-grid correction");
+  cells.clear();
+  for (int c = m0; c <= n; c *= 2) cells.push_back(c);
+  const int L = (int)cells.size();
+  fac.assign(L, std::vector<double>());
+  {
+    const int n1 = n + 1;
+    std::vector<double>& f = fac[L - 1];
+    f.assign((size_t)Q * 3 * 3 * 2 * n1, 0.0);
+    for (int q = 0; q < Q; ++q)
+      for (int d = 0; d < 3; ++d)
+        for (int a = 0; a < 3; ++a) {
+          double* dg = &f[(((size_t)(q * 3 + d) * 3 + a) * 2 + 0) * n1];
+          double* up = &f[(((size_t)(q * 3 + d) * 3 + a) * 2 + 1) * n1];
+          if (a == d) {
+            const double* F = face + (size_t)(q * 3 + d) * n;
+            for (int i = 1; i <= n - 1; ++i) dg[i] = F[i - 1] + F[i];
+            for (int i = 1; i <= n - 2; ++i) up[i] = -F[i];
+          } else {
+            const double* N = node + ((size_t)(q * 3 + d) * 3 + a) * n1;
+            for (int i = 1; i <= n - 1; ++i) dg[i] = N[i];
+          }
+        }
+  }
+  for (int l = L - 2; l >= 0; --l) {
+    const int nf = cells[l + 1], nc = cells[l];
+    const int nf1 = nf + 1, nc1 = nc + 1;
+    std::vector<double>& fc = fac[l];
+    const std::vector<double>& ff = fac[l + 1];
+    fc.assign((size_t)Q * 3 * 3 * 2 * nc1, 0.0);
+    for (int t = 0; t < Q * 3; ++t)
+      for (int a = 0; a < 3; ++a)
+        galerkin_1d(&ff[((size_t)t * 3 + a) * 2 * nf1], &ff[(((size_t)t * 3 + a) * 2 + 1) * nf1], nf,
+                    &fc[((size_t)t * 3 + a) * 2 * nc1], &fc[(((size_t)t * 3 + a) * 2 + 1) * nc1]);
+  }
+  return 0;
+}
+
+int hierarchy_create(Hierarchy** out, int n, int m0, int Q, const double* face,
+                     const double* node) {
+  if (n < 8) RBWS_FAIL("finest grid must have at least 8 cells");
+  if ((m0 - 1) * (m0 - 1) * (m0 - 1) > 125) RBWS_FAIL("coarsest grid too large (m0 <= 6)");
+  Hierarchy* h = new Hierarchy();
+  h->n = n; h->m0 = m0; h->Q = Q;
+  if (kron_factors(n, m0, Q, face, node, h->cells, h->h_fac)) { delete h; return 1; }
+  h->levels = (int)h->cells.size();
+  const int L = h->levels;
+  cudaError_t e = dalloc(&h->d_face, (size_t)Q * 3 * n);
+  if (e == cudaSuccess) e = dalloc(&h->d_node, (size_t)Q * 9 * (n + 1));
+  if (e == cudaSuccess) e = cudaMemcpy(h->d_face, face, sizeof(double) * Q * 3 * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(h->d_node, node, sizeof(double) * Q * 9 * (n + 1), cudaMemcpyHostToDevice);
+  h->d_fac.assign(L, nullptr);
+  for (int l = 0; l < L && e == cudaSuccess; ++l) {
+    e = dalloc(&h->d_fac[l], h->h_fac[l].size());
+    if (e == cudaSuccess)
+      e = cudaMemcpy(h->d_fac[l], h->h_fac[l].data(), sizeof(double) * h->h_fac[l].size(),
+                     cudaMemcpyHostToDevice);
+  }
+  if (e != cudaSuccess) { delete h; RBWS_FAIL(cudaGetErrorString(e)); }
+  *out = h;
+  return 0;
+}
+
+// ------------------------------------------------------------ batch
+
+Batch::~Batch() {
+  cudaFree(theta);
+  for (auto& l : lv) {
+    cudaFree(l.b); cudaFree(l.e); cudaFree(l.t1); cudaFree(l.t2); cudaFree(l.t3);
+    cudaFree(l.zero); cudaFree(l.dinv); cudaFree(l.coef);
+  }
+  cudaFree(L0); cudaFree(d_status);
+  cudaFree(r); cudaFree(p); cudaFree(s);
+  cudaFree(rs); cudaFree(alpha); cudaFree(beta); cudaFree(scale);
+  cudaFree(active); cudaFree(iters); cudaFree(pstatus); cudaFree(nactive);
+  cudaFreeHost(h_nactive);
+  cudaFree(partial); cudaFree(partial2); cudaFree(hist);
+  for (cudaEvent_t e : ev) cudaEventDestroy(e);
+}
+
+Sep7 Batch::fine_op() const {
+  Sep7 op;
+  op.n = h->n; op.Q = h->Q; op.face = h->d_face; op.node = h->d_node; op.theta = theta;
+  return op;
+}
+
+int batch_create(Batch** out, Hierarchy* h, int cap, int nu, double omega) {
+  if (cap < 1) RBWS_FAIL("batch capacity must be positive");
+  if (nu < 0) RBWS_FAIL("smoothing count must be non-negative");
+  if (nu == 0) RBWS_FAIL("nu = 0 (no smoothing) is not supported by the batched V-cycle");
+  Batch* b = new Batch();
+  b->h = h; b->cap = cap; b->nu = nu; b->omega = omega;
+  const int L = h->levels;
+  cudaError_t e = dalloc(&b->theta, (size_t)cap * h->Q);
+  b->lv.resize(L);
+  for (int l = 0; l < L && e == cudaSuccess; ++l) {
+    LevelBuf& lb = b->lv[l];
+    lb.n = h->cells[l];
+    const size_t V = (size_t)vec_doubles(lb.n, cap);
+    const size_t n3 = (size_t)lb.n * lb.n * lb.n;
+    auto zalloc = [&](double** p, size_t cnt) {
+      if (e != cudaSuccess) return;
+      e = dalloc(p, cnt);
+      if (e == cudaSuccess) e = cudaMemset(*p, 0, cnt * sizeof(double));
+    };
+    zalloc(&lb.t1, V);
+    zalloc(&lb.dinv, V);
+    if (nu != 1) { zalloc(&lb.t2, V); zalloc(&lb.t3, V); zalloc(&lb.zero, V); }
+    if (l < L - 1) {
+      zalloc(&lb.b, V);
+      zalloc(&lb.e, V);
+      zalloc(&lb.coef, 14 * n3 * cap + n3);
+    }
+  }
+  if (e == cudaSuccess) {
+    const int m1 = h->m0 - 1, m = m1 * m1 * m1;
+    e = dalloc(&b->L0, (size_t)cap * m * m);
+  }
+  const size_t VF = (size_t)vec_doubles(h->n, cap);
+  if (e == cudaSuccess) e = dalloc(&b->d_status, cap);
+  for (double** pp : {&b->r, &b->p, &b->s}) {
+    if (e == cudaSuccess) e = dalloc(pp, VF);
+    if (e == cudaSuccess) e = cudaMemset(*pp, 0, VF * sizeof(double));
+  }
+  for (double** pp : {&b->rs, &b->alpha, &b->beta, &b->scale})
+    if (e == cudaSuccess) e = dalloc(pp, cap);
+  for (int** pp : {&b->active, &b->iters, &b->pstatus})
+    if (e == cudaSuccess) e = dalloc(pp, cap);
+  if (e == cudaSuccess) e = dalloc(&b->nactive, 1);
+  if (e == cudaSuccess) e = cudaMallocHost((void**)&b->h_nactive, sizeof(int));
+  if (e == cudaSuccess) {
+    int64_t t = sep7_geom(h->n, 1).tiles;
+    for (int c = 2; c <= cap; c *= 2) t = std::max<int64_t>(t, sep7_geom(h->n, c).tiles);
+    t = std::max<int64_t>(t, sep7_geom(h->n, cap).tiles);
+    t = std::max<int64_t>(t, vec_tiles(h->n));
+    b->partial_cap = t;
+    e = dalloc(&b->partial, (size_t)cap * t);
+    if (e == cudaSuccess) e = dalloc(&b->partial2, (size_t)cap * t);
+  }
+  if (e != cudaSuccess) { delete b; RBWS_FAIL(cudaGetErrorString(e)); }
+  *out = b;
+  return 0;
+}
+
+int batch_setup(Batch* b, const double* theta, int count, cudaStream_t stream) {
+  if (count < 1 || count > b->cap) RBWS_FAIL("batch count outside [1, capacity]");
+  Hierarchy* h = b->h;
+  b->count = count;
+  cudaError_t e = cudaMemcpyAsync(b->theta, theta, sizeof(double) * count * h->Q,
+                                  cudaMemcpyDeviceToDevice, stream);
+  if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+  const int L = h->levels;
+  LaunchCtx lc{stream, nullptr};
+  // fine level 1/diag
+  e = sep7_launch(b->fine_op(), count, MODE_DINV, DOT_NONE, nullptr, nullptr, nullptr,
+                  b->lv[L - 1].dinv, nullptr, b->omega, lc);
+  for (int l = 0; l < L - 1 && e == cudaSuccess; ++l)
+    e = st27_build(h->cells[l], h->Q, h->d_fac[l], b->theta, count, b->lv[l].coef,
+                   b->lv[l].dinv, stream);
+  if (e == cudaSuccess) e = coarse_factor(h->m0, count, b->lv[0].coef, b->L0, b->d_status, stream);
+  if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+  return 0;
+}
+
+int Batch::prof_begin(cudaStream_t s) {
+  if (ev_used + 2 > ev.size()) {
+    for (int k = 0; k < 64; ++k) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev.push_back(e);
+    }
+  }
+  const int idx = (int)ev_used++;
+  cudaEventRecord(ev[idx], s);
+  return idx;
+}
+
+void Batch::prof_end(int cls, int start, cudaStream_t s) {
+  const int idx = (int)ev_used++;
+  cudaEventRecord(ev[idx], s);
+  recs.push_back({cls, start, idx, cur_active});
+}
+
+void Batch::prof_flush() {
+  for (auto& r : recs) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ev[r[1]], ev[r[2]]) == cudaSuccess) {
+      prof_ms[r[0]] += ms;
+      prof_calls[r[0]] += 1;
+      prof_units[r[0]] += r[3];
+    }
+  }
+  recs.clear();
+  ev_used = 0;
+}
+
+// one V-cycle for A^lvl out = b from zero, per active instance
+int Batch::vcycle(int lvl, const double* bb, double* out, double* dot_partial,
+                  const LaunchCtx& lc) {
+  cudaError_t e = cudaSuccess;
+  if (lvl == 0) {
+    e = coarse_solve(h->m0, count, L0, bb, out, lc);
+    if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+    return 0;
+  }
+  const bool fine = (lvl == h->levels - 1);
+  LevelBuf& l = lv[lvl];
+  LevelBuf& c = lv[lvl - 1];
+  const int n = l.n;
+  auto op = [&](int mode, int dot, const double* x, const double* rhs, double* y,
+                double* part) -> cudaError_t {
+    if (fine) return sep7_launch(fine_op(), count, mode, dot, x, rhs, l.dinv, y, part, omega, lc);
+    St27 s27{n, l.coef};
+    return st27_launch(s27, count, mode, x, rhs, l.dinv, y, omega, lc);
+  };
+  const int fdot = (fine && dot_partial) ? DOT_BY : DOT_NONE;
+  const bool pf = fine && prof_on;
+  if (nu == 1) {
+    int t0 = pf ? prof_begin(lc.stream) : -1;
+    e = op(MODE_PRE, DOT_NONE, nullptr, bb, l.t1, nullptr);
+    if (pf) { prof_end(PROF_FINE_PRE, t0, lc.stream); t0 = prof_begin(lc.stream); }
+    if (e == cudaSuccess) e = restrict_launch(n, count, l.t1, c.b, lc);
+    if (pf) { prof_end(PROF_FINE_RESTRICT, t0, lc.stream); t0 = prof_begin(lc.stream); }
+    if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+    if (vcycle(lvl - 1, c.b, c.e, nullptr, lc)) return 1;
+    if (pf) { prof_end(PROF_COARSE, t0, lc.stream); t0 = prof_begin(lc.stream); }
+    e = prolong_launch(n, count, 1, c.e, l.t1, bb, l.dinv, omega, lc);
+    if (pf) { prof_end(PROF_FINE_PROLONG, t0, lc.stream); t0 = prof_begin(lc.stream); }
+    if (e == cudaSuccess) e = op(MODE_JACOBI, fdot, l.t1, bb, out, dot_partial);
+    if (pf) prof_end(PROF_FINE_POST, t0, lc.stream);
+    if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+    return 0;
+  }
+  // generic nu: u in t1/t2 ping-pong, residual in t3
+  double* u = l.zero;
+  double* bufs[2] = {l.t1, l.t2};
+  int nb = 0;
+  for (int s = 0; s < nu && e == cudaSuccess; ++s) {
+    e = op(MODE_JACOBI, DOT_NONE, u, bb, bufs[nb], nullptr);
+    u = bufs[nb];
+    nb ^= 1;
+  }
+  if (e == cudaSuccess) e = op(MODE_RESID, DOT_NONE, u, bb, l.t3, nullptr);
+  if (e == cudaSuccess) e = restrict_launch(n, count, l.t3, c.b, lc);
+  if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+  if (vcycle(lvl - 1, c.b, c.e, nullptr, lc)) return 1;
+  if (nu == 0) {
+    // u = P e (u currently the zero vector): write into out
+    e = vec_copy(n, count, l.zero, (int64_t)n * n * n, out, lc);
+    if (e == cudaSuccess) e = prolong_launch(n, count, 0, c.e, out, nullptr, nullptr, 0.0, lc);
+    if (e == cudaSuccess && fine && dot_partial)
+      e = vec_dot(n, count, bb, (int64_t)n * n * n, out, (int64_t)n * n * n, dot_partial, lc);
+    if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+    return 0;
+  }
+  e = prolong_launch(n, count, 0, c.e, u, nullptr, nullptr, 0.0, lc);
+  for (int s = 0; s < nu && e == cudaSuccess; ++s) {
+    const bool last = (s == nu - 1);
+    double* dst = last ? out : (u == l.t1 ? l.t2 : l.t1);
+    e = op(MODE_JACOBI, last ? fdot : DOT_NONE, u, bb, dst, last ? dot_partial : nullptr);
+    u = dst;
+  }
+  if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+  return 0;
+}
+
+// ------------------------------------------------------------ PCG scalars
+
+// one warp per instance: deterministic sum of `tiles` partials
+__device__ __forceinline__ double warp_sum_partials(const double* part, int tiles) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int t = lane; t < tiles; t += 32) s += part[t];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  return __shfl_sync(0xffffffffu, s, 0);
+}
+
+#define WARP_MU                                                       \
+  const int mu = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); \
+  const int lane = threadIdx.x & 31;                                  \
+  if (mu >= count) return;
+
+__global__ void pcg_init_kernel(int count, const double* pf, int ftiles, int fshared,
+                                const double* prr, int tiles, double delta, int l_max,
+                                double* scale, double* hist, int hist_len, int* active,
+                                int* iters, int* status, int* nactive) {
+  WARP_MU
+  const double ff = warp_sum_partials(pf + (fshared ? 0 : (int64_t)mu * ftiles), ftiles);
+  const double rr = warp_sum_partials(prr + (int64_t)mu * tiles, tiles);
+  if (lane == 0) {
+    const double fn = sqrt(ff);
+    const double sc = (fn == 0.0) ? 1.0 : fn;
+    scale[mu] = sc;
+    const double h0 = sqrt(rr) / sc;
+    double* H = hist + (int64_t)mu * hist_len;
+    H[0] = h0;
+    for (int k = 1; k < hist_len; ++k) H[k] = nan("");
+    iters[mu] = 0;
+    status[mu] = (fn == 0.0) ? 4 : 0;  // bit 2: absolute norms
+    const int a = (h0 > delta && l_max > 0) ? 1 : 0;
+    active[mu] = a;
+    if (a) atomicAdd(nactive, 1);
+  }
+}
+
+__global__ void pcg_rs_kernel(int count, const double* prs, int tiles, double* rs,
+                              const int* active) {
+  WARP_MU
+  if (!active[mu]) return;
+  const double v = warp_sum_partials(prs + (int64_t)mu * tiles, tiles);
+  if (lane == 0) rs[mu] = v;
+}
+
+__global__ void pcg_alpha_kernel(int count, const double* ppap, int tiles, const double* rs,
+                                 double* alpha, int* active, int* status) {
+  WARP_MU
+  if (!active[mu]) return;
+  const double pap = warp_sum_partials(ppap + (int64_t)mu * tiles, tiles);
+  if (lane == 0) {
+    if (!(pap > 0.0)) {
+      status[mu] |= 1;  // non-positive curvature: operator not SPD
+      active[mu] = 0;
+      alpha[mu] = 0.0;
+    } else {
+      alpha[mu] = rs[mu] / pap;
+    }
+  }
+}
+
+__global__ void pcg_check_kernel(int count, const double* prr, int tiles, const double* scale,
+                                 double delta, int l_max, double* hist, int hist_len,
+                                 int* active, int* iters, int* nactive) {
+  WARP_MU
+  if (!active[mu]) return;
+  const double rr = warp_sum_partials(prr + (int64_t)mu * tiles, tiles);
+  if (lane == 0) {
+    const double rel = sqrt(rr) / scale[mu];
+    const int k = iters[mu] + 1;
+    iters[mu] = k;
+    hist[(int64_t)mu * hist_len + k] = rel;
+    if (rel <= delta || k >= l_max) active[mu] = 0;
+    else atomicAdd(nactive, 1);
+  }
+}
+
+__global__ void pcg_beta_kernel(int count, const double* prs, int tiles, double* rs,
+                                double* beta, const int* active) {
+  WARP_MU
+  if (!active[mu]) return;
+  const double v = warp_sum_partials(prs + (int64_t)mu * tiles, tiles);
+  if (lane == 0) {
+    beta[mu] = v / rs[mu];
+    rs[mu] = v;
+  }
+}
+
+__global__ void pcg_true_kernel(int count, const double* prr, int tiles, const double* scale,
+                                double* out) {
+  WARP_MU
+  const double rr = warp_sum_partials(prr + (int64_t)mu * tiles, tiles);
+  if (lane == 0) out[mu] = sqrt(rr) / scale[mu];
+}
+
+static inline dim3 warp_grid(int count) { return dim3((count + 7) / 8); }
+
+int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double delta, int l_max,
+              const PcgOut& out, cudaStream_t stream) {
+  if (!(delta > 0)) RBWS_FAIL("tolerance must be positive");
+  if (l_max < 0) RBWS_FAIL("l_max must be non-negative");
+  Hierarchy* h = b->h;
+  const int count = b->count;
+  if (count < 1) RBWS_FAIL("batch_setup must be called before solving");
+  const int n = h->n;
+  const int64_t n3 = (int64_t)n * n * n;
+  const int L = h->levels;
+  const int hist_len = l_max + 1;
+  cudaError_t e = cudaSuccess;
+  if (hist_len * b->cap > b->hist_len * b->cap || !b->hist) {
+    cudaFree(b->hist);
+    e = dalloc(&b->hist, (size_t)b->cap * hist_len);
+    if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+    b->hist_len = hist_len;
+  }
+  const int hl = b->hist_len;
+  const Sep7 op = b->fine_op();
+  const Sep7Geom g = sep7_geom(n, count);
+  const int tiles = g.tiles;
+  LaunchCtx all{stream, nullptr};
+  LaunchCtx act{stream, b->active};
+  const int fshared = (f_stride == 0);
+  const int ftiles = vec_tiles(n);
+  // ||f||
+  e = vec_dot(n, fshared ? 1 : count, f, f_stride, f, f_stride, b->partial2, all);
+  // r = f - A x0, ||r||^2
+  if (e == cudaSuccess && fshared) {
+    e = vec_copy(n, count, f, 0, b->s, all);  // s <- broadcast f
+    if (e == cudaSuccess)
+      e = sep7_launch(op, count, MODE_RESID, DOT_YY, x, b->s, nullptr, b->r, b->partial, 0.0, all);
+  } else if (e == cudaSuccess) {
+    e = sep7_launch(op, count, MODE_RESID, DOT_YY, x, f, nullptr, b->r, b->partial, 0.0, all);
+  }
+  if (e == cudaSuccess) e = cudaMemsetAsync(b->nactive, 0, sizeof(int), stream);
+  if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+  count_launch();
+  pcg_init_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial2, ftiles, fshared,
+                                                        b->partial, tiles, delta, l_max, b->scale,
+                                                        b->hist, hl, b->active, b->iters,
+                                                        b->pstatus, b->nactive);
+  e = cudaMemcpyAsync(b->h_nactive, b->nactive, sizeof(int), cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+  b->cur_active = *b->h_nactive;
+  if (*b->h_nactive > 0) {
+    if (b->vcycle(L - 1, b->r, b->s, b->partial, act)) return 1;
+    count_launch();
+    pcg_rs_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, tiles, b->rs, b->active);
+    e = vec_copy(n, count, b->s, n3, b->p, act);
+    if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+    const bool pf = b->prof_on;
+    for (int k = 0; k < l_max; ++k) {
+      int t0 = pf ? b->prof_begin(stream) : -1;
+      e = sep7_launch(op, count, MODE_APPLY, DOT_XAX, b->p, nullptr, nullptr, nullptr, b->partial,
+                      0.0, act);
+      if (pf) { b->prof_end(PROF_FINE_APPLY_DOT, t0, stream); t0 = b->prof_begin(stream); }
+      if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+      count_launch();
+      pcg_alpha_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, tiles, b->rs,
+                                                             b->alpha, b->active, b->pstatus);
+      if (pf) { b->prof_end(PROF_SCALARS, t0, stream); t0 = b->prof_begin(stream); }
+      e = sep7_cg_update(op, count, b->p, x, b->r, b->alpha, b->partial, act);
+      if (pf) { b->prof_end(PROF_FINE_CG_UPDATE, t0, stream); t0 = b->prof_begin(stream); }
+      if (e == cudaSuccess) e = cudaMemsetAsync(b->nactive, 0, sizeof(int), stream);
+      if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+      count_launch();
+      pcg_check_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, tiles, b->scale,
+                                                             delta, l_max, b->hist, hl, b->active,
+                                                             b->iters, b->nactive);
+      if (pf) b->prof_end(PROF_SCALARS, t0, stream);
+      e = cudaMemcpyAsync(b->h_nactive, b->nactive, sizeof(int), cudaMemcpyDeviceToHost, stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+      if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+      if (*b->h_nactive == 0) break;
+      b->cur_active = *b->h_nactive;
+      if (b->vcycle(L - 1, b->r, b->s, b->partial, act)) return 1;
+      if (pf) t0 = b->prof_begin(stream);
+      count_launch();
+      pcg_beta_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, tiles, b->rs,
+                                                            b->beta, b->active);
+      if (pf) { b->prof_end(PROF_SCALARS, t0, stream); t0 = b->prof_begin(stream); }
+      e = vec_xpby(n, count, b->s, b->beta, b->p, act);
+      if (pf) b->prof_end(PROF_FINE_XPBY, t0, stream);
+      if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+    }
+  }
+  // true residual ||f - A x|| / scale for every instance
+  const double* fb = fshared ? b->s : f;
+  if (fshared) e = vec_copy(n, count, f, 0, b->s, all);
+  if (e == cudaSuccess)
+    e = sep7_launch(op, count, MODE_RESID, DOT_YY, x, fb, nullptr, b->p, b->partial, 0.0, all);
+  if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+  double* d_true = b->beta;  // reuse as scratch
+  count_launch();
+  pcg_true_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, tiles, b->scale, d_true);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+  // results to host
+  std::vector<double> hh((size_t)count * hl);
+  e = cudaMemcpyAsync(hh.data(), b->hist, sizeof(double) * count * hl, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess && out.iters)
+    e = cudaMemcpyAsync(out.iters, b->iters, sizeof(int) * count, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess && out.true_res)
+    e = cudaMemcpyAsync(out.true_res, d_true, sizeof(double) * count, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess && out.status)
+    e = cudaMemcpyAsync(out.status, b->pstatus, sizeof(int) * count, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+  if (b->prof_on) b->prof_flush();
+  if (out.hist)
+    for (int m = 0; m < count; ++m)
+      memcpy(out.hist + (size_t)m * hist_len, hh.data() + (size_t)m * hl, sizeof(double) * hist_len);
+  if (out.status && out.true_res)
+    for (int m = 0; m < count; ++m)
+      if (!(out.status[m] & 1) && !(out.true_res[m] <= delta)) out.status[m] |= 2;
+  return 0;
+}
+
+}  // namespace rbws

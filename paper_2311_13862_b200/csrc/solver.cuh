@@ -1,0 +1,105 @@
+// Native runtime of the batched MGCG path: the multigrid hierarchy of a
+// separable affine problem (mu-independent), the per-batch context
+// (mu-dependent coarse operators, Cholesky factors, work vectors), the
+// batched V-cycle and the batched PCG driver.
+#pragma once
+
+#include <array>
+#include <vector>
+
+#include "stencil.cuh"
+
+namespace rbws {
+
+struct Hierarchy {
+  int n = 0, m0 = 0, levels = 0, Q = 0;
+  std::vector<int> cells;           // coarse (0) .. fine (levels-1)
+  double* d_face = nullptr;         // fine separable tables
+  double* d_node = nullptr;
+  std::vector<double*> d_fac;       // per level 1D Kronecker factors [Q*3][3][2][n+1]
+  std::vector<std::vector<double>> h_fac;
+
+  ~Hierarchy();
+};
+
+int kron_factors(int n, int m0, int Q, const double* face, const double* node,
+                 std::vector<int>& cells, std::vector<std::vector<double>>& fac);
+int hierarchy_create(Hierarchy** out, int n, int m0, int Q, const double* face,
+                     const double* node);
+
+struct LevelBuf {
+  int n = 0;
+  double* b = nullptr;     // level rhs (coarse levels)
+  double* e = nullptr;     // level correction (coarse levels)
+  double* t1 = nullptr;    // scratch
+  double* t2 = nullptr;    // scratch (nu != 1)
+  double* t3 = nullptr;    // scratch (nu != 1)
+  double* zero = nullptr;  // zeros (nu != 1)
+  double* dinv = nullptr;  // 1/diag per instance
+  double* coef = nullptr;  // 27-point coefficients (coarse levels)
+};
+
+// kernel classes timed by the optional event profiler (bench.py roofline)
+enum ProfClass : int {
+  PROF_FINE_APPLY_DOT = 0,  // p . A p                     (reads p)
+  PROF_FINE_CG_UPDATE = 1,  // x += a p, r -= a A p, |r|^2 (reads p x r, writes x r)
+  PROF_FINE_PRE = 2,        // r1 = b - A(w D^-1 b)        (reads b dinv, writes r1)
+  PROF_FINE_RESTRICT = 3,   // bc = P^T r1
+  PROF_FINE_PROLONG = 4,    // u0 = w D^-1 b + P e
+  PROF_FINE_POST = 5,       // s = u0 + w (b - A u0)/d, r.s
+  PROF_FINE_XPBY = 6,       // p = s + beta p
+  PROF_COARSE = 7,          // all coarse levels of one V-cycle
+  PROF_SCALARS = 8,         // per-instance scalar kernels
+  PROF_NCLASS = 9
+};
+
+struct Batch {
+  Hierarchy* h = nullptr;
+  int cap = 0, count = 0, nu = 1;
+  double omega = 0.7;
+  double* theta = nullptr;          // [cap][Q]
+  std::vector<LevelBuf> lv;
+  double* L0 = nullptr;             // coarsest Cholesky factors [cap][m][m]
+  int* d_status = nullptr;          // coarse factor status per instance
+  // PCG state (fine level)
+  double *r = nullptr, *p = nullptr, *s = nullptr;
+  double *rs = nullptr, *alpha = nullptr, *beta = nullptr, *scale = nullptr;
+  int *active = nullptr, *iters = nullptr, *pstatus = nullptr, *nactive = nullptr;
+  int* h_nactive = nullptr;         // pinned
+  double* partial = nullptr;        // [cap][max tiles]
+  double* partial2 = nullptr;
+  double* hist = nullptr;           // [cap][hist_len]
+  int hist_len = 0;
+  int64_t partial_cap = 0;
+
+  bool prof_on = false;
+  std::vector<cudaEvent_t> ev;
+  size_t ev_used = 0;
+  std::vector<std::array<int, 4>> recs;
+  double prof_ms[PROF_NCLASS] = {0};
+  int64_t prof_calls[PROF_NCLASS] = {0};
+  int64_t prof_units[PROF_NCLASS] = {0};  // instance-launches (active instances summed)
+  int cur_active = 0;                     // host-known active instances
+  int prof_begin(cudaStream_t s);
+  void prof_end(int cls, int start, cudaStream_t s);
+  void prof_flush();
+
+  ~Batch();
+  Sep7 fine_op() const;
+  int vcycle(int lvl, const double* b, double* out, double* dot_partial, const LaunchCtx& lc);
+};
+
+int batch_create(Batch** out, Hierarchy* h, int cap, int nu, double omega);
+int batch_setup(Batch* b, const double* theta, int count, cudaStream_t stream);
+
+struct PcgOut {
+  int* iters;          // host [count]
+  double* hist;        // host [count][l_max+1] (NaN padded)
+  double* true_res;    // host [count]
+  int* status;         // host [count]: 0 ok, 1 breakdown (non-SPD), 2 not converged
+};
+
+int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double delta, int l_max,
+              const PcgOut& out, cudaStream_t stream);
+
+}  // namespace rbws

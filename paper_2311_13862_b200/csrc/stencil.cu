@@ -1,0 +1,704 @@
+// Batched stencil / transfer / vector kernels (sm_100a).
+//
+// Finest level: matrix-free separable 7-point operator.  One thread owns a
+// grid column (i, j) of one parameter instance and marches in z: the
+// Kronecker factors of the affine terms reduce to 5Q per-column constants
+// held in registers, so each face weight costs Q FMAs and the z-neighbours
+// of the input stay in registers.  Lateral neighbours come through L1.
+// Coarse levels: per-instance symmetric 27-point stencils (14 stored
+// coefficients per node) produced by the batched affine assembly st27_build.
+#include "stencil.cuh"
+
+namespace rbws {
+
+// ========================================================================
+// finest level: separable 7-point
+// ========================================================================
+
+Sep7Geom sep7_geom(int n, int batch) {
+  Sep7Geom g;
+  g.tx = n < 32 ? n : 32;
+  g.ty = 256 / g.tx;
+  if (g.ty > n) g.ty = n;
+  int bxy = (n / g.tx) * (n / g.ty);
+  g.zc = 1;
+  while ((int64_t)bxy * batch * g.zc < 4 * 148 && g.zc * 8 <= n) g.zc *= 2;
+  g.tiles = bxy * g.zc;
+  return g;
+}
+
+template <int Q>
+struct ColConst {
+  double cxp[Q], cxm[Q], cyp[Q], cym[Q], cz[Q];
+  const double* zx[Q];  // node factor along z of the x-part
+  const double* zy[Q];  // node factor along z of the y-part
+  const double* fz[Q];  // face factor along z of the z-part
+
+  __device__ __forceinline__ void init(const Sep7& op, int mu, int i, int j) {
+    const int n = op.n, n1 = n + 1;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const double t = op.theta[mu * Q + q];
+      const double* F = op.face + (size_t)q * 3 * n;
+      const double* N = op.node + (size_t)q * 9 * n1;
+      const double nxy = N[(0 * 3 + 1) * n1 + j];  // x-part, along y
+      const double nyx = N[(1 * 3 + 0) * n1 + i];  // y-part, along x
+      cxp[q] = t * F[0 * n + i] * nxy;
+      cxm[q] = t * F[0 * n + i - 1] * nxy;
+      cyp[q] = t * F[1 * n + j] * nyx;
+      cym[q] = t * F[1 * n + j - 1] * nyx;
+      cz[q] = t * N[(2 * 3 + 0) * n1 + i] * N[(2 * 3 + 1) * n1 + j];
+      zx[q] = N + (0 * 3 + 2) * n1;
+      zy[q] = N + (1 * 3 + 2) * n1;
+      fz[q] = F + 2 * n;
+    }
+  }
+  __device__ __forceinline__ double wz(int k) const {  // z-face between k, k+1
+    double w = 0.0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) w = fma(cz[q], __ldg(fz[q] + k), w);
+    return w;
+  }
+  __device__ __forceinline__ void wxy(int k, double& wxp, double& wxm, double& wyp,
+                                      double& wym) const {
+    wxp = wxm = wyp = wym = 0.0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const double a = __ldg(zx[q] + k), b = __ldg(zy[q] + k);
+      wxp = fma(cxp[q], a, wxp);
+      wxm = fma(cxm[q], a, wxm);
+      wyp = fma(cyp[q], b, wyp);
+      wym = fma(cym[q], b, wym);
+    }
+  }
+};
+
+template <int Q, int MODE>
+__global__ void __launch_bounds__(256) sep7_kernel(Sep7 op, int zc, int dot,
+                                                   const double* __restrict__ x,
+                                                   const double* __restrict__ b,
+                                                   const double* __restrict__ dinv,
+                                                   double* __restrict__ y,
+                                                   double* __restrict__ partial,
+                                                   const int* __restrict__ active,
+                                                   double omega) {
+  __shared__ double red[32];
+  const int n = op.n;
+  const int kc = blockIdx.z % zc, mu = blockIdx.z / zc;
+  if (active && !active[mu]) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  const bool valid = (i >= 1) && (j >= 1);
+  const int kz = n / zc;
+  const int kb = max(1, kc * kz), ke = min(n, (kc + 1) * kz);
+  const int64_t n2 = (int64_t)n * n;
+  const int64_t base = (int64_t)mu * n2 * n;
+  double acc = 0.0;
+  if (valid) {
+    ColConst<Q> cc;
+    cc.init(op, mu, i, j);
+    const int64_t col = base + i + (int64_t)n * j;
+    auto ld = [&](int64_t idx) -> double {
+      if (MODE == MODE_PRE) return omega * __ldg(dinv + idx) * __ldg(b + idx);
+      if (MODE == MODE_DINV) return 0.0;
+      return __ldg(x + idx);
+    };
+    double um = ld(col + (int64_t)(kb - 1) * n2);
+    double uc = ld(col + (int64_t)kb * n2);
+    double wzm = cc.wz(kb - 1);
+    for (int k = kb; k < ke; ++k) {
+      const int64_t idx = col + (int64_t)k * n2;
+      const double up = ld(idx + n2);
+      const double ue = ld(idx + 1), uw = ld(idx - 1), un = ld(idx + n), us = ld(idx - n);
+      double wxp, wxm, wyp, wym;
+      cc.wxy(k, wxp, wxm, wyp, wym);
+      const double wzp = cc.wz(k);
+      const double d = ((wxp + wxm) + (wyp + wym)) + (wzp + wzm);
+      double out;
+      if (MODE == MODE_DINV) {
+        out = 1.0 / d;
+      } else {
+        double off = wxp * ue;
+        off = fma(wxm, uw, off);
+        off = fma(wyp, un, off);
+        off = fma(wym, us, off);
+        off = fma(wzp, up, off);
+        off = fma(wzm, um, off);
+        const double Au = fma(d, uc, -off);
+        if (MODE == MODE_APPLY) {
+          out = Au;
+        } else if (MODE == MODE_RESID || MODE == MODE_PRE) {
+          out = __ldg(b + idx) - Au;
+        } else {  // MODE_JACOBI
+          out = uc + omega * (__ldg(b + idx) - Au) / d;
+        }
+        if (dot == DOT_XAX) acc = fma(uc, Au, acc);
+      }
+      if (dot == DOT_YY) acc = fma(out, out, acc);
+      else if (dot == DOT_BY) acc = fma(__ldg(b + idx), out, acc);
+      if (y) y[idx] = out;
+      um = uc;
+      uc = up;
+      wzm = wzp;
+    }
+  }
+  if (dot != DOT_NONE) {
+    const double s = block_reduce_sum(acc, red);
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+      const int tile = (blockIdx.y * gridDim.x + blockIdx.x) * zc + kc;
+      const int tiles = gridDim.x * gridDim.y * zc;
+      partial[(int64_t)mu * tiles + tile] = s;
+    }
+  }
+}
+
+template <int Q>
+__global__ void __launch_bounds__(256) sep7_cg_kernel(Sep7 op, int zc,
+                                                      const double* __restrict__ p,
+                                                      double* __restrict__ x,
+                                                      double* __restrict__ r,
+                                                      const double* __restrict__ alpha,
+                                                      double* __restrict__ partial,
+                                                      const int* __restrict__ active) {
+  __shared__ double red[32];
+  const int n = op.n;
+  const int kc = blockIdx.z % zc, mu = blockIdx.z / zc;
+  if (active && !active[mu]) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  const bool valid = (i >= 1) && (j >= 1);
+  const int kz = n / zc;
+  const int kb = max(1, kc * kz), ke = min(n, (kc + 1) * kz);
+  const int64_t n2 = (int64_t)n * n;
+  const int64_t base = (int64_t)mu * n2 * n;
+  const double a = alpha[mu];
+  double acc = 0.0;
+  if (valid) {
+    ColConst<Q> cc;
+    cc.init(op, mu, i, j);
+    const int64_t col = base + i + (int64_t)n * j;
+    double um = __ldg(p + col + (int64_t)(kb - 1) * n2);
+    double uc = __ldg(p + col + (int64_t)kb * n2);
+    double wzm = cc.wz(kb - 1);
+    for (int k = kb; k < ke; ++k) {
+      const int64_t idx = col + (int64_t)k * n2;
+      const double up = __ldg(p + idx + n2);
+      const double ue = __ldg(p + idx + 1), uw = __ldg(p + idx - 1);
+      const double un = __ldg(p + idx + n), us = __ldg(p + idx - n);
+      double wxp, wxm, wyp, wym;
+      cc.wxy(k, wxp, wxm, wyp, wym);
+      const double wzp = cc.wz(k);
+      const double d = ((wxp + wxm) + (wyp + wym)) + (wzp + wzm);
+      double off = wxp * ue;
+      off = fma(wxm, uw, off);
+      off = fma(wyp, un, off);
+      off = fma(wym, us, off);
+      off = fma(wzp, up, off);
+      off = fma(wzm, um, off);
+      const double Ap = fma(d, uc, -off);
+      x[idx] = fma(a, uc, x[idx]);
+      const double rn = fma(-a, Ap, r[idx]);
+      r[idx] = rn;
+      acc = fma(rn, rn, acc);
+      um = uc;
+      uc = up;
+      wzm = wzp;
+    }
+  }
+  const double s = block_reduce_sum(acc, red);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    const int tile = (blockIdx.y * gridDim.x + blockIdx.x) * zc + kc;
+    const int tiles = gridDim.x * gridDim.y * zc;
+    partial[(int64_t)mu * tiles + tile] = s;
+  }
+}
+
+template <int Q>
+static cudaError_t sep7_launch_q(const Sep7& op, int batch, int mode, int dot, const double* x,
+                                 const double* b, const double* dinv, double* y,
+                                 double* partial, double omega, const LaunchCtx& lc) {
+  Sep7Geom g = sep7_geom(op.n, batch);
+  dim3 blk(g.tx, g.ty), grd(op.n / g.tx, op.n / g.ty, batch * g.zc);
+  count_launch();
+#define RBWS_SEP7_CASE(M)                                                             \
+  case M:                                                                             \
+    sep7_kernel<Q, M><<<grd, blk, 0, lc.stream>>>(op, g.zc, dot, x, b, dinv, y, partial, \
+                                                 lc.active, omega);                   \
+    break;
+  switch (mode) {
+    RBWS_SEP7_CASE(MODE_APPLY)
+    RBWS_SEP7_CASE(MODE_RESID)
+    RBWS_SEP7_CASE(MODE_JACOBI)
+    RBWS_SEP7_CASE(MODE_PRE)
+    RBWS_SEP7_CASE(MODE_DINV)
+    default:
+      return cudaErrorInvalidValue;
+  }
+#undef RBWS_SEP7_CASE
+  return cudaGetLastError();
+}
+
+#define RBWS_Q_DISPATCH(Qv, CALL)        \
+  switch (Qv) {                          \
+    case 1: return CALL(1);              \
+    case 2: return CALL(2);              \
+    case 3: return CALL(3);              \
+    case 4: return CALL(4);              \
+    case 5: return CALL(5);              \
+    case 6: return CALL(6);              \
+    case 7: return CALL(7);              \
+    case 8: return CALL(8);              \
+    default: return cudaErrorInvalidValue; \
+  }
+
+cudaError_t sep7_launch(const Sep7& op, int batch, int mode, int dot, const double* x,
+                        const double* b, const double* dinv, double* y, double* partial,
+                        double omega, const LaunchCtx& lc) {
+#define CALL(QQ) sep7_launch_q<QQ>(op, batch, mode, dot, x, b, dinv, y, partial, omega, lc)
+  RBWS_Q_DISPATCH(op.Q, CALL)
+#undef CALL
+}
+
+template <int Q>
+static cudaError_t sep7_cg_q(const Sep7& op, int batch, const double* p, double* x, double* r,
+                             const double* alpha, double* partial, const LaunchCtx& lc) {
+  Sep7Geom g = sep7_geom(op.n, batch);
+  dim3 blk(g.tx, g.ty), grd(op.n / g.tx, op.n / g.ty, batch * g.zc);
+  count_launch();
+  sep7_cg_kernel<Q><<<grd, blk, 0, lc.stream>>>(op, g.zc, p, x, r, alpha, partial, lc.active);
+  return cudaGetLastError();
+}
+
+cudaError_t sep7_cg_update(const Sep7& op, int batch, const double* p, double* x, double* r,
+                           const double* alpha, double* partial, const LaunchCtx& lc) {
+#define CALL(QQ) sep7_cg_q<QQ>(op, batch, p, x, r, alpha, partial, lc)
+  RBWS_Q_DISPATCH(op.Q, CALL)
+#undef CALL
+}
+
+// ========================================================================
+// coarse levels: per-instance symmetric 27-point
+// ========================================================================
+
+__constant__ int c_off_dx[14], c_off_dy[14], c_off_dz[14];
+
+static bool g_offsets_ready = false;
+static cudaError_t ensure_offsets() {
+  if (g_offsets_ready) return cudaSuccess;
+  int dx[14] = {0}, dy[14] = {0}, dz[14] = {0};
+  for (int o = 1; o < 14; ++o) fwd_offset(o, dx[o], dy[o], dz[o]);
+  cudaError_t e = cudaMemcpyToSymbol(c_off_dx, dx, sizeof(dx));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_off_dy, dy, sizeof(dy));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_off_dz, dz, sizeof(dz));
+  if (e == cudaSuccess) g_offsets_ready = true;
+  return e;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) st27_kernel(St27 op, const double* __restrict__ x,
+                                                   const double* __restrict__ b,
+                                                   const double* __restrict__ dinv,
+                                                   double* __restrict__ y,
+                                                   const int* __restrict__ active,
+                                                   double omega) {
+  const int n = op.n;
+  const int mu = blockIdx.y;
+  if (active && !active[mu]) return;
+  const int64_t n3 = (int64_t)n * n * n;
+  const int64_t X = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (X >= n3) return;
+  const int i = X % n, j = (X / n) % n, k = X / ((int64_t)n * n);
+  if (i == 0 || j == 0 || k == 0) return;
+  const int64_t base = (int64_t)mu * n3;
+  const double* C = op.coef + (int64_t)mu * 14 * n3;
+  auto ld = [&](int64_t idx) -> double {
+    if (MODE == MODE_PRE) return omega * __ldg(dinv + base + idx) * __ldg(b + base + idx);
+    return __ldg(x + base + idx);
+  };
+  const double c0 = __ldg(C + X);
+  double Au = c0 * ld(X);
+#pragma unroll
+  for (int o = 1; o < 14; ++o) {
+    const int64_t off = c_off_dx[o] + (int64_t)n * (c_off_dy[o] + (int64_t)n * c_off_dz[o]);
+    Au = fma(__ldg(C + o * n3 + X), ld(X + off), Au);
+    Au = fma(__ldg(C + o * n3 + X - off), ld(X - off), Au);
+  }
+  double out;
+  if (MODE == MODE_APPLY) out = Au;
+  else if (MODE == MODE_RESID || MODE == MODE_PRE) out = __ldg(b + base + X) - Au;
+  else if (MODE == MODE_JACOBI) out = ld(X) + omega * __ldg(dinv + base + X) * (__ldg(b + base + X) - Au);
+  else out = 1.0 / c0;
+  y[base + X] = out;
+}
+
+cudaError_t st27_launch(const St27& op, int batch, int mode, const double* x, const double* b,
+                        const double* dinv, double* y, double omega, const LaunchCtx& lc) {
+  cudaError_t e = ensure_offsets();
+  if (e != cudaSuccess) return e;
+  const int64_t n3 = (int64_t)op.n * op.n * op.n;
+  dim3 blk(256), grd((unsigned)((n3 + 255) / 256), batch);
+  count_launch();
+  switch (mode) {
+    case MODE_APPLY: st27_kernel<MODE_APPLY><<<grd, blk, 0, lc.stream>>>(op, x, b, dinv, y, lc.active, omega); break;
+    case MODE_RESID: st27_kernel<MODE_RESID><<<grd, blk, 0, lc.stream>>>(op, x, b, dinv, y, lc.active, omega); break;
+    case MODE_JACOBI: st27_kernel<MODE_JACOBI><<<grd, blk, 0, lc.stream>>>(op, x, b, dinv, y, lc.active, omega); break;
+    case MODE_PRE: st27_kernel<MODE_PRE><<<grd, blk, 0, lc.stream>>>(op, x, b, dinv, y, lc.active, omega); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+// 1D factor entry T(i, i+o), o in {-1,0,1}; fac points at [2][n+1] (diag, upper)
+__device__ __forceinline__ double fac1(const double* f, int n1, int i, int o) {
+  if (o == 0) return __ldg(f + i);
+  if (o > 0) return __ldg(f + n1 + i);
+  return __ldg(f + n1 + i - 1);
+}
+
+__global__ void __launch_bounds__(256) st27_build_kernel(int n, int Q,
+                                                         const double* __restrict__ fac,
+                                                         const double* __restrict__ theta,
+                                                         double* __restrict__ coef,
+                                                         double* __restrict__ dinv) {
+  const int mu = blockIdx.y;
+  const int64_t n3 = (int64_t)n * n * n;
+  const int64_t X = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (X >= n3) return;
+  const int i = X % n, j = (X / n) % n, k = X / ((int64_t)n * n);
+  double* C = coef + (int64_t)mu * 14 * n3;
+  const bool ghost = (i == 0 || j == 0 || k == 0);
+  const int n1 = n + 1;
+  double c0 = 0.0;
+  for (int o = 0; o < 14; ++o) {
+    int dx = 0, dy = 0, dz = 0;
+    if (o > 0) { dx = c_off_dx[o]; dy = c_off_dy[o]; dz = c_off_dz[o]; }
+    double c = 0.0;
+    if (!ghost) {
+      for (int q = 0; q < Q; ++q) {
+        const double t = theta[mu * Q + q];
+        double s = 0.0;
+        for (int d = 0; d < 3; ++d) {
+          const double* f = fac + (size_t)((q * 3 + d) * 3) * 2 * n1;
+          const double fx = fac1(f + 0 * 2 * n1, n1, i, dx);
+          const double fy = fac1(f + 1 * 2 * n1, n1, j, dy);
+          const double fzv = fac1(f + 2 * 2 * n1, n1, k, dz);
+          s += fx * fy * fzv;
+        }
+        c = fma(t, s, c);
+      }
+    }
+    C[o * n3 + X] = c;
+    if (o == 0) c0 = c;
+  }
+  dinv[(int64_t)mu * n3 + X] = ghost ? 0.0 : 1.0 / c0;
+}
+
+cudaError_t st27_build(int n, int Q, const double* fac, const double* theta, int batch,
+                       double* coef, double* dinv, cudaStream_t stream) {
+  cudaError_t e = ensure_offsets();
+  if (e != cudaSuccess) return e;
+  const int64_t n3 = (int64_t)n * n * n;
+  dim3 blk(256), grd((unsigned)((n3 + 255) / 256), batch);
+  count_launch();
+  st27_build_kernel<<<grd, blk, 0, stream>>>(n, Q, fac, theta, coef, dinv);
+  return cudaGetLastError();
+}
+
+// ========================================================================
+// transfers (trilinear prolongation and its transpose)
+// ========================================================================
+
+__global__ void __launch_bounds__(256) restrict_kernel(int nf, const double* __restrict__ rf,
+                                                       double* __restrict__ bc,
+                                                       const int* __restrict__ active) {
+  const int nc = nf / 2;
+  const int mu = blockIdx.y;
+  if (active && !active[mu]) return;
+  const int64_t nc3 = (int64_t)nc * nc * nc, nf3 = (int64_t)nf * nf * nf;
+  const int64_t X = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (X >= nc3) return;
+  const int I = X % nc, J = (X / nc) % nc, K = X / ((int64_t)nc * nc);
+  if (I == 0 || J == 0 || K == 0) return;
+  const double* r = rf + (int64_t)mu * nf3;
+  const int64_t nf2 = (int64_t)nf * nf;
+  const int64_t c = 2 * I + (int64_t)nf * 2 * J + nf2 * 2 * K;
+  double acc = 0.0;
+#pragma unroll
+  for (int dz = -1; dz <= 1; ++dz) {
+    double pz = 0.0;
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy) {
+      const int64_t row = c + dz * nf2 + dy * (int64_t)nf;
+      const double px = 0.5 * (__ldg(r + row - 1) + __ldg(r + row + 1)) + __ldg(r + row);
+      pz += (dy == 0 ? 1.0 : 0.5) * px;
+    }
+    acc += (dz == 0 ? 1.0 : 0.5) * pz;
+  }
+  bc[(int64_t)mu * nc3 + X] = acc;
+}
+
+cudaError_t restrict_launch(int nf, int batch, const double* rf, double* bc, const LaunchCtx& lc) {
+  const int nc = nf / 2;
+  const int64_t nc3 = (int64_t)nc * nc * nc;
+  dim3 blk(256), grd((unsigned)((nc3 + 255) / 256), batch);
+  count_launch();
+  restrict_kernel<<<grd, blk, 0, lc.stream>>>(nf, rf, bc, lc.active);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256) prolong_kernel(int nf, int mode,
+                                                      const double* __restrict__ ec,
+                                                      double* __restrict__ u,
+                                                      const double* __restrict__ b,
+                                                      const double* __restrict__ dinv,
+                                                      double omega,
+                                                      const int* __restrict__ active) {
+  const int nc = nf / 2;
+  const int mu = blockIdx.y;
+  if (active && !active[mu]) return;
+  const int64_t nf3 = (int64_t)nf * nf * nf, nc3 = (int64_t)nc * nc * nc;
+  const int64_t X = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (X >= nf3) return;
+  const int i = X % nf, j = (X / nf) % nf, k = X / ((int64_t)nf * nf);
+  if (i == 0 || j == 0 || k == 0) return;
+  const double* e = ec + (int64_t)mu * nc3;
+  // coarse support along each axis: even -> {i/2}, odd -> {(i-1)/2, (i+1)/2}
+  const int i0 = i >> 1, j0 = j >> 1, k0 = k >> 1;
+  const int ni = (i & 1) ? 2 : 1, nj = (j & 1) ? 2 : 1, nk = (k & 1) ? 2 : 1;
+  const double wi = (i & 1) ? 0.5 : 1.0, wj = (j & 1) ? 0.5 : 1.0, wk = (k & 1) ? 0.5 : 1.0;
+  double pe = 0.0;
+  for (int c = 0; c < nk; ++c) {
+    double sy = 0.0;
+    for (int bb = 0; bb < nj; ++bb) {
+      double sx = 0.0;
+      const int64_t row = (int64_t)(k0 + c) * nc * nc + (int64_t)(j0 + bb) * nc + i0;
+      for (int a = 0; a < ni; ++a) sx += __ldg(e + row + a);
+      sy += wi * sx;
+    }
+    pe += wj * sy;
+  }
+  pe *= wk;
+  const int64_t idx = (int64_t)mu * nf3 + X;
+  if (mode == 0) u[idx] += pe;
+  else u[idx] = omega * __ldg(dinv + idx) * __ldg(b + idx) + pe;
+}
+
+cudaError_t prolong_launch(int nf, int batch, int mode, const double* ec, double* u,
+                           const double* b, const double* dinv, double omega,
+                           const LaunchCtx& lc) {
+  const int64_t nf3 = (int64_t)nf * nf * nf;
+  dim3 blk(256), grd((unsigned)((nf3 + 255) / 256), batch);
+  count_launch();
+  prolong_kernel<<<grd, blk, 0, lc.stream>>>(nf, mode, ec, u, b, dinv, omega, lc.active);
+  return cudaGetLastError();
+}
+
+// ========================================================================
+// coarsest level: dense Cholesky per instance
+// ========================================================================
+
+__global__ void coarse_factor_kernel(int n0, const double* __restrict__ coef,
+                                     double* __restrict__ Lout, int* __restrict__ status) {
+  extern __shared__ double A[];
+  const int m1 = n0 - 1, m = m1 * m1 * m1;
+  const int mu = blockIdx.x;
+  const int64_t n3 = (int64_t)n0 * n0 * n0;
+  const double* C = coef + (int64_t)mu * 14 * n3;
+  for (int t = threadIdx.x; t < m * m; t += blockDim.x) A[t] = 0.0;
+  __syncthreads();
+  for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    const int i = r % m1 + 1, j = (r / m1) % m1 + 1, k = r / (m1 * m1) + 1;
+    const int64_t X = i + (int64_t)n0 * (j + (int64_t)n0 * k);
+    A[r * m + r] = C[X];
+    for (int o = 1; o < 14; ++o) {
+      int dx, dy, dz;
+      fwd_offset(o, dx, dy, dz);
+      // forward neighbour
+      int a = i + dx, bq = j + dy, c = k + dz;
+      if (a >= 1 && a <= m1 && bq >= 1 && bq <= m1 && c >= 1 && c <= m1) {
+        const int col = (a - 1) + m1 * ((bq - 1) + m1 * (c - 1));
+        A[r * m + col] = C[o * n3 + X];
+      }
+      a = i - dx; bq = j - dy; c = k - dz;
+      if (a >= 1 && a <= m1 && bq >= 1 && bq <= m1 && c >= 1 && c <= m1) {
+        const int col = (a - 1) + m1 * ((bq - 1) + m1 * (c - 1));
+        const int64_t Y = a + (int64_t)n0 * (bq + (int64_t)n0 * c);
+        A[r * m + col] = C[o * n3 + Y];
+      }
+    }
+  }
+  __syncthreads();
+  // right-looking Cholesky, lower triangle
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int c = 0; c < m; ++c) {
+    if (threadIdx.x == 0) {
+      const double dd = A[c * m + c];
+      if (!(dd > 0.0)) bad = 1;
+      A[c * m + c] = sqrt(dd > 0.0 ? dd : 1.0);
+    }
+    __syncthreads();
+    const double piv = A[c * m + c];
+    for (int r = c + 1 + threadIdx.x; r < m; r += blockDim.x) A[r * m + c] /= piv;
+    __syncthreads();
+    for (int t = threadIdx.x; t < (m - c - 1) * (m - c - 1); t += blockDim.x) {
+      const int r = c + 1 + t / (m - c - 1), s = c + 1 + t % (m - c - 1);
+      if (s <= r) A[r * m + s] -= A[r * m + c] * A[s * m + c];
+    }
+    __syncthreads();
+  }
+  double* L = Lout + (int64_t)mu * m * m;
+  for (int t = threadIdx.x; t < m * m; t += blockDim.x) {
+    const int r = t / m, s = t % m;
+    L[t] = (s <= r) ? A[t] : 0.0;
+  }
+  if (threadIdx.x == 0 && status) status[mu] = bad;
+}
+
+cudaError_t coarse_factor(int n0, int batch, const double* coef, double* L, int* status,
+                          cudaStream_t stream) {
+  const int m1 = n0 - 1, m = m1 * m1 * m1;
+  const size_t smem = (size_t)m * m * sizeof(double);
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(coarse_factor_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  count_launch();
+  coarse_factor_kernel<<<batch, 128, smem, stream>>>(n0, coef, L, status);
+  return cudaGetLastError();
+}
+
+// one warp per instance: forward then backward substitution
+__global__ void coarse_solve_kernel(int n0, int batch, const double* __restrict__ Lall,
+                                    const double* __restrict__ b, double* __restrict__ x,
+                                    const int* __restrict__ active) {
+  extern __shared__ double sh[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mu = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (mu >= batch) return;
+  if (active && !active[mu]) return;
+  const int m1 = n0 - 1, m = m1 * m1 * m1;
+  double* y = sh + warp * m;
+  const int64_t n3 = (int64_t)n0 * n0 * n0;
+  const double* L = Lall + (int64_t)mu * m * m;
+  auto pad = [&](int r) -> int64_t {
+    const int i = r % m1 + 1, j = (r / m1) % m1 + 1, k = r / (m1 * m1) + 1;
+    return (int64_t)mu * n3 + i + (int64_t)n0 * (j + (int64_t)n0 * k);
+  };
+  for (int r = lane; r < m; r += 32) y[r] = b[pad(r)];
+  __syncwarp();
+  for (int r = 0; r < m; ++r) {  // L y = b
+    double s = 0.0;
+    for (int c = lane; c < r; c += 32) s = fma(L[r * m + c], y[c], s);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) y[r] = (y[r] - s) / L[r * m + r];
+    __syncwarp();
+  }
+  for (int r = m - 1; r >= 0; --r) {  // L^T x = y
+    double s = 0.0;
+    for (int c = r + 1 + lane; c < m; c += 32) s = fma(L[c * m + r], y[c], s);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) y[r] = (y[r] - s) / L[r * m + r];
+    __syncwarp();
+  }
+  for (int r = lane; r < m; r += 32) x[pad(r)] = y[r];
+}
+
+cudaError_t coarse_solve(int n0, int batch, const double* L, const double* b, double* x,
+                         const LaunchCtx& lc) {
+  const int m1 = n0 - 1, m = m1 * m1 * m1;
+  const int wpb = 4;
+  const size_t smem = (size_t)wpb * m * sizeof(double);
+  count_launch();
+  coarse_solve_kernel<<<(batch + wpb - 1) / wpb, 32 * wpb, smem, lc.stream>>>(n0, batch, L, b, x,
+                                                                           lc.active);
+  return cudaGetLastError();
+}
+
+// ========================================================================
+// vector ops on padded batch vectors
+// ========================================================================
+
+int vec_tiles(int n) {
+  const int64_t n3 = (int64_t)n * n * n;
+  int64_t t = (n3 + 2047) / 2048;  // 256 threads x 8 elements
+  return (int)t;
+}
+
+__global__ void __launch_bounds__(256) dot_kernel(int64_t n3, const double* __restrict__ x,
+                                                  int64_t xs, const double* __restrict__ y,
+                                                  int64_t ys, double* __restrict__ partial,
+                                                  const int* __restrict__ active) {
+  __shared__ double red[32];
+  const int mu = blockIdx.y;
+  if (active && !active[mu]) return;
+  const double* a = x + mu * xs;
+  const double* b = y + mu * ys;
+  double acc = 0.0;
+  const int64_t start = (int64_t)blockIdx.x * 2048;
+  for (int t = 0; t < 8; ++t) {
+    const int64_t idx = start + t * 256 + threadIdx.x;
+    if (idx < n3) acc = fma(__ldg(a + idx), __ldg(b + idx), acc);
+  }
+  const double s = block_reduce_sum(acc, red);
+  if (threadIdx.x == 0) partial[(int64_t)mu * gridDim.x + blockIdx.x] = s;
+}
+
+cudaError_t vec_dot(int n, int batch, const double* x, int64_t x_stride, const double* y,
+                    int64_t y_stride, double* partial, const LaunchCtx& lc) {
+  const int64_t n3 = (int64_t)n * n * n;
+  dim3 blk(256), grd(vec_tiles(n), batch);
+  count_launch();
+  dot_kernel<<<grd, blk, 0, lc.stream>>>(n3, x, x_stride, y, y_stride, partial, lc.active);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256) xpby_kernel(int64_t n3, const double* __restrict__ x,
+                                                   const double* __restrict__ beta,
+                                                   double* __restrict__ y,
+                                                   const int* __restrict__ active) {
+  const int mu = blockIdx.y;
+  if (active && !active[mu]) return;
+  const double bt = beta ? beta[mu] : 0.0;
+  const int64_t base = (int64_t)mu * n3;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n3;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    y[base + idx] = fma(bt, y[base + idx], __ldg(x + base + idx));
+  }
+}
+
+cudaError_t vec_xpby(int n, int batch, const double* x, const double* beta, double* y,
+                     const LaunchCtx& lc) {
+  const int64_t n3 = (int64_t)n * n * n;
+  int gx = (int)((n3 + 1023) / 1024);
+  dim3 blk(256), grd(gx, batch);
+  count_launch();
+  xpby_kernel<<<grd, blk, 0, lc.stream>>>(n3, x, beta, y, lc.active);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256) copy_kernel(int64_t n3, const double* __restrict__ x,
+                                                   int64_t xs, double* __restrict__ y,
+                                                   const int* __restrict__ active) {
+  const int mu = blockIdx.y;
+  if (active && !active[mu]) return;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n3;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    y[(int64_t)mu * n3 + idx] = __ldg(x + mu * xs + idx);
+  }
+}
+
+cudaError_t vec_copy(int n, int batch, const double* x, int64_t x_stride, double* y,
+                     const LaunchCtx& lc) {
+  const int64_t n3 = (int64_t)n * n * n;
+  int gx = (int)((n3 + 1023) / 1024);
+  dim3 blk(256), grd(gx, batch);
+  count_launch();
+  copy_kernel<<<grd, blk, 0, lc.stream>>>(n3, x, x_stride, y, lc.active);
+  return cudaGetLastError();
+}
+
+}  // namespace rbws

@@ -1,0 +1,72 @@
+// Stencil, transfer and vector kernels of the batched V-cycle / PCG path.
+#pragma once
+
+#include "common.cuh"
+
+namespace rbws {
+
+enum StencilMode : int {
+  MODE_APPLY = 0,   // y = A x
+  MODE_RESID = 1,   // y = b - A x
+  MODE_JACOBI = 2,  // y = x + omega (b - A x) / d
+  MODE_PRE = 3,     // y = b - A (omega dinv b)     (nu=1 pre-smooth from zero + residual)
+  MODE_DINV = 4,    // y = 1 / d
+};
+
+enum DotMode : int { DOT_NONE = 0, DOT_XAX = 1, DOT_BY = 2, DOT_YY = 3 };
+
+struct LaunchCtx {
+  cudaStream_t stream;
+  const int* active;  // per-instance flag (nullptr = all active)
+};
+
+// ---- finest level (separable 7-point) -----------------------------------
+struct Sep7Geom {
+  int tx, ty, zc;     // block dims and z-chunks
+  int tiles;          // partial-sum slots per instance
+};
+Sep7Geom sep7_geom(int n, int batch);
+
+// generic mode kernel; partial (if dot != DOT_NONE) gets tiles doubles per instance
+cudaError_t sep7_launch(const Sep7& op, int batch, int mode, int dot, const double* x,
+                        const double* b, const double* dinv, double* y, double* partial,
+                        double omega, const LaunchCtx& lc);
+// x += alpha p ; r -= alpha A p ; partial = sum r^2
+cudaError_t sep7_cg_update(const Sep7& op, int batch, const double* p, double* x, double* r,
+                           const double* alpha, double* partial, const LaunchCtx& lc);
+
+// ---- coarse levels (per-instance 27-point) -------------------------------
+cudaError_t st27_launch(const St27& op, int batch, int mode, const double* x, const double* b,
+                        const double* dinv, double* y, double omega, const LaunchCtx& lc);
+
+// coefficients of a coarse level from its Kronecker 1D factors
+// fac[((t*3 + a)*2 + s)*(n+1) + i], t = q*3+d, s=0 diag / s=1 upper off-diagonal
+cudaError_t st27_build(int n, int Q, const double* fac, const double* theta, int batch,
+                       double* coef, double* dinv, cudaStream_t stream);
+
+// ---- transfers -----------------------------------------------------------
+// bc = P^T r  (coarse n_c = n_f/2)
+cudaError_t restrict_launch(int nf, int batch, const double* rf, double* bc, const LaunchCtx& lc);
+// mode 0: u += P e ;  mode 1: u = omega dinv b + P e
+cudaError_t prolong_launch(int nf, int batch, int mode, const double* ec, double* u,
+                           const double* b, const double* dinv, double omega, const LaunchCtx& lc);
+
+// ---- coarsest dense solve ------------------------------------------------
+cudaError_t coarse_factor(int n0, int batch, const double* coef, double* L, int* status,
+                          cudaStream_t stream);
+cudaError_t coarse_solve(int n0, int batch, const double* L, const double* b, double* x,
+                         const LaunchCtx& lc);
+
+// ---- vector ops ----------------------------------------------------------
+// partial[mu*tiles + t] = sum x*y over instance mu (tiles from vec_tiles)
+int vec_tiles(int n);
+cudaError_t vec_dot(int n, int batch, const double* x, int64_t x_stride, const double* y,
+                    int64_t y_stride, double* partial, const LaunchCtx& lc);
+// y = a*x + beta[mu]*y   (beta may be null -> 0);  ghosts untouched (they are 0)
+cudaError_t vec_xpby(int n, int batch, const double* x, const double* beta, double* y,
+                     const LaunchCtx& lc);
+// y = x (instance-strided broadcast allowed: x_stride 0)
+cudaError_t vec_copy(int n, int batch, const double* x, int64_t x_stride, double* y,
+                     const LaunchCtx& lc);
+
+}  // namespace rbws

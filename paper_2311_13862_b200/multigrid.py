@@ -1,0 +1,154 @@
+"""Batched geometric multigrid and MGCG on the B200.
+
+B200 counterpart of reference multigrid.py:
+  * ``mg_context_for`` (multigrid.py:530-541) -> per-batch native context:
+    operators of every level for every mu (coarse levels as per-instance
+    27-point stencils assembled from the Kronecker factors), Jacobi
+    diagonals, Cholesky of the coarsest level;
+  * ``mg_vcycle`` (multigrid.py:544-561) -> one V-cycle for the whole batch;
+  * ``mgcg_solve`` (multigrid.py:564-571) -> native batched PCG.
+The smoother is the reference's isotropic default, damped Jacobi with
+omega = 0.7 (multigrid.py:366-367, 522-527).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+
+import numpy as np
+
+from . import _native
+from .grid import BatchOperator, ParametricProblem, padded_len
+from .krylov import OperatorError, SolveReport
+
+JACOBI_OMEGA = 0.7
+
+
+class MgContext:
+    """Per-batch multigrid state (reference MgContext, multigrid.py:455-468)."""
+
+    def __init__(self, problem: ParametricProblem, capacity: int, nu: int = 1,
+                 omega: float = JACOBI_OMEGA):
+        if nu < 1:
+            raise ValueError("the batched V-cycle needs nu >= 1 smoothing sweeps")
+        self.problem = problem
+        self.capacity = int(capacity)
+        self.nu = nu
+        self.omega = omega
+        self.smoother_kind = "jacobi"
+        b = ctypes.c_void_p()
+        _native.call("rbws_batch_create", ctypes.byref(b), problem.handle, self.capacity, nu,
+                     float(omega))
+        self._b = b
+        self.count = 0
+        self.mus = None
+        self.theta = None
+
+    def __del__(self):
+        b = getattr(self, "_b", None)
+        if b is not None and b.value and _native._lib is not None:
+            _native._lib.rbws_batch_destroy(b)
+
+    @property
+    def handle(self):
+        return self._b
+
+    @property
+    def levels(self) -> int:
+        return self.problem.levels
+
+    def setup(self, mus, stream=None):
+        """Bind the context to a batch of parameters (per-mu operators + factors)."""
+        import torch
+        mus = self.problem.spec.check_mus(mus)
+        if len(mus) > self.capacity:
+            raise ValueError(f"batch of {len(mus)} exceeds context capacity {self.capacity}")
+        self.mus = mus
+        self.count = len(mus)
+        self.theta = torch.as_tensor(self.problem.spec.thetas(mus), dtype=torch.float64,
+                                     device="cuda").contiguous()
+        bad = ctypes.c_int(0)
+        _native.call("rbws_batch_setup", self._b, self.theta.data_ptr(), self.count,
+                     ctypes.byref(bad), _native.stream_ptr(stream))
+        if bad.value:
+            raise OperatorError(f"coarsest operator not SPD for {bad.value} parameter(s)")
+        return self
+
+
+def mg_context_for(problem: ParametricProblem, mus, nu: int = 1, smoother: str = "auto",
+                   ctx: MgContext | None = None) -> MgContext:
+    """Batched mg_context_for (multigrid.py:530-541).
+
+    ``mus``: one parameter or an array (count, p).  Pass an existing ``ctx``
+    to reuse its device buffers for a new batch.
+    """
+    if smoother not in ("auto", "jacobi"):
+        raise ValueError(f"smoother {smoother!r} is not on the B200 path (jacobi only)")
+    mus = problem.spec.check_mus(mus)
+    if ctx is None or ctx.capacity < len(mus) or ctx.nu != nu or ctx.problem is not problem:
+        ctx = MgContext(problem, len(mus), nu=nu)
+    return ctx.setup(mus)
+
+
+def mg_vcycle(b, ctx: MgContext, level=None):
+    """One V-cycle from zero for every instance of the batch (multigrid.py:544-561)."""
+    import torch
+    if level is not None and level != ctx.levels - 1:
+        raise ValueError("the batched V-cycle is entered on the finest level")
+    n = ctx.problem.n
+    if b.numel() != padded_len(n, ctx.count) and b.numel() < padded_len(n, ctx.count):
+        raise ValueError("right-hand side does not match level size")
+    out = torch.zeros_like(b)
+    _native.call("rbws_vcycle", ctx.handle, b.data_ptr(), out.data_ptr(), _native.stream_ptr())
+    return out
+
+
+def mgcg_solve(A, f, x0, ctx: MgContext, delta: float = 1e-16, l_max: int = 40, mu=None,
+               method: str = "mgcg", raise_on_breakdown: bool = True):
+    """Batched MGCG (multigrid.py:564-571 -> krylov.py:267-334).
+
+    f: padded rhs, either one instance (shared) or a full batch; x0: padded
+    batch of initial guesses (None = zeros).  Returns (x, [SolveReport]).
+    """
+    import torch
+    if delta <= 0:
+        raise ValueError("tolerance must be positive")
+    if l_max < 0:
+        raise ValueError("l_max must be non-negative")
+    prob = ctx.problem
+    n, count = prob.n, ctx.count
+    if f is None:
+        f = prob.rhs()
+    nb = padded_len(n, count)
+    if f.numel() == padded_len(n, 1) and count > 1:
+        f_stride = 0
+    elif f.numel() >= nb:
+        f_stride = n ** 3
+    else:
+        raise ValueError("rhs does not match the batch")
+    x = torch.zeros(nb, dtype=torch.float64, device="cuda") if x0 is None else x0.clone()
+    iters = np.zeros(count, dtype=np.int32)
+    hist = np.zeros((count, l_max + 1))
+    tres = np.zeros(count)
+    status = np.zeros(count, dtype=np.int32)
+    t0 = time.perf_counter()
+    _native.call("rbws_mgcg_solve", ctx.handle, f.data_ptr(), f_stride, x.data_ptr(),
+                 float(delta), int(l_max), iters.ctypes.data, hist.ctypes.data,
+                 tres.ctypes.data, status.ctypes.data, _native.stream_ptr())
+    wall = time.perf_counter() - t0
+    if raise_on_breakdown and np.any(status & 1):
+        bad = int(np.flatnonzero(status & 1)[0])
+        raise OperatorError(f"non-positive curvature for parameter #{bad}; operator not SPD")
+    reports = []
+    for m in range(count):
+        k = int(iters[m])
+        reports.append(SolveReport(
+            method=method, iterations=k, history=[float(v) for v in hist[m, :k + 1]],
+            converged=bool(tres[m] <= delta), true_residual=float(tres[m]),
+            wall_time=wall / count, delta=delta, l_max=l_max,
+            mu=None if ctx.mus is None else np.asarray(ctx.mus[m]),
+            absolute_norms=bool(status[m] & 4),
+            config={"batch": count, "batch_wall_time": wall, "smoother": "jacobi",
+                    "nu": ctx.nu}))
+    return x, reports
