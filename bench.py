@@ -253,15 +253,20 @@ def run_b200(args, rank, world, dist):
             gbs = CLASS_BYTES[k] * nodes * punits[k] / (pms[k] / 1e3) / 1e9
             row["achieved_gbs"] = round(gbs, 1)
         table[CLASS_NAMES[k]] = row
-    dom = max((k for k in CLASS_BYTES if pcalls[k]), key=lambda k: pms[k])
-    dom_bytes = CLASS_BYTES[dom] * nodes * punits[dom] / pcalls[dom]
-    dom_s = pms[dom] / pcalls[dom] / 1e3
-    achieved = dom_bytes / dom_s / 1e9
-    roofline = {"bound": "hbm", "kernel": CLASS_NAMES[dom], "achieved": round(achieved, 1),
-                "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                "traffic": None, "peak_source": peak_kind,
-                "bytes_per_launch": int(dom_bytes),
-                "bytes_per_node": CLASS_BYTES[dom]}
+    ran = [k for k in CLASS_BYTES if pcalls[k]]
+    if ran:
+        dom = max(ran, key=lambda k: pms[k])
+        dom_bytes = CLASS_BYTES[dom] * nodes * punits[dom] / pcalls[dom]
+        dom_s = pms[dom] / pcalls[dom] / 1e3
+        achieved = dom_bytes / dom_s / 1e9
+        roofline = {"bound": "hbm", "kernel": CLASS_NAMES[dom], "achieved": round(achieved, 1),
+                    "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                    "traffic": None, "peak_source": peak_kind,
+                    "bytes_per_launch": int(dom_bytes),
+                    "bytes_per_node": CLASS_BYTES[dom]}
+    else:  # the warm start already met the tolerance: no PCG iteration ran
+        roofline = {"bound": "hbm", "kernel": None, "achieved": None, "peak": peak,
+                    "unit": "GB/s", "frac": None, "traffic": None, "peak_source": peak_kind}
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1)
     cpu = None

@@ -15,7 +15,8 @@
  *  - Grid vectors use the padded batch layout: instance `mu` of a level with
  *    n cells occupies doubles [mu*n^3, (mu+1)*n^3) indexed i + n*(j + n*k);
  *    interior (free) DoFs are i,j,k in [1, n-1], all other entries are 0.
- *    A buffer for `count` instances holds count*n^3 + n^2 doubles.
+ *    A buffer for `count` instances holds count*n^3 + 2*n^2 doubles (the
+ *    trailing ghost region absorbs diagonal stencil reads of the last instance).
  *    Interior ordering inside the padded block equals the reference's free-DoF
  *    ordering (lexicographic, x fastest; reference grid.py:29-34,
  *    problems.py:409-421).

@@ -7,7 +7,8 @@
 // 0.0.  Neighbour addresses of interior nodes that step onto the far
 // boundary (coordinate n) wrap onto the next row/plane/instance's ghost
 // entries, so stencils need no bounds checks.  A batch of B instances is
-// B*n^3 + n^2 doubles (one trailing ghost plane).
+// B*n^3 + 2n^2 doubles (a trailing ghost region of two planes, enough for
+// the diagonal 27-point / trilinear reads of the last instance's top corner).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -24,7 +25,7 @@ void count_launch();
 int64_t launch_count();
 
 RBWS_HD int64_t vec_doubles(int n, int batch) {
-  return (int64_t)batch * n * n * n + (int64_t)n * n;
+  return (int64_t)batch * n * n * n + 2 * (int64_t)n * n;
 }
 
 // Separable 7-point operator of the finest level.

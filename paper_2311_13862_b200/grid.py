@@ -20,7 +20,7 @@ from .problems import ProblemSpec, levels_for
 
 def padded_len(n: int, count: int) -> int:
     """Doubles in a padded batch vector of `count` instances on n cells."""
-    return count * n ** 3 + n * n
+    return count * n ** 3 + 2 * n * n
 
 
 def to_padded(v, n: int, device="cuda"):

@@ -111,7 +111,7 @@ class ProblemSpec:
         """h^3 f(X) in the padded single-instance layout (n^3 + n^2 doubles)."""
         import torch
         h = 1.0 / n
-        out = torch.zeros(n * n * n + n * n, dtype=torch.float64, device=device)
+        out = torch.zeros(n * n * n + 2 * n * n, dtype=torch.float64, device=device)
         idx = torch.arange(n, dtype=torch.float64, device=device) * h
         if self.kind == "thermal-block":
             f = torch.ones((n, n, n), dtype=torch.float64, device=device)

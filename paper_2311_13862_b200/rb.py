@@ -180,10 +180,10 @@ def deim_extend(n: int, W, X, v, exclude=None) -> DeimStep:
     else:
         cvec = torch.zeros(1, dtype=torch.float64, device="cuda")
         wptr = v.data_ptr()
-    excl = torch.zeros(n3 + n * n, dtype=torch.uint8, device="cuda")
+    excl = torch.zeros(padded_len(n, 1), dtype=torch.uint8, device="cuda")
     if exclude:
         excl[torch.as_tensor(interior_to_padded_index(sorted(exclude), n), device="cuda")] = 1
-    col = torch.zeros(n3 + n * n, dtype=torch.float64, device="cuda")
+    col = torch.zeros(padded_len(n, 1), dtype=torch.float64, device="cuda")
     idx = torch.zeros(1, dtype=torch.int64, device="cuda")
     vals = torch.zeros(3, dtype=torch.float64, device="cuda")
     _native.call("rbws_deim_step", n, wptr, n3, N, cvec.data_ptr(), v.data_ptr(), excl.data_ptr(),

@@ -73,9 +73,10 @@ def test_transfers_match_prolongation():
     rf = rng.standard_normal((2, (nf - 1) ** 3))
     ec = rng.standard_normal((2, (nc - 1) ** 3))
     bc = torch.zeros(pkg.padded_len(nc, 2), dtype=torch.float64, device="cuda")
-    _native.call("rbws_restrict", nf, 2, pkg.to_padded(rf, nf).data_ptr(), bc.data_ptr(), 0)
+    rft, ect = pkg.to_padded(rf, nf), pkg.to_padded(ec, nc)
+    _native.call("rbws_restrict", nf, 2, rft.data_ptr(), bc.data_ptr(), 0)
     u = pkg.to_padded(rf, nf)
-    _native.call("rbws_prolong_add", nf, 2, pkg.to_padded(ec, nc).data_ptr(), u.data_ptr(), 0)
+    _native.call("rbws_prolong_add", nf, 2, ect.data_ptr(), u.data_ptr(), 0)
     torch.cuda.synchronize()
     got_r, got_p = pkg.from_padded(bc, nc, 2), pkg.from_padded(u, nf, 2)
     for m in range(2):
@@ -95,8 +96,9 @@ def test_jacobi_sweep_matches_oracle():
         x = rng.standard_normal((2, (nl - 1) ** 3))
         b = rng.standard_normal((2, (nl - 1) ** 3))
         y = torch.zeros(pkg.padded_len(nl, 2), dtype=torch.float64, device="cuda")
-        _native.call("rbws_jacobi_sweep", ctx.handle, lvl, pkg.to_padded(x, nl).data_ptr(),
-                     pkg.to_padded(b, nl).data_ptr(), y.data_ptr(), 0)
+        xt, bt = pkg.to_padded(x, nl), pkg.to_padded(b, nl)  # keep alive across the call
+        _native.call("rbws_jacobi_sweep", ctx.handle, lvl, xt.data_ptr(), bt.data_ptr(),
+                     y.data_ptr(), 0)
         got = pkg.from_padded(y, nl, 2)
         for m in range(2):
             A = oprob.operator(mus[m], level=lvl)
@@ -278,9 +280,9 @@ def test_deim_known_answers():
     n = 8
     v = np.zeros(7 ** 3)
     v[[0, 1, 2]] = [1.0, 3.0, 2.0]
-    step = pkg.deim_extend(n, None, [], pkg.to_padded(v, n)[: n ** 3 + n * n])
+    step = pkg.deim_extend(n, None, [], pkg.to_padded(v, n)[: pkg.padded_len(n, 1)])
     assert step.index == 1 and step.pivot == 3.0
     col = pkg.from_padded(step.column, n, 1)[0]
     np.testing.assert_allclose(col[:3], [1 / 3, 1.0, 2 / 3])
-    step2 = pkg.deim_extend(n, None, [], pkg.to_padded(v, n)[: n ** 3 + n * n], exclude={1})
+    step2 = pkg.deim_extend(n, None, [], pkg.to_padded(v, n)[: pkg.padded_len(n, 1)], exclude={1})
     assert step2.index == 2
