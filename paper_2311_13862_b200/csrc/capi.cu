@@ -1,5 +1,6 @@
 // extern "C" boundary (include/rbws_b200.h).
 #include "../../include/rbws_b200.h"
+#include "fine.cuh"
 #include "l1roc.cuh"
 #include "solver.cuh"
 
@@ -104,8 +105,7 @@ int rbws_apply(rbws_batch* b, int level, const double* x, double* y, void* strea
   if (bb->count < 1) RBWS_FAIL("batch_setup must be called first");
   rbws::LaunchCtx lc{S(stream), nullptr};
   if (level == h->levels - 1) {
-    RBWS_CHECK(rbws::sep7_launch(bb->fine_op(), bb->count, rbws::MODE_APPLY, rbws::DOT_NONE, x,
-                                 nullptr, nullptr, y, nullptr, 0.0, lc));
+    RBWS_CHECK(rbws::fine_apply(bb->fine_op(), bb->count, x, y, nullptr, lc));
   } else {
     rbws::St27 op{h->cells[level], bb->lv[level].coef};
     RBWS_CHECK(rbws::st27_launch(op, bb->count, rbws::MODE_APPLY, x, nullptr, nullptr, y, 0.0, lc));
@@ -121,8 +121,7 @@ int rbws_jacobi_sweep(rbws_batch* b, int level, const double* x, const double* r
   if (bb->count < 1) RBWS_FAIL("batch_setup must be called first");
   rbws::LaunchCtx lc{S(stream), nullptr};
   if (level == h->levels - 1) {
-    RBWS_CHECK(rbws::sep7_launch(bb->fine_op(), bb->count, rbws::MODE_JACOBI, rbws::DOT_NONE, x,
-                                 rhs, nullptr, y, nullptr, bb->omega, lc));
+    RBWS_CHECK(rbws::fine_jacobi(bb->fine_op(), bb->count, x, rhs, y, bb->omega, nullptr, lc));
   } else {
     rbws::St27 op{h->cells[level], bb->lv[level].coef};
     RBWS_CHECK(rbws::st27_launch(op, bb->count, rbws::MODE_JACOBI, x, rhs, bb->lv[level].dinv, y,

@@ -1,0 +1,39 @@
+// Finest-level kernels with TMA-engine plane staging (see fine.cu).
+#pragma once
+
+#include "stencil.cuh"
+
+namespace rbws {
+
+struct FineGeom {
+  int threads;  // threads per CTA (rows-per-pass x n)
+  int rpp;      // grid rows covered per pass of the CTA
+  int npt;      // nodes per thread per plane
+  int ty;       // rows per tile = rpp * npt
+  int ytiles;   // tiles per plane
+  int zc;       // z-chunks per instance
+  int tiles;    // partial-sum slots per instance = ytiles * zc
+};
+FineGeom fine_geom(int n, int batch);
+
+// y = A x (y may be null), partial (may be null) = x . A x
+cudaError_t fine_apply(const Sep7& op, int batch, const double* x, double* y, double* partial,
+                       const LaunchCtx& lc);
+// r = b - A x, partial = |r|^2
+cudaError_t fine_resid(const Sep7& op, int batch, const double* x, const double* b, double* r,
+                       double* partial, const LaunchCtx& lc);
+// y = x + omega (b - A x)/diag, partial (may be null) = b . y
+cudaError_t fine_jacobi(const Sep7& op, int batch, const double* x, const double* b, double* y,
+                        double omega, double* partial, const LaunchCtx& lc);
+// r1 = b - A (omega dinv b)
+cudaError_t fine_pre(const Sep7& op, int batch, const double* b, const double* dinv, double* r1,
+                     double omega, const LaunchCtx& lc);
+// x += alpha p, r -= alpha A p, partial = |r|^2
+cudaError_t fine_cg_update(const Sep7& op, int batch, const double* p, double* x, double* r,
+                           const double* alpha, double* partial, const LaunchCtx& lc);
+// p_new = s + beta p_old (beta null: p_new = s), partial = p_new . A p_new
+cudaError_t fine_papply(const Sep7& op, int batch, const double* s, const double* p_old,
+                        const double* beta, double* p_new, double* partial, const LaunchCtx& lc);
+
+}  // namespace rbws
+

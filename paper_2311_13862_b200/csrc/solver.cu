@@ -11,6 +11,7 @@
 #include <cstring>
 #include <string>
 
+#include "fine.cuh"
 #include "solver.cuh"
 
 static thread_local std::string g_err;
@@ -154,7 +155,7 @@ Batch::~Batch() {
     cudaFree(l.zero); cudaFree(l.dinv); cudaFree(l.coef);
   }
   cudaFree(L0); cudaFree(d_status);
-  cudaFree(r); cudaFree(p); cudaFree(s);
+  cudaFree(r); cudaFree(p); cudaFree(p2); cudaFree(s); cudaFree(t_res);
   cudaFree(rs); cudaFree(alpha); cudaFree(beta); cudaFree(scale);
   cudaFree(active); cudaFree(iters); cudaFree(pstatus); cudaFree(nactive);
   cudaFreeHost(h_nactive);
@@ -202,7 +203,7 @@ int batch_create(Batch** out, Hierarchy* h, int cap, int nu, double omega) {
   }
   const size_t VF = (size_t)vec_doubles(h->n, cap);
   if (e == cudaSuccess) e = dalloc(&b->d_status, cap);
-  for (double** pp : {&b->r, &b->p, &b->s}) {
+  for (double** pp : {&b->r, &b->p, &b->p2, &b->s, &b->t_res}) {
     if (e == cudaSuccess) e = dalloc(pp, VF);
     if (e == cudaSuccess) e = cudaMemset(*pp, 0, VF * sizeof(double));
   }
@@ -217,6 +218,8 @@ int batch_create(Batch** out, Hierarchy* h, int cap, int nu, double omega) {
     for (int c = 2; c <= cap; c *= 2) t = std::max<int64_t>(t, sep7_geom(h->n, c).tiles);
     t = std::max<int64_t>(t, sep7_geom(h->n, cap).tiles);
     t = std::max<int64_t>(t, vec_tiles(h->n));
+    for (int c = 1; c <= cap; c *= 2) t = std::max<int64_t>(t, fine_geom(h->n, c).tiles);
+    t = std::max<int64_t>(t, fine_geom(h->n, cap).tiles);
     b->partial_cap = t;
     e = dalloc(&b->partial, (size_t)cap * t);
     if (e == cudaSuccess) e = dalloc(&b->partial2, (size_t)cap * t);
@@ -293,7 +296,14 @@ int Batch::vcycle(int lvl, const double* bb, double* out, double* dot_partial,
   const int n = l.n;
   auto op = [&](int mode, int dot, const double* x, const double* rhs, double* y,
                 double* part) -> cudaError_t {
-    if (fine) return sep7_launch(fine_op(), count, mode, dot, x, rhs, l.dinv, y, part, omega, lc);
+    if (fine) {
+      const Sep7 fo = fine_op();
+      if (mode == MODE_PRE) return fine_pre(fo, count, rhs, l.dinv, y, omega, lc);
+      if (mode == MODE_JACOBI)
+        return fine_jacobi(fo, count, x, rhs, y, omega, dot == DOT_NONE ? nullptr : part, lc);
+      if (mode == MODE_RESID) return fine_resid(fo, count, x, rhs, y, nullptr, lc);
+      return sep7_launch(fo, count, mode, dot, x, rhs, l.dinv, y, part, omega, lc);
+    }
     St27 s27{n, l.coef};
     return st27_launch(s27, count, mode, x, rhs, l.dinv, y, omega, lc);
   };
@@ -467,22 +477,20 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
   }
   const int hl = b->hist_len;
   const Sep7 op = b->fine_op();
-  const Sep7Geom g = sep7_geom(n, count);
-  const int tiles = g.tiles;
+  const int tiles = fine_geom(n, count).tiles;
   LaunchCtx all{stream, nullptr};
   LaunchCtx act{stream, b->active};
   const int fshared = (f_stride == 0);
   const int ftiles = vec_tiles(n);
   // ||f||
   e = vec_dot(n, fshared ? 1 : count, f, f_stride, f, f_stride, b->partial2, all);
-  // r = f - A x0, ||r||^2
+  // r = f - A x0, ||r||^2  (a shared rhs is broadcast into s first)
+  const double* fb = f;
   if (e == cudaSuccess && fshared) {
-    e = vec_copy(n, count, f, 0, b->s, all);  // s <- broadcast f
-    if (e == cudaSuccess)
-      e = sep7_launch(op, count, MODE_RESID, DOT_YY, x, b->s, nullptr, b->r, b->partial, 0.0, all);
-  } else if (e == cudaSuccess) {
-    e = sep7_launch(op, count, MODE_RESID, DOT_YY, x, f, nullptr, b->r, b->partial, 0.0, all);
+    e = vec_copy(n, count, f, 0, b->s, all);
+    fb = b->s;
   }
+  if (e == cudaSuccess) e = fine_resid(op, count, x, fb, b->r, b->partial, all);
   if (e == cudaSuccess) e = cudaMemsetAsync(b->nactive, 0, sizeof(int), stream);
   if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
   count_launch();
@@ -498,20 +506,22 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
     if (b->vcycle(L - 1, b->r, b->s, b->partial, act)) return 1;
     count_launch();
     pcg_rs_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, tiles, b->rs, b->active);
-    e = vec_copy(n, count, b->s, n3, b->p, act);
-    if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+    // search directions ping-pong between p and p2 (the p-update reads the old
+    // direction with a halo, so it cannot be updated in place)
+    double* p_old = nullptr;
+    double* p_new = b->p;
+    const double* beta = nullptr;
     const bool pf = b->prof_on;
     for (int k = 0; k < l_max; ++k) {
       int t0 = pf ? b->prof_begin(stream) : -1;
-      e = sep7_launch(op, count, MODE_APPLY, DOT_XAX, b->p, nullptr, nullptr, nullptr, b->partial,
-                      0.0, act);
+      e = fine_papply(op, count, b->s, p_old, beta, p_new, b->partial, act);
       if (pf) { b->prof_end(PROF_FINE_APPLY_DOT, t0, stream); t0 = b->prof_begin(stream); }
       if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
       count_launch();
       pcg_alpha_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, tiles, b->rs,
                                                              b->alpha, b->active, b->pstatus);
       if (pf) { b->prof_end(PROF_SCALARS, t0, stream); t0 = b->prof_begin(stream); }
-      e = sep7_cg_update(op, count, b->p, x, b->r, b->alpha, b->partial, act);
+      e = fine_cg_update(op, count, p_new, x, b->r, b->alpha, b->partial, act);
       if (pf) { b->prof_end(PROF_FINE_CG_UPDATE, t0, stream); t0 = b->prof_begin(stream); }
       if (e == cudaSuccess) e = cudaMemsetAsync(b->nactive, 0, sizeof(int), stream);
       if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
@@ -530,17 +540,15 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
       count_launch();
       pcg_beta_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, tiles, b->rs,
                                                             b->beta, b->active);
-      if (pf) { b->prof_end(PROF_SCALARS, t0, stream); t0 = b->prof_begin(stream); }
-      e = vec_xpby(n, count, b->s, b->beta, b->p, act);
-      if (pf) b->prof_end(PROF_FINE_XPBY, t0, stream);
-      if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+      if (pf) b->prof_end(PROF_SCALARS, t0, stream);
+      beta = b->beta;
+      p_old = p_new;
+      p_new = (p_new == b->p) ? b->p2 : b->p;
     }
   }
   // true residual ||f - A x|| / scale for every instance
-  const double* fb = fshared ? b->s : f;
   if (fshared) e = vec_copy(n, count, f, 0, b->s, all);
-  if (e == cudaSuccess)
-    e = sep7_launch(op, count, MODE_RESID, DOT_YY, x, fb, nullptr, b->p, b->partial, 0.0, all);
+  if (e == cudaSuccess) e = fine_resid(op, count, x, fb, b->t_res, b->partial, all);
   if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
   double* d_true = b->beta;  // reuse as scratch
   count_launch();

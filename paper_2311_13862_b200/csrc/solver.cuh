@@ -62,7 +62,7 @@ struct Batch {
   double* L0 = nullptr;             // coarsest Cholesky factors [cap][m][m]
   int* d_status = nullptr;          // coarse factor status per instance
   // PCG state (fine level)
-  double *r = nullptr, *p = nullptr, *s = nullptr;
+  double *r = nullptr, *p = nullptr, *p2 = nullptr, *s = nullptr, *t_res = nullptr;
   double *rs = nullptr, *alpha = nullptr, *beta = nullptr, *scale = nullptr;
   int *active = nullptr, *iters = nullptr, *pstatus = nullptr, *nactive = nullptr;
   int* h_nactive = nullptr;         // pinned
