@@ -100,6 +100,15 @@ int rbws_mgcg_solve(rbws_batch* b, const double* f, int64_t f_stride, double* x,
                     int l_max, int* iters, double* hist, double* true_res, int* status,
                     void* stream);
 
+/* One smoothing-level kernel on `level` (>= 1): mode 0 y = A x, 1 y = rhs - A x,
+ * 2 y = x + omega (rhs - A x)/diag, 3 y = rhs - A (omega dinv rhs) (the nu=1
+ * pre-smoothing residual, multigrid.py:557-558).  (dev) padded vectors. */
+int rbws_level_kernel(rbws_batch* b, int level, int mode, const double* x, const double* rhs,
+                      double* y, void* stream);
+/* Copy of the per-instance Jacobi inverse diagonals 1/diag(A^level(mu)) of a
+ * set-up batch into `out` (dev, padded layout of that level). */
+int rbws_batch_dinv(rbws_batch* b, int level, double* out, void* stream);
+
 /* Optional per-kernel-class timing with CUDA events on the launch stream
  * (enable resets the counters).  Classes (9): fine apply+dot, fine CG update,
  * fine pre-smooth+residual, fine restriction, fine prolongation, fine

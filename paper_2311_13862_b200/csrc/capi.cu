@@ -1,5 +1,6 @@
 // extern "C" boundary (include/rbws_b200.h).
 #include "../../include/rbws_b200.h"
+#include "coarse.cuh"
 #include "fine.cuh"
 #include "l1roc.cuh"
 #include "solver.cuh"
@@ -107,8 +108,8 @@ int rbws_apply(rbws_batch* b, int level, const double* x, double* y, void* strea
   if (level == h->levels - 1) {
     RBWS_CHECK(rbws::fine_apply(bb->fine_op(), bb->count, x, y, nullptr, lc));
   } else {
-    rbws::St27 op{h->cells[level], bb->lv[level].coef};
-    RBWS_CHECK(rbws::st27_launch(op, bb->count, rbws::MODE_APPLY, x, nullptr, nullptr, y, 0.0, lc));
+    RBWS_CHECK(rbws::coarse_launch(0, h->cells[level], h->Q, h->d_fac[level], bb->theta, bb->count,
+                                   x, nullptr, nullptr, y, 0.0, lc));
   }
   return 0;
 }
@@ -123,9 +124,8 @@ int rbws_jacobi_sweep(rbws_batch* b, int level, const double* x, const double* r
   if (level == h->levels - 1) {
     RBWS_CHECK(rbws::fine_jacobi(bb->fine_op(), bb->count, x, rhs, y, bb->omega, nullptr, lc));
   } else {
-    rbws::St27 op{h->cells[level], bb->lv[level].coef};
-    RBWS_CHECK(rbws::st27_launch(op, bb->count, rbws::MODE_JACOBI, x, rhs, bb->lv[level].dinv, y,
-                                 bb->omega, lc));
+    RBWS_CHECK(rbws::coarse_launch(2, h->cells[level], h->Q, h->d_fac[level], bb->theta,
+                                   bb->count, x, rhs, bb->lv[level].dinv, y, bb->omega, lc));
   }
   return 0;
 }
@@ -156,6 +156,41 @@ int rbws_mgcg_solve(rbws_batch* b, const double* f, int64_t f_stride, double* x,
                     void* stream) {
   rbws::PcgOut o{iters, hist, true_res, status};
   return rbws::pcg_solve(B(b), f, f_stride, x, delta, l_max, o, S(stream));
+}
+
+int rbws_level_kernel(rbws_batch* b, int level, int mode, const double* x, const double* rhs,
+                      double* y, void* stream) {
+  Batch* bb = B(b);
+  Hierarchy* h = bb->h;
+  if (level < 1 || level >= h->levels) RBWS_FAIL("level must be in [1, levels)");
+  if (mode < 0 || mode > 3) RBWS_FAIL("mode must be 0 apply, 1 resid, 2 jacobi, 3 pre");
+  if (bb->count < 1) RBWS_FAIL("batch_setup must be called first");
+  rbws::LaunchCtx lc{S(stream), nullptr};
+  const double* dinv = bb->lv[level].dinv;
+  if (level == h->levels - 1) {
+    const rbws::Sep7 op = bb->fine_op();
+    cudaError_t e;
+    if (mode == 0) e = rbws::fine_apply(op, bb->count, x, y, nullptr, lc);
+    else if (mode == 1) e = rbws::fine_resid(op, bb->count, x, rhs, y, nullptr, lc);
+    else if (mode == 2) e = rbws::fine_jacobi(op, bb->count, x, rhs, y, bb->omega, nullptr, lc);
+    else e = rbws::fine_pre(op, bb->count, rhs, dinv, y, bb->omega, lc);
+    RBWS_CHECK(e);
+  } else {
+    RBWS_CHECK(rbws::coarse_launch(mode, h->cells[level], h->Q, h->d_fac[level], bb->theta,
+                                   bb->count, x, rhs, dinv, y, bb->omega, lc));
+  }
+  return 0;
+}
+
+int rbws_batch_dinv(rbws_batch* b, int level, double* out, void* stream) {
+  Batch* bb = B(b);
+  if (level < 1 || level >= bb->h->levels) RBWS_FAIL("level must be in [1, levels)");
+  if (bb->count < 1) RBWS_FAIL("batch_setup must be called first");
+  const int n = bb->h->cells[level];
+  RBWS_CHECK(cudaMemcpyAsync(out, bb->lv[level].dinv,
+                             sizeof(double) * rbws::vec_doubles(n, bb->count),
+                             cudaMemcpyDeviceToDevice, S(stream)));
+  return 0;
 }
 
 int rbws_batch_profile(rbws_batch* b, int enable) {

@@ -11,6 +11,7 @@
 #include <cstring>
 #include <string>
 
+#include "coarse.cuh"
 #include "fine.cuh"
 #include "solver.cuh"
 
@@ -194,7 +195,7 @@ int batch_create(Batch** out, Hierarchy* h, int cap, int nu, double omega) {
     if (l < L - 1) {
       zalloc(&lb.b, V);
       zalloc(&lb.e, V);
-      zalloc(&lb.coef, 14 * n3 * cap + n3);
+      (void)n3;
     }
   }
   if (e == cudaSuccess) {
@@ -241,10 +242,12 @@ int batch_setup(Batch* b, const double* theta, int count, cudaStream_t stream) {
   // fine level 1/diag
   e = sep7_launch(b->fine_op(), count, MODE_DINV, DOT_NONE, nullptr, nullptr, nullptr,
                   b->lv[L - 1].dinv, nullptr, b->omega, lc);
-  for (int l = 0; l < L - 1 && e == cudaSuccess; ++l)
-    e = st27_build(h->cells[l], h->Q, h->d_fac[l], b->theta, count, b->lv[l].coef,
-                   b->lv[l].dinv, stream);
-  if (e == cudaSuccess) e = coarse_factor(h->m0, count, b->lv[0].coef, b->L0, b->d_status, stream);
+  // coarse levels are matrix-free (Kronecker factors): only 1/diag is stored
+  for (int l = 1; l < L - 1 && e == cudaSuccess; ++l)
+    e = coarse_launch(4, h->cells[l], h->Q, h->d_fac[l], b->theta, count, nullptr, nullptr,
+                      nullptr, b->lv[l].dinv, 0.0, lc);
+  if (e == cudaSuccess)
+    e = coarse_factor_kf(h->m0, h->Q, h->d_fac[0], b->theta, count, b->L0, b->d_status, stream);
   if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
   return 0;
 }
@@ -304,8 +307,8 @@ int Batch::vcycle(int lvl, const double* bb, double* out, double* dot_partial,
       if (mode == MODE_RESID) return fine_resid(fo, count, x, rhs, y, nullptr, lc);
       return sep7_launch(fo, count, mode, dot, x, rhs, l.dinv, y, part, omega, lc);
     }
-    St27 s27{n, l.coef};
-    return st27_launch(s27, count, mode, x, rhs, l.dinv, y, omega, lc);
+    const int cm = (mode == MODE_PRE) ? 3 : (mode == MODE_JACOBI) ? 2 : (mode == MODE_RESID) ? 1 : 0;
+    return coarse_launch(cm, n, h->Q, h->d_fac[lvl], theta, count, x, rhs, l.dinv, y, omega, lc);
   };
   const int fdot = (fine && dot_partial) ? DOT_BY : DOT_NONE;
   const bool pf = fine && prof_on;

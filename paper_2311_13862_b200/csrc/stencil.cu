@@ -446,7 +446,10 @@ cudaError_t restrict_launch(int nf, int batch, const double* rf, double* bc, con
   return cudaGetLastError();
 }
 
-__global__ void __launch_bounds__(256) prolong_kernel(int nf, int mode,
+// z-marching trilinear prolongation: one thread per fine column (i, j); the
+// xy-interpolated coarse values of the two bracketing coarse planes are kept in
+// registers, so each fine node costs one coarse gather per two fine planes.
+__global__ void __launch_bounds__(256) prolong_kernel(int nf, int mode, int ty, int zc,
                                                       const double* __restrict__ ec,
                                                       double* __restrict__ u,
                                                       const double* __restrict__ b,
@@ -454,44 +457,57 @@ __global__ void __launch_bounds__(256) prolong_kernel(int nf, int mode,
                                                       double omega,
                                                       const int* __restrict__ active) {
   const int nc = nf / 2;
-  const int mu = blockIdx.y;
+  const int mu = blockIdx.z / zc, kc = blockIdx.z % zc;
   if (active && !active[mu]) return;
-  const int64_t nf3 = (int64_t)nf * nf * nf, nc3 = (int64_t)nc * nc * nc;
-  const int64_t X = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (X >= nf3) return;
-  const int i = X % nf, j = (X / nf) % nf, k = X / ((int64_t)nf * nf);
-  if (i == 0 || j == 0 || k == 0) return;
-  const double* e = ec + (int64_t)mu * nc3;
-  // coarse support along each axis: even -> {i/2}, odd -> {(i-1)/2, (i+1)/2}
-  const int i0 = i >> 1, j0 = j >> 1, k0 = k >> 1;
-  const int ni = (i & 1) ? 2 : 1, nj = (j & 1) ? 2 : 1, nk = (k & 1) ? 2 : 1;
-  const double wi = (i & 1) ? 0.5 : 1.0, wj = (j & 1) ? 0.5 : 1.0, wk = (k & 1) ? 0.5 : 1.0;
-  double pe = 0.0;
-  for (int c = 0; c < nk; ++c) {
-    double sy = 0.0;
-    for (int bb = 0; bb < nj; ++bb) {
-      double sx = 0.0;
-      const int64_t row = (int64_t)(k0 + c) * nc * nc + (int64_t)(j0 + bb) * nc + i0;
-      for (int a = 0; a < ni; ++a) sx += __ldg(e + row + a);
-      sy += wi * sx;
+  const int i = threadIdx.x % nf;
+  const int j = blockIdx.y * ty + threadIdx.x / nf;
+  if (i == 0 || j == 0) return;
+  const int64_t nf2 = (int64_t)nf * nf, nc2 = (int64_t)nc * nc;
+  const double* e = ec + (int64_t)mu * nc2 * nc + (i >> 1) + (int64_t)nc * (j >> 1);
+  const bool oi = i & 1, oj = j & 1;
+  auto vxy = [&](int K) -> double {  // coarse plane K interpolated to (i, j)
+    const double* q = e + nc2 * K;
+    double r0 = oi ? 0.5 * (__ldg(q) + __ldg(q + 1)) : __ldg(q);
+    if (!oj) return r0;
+    const double* q1 = q + nc;
+    const double r1 = oi ? 0.5 * (__ldg(q1) + __ldg(q1 + 1)) : __ldg(q1);
+    return 0.5 * (r0 + r1);
+  };
+  const int kz = nf / zc;
+  const int kb = max(1, kc * kz), ke = min(nf, (kc + 1) * kz);
+  int Kc = kb >> 1;
+  double v0 = vxy(Kc), v1 = vxy(Kc + 1);
+  const int64_t col = (int64_t)mu * nf2 * nf + i + (int64_t)nf * j;
+  for (int k = kb; k < ke; ++k) {
+    const int K = k >> 1;
+    if (K != Kc) {  // advance one coarse plane
+      v0 = v1;
+      v1 = vxy(K + 1);
+      Kc = K;
     }
-    pe += wj * sy;
+    const double pe = (k & 1) ? 0.5 * (v0 + v1) : v0;
+    const int64_t idx = col + (int64_t)k * nf2;
+    if (mode == 0) u[idx] += pe;
+    else u[idx] = fma(omega * __ldg(dinv + idx), __ldg(b + idx), pe);
   }
-  pe *= wk;
-  const int64_t idx = (int64_t)mu * nf3 + X;
-  if (mode == 0) u[idx] += pe;
-  else u[idx] = omega * __ldg(dinv + idx) * __ldg(b + idx) + pe;
 }
 
 cudaError_t prolong_launch(int nf, int batch, int mode, const double* ec, double* u,
                            const double* b, const double* dinv, double omega,
                            const LaunchCtx& lc) {
-  const int64_t nf3 = (int64_t)nf * nf * nf;
-  dim3 blk(256), grd((unsigned)((nf3 + 255) / 256), batch);
+  int ty = 256 / nf;
+  if (ty < 1) ty = 1;
+  if (ty > nf) ty = nf;
+  const int threads = ty * nf;
+  int zc = 1;
+  while ((int64_t)(nf / ty) * batch * zc < 4 * 148 && nf / (zc * 2) >= 4) zc *= 2;
+  dim3 grd(1, nf / ty, batch * zc);
   count_launch();
-  prolong_kernel<<<grd, blk, 0, lc.stream>>>(nf, mode, ec, u, b, dinv, omega, lc.active);
+  prolong_kernel<<<grd, threads, 0, lc.stream>>>(nf, mode, ty, zc, ec, u, b, dinv, omega,
+                                                 lc.active);
   return cudaGetLastError();
 }
+
 
 // ========================================================================
 // coarsest level: dense Cholesky per instance
