@@ -108,8 +108,8 @@ int rbws_apply(rbws_batch* b, int level, const double* x, double* y, void* strea
   if (level == h->levels - 1) {
     RBWS_CHECK(rbws::fine_apply(bb->fine_op(), bb->count, x, y, nullptr, lc));
   } else {
-    RBWS_CHECK(rbws::coarse_launch(0, h->cells[level], h->Q, h->d_fac[level], bb->theta, bb->count,
-                                   x, nullptr, nullptr, y, 0.0, lc));
+    RBWS_CHECK(rbws::coarse_launch(0, h->cells[level], h->Q, h->d_fac[level], h->d_zsame[level],
+                                   bb->theta, bb->count, x, nullptr, y, 0.0, lc));
   }
   return 0;
 }
@@ -124,8 +124,8 @@ int rbws_jacobi_sweep(rbws_batch* b, int level, const double* x, const double* r
   if (level == h->levels - 1) {
     RBWS_CHECK(rbws::fine_jacobi(bb->fine_op(), bb->count, x, rhs, y, bb->omega, nullptr, lc));
   } else {
-    RBWS_CHECK(rbws::coarse_launch(2, h->cells[level], h->Q, h->d_fac[level], bb->theta,
-                                   bb->count, x, rhs, bb->lv[level].dinv, y, bb->omega, lc));
+    RBWS_CHECK(rbws::coarse_launch(2, h->cells[level], h->Q, h->d_fac[level], h->d_zsame[level],
+                                   bb->theta, bb->count, x, rhs, y, bb->omega, lc));
   }
   return 0;
 }
@@ -175,9 +175,15 @@ int rbws_level_kernel(rbws_batch* b, int level, int mode, const double* x, const
     else if (mode == 2) e = rbws::fine_jacobi(op, bb->count, x, rhs, y, bb->omega, nullptr, lc);
     else e = rbws::fine_pre(op, bb->count, rhs, dinv, y, bb->omega, lc);
     RBWS_CHECK(e);
+  } else if (mode == 3) {  // pre-smoothing residual = residual of u = w D^-1 rhs
+    const int n = h->cells[level];
+    RBWS_CHECK(rbws::vec_scale_dinv(n, bb->count, bb->omega, dinv, rhs, bb->lv[level].u, S(stream)));
+    RBWS_CHECK(rbws::coarse_launch(1, n, h->Q, h->d_fac[level], h->d_zsame[level], bb->theta,
+                                   bb->count, bb->lv[level].u, rhs, y, bb->omega, lc));
   } else {
-    RBWS_CHECK(rbws::coarse_launch(mode, h->cells[level], h->Q, h->d_fac[level], bb->theta,
-                                   bb->count, x, rhs, dinv, y, bb->omega, lc));
+    RBWS_CHECK(rbws::coarse_launch(mode, h->cells[level], h->Q, h->d_fac[level],
+                                   h->d_zsame[level], bb->theta, bb->count, x, rhs, y, bb->omega,
+                                   lc));
   }
   return 0;
 }

@@ -9,8 +9,13 @@
 // are cached in registers and recomputed only on planes whose z factors differ
 // from the previous plane's (a CTA-uniform flag); for thermal blocks that is
 // a handful of planes per column, so per-instance coefficient arrays never
-// exist in HBM.  Input planes (tile rows + one halo row each side) are staged
-// with one TMA bulk copy per array per plane into an 8-slot mbarrier ring.
+// exist in HBM.  The stencil input (tile rows + one halo row each side) and the
+// centre rhs are staged with one TMA bulk copy per array per plane into an
+// 8-slot mbarrier ring.
+//
+// The nu=1 pre-smoothing residual b - A(w D^-1 b) is evaluated as a plain
+// residual of u = w D^-1 b, which the restriction kernel writes next to the
+// coarse rhs (restrict_launch with dinv), so no per-neighbour scaling is needed.
 #include "coarse.cuh"
 #include "tma.cuh"
 
@@ -34,12 +39,12 @@ CoarseGeom coarse_geom(int n, int batch) {
 
 struct CoarseArgs {
   int n, Q;
+  const int* zsame;     // [n+1] plane k repeats plane k-1's z factors (host precomputed)
   CoarseGeom g;
   const double* fac;    // [Q*3][3][2][n+1]
   const double* theta;  // [batch][Q]
-  const double* x;      // staged (halo)
-  const double* dinv;   // staged (halo), PRE only
-  const double* b;      // centre (global loads)
+  const double* x;      // stencil input, staged with halo rows
+  const double* b;      // centre rhs, staged (RESID / JACOBI)
   double* y;
   const int* active;
   double omega;
@@ -54,12 +59,13 @@ __device__ __forceinline__ double tri(const double* f, int n1, int i, int o) {
   return __ldg(f + n1 + i - 1);
 }
 
-template <int MODE>
+template <int Q, int MODE>
 __global__ void __launch_bounds__(256) coarse_kernel(CoarseArgs a) {
-  constexpr int NH = (MODE == CM_PRE) ? 2 : ((MODE == CM_DINV) ? 0 : 1);
+  constexpr int NH = (MODE == CM_DINV) ? 0 : 1;                          // halo-staged arrays
+  constexpr int NC = (MODE == CM_RESID || MODE == CM_JACOBI) ? 1 : 0;     // centre-staged arrays
   constexpr int S = kCStages;
   extern __shared__ __align__(128) unsigned char smem[];
-  const int n = a.n, n1 = n + 1, Q = a.Q;
+  const int n = a.n, n1 = n + 1;
   const int ty = a.g.ty, zc = a.g.zc;
   const int kc = blockIdx.z % zc, mu = blockIdx.z / zc;
   if (a.active && !a.active[mu]) return;
@@ -77,45 +83,39 @@ __global__ void __launch_bounds__(256) coarse_kernel(CoarseArgs a) {
   double* ring = reinterpret_cast<double*>(smem + 64 + 4 * kCMaxPlanes + 64);
   // slot = (ty+2) staged rows + 2 zero pad doubles: the 27-point corner neighbour of
   // the tile's last column/row reads one element past the staged rows (a ghost, 0)
-  const int hsz = (ty + 2) * n + 2;
-  auto hptr = [&](int st, int arr) { return ring + (st * NH + arr) * hsz; };
+  const int hsz = (ty + 2) * n + 2, csz = ty * n;
+  const int ssz = NH * hsz + NC * csz;
+  double* const xring = ring;
+  auto xs = [&](int st) { return xring + st * ssz; };
+  auto bs = [&](int st) { return xring + st * ssz + NH * hsz; };
 
   const double* fac = a.fac;
   const int fstride = 2 * n1;  // one axis factor [diag | upper]
-  auto zfac = [&](int t, int k, int oz) {  // Z factor of part t at plane k, offset oz
-    return tri(fac + ((size_t)t * 3 + 2) * fstride, n1, k, oz);
-  };
   if (tid == 0 && NH > 0) {
 #pragma unroll
     for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
     mbar_fence_init();
   }
   if (NH > 0) {  // zero the pads and (first tile) the never-staged halo row above row 0
-    for (int t = tid; t < S * NH; t += blockDim.x) {
-      double* sl = ring + t * hsz;
-      sl[hsz - 2] = 0.0;
-      sl[hsz - 1] = 0.0;
+    for (int t = tid; t < S; t += blockDim.x) {
+      xs(t)[hsz - 2] = 0.0;
+      xs(t)[hsz - 1] = 0.0;
     }
     if (j0 == 0)
-      for (int t = tid; t < S * NH * n; t += blockDim.x) ring[(t / n) * hsz + t % n] = 0.0;
+      for (int t = tid; t < S * n; t += blockDim.x) xs(t / n)[t % n] = 0.0;
   }
-  for (int p = 1 + tid; p < np; p += blockDim.x) {
-    const int k = p_first + p;
-    int same = 1;
-    for (int t = 0; t < 3 * Q && same; ++t)
-      for (int oz = -1; oz <= 1; ++oz) same &= (zfac(t, k, oz) == zfac(t, k - 1, oz));
-    zsame[p] = same;
-  }
+  for (int p = 1 + tid; p < np; p += blockDim.x) zsame[p] = a.zsame[p_first + p];
   __syncthreads();
 
   auto issue = [&](int p) {
     const int st = (p - p_first) & (S - 1);
     const int skip = (j0 == 0) ? 1 : 0;
-    const uint32_t bytes = (uint32_t)((ty + 2 - skip) * n * 8);
-    mbar_arrive_expect_tx(&bar[st], NH * bytes);
-    const int64_t plane = base + (int64_t)p * n2 + (int64_t)(j0 - 1 + skip) * n;
-    bulk_g2s(hptr(st, 0) + skip * n, a.x + plane, bytes, &bar[st]);
-    if (NH == 2) bulk_g2s(hptr(st, 1) + skip * n, a.dinv + plane, bytes, &bar[st]);
+    const uint32_t hbytes = (uint32_t)((ty + 2 - skip) * n * 8);
+    const uint32_t cbytes = (uint32_t)(ty * n * 8);
+    mbar_arrive_expect_tx(&bar[st], NH * hbytes + NC * cbytes);
+    const int64_t plane = base + (int64_t)p * n2;
+    bulk_g2s(xs(st) + skip * n, a.x + plane + (int64_t)(j0 - 1 + skip) * n, hbytes, &bar[st]);
+    if (NC) bulk_g2s(bs(st), a.b + plane + (int64_t)j0 * n, cbytes, &bar[st]);
   };
   if (NH > 0 && tid == 0)
     for (int p = p_first; p <= p_last && p < p_first + S; ++p) issue(p);
@@ -123,30 +123,38 @@ __global__ void __launch_bounds__(256) coarse_kernel(CoarseArgs a) {
   const int i = tid % n, jl = tid / n, j = j0 + jl;
   const bool on = (i >= 1) && (j >= 1);
   const double* th = a.theta + (size_t)mu * Q;
-  double c[27];  // c[(oz+1)*9 + (oy+1)*3 + (ox+1)]
+  // 27 coefficients, c<oz><oy><ox> with m/0/p = -1/0/+1
+  double cmmm, cmm0, cmmp, cm0m, cm00, cm0p, cmpm, cmp0, cmpp;
+  double c0mm, c0m0, c0mp, c00m, c000, c00p, c0pm, c0p0, c0pp;
+  double cpmm, cpm0, cpmp, cp0m, cp00, cp0p, cppm, cpp0, cppp;
   auto coeffs = [&](int k) {
-#pragma unroll
-    for (int o = 0; o < 27; ++o) c[o] = 0.0;
+    cmmm = cmm0 = cmmp = cm0m = cm00 = cm0p = cmpm = cmp0 = cmpp = 0.0;
+    c0mm = c0m0 = c0mp = c00m = c000 = c00p = c0pm = c0p0 = c0pp = 0.0;
+    cpmm = cpm0 = cpmp = cp0m = cp00 = cp0p = cppm = cpp0 = cppp = 0.0;
     if (!on) return;
+#pragma unroll
     for (int t = 0; t < 3 * Q; ++t) {
       const double tq = th[t / 3];
       const double* fx = fac + ((size_t)t * 3 + 0) * fstride;
       const double* fy = fac + ((size_t)t * 3 + 1) * fstride;
-      double X[3], Y[3], Z[3];
-#pragma unroll
-      for (int o = -1; o <= 1; ++o) {
-        X[o + 1] = tri(fx, n1, i, o);
-        Y[o + 1] = tq * tri(fy, n1, j, o);
-        Z[o + 1] = zfac(t, k, o);
-      }
-#pragma unroll
-      for (int oz = 0; oz < 3; ++oz)
-#pragma unroll
-        for (int oy = 0; oy < 3; ++oy) {
-          const double yz = Y[oy] * Z[oz];
-#pragma unroll
-          for (int ox = 0; ox < 3; ++ox) c[oz * 9 + oy * 3 + ox] = fma(X[ox], yz, c[oz * 9 + oy * 3 + ox]);
-        }
+      const double* fz = fac + ((size_t)t * 3 + 2) * fstride;
+      const double xm = tri(fx, n1, i, -1), x0 = tri(fx, n1, i, 0), xp = tri(fx, n1, i, 1);
+      const double ym = tq * tri(fy, n1, j, -1), y0 = tq * tri(fy, n1, j, 0),
+                   yp = tq * tri(fy, n1, j, 1);
+      const double zm = tri(fz, n1, k, -1), z0 = tri(fz, n1, k, 0), zp = tri(fz, n1, k, 1);
+#define RBWS_ROW(Z, Y, YZ, C_M, C_0, C_P) \
+  {                                       \
+    const double YZ = Y * Z;              \
+    C_M = fma(xm, YZ, C_M);               \
+    C_0 = fma(x0, YZ, C_0);               \
+    C_P = fma(xp, YZ, C_P);               \
+  }
+      RBWS_ROW(zm, ym, a1, cmmm, cmm0, cmmp) RBWS_ROW(zm, y0, a2, cm0m, cm00, cm0p)
+      RBWS_ROW(zm, yp, a3, cmpm, cmp0, cmpp) RBWS_ROW(z0, ym, a4, c0mm, c0m0, c0mp)
+      RBWS_ROW(z0, y0, a5, c00m, c000, c00p) RBWS_ROW(z0, yp, a6, c0pm, c0p0, c0pp)
+      RBWS_ROW(zp, ym, a7, cpmm, cpm0, cpmp) RBWS_ROW(zp, y0, a8, cp0m, cp00, cp0p)
+      RBWS_ROW(zp, yp, a9, cppm, cpp0, cppp)
+#undef RBWS_ROW
     }
   };
 
@@ -156,86 +164,114 @@ __global__ void __launch_bounds__(256) coarse_kernel(CoarseArgs a) {
     mbar_wait(&bar[0], 0u);
     mbar_wait(&bar[1], 0u);
   }
-  for (int k = kb; k < ke; ++k) {
-    const int idx = k + 1 - p_first;
-    if (NH > 0) mbar_wait(&bar[idx & (S - 1)], (uint32_t)((idx / S) & 1));
-    if (k == kb || !zsame[k - p_first]) coeffs(k);
-    const int64_t gidx = base + (int64_t)k * n2 + (int64_t)j * n + i;
-    if (MODE == CM_DINV) {
-      if (on) a.y[gidx] = 1.0 / c[13];
-      continue;
-    }
-    const int s0 = (idx - 1) & (S - 1);
-
-    double Au = 0.0, uc = 0.0;
+  // KB planes per trip: one CTA barrier and KB TMA issues amortised over KB nodes
+  constexpr int KB = 2;
+  for (int k0 = kb; k0 < ke; k0 += KB) {
 #pragma unroll
-    for (int oz = 0; oz < 3; ++oz) {
-      const double* X = hptr((idx - 2 + oz) & (S - 1), 0);
-      const double* D = (MODE == CM_PRE) ? hptr((idx - 2 + oz) & (S - 1), 1) : nullptr;
-#pragma unroll
-      for (int oy = 0; oy < 3; ++oy)
-#pragma unroll
-        for (int ox = 0; ox < 3; ++ox) {
-          const int id = hi + (oy - 1) * n + (ox - 1);
-          const double u = (MODE == CM_PRE) ? om * D[id] * X[id] : X[id];
-          Au = fma(c[oz * 9 + oy * 3 + ox], u, Au);
-          if (oz == 1 && oy == 1 && ox == 1) uc = u;
+    for (int u = 0; u < KB; ++u) {
+      const int k = k0 + u;
+      if (k >= ke) break;
+      const int idx = k + 1 - p_first;
+      if (NH > 0) mbar_wait(&bar[idx & (S - 1)], (uint32_t)((idx / S) & 1));
+      if (k == kb || !zsame[k - p_first]) coeffs(k);
+      const int64_t gidx = base + (int64_t)k * n2 + (int64_t)j * n + i;
+      if (MODE == CM_DINV) {
+        if (on) a.y[gidx] = 1.0 / c000;
+        continue;
+      }
+      const double* XM = xs((idx - 2) & (S - 1)) + hi;
+      const double* X0 = xs((idx - 1) & (S - 1)) + hi;
+      const double* XP = xs(idx & (S - 1)) + hi;
+#define RBWS_PL(P, CMM, CM0, CMP, C0M, C00, C0P, CPM, CP0, CPP, R)                       \
+  const double R##a = fma(CMP, P[-n + 1], fma(CM0, P[-n], CMM * P[-n - 1]));                 \
+  const double R##b = fma(C0P, P[1], fma(C00, P[0], C0M * P[-1]));                          \
+  const double R##c = fma(CPP, P[n + 1], fma(CP0, P[n], CPM * P[n - 1]));                   \
+  const double R = (R##a + R##b) + R##c;
+      RBWS_PL(XM, cmmm, cmm0, cmmp, cm0m, cm00, cm0p, cmpm, cmp0, cmpp, am)
+      RBWS_PL(X0, c0mm, c0m0, c0mp, c00m, c000, c00p, c0pm, c0p0, c0pp, a0)
+      RBWS_PL(XP, cpmm, cpm0, cpmp, cp0m, cp00, cp0p, cppm, cpp0, cppp, ap)
+      const double Au = (am + ap) + a0;
+#undef RBWS_PL
+      if (on) {
+        if (MODE == CM_APPLY) {
+          a.y[gidx] = Au;
+        } else if (MODE == CM_RESID) {
+          a.y[gidx] = bs((idx - 1) & (S - 1))[jl * n + i] - Au;
+        } else {  // CM_JACOBI
+          const double bv = bs((idx - 1) & (S - 1))[jl * n + i];
+          a.y[gidx] = X0[0] + om * (bv - Au) / c000;
         }
-    }
-    if (on) {
-      if (MODE == CM_APPLY) a.y[gidx] = Au;
-      else if (MODE == CM_RESID) a.y[gidx] = __ldg(a.b + gidx) - Au;
-      else if (MODE == CM_PRE) a.y[gidx] = hptr(s0, 0)[hi] - Au;
-      else a.y[gidx] = uc + om * (__ldg(a.b + gidx) - Au) / c[13];  // CM_JACOBI
+      }
     }
     if (NH > 0) {
-      __syncthreads();
-      if (tid == 0 && k - 1 + S <= p_last) issue(k - 1 + S);
+      __syncthreads();  // every thread is done with planes k0-1 .. k0+KB-2
+      if (tid == 0) {
+#pragma unroll
+        for (int u = 0; u < KB; ++u) {
+          const int pn = k0 - 1 + u + S;
+          if (pn <= p_last) issue(pn);
+        }
+      }
     }
   }
 }
 
-template <int MODE>
+template <int Q, int MODE>
 static cudaError_t coarse_launch_m(CoarseArgs a, int batch, cudaStream_t stream) {
-  constexpr int NH = (MODE == CM_PRE) ? 2 : ((MODE == CM_DINV) ? 0 : 1);
+  constexpr int NH = (MODE == CM_DINV) ? 0 : 1;
+  constexpr int NC = (MODE == CM_RESID || MODE == CM_JACOBI) ? 1 : 0;
   a.g = coarse_geom(a.n, batch);
   if (a.n / a.g.zc + 2 > kCMaxPlanes) return cudaErrorInvalidValue;
-  const size_t smem =
-      64 + 4 * kCMaxPlanes + 64 + (size_t)kCStages * NH * ((a.g.ty + 2) * a.n + 2) * 8;
+  const size_t smem = 64 + 4 * kCMaxPlanes + 64 +
+                      (size_t)kCStages * (NH * ((a.g.ty + 2) * a.n + 2) + NC * a.g.ty * a.n) * 8;
   static size_t attr = 48 * 1024;
   if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(coarse_kernel<MODE>,
+    cudaError_t e = cudaFuncSetAttribute(coarse_kernel<Q, MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = smem;
   }
   dim3 grd(1, a.g.ytiles, batch * a.g.zc);
   count_launch();
-  coarse_kernel<MODE><<<grd, a.g.threads, smem, stream>>>(a);
+  coarse_kernel<Q, MODE><<<grd, a.g.threads, smem, stream>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t coarse_launch(int mode, int n, int Q, const double* fac, const double* theta,
-                          int batch, const double* x, const double* b, const double* dinv,
+template <int Q>
+static cudaError_t coarse_launch_q(int mode, const CoarseArgs& a, int batch, cudaStream_t stream) {
+  switch (mode) {
+    case CM_APPLY: return coarse_launch_m<Q, CM_APPLY>(a, batch, stream);
+    case CM_RESID: return coarse_launch_m<Q, CM_RESID>(a, batch, stream);
+    case CM_JACOBI: return coarse_launch_m<Q, CM_JACOBI>(a, batch, stream);
+    case CM_DINV: return coarse_launch_m<Q, CM_DINV>(a, batch, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t coarse_launch(int mode, int n, int Q, const double* fac, const int* zsame,
+                          const double* theta, int batch, const double* x, const double* b,
                           double* y, double omega, const LaunchCtx& lc) {
   if (n < 2 || n > 256) return cudaErrorInvalidValue;
   CoarseArgs a{};
   a.n = n;
   a.Q = Q;
+  a.zsame = zsame;
   a.fac = fac;
   a.theta = theta;
-  a.x = (mode == CM_PRE) ? b : x;  // PRE stages the right-hand side (u = w dinv b)
+  a.x = x;
   a.b = b;
-  a.dinv = dinv;
   a.y = y;
   a.active = lc.active;
   a.omega = omega;
-  switch (mode) {
-    case CM_APPLY: return coarse_launch_m<CM_APPLY>(a, batch, lc.stream);
-    case CM_RESID: return coarse_launch_m<CM_RESID>(a, batch, lc.stream);
-    case CM_JACOBI: return coarse_launch_m<CM_JACOBI>(a, batch, lc.stream);
-    case CM_PRE: return coarse_launch_m<CM_PRE>(a, batch, lc.stream);
-    case CM_DINV: return coarse_launch_m<CM_DINV>(a, batch, lc.stream);
+  switch (Q) {
+    case 1: return coarse_launch_q<1>(mode, a, batch, lc.stream);
+    case 2: return coarse_launch_q<2>(mode, a, batch, lc.stream);
+    case 3: return coarse_launch_q<3>(mode, a, batch, lc.stream);
+    case 4: return coarse_launch_q<4>(mode, a, batch, lc.stream);
+    case 5: return coarse_launch_q<5>(mode, a, batch, lc.stream);
+    case 6: return coarse_launch_q<6>(mode, a, batch, lc.stream);
+    case 7: return coarse_launch_q<7>(mode, a, batch, lc.stream);
+    case 8: return coarse_launch_q<8>(mode, a, batch, lc.stream);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -12,8 +12,9 @@ CoarseGeom coarse_geom(int n, int batch);
 
 // mode: 0 apply y=Ax | 1 resid y=b-Ax | 2 jacobi y=x+w(b-Ax)/diag | 3 pre y=b-A(w dinv b)
 //       4 dinv y=1/diag.  fac: the level's Kronecker factors [Q*3][3][2][n+1].
-cudaError_t coarse_launch(int mode, int n, int Q, const double* fac, const double* theta,
-                          int batch, const double* x, const double* b, const double* dinv,
+//       zsame: [n+1] per-plane flag "z factors equal the previous plane's" (host built).
+cudaError_t coarse_launch(int mode, int n, int Q, const double* fac, const int* zsame,
+                          const double* theta, int batch, const double* x, const double* b,
                           double* y, double omega, const LaunchCtx& lc);
 // coarsest level: dense Galerkin operator from the factors + Cholesky per instance
 cudaError_t coarse_factor_kf(int n0, int Q, const double* fac, const double* theta, int batch,

@@ -31,7 +31,7 @@ FineGeom fine_geom(int n, int batch) {
   if (rpp < 1) rpp = 1;
   if (rpp > n) rpp = n;
   g.rpp = rpp;
-  g.npt = 1;
+  g.npt = (rpp * 2 <= n) ? 2 : 1;
   g.ty = rpp * g.npt;
   g.threads = rpp * n;
   g.ytiles = n / g.ty;
@@ -236,12 +236,11 @@ __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
           uc = X0[hi]; ue = X0[hi + 1]; uw = X0[hi - 1]; un = X0[hi + n]; us = X0[hi - n];
           uu = XP[hi]; ud = XM[hi];
         }
-        double off = wxp[r] * ue;
-        off = fma(wxm[r], uw, off);
-        off = fma(wyp[r], un, off);
-        off = fma(wym[r], us, off);
-        off = fma(wzp[r], uu, off);
-        off = fma(wzm[r], ud, off);
+        // shallow FMA tree (a dependent chain of 6 would be latency bound)
+        const double offx = fma(wxm[r], uw, wxp[r] * ue);
+        const double offy = fma(wym[r], us, wyp[r] * un);
+        const double offz = fma(wzm[r], ud, wzp[r] * uu);
+        const double off = (offx + offy) + offz;
         const double d = dg[r];
         const double Au = fma(d, uc, -off);
         const bool on = (i != 0) && (j != 0);  // Dirichlet ghost column / row
@@ -314,7 +313,7 @@ static cudaError_t fine_launch_qmn(const FineArgs& a, int batch, cudaStream_t st
 
 template <int Q, int MODE>
 static cudaError_t fine_launch_qm(const FineArgs& a, int batch, cudaStream_t stream) {
-  if (a.g.npt == 4) return fine_launch_qmn<Q, MODE, 4>(a, batch, stream);
+  if (a.g.npt == 2) return fine_launch_qmn<Q, MODE, 2>(a, batch, stream);
   if (a.g.npt == 1) return fine_launch_qmn<Q, MODE, 1>(a, batch, stream);
   return cudaErrorInvalidValue;
 }

@@ -45,6 +45,7 @@ Hierarchy::~Hierarchy() {
   cudaFree(d_face);
   cudaFree(d_node);
   for (double* p : d_fac) cudaFree(p);
+  for (int* p : d_zsame) cudaFree(p);
 }
 
 // 1D Galerkin product P^T T P of a tridiagonal interior operator
@@ -136,11 +137,31 @@ int hierarchy_create(Hierarchy** out, int n, int m0, int Q, const double* face,
   if (e == cudaSuccess) e = cudaMemcpy(h->d_face, face, sizeof(double) * Q * 3 * n, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(h->d_node, node, sizeof(double) * Q * 9 * (n + 1), cudaMemcpyHostToDevice);
   h->d_fac.assign(L, nullptr);
+  h->d_zsame.assign(L, nullptr);
   for (int l = 0; l < L && e == cudaSuccess; ++l) {
     e = dalloc(&h->d_fac[l], h->h_fac[l].size());
     if (e == cudaSuccess)
       e = cudaMemcpy(h->d_fac[l], h->h_fac[l].data(), sizeof(double) * h->h_fac[l].size(),
                      cudaMemcpyHostToDevice);
+    // per plane k: do all z factors (offsets -1, 0, +1 of every part) equal plane k-1's?
+    const int nl = h->cells[l], n1 = nl + 1;
+    const std::vector<double>& f = h->h_fac[l];
+    std::vector<int> zs(nl + 1, 0);
+    auto zt = [&](int t, int k, int o) {
+      const double* fz = &f[((size_t)t * 3 + 2) * 2 * n1];
+      if (o == 0) return fz[k];
+      if (o > 0) return fz[n1 + k];
+      return k >= 1 ? fz[n1 + k - 1] : 0.0;
+    };
+    for (int k = 1; k <= nl; ++k) {
+      int same = 1;
+      for (int t = 0; t < 3 * Q && same; ++t)
+        for (int o = -1; o <= 1; ++o) same &= (zt(t, k, o) == zt(t, k - 1, o)) ? 1 : 0;
+      zs[k] = same;
+    }
+    if (e == cudaSuccess) e = dalloc(&h->d_zsame[l], zs.size());
+    if (e == cudaSuccess)
+      e = cudaMemcpy(h->d_zsame[l], zs.data(), sizeof(int) * zs.size(), cudaMemcpyHostToDevice);
   }
   if (e != cudaSuccess) { delete h; RBWS_FAIL(cudaGetErrorString(e)); }
   *out = h;
@@ -153,7 +174,7 @@ Batch::~Batch() {
   cudaFree(theta);
   for (auto& l : lv) {
     cudaFree(l.b); cudaFree(l.e); cudaFree(l.t1); cudaFree(l.t2); cudaFree(l.t3);
-    cudaFree(l.zero); cudaFree(l.dinv); cudaFree(l.coef);
+    cudaFree(l.zero); cudaFree(l.dinv); cudaFree(l.coef); cudaFree(l.u);
   }
   cudaFree(L0); cudaFree(d_status);
   cudaFree(r); cudaFree(p); cudaFree(p2); cudaFree(s); cudaFree(t_res);
@@ -192,6 +213,7 @@ int batch_create(Batch** out, Hierarchy* h, int cap, int nu, double omega) {
     zalloc(&lb.t1, V);
     zalloc(&lb.dinv, V);
     if (nu != 1) { zalloc(&lb.t2, V); zalloc(&lb.t3, V); zalloc(&lb.zero, V); }
+    if (l >= 1 && l < L - 1) zalloc(&lb.u, V);
     if (l < L - 1) {
       zalloc(&lb.b, V);
       zalloc(&lb.e, V);
@@ -244,8 +266,8 @@ int batch_setup(Batch* b, const double* theta, int count, cudaStream_t stream) {
                   b->lv[L - 1].dinv, nullptr, b->omega, lc);
   // coarse levels are matrix-free (Kronecker factors): only 1/diag is stored
   for (int l = 1; l < L - 1 && e == cudaSuccess; ++l)
-    e = coarse_launch(4, h->cells[l], h->Q, h->d_fac[l], b->theta, count, nullptr, nullptr,
-                      nullptr, b->lv[l].dinv, 0.0, lc);
+    e = coarse_launch(4, h->cells[l], h->Q, h->d_fac[l], h->d_zsame[l], b->theta, count,
+                      nullptr, nullptr, b->lv[l].dinv, 0.0, lc);
   if (e == cudaSuccess)
     e = coarse_factor_kf(h->m0, h->Q, h->d_fac[0], b->theta, count, b->L0, b->d_status, stream);
   if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
@@ -307,8 +329,13 @@ int Batch::vcycle(int lvl, const double* bb, double* out, double* dot_partial,
       if (mode == MODE_RESID) return fine_resid(fo, count, x, rhs, y, nullptr, lc);
       return sep7_launch(fo, count, mode, dot, x, rhs, l.dinv, y, part, omega, lc);
     }
-    const int cm = (mode == MODE_PRE) ? 3 : (mode == MODE_JACOBI) ? 2 : (mode == MODE_RESID) ? 1 : 0;
-    return coarse_launch(cm, n, h->Q, h->d_fac[lvl], theta, count, x, rhs, l.dinv, y, omega, lc);
+    // coarse levels: the pre-smoothing residual is a residual of the pre-scaled rhs l.u
+    if (mode == MODE_PRE)
+      return coarse_launch(1, n, h->Q, h->d_fac[lvl], h->d_zsame[lvl], theta, count, l.u, rhs, y,
+                           omega, lc);
+    const int cm = (mode == MODE_JACOBI) ? 2 : (mode == MODE_RESID) ? 1 : 0;
+    return coarse_launch(cm, n, h->Q, h->d_fac[lvl], h->d_zsame[lvl], theta, count, x, rhs, y,
+                         omega, lc);
   };
   const int fdot = (fine && dot_partial) ? DOT_BY : DOT_NONE;
   const bool pf = fine && prof_on;
@@ -316,12 +343,16 @@ int Batch::vcycle(int lvl, const double* bb, double* out, double* dot_partial,
     int t0 = pf ? prof_begin(lc.stream) : -1;
     e = op(MODE_PRE, DOT_NONE, nullptr, bb, l.t1, nullptr);
     if (pf) { prof_end(PROF_FINE_PRE, t0, lc.stream); t0 = prof_begin(lc.stream); }
-    if (e == cudaSuccess) e = restrict_launch(n, count, l.t1, c.b, lc);
+    // the restriction also writes the next level's pre-scaled rhs u = w D^-1 b
+    if (e == cudaSuccess)
+      e = (lvl - 1 >= 1) ? restrict_launch(n, count, l.t1, c.b, lc, c.dinv, c.u, omega)
+                         : restrict_launch(n, count, l.t1, c.b, lc);
     if (pf) { prof_end(PROF_FINE_RESTRICT, t0, lc.stream); t0 = prof_begin(lc.stream); }
     if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
     if (vcycle(lvl - 1, c.b, c.e, nullptr, lc)) return 1;
     if (pf) { prof_end(PROF_COARSE, t0, lc.stream); t0 = prof_begin(lc.stream); }
-    e = prolong_launch(n, count, 1, c.e, l.t1, bb, l.dinv, omega, lc);
+    e = fine ? prolong_launch(n, count, 1, c.e, l.t1, bb, l.dinv, omega, lc)
+             : prolong_launch(n, count, 2, c.e, l.t1, l.u, nullptr, omega, lc);
     if (pf) { prof_end(PROF_FINE_PROLONG, t0, lc.stream); t0 = prof_begin(lc.stream); }
     if (e == cudaSuccess) e = op(MODE_JACOBI, fdot, l.t1, bb, out, dot_partial);
     if (pf) prof_end(PROF_FINE_POST, t0, lc.stream);

@@ -17,6 +17,7 @@ struct Hierarchy {
   double* d_face = nullptr;         // fine separable tables
   double* d_node = nullptr;
   std::vector<double*> d_fac;       // per level 1D Kronecker factors [Q*3][3][2][n+1]
+  std::vector<int*> d_zsame;        // per level [n+1]: z factors of plane k == plane k-1
   std::vector<std::vector<double>> h_fac;
 
   ~Hierarchy();
@@ -36,7 +37,8 @@ struct LevelBuf {
   double* t3 = nullptr;    // scratch (nu != 1)
   double* zero = nullptr;  // zeros (nu != 1)
   double* dinv = nullptr;  // 1/diag per instance
-  double* coef = nullptr;  // 27-point coefficients (coarse levels)
+  double* coef = nullptr;  // (unused: coarse operators are matrix-free)
+  double* u = nullptr;     // pre-scaled rhs w D^-1 b (coarse levels 1..L-2, nu=1)
 };
 
 // kernel classes timed by the optional event profiler (bench.py roofline)

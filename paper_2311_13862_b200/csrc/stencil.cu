@@ -410,7 +410,9 @@ cudaError_t st27_build(int n, int Q, const double* fac, const double* theta, int
 
 __global__ void __launch_bounds__(256) restrict_kernel(int nf, const double* __restrict__ rf,
                                                        double* __restrict__ bc,
-                                                       const int* __restrict__ active) {
+                                                       const int* __restrict__ active,
+                                                       const double* __restrict__ dinv_c,
+                                                       double* __restrict__ uc, double omega) {
   const int nc = nf / 2;
   const int mu = blockIdx.y;
   if (active && !active[mu]) return;
@@ -434,15 +436,18 @@ __global__ void __launch_bounds__(256) restrict_kernel(int nf, const double* __r
     }
     acc += (dz == 0 ? 1.0 : 0.5) * pz;
   }
-  bc[(int64_t)mu * nc3 + X] = acc;
+  const int64_t o = (int64_t)mu * nc3 + X;
+  bc[o] = acc;
+  if (uc) uc[o] = omega * __ldg(dinv_c + o) * acc;  // pre-scaled rhs of the coarse pre-smoother
 }
 
-cudaError_t restrict_launch(int nf, int batch, const double* rf, double* bc, const LaunchCtx& lc) {
+cudaError_t restrict_launch(int nf, int batch, const double* rf, double* bc, const LaunchCtx& lc,
+                            const double* dinv_c, double* uc, double omega) {
   const int nc = nf / 2;
   const int64_t nc3 = (int64_t)nc * nc * nc;
   dim3 blk(256), grd((unsigned)((nc3 + 255) / 256), batch);
   count_launch();
-  restrict_kernel<<<grd, blk, 0, lc.stream>>>(nf, rf, bc, lc.active);
+  restrict_kernel<<<grd, blk, 0, lc.stream>>>(nf, rf, bc, lc.active, dinv_c, uc, omega);
   return cudaGetLastError();
 }
 
@@ -488,6 +493,7 @@ __global__ void __launch_bounds__(256) prolong_kernel(int nf, int mode, int ty, 
     const double pe = (k & 1) ? 0.5 * (v0 + v1) : v0;
     const int64_t idx = col + (int64_t)k * nf2;
     if (mode == 0) u[idx] += pe;
+    else if (mode == 2) u[idx] = __ldg(b + idx) + pe;  // b holds the pre-scaled rhs w D^-1 b
     else u[idx] = fma(omega * __ldg(dinv + idx), __ldg(b + idx), pe);
   }
 }
@@ -637,6 +643,25 @@ cudaError_t coarse_solve(int n0, int batch, const double* L, const double* b, do
 // ========================================================================
 // vector ops on padded batch vectors
 // ========================================================================
+
+__global__ void __launch_bounds__(256) scale_dinv_kernel(int64_t n3, double omega,
+                                                         const double* __restrict__ dinv,
+                                                         const double* __restrict__ b,
+                                                         double* __restrict__ u) {
+  const int64_t base = (int64_t)blockIdx.y * n3;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n3;
+       idx += (int64_t)gridDim.x * blockDim.x)
+    u[base + idx] = omega * __ldg(dinv + base + idx) * __ldg(b + base + idx);
+}
+
+cudaError_t vec_scale_dinv(int n, int batch, double omega, const double* dinv, const double* b,
+                           double* u, cudaStream_t stream) {
+  const int64_t n3 = (int64_t)n * n * n;
+  dim3 blk(256), grd((unsigned)((n3 + 1023) / 1024), batch);
+  count_launch();
+  scale_dinv_kernel<<<grd, blk, 0, stream>>>(n3, omega, dinv, b, u);
+  return cudaGetLastError();
+}
 
 int vec_tiles(int n) {
   const int64_t n3 = (int64_t)n * n * n;

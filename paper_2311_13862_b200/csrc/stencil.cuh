@@ -45,9 +45,11 @@ cudaError_t st27_build(int n, int Q, const double* fac, const double* theta, int
                        double* coef, double* dinv, cudaStream_t stream);
 
 // ---- transfers -----------------------------------------------------------
-// bc = P^T r  (coarse n_c = n_f/2)
-cudaError_t restrict_launch(int nf, int batch, const double* rf, double* bc, const LaunchCtx& lc);
-// mode 0: u += P e ;  mode 1: u = omega dinv b + P e
+// bc = P^T r  (coarse n_c = n_f/2); with dinv_c/uc also uc = omega dinv_c bc
+cudaError_t restrict_launch(int nf, int batch, const double* rf, double* bc, const LaunchCtx& lc,
+                            const double* dinv_c = nullptr, double* uc = nullptr,
+                            double omega = 0.0);
+// mode 0: u += P e ;  mode 1: u = omega dinv b + P e ;  mode 2: u = b + P e
 cudaError_t prolong_launch(int nf, int batch, int mode, const double* ec, double* u,
                            const double* b, const double* dinv, double omega, const LaunchCtx& lc);
 
@@ -60,6 +62,9 @@ cudaError_t coarse_solve(int n0, int batch, const double* L, const double* b, do
 // ---- vector ops ----------------------------------------------------------
 // partial[mu*tiles + t] = sum x*y over instance mu (tiles from vec_tiles)
 int vec_tiles(int n);
+// u = omega dinv b (elementwise, padded batch vectors)
+cudaError_t vec_scale_dinv(int n, int batch, double omega, const double* dinv, const double* b,
+                           double* u, cudaStream_t stream);
 cudaError_t vec_dot(int n, int batch, const double* x, int64_t x_stride, const double* y,
                     int64_t y_stride, double* partial, const LaunchCtx& lc);
 // y = a*x + beta[mu]*y   (beta may be null -> 0);  ghosts untouched (they are 0)
