@@ -306,6 +306,7 @@ def run_b200(args, rank, world, dist):
 
 def cpu_baseline(cfg, model, test, gpu_iters, budget_s=15.0):
     """Oracle RBI-MGCG per parameter (single core) on a bounded sample."""
+    _single_thread_blas()
     from oracle import problems as op
     from oracle import solvers as so
     ospec = make_ospec(cfg)
@@ -337,7 +338,17 @@ def cpu_baseline(cfg, model, test, gpu_iters, budget_s=15.0):
 _W = {}
 
 
+def _single_thread_blas():
+    """One BLAS/OpenMP thread per process (the pool supplies the parallelism)."""
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:
+        pass
+
+
 def _ref_worker_init(cfg, model_state):
+    _single_thread_blas()
     from oracle import problems as op
     from oracle import solvers as so
     _W["oprob"] = op.OracleProblem(make_ospec(cfg), cfg["n"], cfg["m0"])
@@ -421,7 +432,7 @@ def main():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
-    ap.add_argument("--ref-per-core", type=int, default=1)
+    ap.add_argument("--ref-per-core", type=int, default=2)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         log("note: fewer than 3 warm-up steps requested")

@@ -286,3 +286,80 @@ def test_deim_known_answers():
     np.testing.assert_allclose(col[:3], [1 / 3, 1.0, 2 / 3])
     step2 = pkg.deim_extend(n, None, [], pkg.to_padded(v, n)[: pkg.padded_len(n, 1)], exclude={1})
     assert step2.index == 2
+
+
+# ------------------------------------------------------------- level kernels / full size
+
+@pytest.mark.parametrize("case,n,m0", [((2, 2, 1), 16, 4), ((2, 2, 2), 32, 4), ("smooth", 16, 4)])
+def test_level_kernels_every_mode(case, n, m0):
+    """apply / residual / Jacobi / pre-smoothing residual on every smoothed level."""
+    pkg = _pkg()
+    from paper_2311_13862_b200 import _native
+    prob, oprob, ospec = _pair(case, n, m0)
+    mus = op.sample_mus(ospec, 5, seed=13)
+    ctx = pkg.mg_context_for(prob, mus)
+    rng = np.random.default_rng(7)
+    for lvl in range(1, prob.levels):
+        nl = prob.cells[lvl]
+        x = rng.standard_normal((5, (nl - 1) ** 3))
+        r = rng.standard_normal((5, (nl - 1) ** 3))
+        xt, rt = pkg.to_padded(x, nl), pkg.to_padded(r, nl)
+        for mode in range(4):
+            ys = []
+            for _ in range(2):
+                y = torch.zeros_like(xt)
+                _native.call("rbws_level_kernel", ctx.handle, lvl, mode, xt.data_ptr(),
+                             rt.data_ptr(), y.data_ptr(), 0)
+                ys.append(y)
+            assert torch.equal(ys[0], ys[1]), "level kernel not deterministic"
+            g = pkg.from_padded(ys[0], nl, 5)
+            for m in range(5):
+                A = oprob.operator(mus[m], level=lvl)
+                d = A.diagonal()
+                ref = [A @ x[m], r[m] - A @ x[m], so.jacobi_sweep(A, d, x[m], r[m]),
+                       r[m] - A @ (0.7 * r[m] / d)][mode]
+                assert _rel(g[m], ref) <= 1e-13, (lvl, mode, m)
+
+
+def test_bench_config_properties_64():
+    """configs[1]-shaped problem: every instance converges to tol; oracle agrees on a sample."""
+    pkg = _pkg()
+    prob, oprob, ospec = _pair((2, 2, 1), 64, 4)
+    mus = op.sample_mus(ospec, 24, seed=2000)
+    ctx = pkg.mg_context_for(prob, mus)
+    x, reps = pkg.mgcg_solve(None, prob.rhs(), None, ctx, delta=1e-10, l_max=60)
+    assert all(r.converged and r.true_residual <= 1e-10 for r in reps)
+    got = pkg.from_padded(x, 64, len(mus))
+    for m in (0, 11):
+        A, f = oprob.operator(mus[m]), oprob.rhs()
+        xr, rr = so.mgcg_solve(A, f, np.zeros_like(f), so.mg_context_for(oprob, mus[m]),
+                               delta=1e-10, l_max=60)
+        assert abs(reps[m].iterations - rr.iterations) <= 1
+        assert _rel(got[m], xr) <= 1e-8
+    # the same batch solved twice is bitwise identical (deterministic reductions)
+    x2, _ = pkg.mgcg_solve(None, prob.rhs(), None, ctx, delta=1e-10, l_max=60)
+    assert torch.equal(x, x2)
+
+
+def test_l1roc_online_matches_oracle_with_device_model():
+    """GPU-trained model, GPU online stage vs the oracle's online stage on that model."""
+    pkg = _pkg()
+    prob, oprob, ospec = _pair((2, 2, 1), 32, 4)
+    train = op.sample_mus(ospec, 64, seed=5)
+    model = pkg.l1roc_offline(train, 8, pkg.HighFidelitySolver(prob), prob, seed=1)
+    omodel = so.OracleL1rocModel(model.basis_numpy(), model.transform, model.collocation,
+                                 model.solution_points, model.residual_points, model.chosen,
+                                 model.indicator_history, model.saturated)
+    test = op.sample_mus(ospec, 6, seed=6)
+    ctx = pkg.mg_context_for(prob, test)
+    u0, c = pkg.l1roc_online(model, pkg.BatchOperator(ctx), prob.rhs())
+    got = pkg.from_padded(u0, 32, len(test))
+    for m in range(len(test)):
+        ur, cr, _ = so.l1roc_online(omodel, oprob.operator(test[m]), oprob.rhs())
+        assert _rel(got[m], ur) <= 1e-9
+        np.testing.assert_allclose(c[m], cr, rtol=1e-7, atol=1e-12)
+    # prefix models (nested) agree with the oracle too
+    sub = model.prefix(4)
+    u4, _ = pkg.l1roc_online(sub, pkg.BatchOperator(ctx), prob.rhs())
+    ur4, _, _ = so.l1roc_online(omodel.prefix(4), oprob.operator(test[0]), oprob.rhs())
+    assert _rel(pkg.from_padded(u4, 32, len(test))[0], ur4) <= 1e-9
