@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(256) coarse_kernel(CoarseArgs a) {
 
   const int hi = (jl + 1) * n + i;
   const double om = a.omega;
+  double cdi = 0.0;
   if (NH > 0) {
     mbar_wait(&bar[0], 0u);
     mbar_wait(&bar[1], 0u);
@@ -173,7 +174,10 @@ __global__ void __launch_bounds__(256) coarse_kernel(CoarseArgs a) {
       if (k >= ke) break;
       const int idx = k + 1 - p_first;
       if (NH > 0) mbar_wait(&bar[idx & (S - 1)], (uint32_t)((idx / S) & 1));
-      if (k == kb || !zsame[k - p_first]) coeffs(k);
+      if (k == kb || !zsame[k - p_first]) {
+        coeffs(k);
+        cdi = om / c000;  // cached damping / diagonal (no per-node division)
+      }
       const int64_t gidx = base + (int64_t)k * n2 + (int64_t)j * n + i;
       if (MODE == CM_DINV) {
         if (on) a.y[gidx] = 1.0 / c000;
@@ -199,7 +203,7 @@ __global__ void __launch_bounds__(256) coarse_kernel(CoarseArgs a) {
           a.y[gidx] = bs((idx - 1) & (S - 1))[jl * n + i] - Au;
         } else {  // CM_JACOBI
           const double bv = bs((idx - 1) & (S - 1))[jl * n + i];
-          a.y[gidx] = X0[0] + om * (bv - Au) / c000;
+          a.y[gidx] = fma(cdi, bv - Au, X0[0]);
         }
       }
     }

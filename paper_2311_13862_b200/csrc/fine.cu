@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
   const double om = a.omega;
   double acc = 0.0;
   // cached face weights per owned row (recomputed only when the z factors change)
-  double wxp[NPT], wxm[NPT], wyp[NPT], wym[NPT], wzp[NPT], wzm[NPT], dg[NPT];
+  double wxp[NPT], wxm[NPT], wyp[NPT], wym[NPT], wzp[NPT], wzm[NPT], dg[NPT], wdi[NPT];
   auto weights = [&](int r, const double* zk, bool first_plane) {
     const int j = j0 + rl0 + r * rpp;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
@@ -196,9 +196,11 @@ __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
         if (fresh) {
           weights(r, zf + (k - p_first) * ZW, false);
           dg[r] = ((wxp[r] + wxm[r]) + (wyp[r] + wym[r])) + (wzp[r] + wzm[r]);
+          wdi[r] = om / dg[r];  // cached damping / diagonal (no per-node division)
         } else if (wzm[r] != wzp[r]) {
           wzm[r] = wzp[r];
           dg[r] = ((wxp[r] + wxm[r]) + (wyp[r] + wym[r])) + (wzp[r] + wzm[r]);
+          wdi[r] = om / dg[r];
         }
       }
       const int sm = (idx - 2) & (S - 1), s0 = (idx - 1) & (S - 1), sp = idx & (S - 1);
@@ -254,7 +256,7 @@ __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
           acc = on ? fma(rv, rv, acc) : acc;
         } else if (MODE == FM_JACOBI) {
           const double bv = cptr(s0, 0)[ci];
-          const double y = uc + om * (bv - Au) / d;
+          const double y = fma(wdi[r], bv - Au, uc);
           if (on) a.out0[gidx] = y;
           acc = on ? fma(bv, y, acc) : acc;
         } else if (MODE == FM_PRE) {
