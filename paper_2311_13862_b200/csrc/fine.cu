@@ -56,6 +56,7 @@ struct FineArgs {
   double* partial;
   const int* active;
   double omega;
+  int c0_shared;  // c0 is one instance shared by the whole batch (e.g. the rhs f)
 };
 
 enum FineMode : int {
@@ -139,7 +140,9 @@ __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
                &bar[st]);
 #pragma unroll
     for (int c = 0; c < NC; ++c)
-      bulk_g2s(cptr(st, c), csrc[c] + plane + (int64_t)j0 * n, cbytes, &bar[st]);
+      bulk_g2s(cptr(st, c),
+               csrc[c] + (c == 0 && a.c0_shared ? plane - base : plane) + (int64_t)j0 * n, cbytes,
+               &bar[st]);
   };
   if (tid == 0)
     for (int p = p_first; p <= p_last && p < p_first + S; ++p) issue(p);
@@ -349,6 +352,58 @@ static cudaError_t fine_launch(int mode, FineArgs& a, int batch, cudaStream_t st
   }
 }
 
+// 1/diag of the finest operator for every instance (batch setup); weights are
+// recomputed only on planes whose z factors change (host-built flags)
+template <int Q>
+__global__ void __launch_bounds__(256) fine_dinv_kernel(Sep7 op, FineGeom g, const int* zsame,
+                                                       double* __restrict__ dinv) {
+  const int n = op.n, n1 = n + 1;
+  const int kc = blockIdx.z % g.zc, mu = blockIdx.z / g.zc;
+  const int kz = n / g.zc;
+  const int kb = max(1, kc * kz), ke = min(n, (kc + 1) * kz);
+  const int i = threadIdx.x % n;
+  const int64_t n2 = (int64_t)n * n, base = (int64_t)mu * n2 * n;
+  const double* th = op.theta + (size_t)mu * Q;
+  for (int r = 0; r < g.npt; ++r) {
+    const int j = blockIdx.y * g.ty + threadIdx.x / n + r * g.rpp;
+    if (i == 0 || j == 0) continue;
+    double d = 0.0;
+    for (int k = kb; k < ke; ++k) {
+      if (k == kb || !zsame[k]) {
+        d = 0.0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const double* F = op.face + (size_t)q * 3 * n;
+          const double* N = op.node + (size_t)q * 9 * n1;
+          const double xy = N[(0 * 3 + 1) * n1 + j] * N[(0 * 3 + 2) * n1 + k];
+          const double yx = N[(1 * 3 + 0) * n1 + i] * N[(1 * 3 + 2) * n1 + k];
+          const double zz = N[(2 * 3 + 0) * n1 + i] * N[(2 * 3 + 1) * n1 + j];
+          const double s = (F[0 * n + i] + F[0 * n + i - 1]) * xy +
+                           (F[1 * n + j] + F[1 * n + j - 1]) * yx +
+                           (F[2 * n + k] + F[2 * n + k - 1]) * zz;
+          d = fma(th[q], s, d);
+        }
+      }
+      dinv[base + (int64_t)k * n2 + (int64_t)j * n + i] = 1.0 / d;
+    }
+  }
+}
+
+cudaError_t fine_dinv(const Sep7& op, int batch, const int* zsame, double* dinv,
+                      cudaStream_t stream) {
+  const FineGeom g = fine_geom(op.n, batch);
+  dim3 grd(1, g.ytiles, batch * g.zc);
+  count_launch();
+#define RBWS_DQ(QQ) \
+  case QQ: fine_dinv_kernel<QQ><<<grd, g.threads, 0, stream>>>(op, g, zsame, dinv); break;
+  switch (op.Q) {
+    RBWS_DQ(1) RBWS_DQ(2) RBWS_DQ(3) RBWS_DQ(4) RBWS_DQ(5) RBWS_DQ(6) RBWS_DQ(7) RBWS_DQ(8)
+    default: return cudaErrorInvalidValue;
+  }
+#undef RBWS_DQ
+  return cudaGetLastError();
+}
+
 static FineArgs base_args(const Sep7& op, int dot, double* partial, const LaunchCtx& lc,
                           double omega) {
   FineArgs a{};
@@ -369,10 +424,11 @@ cudaError_t fine_apply(const Sep7& op, int batch, const double* x, double* y, do
 }
 
 cudaError_t fine_resid(const Sep7& op, int batch, const double* x, const double* b, double* r,
-                       double* partial, const LaunchCtx& lc) {
+                       double* partial, const LaunchCtx& lc, bool b_shared) {
   FineArgs a = base_args(op, partial ? DOT_YY : DOT_NONE, partial, lc, 0.0);
   a.h0 = x;
   a.c0 = b;
+  a.c0_shared = b_shared ? 1 : 0;
   a.out0 = r;
   return fine_launch(FM_RESID, a, batch, lc.stream);
 }

@@ -19,9 +19,12 @@ FineGeom fine_geom(int n, int batch);
 // y = A x (y may be null), partial (may be null) = x . A x
 cudaError_t fine_apply(const Sep7& op, int batch, const double* x, double* y, double* partial,
                        const LaunchCtx& lc);
-// r = b - A x, partial = |r|^2
+// r = b - A x, partial = |r|^2 (b_shared: b is one instance used by every instance)
 cudaError_t fine_resid(const Sep7& op, int batch, const double* x, const double* b, double* r,
-                       double* partial, const LaunchCtx& lc);
+                       double* partial, const LaunchCtx& lc, bool b_shared = false);
+// dinv = 1/diag(A(mu)) (batch setup); zsame: per-plane "z factors unchanged" flags
+cudaError_t fine_dinv(const Sep7& op, int batch, const int* zsame, double* dinv,
+                      cudaStream_t stream);
 // y = x + omega (b - A x)/diag, partial (may be null) = b . y
 cudaError_t fine_jacobi(const Sep7& op, int batch, const double* x, const double* b, double* y,
                         double omega, double* partial, const LaunchCtx& lc);

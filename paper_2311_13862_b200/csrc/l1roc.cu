@@ -161,43 +161,67 @@ cudaError_t l1roc_online(int count, int Q, int M, int N, const double* theta, co
 }
 
 // ---------------------------------------------------------------- expansion
-// x[mu] = W a[mu]; a block holds a 256-node tile of W in smem and sweeps a
-// chunk of instances, so W is read count/kChunk times in total.
-constexpr int kExpandChunk = 128;
+// x[mu] = W a[mu].  A thread holds its node's N basis values in registers
+// (NB >= N, zero padded) and sweeps a chunk of instances whose coefficient
+// vectors sit in shared memory (broadcast reads), so W is read once per chunk
+// and each output costs N FMAs + N/2 128-bit shared loads.
+template <int NB>
+struct ExpandChunk {
+  static constexpr int value = NB <= 16 ? 256 : (NB <= 32 ? 128 : 64);  // <= 32 KB of smem
+};
 
+template <int NB>
 __global__ void __launch_bounds__(256) expand_kernel(int64_t n3, const double* __restrict__ W,
                                                      int64_t Wstride, int N,
                                                      const double* __restrict__ a, int count,
                                                      double* __restrict__ x) {
-  extern __shared__ double wt[];  // [N][256]
-  const int64_t X = (int64_t)blockIdx.x * 256 + threadIdx.x;
-  for (int c = 0; c < N; ++c) wt[c * 256 + threadIdx.x] = (X < n3) ? W[c * Wstride + X] : 0.0;
-  __syncthreads();
-  if (X >= n3) return;
+  constexpr int kExpandChunk = ExpandChunk<NB>::value;
+  __shared__ __align__(16) double as[kExpandChunk * NB];
   const int m0 = blockIdx.y * kExpandChunk;
   const int m1 = min(count, m0 + kExpandChunk);
-  for (int mu = m0; mu < m1; ++mu) {
-    const double* am = a + (int64_t)mu * N;
-    double s = 0.0;
-    for (int c = 0; c < N; ++c) s = fma(wt[c * 256 + threadIdx.x], __ldg(am + c), s);
-    x[(int64_t)mu * n3 + X] = s;
+  for (int t = threadIdx.x; t < kExpandChunk * NB; t += blockDim.x) {
+    const int mu = m0 + t / NB, c = t % NB;
+    as[t] = (mu < m1 && c < N) ? a[(int64_t)mu * N + c] : 0.0;
   }
+  __syncthreads();
+  const int64_t X = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (X >= n3) return;
+  double w[NB];
+#pragma unroll
+  for (int c = 0; c < NB; ++c) w[c] = (c < N) ? __ldg(W + c * Wstride + X) : 0.0;
+  for (int mu = m0; mu < m1; ++mu) {
+    const double2* am = reinterpret_cast<const double2*>(as + (mu - m0) * NB);
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int c = 0; c < NB / 2; ++c) {
+      const double2 v = am[c];
+      s0 = fma(w[2 * c], v.x, s0);
+      s1 = fma(w[2 * c + 1], v.y, s1);
+    }
+    x[(int64_t)mu * n3 + X] = s0 + s1;
+  }
+}
+
+template <int NB>
+static cudaError_t expand_nb(int64_t n3, int count, const double* W, int64_t Wstride, int N,
+                            const double* a, double* x, cudaStream_t stream) {
+  constexpr int ch = ExpandChunk<NB>::value;
+  dim3 grd((unsigned)((n3 + 255) / 256), (count + ch - 1) / ch);
+  count_launch();
+  expand_kernel<NB><<<grd, 256, 0, stream>>>(n3, W, Wstride, N, a, count, x);
+  return cudaGetLastError();
 }
 
 cudaError_t expand(int n, int count, const double* W, int64_t Wstride, int N, const double* a,
                    double* x, cudaStream_t stream) {
   const int64_t n3 = (int64_t)n * n * n;
-  const size_t smem = sizeof(double) * 256 * (size_t)N;
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(expand_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  dim3 grd((unsigned)((n3 + 255) / 256), (count + kExpandChunk - 1) / kExpandChunk);
-  count_launch();
-  expand_kernel<<<grd, 256, smem, stream>>>(n3, W, Wstride, N, a, count, x);
-  return cudaGetLastError();
+  if (N <= 8) return expand_nb<8>(n3, count, W, Wstride, N, a, x, stream);
+  if (N <= 16) return expand_nb<16>(n3, count, W, Wstride, N, a, x, stream);
+  if (N <= 24) return expand_nb<24>(n3, count, W, Wstride, N, a, x, stream);
+  if (N <= 32) return expand_nb<32>(n3, count, W, Wstride, N, a, x, stream);
+  if (N <= 48) return expand_nb<48>(n3, count, W, Wstride, N, a, x, stream);
+  if (N <= 64) return expand_nb<64>(n3, count, W, Wstride, N, a, x, stream);
+  return cudaErrorInvalidValue;
 }
 
 // ---------------------------------------------------------------- DEIM step

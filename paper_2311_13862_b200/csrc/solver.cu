@@ -46,6 +46,7 @@ Hierarchy::~Hierarchy() {
   cudaFree(d_node);
   for (double* p : d_fac) cudaFree(p);
   for (int* p : d_zsame) cudaFree(p);
+  cudaFree(d_fzsame);
 }
 
 // 1D Galerkin product P^T T P of a tridiagonal interior operator
@@ -136,6 +137,25 @@ int hierarchy_create(Hierarchy** out, int n, int m0, int Q, const double* face,
   if (e == cudaSuccess) e = dalloc(&h->d_node, (size_t)Q * 9 * (n + 1));
   if (e == cudaSuccess) e = cudaMemcpy(h->d_face, face, sizeof(double) * Q * 3 * n, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(h->d_node, node, sizeof(double) * Q * 9 * (n + 1), cudaMemcpyHostToDevice);
+  {  // finest level: plane k's z factors (x/y node factors, z faces k-1, k) equal plane k-1's?
+    const int n1 = n + 1;
+    std::vector<int> fz(n + 1, 0);
+    for (int k = 2; k <= n - 1; ++k) {
+      int same = 1;
+      for (int q = 0; q < Q && same; ++q) {
+        const double* F = face + (size_t)q * 3 * n;
+        const double* N = node + (size_t)q * 9 * n1;
+        same &= N[(0 * 3 + 2) * n1 + k] == N[(0 * 3 + 2) * n1 + k - 1];
+        same &= N[(1 * 3 + 2) * n1 + k] == N[(1 * 3 + 2) * n1 + k - 1];
+        same &= F[2 * n + k] == F[2 * n + k - 1];
+        same &= F[2 * n + k - 1] == F[2 * n + k - 2];
+      }
+      fz[k] = same;
+    }
+    if (e == cudaSuccess) e = dalloc(&h->d_fzsame, fz.size());
+    if (e == cudaSuccess)
+      e = cudaMemcpy(h->d_fzsame, fz.data(), sizeof(int) * fz.size(), cudaMemcpyHostToDevice);
+  }
   h->d_fac.assign(L, nullptr);
   h->d_zsame.assign(L, nullptr);
   for (int l = 0; l < L && e == cudaSuccess; ++l) {
@@ -262,8 +282,7 @@ int batch_setup(Batch* b, const double* theta, int count, cudaStream_t stream) {
   const int L = h->levels;
   LaunchCtx lc{stream, nullptr};
   // fine level 1/diag
-  e = sep7_launch(b->fine_op(), count, MODE_DINV, DOT_NONE, nullptr, nullptr, nullptr,
-                  b->lv[L - 1].dinv, nullptr, b->omega, lc);
+  e = fine_dinv(b->fine_op(), count, h->d_fzsame, b->lv[L - 1].dinv, stream);
   // coarse levels are matrix-free (Kronecker factors): only 1/diag is stored
   for (int l = 1; l < L - 1 && e == cudaSuccess; ++l)
     e = coarse_launch(4, h->cells[l], h->Q, h->d_fac[l], h->d_zsame[l], b->theta, count,
@@ -518,13 +537,8 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
   const int ftiles = vec_tiles(n);
   // ||f||
   e = vec_dot(n, fshared ? 1 : count, f, f_stride, f, f_stride, b->partial2, all);
-  // r = f - A x0, ||r||^2  (a shared rhs is broadcast into s first)
-  const double* fb = f;
-  if (e == cudaSuccess && fshared) {
-    e = vec_copy(n, count, f, 0, b->s, all);
-    fb = b->s;
-  }
-  if (e == cudaSuccess) e = fine_resid(op, count, x, fb, b->r, b->partial, all);
+  // r = f - A x0, ||r||^2  (a shared rhs is staged once per plane for every instance)
+  if (e == cudaSuccess) e = fine_resid(op, count, x, f, b->r, b->partial, all, fshared);
   if (e == cudaSuccess) e = cudaMemsetAsync(b->nactive, 0, sizeof(int), stream);
   if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
   count_launch();
@@ -581,8 +595,7 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
     }
   }
   // true residual ||f - A x|| / scale for every instance
-  if (fshared) e = vec_copy(n, count, f, 0, b->s, all);
-  if (e == cudaSuccess) e = fine_resid(op, count, x, fb, b->t_res, b->partial, all);
+  if (e == cudaSuccess) e = fine_resid(op, count, x, f, b->t_res, b->partial, all, fshared);
   if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
   double* d_true = b->beta;  // reuse as scratch
   count_launch();

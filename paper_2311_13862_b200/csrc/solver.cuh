@@ -18,6 +18,7 @@ struct Hierarchy {
   double* d_node = nullptr;
   std::vector<double*> d_fac;       // per level 1D Kronecker factors [Q*3][3][2][n+1]
   std::vector<int*> d_zsame;        // per level [n+1]: z factors of plane k == plane k-1
+  int* d_fzsame = nullptr;          // finest level [n+1]: same flags for the separable tables
   std::vector<std::vector<double>> h_fac;
 
   ~Hierarchy();
