@@ -44,7 +44,8 @@ CONFIGS = {
     2: dict(workload="thermal-block 2x2x2, 128^3 cells, r=30 from 4096 train, batch 512, tol 1e-12",
             kind="tb", blocks=(2, 2, 2), n=128, m0=4, r=30, n_train=4096, batch=512, delta=1e-12),
     3: dict(workload="smooth affine (6 modes), 256^3 cells, r=40 from 2048 train, batch 128, tol 1e-12",
-            kind="smooth", blocks=None, n=256, m0=4, r=40, n_train=2048, batch=128, delta=1e-12),
+            kind="smooth", blocks=None, n=256, m0=4, r=40, n_train=2048, batch=128, delta=1e-12,
+            chunk=64),
 }
 L_MAX = 60
 
@@ -158,22 +159,28 @@ def run_b200(args, rank, world, dist):
 
     t0 = time.perf_counter()
     hf = rb.HighFidelitySolver(prob, delta=1e-14, l_max=100)
-    model = rb.l1roc_offline(train, cfg["r"], hf, prob, seed=0)
+    model = rb.l1roc_offline(train, cfg["r"], hf, prob, seed=0, on_degenerate="stop")
     torch.cuda.synchronize()
     t_off = time.perf_counter() - t0
     log(f"[rank {rank}] offline greedy: N={model.dim} saturated={model.saturated} "
         f"in {t_off:.2f}s")
 
-    ctx = rb.MgContext(prob, batch)
+    # instances per device-resident sub-batch (bounded by HBM for the largest grids)
+    chunk = min(batch, args.chunk or cfg.get("chunk", batch))
+    chunks = [test[c:c + chunk] for c in range(0, batch, chunk)]
+    ctx = rb.MgContext(prob, chunk)
     f = prob.rhs()
     method = rb.MethodConfig("rbi-mgcg", delta=delta, l_max=L_MAX, N=model.dim)
-    xbuf = torch.empty(rb.padded_len(n, batch), dtype=torch.float64, device="cuda")
+    xbuf = torch.empty(rb.padded_len(n, chunk), dtype=torch.float64, device="cuda")
     state = {}
 
     def step():
-        rb.mg_context_for(prob, test, ctx=ctx)
-        x, reps = rb.rbi_pcg_solve(rb.BatchOperator(ctx), f, method, mg_ctx=ctx,
-                                   l1roc_model=model, x0_out=xbuf)
+        reps = []
+        for part in chunks:
+            rb.mg_context_for(prob, part, ctx=ctx)
+            x, r = rb.rbi_pcg_solve(rb.BatchOperator(ctx), f, method, mg_ctx=ctx,
+                                    l1roc_model=model, x0_out=xbuf)
+            reps += r
         state["reps"], state["x"] = reps, x
         return x
 
@@ -181,7 +188,7 @@ def run_b200(args, rank, world, dist):
         step()
     torch.cuda.synchronize()
     # zero-initialised MGCG on the same batch for reference (outside the timed region)
-    _, zreps = rb.mgcg_solve(None, f, None, ctx, delta=delta, l_max=L_MAX)
+    _, zreps = rb.mgcg_solve(None, f, None, ctx, delta=delta, l_max=L_MAX)  # last sub-batch
     zero_iters = float(np.mean([r.iterations for r in zreps]))
 
     # ---- timed region (device-resident inputs)
@@ -229,10 +236,11 @@ def run_b200(args, rank, world, dist):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        rb.mg_context_for(prob, mus_host, ctx=ctx)  # theta(mu) host -> device
-        x, reps_e = rb.rbi_pcg_solve(rb.BatchOperator(ctx), f, method, mg_ctx=ctx,
-                                     l1roc_model=model, x0_out=xbuf)
-        hbuf.copy_(x, non_blocking=True)          # solutions device -> host
+        for c0 in range(0, batch, chunk):
+            rb.mg_context_for(prob, mus_host[c0:c0 + chunk], ctx=ctx)  # theta(mu) host -> device
+            x, reps_e = rb.rbi_pcg_solve(rb.BatchOperator(ctx), f, method, mg_ctx=ctx,
+                                         l1roc_model=model, x0_out=xbuf)
+            hbuf.copy_(x, non_blocking=True)      # solutions device -> host
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
@@ -240,7 +248,7 @@ def run_b200(args, rank, world, dist):
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_value = world * batch * args.steps / (float(e2e_ms.item()) / 1e3)
     h2d = batch * spec.n_terms * 8
-    d2h = xbuf.numel() * 8 + batch * (L_MAX + 1) * 8 + batch * (4 + 8 + 4)
+    d2h = len(chunks) * xbuf.numel() * 8 + batch * (L_MAX + 1) * 8 + batch * (4 + 8 + 4)
 
     # ---- roofline of the dominant fine-level kernel class
     peak, peak_kind = peaks()
@@ -281,7 +289,8 @@ def run_b200(args, rank, world, dist):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded log-uniform parameters; no dataset)",
-        "config": {"workload": cfg["workload"], "batch_per_gpu": batch, "grid_cells": n,
+        "config": {"workload": cfg["workload"], "batch_per_gpu": batch, "sub_batch": chunk,
+                   "grid_cells": n,
                    "levels": levels, "rb_dim": model.dim, "n_train": cfg["n_train"],
                    "tolerance": delta, "smoother": "jacobi(0.7), nu=1",
                    "parallelism": f"parameter-sharded x{world}",
@@ -384,7 +393,7 @@ def run_reference(args, rank, world):
 
     t0 = time.perf_counter()
     model = so.l1roc_offline(list(train), cfg["r"], hf, oprob.operator, oprob.operator_rows,
-                             oprob.rhs, seed=0)
+                             oprob.rhs, seed=0, on_degenerate="stop")
     t_off = time.perf_counter() - t0
     log(f"[reference] offline greedy N={model.dim} in {t_off:.1f}s")
     state = (model.basis, model.transform, model.collocation, model.solution_points,
@@ -430,6 +439,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--chunk", type=int, default=0, help="instances per device sub-batch")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-per-core", type=int, default=2)

@@ -242,8 +242,12 @@ def l1roc_online(model: OracleL1rocModel, A, b):
     return model.basis @ a, sla.solve_triangular(model.transform, a, lower=False), a
 
 
-def l1roc_offline(mus, N, hf_solve, operator, operator_rows, rhs, seed=0):
-    """Greedy over-collocation training (rb.py:208-293)."""
+def l1roc_offline(mus, N, hf_solve, operator, operator_rows, rhs, seed=0, on_degenerate="raise"):
+    """Greedy over-collocation training (rb.py:208-293).
+
+    on_degenerate="stop" ends the greedy (flagged saturated) instead of raising
+    when a picked snapshot is numerically inside the basis (bench harness only).
+    """
     mus = [np.asarray(m, dtype=np.float64) for m in mus]
     if not 1 <= N <= len(mus):
         raise ValueError("need 1 <= N <= number of training parameters")
@@ -273,7 +277,14 @@ def l1roc_offline(mus, N, hf_solve, operator, operator_rows, rhs, seed=0):
             saturated = True
             break
         chosen.append(pick)
-        col, idx, c, piv = deim_extend(W, xs, hf_solve(mus[pick]), exclude=taken)
+        try:
+            col, idx, c, piv = deim_extend(W, xs, hf_solve(mus[pick]), exclude=taken)
+        except DegenerateBasisError:
+            if on_degenerate != "stop":
+                raise
+            chosen.pop()
+            saturated = True
+            break
         taken.add(idx)
         T = np.block([[T, c[:, None]], [np.zeros((1, T.shape[1])), np.array([[piv]])]])
         W = np.column_stack([W, col])

@@ -201,8 +201,12 @@ def deim_extend(n: int, W, X, v, exclude=None) -> DeimStep:
 # ----------------------------------------------------------------- offline
 
 def l1roc_offline(mus, N: int, hf_solve, problem: ParametricProblem, seed: int = 0,
-                  progress=None) -> L1rocModel:
+                  progress=None, on_degenerate: str = "raise") -> L1rocModel:
     """Greedy offline training (rb.py:208-293) with device-side data work.
+
+    on_degenerate: "raise" (reference behaviour, rb.py:116-117) or "stop" — end
+    the greedy with the basis built so far (flagged as saturated) when a picked
+    snapshot lies numerically inside the current basis.
 
     hf_solve(mu) -> padded device solution (e.g. hf.HighFidelitySolver).
     """
@@ -246,7 +250,14 @@ def l1roc_offline(mus, N: int, hf_solve, problem: ParametricProblem, seed: int =
         chosen.append(pick)
         u = hf_solve(mus[pick])
         m = nn - 1  # current basis width
-        step = deim_extend(n, W, xs, u, exclude=taken)
+        try:
+            step = deim_extend(n, W, xs, u, exclude=taken)
+        except DegenerateBasisError:
+            if on_degenerate != "stop":
+                raise
+            chosen.pop()
+            saturated = True
+            break
         taken.add(step.index)
         T = np.block([[T, step.coeffs[:, None]], [np.zeros((1, m)), np.array([[step.pivot]])]])
         W[m * n3:(m + 1) * n3] = step.column[:n3]
