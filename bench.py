@@ -136,6 +136,21 @@ def make_ospec(cfg):
 
 # ---------------------------------------------------------------- b200 arm
 
+def _traffic(kernel, bytes_per_launch, cfg):
+    """DRAM bytes per launch for the dominant kernel from the committed ncu capture
+    (profiles/r01_traffic.json, configs[1]); scaled to this run's average launch by the
+    captured traffic/algorithmic ratio. None for workloads that were not captured."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
+    if cfg["workload"] != CONFIGS[1]["workload"] or not os.path.exists(path):
+        return None, None
+    with open(path) as fh:
+        cap = json.load(fh)
+    if kernel not in cap:
+        return None, None
+    ratio = cap[kernel]["dram_bytes"] / cap[kernel]["algorithmic_bytes"]
+    return int(ratio * bytes_per_launch), f"{cap['source']}; dram/algorithmic = {ratio:.3f}"
+
+
 def run_b200(args, rank, world, dist):
     import torch
 
@@ -200,11 +215,13 @@ def run_b200(args, rank, world, dist):
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device()) as clocks:
+        torch.cuda.nvtx.range_push("rbws_timed")   # ncu --nvtx-include rbws_timed/
         ev0.record(stream)
         for _ in range(args.steps):
             step()
         ev1.record(stream)
         torch.cuda.synchronize()
+        torch.cuda.nvtx.range_pop()
     launches = _native.launch_count() - lc0
     ms = ev0.elapsed_time(ev1)
     NC = len(CLASS_NAMES)
@@ -270,9 +287,10 @@ def run_b200(args, rank, world, dist):
         dom_bytes = CLASS_BYTES[dom] * nodes * punits[dom] / pcalls[dom]
         dom_s = pms[dom] / pcalls[dom] / 1e3
         achieved = dom_bytes / dom_s / 1e9
+        traffic, tsrc = _traffic(CLASS_NAMES[dom], dom_bytes, cfg)
         roofline = {"bound": "hbm", "kernel": CLASS_NAMES[dom], "achieved": round(achieved, 1),
                     "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                    "traffic": None, "peak_source": peak_kind,
+                    "traffic": traffic, "traffic_source": tsrc, "peak_source": peak_kind,
                     "bytes_per_launch": int(dom_bytes),
                     "bytes_per_node": CLASS_BYTES[dom]}
     else:  # the warm start already met the tolerance: no PCG iteration ran

@@ -1,0 +1,16 @@
+# Round-1 profiling recipe: plain run, launch list of the timed region, full captures.
+# Reports stay in /tmp on the box; only CSV exports (and the small fine report) come back.
+mkdir -p gpurun_out
+CMD="python bench.py --steps 1 --warmup 3 --no-cpu"
+$CMD > gpurun_out/plain.log 2>&1 || { echo plain failed; tail -5 gpurun_out/plain.log; exit 1; }
+tail -1 gpurun_out/plain.log | head -c 300; echo
+NV='--nvtx --nvtx-include rbws_timed/'
+timeout 900 ncu $NV --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r01_launches.csv $CMD > gpurun_out/ncu_list.log 2>&1; echo list=$?
+timeout 900 ncu $NV --set full --clock-control none --import-source on -k regex:fine_kernel -c 8 -o /tmp/r01_fine $CMD > gpurun_out/ncu_fine.log 2>&1; echo fine=$?
+timeout 900 ncu $NV --set full --clock-control none -k regex:"coarse_kernel|restrict|prolong" -c 10 -o /tmp/r01_other $CMD > gpurun_out/ncu_other.log 2>&1; echo other=$?
+for r in r01_fine r01_other; do
+  ncu -i /tmp/$r.ncu-rep --page raw --csv > gpurun_out/${r}_raw.csv 2>/dev/null
+  ncu -i /tmp/$r.ncu-rep --page details --csv > gpurun_out/${r}_details.csv 2>/dev/null
+done
+ncu -i /tmp/r01_fine.ncu-rep --page source --csv > gpurun_out/r01_fine_source.csv 2>/dev/null
+ls -la /tmp/*.ncu-rep gpurun_out/
