@@ -25,6 +25,20 @@ constexpr int kStages = 8;  // ring slots (power of two)
 constexpr int kMaxKz = 64;  // planes per z-chunk (bounds the z-factor table)
 constexpr int kThreads = 256;  // threads per CTA (one per grid column of the tile)
 
+// Compile-time tile geometry for a grid with N cells per axis: RPP rows per pass
+// of the CTA, NPT rows per thread, TY = RPP*NPT rows per tile.  All shared-memory
+// and global offsets below are compile-time multiples of N, so a neighbour read
+// is one LDS with an immediate offset from a per-plane base register.
+template <int N>
+struct FT {
+  static constexpr int RPP = (kThreads / N) < N ? kThreads / N : N;
+  static constexpr int NPT = (RPP * 2 <= N) ? 2 : 1;
+  static constexpr int TY = RPP * NPT;
+  static constexpr int THREADS = RPP * N;
+  static constexpr int HSZ = (TY + 2) * N;  // doubles per staged array with halo rows
+  static constexpr int CSZ = TY * N;        // doubles per staged array, tile rows only
+};
+
 FineGeom fine_geom(int n, int batch) {
   FineGeom g;
   int rpp = kThreads / n;
@@ -70,26 +84,46 @@ enum FineMode : int {
 
 template <int MODE>
 struct SL {
-  static constexpr int NH = (MODE == FM_PRE || MODE == FM_PAPPLY) ? 2 : 1;
+  // PRE / PAPPLY stencil a derived vector (w dinv b, s + beta p_old): each staged
+  // plane is transformed once into a second ring, so neighbours cost one LDS
+  static constexpr bool XF = (MODE == FM_PRE || MODE == FM_PAPPLY);
+  static constexpr int NH = XF ? 2 : 1;
   static constexpr int NC = (MODE == FM_CG) ? 2 : ((MODE == FM_RESID || MODE == FM_JACOBI) ? 1 : 0);
+  static constexpr int S = XF ? 6 : kStages;  // raw ring slots
+  static constexpr int U = 6;                 // transformed-plane ring slots (XF)
 };
 
-template <int Q, int MODE, int NPT>
+template <int N, int MODE>
+struct FSmem {
+  static constexpr int STAGE = SL<MODE>::NH * FT<N>::HSZ + SL<MODE>::NC * FT<N>::CSZ;
+  static constexpr int RING = SL<MODE>::S * STAGE + (SL<MODE>::XF ? SL<MODE>::U * FT<N>::HSZ : 0);
+  static size_t bytes(int np, int Q) {
+    return 64 + 4 * (kMaxKz + 4) + 8 * (((size_t)np * 3 * Q + 1) & ~(size_t)1) + 8 * (size_t)RING;
+  }
+};
+
+template <int MODE, int N>
 __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
-  constexpr int NH = SL<MODE>::NH, NC = SL<MODE>::NC, S = kStages, ZW = 3 * Q;
+  using G = FT<N>;
+  using L = SL<MODE>;
+  constexpr bool XF = L::XF;
+  constexpr int NH = L::NH, NC = L::NC, S = L::S, U = L::U;
+  constexpr int NPT = G::NPT, RPP = G::RPP, TY = G::TY;
+  constexpr int HSZ = G::HSZ, CSZ = G::CSZ;
+  constexpr int STAGE = FSmem<N, MODE>::STAGE;  // doubles per raw ring slot
+  constexpr int64_t N2 = (int64_t)N * N;
   extern __shared__ __align__(128) unsigned char smem[];
   const Sep7& op = a.op;
-  const int n = op.n, n1 = n + 1;
-  const int ty = a.g.ty, zc = a.g.zc;
+  const int Q = op.Q, ZW = 3 * Q;
+  const int zc = a.g.zc;
   const int kc = blockIdx.z % zc, mu = blockIdx.z / zc;
   if (a.active && !a.active[mu]) return;
   const int yt = blockIdx.y;
-  const int j0 = yt * ty;
-  const int tid = threadIdx.x, nthr = blockDim.x;
-  const int64_t n2 = (int64_t)n * n;
-  const int64_t base = (int64_t)mu * n2 * n;
-  const int kz = n / zc;
-  const int kb = max(1, kc * kz), ke = min(n, (kc + 1) * kz);
+  const int j0 = yt * TY;
+  const int tid = threadIdx.x;
+  const int64_t base = (int64_t)mu * N2 * N;
+  const int kz = N / zc;
+  const int kb = max(1, kc * kz), ke = min(N, (kc + 1) * kz);
   const int p_first = kb - 1, p_last = ke;  // staged planes (inclusive)
   const int np = p_last - p_first + 1;
 
@@ -97,20 +131,17 @@ __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);            // [S]
   int* zsame = reinterpret_cast<int*>(smem + 64);                // [kMaxKz + 2]
   double* zf = reinterpret_cast<double*>(smem + 64 + 4 * (kMaxKz + 4));  // [np][3Q]
-  double* ring = zf + ((np * ZW + 1) & ~1);
-  const int hsz = (ty + 2) * n, csz = ty * n;
-  const int stage_d = NH * hsz + NC * csz;
-  auto hptr = [&](int st, int arr) { return ring + st * stage_d + arr * hsz; };
-  auto cptr = [&](int st, int arr) { return ring + st * stage_d + NH * hsz + arr * csz; };
+  double* ring = zf + ((np * ZW + 1) & ~1);                      // [S][STAGE]
+  double* uring = ring + S * STAGE;                              // [U][HSZ] (XF)
 
-  for (int t = tid; t < np * ZW; t += nthr) {  // z factors of the staged planes
+  for (int t = tid; t < np * ZW; t += G::THREADS) {  // z factors of the staged planes
     const int p = t / ZW, f = (t / Q) % 3, q = t % Q, k = p_first + p;
-    const double* F = op.face + (size_t)q * 3 * n;
-    const double* N = op.node + (size_t)q * 9 * n1;
+    const double* F = op.face + (size_t)q * 3 * N;
+    const double* NF = op.node + (size_t)q * 9 * (N + 1);
     double v;
-    if (f == 0) v = N[(0 * 3 + 2) * n1 + k];       // x-part along z
-    else if (f == 1) v = N[(1 * 3 + 2) * n1 + k];  // y-part along z
-    else v = (k < n) ? F[2 * n + k] : 0.0;         // z-face k, k+1
+    if (f == 0) v = NF[(0 * 3 + 2) * (N + 1) + k];       // x-part along z
+    else if (f == 1) v = NF[(1 * 3 + 2) * (N + 1) + k];  // y-part along z
+    else v = (k < N) ? F[2 * N + k] : 0.0;               // z-face k, k+1
     zf[t] = v;
   }
   if (tid == 0) {
@@ -119,38 +150,45 @@ __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
     mbar_fence_init();
   }
   __syncthreads();
-  for (int p = 1 + tid; p < np; p += nthr) {  // plane p repeats plane p-1's z factors?
+  for (int p = 1 + tid; p < np; p += G::THREADS) {  // plane p repeats plane p-1's z factors?
     int same = 1;
     for (int t = 0; t < ZW; ++t) same &= (zf[p * ZW + t] == zf[(p - 1) * ZW + t]);
     zsame[p] = same;
   }
 
-  const double* hsrc[2] = {a.h0, a.h1};
-  const double* csrc[2] = {a.c0, a.c1};
+  const int skip = (j0 == 0) ? 1 : 0;  // row j0-1 does not exist for the first tile
   auto issue = [&](int p) {
-    const int st = (p - p_first) & (S - 1);
-    const int skip = (j0 == 0) ? 1 : 0;
-    const uint32_t hbytes = (uint32_t)((ty + 2 - skip) * n * 8);
-    const uint32_t cbytes = (uint32_t)(ty * n * 8);
-    mbar_arrive_expect_tx(&bar[st], NH * hbytes + NC * cbytes);
-    const int64_t plane = base + (int64_t)p * n2;
-#pragma unroll
-    for (int h = 0; h < NH; ++h)
-      bulk_g2s(hptr(st, h) + skip * n, hsrc[h] + plane + (int64_t)(j0 - 1 + skip) * n, hbytes,
-               &bar[st]);
-#pragma unroll
-    for (int c = 0; c < NC; ++c)
-      bulk_g2s(cptr(st, c),
-               csrc[c] + (c == 0 && a.c0_shared ? plane - base : plane) + (int64_t)j0 * n, cbytes,
-               &bar[st]);
+    const int sl = (p - p_first) % S;
+    double* st = ring + sl * STAGE;
+    const uint32_t hbytes = (uint32_t)((TY + 2 - skip) * N * 8);
+    constexpr uint32_t cbytes = (uint32_t)(CSZ * 8);
+    mbar_arrive_expect_tx(&bar[sl], NH * hbytes + NC * cbytes);
+    const int64_t plane = base + (int64_t)p * N2;
+    const int64_t hrow = plane + (int64_t)(j0 - 1 + skip) * N;
+    bulk_g2s(st + skip * N, a.h0 + hrow, hbytes, &bar[sl]);
+    if (NH > 1) bulk_g2s(st + HSZ + skip * N, a.h1 + hrow, hbytes, &bar[sl]);
+    if (NC > 0)
+      bulk_g2s(st + NH * HSZ, a.c0 + (a.c0_shared ? plane - base : plane) + (int64_t)j0 * N,
+               cbytes, &bar[sl]);
+    if (NC > 1) bulk_g2s(st + NH * HSZ + CSZ, a.c1 + plane + (int64_t)j0 * N, cbytes, &bar[sl]);
   };
+  auto wait = [&](int p) {
+    const int t = p - p_first;
+    mbar_wait(&bar[t % S], (uint32_t)((t / S) & 1));
+  };
+  auto raw = [&](int p) -> const double* { return ring + ((p - p_first) % S) * STAGE; };
   if (tid == 0)
     for (int p = p_first; p <= p_last && p < p_first + S; ++p) issue(p);
 
-  // ---- this thread's column i and rows j = j0 + rl0 + r*rpp
-  const int i = tid % n;
-  const int rl0 = tid / n;
-  const int rpp = a.g.rpp;
+  // ---- this thread's column i and rows j = j0 + rl0 + r*RPP
+  const int i = tid % N;
+  const int rl0 = tid / N;
+  const int hoff = (rl0 + 1) * N + i;  // thread's centre in a halo-staged array
+  const int coff = rl0 * N + i;        // ... in a tile-only array
+  const int64_t goff = base + (int64_t)(j0 + rl0) * N + i;
+  bool on[NPT];
+#pragma unroll
+  for (int r = 0; r < NPT; ++r) on[r] = (i != 0) && (j0 + rl0 + r * RPP != 0);  // Dirichlet ghosts
   const double* th = op.theta + (size_t)mu * Q;
   const double sc = a.scal ? a.scal[mu] : 0.0;
   const double om = a.omega;
@@ -158,21 +196,21 @@ __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
   // cached face weights per owned row (recomputed only when the z factors change)
   double wxp[NPT], wxm[NPT], wyp[NPT], wym[NPT], wzp[NPT], wzm[NPT], dg[NPT], wdi[NPT];
   auto weights = [&](int r, const double* zk, bool first_plane) {
-    const int j = j0 + rl0 + r * rpp;
+    const int j = j0 + rl0 + r * RPP;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
     if (i >= 1 && j >= 1) {
-#pragma unroll
+#pragma unroll 2
       for (int q = 0; q < Q; ++q) {
-        const double* F = op.face + (size_t)q * 3 * n;
-        const double* N = op.node + (size_t)q * 9 * n1;
+        const double* F = op.face + (size_t)q * 3 * N;
+        const double* NF = op.node + (size_t)q * 9 * (N + 1);
         const double t = th[q];
-        const double tx = t * __ldg(N + (0 * 3 + 1) * n1 + j) * zk[q];          // theta N_xy(j) zx(k)
-        const double tyv = t * __ldg(N + (1 * 3 + 0) * n1 + i) * zk[Q + q];     // theta N_yx(i) zy(k)
-        const double tz = t * __ldg(N + (2 * 3 + 0) * n1 + i) * __ldg(N + (2 * 3 + 1) * n1 + j);
-        a0 = fma(__ldg(F + 0 * n + i), tx, a0);
-        a1 = fma(__ldg(F + 0 * n + i - 1), tx, a1);
-        a2 = fma(__ldg(F + 1 * n + j), tyv, a2);
-        a3 = fma(__ldg(F + 1 * n + j - 1), tyv, a3);
+        const double tx = t * __ldg(NF + (0 * 3 + 1) * (N + 1) + j) * zk[q];       // theta N_xy(j) zx(k)
+        const double tyv = t * __ldg(NF + (1 * 3 + 0) * (N + 1) + i) * zk[Q + q];  // theta N_yx(i) zy(k)
+        const double tz = t * __ldg(NF + (2 * 3 + 0) * (N + 1) + i) * __ldg(NF + (2 * 3 + 1) * (N + 1) + j);
+        a0 = fma(__ldg(F + 0 * N + i), tx, a0);
+        a1 = fma(__ldg(F + 0 * N + i - 1), tx, a1);
+        a2 = fma(__ldg(F + 1 * N + j), tyv, a2);
+        a3 = fma(__ldg(F + 1 * N + j - 1), tyv, a3);
         a4 = fma(tz, zk[2 * Q + q], a4);
       }
     }
@@ -182,17 +220,76 @@ __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
 #pragma unroll
   for (int r = 0; r < NPT; ++r) weights(r, zf, true);  // plane kb-1: its z face is wzm of kb
 
-  mbar_wait(&bar[0], 0u);
-  mbar_wait(&bar[1], 0u);
+  // Own-column values march in registers: xd = u(k-1), xc = u(k); only the four
+  // in-plane neighbours are read from shared memory.
+  double xd[NPT], xc[NPT], bcv[NPT];
+  // XF: transform staged plane p (h0, h1) into the u ring; returns own rows in xo / bo
+  auto transform = [&](int p, double* xo, double* bo) {
+    const double* R = raw(p);
+    double* T = uring + (p - p_first) % U * HSZ;
+    auto f = [&](int e) -> double {
+      if (MODE == FM_PRE) return (om * R[HSZ + e]) * R[e];  // w dinv b
+      else return fma(sc, R[HSZ + e], R[e]);                // s + beta p_old
+    };
+#pragma unroll
+    for (int r = 0; r < NPT; ++r) {
+      const int e = hoff + r * RPP * N;
+      const double v = f(e);
+      T[e] = v;
+      xo[r] = v;
+      bo[r] = R[e];
+    }
+    if (rl0 == 0 && !skip) T[i] = f(i);                                     // halo row j0-1
+    if (rl0 == RPP - 1) T[(TY + 1) * N + i] = f((TY + 1) * N + i);         // halo row j0+TY
+  };
+
+  if (XF) {
+    wait(p_first);
+    wait(p_first + 1);
+    transform(p_first, xd, bcv);
+    transform(p_first + 1, xc, bcv);
+    __syncthreads();
+    if (tid == 0) {
+      if (p_first + S <= p_last) issue(p_first + S);
+      if (p_first + 1 + S <= p_last) issue(p_first + 1 + S);
+    }
+  } else {
+    wait(p_first);
+    wait(p_first + 1);
+#pragma unroll
+    for (int r = 0; r < NPT; ++r) {
+      xd[r] = raw(p_first)[hoff + r * RPP * N];
+      xc[r] = raw(p_first + 1)[hoff + r * RPP * N];
+    }
+  }
+
   // KB planes per trip: one CTA barrier and KB TMA issues amortised over KB nodes per row
   constexpr int KB = 2;
   for (int k0 = kb; k0 < ke; k0 += KB) {
+    double xn[KB][NPT], bn[KB][NPT];
+    if (XF) {
+#pragma unroll
+      for (int u = 0; u < KB; ++u) {
+        const int pu = k0 + 1 + u;
+        if (pu <= p_last) {
+          wait(pu);
+          transform(pu, xn[u], bn[u]);
+        }
+      }
+      __syncthreads();  // transformed planes visible; raw slots of k0+1, k0+2 free
+      if (tid == 0) {
+#pragma unroll
+        for (int u = 0; u < KB; ++u) {
+          const int pn = k0 + 1 + u + S;
+          if (pn <= p_last) issue(pn);
+        }
+      }
+    }
 #pragma unroll
     for (int u = 0; u < KB; ++u) {
       const int k = k0 + u;
       if (k >= ke) break;
-      const int idx = k + 1 - p_first;
-      mbar_wait(&bar[idx & (S - 1)], (uint32_t)((idx / S) & 1));
+      if (!XF) wait(k + 1);
       const bool fresh = (k == kb) || !zsame[k - p_first];  // CTA-uniform
 #pragma unroll
       for (int r = 0; r < NPT; ++r) {
@@ -206,84 +303,66 @@ __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
           wdi[r] = om / dg[r];
         }
       }
-      const int sm = (idx - 2) & (S - 1), s0 = (idx - 1) & (S - 1), sp = idx & (S - 1);
-      const int64_t kofs = base + (int64_t)k * n2 + i;
+      // plane k's in-plane neighbours (transformed ring for XF, raw ring otherwise)
+      const double* P0 = (XF ? uring + (k - p_first) % U * HSZ : raw(k)) + hoff;
+      const double* PU = raw(k + 1) + hoff;  // raw plane k+1 (non-XF: own column up value)
+      const double* C0 = raw(k) + NH * HSZ + coff;
+      const int64_t gk = goff + (int64_t)k * N2;
 #pragma unroll
       for (int r = 0; r < NPT; ++r) {
-        const int jl = rl0 + r * rpp;
-        const int j = j0 + jl;
-        const int hi = (jl + 1) * n + i;
-        const int ci = jl * n + i;
-        double uc, ue, uw, un, us, uu, ud;
-        if (MODE == FM_PRE) {
-          const double* B0 = hptr(s0, 0); const double* D0 = hptr(s0, 1);
-          const double* BM = hptr(sm, 0); const double* DM = hptr(sm, 1);
-          const double* BP = hptr(sp, 0); const double* DP = hptr(sp, 1);
-          uc = om * D0[hi] * B0[hi];
-          ue = om * D0[hi + 1] * B0[hi + 1];
-          uw = om * D0[hi - 1] * B0[hi - 1];
-          un = om * D0[hi + n] * B0[hi + n];
-          us = om * D0[hi - n] * B0[hi - n];
-          uu = om * DP[hi] * BP[hi];
-          ud = om * DM[hi] * BM[hi];
-        } else if (MODE == FM_PAPPLY) {
-          const double* X0 = hptr(s0, 0); const double* XM = hptr(sm, 0); const double* XP = hptr(sp, 0);
-          const double* P0 = hptr(s0, 1); const double* PM = hptr(sm, 1); const double* PP = hptr(sp, 1);
-          uc = fma(sc, P0[hi], X0[hi]);
-          ue = fma(sc, P0[hi + 1], X0[hi + 1]);
-          uw = fma(sc, P0[hi - 1], X0[hi - 1]);
-          un = fma(sc, P0[hi + n], X0[hi + n]);
-          us = fma(sc, P0[hi - n], X0[hi - n]);
-          uu = fma(sc, PP[hi], XP[hi]);
-          ud = fma(sc, PM[hi], XM[hi]);
-        } else {
-          const double* X0 = hptr(s0, 0); const double* XM = hptr(sm, 0); const double* XP = hptr(sp, 0);
-          uc = X0[hi]; ue = X0[hi + 1]; uw = X0[hi - 1]; un = X0[hi + n]; us = X0[hi - n];
-          uu = XP[hi]; ud = XM[hi];
-        }
+        const int o = r * RPP * N;  // compile-time after unrolling
+        const double uu = XF ? xn[u][r] : PU[o];
+        const double uc = xc[r], ud = xd[r];
+        const double ue = P0[o + 1], uw = P0[o - 1], un = P0[o + N], us = P0[o - N];
         // shallow FMA tree (a dependent chain of 6 would be latency bound)
         const double offx = fma(wxm[r], uw, wxp[r] * ue);
         const double offy = fma(wym[r], us, wyp[r] * un);
         const double offz = fma(wzm[r], ud, wzp[r] * uu);
         const double off = (offx + offy) + offz;
-        const double d = dg[r];
-        const double Au = fma(d, uc, -off);
-        const bool on = (i != 0) && (j != 0);  // Dirichlet ghost column / row
-        const int64_t gidx = kofs + (int64_t)j * n;
-        if (MODE == FM_APPLY) {
-          if (on && a.out0) a.out0[gidx] = Au;
-          acc = on ? fma(uc, Au, acc) : acc;
-        } else if (MODE == FM_RESID) {
-          const double rv = cptr(s0, 0)[ci] - Au;
-          if (on) a.out0[gidx] = rv;
-          acc = on ? fma(rv, rv, acc) : acc;
-        } else if (MODE == FM_JACOBI) {
-          const double bv = cptr(s0, 0)[ci];
-          const double y = fma(wdi[r], bv - Au, uc);
-          if (on) a.out0[gidx] = y;
-          acc = on ? fma(bv, y, acc) : acc;
-        } else if (MODE == FM_PRE) {
-          if (on) a.out0[gidx] = hptr(s0, 0)[hi] - Au;
-        } else if (MODE == FM_CG) {
-          const double xv = fma(sc, uc, cptr(s0, 0)[ci]);
-          const double rv = fma(-sc, Au, cptr(s0, 1)[ci]);
-          if (on) {
-            a.out0[gidx] = xv;
-            a.out1[gidx] = rv;
+        const int64_t gidx = gk + o;
+        if (MODE == FM_PRE) {
+          // b - A (w D^-1 b) = (1 - w) b + off(w D^-1 b): the diagonal term is w b
+          if (on[r]) a.out0[gidx] = fma(1.0 - om, bcv[r], off);
+          bcv[r] = bn[u][r];
+        } else {
+          const double Au = fma(dg[r], uc, -off);
+          if (MODE == FM_APPLY) {
+            if (on[r] && a.out0) a.out0[gidx] = Au;
+            acc = on[r] ? fma(uc, Au, acc) : acc;
+          } else if (MODE == FM_RESID) {
+            const double rv = C0[o] - Au;
+            if (on[r]) a.out0[gidx] = rv;
+            acc = on[r] ? fma(rv, rv, acc) : acc;
+          } else if (MODE == FM_JACOBI) {
+            const double bv = C0[o];
+            const double y = fma(wdi[r], bv - Au, uc);
+            if (on[r]) a.out0[gidx] = y;
+            acc = on[r] ? fma(bv, y, acc) : acc;
+          } else if (MODE == FM_CG) {
+            const double xv = fma(sc, uc, C0[o]);
+            const double rv = fma(-sc, Au, C0[CSZ + o]);
+            if (on[r]) {
+              a.out0[gidx] = xv;
+              a.out1[gidx] = rv;
+            }
+            acc = on[r] ? fma(rv, rv, acc) : acc;
+          } else {  // FM_PAPPLY
+            if (on[r]) a.out0[gidx] = uc;
+            acc = on[r] ? fma(uc, Au, acc) : acc;
           }
-          acc = on ? fma(rv, rv, acc) : acc;
-        } else {  // FM_PAPPLY
-          if (on) a.out0[gidx] = uc;
-          acc = on ? fma(uc, Au, acc) : acc;
         }
+        xd[r] = uc;
+        xc[r] = uu;
       }
     }
-    __syncthreads();  // every thread is done with planes k0-1 .. k0+KB-2
-    if (tid == 0) {
+    if (!XF) {
+      __syncthreads();  // every thread is done with planes k0-1 .. k0+KB-1
+      if (tid == 0) {
 #pragma unroll
-      for (int u = 0; u < KB; ++u) {
-        const int pn = k0 - 1 + u + S;
-        if (pn <= p_last) issue(pn);
+        for (int u = 0; u < KB; ++u) {
+          const int pn = k0 - 1 + u + S;
+          if (pn <= p_last) issue(pn);
+        }
       }
     }
   }
@@ -294,60 +373,49 @@ __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
   }
 }
 
-template <int Q, int MODE, int NPT>
-static cudaError_t fine_launch_qmn(const FineArgs& a, int batch, cudaStream_t stream) {
-  using L = SL<MODE>;
-  const int n = a.op.n, ty = a.g.ty;
-  const int np = n / a.g.zc + 2;
-  const size_t stage_bytes = (size_t)(L::NH * (ty + 2) + L::NC * ty) * n * 8;
-  const size_t smem = 64 + 4 * (kMaxKz + 4) + 8 * (((size_t)np * 3 * Q + 1) & ~(size_t)1) +
-                      kStages * stage_bytes;
+template <int MODE, int N>
+static cudaError_t fine_launch_mn(const FineArgs& a, int batch, cudaStream_t stream) {
+  using G = FT<N>;
+  if (a.g.threads != G::THREADS || a.g.ty != G::TY) return cudaErrorInvalidValue;
+  const int np = N / a.g.zc + 2;
+  const size_t smem = FSmem<N, MODE>::bytes(np, a.op.Q);
   if (smem > 220 * 1024) return cudaErrorInvalidValue;
   static size_t attr = 48 * 1024;
   if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(fine_kernel<Q, MODE, NPT>,
+    cudaError_t e = cudaFuncSetAttribute(fine_kernel<MODE, N>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = smem;
   }
   dim3 grd(1, a.g.ytiles, batch * a.g.zc);
   count_launch();
-  fine_kernel<Q, MODE, NPT><<<grd, a.g.threads, smem, stream>>>(a);
+  fine_kernel<MODE, N><<<grd, G::THREADS, smem, stream>>>(a);
   return cudaGetLastError();
 }
 
-template <int Q, int MODE>
-static cudaError_t fine_launch_qm(const FineArgs& a, int batch, cudaStream_t stream) {
-  if (a.g.npt == 2) return fine_launch_qmn<Q, MODE, 2>(a, batch, stream);
-  if (a.g.npt == 1) return fine_launch_qmn<Q, MODE, 1>(a, batch, stream);
-  return cudaErrorInvalidValue;
-}
-
-template <int Q>
-static cudaError_t fine_launch_q(int mode, const FineArgs& a, int batch, cudaStream_t stream) {
-  switch (mode) {
-    case FM_APPLY: return fine_launch_qm<Q, FM_APPLY>(a, batch, stream);
-    case FM_RESID: return fine_launch_qm<Q, FM_RESID>(a, batch, stream);
-    case FM_JACOBI: return fine_launch_qm<Q, FM_JACOBI>(a, batch, stream);
-    case FM_PRE: return fine_launch_qm<Q, FM_PRE>(a, batch, stream);
-    case FM_CG: return fine_launch_qm<Q, FM_CG>(a, batch, stream);
-    case FM_PAPPLY: return fine_launch_qm<Q, FM_PAPPLY>(a, batch, stream);
+template <int MODE>
+static cudaError_t fine_launch_m(const FineArgs& a, int batch, cudaStream_t stream) {
+  switch (a.op.n) {
+    case 8: return fine_launch_mn<MODE, 8>(a, batch, stream);
+    case 16: return fine_launch_mn<MODE, 16>(a, batch, stream);
+    case 32: return fine_launch_mn<MODE, 32>(a, batch, stream);
+    case 64: return fine_launch_mn<MODE, 64>(a, batch, stream);
+    case 128: return fine_launch_mn<MODE, 128>(a, batch, stream);
+    case 256: return fine_launch_mn<MODE, 256>(a, batch, stream);
     default: return cudaErrorInvalidValue;
   }
 }
 
 static cudaError_t fine_launch(int mode, FineArgs& a, int batch, cudaStream_t stream) {
-  if (a.op.n > 256 || a.op.n < 8) return cudaErrorInvalidValue;
+  if (a.op.Q < 1 || a.op.Q > kMaxTerms) return cudaErrorInvalidValue;
   a.g = fine_geom(a.op.n, batch);
-  switch (a.op.Q) {
-    case 1: return fine_launch_q<1>(mode, a, batch, stream);
-    case 2: return fine_launch_q<2>(mode, a, batch, stream);
-    case 3: return fine_launch_q<3>(mode, a, batch, stream);
-    case 4: return fine_launch_q<4>(mode, a, batch, stream);
-    case 5: return fine_launch_q<5>(mode, a, batch, stream);
-    case 6: return fine_launch_q<6>(mode, a, batch, stream);
-    case 7: return fine_launch_q<7>(mode, a, batch, stream);
-    case 8: return fine_launch_q<8>(mode, a, batch, stream);
+  switch (mode) {
+    case FM_APPLY: return fine_launch_m<FM_APPLY>(a, batch, stream);
+    case FM_RESID: return fine_launch_m<FM_RESID>(a, batch, stream);
+    case FM_JACOBI: return fine_launch_m<FM_JACOBI>(a, batch, stream);
+    case FM_PRE: return fine_launch_m<FM_PRE>(a, batch, stream);
+    case FM_CG: return fine_launch_m<FM_CG>(a, batch, stream);
+    case FM_PAPPLY: return fine_launch_m<FM_PAPPLY>(a, batch, stream);
     default: return cudaErrorInvalidValue;
   }
 }
