@@ -45,7 +45,7 @@ CONFIGS = {
             kind="tb", blocks=(2, 2, 2), n=128, m0=4, r=30, n_train=4096, batch=512, delta=1e-12),
     3: dict(workload="smooth affine (6 modes), 256^3 cells, r=40 from 2048 train, batch 128, tol 1e-12",
             kind="smooth", blocks=None, n=256, m0=4, r=40, n_train=2048, batch=128, delta=1e-12,
-            chunk=64),
+            chunk=64, e2e_sub=32),
 }
 L_MAX = 60
 
@@ -244,28 +244,32 @@ def run_b200(args, rank, world, dist):
     worst_res = max(r.true_residual for r in reps)
     converged = all(r.converged for r in reps)
 
-    # ---- end to end through the public API with host buffers
-    hbuf = torch.empty(xbuf.numel(), dtype=torch.float64, pin_memory=True)
+    # ---- end to end through the public API with host buffers: host mu in, solutions
+    # out to pinned host memory, sub-batches pipelined (paper_2311_13862_b200.pipeline)
+    del state["x"]
+    del ctx, xbuf
+    torch.cuda.empty_cache()
+    e2e_sub = min(batch, args.e2e_sub or cfg.get("e2e_sub", 512))
+    pipe = rb.HostPipeline(prob, method, model, sub_batch=e2e_sub)
+    hbuf = torch.empty(batch * n ** 3, dtype=torch.float64, pin_memory=True)
     mus_host = np.ascontiguousarray(test)
+    pipe.solve(mus_host, hbuf)  # warm-up (untimed)
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        for c0 in range(0, batch, chunk):
-            rb.mg_context_for(prob, mus_host[c0:c0 + chunk], ctx=ctx)  # theta(mu) host -> device
-            x, reps_e = rb.rbi_pcg_solve(rb.BatchOperator(ctx), f, method, mg_ctx=ctx,
-                                         l1roc_model=model, x0_out=xbuf)
-            hbuf.copy_(x, non_blocking=True)      # solutions device -> host
+        reps_e = pipe.solve(mus_host, hbuf)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
     if dist is not None:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_value = world * batch * args.steps / (float(e2e_ms.item()) / 1e3)
+    e2e_iters_ok = all(a.iterations == b.iterations for a, b in zip(reps_e, reps))
     h2d = batch * spec.n_terms * 8
-    d2h = len(chunks) * xbuf.numel() * 8 + batch * (L_MAX + 1) * 8 + batch * (4 + 8 + 4)
+    d2h = batch * n ** 3 * 8 + batch * (L_MAX + 1) * 8 + batch * (4 + 8 + 4)
 
     # ---- roofline of the dominant fine-level kernel class
     peak, peak_kind = peaks()
@@ -319,7 +323,10 @@ def run_b200(args, rank, world, dist):
                    "all_converged": converged, "max_true_residual": worst_res,
                    "t_offline_s": round(t_off, 3)},
         "e2e": {"value": round(e2e_value, 2), "unit": "solves/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
+                "d2h_bytes_per_step": d2h,
+                "sub_batches": rb.pipeline.schedule(batch, e2e_sub, pipe.tail),
+                "api": "HostPipeline.solve (host mu -> pinned host solutions)",
+                "iterations_match_device_run": bool(e2e_iters_ok)},
         "gpu_launches": int(launches),
         "roofline": roofline,
         "kernels": table,
@@ -458,6 +465,8 @@ def main():
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--chunk", type=int, default=0, help="instances per device sub-batch")
+    ap.add_argument("--e2e-sub", type=int, default=0,
+                    help="instances per pipelined sub-batch of the end-to-end (host buffer) run")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-per-core", type=int, default=2)

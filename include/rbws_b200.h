@@ -44,6 +44,11 @@ int rbws_version(void);
 const char* rbws_last_error(void);
 /* Kernel launches issued by this library so far (process-wide counter). */
 int64_t rbws_launch_count(void);
+/* Copy `bytes` of device data to host memory through mapped pinned staging (a
+ * kernel store, not a copy-engine DMA), then synchronise `stream`.  Control-data
+ * readbacks (the reference's `.item()` / numpy conversions of small arrays)
+ * use it so they never queue behind a bulk solution download on another stream. */
+int rbws_fetch(void* dst_host, const void* src_device, int64_t bytes, void* stream);
 
 /* ---- hierarchy: mu-independent part of ParametricProblem -------------------
  * Replaces ParametricProblem.__init__ hierarchy/coarsening

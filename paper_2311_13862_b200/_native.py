@@ -24,6 +24,7 @@ SIGNATURES = {
     "rbws_version": [],
     "rbws_last_error": [],
     "rbws_launch_count": [],
+    "rbws_fetch": [_vp, _vp, _c_int64, _vp],
     "rbws_hierarchy_create": [_pp, _c_int, _c_int, _c_int, _vp, _vp],
     "rbws_hierarchy_destroy": [_vp],
     "rbws_hierarchy_levels": [_vp],
@@ -97,6 +98,20 @@ def require_cuda():
     if not torch.cuda.is_available():
         raise NativeError("no CUDA device: the RBWS B200 path has no CPU fallback")
     load()
+
+
+def fetch(t):
+    """Small device tensor -> numpy array through rbws_fetch (kernel stores into
+    mapped pinned memory; no copy-engine DMA that could queue behind a bulk
+    download on another stream).  Synchronises the current stream."""
+    import numpy as np
+    import torch
+    dt = {torch.float64: np.float64, torch.float32: np.float32, torch.int32: np.int32,
+          torch.int64: np.int64, torch.bool: np.bool_, torch.uint8: np.uint8}[t.dtype]
+    t = t.contiguous()
+    out = np.empty(tuple(t.shape), dtype=dt)
+    call("rbws_fetch", out.ctypes.data, t.data_ptr(), t.numel() * t.element_size(), stream_ptr())
+    return out
 
 
 def stream_ptr(stream=None) -> int:

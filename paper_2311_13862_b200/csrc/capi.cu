@@ -30,6 +30,12 @@ const char* rbws_last_error(void) { return rbws_get_error(); }
 
 int64_t rbws_launch_count(void) { return rbws::launch_count(); }
 
+int rbws_fetch(void* dst_host, const void* src_device, int64_t bytes, void* stream) {
+  if (bytes < 0) RBWS_FAIL("negative byte count");
+  RBWS_CHECK(rbws::fetch_to_host(dst_host, src_device, (size_t)bytes, S(stream)));
+  return 0;
+}
+
 int rbws_hierarchy_create(rbws_hierarchy** out, int n, int m0, int nterms, const double* face,
                           const double* node) {
   if (!out || !face || !node) RBWS_FAIL("null argument");
@@ -89,9 +95,7 @@ int rbws_batch_setup(rbws_batch* b, const double* theta, int count, int* n_bad, 
   if (rbws::batch_setup(bb, theta, count, S(stream))) return 1;
   if (n_bad) {
     std::vector<int> st(count);
-    RBWS_CHECK(cudaMemcpyAsync(st.data(), bb->d_status, sizeof(int) * count,
-                               cudaMemcpyDeviceToHost, S(stream)));
-    RBWS_CHECK(cudaStreamSynchronize(S(stream)));
+    RBWS_CHECK(rbws::fetch_to_host(st.data(), bb->d_status, sizeof(int) * count, S(stream)));
     int bad = 0;
     for (int v : st) bad += v ? 1 : 0;
     *n_bad = bad;

@@ -123,14 +123,11 @@ __global__ void __launch_bounds__(256) coarse_kernel(CoarseArgs a) {
   const int i = tid % n, jl = tid / n, j = j0 + jl;
   const bool on = (i >= 1) && (j >= 1);
   const double* th = a.theta + (size_t)mu * Q;
-  // 27 coefficients, c<oz><oy><ox> with m/0/p = -1/0/+1
-  double cmmm, cmm0, cmmp, cm0m, cm00, cm0p, cmpm, cmp0, cmpp;
-  double c0mm, c0m0, c0mp, c00m, c000, c00p, c0pm, c0p0, c0pp;
-  double cpmm, cpm0, cpmp, cp0m, cp00, cp0p, cppm, cpp0, cppp;
+  // 27 coefficients c[(oz+1)*9 + (oy+1)*3 + (ox+1)]
+  double c[27];
   auto coeffs = [&](int k) {
-    cmmm = cmm0 = cmmp = cm0m = cm00 = cm0p = cmpm = cmp0 = cmpp = 0.0;
-    c0mm = c0m0 = c0mp = c00m = c000 = c00p = c0pm = c0p0 = c0pp = 0.0;
-    cpmm = cpm0 = cpmp = cp0m = cp00 = cp0p = cppm = cpp0 = cppp = 0.0;
+#pragma unroll
+    for (int o = 0; o < 27; ++o) c[o] = 0.0;
     if (!on) return;
 #pragma unroll
     for (int t = 0; t < 3 * Q; ++t) {
@@ -138,80 +135,88 @@ __global__ void __launch_bounds__(256) coarse_kernel(CoarseArgs a) {
       const double* fx = fac + ((size_t)t * 3 + 0) * fstride;
       const double* fy = fac + ((size_t)t * 3 + 1) * fstride;
       const double* fz = fac + ((size_t)t * 3 + 2) * fstride;
-      const double xm = tri(fx, n1, i, -1), x0 = tri(fx, n1, i, 0), xp = tri(fx, n1, i, 1);
-      const double ym = tq * tri(fy, n1, j, -1), y0 = tq * tri(fy, n1, j, 0),
-                   yp = tq * tri(fy, n1, j, 1);
-      const double zm = tri(fz, n1, k, -1), z0 = tri(fz, n1, k, 0), zp = tri(fz, n1, k, 1);
-#define RBWS_ROW(Z, Y, YZ, C_M, C_0, C_P) \
-  {                                       \
-    const double YZ = Y * Z;              \
-    C_M = fma(xm, YZ, C_M);               \
-    C_0 = fma(x0, YZ, C_0);               \
-    C_P = fma(xp, YZ, C_P);               \
-  }
-      RBWS_ROW(zm, ym, a1, cmmm, cmm0, cmmp) RBWS_ROW(zm, y0, a2, cm0m, cm00, cm0p)
-      RBWS_ROW(zm, yp, a3, cmpm, cmp0, cmpp) RBWS_ROW(z0, ym, a4, c0mm, c0m0, c0mp)
-      RBWS_ROW(z0, y0, a5, c00m, c000, c00p) RBWS_ROW(z0, yp, a6, c0pm, c0p0, c0pp)
-      RBWS_ROW(zp, ym, a7, cpmm, cpm0, cpmp) RBWS_ROW(zp, y0, a8, cp0m, cp00, cp0p)
-      RBWS_ROW(zp, yp, a9, cppm, cpp0, cppp)
-#undef RBWS_ROW
+      const double xv[3] = {tri(fx, n1, i, -1), tri(fx, n1, i, 0), tri(fx, n1, i, 1)};
+      const double yv[3] = {tq * tri(fy, n1, j, -1), tq * tri(fy, n1, j, 0), tq * tri(fy, n1, j, 1)};
+      const double zv[3] = {tri(fz, n1, k, -1), tri(fz, n1, k, 0), tri(fz, n1, k, 1)};
+#pragma unroll
+      for (int dz = 0; dz < 3; ++dz)
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy) {
+          const double yz = yv[dy] * zv[dz];
+#pragma unroll
+          for (int dx = 0; dx < 3; ++dx) c[dz * 9 + dy * 3 + dx] = fma(xv[dx], yz, c[dz * 9 + dy * 3 + dx]);
+        }
     }
   };
 
   const int hi = (jl + 1) * n + i;
   const double om = a.omega;
   double cdi = 0.0;
+  // the 3x3 neighbourhood of this column in planes k-1, k, k+1 marches in registers:
+  // each step reads only plane k+1's nine values from shared memory
+  double va[9], vb[9], vcc[9];
+  auto load9 = [&](int p, double* v) {
+    const double* P = xs((p - p_first) & (S - 1)) + hi;
+    v[0] = P[-n - 1]; v[1] = P[-n]; v[2] = P[-n + 1];
+    v[3] = P[-1];     v[4] = P[0];  v[5] = P[1];
+    v[6] = P[n - 1];  v[7] = P[n];  v[8] = P[n + 1];
+  };
+  auto wait = [&](int p) {
+    const int t = p - p_first;
+    mbar_wait(&bar[t & (S - 1)], (uint32_t)((t / S) & 1));
+  };
   if (NH > 0) {
-    mbar_wait(&bar[0], 0u);
-    mbar_wait(&bar[1], 0u);
+    wait(p_first);
+    wait(p_first + 1);
+    load9(p_first, va);
+    load9(p_first + 1, vb);
   }
-  // KB planes per trip: one CTA barrier and KB TMA issues amortised over KB nodes
-  constexpr int KB = 2;
-  for (int k0 = kb; k0 < ke; k0 += KB) {
+  // one node: down / centre / up neighbourhoods in registers
+  auto step = [&](int k, const double* vd, const double* vc, double* vu) {
+    if (k == kb || !zsame[k - p_first]) {
+      coeffs(k);
+      cdi = om / c[13];  // cached damping / diagonal (no per-node division)
+    }
+    const int64_t gidx = base + (int64_t)k * n2 + (int64_t)j * n + i;
+    if (MODE == CM_DINV) {
+      if (on) a.y[gidx] = 1.0 / c[13];
+      return;
+    }
+    wait(k + 1);
+    load9(k + 1, vu);
+    double part[3];
+    const double* V3[3] = {vd, vc, vu};
 #pragma unroll
-    for (int u = 0; u < KB; ++u) {
-      const int k = k0 + u;
-      if (k >= ke) break;
-      const int idx = k + 1 - p_first;
-      if (NH > 0) mbar_wait(&bar[idx & (S - 1)], (uint32_t)((idx / S) & 1));
-      if (k == kb || !zsame[k - p_first]) {
-        coeffs(k);
-        cdi = om / c000;  // cached damping / diagonal (no per-node division)
-      }
-      const int64_t gidx = base + (int64_t)k * n2 + (int64_t)j * n + i;
-      if (MODE == CM_DINV) {
-        if (on) a.y[gidx] = 1.0 / c000;
-        continue;
-      }
-      const double* XM = xs((idx - 2) & (S - 1)) + hi;
-      const double* X0 = xs((idx - 1) & (S - 1)) + hi;
-      const double* XP = xs(idx & (S - 1)) + hi;
-#define RBWS_PL(P, CMM, CM0, CMP, C0M, C00, C0P, CPM, CP0, CPP, R)                       \
-  const double R##a = fma(CMP, P[-n + 1], fma(CM0, P[-n], CMM * P[-n - 1]));                 \
-  const double R##b = fma(C0P, P[1], fma(C00, P[0], C0M * P[-1]));                          \
-  const double R##c = fma(CPP, P[n + 1], fma(CP0, P[n], CPM * P[n - 1]));                   \
-  const double R = (R##a + R##b) + R##c;
-      RBWS_PL(XM, cmmm, cmm0, cmmp, cm0m, cm00, cm0p, cmpm, cmp0, cmpp, am)
-      RBWS_PL(X0, c0mm, c0m0, c0mp, c00m, c000, c00p, c0pm, c0p0, c0pp, a0)
-      RBWS_PL(XP, cpmm, cpm0, cpmp, cp0m, cp00, cp0p, cppm, cpp0, cppp, ap)
-      const double Au = (am + ap) + a0;
-#undef RBWS_PL
-      if (on) {
-        if (MODE == CM_APPLY) {
-          a.y[gidx] = Au;
-        } else if (MODE == CM_RESID) {
-          a.y[gidx] = bs((idx - 1) & (S - 1))[jl * n + i] - Au;
-        } else {  // CM_JACOBI
-          const double bv = bs((idx - 1) & (S - 1))[jl * n + i];
-          a.y[gidx] = fma(cdi, bv - Au, X0[0]);
-        }
+    for (int dz = 0; dz < 3; ++dz) {
+      const double* v = V3[dz];
+      const double* cc = c + dz * 9;
+      const double ra = fma(cc[2], v[2], fma(cc[1], v[1], cc[0] * v[0]));
+      const double rb = fma(cc[5], v[5], fma(cc[4], v[4], cc[3] * v[3]));
+      const double rc = fma(cc[8], v[8], fma(cc[7], v[7], cc[6] * v[6]));
+      part[dz] = (ra + rb) + rc;
+    }
+    const double Au = (part[0] + part[2]) + part[1];
+    if (on) {
+      if (MODE == CM_APPLY) {
+        a.y[gidx] = Au;
+      } else if (MODE == CM_RESID) {
+        a.y[gidx] = bs((k - p_first) & (S - 1))[jl * n + i] - Au;
+      } else {  // CM_JACOBI
+        const double bv = bs((k - p_first) & (S - 1))[jl * n + i];
+        a.y[gidx] = fma(cdi, bv - Au, vc[4]);
       }
     }
+  };
+  // three planes per trip: the register roles rotate with period 3 (no moves)
+  for (int k0 = kb; k0 < ke; k0 += 3) {
+    step(k0, va, vb, vcc);
+    if (k0 + 1 < ke) step(k0 + 1, vb, vcc, va);
+    if (k0 + 2 < ke) step(k0 + 2, vcc, va, vb);
     if (NH > 0) {
-      __syncthreads();  // every thread is done with planes k0-1 .. k0+KB-2
+      __syncthreads();  // every thread is done with planes <= k0+3
       if (tid == 0) {
 #pragma unroll
-        for (int u = 0; u < KB; ++u) {
+        for (int u = 0; u < 3; ++u) {
           const int pn = k0 - 1 + u + S;
           if (pn <= p_last) issue(pn);
         }

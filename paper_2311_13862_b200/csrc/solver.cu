@@ -15,6 +15,9 @@
 #include "fine.cuh"
 #include "solver.cuh"
 
+#include <algorithm>
+#include <mutex>
+
 static thread_local std::string g_err;
 
 int rbws_set_error(const char* msg, const char* file, int line) {
@@ -29,6 +32,56 @@ const char* rbws_get_error() { return g_err.c_str(); }
 #define RBWS_FAIL(msg) return rbws_set_error(msg, __FILE__, __LINE__)
 
 namespace rbws {
+
+// ---- small device -> host readbacks without the copy engines
+// A kernel stores into mapped pinned memory; the stream is synchronised and the
+// bytes are memcpy'd to dst.  Control data (active counts, iteration reports)
+// must not wait behind a bulk cudaMemcpyAsync queued on a copy engine by
+// another stream (the solution download of a pipelined sub-batch).
+__global__ void fetch_kernel(const unsigned char* __restrict__ src, unsigned char* dst,
+                             int64_t bytes) {
+  const int64_t words = bytes / 4;
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(src) & 3) == 0);
+  if (aligned) {
+    const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src);
+    volatile uint32_t* d4 = reinterpret_cast<volatile uint32_t*>(dst);
+    for (int64_t t = t0; t < words; t += stride) d4[t] = s4[t];
+    for (int64_t t = words * 4 + t0; t < bytes; t += stride) dst[t] = src[t];
+  } else {
+    for (int64_t t = t0; t < bytes; t += stride) dst[t] = src[t];
+  }
+}
+
+cudaError_t fetch_to_host(void* dst, const void* src, size_t bytes, cudaStream_t stream) {
+  static std::mutex mu;
+  static unsigned char* stage = nullptr;
+  static size_t cap = 0;
+  if (bytes == 0) return cudaSuccess;
+  std::lock_guard<std::mutex> guard(mu);
+  if (bytes > cap) {
+    if (stage) cudaFreeHost(stage);
+    stage = nullptr;
+    cap = std::max<size_t>(bytes, 1 << 16);
+    cudaError_t e = cudaHostAlloc((void**)&stage, cap, cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e != cudaSuccess) { cap = 0; return e; }
+  }
+  unsigned char* dstage = nullptr;
+  cudaError_t e = cudaHostGetDevicePointer((void**)&dstage, stage, 0);
+  if (e != cudaSuccess) return e;
+  const int threads = 256;
+  const int64_t need = ((int64_t)bytes / 4 + threads - 1) / threads;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(need, 148));
+  count_launch();
+  fetch_kernel<<<blocks, threads, 0, stream>>>(static_cast<const unsigned char*>(src), dstage,
+                                               (int64_t)bytes);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e == cudaSuccess) memcpy(dst, stage, bytes);
+  return e;
+}
+
 
 static std::atomic<int64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -546,8 +599,7 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
                                                         b->partial, tiles, delta, l_max, b->scale,
                                                         b->hist, hl, b->active, b->iters,
                                                         b->pstatus, b->nactive);
-  e = cudaMemcpyAsync(b->h_nactive, b->nactive, sizeof(int), cudaMemcpyDeviceToHost, stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  e = fetch_to_host(b->h_nactive, b->nactive, sizeof(int), stream);
   if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
   b->cur_active = *b->h_nactive;
   if (*b->h_nactive > 0) {
@@ -578,8 +630,7 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
                                                              delta, l_max, b->hist, hl, b->active,
                                                              b->iters, b->nactive);
       if (pf) b->prof_end(PROF_SCALARS, t0, stream);
-      e = cudaMemcpyAsync(b->h_nactive, b->nactive, sizeof(int), cudaMemcpyDeviceToHost, stream);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+      e = fetch_to_host(b->h_nactive, b->nactive, sizeof(int), stream);
       if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
       if (*b->h_nactive == 0) break;
       b->cur_active = *b->h_nactive;
@@ -604,14 +655,13 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
   if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
   // results to host
   std::vector<double> hh((size_t)count * hl);
-  e = cudaMemcpyAsync(hh.data(), b->hist, sizeof(double) * count * hl, cudaMemcpyDeviceToHost, stream);
-  if (e == cudaSuccess && out.iters)
-    e = cudaMemcpyAsync(out.iters, b->iters, sizeof(int) * count, cudaMemcpyDeviceToHost, stream);
+  // (zero-copy readbacks: they must not queue behind bulk DMA on the copy engines)
+  e = fetch_to_host(hh.data(), b->hist, sizeof(double) * count * hl, stream);
+  if (e == cudaSuccess && out.iters) e = fetch_to_host(out.iters, b->iters, sizeof(int) * count, stream);
   if (e == cudaSuccess && out.true_res)
-    e = cudaMemcpyAsync(out.true_res, d_true, sizeof(double) * count, cudaMemcpyDeviceToHost, stream);
+    e = fetch_to_host(out.true_res, d_true, sizeof(double) * count, stream);
   if (e == cudaSuccess && out.status)
-    e = cudaMemcpyAsync(out.status, b->pstatus, sizeof(int) * count, cudaMemcpyDeviceToHost, stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    e = fetch_to_host(out.status, b->pstatus, sizeof(int) * count, stream);
   if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
   if (b->prof_on) b->prof_flush();
   if (out.hist)

@@ -11,6 +11,10 @@
 
 namespace rbws {
 
+// device -> host copy of control data through mapped pinned memory (no copy engine);
+// synchronises the stream
+cudaError_t fetch_to_host(void* dst, const void* src, size_t bytes, cudaStream_t stream);
+
 struct Hierarchy {
   int n = 0, m0 = 0, levels = 0, Q = 0;
   std::vector<int> cells;           // coarse (0) .. fine (levels-1)

@@ -105,11 +105,13 @@ def mg_vcycle(b, ctx: MgContext, level=None):
 
 
 def mgcg_solve(A, f, x0, ctx: MgContext, delta: float = 1e-16, l_max: int = 40, mu=None,
-               method: str = "mgcg", raise_on_breakdown: bool = True):
+               method: str = "mgcg", raise_on_breakdown: bool = True,
+               overwrite_x0: bool = False):
     """Batched MGCG (multigrid.py:564-571 -> krylov.py:267-334).
 
     f: padded rhs, either one instance (shared) or a full batch; x0: padded
-    batch of initial guesses (None = zeros).  Returns (x, [SolveReport]).
+    batch of initial guesses (None = zeros), left untouched unless
+    ``overwrite_x0`` (then the solve runs in x0's storage).  Returns (x, [SolveReport]).
     """
     import torch
     if delta <= 0:
@@ -127,7 +129,14 @@ def mgcg_solve(A, f, x0, ctx: MgContext, delta: float = 1e-16, l_max: int = 40, 
         f_stride = n ** 3
     else:
         raise ValueError("rhs does not match the batch")
-    x = torch.zeros(nb, dtype=torch.float64, device="cuda") if x0 is None else x0.clone()
+    if x0 is None:
+        x = torch.zeros(nb, dtype=torch.float64, device="cuda")
+    elif overwrite_x0:
+        if x0.numel() < nb or not x0.is_contiguous():
+            raise ValueError("x0 does not hold the batch")
+        x = x0
+    else:
+        x = x0.clone()
     iters = np.zeros(count, dtype=np.int32)
     hist = np.zeros((count, l_max + 1))
     tres = np.zeros(count)

@@ -1,0 +1,102 @@
+"""Host-to-host solving of a large parameter set (the reference's per-parameter
+loop, experiment.py:149-157, as one streamed call).
+
+Parameters are solved in device-resident sub-batches; while sub-batch c+1 is
+being solved on the compute stream, the solutions of sub-batch c are copied to
+pinned host memory on a side stream.  Two multigrid contexts and two solution
+buffers alternate, so the device->host transfer of all but the last
+sub-batch hides behind compute.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native
+from .grid import BatchOperator, ParametricProblem, padded_len
+from .multigrid import MgContext, mg_context_for
+from .warmstart import MethodConfig, rbi_pcg_solve
+
+
+def schedule(count: int, sub_batch: int, tail: int) -> list[int]:
+    """Sub-batch sizes: full sub-batches, then halving down to ``tail`` so the
+    download of the last (un-overlapped) sub-batch is short."""
+    sizes, rem = [], int(count)
+    while rem > 0:
+        if rem > 2 * sub_batch:
+            take = sub_batch
+        elif rem > tail:
+            take = max(tail, min(sub_batch, (rem + 1) // 2))
+        else:
+            take = rem
+        sizes.append(take)
+        rem -= take
+    return sizes
+
+
+class HostPipeline:
+    """Solve ``mus`` (host array) into a pinned host buffer, sub-batch by sub-batch.
+
+    ``out_host``: pinned float64 tensor with at least ``len(mus) * n**3``
+    elements; instance m's padded solution (n^3 doubles) lands at
+    ``out_host[m*n^3 : (m+1)*n^3]``.
+    """
+
+    def __init__(self, problem: ParametricProblem, method: MethodConfig, model=None,
+                 sub_batch: int = 512, nu: int = 1, tail: int | None = None):
+        import torch
+        _native.require_cuda()
+        if sub_batch < 1:
+            raise ValueError("sub_batch must be positive")
+        self.problem, self.method, self.model, self.sub = problem, method, model, sub_batch
+        self.tail = max(1, sub_batch // 4) if tail is None else max(1, int(tail))
+        n = problem.n
+        self.ctx = [MgContext(problem, sub_batch, nu=nu) for _ in range(2)]
+        self.x = [torch.empty(padded_len(n, sub_batch), dtype=torch.float64, device="cuda")
+                  for _ in range(2)]
+        self.f = problem.rhs()
+        # both streams are side streams: the legacy default stream would serialise
+        # with the copies
+        self.compute_stream = torch.cuda.Stream()
+        self.copy_stream = torch.cuda.Stream()
+        self.freed = [torch.cuda.Event() for _ in range(2)]
+        self.solved = [torch.cuda.Event() for _ in range(2)]
+        for ev in self.freed:
+            ev.record()
+
+    def solve(self, mus, out_host):
+        import torch
+        mus = np.ascontiguousarray(mus, dtype=np.float64)
+        n3 = self.problem.n ** 3
+        if out_host.numel() < len(mus) * n3 or not out_host.is_pinned():
+            raise ValueError("out_host must be a pinned buffer of len(mus) * n^3 doubles")
+        caller = torch.cuda.current_stream()
+        compute = self.compute_stream
+        compute.wait_stream(caller)
+        reports = []
+        with torch.cuda.stream(compute):
+            reports = self._run(mus, out_host, compute, n3)
+        caller.wait_stream(compute)
+        caller.wait_stream(self.copy_stream)
+        return reports
+
+    def _run(self, mus, out_host, compute, n3):
+        import torch
+        reports = []
+        c0 = 0
+        for c, size in enumerate(schedule(len(mus), self.sub, self.tail)):
+            part = mus[c0:c0 + size]
+            s = c % 2
+            compute.wait_event(self.freed[s])     # buffer s no longer being copied out
+            ctx = mg_context_for(self.problem, part, ctx=self.ctx[s])
+            x, reps = rbi_pcg_solve(BatchOperator(ctx), self.f, self.method, mg_ctx=ctx,
+                                    l1roc_model=self.model, x0_out=self.x[s])
+            reports += reps
+            self.solved[s].record(compute)
+            with torch.cuda.stream(self.copy_stream):
+                self.copy_stream.wait_event(self.solved[s])
+                m = len(part)
+                out_host[c0 * n3:(c0 + m) * n3].copy_(x[:m * n3], non_blocking=True)
+                self.freed[s].record(self.copy_stream)
+            c0 += size
+        return reports

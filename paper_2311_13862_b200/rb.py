@@ -134,7 +134,7 @@ def l1roc_online(model: L1rocModel, A, b, out=None):
     ctx = A.ctx
     problem, count = ctx.problem, ctx.count
     a, c, _, st = _online_batch(model, problem, ctx.theta, b, count)
-    if bool((st != 0).any()):
+    if np.any(_native.fetch(st) != 0):
         raise DegenerateBasisError("sub-sampled reduced system is rank deficient")
     n = model.n
     x = out if out is not None else torch.empty(padded_len(n, count), dtype=torch.float64,
@@ -142,7 +142,7 @@ def l1roc_online(model: L1rocModel, A, b, out=None):
     _native.call("rbws_expand", n, count, model.basis.data_ptr(), n ** 3, model.dim,
                  a.data_ptr(), x.data_ptr(), _native.stream_ptr())
     x[count * n ** 3:] = 0.0
-    return x, c.view(count, model.dim).cpu().numpy()
+    return x, _native.fetch(c.view(count, model.dim))
 
 
 # ----------------------------------------------------------------- DEIM
