@@ -51,11 +51,12 @@ L_MAX = 60
 
 # algorithmic bytes per interior node and instance for each profiled kernel class
 CLASS_NAMES = ["fine_p_update_apply_dot", "fine_cg_update", "fine_pre_residual", "fine_restrict",
-               "fine_prolong", "fine_post_smooth", "fine_p_update", "coarse_levels", "scalars"]
+               "fine_prolong", "fine_prolong_post_smooth", "fine_p_update", "coarse_levels",
+               "scalars"]
 # reads + writes per interior node and instance:
 #  p-update+apply: s, p_old -> p_new | cg: p, x, r -> x, r | pre: b, dinv -> r1
-#  restrict: r1 -> bc (1/8) | prolong: b, dinv, e (1/8) -> u0 | post: u0, b -> s
-CLASS_BYTES = {0: 24.0, 1: 40.0, 2: 24.0, 3: 9.0, 4: 25.0, 5: 24.0, 6: 24.0}
+#  restrict: r1 -> bc, uc (2/8) + dinv_c (1/8) | prolong+post (fused): b, dinv, e (1/8) -> s
+CLASS_BYTES = {0: 24.0, 1: 40.0, 2: 24.0, 3: 11.0, 4: 25.0, 5: 25.0, 6: 24.0}
 
 
 def log(*a):

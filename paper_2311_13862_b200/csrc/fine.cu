@@ -71,6 +71,7 @@ struct FineArgs {
   const int* active;
   double omega;
   int c0_shared;  // c0 is one instance shared by the whole batch (e.g. the rhs f)
+  const double* ec;  // FM_POSTP: coarse-grid correction (n/2 cells, padded batch layout)
 };
 
 enum FineMode : int {
@@ -80,22 +81,33 @@ enum FineMode : int {
   FM_PRE = 3,     // h0 = b, h1 = dinv       out0 = b - A (w dinv b)
   FM_CG = 4,      // h0 = p, c0 = x, c1 = r  x += a p, r -= a A p (in place), dot |r|^2
   FM_PAPPLY = 5,  // h0 = s, h1 = p_old      out0 = p = s + b p_old, dot p.Ap
+  FM_POSTP = 6,   // h0 = b, h1 = dinv, ec   u = w dinv b + P ec; out0 = u + w (b - A u)/d, dot b.out
 };
 
 template <int MODE>
 struct SL {
   // PRE / PAPPLY stencil a derived vector (w dinv b, s + beta p_old): each staged
   // plane is transformed once into a second ring, so neighbours cost one LDS
-  static constexpr bool XF = (MODE == FM_PRE || MODE == FM_PAPPLY);
+  static constexpr bool XF = (MODE == FM_PRE || MODE == FM_PAPPLY || MODE == FM_POSTP);
   static constexpr int NH = XF ? 2 : 1;
   static constexpr int NC = (MODE == FM_CG) ? 2 : ((MODE == FM_RESID || MODE == FM_JACOBI) ? 1 : 0);
   static constexpr int S = XF ? 6 : kStages;  // raw ring slots
   static constexpr int U = 6;                 // transformed-plane ring slots (XF)
 };
 
+// FM_POSTP stages, with every even fine plane p, coarse plane p/2 + 1 rows
+// [cj0, cj0 + CR) (cj0 = first coarse row the tile's rows j0-1 .. j0+TY touch)
+template <int N>
+struct FCoarse {
+  static constexpr int NCC = N / 2;
+  static constexpr int CR = FT<N>::TY / 2 + 3;
+  static constexpr int CSZ = CR * NCC;
+};
+
 template <int N, int MODE>
 struct FSmem {
-  static constexpr int STAGE = SL<MODE>::NH * FT<N>::HSZ + SL<MODE>::NC * FT<N>::CSZ;
+  static constexpr int STAGE = SL<MODE>::NH * FT<N>::HSZ + SL<MODE>::NC * FT<N>::CSZ +
+                               (MODE == FM_POSTP ? FCoarse<N>::CSZ : 0);
   static constexpr int RING = SL<MODE>::S * STAGE + (SL<MODE>::XF ? SL<MODE>::U * FT<N>::HSZ : 0);
   static size_t bytes(int np, int Q) {
     return 64 + 4 * (kMaxKz + 4) + 8 * (((size_t)np * 3 * Q + 1) & ~(size_t)1) + 8 * (size_t)RING;
@@ -157,12 +169,18 @@ __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
   }
 
   const int skip = (j0 == 0) ? 1 : 0;  // row j0-1 does not exist for the first tile
+  constexpr int NCC = FCoarse<N>::NCC;
+  const int cj0 = (j0 == 0) ? 0 : (j0 >> 1) - 1;  // first staged coarse row (FM_POSTP)
   auto issue = [&](int p) {
     const int sl = (p - p_first) % S;
     double* st = ring + sl * STAGE;
     const uint32_t hbytes = (uint32_t)((TY + 2 - skip) * N * 8);
     constexpr uint32_t cbytes = (uint32_t)(CSZ * 8);
-    mbar_arrive_expect_tx(&bar[sl], NH * hbytes + NC * cbytes);
+    constexpr uint32_t ebytes = (uint32_t)(FCoarse<N>::CSZ * 8);
+    // coarse plane p/2 + 1 (for the z march of P ec) with every even fine plane;
+    // none past the last coarse plane (its ghost plane p/2 = n/2 is never advanced from)
+    const bool stage_c = (MODE == FM_POSTP) && !(p & 1) && ((p >> 1) + 1 <= NCC);
+    mbar_arrive_expect_tx(&bar[sl], NH * hbytes + NC * cbytes + (stage_c ? ebytes : 0u));
     const int64_t plane = base + (int64_t)p * N2;
     const int64_t hrow = plane + (int64_t)(j0 - 1 + skip) * N;
     bulk_g2s(st + skip * N, a.h0 + hrow, hbytes, &bar[sl]);
@@ -171,6 +189,11 @@ __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
       bulk_g2s(st + NH * HSZ, a.c0 + (a.c0_shared ? plane - base : plane) + (int64_t)j0 * N,
                cbytes, &bar[sl]);
     if (NC > 1) bulk_g2s(st + NH * HSZ + CSZ, a.c1 + plane + (int64_t)j0 * N, cbytes, &bar[sl]);
+    if (stage_c) {
+      const int64_t cpl = (int64_t)mu * NCC * NCC * NCC + (int64_t)((p >> 1) + 1) * NCC * NCC +
+                          (int64_t)cj0 * NCC;
+      bulk_g2s(st + NH * HSZ, a.ec + cpl, ebytes, &bar[sl]);
+    }
   };
   auto wait = [&](int p) {
     const int t = p - p_first;
@@ -194,7 +217,8 @@ __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
   const double om = a.omega;
   double acc = 0.0;
   // cached face weights per owned row (recomputed only when the z factors change)
-  double wxp[NPT], wxm[NPT], wyp[NPT], wym[NPT], wzp[NPT], wzm[NPT], dg[NPT], wdi[NPT];
+  double wxp[NPT] = {}, wxm[NPT] = {}, wyp[NPT] = {}, wym[NPT] = {}, wzp[NPT] = {}, wzm[NPT] = {};
+  double dg[NPT] = {}, wdi[NPT] = {};
   auto weights = [&](int r, const double* zk, bool first_plane) {
     const int j = j0 + rl0 + r * RPP;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
@@ -223,24 +247,57 @@ __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
   // Own-column values march in registers: xd = u(k-1), xc = u(k); only the four
   // in-plane neighbours are read from shared memory.
   double xd[NPT], xc[NPT], bcv[NPT];
+  // FM_POSTP: xy-interpolated coarse correction of every transformed row at coarse
+  // planes K = p/2 and K+1 (rows: NPT own, then the halo rows j0-1 and j0+TY)
+  double cv0[NPT + 2], cv1[NPT + 2];
+  auto trow_j = [&](int t) { return t < NPT ? j0 + rl0 + t * RPP : (t == NPT ? j0 - 1 : j0 + TY); };
+  auto trow_e = [&](int t) { return t < NPT ? hoff + t * RPP * N : (t == NPT ? i : (TY + 1) * N + i); };
+  auto trow_on = [&](int t) { return t < NPT || (t == NPT ? (rl0 == 0 && !skip) : (rl0 == RPP - 1)); };
+  // trilinear prolongation in x, y from a coarse plane C whose first row is crow0
+  auto vxy = [&](const double* C, int crow0, int j) -> double {
+    const double hx = (i & 1) ? 0.5 : 0.0, hy = (j & 1) ? 0.5 : 0.0;
+    const double* q = C + ((j >> 1) - crow0) * NCC + (i >> 1);
+    const double r0 = fma(hx, q[1] - q[0], q[0]);
+    const double r1 = fma(hx, q[NCC + 1] - q[NCC], q[NCC]);
+    return fma(hy, r1 - r0, r0);
+  };
+  if (MODE == FM_POSTP) {
+    const double* E = a.ec + (int64_t)mu * NCC * NCC * NCC + (int64_t)(p_first >> 1) * NCC * NCC;
+#pragma unroll
+    for (int t = 0; t < NPT + 2; ++t)
+      if (trow_on(t)) {
+        cv0[t] = vxy(E, 0, trow_j(t));
+        cv1[t] = vxy(E + NCC * NCC, 0, trow_j(t));
+      }
+  }
   // XF: transform staged plane p (h0, h1) into the u ring; returns own rows in xo / bo
   auto transform = [&](int p, double* xo, double* bo) {
     const double* R = raw(p);
     double* T = uring + (p - p_first) % U * HSZ;
-    auto f = [&](int e) -> double {
-      if (MODE == FM_PRE) return (om * R[HSZ + e]) * R[e];  // w dinv b
-      else return fma(sc, R[HSZ + e], R[e]);                // s + beta p_old
-    };
+    const bool adv = (MODE == FM_POSTP) && p != p_first && !(p & 1);
 #pragma unroll
-    for (int r = 0; r < NPT; ++r) {
-      const int e = hoff + r * RPP * N;
-      const double v = f(e);
+    for (int t = 0; t < NPT + 2; ++t) {
+      if (!trow_on(t)) continue;
+      const int e = trow_e(t);
+      double v;
+      if (MODE == FM_PRE) {
+        v = (om * R[HSZ + e]) * R[e];  // w dinv b
+      } else if (MODE == FM_PAPPLY) {
+        v = fma(sc, R[HSZ + e], R[e]);  // s + beta p_old
+      } else {  // FM_POSTP: w dinv b + P ec
+        if (adv) {
+          cv0[t] = cv1[t];
+          cv1[t] = vxy(R + NH * HSZ, cj0, trow_j(t));
+        }
+        const double pe = (p & 1) ? 0.5 * (cv0[t] + cv1[t]) : cv0[t];
+        v = fma(om * R[HSZ + e], R[e], pe);
+      }
       T[e] = v;
-      xo[r] = v;
-      bo[r] = R[e];
+      if (t < NPT) {
+        xo[t] = v;
+        bo[t] = R[e];
+      }
     }
-    if (rl0 == 0 && !skip) T[i] = f(i);                                     // halo row j0-1
-    if (rl0 == RPP - 1) T[(TY + 1) * N + i] = f((TY + 1) * N + i);         // halo row j0+TY
   };
 
   if (XF) {
@@ -323,6 +380,12 @@ __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
         if (MODE == FM_PRE) {
           // b - A (w D^-1 b) = (1 - w) b + off(w D^-1 b): the diagonal term is w b
           if (on[r]) a.out0[gidx] = fma(1.0 - om, bcv[r], off);
+          bcv[r] = bn[u][r];
+        } else if (MODE == FM_POSTP) {
+          const double Au = fma(dg[r], uc, -off);
+          const double y = fma(wdi[r], bcv[r] - Au, uc);
+          if (on[r]) a.out0[gidx] = y;
+          acc = on[r] ? fma(bcv[r], y, acc) : acc;
           bcv[r] = bn[u][r];
         } else {
           const double Au = fma(dg[r], uc, -off);
@@ -416,6 +479,7 @@ static cudaError_t fine_launch(int mode, FineArgs& a, int batch, cudaStream_t st
     case FM_PRE: return fine_launch_m<FM_PRE>(a, batch, stream);
     case FM_CG: return fine_launch_m<FM_CG>(a, batch, stream);
     case FM_PAPPLY: return fine_launch_m<FM_PAPPLY>(a, batch, stream);
+    case FM_POSTP: return fine_launch_m<FM_POSTP>(a, batch, stream);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -517,6 +581,17 @@ cudaError_t fine_pre(const Sep7& op, int batch, const double* b, const double* d
   a.h1 = dinv;
   a.out0 = r1;
   return fine_launch(FM_PRE, a, batch, lc.stream);
+}
+
+cudaError_t fine_post_prolong(const Sep7& op, int batch, const double* b, const double* dinv,
+                              const double* ec, double* y, double omega, double* partial,
+                              const LaunchCtx& lc) {
+  FineArgs a = base_args(op, partial ? DOT_BY : DOT_NONE, partial, lc, omega);
+  a.h0 = b;
+  a.h1 = dinv;
+  a.ec = ec;
+  a.out0 = y;
+  return fine_launch(FM_POSTP, a, batch, lc.stream);
 }
 
 cudaError_t fine_cg_update(const Sep7& op, int batch, const double* p, double* x, double* r,

@@ -31,6 +31,12 @@ cudaError_t fine_jacobi(const Sep7& op, int batch, const double* x, const double
 // r1 = b - A (omega dinv b)
 cudaError_t fine_pre(const Sep7& op, int batch, const double* b, const double* dinv, double* r1,
                      double omega, const LaunchCtx& lc);
+// fused prolongation + post-smoothing of the nu=1 V-cycle:
+// u = w dinv b + P ec (ec: coarse correction, n/2 cells), y = u + w (b - A u)/diag,
+// partial (may be null) = b . y
+cudaError_t fine_post_prolong(const Sep7& op, int batch, const double* b, const double* dinv,
+                              const double* ec, double* y, double omega, double* partial,
+                              const LaunchCtx& lc);
 // x += alpha p, r -= alpha A p, partial = |r|^2
 cudaError_t fine_cg_update(const Sep7& op, int batch, const double* p, double* x, double* r,
                            const double* alpha, double* partial, const LaunchCtx& lc);

@@ -423,11 +423,14 @@ int Batch::vcycle(int lvl, const double* bb, double* out, double* dot_partial,
     if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
     if (vcycle(lvl - 1, c.b, c.e, nullptr, lc)) return 1;
     if (pf) { prof_end(PROF_COARSE, t0, lc.stream); t0 = prof_begin(lc.stream); }
-    e = fine ? prolong_launch(n, count, 1, c.e, l.t1, bb, l.dinv, omega, lc)
-             : prolong_launch(n, count, 2, c.e, l.t1, l.u, nullptr, omega, lc);
-    if (pf) { prof_end(PROF_FINE_PROLONG, t0, lc.stream); t0 = prof_begin(lc.stream); }
-    if (e == cudaSuccess) e = op(MODE_JACOBI, fdot, l.t1, bb, out, dot_partial);
-    if (pf) prof_end(PROF_FINE_POST, t0, lc.stream);
+    if (fine) {  // prolongation fused into the post-smoothing sweep
+      e = fine_post_prolong(fine_op(), count, bb, l.dinv, c.e, out, omega,
+                            fdot == DOT_NONE ? nullptr : dot_partial, lc);
+      if (pf) prof_end(PROF_FINE_POST, t0, lc.stream);
+    } else {
+      e = prolong_launch(n, count, 2, c.e, l.t1, l.u, nullptr, omega, lc);
+      if (e == cudaSuccess) e = op(MODE_JACOBI, fdot, l.t1, bb, out, dot_partial);
+    }
     if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
     return 0;
   }
