@@ -202,13 +202,21 @@ __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
   auto raw = [&](int p) -> const double* { return ring + ((p - p_first) % S) * STAGE; };
   if (tid == 0)
     for (int p = p_first; p <= p_last && p < p_first + S; ++p) issue(p);
+  __syncthreads();  // zsame flags visible
+  // bit p - p_first of zmask: plane p repeats plane p-1's z factors (np <= 66 planes)
+  uint64_t zmask = 0;
+  for (int p = 1; p < np && p < 64; ++p) zmask |= (uint64_t)(zsame[p] != 0) << p;
+  const bool zlast = (np > 64) ? zsame[64] != 0 : false;  // kz = 64: plane p_first + 64 = ke - 1
+  auto repeats = [&](int k) -> bool {  // CTA-uniform
+    const int t = k - p_first;
+    return t < 64 ? ((zmask >> t) & 1) != 0 : zlast;
+  };
 
   // ---- this thread's column i and rows j = j0 + rl0 + r*RPP
   const int i = tid % N;
   const int rl0 = tid / N;
   const int hoff = (rl0 + 1) * N + i;  // thread's centre in a halo-staged array
   const int coff = rl0 * N + i;        // ... in a tile-only array
-  const int64_t goff = base + (int64_t)(j0 + rl0) * N + i;
   bool on[NPT];
 #pragma unroll
   for (int r = 0; r < NPT; ++r) on[r] = (i != 0) && (j0 + rl0 + r * RPP != 0);  // Dirichlet ghosts
@@ -219,7 +227,7 @@ __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
   // cached face weights per owned row (recomputed only when the z factors change)
   double wxp[NPT] = {}, wxm[NPT] = {}, wyp[NPT] = {}, wym[NPT] = {}, wzp[NPT] = {}, wzm[NPT] = {};
   double dg[NPT] = {}, wdi[NPT] = {};
-  auto weights = [&](int r, const double* zk, bool first_plane) {
+  auto weights = [&](int r, const double* zk) {
     const int j = j0 + rl0 + r * RPP;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
     if (i >= 1 && j >= 1) {
@@ -238,24 +246,29 @@ __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
         a4 = fma(tz, zk[2 * Q + q], a4);
       }
     }
-    wzm[r] = first_plane ? a4 : wzp[r];
     wxp[r] = a0; wxm[r] = a1; wyp[r] = a2; wym[r] = a3; wzp[r] = a4;
   };
+  auto diag = [&](int r) {
+    dg[r] = ((wxp[r] + wxm[r]) + (wyp[r] + wym[r])) + (wzp[r] + wzm[r]);
+    wdi[r] = om / dg[r];  // cached damping / diagonal (no per-node division)
+  };
 #pragma unroll
-  for (int r = 0; r < NPT; ++r) weights(r, zf, true);  // plane kb-1: its z face is wzm of kb
+  for (int r = 0; r < NPT; ++r) {  // plane kb-1: its z face (kb-1, kb) is wzm of plane kb
+    weights(r, zf);
+    wzm[r] = wzp[r];
+  }
+  bool pend = false;  // wzm must take the previous plane's wzp on the next repeated plane
 
-  // Own-column values march in registers: xd = u(k-1), xc = u(k); only the four
-  // in-plane neighbours are read from shared memory.
-  double xd[NPT], xc[NPT], bcv[NPT];
   // FM_POSTP: xy-interpolated coarse correction of every transformed row at coarse
   // planes K = p/2 and K+1 (rows: NPT own, then the halo rows j0-1 and j0+TY)
   double cv0[NPT + 2], cv1[NPT + 2];
   auto trow_j = [&](int t) { return t < NPT ? j0 + rl0 + t * RPP : (t == NPT ? j0 - 1 : j0 + TY); };
   auto trow_e = [&](int t) { return t < NPT ? hoff + t * RPP * N : (t == NPT ? i : (TY + 1) * N + i); };
   auto trow_on = [&](int t) { return t < NPT || (t == NPT ? (rl0 == 0 && !skip) : (rl0 == RPP - 1)); };
+  const double hx = (i & 1) ? 0.5 : 0.0;
   // trilinear prolongation in x, y from a coarse plane C whose first row is crow0
   auto vxy = [&](const double* C, int crow0, int j) -> double {
-    const double hx = (i & 1) ? 0.5 : 0.0, hy = (j & 1) ? 0.5 : 0.0;
+    const double hy = (j & 1) ? 0.5 : 0.0;
     const double* q = C + ((j >> 1) - crow0) * NCC + (i >> 1);
     const double r0 = fma(hx, q[1] - q[0], q[0]);
     const double r1 = fma(hx, q[NCC + 1] - q[NCC], q[NCC]);
@@ -270,7 +283,7 @@ __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
         cv1[t] = vxy(E + NCC * NCC, 0, trow_j(t));
       }
   }
-  // XF: transform staged plane p (h0, h1) into the u ring; returns own rows in xo / bo
+  // XF: transform staged plane p (h0, h1) into the u ring; own rows returned in xo / bo
   auto transform = [&](int p, double* xo, double* bo) {
     const double* R = raw(p);
     double* T = uring + (p - p_first) % U * HSZ;
@@ -300,6 +313,9 @@ __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
     }
   };
 
+  // Own-column values march in registers: xd = u(k-1), xc = u(k); only the four
+  // in-plane neighbours are read from shared memory.
+  double xd[NPT], xc[NPT], bcv[NPT];
   if (XF) {
     wait(p_first);
     wait(p_first + 1);
@@ -320,112 +336,120 @@ __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
     }
   }
 
-  // KB planes per trip: one CTA barrier and KB TMA issues amortised over KB nodes per row
-  constexpr int KB = 2;
-  for (int k0 = kb; k0 < ke; k0 += KB) {
-    double xn[KB][NPT], bn[KB][NPT];
-    if (XF) {
+  // one plane: vd / vc / vu = own-column input at k-1 / k / k+1, vb = own b at k
+  int64_t gk = base + (int64_t)(j0 + rl0) * N + i + (int64_t)kb * N2;  // (i, j0+rl0, k)
+  auto step = [&](int k, const double* vd, const double* vc, const double* vu, const double* vb) {
+    if (k == kb || !repeats(k)) {  // CTA-uniform
 #pragma unroll
-      for (int u = 0; u < KB; ++u) {
-        const int pu = k0 + 1 + u;
-        if (pu <= p_last) {
-          wait(pu);
-          transform(pu, xn[u], bn[u]);
+      for (int r = 0; r < NPT; ++r) {
+        const double prev = wzp[r];
+        weights(r, zf + (k - p_first) * ZW);
+        wzm[r] = prev;
+        diag(r);
+      }
+      pend = true;
+    } else if (pend) {
+#pragma unroll
+      for (int r = 0; r < NPT; ++r) {
+        wzm[r] = wzp[r];
+        diag(r);
+      }
+      pend = false;
+    }
+    // plane k's in-plane neighbours (transformed ring for XF, raw ring otherwise)
+    const double* P0 = (XF ? uring + (k - p_first) % U * HSZ : raw(k)) + hoff;
+    const double* C0 = raw(k) + NH * HSZ + coff;
+#pragma unroll
+    for (int r = 0; r < NPT; ++r) {
+      const int o = r * RPP * N;  // compile-time after unrolling
+      const double uc = vc[r], ud = vd[r], uu = vu[r];
+      const double ue = P0[o + 1], uw = P0[o - 1], un = P0[o + N], us = P0[o - N];
+      // shallow FMA tree (a dependent chain of 6 would be latency bound)
+      const double offx = fma(wxm[r], uw, wxp[r] * ue);
+      const double offy = fma(wym[r], us, wyp[r] * un);
+      const double offz = fma(wzm[r], ud, wzp[r] * uu);
+      const double off = (offx + offy) + offz;
+      const int64_t gidx = gk + o;
+      if (MODE == FM_PRE) {
+        // b - A (w D^-1 b) = (1 - w) b + off(w D^-1 b): the diagonal term is w b
+        if (on[r]) a.out0[gidx] = fma(1.0 - om, vb[r], off);
+      } else if (MODE == FM_POSTP) {
+        const double Au = fma(dg[r], uc, -off);
+        const double y = fma(wdi[r], vb[r] - Au, uc);
+        if (on[r]) a.out0[gidx] = y;
+        acc = on[r] ? fma(vb[r], y, acc) : acc;
+      } else {
+        const double Au = fma(dg[r], uc, -off);
+        if (MODE == FM_APPLY) {
+          if (on[r] && a.out0) a.out0[gidx] = Au;
+          acc = on[r] ? fma(uc, Au, acc) : acc;
+        } else if (MODE == FM_RESID) {
+          const double rv = C0[o] - Au;
+          if (on[r]) a.out0[gidx] = rv;
+          acc = on[r] ? fma(rv, rv, acc) : acc;
+        } else if (MODE == FM_JACOBI) {
+          const double bv = C0[o];
+          const double y = fma(wdi[r], bv - Au, uc);
+          if (on[r]) a.out0[gidx] = y;
+          acc = on[r] ? fma(bv, y, acc) : acc;
+        } else if (MODE == FM_CG) {
+          const double xv = fma(sc, uc, C0[o]);
+          const double rv = fma(-sc, Au, C0[CSZ + o]);
+          if (on[r]) {
+            a.out0[gidx] = xv;
+            a.out1[gidx] = rv;
+          }
+          acc = on[r] ? fma(rv, rv, acc) : acc;
+        } else {  // FM_PAPPLY
+          if (on[r]) a.out0[gidx] = uc;
+          acc = on[r] ? fma(uc, Au, acc) : acc;
         }
+      }
+    }
+    gk += N2;
+  };
+
+  // two planes per trip with statically rotating register roles: one CTA barrier
+  // and two TMA issues amortised over two nodes per row
+  for (int k0 = kb; k0 < ke; k0 += 2) {
+    double u0[NPT], u1[NPT], b0[NPT], b1[NPT];
+    if (XF) {
+      wait(k0 + 1);
+      transform(k0 + 1, u0, b0);
+      if (k0 + 2 <= p_last) {
+        wait(k0 + 2);
+        transform(k0 + 2, u1, b1);
       }
       __syncthreads();  // transformed planes visible; raw slots of k0+1, k0+2 free
       if (tid == 0) {
-#pragma unroll
-        for (int u = 0; u < KB; ++u) {
-          const int pn = k0 + 1 + u + S;
-          if (pn <= p_last) issue(pn);
-        }
+        if (k0 + 1 + S <= p_last) issue(k0 + 1 + S);
+        if (k0 + 2 + S <= p_last) issue(k0 + 2 + S);
       }
+    } else {
+      wait(k0 + 1);
+#pragma unroll
+      for (int r = 0; r < NPT; ++r) u0[r] = raw(k0 + 1)[hoff + r * RPP * N];
+    }
+    step(k0, xd, xc, u0, bcv);
+    if (k0 + 1 < ke) {
+      if (!XF) {
+        wait(k0 + 2);
+#pragma unroll
+        for (int r = 0; r < NPT; ++r) u1[r] = raw(k0 + 2)[hoff + r * RPP * N];
+      }
+      step(k0 + 1, xc, u0, u1, b0);
     }
 #pragma unroll
-    for (int u = 0; u < KB; ++u) {
-      const int k = k0 + u;
-      if (k >= ke) break;
-      if (!XF) wait(k + 1);
-      const bool fresh = (k == kb) || !zsame[k - p_first];  // CTA-uniform
-#pragma unroll
-      for (int r = 0; r < NPT; ++r) {
-        if (fresh) {
-          weights(r, zf + (k - p_first) * ZW, false);
-          dg[r] = ((wxp[r] + wxm[r]) + (wyp[r] + wym[r])) + (wzp[r] + wzm[r]);
-          wdi[r] = om / dg[r];  // cached damping / diagonal (no per-node division)
-        } else if (wzm[r] != wzp[r]) {
-          wzm[r] = wzp[r];
-          dg[r] = ((wxp[r] + wxm[r]) + (wyp[r] + wym[r])) + (wzp[r] + wzm[r]);
-          wdi[r] = om / dg[r];
-        }
-      }
-      // plane k's in-plane neighbours (transformed ring for XF, raw ring otherwise)
-      const double* P0 = (XF ? uring + (k - p_first) % U * HSZ : raw(k)) + hoff;
-      const double* PU = raw(k + 1) + hoff;  // raw plane k+1 (non-XF: own column up value)
-      const double* C0 = raw(k) + NH * HSZ + coff;
-      const int64_t gk = goff + (int64_t)k * N2;
-#pragma unroll
-      for (int r = 0; r < NPT; ++r) {
-        const int o = r * RPP * N;  // compile-time after unrolling
-        const double uu = XF ? xn[u][r] : PU[o];
-        const double uc = xc[r], ud = xd[r];
-        const double ue = P0[o + 1], uw = P0[o - 1], un = P0[o + N], us = P0[o - N];
-        // shallow FMA tree (a dependent chain of 6 would be latency bound)
-        const double offx = fma(wxm[r], uw, wxp[r] * ue);
-        const double offy = fma(wym[r], us, wyp[r] * un);
-        const double offz = fma(wzm[r], ud, wzp[r] * uu);
-        const double off = (offx + offy) + offz;
-        const int64_t gidx = gk + o;
-        if (MODE == FM_PRE) {
-          // b - A (w D^-1 b) = (1 - w) b + off(w D^-1 b): the diagonal term is w b
-          if (on[r]) a.out0[gidx] = fma(1.0 - om, bcv[r], off);
-          bcv[r] = bn[u][r];
-        } else if (MODE == FM_POSTP) {
-          const double Au = fma(dg[r], uc, -off);
-          const double y = fma(wdi[r], bcv[r] - Au, uc);
-          if (on[r]) a.out0[gidx] = y;
-          acc = on[r] ? fma(bcv[r], y, acc) : acc;
-          bcv[r] = bn[u][r];
-        } else {
-          const double Au = fma(dg[r], uc, -off);
-          if (MODE == FM_APPLY) {
-            if (on[r] && a.out0) a.out0[gidx] = Au;
-            acc = on[r] ? fma(uc, Au, acc) : acc;
-          } else if (MODE == FM_RESID) {
-            const double rv = C0[o] - Au;
-            if (on[r]) a.out0[gidx] = rv;
-            acc = on[r] ? fma(rv, rv, acc) : acc;
-          } else if (MODE == FM_JACOBI) {
-            const double bv = C0[o];
-            const double y = fma(wdi[r], bv - Au, uc);
-            if (on[r]) a.out0[gidx] = y;
-            acc = on[r] ? fma(bv, y, acc) : acc;
-          } else if (MODE == FM_CG) {
-            const double xv = fma(sc, uc, C0[o]);
-            const double rv = fma(-sc, Au, C0[CSZ + o]);
-            if (on[r]) {
-              a.out0[gidx] = xv;
-              a.out1[gidx] = rv;
-            }
-            acc = on[r] ? fma(rv, rv, acc) : acc;
-          } else {  // FM_PAPPLY
-            if (on[r]) a.out0[gidx] = uc;
-            acc = on[r] ? fma(uc, Au, acc) : acc;
-          }
-        }
-        xd[r] = uc;
-        xc[r] = uu;
-      }
+    for (int r = 0; r < NPT; ++r) {
+      xd[r] = u0[r];
+      xc[r] = u1[r];
+      bcv[r] = b1[r];
     }
     if (!XF) {
-      __syncthreads();  // every thread is done with planes k0-1 .. k0+KB-1
+      __syncthreads();  // every thread is done with planes k0-1 .. k0+1
       if (tid == 0) {
-#pragma unroll
-        for (int u = 0; u < KB; ++u) {
-          const int pn = k0 - 1 + u + S;
-          if (pn <= p_last) issue(pn);
-        }
+        if (k0 - 1 + S <= p_last) issue(k0 - 1 + S);
+        if (k0 + S <= p_last) issue(k0 + S);
       }
     }
   }
