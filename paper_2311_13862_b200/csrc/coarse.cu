@@ -40,6 +40,7 @@ CoarseGeom coarse_geom(int n, int batch) {
 struct CoarseArgs {
   int n, Q;
   const int* zsame;     // [n+1] plane k repeats plane k-1's z factors (host precomputed)
+  const int* grp;       // [3Q] z-group of every term (kron kernel)
   CoarseGeom g;
   const double* fac;    // [Q*3][3][2][n+1]
   const double* theta;  // [batch][Q]
@@ -225,6 +226,226 @@ __global__ void __launch_bounds__(256) coarse_kernel(CoarseArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// z-grouped Kronecker form (the fast path when few distinct z factors exist):
+//   A = sum_g Z_g (x) W_g,   W_g = sum_{t in g} theta_t Y_t (x) X_t,
+// so at node (I,J,K):  (A u) = sum_g sum_oz Z_g(K,oz) s_g(K+oz),
+//   s_g(k) = sum_{ox,oy} W_g(I,J; ox,oy) u(I+ox, J+oy, k)   (9 FMAs per group).
+// W_g (9G doubles) is plane-independent: computed once per CTA, never refreshed;
+// s_g of planes k-1, k, k+1 march in registers; Z_g(k, .) is a CTA-uniform table.
+// For thermal blocks G = 2 (4 with a z split): ~12G FMAs and 9 LDS per node and
+// about a third of the 27-coefficient kernel's registers (two CTAs per SM).
+template <int G, int MODE>
+__global__ void __launch_bounds__(256, 2) coarse_kron_kernel(CoarseArgs a) {
+  constexpr int NH = (MODE == CM_DINV) ? 0 : 1;
+  constexpr int NC = (MODE == CM_RESID || MODE == CM_JACOBI) ? 1 : 0;
+  constexpr int S = kCStages;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int n = a.n, n1 = n + 1, Q = a.Q;
+  const int ty = a.g.ty, zc = a.g.zc;
+  const int kc = blockIdx.z % zc, mu = blockIdx.z / zc;
+  if (a.active && !a.active[mu]) return;
+  const int j0 = blockIdx.y * ty;
+  const int tid = threadIdx.x;
+  const int64_t n2 = (int64_t)n * n;
+  const int64_t base = (int64_t)mu * n2 * n;
+  const int kz = n / zc;
+  const int kb = max(1, kc * kz), ke = min(n, (kc + 1) * kz);
+  const int p_first = kb - 1, p_last = ke;
+  const int np = p_last - p_first + 1;
+
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  int* zdsame = reinterpret_cast<int*>(smem + 64);                      // [kCMaxPlanes]
+  double* zg = reinterpret_cast<double*>(smem + 64 + 4 * kCMaxPlanes);   // [np][G][3]
+  double* ring = zg + ((np * G * 3 + 1) & ~1);
+  const int hsz = (ty + 2) * n + 2, csz = ty * n;
+  const int ssz = NH * hsz + NC * csz;
+  auto xs = [&](int st) { return ring + st * ssz; };
+  auto bs = [&](int st) { return ring + st * ssz + NH * hsz; };
+  const double* fac = a.fac;
+  const int fstride = 2 * n1;
+
+  if (tid == 0 && NH > 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+    mbar_fence_init();
+  }
+  if (NH > 0) {  // zero the pads and (first tile) the never-staged halo row above row 0
+    for (int t = tid; t < S; t += blockDim.x) {
+      xs(t)[hsz - 2] = 0.0;
+      xs(t)[hsz - 1] = 0.0;
+    }
+    if (j0 == 0)
+      for (int t = tid; t < S * n; t += blockDim.x) xs(t / n)[t % n] = 0.0;
+  }
+  // z stencil of every group at every staged plane (from the group's first term)
+  for (int t = tid; t < np * G * 3; t += blockDim.x) {
+    const int p = t / (3 * G), g = (t / 3) % G, o = t % 3 - 1, k = p_first + p;
+    int rep = 0;
+    for (int u = 3 * Q - 1; u >= 0; --u)
+      if (a.grp[u] == g) rep = u;
+    const double* fz = fac + ((size_t)rep * 3 + 2) * fstride;
+    zg[t] = (k >= 1 && k <= n - 1) ? tri(fz, n1, k, o) : 0.0;
+  }
+  __syncthreads();
+  for (int p = 1 + tid; p < np; p += blockDim.x) {  // diagonal z entries repeat plane p-1's?
+    int same = 1;
+    for (int g = 0; g < G; ++g) same &= (zg[(p * G + g) * 3 + 1] == zg[((p - 1) * G + g) * 3 + 1]);
+    zdsame[p] = same;
+  }
+
+  auto issue = [&](int p) {
+    const int st = (p - p_first) & (S - 1);
+    const int skip = (j0 == 0) ? 1 : 0;
+    const uint32_t hbytes = (uint32_t)((ty + 2 - skip) * n * 8);
+    const uint32_t cbytes = (uint32_t)(ty * n * 8);
+    mbar_arrive_expect_tx(&bar[st], NH * hbytes + NC * cbytes);
+    const int64_t plane = base + (int64_t)p * n2;
+    bulk_g2s(xs(st) + skip * n, a.x + plane + (int64_t)(j0 - 1 + skip) * n, hbytes, &bar[st]);
+    if (NC) bulk_g2s(bs(st), a.b + plane + (int64_t)j0 * n, cbytes, &bar[st]);
+  };
+  if (NH > 0 && tid == 0)
+    for (int p = p_first; p <= p_last && p < p_first + S; ++p) issue(p);
+
+  const int i = tid % n, jl = tid / n, j = j0 + jl;
+  const bool on = (i >= 1) && (j >= 1);
+  const double* th = a.theta + (size_t)mu * Q;
+  // W_g(ox, oy) of this column, w[g*9 + (oy+1)*3 + (ox+1)]
+  double w[G * 9];
+#pragma unroll
+  for (int o = 0; o < G * 9; ++o) w[o] = 0.0;
+  if (on) {
+    for (int t = 0; t < 3 * Q; ++t) {
+      const int gt = __ldg(a.grp + t);
+      const double tq = th[t / 3];
+      const double* fx = fac + ((size_t)t * 3 + 0) * fstride;
+      const double* fy = fac + ((size_t)t * 3 + 1) * fstride;
+      const double xv[3] = {tri(fx, n1, i, -1), tri(fx, n1, i, 0), tri(fx, n1, i, 1)};
+      const double yv[3] = {tq * tri(fy, n1, j, -1), tq * tri(fy, n1, j, 0), tq * tri(fy, n1, j, 1)};
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+        if (gt == g) {
+#pragma unroll
+          for (int oy = 0; oy < 3; ++oy)
+#pragma unroll
+            for (int ox = 0; ox < 3; ++ox) w[g * 9 + oy * 3 + ox] = fma(yv[oy], xv[ox], w[g * 9 + oy * 3 + ox]);
+        }
+    }
+  }
+  __syncthreads();  // zdsame visible
+
+  const int hi = (jl + 1) * n + i;
+  const double om = a.omega;
+  double cdi = 0.0, dg = 0.0;
+  auto wait = [&](int p) {
+    const int t = p - p_first;
+    mbar_wait(&bar[t & (S - 1)], (uint32_t)((t / S) & 1));
+  };
+  // s_g of one staged plane; centre value returned in xc
+  auto conv = [&](int p, double* s, double& xc) {
+    const double* P = xs((p - p_first) & (S - 1)) + hi;
+    const double v[9] = {P[-n - 1], P[-n], P[-n + 1], P[-1], P[0], P[1], P[n - 1], P[n], P[n + 1]};
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const double* wg = w + g * 9;
+      const double ra = fma(wg[2], v[2], fma(wg[1], v[1], wg[0] * v[0]));
+      const double rb = fma(wg[5], v[5], fma(wg[4], v[4], wg[3] * v[3]));
+      const double rc = fma(wg[8], v[8], fma(wg[7], v[7], wg[6] * v[6]));
+      s[g] = (ra + rb) + rc;
+    }
+    xc = v[4];
+  };
+  double sa[G], sb[G], sc[G], xa = 0.0, xb = 0.0, xcv = 0.0;
+  if (NH > 0) {
+    wait(p_first);
+    wait(p_first + 1);
+    conv(p_first, sa, xa);
+    conv(p_first + 1, sb, xb);
+  }
+  auto step = [&](int k, const double* sd, const double* s0, double* su, double x0, double& xu) {
+    const double* zk = zg + (k - p_first) * G * 3;
+    if (MODE == CM_DINV || MODE == CM_JACOBI) {
+      if (k == kb || !zdsame[k - p_first]) {
+        dg = 0.0;
+#pragma unroll
+        for (int g = 0; g < G; ++g) dg = fma(zk[g * 3 + 1], w[g * 9 + 4], dg);
+        cdi = om / dg;  // cached damping / diagonal (no per-node division)
+      }
+    }
+    const int64_t gidx = base + (int64_t)k * n2 + (int64_t)j * n + i;
+    if (MODE == CM_DINV) {
+      if (on) a.y[gidx] = 1.0 / dg;
+      return;
+    }
+    wait(k + 1);
+    conv(k + 1, su, xu);
+    double Au = 0.0;
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      Au = fma(zk[g * 3 + 0], sd[g], fma(zk[g * 3 + 1], s0[g], fma(zk[g * 3 + 2], su[g], Au)));
+    if (on) {
+      if (MODE == CM_APPLY) {
+        a.y[gidx] = Au;
+      } else if (MODE == CM_RESID) {
+        a.y[gidx] = bs((k - p_first) & (S - 1))[jl * n + i] - Au;
+      } else {  // CM_JACOBI
+        const double bv = bs((k - p_first) & (S - 1))[jl * n + i];
+        a.y[gidx] = fma(cdi, bv - Au, x0);
+      }
+    }
+  };
+  // three planes per trip: the register roles rotate with period 3 (no moves)
+  for (int k0 = kb; k0 < ke; k0 += 3) {
+    step(k0, sa, sb, sc, xb, xcv);
+    if (k0 + 1 < ke) step(k0 + 1, sb, sc, sa, xcv, xa);
+    if (k0 + 2 < ke) step(k0 + 2, sc, sa, sb, xa, xb);
+    if (NH > 0) {
+      __syncthreads();  // every thread is done with planes <= k0+3
+      if (tid == 0) {
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+          const int pn = k0 - 1 + u + S;
+          if (pn <= p_last) issue(pn);
+        }
+      }
+    }
+  }
+}
+
+template <int G, int MODE>
+static cudaError_t coarse_kron_launch_m(CoarseArgs a, int batch, cudaStream_t stream) {
+  constexpr int NH = (MODE == CM_DINV) ? 0 : 1;
+  constexpr int NC = (MODE == CM_RESID || MODE == CM_JACOBI) ? 1 : 0;
+  a.g = coarse_geom(a.n, batch);
+  const int np = a.n / a.g.zc + 2;
+  if (np > kCMaxPlanes) return cudaErrorInvalidValue;
+  const size_t smem = 64 + 4 * kCMaxPlanes + 8 * (((size_t)np * G * 3 + 1) & ~(size_t)1) +
+                      (size_t)kCStages * (NH * ((a.g.ty + 2) * a.n + 2) + NC * a.g.ty * a.n) * 8;
+  static size_t attr = 48 * 1024;
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(coarse_kron_kernel<G, MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  dim3 grd(1, a.g.ytiles, batch * a.g.zc);
+  count_launch();
+  coarse_kron_kernel<G, MODE><<<grd, a.g.threads, smem, stream>>>(a);
+  return cudaGetLastError();
+}
+
+template <int G>
+static cudaError_t coarse_kron_launch_g(int mode, const CoarseArgs& a, int batch,
+                                        cudaStream_t stream) {
+  switch (mode) {
+    case CM_APPLY: return coarse_kron_launch_m<G, CM_APPLY>(a, batch, stream);
+    case CM_RESID: return coarse_kron_launch_m<G, CM_RESID>(a, batch, stream);
+    case CM_JACOBI: return coarse_kron_launch_m<G, CM_JACOBI>(a, batch, stream);
+    case CM_DINV: return coarse_kron_launch_m<G, CM_DINV>(a, batch, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 template <int Q, int MODE>
 static cudaError_t coarse_launch_m(CoarseArgs a, int batch, cudaStream_t stream) {
   constexpr int NH = (MODE == CM_DINV) ? 0 : 1;
@@ -257,22 +478,31 @@ static cudaError_t coarse_launch_q(int mode, const CoarseArgs& a, int batch, cud
   }
 }
 
-cudaError_t coarse_launch(int mode, int n, int Q, const double* fac, const int* zsame,
-                          const double* theta, int batch, const double* x, const double* b,
-                          double* y, double omega, const LaunchCtx& lc) {
+cudaError_t coarse_launch(int mode, const CoarseOp& op, const double* theta, int batch,
+                          const double* x, const double* b, double* y, double omega,
+                          const LaunchCtx& lc) {
+  const int n = op.n;
   if (n < 2 || n > 256) return cudaErrorInvalidValue;
   CoarseArgs a{};
   a.n = n;
-  a.Q = Q;
-  a.zsame = zsame;
-  a.fac = fac;
+  a.Q = op.Q;
+  a.zsame = op.zsame;
+  a.grp = op.grp;
+  a.fac = op.fac;
   a.theta = theta;
   a.x = x;
   a.b = b;
   a.y = y;
   a.active = lc.active;
   a.omega = omega;
-  switch (Q) {
+  switch (op.G) {  // few z-groups: grouped Kronecker kernel
+    case 1: return coarse_kron_launch_g<1>(mode, a, batch, lc.stream);
+    case 2: return coarse_kron_launch_g<2>(mode, a, batch, lc.stream);
+    case 3: return coarse_kron_launch_g<3>(mode, a, batch, lc.stream);
+    case 4: return coarse_kron_launch_g<4>(mode, a, batch, lc.stream);
+    default: break;
+  }
+  switch (op.Q) {  // general: 27 register coefficients per column
     case 1: return coarse_launch_q<1>(mode, a, batch, lc.stream);
     case 2: return coarse_launch_q<2>(mode, a, batch, lc.stream);
     case 3: return coarse_launch_q<3>(mode, a, batch, lc.stream);

@@ -10,12 +10,21 @@ struct CoarseGeom {
 };
 CoarseGeom coarse_geom(int n, int batch);
 
-// mode: 0 apply y=Ax | 1 resid y=b-Ax | 2 jacobi y=x+w(b-Ax)/diag | 3 pre y=b-A(w dinv b)
-//       4 dinv y=1/diag.  fac: the level's Kronecker factors [Q*3][3][2][n+1].
-//       zsame: [n+1] per-plane flag "z factors equal the previous plane's" (host built).
-cudaError_t coarse_launch(int mode, int n, int Q, const double* fac, const int* zsame,
-                          const double* theta, int batch, const double* x, const double* b,
-                          double* y, double omega, const LaunchCtx& lc);
+// One coarse level's matrix-free operator description.
+//   fac:   the level's Kronecker factors [Q*3][3][2][n+1]
+//   zsame: [n+1] per-plane flag "z factors equal the previous plane's" (host built)
+//   grp:   [3Q] z-group of every term (terms with bitwise identical z factors), G groups
+struct CoarseOp {
+  int n = 0, Q = 0, G = 0;
+  const double* fac = nullptr;
+  const int* zsame = nullptr;
+  const int* grp = nullptr;
+};
+
+// mode: 0 apply y=Ax | 1 resid y=b-Ax | 2 jacobi y=x+w(b-Ax)/diag | 4 dinv y=1/diag
+cudaError_t coarse_launch(int mode, const CoarseOp& op, const double* theta, int batch,
+                          const double* x, const double* b, double* y, double omega,
+                          const LaunchCtx& lc);
 // coarsest level: dense Galerkin operator from the factors + Cholesky per instance
 cudaError_t coarse_factor_kf(int n0, int Q, const double* fac, const double* theta, int batch,
                              double* L, int* status, cudaStream_t stream);

@@ -99,6 +99,7 @@ Hierarchy::~Hierarchy() {
   cudaFree(d_node);
   for (double* p : d_fac) cudaFree(p);
   for (int* p : d_zsame) cudaFree(p);
+  for (int* p : d_grp) cudaFree(p);
   cudaFree(d_fzsame);
 }
 
@@ -211,6 +212,8 @@ int hierarchy_create(Hierarchy** out, int n, int m0, int Q, const double* face,
   }
   h->d_fac.assign(L, nullptr);
   h->d_zsame.assign(L, nullptr);
+  h->d_grp.assign(L, nullptr);
+  h->G.assign(L, 0);
   for (int l = 0; l < L && e == cudaSuccess; ++l) {
     e = dalloc(&h->d_fac[l], h->h_fac[l].size());
     if (e == cudaSuccess)
@@ -235,6 +238,24 @@ int hierarchy_create(Hierarchy** out, int n, int m0, int Q, const double* face,
     if (e == cudaSuccess) e = dalloc(&h->d_zsame[l], zs.size());
     if (e == cudaSuccess)
       e = cudaMemcpy(h->d_zsame[l], zs.data(), sizeof(int) * zs.size(), cudaMemcpyHostToDevice);
+    // z-groups: terms whose z factors (diagonal and off-diagonal, every plane) are
+    // bitwise identical share one z stencil, A = sum_g Z_g (x) (sum_{t in g} theta_t Y_t (x) X_t)
+    std::vector<int> grp(3 * Q, -1);
+    int G = 0;
+    for (int t = 0; t < 3 * Q; ++t) {
+      if (grp[t] >= 0) continue;
+      grp[t] = G;
+      const double* zt0 = &f[((size_t)t * 3 + 2) * 2 * n1];
+      for (int t2 = t + 1; t2 < 3 * Q; ++t2)
+        if (grp[t2] < 0 &&
+            memcmp(zt0, &f[((size_t)t2 * 3 + 2) * 2 * n1], sizeof(double) * 2 * n1) == 0)
+          grp[t2] = G;
+      ++G;
+    }
+    h->G[l] = G;
+    if (e == cudaSuccess) e = dalloc(&h->d_grp[l], grp.size());
+    if (e == cudaSuccess)
+      e = cudaMemcpy(h->d_grp[l], grp.data(), sizeof(int) * grp.size(), cudaMemcpyHostToDevice);
   }
   if (e != cudaSuccess) { delete h; RBWS_FAIL(cudaGetErrorString(e)); }
   *out = h;
@@ -338,7 +359,7 @@ int batch_setup(Batch* b, const double* theta, int count, cudaStream_t stream) {
   e = fine_dinv(b->fine_op(), count, h->d_fzsame, b->lv[L - 1].dinv, stream);
   // coarse levels are matrix-free (Kronecker factors): only 1/diag is stored
   for (int l = 1; l < L - 1 && e == cudaSuccess; ++l)
-    e = coarse_launch(4, h->cells[l], h->Q, h->d_fac[l], h->d_zsame[l], b->theta, count,
+    e = coarse_launch(4, h->coarse_op(l), b->theta, count,
                       nullptr, nullptr, b->lv[l].dinv, 0.0, lc);
   if (e == cudaSuccess)
     e = coarse_factor_kf(h->m0, h->Q, h->d_fac[0], b->theta, count, b->L0, b->d_status, stream);
@@ -403,10 +424,10 @@ int Batch::vcycle(int lvl, const double* bb, double* out, double* dot_partial,
     }
     // coarse levels: the pre-smoothing residual is a residual of the pre-scaled rhs l.u
     if (mode == MODE_PRE)
-      return coarse_launch(1, n, h->Q, h->d_fac[lvl], h->d_zsame[lvl], theta, count, l.u, rhs, y,
+      return coarse_launch(1, h->coarse_op(lvl), theta, count, l.u, rhs, y,
                            omega, lc);
     const int cm = (mode == MODE_JACOBI) ? 2 : (mode == MODE_RESID) ? 1 : 0;
-    return coarse_launch(cm, n, h->Q, h->d_fac[lvl], h->d_zsame[lvl], theta, count, x, rhs, y,
+    return coarse_launch(cm, h->coarse_op(lvl), theta, count, x, rhs, y,
                          omega, lc);
   };
   const int fdot = (fine && dot_partial) ? DOT_BY : DOT_NONE;

@@ -7,6 +7,7 @@
 #include <array>
 #include <vector>
 
+#include "coarse.cuh"
 #include "stencil.cuh"
 
 namespace rbws {
@@ -23,9 +24,17 @@ struct Hierarchy {
   std::vector<double*> d_fac;       // per level 1D Kronecker factors [Q*3][3][2][n+1]
   std::vector<int*> d_zsame;        // per level [n+1]: z factors of plane k == plane k-1
   int* d_fzsame = nullptr;          // finest level [n+1]: same flags for the separable tables
+  std::vector<int*> d_grp;          // per level [3Q]: z-group of every term
+  std::vector<int> G;               // per level: number of z-groups
   std::vector<std::vector<double>> h_fac;
 
   ~Hierarchy();
+  CoarseOp coarse_op(int l) const {
+    CoarseOp o;
+    o.n = cells[l]; o.Q = Q; o.G = G[l];
+    o.fac = d_fac[l]; o.zsame = d_zsame[l]; o.grp = d_grp[l];
+    return o;
+  }
 };
 
 int kron_factors(int n, int m0, int Q, const double* face, const double* node,
