@@ -2,7 +2,8 @@
 
     python build.py            # builds paper_2311_13862_b200/_rbws_b200.so
 
-The .so is git-ignored but travels to the GPU box with the gpurun snapshot.
+Every .cu is compiled to an object in parallel (build/obj), then linked.  The
+.so is git-ignored but travels to the GPU box with the gpurun snapshot.
 """
 
 from __future__ import annotations
@@ -10,23 +11,40 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
 PKG = ROOT / "paper_2311_13862_b200"
 CSRC = PKG / "csrc"
+OBJ = ROOT / "build" / "obj"
 OUT = PKG / "_rbws_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-O3"]
+CFLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+          "-Xcompiler", "-fPIC", "-Xptxas", "-O3"]
 
 
 def sources():
     return sorted(CSRC.glob("*.cu"))
 
 
+def headers():
+    return sorted(CSRC.glob("*.cuh")) + [ROOT / "include/rbws_b200.h"]
+
+
 def deps():
-    return sources() + sorted(CSRC.glob("*.cuh")) + [ROOT / "include/rbws_b200.h"]
+    return sources() + headers()
+
+
+def _compile(src: Path, newest_hdr: float, force: bool, verbose: bool) -> Path:
+    obj = OBJ / (src.stem + ".o")
+    if not force and obj.exists() and obj.stat().st_mtime >= max(newest_hdr, src.stat().st_mtime):
+        return obj
+    cmd = [NVCC, *CFLAGS, "-c", str(src), "-o", str(obj)]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True, cwd=CSRC)
+    return obj
 
 
 def build(force: bool = False, verbose: bool = True) -> Path:
@@ -34,7 +52,12 @@ def build(force: bool = False, verbose: bool = True) -> Path:
         newest = max(p.stat().st_mtime for p in deps())
         if OUT.stat().st_mtime >= newest:
             return OUT
-    cmd = [NVCC, *FLAGS, "-o", str(OUT), *map(str, sources())]
+    OBJ.mkdir(parents=True, exist_ok=True)
+    newest_hdr = max(p.stat().st_mtime for p in headers())
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, newest_hdr, force, verbose), sources()))
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(OUT),
+           *map(str, objs), "-ldl"]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True, cwd=CSRC)

@@ -155,6 +155,40 @@ int rbws_deim_step(int n, const double* W, int64_t Wstride, int N, const double*
 int rbws_dense_solve(int m, const double* A, const double* b, double* x, int* status,
                      void* stream);
 
+/* ---- slab-decomposed single instance (BASELINE configs[4]) ----------------
+ * One large instance of pcg_solve + mg_vcycle (krylov.py:267-334,
+ * multigrid.py:544-571) with every level cut into `nslabs` slabs of whole
+ * z-planes; slab r owns planes [r n_l/nslabs, (r+1) n_l/nslabs) of level l.
+ * Coarse levels with fewer than 8 planes per slab are replicated.  Slabs in
+ * one process exchange halo planes with device copies; across processes (one
+ * per GPU) with NCCL send/recv, and dot-product partials are all-gathered, so
+ * every slab computes bitwise identical PCG scalars.
+ *   nccl_id: (host) 128 bytes from rbws_comm_unique_id on process 0, shared
+ *            by every process (NULL when all slabs live in this process);
+ *   nprocs/proc_rank: processes and this process's rank (slabs are assigned
+ *            in process order: first = proc_rank * nlocal). */
+typedef struct rbws_slab rbws_slab;
+int rbws_comm_unique_id(uint8_t* out128);
+int rbws_slab_create(rbws_slab** out, rbws_hierarchy* h, int nslabs, int nlocal,
+                     const uint8_t* nccl_id, int nprocs, int proc_rank, double omega);
+int rbws_slab_destroy(rbws_slab* s);
+/* distributed levels start at *first_dist_level; owned planes of local slab i */
+int rbws_slab_info(const rbws_slab* s, int* first_dist_level, int local, int* k0, int* k1);
+/* mg_context_for for one parameter: theta (dev or host) [Q] */
+int rbws_slab_setup(rbws_slab* s, const double* theta, int* n_bad, void* stream);
+/* which: 0 = solution x, 1 = rhs f.  Copies the owned planes that fall in global
+ * planes [p0, p0 + planes) from / to `buf` (device or host pointer holding those
+ * planes of one padded instance, n^2 doubles per plane). */
+int rbws_slab_load(rbws_slab* s, int which, const double* buf, int64_t p0, int planes,
+                   void* stream);
+int rbws_slab_store(rbws_slab* s, int which, double* buf, int64_t p0, int planes, void* stream);
+/* x = P ec on the owned planes: a warm start prolonged from a full coarse
+ * solution ec (dev, n/2 cells, one padded instance) */
+int rbws_slab_prolong_x(rbws_slab* s, const double* ec, void* stream);
+/* PCG to delta from the loaded x; outputs (host) as rbws_mgcg_solve for one instance */
+int rbws_slab_solve(rbws_slab* s, double delta, int l_max, int* iters, double* hist,
+                    double* true_res, int* status, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

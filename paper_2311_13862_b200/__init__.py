@@ -14,6 +14,7 @@ from .multigrid import MgContext, mg_context_for, mg_vcycle, mgcg_solve
 from .pipeline import HostPipeline
 from .problems import (ProblemSpec, get_problem, sample_mus, smooth_affine,
                        thermal_block)
+from .slab import SlabSolver, slab_mgcg_solve, slab_partition
 from .rb import (DegenerateBasisError, L1rocModel, deim_extend, l1_indicator,
                  l1roc_offline, l1roc_online)
 from .warmstart import (METHODS, MethodConfig, initial_residual,

@@ -50,6 +50,15 @@ SIGNATURES = {
     "rbws_expand": [_c_int, _c_int, _vp, _c_int64, _c_int, _vp, _vp, _vp],
     "rbws_deim_step": [_c_int, _vp, _c_int64, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "rbws_dense_solve": [_c_int, _vp, _vp, _vp, _vp, _vp],
+    "rbws_comm_unique_id": [_vp],
+    "rbws_slab_create": [_pp, _vp, _c_int, _c_int, _vp, _c_int, _c_int, _c_double],
+    "rbws_slab_destroy": [_vp],
+    "rbws_slab_info": [_vp, _ip, _c_int, _ip, _ip],
+    "rbws_slab_setup": [_vp, _vp, _ip, _vp],
+    "rbws_slab_load": [_vp, _c_int, _vp, _c_int64, _c_int, _vp],
+    "rbws_slab_store": [_vp, _c_int, _vp, _c_int64, _c_int, _vp],
+    "rbws_slab_prolong_x": [_vp, _vp, _vp],
+    "rbws_slab_solve": [_vp, _c_double, _c_int, _ip, _vp, _vp, _ip, _vp],
 }
 _RESTYPES = {"rbws_last_error": ctypes.c_char_p, "rbws_launch_count": ctypes.c_int64}
 

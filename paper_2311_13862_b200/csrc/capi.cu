@@ -3,6 +3,7 @@
 #include "coarse.cuh"
 #include "fine.cuh"
 #include "l1roc.cuh"
+#include "slab.cuh"
 #include "solver.cuh"
 
 const char* rbws_get_error();
@@ -263,6 +264,79 @@ int rbws_dense_solve(int m, const double* A, const double* b, double* x, int* st
   if (m < 1) RBWS_FAIL("empty system");
   RBWS_CHECK(rbws::dense_solve(m, A, b, x, status, S(stream)));
   return 0;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int rbws_comm_unique_id(uint8_t* out128) {
+  if (!out128) RBWS_FAIL("null argument");
+  return rbws::comm_unique_id(out128);
+}
+
+int rbws_slab_create(rbws_slab** out, rbws_hierarchy* h, int nslabs, int nlocal,
+                     const uint8_t* nccl_id, int nprocs, int proc_rank, double omega) {
+  if (!out || !h) RBWS_FAIL("null argument");
+  rbws::Comm* comm = nullptr;
+  if (nprocs > 1) {
+    if (!nccl_id) RBWS_FAIL("multi-process slabs need an NCCL id");
+    if (rbws::comm_create(&comm, nccl_id, nprocs, proc_rank)) return 1;
+  } else if (nprocs != 1 || proc_rank != 0) {
+    RBWS_FAIL("bad process count / rank");
+  }
+  rbws::Slab* s = nullptr;
+  if (rbws::slab_create(&s, H(h), nslabs, proc_rank * nlocal, nlocal, comm, omega)) {
+    delete comm;
+    return 1;
+  }
+  *out = reinterpret_cast<rbws_slab*>(s);
+  return 0;
+}
+
+int rbws_slab_destroy(rbws_slab* s) {
+  delete reinterpret_cast<rbws::Slab*>(s);
+  return 0;
+}
+
+int rbws_slab_info(const rbws_slab* s, int* first_dist_level, int local, int* k0, int* k1) {
+  const rbws::Slab* sl = reinterpret_cast<const rbws::Slab*>(s);
+  if (!sl) RBWS_FAIL("null slab");
+  if (first_dist_level) *first_dist_level = sl->Ld;
+  if (local < 0 || local >= sl->nloc) RBWS_FAIL("local slab index out of range");
+  if (k0) *k0 = sl->parts[local].k0[sl->L - 1];
+  if (k1) *k1 = sl->parts[local].k1[sl->L - 1];
+  return 0;
+}
+
+int rbws_slab_setup(rbws_slab* s, const double* theta, int* n_bad, void* stream) {
+  if (!s || !theta) RBWS_FAIL("null argument");
+  return rbws::slab_setup(reinterpret_cast<rbws::Slab*>(s), theta, n_bad, S(stream));
+}
+
+int rbws_slab_load(rbws_slab* s, int which, const double* buf, int64_t p0, int planes,
+                   void* stream) {
+  if (!s || !buf) RBWS_FAIL("null argument");
+  return rbws::slab_load(reinterpret_cast<rbws::Slab*>(s), which ? rbws::SV_F : rbws::SV_X, buf,
+                         p0, planes, S(stream));
+}
+
+int rbws_slab_store(rbws_slab* s, int which, double* buf, int64_t p0, int planes, void* stream) {
+  if (!s || !buf) RBWS_FAIL("null argument");
+  return rbws::slab_store(reinterpret_cast<rbws::Slab*>(s), which ? rbws::SV_F : rbws::SV_X, buf,
+                          p0, planes, S(stream));
+}
+
+int rbws_slab_prolong_x(rbws_slab* s, const double* ec, void* stream) {
+  if (!s || !ec) RBWS_FAIL("null argument");
+  return rbws::slab_prolong_x(reinterpret_cast<rbws::Slab*>(s), ec, S(stream));
+}
+
+int rbws_slab_solve(rbws_slab* s, double delta, int l_max, int* iters, double* hist,
+                    double* true_res, int* status, void* stream) {
+  if (!s) RBWS_FAIL("null slab");
+  return rbws::slab_solve(reinterpret_cast<rbws::Slab*>(s), delta, l_max, iters, hist, true_res,
+                          status, S(stream));
 }
 
 }  // extern "C"

@@ -24,7 +24,7 @@ namespace rbws {
 constexpr int kCStages = 8;
 constexpr int kCMaxPlanes = 260;  // z-factor flag table bound (planes per z-chunk + 2)
 
-CoarseGeom coarse_geom(int n, int batch) {
+CoarseGeom coarse_geom(int n, int batch, int nz) {
   CoarseGeom g;
   int ty = 256 / n;
   if (ty < 1) ty = 1;
@@ -32,8 +32,10 @@ CoarseGeom coarse_geom(int n, int batch) {
   g.ty = ty;
   g.threads = ty * n;
   g.ytiles = n / ty;
+  if (nz <= 0) nz = n;
   g.zc = 1;
-  while ((int64_t)g.ytiles * batch * g.zc < 2 * 148 && n / (g.zc * 2) >= 8) g.zc *= 2;
+  while ((int64_t)g.ytiles * batch * g.zc < 2 * 148 && nz / (g.zc * 2) >= 8) g.zc *= 2;
+  g.kz = (nz + g.zc - 1) / g.zc;
   return g;
 }
 
@@ -49,6 +51,7 @@ struct CoarseArgs {
   double* y;
   const int* active;
   double omega;
+  int zlo, zhi;  // output planes [zlo, zhi) (global plane indices, virtual base pointers)
 };
 
 enum CoarseMode : int { CM_APPLY = 0, CM_RESID = 1, CM_JACOBI = 2, CM_PRE = 3, CM_DINV = 4 };
@@ -74,8 +77,9 @@ __global__ void __launch_bounds__(256) coarse_kernel(CoarseArgs a) {
   const int tid = threadIdx.x;
   const int64_t n2 = (int64_t)n * n;
   const int64_t base = (int64_t)mu * n2 * n;
-  const int kz = n / zc;
-  const int kb = max(1, kc * kz), ke = min(n, (kc + 1) * kz);
+  const int kz = a.g.kz;
+  const int kb = max(1, a.zlo + kc * kz), ke = min(min(n, a.zhi), a.zlo + (kc + 1) * kz);
+  if (kb >= ke) return;
   const int p_first = kb - 1, p_last = ke;
   const int np = p_last - p_first + 1;
 
@@ -249,8 +253,9 @@ __global__ void __launch_bounds__(256, 2) coarse_kron_kernel(CoarseArgs a) {
   const int tid = threadIdx.x;
   const int64_t n2 = (int64_t)n * n;
   const int64_t base = (int64_t)mu * n2 * n;
-  const int kz = n / zc;
-  const int kb = max(1, kc * kz), ke = min(n, (kc + 1) * kz);
+  const int kz = a.g.kz;
+  const int kb = max(1, a.zlo + kc * kz), ke = min(min(n, a.zhi), a.zlo + (kc + 1) * kz);
+  if (kb >= ke) return;
   const int p_first = kb - 1, p_last = ke;
   const int np = p_last - p_first + 1;
 
@@ -416,8 +421,8 @@ template <int G, int MODE>
 static cudaError_t coarse_kron_launch_m(CoarseArgs a, int batch, cudaStream_t stream) {
   constexpr int NH = (MODE == CM_DINV) ? 0 : 1;
   constexpr int NC = (MODE == CM_RESID || MODE == CM_JACOBI) ? 1 : 0;
-  a.g = coarse_geom(a.n, batch);
-  const int np = a.n / a.g.zc + 2;
+  a.g = coarse_geom(a.n, batch, a.zhi - a.zlo);
+  const int np = a.g.kz + 2;
   if (np > kCMaxPlanes) return cudaErrorInvalidValue;
   const size_t smem = 64 + 4 * kCMaxPlanes + 8 * (((size_t)np * G * 3 + 1) & ~(size_t)1) +
                       (size_t)kCStages * (NH * ((a.g.ty + 2) * a.n + 2) + NC * a.g.ty * a.n) * 8;
@@ -450,8 +455,8 @@ template <int Q, int MODE>
 static cudaError_t coarse_launch_m(CoarseArgs a, int batch, cudaStream_t stream) {
   constexpr int NH = (MODE == CM_DINV) ? 0 : 1;
   constexpr int NC = (MODE == CM_RESID || MODE == CM_JACOBI) ? 1 : 0;
-  a.g = coarse_geom(a.n, batch);
-  if (a.n / a.g.zc + 2 > kCMaxPlanes) return cudaErrorInvalidValue;
+  a.g = coarse_geom(a.n, batch, a.zhi - a.zlo);
+  if (a.g.kz + 2 > kCMaxPlanes) return cudaErrorInvalidValue;
   const size_t smem = 64 + 4 * kCMaxPlanes + 64 +
                       (size_t)kCStages * (NH * ((a.g.ty + 2) * a.n + 2) + NC * a.g.ty * a.n) * 8;
   static size_t attr = 48 * 1024;
@@ -495,6 +500,8 @@ cudaError_t coarse_launch(int mode, const CoarseOp& op, const double* theta, int
   a.y = y;
   a.active = lc.active;
   a.omega = omega;
+  a.zlo = lc.zhi > 0 ? lc.zlo : 0;
+  a.zhi = lc.zhi > 0 ? lc.zhi : n;
   switch (op.G) {  // few z-groups: grouped Kronecker kernel
     case 1: return coarse_kron_launch_g<1>(mode, a, batch, lc.stream);
     case 2: return coarse_kron_launch_g<2>(mode, a, batch, lc.stream);

@@ -6,9 +6,9 @@
 namespace rbws {
 
 struct CoarseGeom {
-  int ty, threads, ytiles, zc;
+  int ty, threads, ytiles, zc, kz;
 };
-CoarseGeom coarse_geom(int n, int batch);
+CoarseGeom coarse_geom(int n, int batch, int nz = 0);
 
 // One coarse level's matrix-free operator description.
 //   fac:   the level's Kronecker factors [Q*3][3][2][n+1]

@@ -23,7 +23,7 @@ namespace rbws {
 
 constexpr int kStages = 8;  // ring slots (power of two)
 constexpr int kMaxKz = 64;  // planes per z-chunk (bounds the z-factor table)
-constexpr int kThreads = 256;  // threads per CTA (one per grid column of the tile)
+constexpr int kThreads = 256;  // threads per CTA (one per grid column of the tile; N = 512: 512)
 
 // Compile-time tile geometry for a grid with N cells per axis: RPP rows per pass
 // of the CTA, NPT rows per thread, TY = RPP*NPT rows per tile.  All shared-memory
@@ -31,7 +31,7 @@ constexpr int kThreads = 256;  // threads per CTA (one per grid column of the ti
 // is one LDS with an immediate offset from a per-plane base register.
 template <int N>
 struct FT {
-  static constexpr int RPP = (kThreads / N) < N ? kThreads / N : N;
+  static constexpr int RPP = (kThreads / N) < 1 ? 1 : ((kThreads / N) < N ? kThreads / N : N);
   static constexpr int NPT = (RPP * 2 <= N) ? 2 : 1;
   static constexpr int TY = RPP * NPT;
   static constexpr int THREADS = RPP * N;
@@ -39,7 +39,7 @@ struct FT {
   static constexpr int CSZ = TY * N;        // doubles per staged array, tile rows only
 };
 
-FineGeom fine_geom(int n, int batch) {
+FineGeom fine_geom(int n, int batch, int nz) {
   FineGeom g;
   int rpp = kThreads / n;
   if (rpp < 1) rpp = 1;
@@ -49,9 +49,11 @@ FineGeom fine_geom(int n, int batch) {
   g.ty = rpp * g.npt;
   g.threads = rpp * n;
   g.ytiles = n / g.ty;
+  if (nz <= 0) nz = n;
   g.zc = 1;
-  while (n / g.zc > kMaxKz) g.zc *= 2;
-  while ((int64_t)g.ytiles * batch * g.zc < 2 * 148 && (n / (g.zc * 2)) >= 8) g.zc *= 2;
+  while ((nz + g.zc - 1) / g.zc > kMaxKz) g.zc *= 2;
+  while ((int64_t)g.ytiles * batch * g.zc < 2 * 148 && (nz / (g.zc * 2)) >= 8) g.zc *= 2;
+  g.kz = (nz + g.zc - 1) / g.zc;
   g.tiles = g.ytiles * g.zc;
   return g;
 }
@@ -70,6 +72,7 @@ struct FineArgs {
   double* partial;
   const int* active;
   double omega;
+  int zlo, zhi;   // output planes [zlo, zhi) (global plane indices, virtual base pointers)
   int c0_shared;  // c0 is one instance shared by the whole batch (e.g. the rhs f)
   const double* ec;  // FM_POSTP: coarse-grid correction (n/2 cells, padded batch layout)
 };
@@ -84,15 +87,16 @@ enum FineMode : int {
   FM_POSTP = 6,   // h0 = b, h1 = dinv, ec   u = w dinv b + P ec; out0 = u + w (b - A u)/d, dot b.out
 };
 
-template <int MODE>
+template <int MODE, int N>
 struct SL {
   // PRE / PAPPLY stencil a derived vector (w dinv b, s + beta p_old): each staged
   // plane is transformed once into a second ring, so neighbours cost one LDS
   static constexpr bool XF = (MODE == FM_PRE || MODE == FM_PAPPLY || MODE == FM_POSTP);
   static constexpr int NH = XF ? 2 : 1;
   static constexpr int NC = (MODE == FM_CG) ? 2 : ((MODE == FM_RESID || MODE == FM_JACOBI) ? 1 : 0);
-  static constexpr int S = XF ? 6 : kStages;  // raw ring slots
-  static constexpr int U = 6;                 // transformed-plane ring slots (XF)
+  // raw / transformed ring slots (N = 512 rows are 4 KB: shallower rings fit 227 KB)
+  static constexpr int S = XF ? (N >= 512 ? 4 : 6) : (N >= 512 ? 6 : kStages);
+  static constexpr int U = N >= 512 ? 4 : 6;
 };
 
 // FM_POSTP stages, with every even fine plane p, coarse plane p/2 + 1 rows
@@ -106,18 +110,18 @@ struct FCoarse {
 
 template <int N, int MODE>
 struct FSmem {
-  static constexpr int STAGE = SL<MODE>::NH * FT<N>::HSZ + SL<MODE>::NC * FT<N>::CSZ +
+  static constexpr int STAGE = SL<MODE, N>::NH * FT<N>::HSZ + SL<MODE, N>::NC * FT<N>::CSZ +
                                (MODE == FM_POSTP ? FCoarse<N>::CSZ : 0);
-  static constexpr int RING = SL<MODE>::S * STAGE + (SL<MODE>::XF ? SL<MODE>::U * FT<N>::HSZ : 0);
+  static constexpr int RING = SL<MODE, N>::S * STAGE + (SL<MODE, N>::XF ? SL<MODE, N>::U * FT<N>::HSZ : 0);
   static size_t bytes(int np, int Q) {
     return 64 + 4 * (kMaxKz + 4) + 8 * (((size_t)np * 3 * Q + 1) & ~(size_t)1) + 8 * (size_t)RING;
   }
 };
 
 template <int MODE, int N>
-__global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
+__global__ void __launch_bounds__(FT<N>::THREADS) fine_kernel(FineArgs a) {
   using G = FT<N>;
-  using L = SL<MODE>;
+  using L = SL<MODE, N>;
   constexpr bool XF = L::XF;
   constexpr int NH = L::NH, NC = L::NC, S = L::S, U = L::U;
   constexpr int NPT = G::NPT, RPP = G::RPP, TY = G::TY;
@@ -134,8 +138,12 @@ __global__ void __launch_bounds__(kThreads) fine_kernel(FineArgs a) {
   const int j0 = yt * TY;
   const int tid = threadIdx.x;
   const int64_t base = (int64_t)mu * N2 * N;
-  const int kz = N / zc;
-  const int kb = max(1, kc * kz), ke = min(N, (kc + 1) * kz);
+  const int kz = a.g.kz;
+  const int kb = max(1, a.zlo + kc * kz), ke = min(min(N, a.zhi), a.zlo + (kc + 1) * kz);
+  if (kb >= ke) {  // empty chunk (never for the geometries fine_geom builds)
+    if (a.dot != DOT_NONE && tid == 0) a.partial[(int64_t)mu * a.g.tiles + yt * zc + kc] = 0.0;
+    return;
+  }
   const int p_first = kb - 1, p_last = ke;  // staged planes (inclusive)
   const int np = p_last - p_first + 1;
 
@@ -464,9 +472,9 @@ template <int MODE, int N>
 static cudaError_t fine_launch_mn(const FineArgs& a, int batch, cudaStream_t stream) {
   using G = FT<N>;
   if (a.g.threads != G::THREADS || a.g.ty != G::TY) return cudaErrorInvalidValue;
-  const int np = N / a.g.zc + 2;
+  const int np = a.g.kz + 2;
   const size_t smem = FSmem<N, MODE>::bytes(np, a.op.Q);
-  if (smem > 220 * 1024) return cudaErrorInvalidValue;
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
   static size_t attr = 48 * 1024;
   if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(fine_kernel<MODE, N>,
@@ -489,13 +497,15 @@ static cudaError_t fine_launch_m(const FineArgs& a, int batch, cudaStream_t stre
     case 64: return fine_launch_mn<MODE, 64>(a, batch, stream);
     case 128: return fine_launch_mn<MODE, 128>(a, batch, stream);
     case 256: return fine_launch_mn<MODE, 256>(a, batch, stream);
+    case 512: return fine_launch_mn<MODE, 512>(a, batch, stream);
     default: return cudaErrorInvalidValue;
   }
 }
 
 static cudaError_t fine_launch(int mode, FineArgs& a, int batch, cudaStream_t stream) {
   if (a.op.Q < 1 || a.op.Q > kMaxTerms) return cudaErrorInvalidValue;
-  a.g = fine_geom(a.op.n, batch);
+  if (a.zhi <= 0) { a.zlo = 0; a.zhi = a.op.n; }
+  a.g = fine_geom(a.op.n, batch, a.zhi - a.zlo);
   switch (mode) {
     case FM_APPLY: return fine_launch_m<FM_APPLY>(a, batch, stream);
     case FM_RESID: return fine_launch_m<FM_RESID>(a, batch, stream);
@@ -511,12 +521,13 @@ static cudaError_t fine_launch(int mode, FineArgs& a, int batch, cudaStream_t st
 // 1/diag of the finest operator for every instance (batch setup); weights are
 // recomputed only on planes whose z factors change (host-built flags)
 template <int Q>
-__global__ void __launch_bounds__(256) fine_dinv_kernel(Sep7 op, FineGeom g, const int* zsame,
-                                                       double* __restrict__ dinv) {
+__global__ void __launch_bounds__(512) fine_dinv_kernel(Sep7 op, FineGeom g, const int* zsame,
+                                                       double* __restrict__ dinv, int zlo,
+                                                       int zhi) {
   const int n = op.n, n1 = n + 1;
   const int kc = blockIdx.z % g.zc, mu = blockIdx.z / g.zc;
-  const int kz = n / g.zc;
-  const int kb = max(1, kc * kz), ke = min(n, (kc + 1) * kz);
+  const int kz = g.kz;
+  const int kb = max(1, zlo + kc * kz), ke = min(min(n, zhi), zlo + (kc + 1) * kz);
   const int i = threadIdx.x % n;
   const int64_t n2 = (int64_t)n * n, base = (int64_t)mu * n2 * n;
   const double* th = op.theta + (size_t)mu * Q;
@@ -546,12 +557,13 @@ __global__ void __launch_bounds__(256) fine_dinv_kernel(Sep7 op, FineGeom g, con
 }
 
 cudaError_t fine_dinv(const Sep7& op, int batch, const int* zsame, double* dinv,
-                      cudaStream_t stream) {
-  const FineGeom g = fine_geom(op.n, batch);
+                      cudaStream_t stream, int zlo, int zhi) {
+  if (zhi <= 0) { zlo = 0; zhi = op.n; }
+  const FineGeom g = fine_geom(op.n, batch, zhi - zlo);
   dim3 grd(1, g.ytiles, batch * g.zc);
   count_launch();
 #define RBWS_DQ(QQ) \
-  case QQ: fine_dinv_kernel<QQ><<<grd, g.threads, 0, stream>>>(op, g, zsame, dinv); break;
+  case QQ: fine_dinv_kernel<QQ><<<grd, g.threads, 0, stream>>>(op, g, zsame, dinv, zlo, zhi); break;
   switch (op.Q) {
     RBWS_DQ(1) RBWS_DQ(2) RBWS_DQ(3) RBWS_DQ(4) RBWS_DQ(5) RBWS_DQ(6) RBWS_DQ(7) RBWS_DQ(8)
     default: return cudaErrorInvalidValue;
@@ -568,6 +580,8 @@ static FineArgs base_args(const Sep7& op, int dot, double* partial, const Launch
   a.partial = partial;
   a.active = lc.active;
   a.omega = omega;
+  a.zlo = lc.zlo;
+  a.zhi = lc.zhi;
   return a;
 }
 

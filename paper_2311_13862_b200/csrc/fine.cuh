@@ -12,9 +12,11 @@ struct FineGeom {
   int ty;       // rows per tile = rpp * npt
   int ytiles;   // tiles per plane
   int zc;       // z-chunks per instance
+  int kz;       // planes per z-chunk
   int tiles;    // partial-sum slots per instance = ytiles * zc
 };
-FineGeom fine_geom(int n, int batch);
+// nz: planes per instance processed (0 = n; slabs pass their owned plane count)
+FineGeom fine_geom(int n, int batch, int nz = 0);
 
 // y = A x (y may be null), partial (may be null) = x . A x
 cudaError_t fine_apply(const Sep7& op, int batch, const double* x, double* y, double* partial,
@@ -24,7 +26,7 @@ cudaError_t fine_resid(const Sep7& op, int batch, const double* x, const double*
                        double* partial, const LaunchCtx& lc, bool b_shared = false);
 // dinv = 1/diag(A(mu)) (batch setup); zsame: per-plane "z factors unchanged" flags
 cudaError_t fine_dinv(const Sep7& op, int batch, const int* zsame, double* dinv,
-                      cudaStream_t stream);
+                      cudaStream_t stream, int zlo = 0, int zhi = 0);
 // y = x + omega (b - A x)/diag, partial (may be null) = b . y
 cudaError_t fine_jacobi(const Sep7& op, int batch, const double* x, const double* b, double* y,
                         double omega, double* partial, const LaunchCtx& lc);

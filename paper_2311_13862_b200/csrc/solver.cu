@@ -285,16 +285,17 @@ Sep7 Batch::fine_op() const {
   return op;
 }
 
-int batch_create(Batch** out, Hierarchy* h, int cap, int nu, double omega) {
+int batch_create(Batch** out, Hierarchy* h, int cap, int nu, double omega, int maxl) {
   if (cap < 1) RBWS_FAIL("batch capacity must be positive");
   if (nu < 0) RBWS_FAIL("smoothing count must be non-negative");
   if (nu == 0) RBWS_FAIL("nu = 0 (no smoothing) is not supported by the batched V-cycle");
   Batch* b = new Batch();
   b->h = h; b->cap = cap; b->nu = nu; b->omega = omega;
   const int L = h->levels;
+  b->maxl = (maxl <= 0 || maxl > L) ? L : maxl;
   cudaError_t e = dalloc(&b->theta, (size_t)cap * h->Q);
   b->lv.resize(L);
-  for (int l = 0; l < L && e == cudaSuccess; ++l) {
+  for (int l = 0; l < b->maxl && e == cudaSuccess; ++l) {
     LevelBuf& lb = b->lv[l];
     lb.n = h->cells[l];
     const size_t V = (size_t)vec_doubles(lb.n, cap);
@@ -321,6 +322,7 @@ int batch_create(Batch** out, Hierarchy* h, int cap, int nu, double omega) {
   const size_t VF = (size_t)vec_doubles(h->n, cap);
   if (e == cudaSuccess) e = dalloc(&b->d_status, cap);
   for (double** pp : {&b->r, &b->p, &b->p2, &b->s, &b->t_res}) {
+    if (b->maxl < L) break;  // coarse levels only (slab path): no finest-level PCG vectors
     if (e == cudaSuccess) e = dalloc(pp, VF);
     if (e == cudaSuccess) e = cudaMemset(*pp, 0, VF * sizeof(double));
   }
@@ -356,9 +358,9 @@ int batch_setup(Batch* b, const double* theta, int count, cudaStream_t stream) {
   const int L = h->levels;
   LaunchCtx lc{stream, nullptr};
   // fine level 1/diag
-  e = fine_dinv(b->fine_op(), count, h->d_fzsame, b->lv[L - 1].dinv, stream);
+  if (b->maxl == L) e = fine_dinv(b->fine_op(), count, h->d_fzsame, b->lv[L - 1].dinv, stream);
   // coarse levels are matrix-free (Kronecker factors): only 1/diag is stored
-  for (int l = 1; l < L - 1 && e == cudaSuccess; ++l)
+  for (int l = 1; l < std::min(L - 1, b->maxl) && e == cudaSuccess; ++l)
     e = coarse_launch(4, h->coarse_op(l), b->theta, count,
                       nullptr, nullptr, b->lv[l].dinv, 0.0, lc);
   if (e == cudaSuccess)
@@ -586,6 +588,50 @@ __global__ void pcg_true_kernel(int count, const double* prr, int tiles, const d
 }
 
 static inline dim3 warp_grid(int count) { return dim3((count + 7) / 8); }
+
+// host launchers of the per-instance PCG scalar kernels (shared with slab.cu)
+cudaError_t pcg_init(int count, const double* pf, int ftiles, int fshared, const double* prr,
+                     int tiles, double delta, int l_max, double* scale, double* hist,
+                     int hist_len, int* active, int* iters, int* status, int* nactive,
+                     cudaStream_t s) {
+  count_launch();
+  pcg_init_kernel<<<warp_grid(count), 256, 0, s>>>(count, pf, ftiles, fshared, prr, tiles, delta,
+                                                   l_max, scale, hist, hist_len, active, iters,
+                                                   status, nactive);
+  return cudaGetLastError();
+}
+cudaError_t pcg_rs(int count, const double* prs, int tiles, double* rs, const int* active,
+                   cudaStream_t s) {
+  count_launch();
+  pcg_rs_kernel<<<warp_grid(count), 256, 0, s>>>(count, prs, tiles, rs, active);
+  return cudaGetLastError();
+}
+cudaError_t pcg_alpha(int count, const double* ppap, int tiles, const double* rs, double* alpha,
+                      int* active, int* status, cudaStream_t s) {
+  count_launch();
+  pcg_alpha_kernel<<<warp_grid(count), 256, 0, s>>>(count, ppap, tiles, rs, alpha, active, status);
+  return cudaGetLastError();
+}
+cudaError_t pcg_check(int count, const double* prr, int tiles, const double* scale, double delta,
+                      int l_max, double* hist, int hist_len, int* active, int* iters,
+                      int* nactive, cudaStream_t s) {
+  count_launch();
+  pcg_check_kernel<<<warp_grid(count), 256, 0, s>>>(count, prr, tiles, scale, delta, l_max, hist,
+                                                    hist_len, active, iters, nactive);
+  return cudaGetLastError();
+}
+cudaError_t pcg_beta(int count, const double* prs, int tiles, double* rs, double* beta,
+                     const int* active, cudaStream_t s) {
+  count_launch();
+  pcg_beta_kernel<<<warp_grid(count), 256, 0, s>>>(count, prs, tiles, rs, beta, active);
+  return cudaGetLastError();
+}
+cudaError_t pcg_true(int count, const double* prr, int tiles, const double* scale, double* out,
+                     cudaStream_t s) {
+  count_launch();
+  pcg_true_kernel<<<warp_grid(count), 256, 0, s>>>(count, prr, tiles, scale, out);
+  return cudaGetLastError();
+}
 
 int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double delta, int l_max,
               const PcgOut& out, cudaStream_t stream) {

@@ -72,6 +72,7 @@ enum ProfClass : int {
 struct Batch {
   Hierarchy* h = nullptr;
   int cap = 0, count = 0, nu = 1;
+  int maxl = 0;                     // levels with buffers (< levels: coarse-only, slab path)
   double omega = 0.7;
   double* theta = nullptr;          // [cap][Q]
   std::vector<LevelBuf> lv;
@@ -105,7 +106,8 @@ struct Batch {
   int vcycle(int lvl, const double* b, double* out, double* dot_partial, const LaunchCtx& lc);
 };
 
-int batch_create(Batch** out, Hierarchy* h, int cap, int nu, double omega);
+// maxl: allocate levels 0..maxl-1 only (0 = all; the slab path's replicated coarse levels)
+int batch_create(Batch** out, Hierarchy* h, int cap, int nu, double omega, int maxl = 0);
 int batch_setup(Batch* b, const double* theta, int count, cudaStream_t stream);
 
 struct PcgOut {
@@ -114,6 +116,23 @@ struct PcgOut {
   double* true_res;    // host [count]
   int* status;         // host [count]: 0 ok, 1 breakdown (non-SPD), 2 not converged
 };
+
+// per-instance PCG scalar kernels (one warp per instance; partials summed in fixed order)
+cudaError_t pcg_init(int count, const double* pf, int ftiles, int fshared, const double* prr,
+                     int tiles, double delta, int l_max, double* scale, double* hist,
+                     int hist_len, int* active, int* iters, int* status, int* nactive,
+                     cudaStream_t s);
+cudaError_t pcg_rs(int count, const double* prs, int tiles, double* rs, const int* active,
+                   cudaStream_t s);
+cudaError_t pcg_alpha(int count, const double* ppap, int tiles, const double* rs, double* alpha,
+                      int* active, int* status, cudaStream_t s);
+cudaError_t pcg_check(int count, const double* prr, int tiles, const double* scale, double delta,
+                      int l_max, double* hist, int hist_len, int* active, int* iters,
+                      int* nactive, cudaStream_t s);
+cudaError_t pcg_beta(int count, const double* prs, int tiles, double* rs, double* beta,
+                     const int* active, cudaStream_t s);
+cudaError_t pcg_true(int count, const double* prr, int tiles, const double* scale, double* out,
+                     cudaStream_t s);
 
 int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double delta, int l_max,
               const PcgOut& out, cudaStream_t stream);

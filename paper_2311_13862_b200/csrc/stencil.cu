@@ -412,13 +412,14 @@ __global__ void __launch_bounds__(256) restrict_kernel(int nf, const double* __r
                                                        double* __restrict__ bc,
                                                        const int* __restrict__ active,
                                                        const double* __restrict__ dinv_c,
-                                                       double* __restrict__ uc, double omega) {
+                                                       double* __restrict__ uc, double omega,
+                                                       int64_t x0, int64_t x1) {
   const int nc = nf / 2;
   const int mu = blockIdx.y;
   if (active && !active[mu]) return;
   const int64_t nc3 = (int64_t)nc * nc * nc, nf3 = (int64_t)nf * nf * nf;
-  const int64_t X = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (X >= nc3) return;
+  const int64_t X = x0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // coarse node
+  if (X >= x1) return;
   const int I = X % nc, J = (X / nc) % nc, K = X / ((int64_t)nc * nc);
   if (I == 0 || J == 0 || K == 0) return;
   const double* r = rf + (int64_t)mu * nf3;
@@ -444,23 +445,26 @@ __global__ void __launch_bounds__(256) restrict_kernel(int nf, const double* __r
 cudaError_t restrict_launch(int nf, int batch, const double* rf, double* bc, const LaunchCtx& lc,
                             const double* dinv_c, double* uc, double omega) {
   const int nc = nf / 2;
-  const int64_t nc3 = (int64_t)nc * nc * nc;
-  dim3 blk(256), grd((unsigned)((nc3 + 255) / 256), batch);
+  const int64_t nc2 = (int64_t)nc * nc;
+  // coarse planes [zlo, zhi) (slab path) or the whole level
+  const int64_t x0 = lc.zhi > 0 ? lc.zlo * nc2 : 0, x1 = lc.zhi > 0 ? lc.zhi * nc2 : nc2 * nc;
+  dim3 blk(256), grd((unsigned)((x1 - x0 + 255) / 256), batch);
   count_launch();
-  restrict_kernel<<<grd, blk, 0, lc.stream>>>(nf, rf, bc, lc.active, dinv_c, uc, omega);
+  restrict_kernel<<<grd, blk, 0, lc.stream>>>(nf, rf, bc, lc.active, dinv_c, uc, omega, x0, x1);
   return cudaGetLastError();
 }
 
 // z-marching trilinear prolongation: one thread per fine column (i, j); the
 // xy-interpolated coarse values of the two bracketing coarse planes are kept in
 // registers, so each fine node costs one coarse gather per two fine planes.
-__global__ void __launch_bounds__(256) prolong_kernel(int nf, int mode, int ty, int zc,
+__global__ void __launch_bounds__(512) prolong_kernel(int nf, int mode, int ty, int zc,
                                                       const double* __restrict__ ec,
                                                       double* __restrict__ u,
                                                       const double* __restrict__ b,
                                                       const double* __restrict__ dinv,
                                                       double omega,
-                                                      const int* __restrict__ active) {
+                                                      const int* __restrict__ active, int zlo,
+                                                      int zhi) {
   const int nc = nf / 2;
   const int mu = blockIdx.z / zc, kc = blockIdx.z % zc;
   if (active && !active[mu]) return;
@@ -478,8 +482,9 @@ __global__ void __launch_bounds__(256) prolong_kernel(int nf, int mode, int ty, 
     const double r1 = oi ? 0.5 * (__ldg(q1) + __ldg(q1 + 1)) : __ldg(q1);
     return 0.5 * (r0 + r1);
   };
-  const int kz = nf / zc;
-  const int kb = max(1, kc * kz), ke = min(nf, (kc + 1) * kz);
+  const int kz = (zhi - zlo + zc - 1) / zc;
+  const int kb = max(1, zlo + kc * kz), ke = min(min(nf, zhi), zlo + (kc + 1) * kz);
+  if (kb >= ke) return;
   int Kc = kb >> 1;
   double v0 = vxy(Kc), v1 = vxy(Kc + 1);
   const int64_t col = (int64_t)mu * nf2 * nf + i + (int64_t)nf * j;
@@ -505,12 +510,13 @@ cudaError_t prolong_launch(int nf, int batch, int mode, const double* ec, double
   if (ty < 1) ty = 1;
   if (ty > nf) ty = nf;
   const int threads = ty * nf;
+  const int zlo = lc.zhi > 0 ? lc.zlo : 0, zhi = lc.zhi > 0 ? lc.zhi : nf;
   int zc = 1;
-  while ((int64_t)(nf / ty) * batch * zc < 4 * 148 && nf / (zc * 2) >= 4) zc *= 2;
+  while ((int64_t)(nf / ty) * batch * zc < 4 * 148 && (zhi - zlo) / (zc * 2) >= 4) zc *= 2;
   dim3 grd(1, nf / ty, batch * zc);
   count_launch();
   prolong_kernel<<<grd, threads, 0, lc.stream>>>(nf, mode, ty, zc, ec, u, b, dinv, omega,
-                                                 lc.active);
+                                                 lc.active, zlo, zhi);
   return cudaGetLastError();
 }
 
@@ -686,6 +692,14 @@ __global__ void __launch_bounds__(256) dot_kernel(int64_t n3, const double* __re
   }
   const double s = block_reduce_sum(acc, red);
   if (threadIdx.x == 0) partial[(int64_t)mu * gridDim.x + blockIdx.x] = s;
+}
+
+cudaError_t vec_dot_range(int64_t count, const double* x, const double* y, double* partial,
+                          cudaStream_t stream) {
+  dim3 blk(256), grd((unsigned)((count + 2047) / 2048), 1);
+  count_launch();
+  dot_kernel<<<grd, blk, 0, stream>>>(count, x, 0, y, 0, partial, nullptr);
+  return cudaGetLastError();
 }
 
 cudaError_t vec_dot(int n, int batch, const double* x, int64_t x_stride, const double* y,

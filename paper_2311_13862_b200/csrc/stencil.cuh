@@ -18,6 +18,10 @@ enum DotMode : int { DOT_NONE = 0, DOT_XAX = 1, DOT_BY = 2, DOT_YY = 3 };
 struct LaunchCtx {
   cudaStream_t stream;
   const int* active;  // per-instance flag (nullptr = all active)
+  // z-range of output planes [zlo, zhi) of every instance (0, 0 = the whole grid).  The slab
+  // path (slab.cu) passes its owned planes with "virtual" base pointers: a pointer v such
+  // that v + k*n^2 is global plane k, valid for the planes a kernel touches (zlo-1 .. zhi).
+  int zlo = 0, zhi = 0;
 };
 
 // ---- finest level (separable 7-point) -----------------------------------
@@ -67,6 +71,9 @@ cudaError_t vec_scale_dinv(int n, int batch, double omega, const double* dinv, c
                            double* u, cudaStream_t stream);
 cudaError_t vec_dot(int n, int batch, const double* x, int64_t x_stride, const double* y,
                     int64_t y_stride, double* partial, const LaunchCtx& lc);
+// partial[t] = sum x*y over `count` contiguous doubles, (count + 2047)/2048 tiles
+cudaError_t vec_dot_range(int64_t count, const double* x, const double* y, double* partial,
+                          cudaStream_t stream);
 // y = a*x + beta[mu]*y   (beta may be null -> 0);  ghosts untouched (they are 0)
 cudaError_t vec_xpby(int n, int batch, const double* x, const double* beta, double* y,
                      const LaunchCtx& lc);
