@@ -46,6 +46,11 @@ CONFIGS = {
     3: dict(workload="smooth affine (6 modes), 256^3 cells, r=40 from 2048 train, batch 128, tol 1e-12",
             kind="smooth", blocks=None, n=256, m0=4, r=40, n_train=2048, batch=128, delta=1e-12,
             chunk=64, e2e_sub=32),
+    4: dict(workload="thermal-block 2x2x2, 512^3 cells, one instance slab-decomposed along z "
+                     "(one slab per GPU); RB warm start r=30 from 4096 train at 128^3, prolonged; "
+                     "tol 1e-10",
+            kind="tb", blocks=(2, 2, 2), n=512, m0=4, r=30, n_train=4096, rb_n=128, batch=1,
+            delta=1e-10, slab=True),
 }
 L_MAX = 60
 
@@ -339,6 +344,190 @@ def run_b200(args, rank, world, dist):
         print(json.dumps(line), flush=True)
 
 
+def slab_bytes_per_node(cells, iters):
+    """Algorithmic HBM bytes of one slab solve per finest-level node (DESIGN.md §3 table):
+    per PCG iteration the finest level moves 124 B/node and a coarse level l
+    76 B per level-l node (pre 24 + restriction 11 + prolongation 17 + post-smoothing 24);
+    once per solve: ||f|| (8), two residuals (2 x 24), the first V-cycle."""
+    nf = (cells[-1] - 1) ** 3
+    coarse = sum(76.0 * (c - 1) ** 3 for c in cells[1:-1]) / nf
+    vcyc = 24 + 11 + 25 + coarse
+    return iters * (124.0 + coarse) + 8 + 48 + vcyc
+
+
+def run_slab(args, rank, world, dist):
+    """configs[4]: one 512^3 instance per step, slab-decomposed over the GPUs (strong scaling)."""
+    import torch
+
+    import build as _build
+    if rank == 0:
+        _build.build(verbose=False)
+    if dist is not None:
+        dist.barrier()
+    import paper_2311_13862_b200 as rb
+    from paper_2311_13862_b200 import _native
+
+    cfg = CONFIGS[args.config]
+    n, m0, nc = cfg["n"], cfg["m0"], cfg["rb_n"]
+    delta = cfg["delta"]
+    spec = make_spec(cfg, rb)
+    prob = rb.ParametricProblem(spec, levels=rb.problems.levels_for(n, m0), m0=m0)
+    cprob = rb.ParametricProblem(spec, levels=rb.problems.levels_for(nc, m0), m0=m0)
+    train = rb.sample_mus(spec, cfg["n_train"], seed=1000)
+    t0 = time.perf_counter()
+    hf = rb.HighFidelitySolver(cprob, delta=1e-14, l_max=100)
+    model = rb.l1roc_offline(train, cfg["r"], hf, cprob, seed=0, on_degenerate="stop")
+    torch.cuda.synchronize()
+    t_off = time.perf_counter() - t0
+    log(f"[rank {rank}] offline greedy at {nc}^3: N={model.dim} in {t_off:.2f}s")
+
+    group = dist.group.WORLD if dist is not None else None
+    nslabs = world * max(1, args.slabs_per_gpu)
+    solver = rb.SlabSolver(prob, nslabs=nslabs, group=group)
+    f = prob.rhs()
+    solver.load("f", f)
+    k0, k1 = solver.planes
+    mus = rb.sample_mus(spec, args.warmup + args.steps + 1, seed=3000)   # same on every rank
+    cctx = rb.MgContext(cprob, 1)
+    fc = cprob.rhs()
+    lifts = []  # warm start prolonged nc -> 2nc -> ... -> n/2 (full vectors, every rank)
+    c = nc
+    while c < n // 2:
+        lifts.append(torch.zeros(rb.padded_len(2 * c, 1), dtype=torch.float64, device="cuda"))
+        c *= 2
+    stream = torch.cuda.current_stream()
+
+    def warm_start(mu):
+        rb.mg_context_for(cprob, mu[None], ctx=cctx)
+        u, _ = rb.l1roc_online(model, rb.BatchOperator(cctx), fc)
+        c = nc
+        for buf in lifts:
+            buf.zero_()
+            _native.call("rbws_prolong_add", 2 * c, 1, u.data_ptr(), buf.data_ptr(),
+                         _native.stream_ptr())
+            u, c = buf, 2 * c
+        solver.prolong_x(u)
+
+    def step(mu):
+        solver.setup(mu[None])
+        warm_start(mu)
+        return solver.solve(delta=delta, l_max=L_MAX)
+
+    for w in range(args.warmup):
+        step(mus[w])
+    # zero-initialised solve of the first timed parameter (outside the timed region)
+    solver.setup(mus[args.warmup][None])
+    solver.load("x", torch.zeros(rb.padded_len(n, 1), dtype=torch.float64, device="cuda"))
+    zero_rep = solver.solve(delta=delta, l_max=L_MAX)
+    torch.cuda.synchronize()
+
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    lc0 = _native.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = []
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        torch.cuda.nvtx.range_push("rbws_timed")
+        ev0.record(stream)
+        for s_ in range(args.steps):
+            reps.append(step(mus[args.warmup + s_]))
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_pop()
+    launches = _native.launch_count() - lc0
+    ms = ev0.elapsed_time(ev1)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = args.steps / (ms_max / 1e3)
+    iters = [r.iterations for r in reps]
+
+    # ---- end to end: host parameter in, this rank's planes of the solution out to pinned
+    # host memory, every step
+    hbuf = torch.empty((k1 - k0) * n * n, dtype=torch.float64, pin_memory=True)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for s_ in range(args.steps):
+        step(np.asarray(mus[args.warmup + s_]))
+        solver.store(hbuf, p0=k0)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = args.steps / (float(e2e_ms.item()) / 1e3)
+
+    peak, peak_kind = peaks()
+    bpn = slab_bytes_per_node(prob.cells, float(np.mean(iters)))
+    achieved = bpn * (n - 1) ** 3 / (ms_max / args.steps / 1e3) / 1e9 / world
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": "solves/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded log-uniform parameters; no dataset)",
+        "config": {"workload": cfg["workload"], "grid_cells": n, "levels": prob.levels,
+                   "slabs": nslabs, "planes_per_slab": n // nslabs,
+                   "first_distributed_level": solver.ld, "transport": solver.transport,
+                   "rb_dim": model.dim, "rb_grid_cells": nc, "n_train": cfg["n_train"],
+                   "tolerance": delta, "smoother": "jacobi(0.7), nu=1",
+                   "parallelism": f"z-slabs x{nslabs} over {world} GPU(s)",
+                   "l2": "inputs larger than L2 (1 GB per vector)",
+                   "iterations_warm": iters, "iterations_zero_init": zero_rep.iterations,
+                   "all_converged": all(r.converged for r in reps),
+                   "max_true_residual": max(r.true_residual for r in reps),
+                   "t_offline_s": round(t_off, 3)},
+        "e2e": {"value": round(e2e_value, 4), "unit": "solves/s",
+                "h2d_bytes_per_step": spec.n_terms * 8,
+                "d2h_bytes_per_step": (k1 - k0) * n * n * 8,
+                "api": "SlabSolver.setup/prolong_x/solve/store (host mu -> pinned host planes)"},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": "whole slab solve (all levels, per GPU)",
+                     "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "peak_source": peak_kind, "bytes_per_fine_node": round(bpn, 1),
+                     "note": "algorithmic bytes of the whole step / step time (setup, warm "
+                             "start, halo exchanges included)"},
+        "clocks": clocks.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = slab_cpu_baseline(cfg, iters, budget_s=args.cpu_budget)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def slab_cpu_baseline(cfg, gpu_iters, budget_s=15.0):
+    """The oracle MGCG (single core) cannot hold a 512^3 operator in seconds: time its
+    per-iteration cost at 64^3 and scale by DoFs to the GPU's iteration count."""
+    _single_thread_blas()
+    from oracle import problems as op
+    from oracle import solvers as so
+    ospec = make_ospec(cfg)
+    ns = 64
+    oprob = op.OracleProblem(ospec, ns, cfg["m0"])
+    mu = op.sample_mus(ospec, 1, seed=3000)[0]
+    A, f = oprob.operator(mu), oprob.rhs()
+    ctx = so.mg_context_for(oprob, mu)
+    t0 = time.perf_counter()
+    done = 0
+    per_it = []
+    while time.perf_counter() - t0 < budget_s:
+        t1 = time.perf_counter()
+        _, rep = so.mgcg_solve(A, f, np.zeros_like(f), ctx, delta=cfg["delta"], l_max=L_MAX)
+        per_it.append((time.perf_counter() - t1) / max(rep.iterations, 1))
+        done += 1
+    scale = ((cfg["n"] - 1) / (ns - 1)) ** 3
+    t_solve = float(np.median(per_it)) * scale * float(np.mean(gpu_iters))
+    return {"value": round(1.0 / t_solve, 6), "unit": "solves/s", "cores": 1, "kind": "port",
+            "sample": f"{done} zero-init oracle MGCG solves at {ns}^3 (per-iteration time, "
+                      f"single-threaded), scaled by DoFs x{scale:.0f} to 512^3 at the GPU's "
+                      f"mean iteration count; extrapolated, not measured at 512^3"}
+
+
 def cpu_baseline(cfg, model, test, gpu_iters, budget_s=15.0):
     """Oracle RBI-MGCG per parameter (single core) on a bounded sample."""
     _single_thread_blas()
@@ -471,6 +660,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-per-core", type=int, default=2)
+    ap.add_argument("--slabs-per-gpu", type=int, default=1,
+                    help="configs[4]: slabs per GPU (>1: in-process slabs exchanging by copies)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         log("note: fewer than 3 warm-up steps requested")
@@ -486,7 +677,10 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    run_b200(args, rank, world, dist)
+    if CONFIGS[args.config].get("slab"):
+        run_slab(args, rank, world, dist)
+    else:
+        run_b200(args, rank, world, dist)
     if dist is not None:
         dist.destroy_process_group()
 

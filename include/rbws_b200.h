@@ -164,7 +164,10 @@ int rbws_dense_solve(int m, const double* A, const double* b, double* x, int* st
  * per GPU) with NCCL send/recv, and dot-product partials are all-gathered, so
  * every slab computes bitwise identical PCG scalars.
  *   nccl_id: (host) 128 bytes from rbws_comm_unique_id on process 0, shared
- *            by every process (NULL when all slabs live in this process);
+ *            by every process.  NULL: all slabs live in this process and
+ *            exchange by device copies; with nprocs == 1 and an id, the slabs
+ *            of this process exchange through NCCL send/recv to itself
+ *            (loopback: the multi-process code path on one GPU);
  *   nprocs/proc_rank: processes and this process's rank (slabs are assigned
  *            in process order: first = proc_rank * nlocal). */
 typedef struct rbws_slab rbws_slab;

@@ -279,12 +279,10 @@ int rbws_slab_create(rbws_slab** out, rbws_hierarchy* h, int nslabs, int nlocal,
                      const uint8_t* nccl_id, int nprocs, int proc_rank, double omega) {
   if (!out || !h) RBWS_FAIL("null argument");
   rbws::Comm* comm = nullptr;
-  if (nprocs > 1) {
-    if (!nccl_id) RBWS_FAIL("multi-process slabs need an NCCL id");
-    if (rbws::comm_create(&comm, nccl_id, nprocs, proc_rank)) return 1;
-  } else if (nprocs != 1 || proc_rank != 0) {
-    RBWS_FAIL("bad process count / rank");
-  }
+  if (nprocs < 1 || proc_rank < 0 || proc_rank >= nprocs) RBWS_FAIL("bad process count / rank");
+  if (nprocs > 1 && !nccl_id) RBWS_FAIL("multi-process slabs need an NCCL id");
+  // one process with an id: NCCL loopback transport between its own slabs
+  if (nccl_id && rbws::comm_create(&comm, nccl_id, nprocs, proc_rank)) return 1;
   rbws::Slab* s = nullptr;
   if (rbws::slab_create(&s, H(h), nslabs, proc_rank * nlocal, nlocal, comm, omega)) {
     delete comm;

@@ -32,7 +32,7 @@ constexpr int kThreads = 256;  // threads per CTA (one per grid column of the ti
 template <int N>
 struct FT {
   static constexpr int RPP = (kThreads / N) < 1 ? 1 : ((kThreads / N) < N ? kThreads / N : N);
-  static constexpr int NPT = (RPP * 2 <= N) ? 2 : 1;
+  static constexpr int NPT = (RPP * 2 <= N && N < 512) ? 2 : 1;  // N = 512: one row per thread
   static constexpr int TY = RPP * NPT;
   static constexpr int THREADS = RPP * N;
   static constexpr int HSZ = (TY + 2) * N;  // doubles per staged array with halo rows
@@ -45,7 +45,7 @@ FineGeom fine_geom(int n, int batch, int nz) {
   if (rpp < 1) rpp = 1;
   if (rpp > n) rpp = n;
   g.rpp = rpp;
-  g.npt = (rpp * 2 <= n) ? 2 : 1;
+  g.npt = (rpp * 2 <= n && n < 512) ? 2 : 1;
   g.ty = rpp * g.npt;
   g.threads = rpp * n;
   g.ytiles = n / g.ty;
@@ -94,9 +94,11 @@ struct SL {
   static constexpr bool XF = (MODE == FM_PRE || MODE == FM_PAPPLY || MODE == FM_POSTP);
   static constexpr int NH = XF ? 2 : 1;
   static constexpr int NC = (MODE == FM_CG) ? 2 : ((MODE == FM_RESID || MODE == FM_JACOBI) ? 1 : 0);
-  // raw / transformed ring slots (N = 512 rows are 4 KB: shallower rings fit 227 KB)
+  // raw / transformed ring slots (N = 512 rows are 4 KB: a shallower raw ring fits 227 KB).
+  // U >= 6: a trip reads transformed planes k-1 .. k+2 while the next trip's transform
+  // (no barrier in between) writes k+3, k+4.
   static constexpr int S = XF ? (N >= 512 ? 4 : 6) : (N >= 512 ? 6 : kStages);
-  static constexpr int U = N >= 512 ? 4 : 6;
+  static constexpr int U = 6;
 };
 
 // FM_POSTP stages, with every even fine plane p, coarse plane p/2 + 1 rows

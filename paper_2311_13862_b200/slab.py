@@ -55,7 +55,7 @@ class SlabSolver:
     """
 
     def __init__(self, problem: ParametricProblem, nslabs: int | None = None, group=None,
-                 omega: float = JACOBI_OMEGA):
+                 omega: float = JACOBI_OMEGA, transport: str = "auto"):
         _native.require_cuda()
         self.problem = problem
         nprocs, prank = 1, 0
@@ -70,6 +70,15 @@ class SlabSolver:
         self.nslabs, self.nprocs, self.rank = int(nslabs), nprocs, prank
         self.nlocal = self.nslabs // nprocs
         self.ld, self.own = slab_partition(problem.cells, self.nslabs)
+        if transport not in ("auto", "copy", "nccl"):
+            raise ValueError(f"unknown transport {transport!r}")
+        if nprocs > 1 and transport == "copy":
+            raise ValueError("slabs on several processes exchange through NCCL")
+        if nprocs == 1 and transport == "nccl":  # loopback: NCCL send/recv between own slabs
+            buf = (ctypes.c_uint8 * 128)()
+            _native.call("rbws_comm_unique_id", buf)
+            nid = buf
+        self.transport = "nccl" if (nprocs > 1 or transport == "nccl") else "copy"
         if nprocs > 1:
             import torch.distributed as dist
             buf = (ctypes.c_uint8 * 128)()
@@ -156,14 +165,16 @@ class SlabSolver:
             delta=delta, l_max=l_max, mu=None if self.mu is None else np.asarray(self.mu),
             absolute_norms=bool(st.value & 4),
             config={"slabs": self.nslabs, "processes": self.nprocs, "smoother": "jacobi",
+                    "transport": self.transport,
                     "nu": 1, "first_distributed_level": self.ld})
 
 
 def slab_mgcg_solve(problem: ParametricProblem, mu, f=None, x0=None, nslabs: int = 1,
-                    delta: float = 1e-10, l_max: int = 60, solver: SlabSolver | None = None):
+                    delta: float = 1e-10, l_max: int = 60, solver: SlabSolver | None = None,
+                    transport: str = "auto"):
     """Single-process convenience: full padded f / x0 in, full padded x out."""
     import torch
-    s = solver or SlabSolver(problem, nslabs=nslabs)
+    s = solver or SlabSolver(problem, nslabs=nslabs, transport=transport)
     s.setup(mu)
     n = problem.n
     f = problem.rhs() if f is None else f

@@ -147,3 +147,16 @@ def test_slab_edge_cases():
         pkg.SlabSolver(prob, nslabs=3)   # planes per slab must be even
     with pytest.raises(ValueError):
         pkg.SlabSolver(prob, nslabs=16)  # fewer than 4 planes per slab
+
+
+def test_slab_nccl_loopback_transport_is_bitwise_identical():
+    """Halo planes and dot partials through NCCL (send/recv to this rank, all-gather)
+    give bitwise the device-copy result: the multi-process code path on one GPU."""
+    pkg = _pkg()
+    prob, _, ospec = _pair((2, 2, 2), 64, 4)
+    mu = op.sample_mus(ospec, 1, seed=13)
+    xa, ra = pkg.slab_mgcg_solve(prob, mu, nslabs=4, delta=1e-10, transport="copy")
+    xb, rb_ = pkg.slab_mgcg_solve(prob, mu, nslabs=4, delta=1e-10, transport="nccl")
+    assert rb_.config["transport"] == "nccl"
+    assert ra.iterations == rb_.iterations and ra.history == rb_.history
+    assert torch.equal(xa, xb)
