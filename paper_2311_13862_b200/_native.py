@@ -78,7 +78,8 @@ def load(path: str | os.PathLike | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # RBWS_LIB: an alternative build of the same library (kernel-variant experiments)
+    p = Path(path) if path else Path(os.environ.get("RBWS_LIB") or LIB_PATH)
     if not p.exists():
         raise NativeError(
             f"native library {p} not built; run `python build.py` (nvcc, sm_100a). "

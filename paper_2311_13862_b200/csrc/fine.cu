@@ -32,7 +32,10 @@ constexpr int kThreads = 256;  // threads per CTA (one per grid column of the ti
 template <int N>
 struct FT {
   static constexpr int RPP = (kThreads / N) < 1 ? 1 : ((kThreads / N) < N ? kThreads / N : N);
-  static constexpr int NPT = (RPP * 2 <= N && N < 512) ? 2 : 1;  // N = 512: one row per thread
+#ifndef RBWS_N512_NPT
+#define RBWS_N512_NPT 1
+#endif
+  static constexpr int NPT = N >= 512 ? RBWS_N512_NPT : ((RPP * 2 <= N) ? 2 : 1);
   static constexpr int TY = RPP * NPT;
   static constexpr int THREADS = RPP * N;
   static constexpr int HSZ = (TY + 2) * N;  // doubles per staged array with halo rows
@@ -45,7 +48,7 @@ FineGeom fine_geom(int n, int batch, int nz) {
   if (rpp < 1) rpp = 1;
   if (rpp > n) rpp = n;
   g.rpp = rpp;
-  g.npt = (rpp * 2 <= n && n < 512) ? 2 : 1;
+  g.npt = n >= 512 ? RBWS_N512_NPT : ((rpp * 2 <= n) ? 2 : 1);
   g.ty = rpp * g.npt;
   g.threads = rpp * n;
   g.ytiles = n / g.ty;
@@ -97,7 +100,8 @@ struct SL {
   // raw / transformed ring slots (N = 512 rows are 4 KB: a shallower raw ring fits 227 KB).
   // U >= 6: a trip reads transformed planes k-1 .. k+2 while the next trip's transform
   // (no barrier in between) writes k+3, k+4.
-  static constexpr int S = XF ? (N >= 512 ? 4 : 6) : (N >= 512 ? 6 : kStages);
+  static constexpr int S = XF ? (N >= 512 ? (RBWS_N512_NPT == 2 ? (MODE == FM_POSTP ? 2 : 3) : 4) : 6)
+                              : (N >= 512 ? 6 : kStages);
   static constexpr int U = 6;
 };
 
