@@ -33,7 +33,7 @@ template <int N>
 struct FT {
   static constexpr int RPP = (kThreads / N) < 1 ? 1 : ((kThreads / N) < N ? kThreads / N : N);
 #ifndef RBWS_N512_NPT
-#define RBWS_N512_NPT 1
+#define RBWS_N512_NPT 2
 #endif
   static constexpr int NPT = N >= 512 ? RBWS_N512_NPT : ((RPP * 2 <= N) ? 2 : 1);
   static constexpr int TY = RPP * NPT;
