@@ -201,7 +201,7 @@ def run_b200(args, rank, world, dist):
             rb.mg_context_for(prob, part, ctx=ctx)
             x, r = rb.rbi_pcg_solve(rb.BatchOperator(ctx), f, method, mg_ctx=ctx,
                                     l1roc_model=model, x0_out=xbuf)
-            reps += r
+            reps.append(r)   # lazy report batches: no per-instance host work in the step
         state["reps"], state["x"] = reps, x
         return x
 
@@ -245,7 +245,7 @@ def run_b200(args, rank, world, dist):
     ms_max = float(ms_t.item())
     ms_step = ms_max / args.steps
     value = world * batch * args.steps / (ms_max / 1e3)
-    reps = state["reps"]
+    reps = [r for batch_reps in state["reps"] for r in batch_reps]
     iters = [r.iterations for r in reps]
     worst_res = max(r.true_residual for r in reps)
     converged = all(r.converged for r in reps)

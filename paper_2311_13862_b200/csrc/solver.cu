@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -389,9 +390,11 @@ void Batch::prof_end(int cls, int start, cudaStream_t s) {
 }
 
 void Batch::prof_flush() {
+  static const bool dump = getenv("RBWS_PROF_DUMP") != nullptr;  // per-launch trace (stderr)
   for (auto& r : recs) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, ev[r[1]], ev[r[2]]) == cudaSuccess) {
+      if (dump) fprintf(stderr, "PROF %d %d %.4f\n", r[0], r[3], ms);
       prof_ms[r[0]] += ms;
       prof_calls[r[0]] += 1;
       prof_units[r[0]] += r[3];

@@ -20,7 +20,7 @@ import numpy as np
 
 from . import _native
 from .grid import BatchOperator, ParametricProblem, padded_len
-from .krylov import OperatorError, SolveReport
+from .krylov import OperatorError, SolveReport, SolveReports
 
 JACOBI_OMEGA = 0.7
 
@@ -149,15 +149,7 @@ def mgcg_solve(A, f, x0, ctx: MgContext, delta: float = 1e-16, l_max: int = 40, 
     if raise_on_breakdown and np.any(status & 1):
         bad = int(np.flatnonzero(status & 1)[0])
         raise OperatorError(f"non-positive curvature for parameter #{bad}; operator not SPD")
-    reports = []
-    for m in range(count):
-        k = int(iters[m])
-        reports.append(SolveReport(
-            method=method, iterations=k, history=[float(v) for v in hist[m, :k + 1]],
-            converged=bool(tres[m] <= delta), true_residual=float(tres[m]),
-            wall_time=wall / count, delta=delta, l_max=l_max,
-            mu=None if ctx.mus is None else np.asarray(ctx.mus[m]),
-            absolute_norms=bool(status[m] & 4),
-            config={"batch": count, "batch_wall_time": wall, "smoother": "jacobi",
-                    "nu": ctx.nu}))
+    reports = SolveReports(method, iters, hist, tres, status, wall, delta, l_max, ctx.mus,
+                           {"batch": count, "batch_wall_time": wall, "smoother": "jacobi",
+                            "nu": ctx.nu})
     return x, reports

@@ -14,6 +14,7 @@ import numpy as np
 
 from . import _native
 from .grid import BatchOperator, ParametricProblem, padded_len
+from .krylov import SolveReports
 from .multigrid import MgContext, mg_context_for
 from .warmstart import MethodConfig, rbi_pcg_solve
 
@@ -91,7 +92,7 @@ class HostPipeline:
             ctx = mg_context_for(self.problem, part, ctx=self.ctx[s])
             x, reps = rbi_pcg_solve(BatchOperator(ctx), self.f, self.method, mg_ctx=ctx,
                                     l1roc_model=self.model, x0_out=self.x[s])
-            reports += reps
+            reports.append(reps)
             self.solved[s].record(compute)
             with torch.cuda.stream(self.copy_stream):
                 self.copy_stream.wait_event(self.solved[s])
@@ -99,4 +100,4 @@ class HostPipeline:
                 out_host[c0 * n3:(c0 + m) * n3].copy_(x[:m * n3], non_blocking=True)
                 self.freed[s].record(self.copy_stream)
             c0 += size
-        return reports
+        return SolveReports.concat(reports)

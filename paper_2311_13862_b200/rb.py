@@ -121,12 +121,12 @@ def _online_batch(model: L1rocModel, problem, theta, f, count):
     return a, c, ind, st
 
 
-def l1roc_online(model: L1rocModel, A, b, out=None):
+def l1roc_online(model: L1rocModel, A, b, out=None, coords: bool = True):
     """Batched sub-sampled least-squares reduced solve (rb.py:190-205).
 
     A: BatchOperator (its context supplies theta(mu)); b: padded rhs.
     Returns (warm starts as a padded batch tensor, snapshot coordinates
-    (count, N) numpy).
+    (count, N) numpy, or None with ``coords=False``).
     """
     import torch
     if model.dim == 0:
@@ -134,15 +134,16 @@ def l1roc_online(model: L1rocModel, A, b, out=None):
     ctx = A.ctx
     problem, count = ctx.problem, ctx.count
     a, c, _, st = _online_batch(model, problem, ctx.theta, b, count)
-    if np.any(_native.fetch(st) != 0):
-        raise DegenerateBasisError("sub-sampled reduced system is rank deficient")
     n = model.n
     x = out if out is not None else torch.empty(padded_len(n, count), dtype=torch.float64,
                                                 device="cuda")
     _native.call("rbws_expand", n, count, model.basis.data_ptr(), n ** 3, model.dim,
                  a.data_ptr(), x.data_ptr(), _native.stream_ptr())
     x[count * n ** 3:] = 0.0
-    return x, _native.fetch(c.view(count, model.dim))
+    # one host sync, after the expansion is queued (x is discarded if the check fails)
+    if np.any(_native.fetch(st) != 0):
+        raise DegenerateBasisError("sub-sampled reduced system is rank deficient")
+    return x, (_native.fetch(c.view(count, model.dim)) if coords else None)
 
 
 # ----------------------------------------------------------------- DEIM
