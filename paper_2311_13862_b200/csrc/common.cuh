@@ -38,6 +38,8 @@ struct Sep7 {
   const double* face;
   const double* node;
   const double* theta;
+  int zchg = -1;             // planes where the diagonal changes along z (-1: unknown)
+  const int* fz = nullptr;   // [n+1] plane k's diagonal equals plane k-1's (device, host-built)
 };
 
 // Per-instance symmetric 27-point stencil of a coarse level.

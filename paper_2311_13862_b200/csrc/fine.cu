@@ -23,6 +23,7 @@ namespace rbws {
 
 constexpr int kStages = 8;  // ring slots (power of two)
 constexpr int kMaxKz = 64;  // planes per z-chunk (bounds the z-factor table)
+constexpr int kMaxDiagChanges = 16;  // DC kernels when the diagonal changes on <= 16 planes
 constexpr int kThreads = 256;  // threads per CTA (one per grid column of the tile; N = 512: 512)
 
 // Compile-time tile geometry for a grid with N cells per axis: RPP rows per pass
@@ -76,6 +77,7 @@ struct FineArgs {
   const int* active;
   double omega;
   int zlo, zhi;   // output planes [zlo, zhi) (global plane indices, virtual base pointers)
+  int dc;         // PRE / POSTP: w/diag from the cached shared-memory tile (h1 unused)
   int c0_shared;  // c0 is one instance shared by the whole batch (e.g. the rhs f)
   const double* ec;  // FM_POSTP: coarse-grid correction (n/2 cells, padded batch layout)
 };
@@ -90,12 +92,16 @@ enum FineMode : int {
   FM_POSTP = 6,   // h0 = b, h1 = dinv, ec   u = w dinv b + P ec; out0 = u + w (b - A u)/d, dot b.out
 };
 
-template <int MODE, int N>
+// DC ("diagonal cached"): PRE / POSTP keep w/diag of the staged rows in a shared-memory
+// tile, reloaded from the 1/diag vector only on planes where the diagonal changes along z
+// (thermal blocks: a few planes), instead of streaming 1/diag with every plane (8 bytes
+// per node less; bitwise the same values)
+template <int MODE, int N, bool DC = false>
 struct SL {
   // PRE / PAPPLY stencil a derived vector (w dinv b, s + beta p_old): each staged
   // plane is transformed once into a second ring, so neighbours cost one LDS
   static constexpr bool XF = (MODE == FM_PRE || MODE == FM_PAPPLY || MODE == FM_POSTP);
-  static constexpr int NH = XF ? 2 : 1;
+  static constexpr int NH = XF ? 2 : 1;  // DC: h1 (1/diag) staged only on reload planes
   static constexpr int NC = (MODE == FM_CG) ? 2 : ((MODE == FM_RESID || MODE == FM_JACOBI) ? 1 : 0);
   // raw / transformed ring slots (N = 512 rows are 4 KB: a shallower raw ring fits 227 KB).
   // U >= 6: a trip reads transformed planes k-1 .. k+2 while the next trip's transform
@@ -114,25 +120,29 @@ struct FCoarse {
   static constexpr int CSZ = CR * NCC;
 };
 
-template <int N, int MODE>
+template <int N, int MODE, bool DC = false>
 struct FSmem {
-  static constexpr int STAGE = SL<MODE, N>::NH * FT<N>::HSZ + SL<MODE, N>::NC * FT<N>::CSZ +
+  using L = SL<MODE, N, DC>;
+  static constexpr int STAGE = L::NH * FT<N>::HSZ + L::NC * FT<N>::CSZ +
                                (MODE == FM_POSTP ? FCoarse<N>::CSZ : 0);
-  static constexpr int RING = SL<MODE, N>::S * STAGE + (SL<MODE, N>::XF ? SL<MODE, N>::U * FT<N>::HSZ : 0);
+  // raw ring, transformed ring, cached w/diag tile (DC)
+  static constexpr int RING = L::S * STAGE + (L::XF ? L::U * FT<N>::HSZ : 0) +
+                              (DC ? FT<N>::HSZ : 0);
   static size_t bytes(int np, int Q) {
     return 64 + 4 * (kMaxKz + 4) + 8 * (((size_t)np * 3 * Q + 1) & ~(size_t)1) + 8 * (size_t)RING;
   }
 };
 
-template <int MODE, int N>
-__global__ void __launch_bounds__(FT<N>::THREADS) fine_kernel(FineArgs a) {
+template <int MODE, int N, bool DC>
+__global__ void __launch_bounds__(FT<N>::THREADS, FT<N>::THREADS <= 256 ? 2 : 1)
+fine_kernel(FineArgs a) {
   using G = FT<N>;
-  using L = SL<MODE, N>;
+  using L = SL<MODE, N, DC>;
   constexpr bool XF = L::XF;
   constexpr int NH = L::NH, NC = L::NC, S = L::S, U = L::U;
   constexpr int NPT = G::NPT, RPP = G::RPP, TY = G::TY;
   constexpr int HSZ = G::HSZ, CSZ = G::CSZ;
-  constexpr int STAGE = FSmem<N, MODE>::STAGE;  // doubles per raw ring slot
+  constexpr int STAGE = FSmem<N, MODE, DC>::STAGE;  // doubles per raw ring slot
   constexpr int64_t N2 = (int64_t)N * N;
   extern __shared__ __align__(128) unsigned char smem[];
   const Sep7& op = a.op;
@@ -159,6 +169,7 @@ __global__ void __launch_bounds__(FT<N>::THREADS) fine_kernel(FineArgs a) {
   double* zf = reinterpret_cast<double*>(smem + 64 + 4 * (kMaxKz + 4));  // [np][3Q]
   double* ring = zf + ((np * ZW + 1) & ~1);                      // [S][STAGE]
   double* uring = ring + S * STAGE;                              // [U][HSZ] (XF)
+  double* wd = uring + (XF ? U * HSZ : 0);                       // [HSZ] w/diag (DC)
 
   for (int t = tid; t < np * ZW; t += G::THREADS) {  // z factors of the staged planes
     const int p = t / ZW, f = (t / Q) % 3, q = t % Q, k = p_first + p;
@@ -194,11 +205,13 @@ __global__ void __launch_bounds__(FT<N>::THREADS) fine_kernel(FineArgs a) {
     // coarse plane p/2 + 1 (for the z march of P ec) with every even fine plane;
     // none past the last coarse plane (its ghost plane p/2 = n/2 is never advanced from)
     const bool stage_c = (MODE == FM_POSTP) && !(p & 1) && ((p >> 1) + 1 <= NCC);
-    mbar_arrive_expect_tx(&bar[sl], NH * hbytes + NC * cbytes + (stage_c ? ebytes : 0u));
+    const bool h1_on = !DC || p == p_first || !__ldg(op.fz + p);  // DC: reload planes only
+    mbar_arrive_expect_tx(&bar[sl], (NH > 1 && !h1_on ? 1 : NH) * hbytes + NC * cbytes +
+                                        (stage_c ? ebytes : 0u));
     const int64_t plane = base + (int64_t)p * N2;
     const int64_t hrow = plane + (int64_t)(j0 - 1 + skip) * N;
     bulk_g2s(st + skip * N, a.h0 + hrow, hbytes, &bar[sl]);
-    if (NH > 1) bulk_g2s(st + HSZ + skip * N, a.h1 + hrow, hbytes, &bar[sl]);
+    if (NH > 1 && h1_on) bulk_g2s(st + HSZ + skip * N, a.h1 + hrow, hbytes, &bar[sl]);
     if (NC > 0)
       bulk_g2s(st + NH * HSZ, a.c0 + (a.c0_shared ? plane - base : plane) + (int64_t)j0 * N,
                cbytes, &bar[sl]);
@@ -297,8 +310,13 @@ __global__ void __launch_bounds__(FT<N>::THREADS) fine_kernel(FineArgs a) {
         cv1[t] = vxy(E + NCC * NCC, 0, trow_j(t));
       }
   }
+  // DC: w/diag of the staged rows, in shared memory; element e is only ever transformed by
+  // one thread, so each thread refreshes its own elements from the staged 1/diag rows (h1,
+  // bulk-copied only with the planes where the diagonal changes; host-built flags) and no
+  // barrier is needed
   // XF: transform staged plane p (h0, h1) into the u ring; own rows returned in xo / bo
   auto transform = [&](int p, double* xo, double* bo) {
+    const bool reload = DC && (p == p_first || !__ldg(op.fz + p));  // CTA-uniform
     const double* R = raw(p);
     double* T = uring + (p - p_first) % U * HSZ;
     const bool adv = (MODE == FM_POSTP) && p != p_first && !(p & 1);
@@ -307,8 +325,9 @@ __global__ void __launch_bounds__(FT<N>::THREADS) fine_kernel(FineArgs a) {
       if (!trow_on(t)) continue;
       const int e = trow_e(t);
       double v;
+      if (DC && reload) wd[e] = om * R[HSZ + e];  // staged with this plane
       if (MODE == FM_PRE) {
-        v = (om * R[HSZ + e]) * R[e];  // w dinv b
+        v = (DC ? wd[e] : om * R[HSZ + e]) * R[e];  // w dinv b
       } else if (MODE == FM_PAPPLY) {
         v = fma(sc, R[HSZ + e], R[e]);  // s + beta p_old
       } else {  // FM_POSTP: w dinv b + P ec
@@ -317,7 +336,7 @@ __global__ void __launch_bounds__(FT<N>::THREADS) fine_kernel(FineArgs a) {
           cv1[t] = vxy(R + NH * HSZ, cj0, trow_j(t));
         }
         const double pe = (p & 1) ? 0.5 * (cv0[t] + cv1[t]) : cv0[t];
-        v = fma(om * R[HSZ + e], R[e], pe);
+        v = fma(DC ? wd[e] : om * R[HSZ + e], R[e], pe);
       }
       T[e] = v;
       if (t < NPT) {
@@ -474,24 +493,31 @@ __global__ void __launch_bounds__(FT<N>::THREADS) fine_kernel(FineArgs a) {
   }
 }
 
-template <int MODE, int N>
-static cudaError_t fine_launch_mn(const FineArgs& a, int batch, cudaStream_t stream) {
+template <int MODE, int N, bool DC>
+static cudaError_t fine_launch_mnd(const FineArgs& a, int batch, cudaStream_t stream) {
   using G = FT<N>;
   if (a.g.threads != G::THREADS || a.g.ty != G::TY) return cudaErrorInvalidValue;
   const int np = a.g.kz + 2;
-  const size_t smem = FSmem<N, MODE>::bytes(np, a.op.Q);
+  const size_t smem = FSmem<N, MODE, DC>::bytes(np, a.op.Q);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   static size_t attr = 48 * 1024;
   if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(fine_kernel<MODE, N>,
+    cudaError_t e = cudaFuncSetAttribute(fine_kernel<MODE, N, DC>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = smem;
   }
   dim3 grd(1, a.g.ytiles, batch * a.g.zc);
   count_launch();
-  fine_kernel<MODE, N><<<grd, G::THREADS, smem, stream>>>(a);
+  fine_kernel<MODE, N, DC><<<grd, G::THREADS, smem, stream>>>(a);
   return cudaGetLastError();
+}
+
+template <int MODE, int N>
+static cudaError_t fine_launch_mn(const FineArgs& a, int batch, cudaStream_t stream) {
+  if constexpr (MODE == FM_PRE || MODE == FM_POSTP)
+    if (a.dc) return fine_launch_mnd<MODE, N, true>(a, batch, stream);
+  return fine_launch_mnd<MODE, N, false>(a, batch, stream);
 }
 
 template <int MODE>
@@ -588,6 +614,10 @@ static FineArgs base_args(const Sep7& op, int dot, double* partial, const Launch
   a.omega = omega;
   a.zlo = lc.zlo;
   a.zhi = lc.zhi;
+  // few planes where the diagonal changes along z: cache w/diag instead of reading dinv.
+  // Measured: at N <= 128 (two 256-thread CTAs per SM) the transformed-input kernels are
+  // issue-bound and the saved 8 B/node buy nothing; at N = 512 (one CTA per SM) they do.
+  a.dc = (op.fz && op.n >= 256 && op.zchg >= 0 && op.zchg <= kMaxDiagChanges) ? 1 : 0;
   return a;
 }
 

@@ -119,7 +119,7 @@ int Slab::vcycle(int l, int vb, int vout, bool dot, cudaStream_t st) {
   const int c = l - 1;
   const bool cdist = c >= Ld;
   const int n = cells(l), nc = cells(c);
-  const Sep7 fop{h->n, h->Q, h->d_face, h->d_node, theta};
+  const Sep7 fop{h->n, h->Q, h->d_face, h->d_node, theta, h->fine_zchg, h->d_fzsame};
   // pre-smoothing from zero and its residual: t = b - A (w D^-1 b)
   if (fine) {
     for (auto& P : parts)
@@ -252,7 +252,7 @@ int slab_setup(Slab* s, const double* theta, int* n_bad, cudaStream_t st) {
   Hierarchy* h = s->h;
   const int L = s->L;
   RBWS_CK(cudaMemcpyAsync(s->theta, theta, sizeof(double) * h->Q, cudaMemcpyDefault, st));
-  const Sep7 fop{h->n, h->Q, h->d_face, h->d_node, s->theta};
+  const Sep7 fop{h->n, h->Q, h->d_face, h->d_node, s->theta, h->fine_zchg, h->d_fzsame};
   for (auto& P : s->parts) {
     // finest 1/diag including the halo planes (the pre/post-smoothing kernels stage them)
     const int zlo = std::max(1, P.k0[L - 1] - 1), zhi = std::min(h->n, P.k1[L - 1] + 1);
@@ -323,7 +323,7 @@ int slab_solve(Slab* S, double delta, int l_max, int* iters, double* hist, doubl
     S->hist_len = l_max + 1;
   }
   const int hl = S->hist_len;
-  const Sep7 op{n, h->Q, h->d_face, h->d_node, S->theta};
+  const Sep7 op{n, h->Q, h->d_face, h->d_node, S->theta, h->fine_zchg, h->d_fzsame};
   const int T = S->tiles;
   auto part_of = [&](const SlabPart& P) { return S->partial + (int64_t)P.rank * T; };
   // ||f||^2 over the owned planes, r = f - A x0, |r|^2

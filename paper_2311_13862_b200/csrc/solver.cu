@@ -207,6 +207,8 @@ int hierarchy_create(Hierarchy** out, int n, int m0, int Q, const double* face,
       }
       fz[k] = same;
     }
+    h->fine_zchg = 1;  // plane 1
+    for (int k = 2; k <= n - 1; ++k) h->fine_zchg += fz[k] ? 0 : 1;
     if (e == cudaSuccess) e = dalloc(&h->d_fzsame, fz.size());
     if (e == cudaSuccess)
       e = cudaMemcpy(h->d_fzsame, fz.data(), sizeof(int) * fz.size(), cudaMemcpyHostToDevice);
@@ -283,6 +285,8 @@ Batch::~Batch() {
 Sep7 Batch::fine_op() const {
   Sep7 op;
   op.n = h->n; op.Q = h->Q; op.face = h->d_face; op.node = h->d_node; op.theta = theta;
+  op.zchg = h->fine_zchg;
+  op.fz = h->d_fzsame;
   return op;
 }
 

@@ -24,6 +24,7 @@ struct Hierarchy {
   std::vector<double*> d_fac;       // per level 1D Kronecker factors [Q*3][3][2][n+1]
   std::vector<int*> d_zsame;        // per level [n+1]: z factors of plane k == plane k-1
   int* d_fzsame = nullptr;          // finest level [n+1]: same flags for the separable tables
+  int fine_zchg = -1;               // finest planes whose diagonal differs from the previous
   std::vector<int*> d_grp;          // per level [3Q]: z-group of every term
   std::vector<int> G;               // per level: number of z-groups
   std::vector<std::vector<double>> h_fac;
