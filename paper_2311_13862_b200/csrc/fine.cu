@@ -371,8 +371,9 @@ fine_kernel(FineArgs a) {
 
   // one plane: vd / vc / vu = own-column input at k-1 / k / k+1, vb = own b at k
   int64_t gk = base + (int64_t)(j0 + rl0) * N + i + (int64_t)kb * N2;  // (i, j0+rl0, k)
-  auto step = [&](int k, const double* vd, const double* vc, const double* vu, const double* vb) {
-    if (k == kb || !repeats(k)) {  // CTA-uniform
+  // face weights for plane k (refreshed only where the z factors change; CTA-uniform)
+  auto refresh = [&](int k) {
+    if (k == kb || !repeats(k)) {
 #pragma unroll
       for (int r = 0; r < NPT; ++r) {
         const double prev = wzp[r];
@@ -389,56 +390,61 @@ fine_kernel(FineArgs a) {
       }
       pend = false;
     }
-    // plane k's in-plane neighbours (transformed ring for XF, raw ring otherwise)
+  };
+  // true when plane k keeps the current weights (no refresh work)
+  auto steady = [&](int k) { return k != kb && repeats(k) && !pend; };
+  // the NPT nodes of one plane: vd / vc / vu = own-column input at k-1 / k / k+1, vb = own b
+  auto node = [&](int k, int r, int64_t gk_, double ud, double uc, double uu, double vbr) {
     const double* P0 = (XF ? uring + (k - p_first) % U * HSZ : raw(k)) + hoff;
     const double* C0 = raw(k) + NH * HSZ + coff;
-#pragma unroll
-    for (int r = 0; r < NPT; ++r) {
-      const int o = r * RPP * N;  // compile-time after unrolling
-      const double uc = vc[r], ud = vd[r], uu = vu[r];
-      const double ue = P0[o + 1], uw = P0[o - 1], un = P0[o + N], us = P0[o - N];
-      // shallow FMA tree (a dependent chain of 6 would be latency bound)
-      const double offx = fma(wxm[r], uw, wxp[r] * ue);
-      const double offy = fma(wym[r], us, wyp[r] * un);
-      const double offz = fma(wzm[r], ud, wzp[r] * uu);
-      const double off = (offx + offy) + offz;
-      const int64_t gidx = gk + o;
-      if (MODE == FM_PRE) {
-        // b - A (w D^-1 b) = (1 - w) b + off(w D^-1 b): the diagonal term is w b
-        if (on[r]) a.out0[gidx] = fma(1.0 - om, vb[r], off);
-      } else if (MODE == FM_POSTP) {
-        const double Au = fma(dg[r], uc, -off);
-        const double y = fma(wdi[r], vb[r] - Au, uc);
+    const int o = r * RPP * N;  // compile-time after unrolling
+    const double ue = P0[o + 1], uw = P0[o - 1], un = P0[o + N], us = P0[o - N];
+    // shallow FMA tree (a dependent chain of 6 would be latency bound)
+    const double offx = fma(wxm[r], uw, wxp[r] * ue);
+    const double offy = fma(wym[r], us, wyp[r] * un);
+    const double offz = fma(wzm[r], ud, wzp[r] * uu);
+    const double off = (offx + offy) + offz;
+    const int64_t gidx = gk_ + o;
+    if (MODE == FM_PRE) {
+      // b - A (w D^-1 b) = (1 - w) b + off(w D^-1 b): the diagonal term is w b
+      if (on[r]) a.out0[gidx] = fma(1.0 - om, vbr, off);
+    } else if (MODE == FM_POSTP) {
+      const double Au = fma(dg[r], uc, -off);
+      const double y = fma(wdi[r], vbr - Au, uc);
+      if (on[r]) a.out0[gidx] = y;
+      acc = on[r] ? fma(vbr, y, acc) : acc;
+    } else {
+      const double Au = fma(dg[r], uc, -off);
+      if (MODE == FM_APPLY) {
+        if (on[r] && a.out0) a.out0[gidx] = Au;
+        acc = on[r] ? fma(uc, Au, acc) : acc;
+      } else if (MODE == FM_RESID) {
+        const double rv = C0[o] - Au;
+        if (on[r]) a.out0[gidx] = rv;
+        acc = on[r] ? fma(rv, rv, acc) : acc;
+      } else if (MODE == FM_JACOBI) {
+        const double bv = C0[o];
+        const double y = fma(wdi[r], bv - Au, uc);
         if (on[r]) a.out0[gidx] = y;
-        acc = on[r] ? fma(vb[r], y, acc) : acc;
-      } else {
-        const double Au = fma(dg[r], uc, -off);
-        if (MODE == FM_APPLY) {
-          if (on[r] && a.out0) a.out0[gidx] = Au;
-          acc = on[r] ? fma(uc, Au, acc) : acc;
-        } else if (MODE == FM_RESID) {
-          const double rv = C0[o] - Au;
-          if (on[r]) a.out0[gidx] = rv;
-          acc = on[r] ? fma(rv, rv, acc) : acc;
-        } else if (MODE == FM_JACOBI) {
-          const double bv = C0[o];
-          const double y = fma(wdi[r], bv - Au, uc);
-          if (on[r]) a.out0[gidx] = y;
-          acc = on[r] ? fma(bv, y, acc) : acc;
-        } else if (MODE == FM_CG) {
-          const double xv = fma(sc, uc, C0[o]);
-          const double rv = fma(-sc, Au, C0[CSZ + o]);
-          if (on[r]) {
-            a.out0[gidx] = xv;
-            a.out1[gidx] = rv;
-          }
-          acc = on[r] ? fma(rv, rv, acc) : acc;
-        } else {  // FM_PAPPLY
-          if (on[r]) a.out0[gidx] = uc;
-          acc = on[r] ? fma(uc, Au, acc) : acc;
+        acc = on[r] ? fma(bv, y, acc) : acc;
+      } else if (MODE == FM_CG) {
+        const double xv = fma(sc, uc, C0[o]);
+        const double rv = fma(-sc, Au, C0[CSZ + o]);
+        if (on[r]) {
+          a.out0[gidx] = xv;
+          a.out1[gidx] = rv;
         }
+        acc = on[r] ? fma(rv, rv, acc) : acc;
+      } else {  // FM_PAPPLY
+        if (on[r]) a.out0[gidx] = uc;
+        acc = on[r] ? fma(uc, Au, acc) : acc;
       }
     }
+  };
+  auto step = [&](int k, const double* vd, const double* vc, const double* vu, const double* vb) {
+    refresh(k);
+#pragma unroll
+    for (int r = 0; r < NPT; ++r) node(k, r, gk, vd[r], vc[r], vu[r], vb[r]);
     gk += N2;
   };
 
@@ -446,6 +452,7 @@ fine_kernel(FineArgs a) {
   // and two TMA issues amortised over two nodes per row
   for (int k0 = kb; k0 < ke; k0 += 2) {
     double u0[NPT], u1[NPT], b0[NPT], b1[NPT];
+    const bool two = k0 + 1 < ke;
     if (XF) {
       wait(k0 + 1);
       transform(k0 + 1, u0, b0);
@@ -462,15 +469,24 @@ fine_kernel(FineArgs a) {
       wait(k0 + 1);
 #pragma unroll
       for (int r = 0; r < NPT; ++r) u0[r] = raw(k0 + 1)[hoff + r * RPP * N];
-    }
-    step(k0, xd, xc, u0, bcv);
-    if (k0 + 1 < ke) {
-      if (!XF) {
+      if (two) {
         wait(k0 + 2);
 #pragma unroll
         for (int r = 0; r < NPT; ++r) u1[r] = raw(k0 + 2)[hoff + r * RPP * N];
       }
-      step(k0 + 1, xc, u0, u1, b0);
+    }
+    if (two && steady(k0) && repeats(k0 + 1)) {
+      // common case: both planes keep the weights; one straight-line block of 2*NPT
+      // independent nodes (latency hiding by ILP)
+#pragma unroll
+      for (int r = 0; r < NPT; ++r) {
+        node(k0, r, gk, xd[r], xc[r], u0[r], bcv[r]);
+        node(k0 + 1, r, gk + N2, xc[r], u0[r], u1[r], b0[r]);
+      }
+      gk += 2 * N2;
+    } else {
+      step(k0, xd, xc, u0, bcv);
+      if (two) step(k0 + 1, xc, u0, u1, b0);
     }
 #pragma unroll
     for (int r = 0; r < NPT; ++r) {
