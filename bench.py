@@ -40,7 +40,8 @@ CONFIGS = {
     0: dict(workload="thermal-block 2x1x1, 32^3 cells, r=10 from 256 train, batch 64, tol 1e-10",
             kind="tb", blocks=(2, 1, 1), n=32, m0=4, r=10, n_train=256, batch=64, delta=1e-10),
     1: dict(workload="thermal-block 2x2x1, 64^3 cells, r=20 from 1024 train, batch 1024, tol 1e-10",
-            kind="tb", blocks=(2, 2, 1), n=64, m0=4, r=20, n_train=1024, batch=1024, delta=1e-10),
+            kind="tb", blocks=(2, 2, 1), n=64, m0=4, r=20, n_train=1024, batch=1024, delta=1e-10,
+            e2e_sizes=[512, 384, 128]),
     2: dict(workload="thermal-block 2x2x2, 128^3 cells, r=30 from 4096 train, batch 512, tol 1e-12",
             kind="tb", blocks=(2, 2, 2), n=128, m0=4, r=30, n_train=4096, batch=512, delta=1e-12),
     3: dict(workload="smooth affine (6 modes), 256^3 cells, r=40 from 2048 train, batch 128, tol 1e-12",
@@ -256,7 +257,10 @@ def run_b200(args, rank, world, dist):
     del ctx, xbuf
     torch.cuda.empty_cache()
     e2e_sub = min(batch, args.e2e_sub or cfg.get("e2e_sub", 512))
-    pipe = rb.HostPipeline(prob, method, model, sub_batch=e2e_sub)
+    sizes = [int(v) for v in args.e2e_sizes.split(",")] if args.e2e_sizes else \
+        cfg.get("e2e_sizes")
+    pipe = rb.HostPipeline(prob, method, model, sub_batch=e2e_sub,
+                           tail=args.e2e_tail or None, sizes=sizes)
     hbuf = torch.empty(batch * n ** 3, dtype=torch.float64, pin_memory=True)
     mus_host = np.ascontiguousarray(test)
     pipe.solve(mus_host, hbuf)  # warm-up (untimed)
@@ -330,7 +334,7 @@ def run_b200(args, rank, world, dist):
                    "t_offline_s": round(t_off, 3)},
         "e2e": {"value": round(e2e_value, 2), "unit": "solves/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "sub_batches": rb.pipeline.schedule(batch, e2e_sub, pipe.tail),
+                "sub_batches": pipe.schedule(batch),
                 "api": "HostPipeline.solve (host mu -> pinned host solutions)",
                 "iterations_match_device_run": bool(e2e_iters_ok)},
         "gpu_launches": int(launches),
@@ -657,6 +661,10 @@ def main():
     ap.add_argument("--chunk", type=int, default=0, help="instances per device sub-batch")
     ap.add_argument("--e2e-sub", type=int, default=0,
                     help="instances per pipelined sub-batch of the end-to-end (host buffer) run")
+    ap.add_argument("--e2e-tail", type=int, default=0,
+                    help="smallest pipelined sub-batch of the end-to-end run (0: sub/4)")
+    ap.add_argument("--e2e-sizes", default="",
+                    help="explicit end-to-end sub-batch sizes, e.g. 512,384,128")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-per-core", type=int, default=2)

@@ -105,6 +105,17 @@ int rbws_mgcg_solve(rbws_batch* b, const double* f, int64_t f_stride, double* x,
                     int l_max, int* iters, double* hist, double* true_res, int* status,
                     void* stream);
 
+/* rbws_mgcg_solve that also streams the solutions to host memory: instance m's
+ * padded solution (n^3 doubles) is copied to x_host + m*host_stride (pinned host,
+ * host_stride >= n^3) on copy_stream as soon as m stops iterating (converged,
+ * breakdown, or l_max), overlapping the downloads with the iterations of the
+ * instances still running.  All copies are enqueued on copy_stream when the call
+ * returns (record an event there to know when x_host is complete). */
+int rbws_mgcg_solve_to_host(rbws_batch* b, const double* f, int64_t f_stride, double* x,
+                            double delta, int l_max, int* iters, double* hist, double* true_res,
+                            int* status, void* stream, double* x_host, int64_t host_stride,
+                            void* copy_stream);
+
 /* One smoothing-level kernel on `level` (>= 1): mode 0 y = A x, 1 y = rhs - A x,
  * 2 y = x + omega (rhs - A x)/diag, 3 y = rhs - A (omega dinv rhs) (the nu=1
  * pre-smoothing residual, multigrid.py:557-558).  (dev) padded vectors. */

@@ -161,6 +161,21 @@ int rbws_mgcg_solve(rbws_batch* b, const double* f, int64_t f_stride, double* x,
   return rbws::pcg_solve(B(b), f, f_stride, x, delta, l_max, o, S(stream));
 }
 
+int rbws_mgcg_solve_to_host(rbws_batch* b, const double* f, int64_t f_stride, double* x,
+                            double delta, int l_max, int* iters, double* hist, double* true_res,
+                            int* status, void* stream, double* x_host, int64_t host_stride,
+                            void* copy_stream) {
+  if (!x_host) RBWS_FAIL("null host buffer");
+  if (host_stride < 0) RBWS_FAIL("negative host stride");
+  const int64_t n = B(b)->h->n;
+  if (host_stride < n * n * n) RBWS_FAIL("host stride smaller than one padded instance");
+  rbws::PcgOut o{iters, hist, true_res, status};
+  o.x_host = x_host;
+  o.host_stride = host_stride;
+  o.copy_stream = S(copy_stream);
+  return rbws::pcg_solve(B(b), f, f_stride, x, delta, l_max, o, S(stream));
+}
+
 int rbws_level_kernel(rbws_batch* b, int level, int mode, const double* x, const double* rhs,
                       double* y, void* stream) {
   Batch* bb = B(b);

@@ -280,6 +280,7 @@ Batch::~Batch() {
   cudaFreeHost(h_nactive);
   cudaFree(partial); cudaFree(partial2); cudaFree(hist);
   for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : dl_ev) cudaEventDestroy(e);
 }
 
 Sep7 Batch::fine_op() const {
@@ -640,6 +641,49 @@ cudaError_t pcg_true(int count, const double* prr, int tiles, const double* scal
   return cudaGetLastError();
 }
 
+// Streaming download: copy the solutions of instances that stopped iterating since the
+// last call (all remaining ones when `all`) to the host on out.copy_stream, after the
+// compute stream reaches this point.  Consecutive instances go in one copy.
+static int stream_download(Batch* b, const double* x, const PcgOut& out, int call, bool all,
+                           cudaStream_t stream) {
+  if (!out.x_host) return 0;
+  const int count = b->count;
+  const int64_t n3 = (int64_t)b->h->n * b->h->n * b->h->n;
+  if (!all) {
+    cudaError_t e = fetch_to_host(b->h_active.data(), b->active, sizeof(int) * count, stream);
+    if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+  }
+  bool any = false;
+  for (int m = 0; m < count && !any; ++m) any = !b->h_sent[m] && (all || !b->h_active[m]);
+  if (!any) return 0;
+  while ((size_t)call >= b->dl_ev.size()) {
+    cudaEvent_t ev;
+    cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+    b->dl_ev.push_back(ev);
+  }
+  cudaEvent_t ev = b->dl_ev[call];
+  cudaError_t e = cudaEventRecord(ev, stream);
+  if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+  e = cudaStreamWaitEvent(out.copy_stream, ev, 0);
+  if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+  int m = 0;
+  while (m < count && e == cudaSuccess) {
+    if (b->h_sent[m] || !(all || !b->h_active[m])) { ++m; continue; }
+    int m1 = m;
+    while (m1 < count && !b->h_sent[m1] && (all || !b->h_active[m1]) &&
+           (out.host_stride == n3 || m1 == m)) {
+      b->h_sent[m1] = 1;
+      ++m1;
+    }
+    e = cudaMemcpyAsync(out.x_host + (int64_t)m * out.host_stride, x + (int64_t)m * n3,
+                        sizeof(double) * n3 * (m1 - m), cudaMemcpyDeviceToHost, out.copy_stream);
+    m = m1;
+  }
+  if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+  return 0;
+}
+
 int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double delta, int l_max,
               const PcgOut& out, cudaStream_t stream) {
   if (!(delta > 0)) RBWS_FAIL("tolerance must be positive");
@@ -679,6 +723,12 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
   e = fetch_to_host(b->h_nactive, b->nactive, sizeof(int), stream);
   if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
   b->cur_active = *b->h_nactive;
+  int dl_call = 0;
+  if (out.x_host) {
+    b->h_active.assign(count, 1);
+    b->h_sent.assign(count, 0);
+    if (stream_download(b, x, out, dl_call++, false, stream)) return 1;  // converged at x0
+  }
   if (*b->h_nactive > 0) {
     if (b->vcycle(L - 1, b->r, b->s, b->partial, act)) return 1;
     count_launch();
@@ -710,6 +760,10 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
       e = fetch_to_host(b->h_nactive, b->nactive, sizeof(int), stream);
       if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
       if (*b->h_nactive == 0) break;
+      // instances that stopped this iteration: their x is final, start the download
+      if (out.x_host && *b->h_nactive < b->cur_active &&
+          stream_download(b, x, out, dl_call++, false, stream))
+        return 1;
       b->cur_active = *b->h_nactive;
       if (b->vcycle(L - 1, b->r, b->s, b->partial, act)) return 1;
       if (pf) t0 = b->prof_begin(stream);
@@ -722,6 +776,8 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
       p_new = (p_new == b->p) ? b->p2 : b->p;
     }
   }
+  // the rest (last to converge, l_max reached, breakdown)
+  if (out.x_host && stream_download(b, x, out, dl_call++, true, stream)) return 1;
   // true residual ||f - A x|| / scale for every instance
   if (e == cudaSuccess) e = fine_resid(op, count, x, f, b->t_res, b->partial, all, fshared);
   if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));

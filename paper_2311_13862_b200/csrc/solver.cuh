@@ -84,6 +84,8 @@ struct Batch {
   double *rs = nullptr, *alpha = nullptr, *beta = nullptr, *scale = nullptr;
   int *active = nullptr, *iters = nullptr, *pstatus = nullptr, *nactive = nullptr;
   int* h_nactive = nullptr;         // pinned
+  std::vector<int> h_active, h_sent;  // streaming download bookkeeping (host)
+  std::vector<cudaEvent_t> dl_ev;     // compute-stream points the downloads wait for
   double* partial = nullptr;        // [cap][max tiles]
   double* partial2 = nullptr;
   double* hist = nullptr;           // [cap][hist_len]
@@ -116,6 +118,11 @@ struct PcgOut {
   double* hist;        // host [count][l_max+1] (NaN padded)
   double* true_res;    // host [count]
   int* status;         // host [count]: 0 ok, 1 breakdown (non-SPD), 2 not converged
+  // optional streaming download: instance m's padded solution (n^3 doubles) is copied to
+  // x_host + m * host_stride on copy_stream as soon as it stops iterating
+  double* x_host = nullptr;
+  int64_t host_stride = 0;
+  cudaStream_t copy_stream = nullptr;
 };
 
 // per-instance PCG scalar kernels (one warp per instance; partials summed in fixed order)

@@ -106,7 +106,7 @@ def mg_vcycle(b, ctx: MgContext, level=None):
 
 def mgcg_solve(A, f, x0, ctx: MgContext, delta: float = 1e-16, l_max: int = 40, mu=None,
                method: str = "mgcg", raise_on_breakdown: bool = True,
-               overwrite_x0: bool = False):
+               overwrite_x0: bool = False, out_host=None, copy_stream=None):
     """Batched MGCG (multigrid.py:564-571 -> krylov.py:267-334).
 
     f: padded rhs, either one instance (shared) or a full batch; x0: padded
@@ -142,9 +142,22 @@ def mgcg_solve(A, f, x0, ctx: MgContext, delta: float = 1e-16, l_max: int = 40, 
     tres = np.zeros(count)
     status = np.zeros(count, dtype=np.int32)
     t0 = time.perf_counter()
-    _native.call("rbws_mgcg_solve", ctx.handle, f.data_ptr(), f_stride, x.data_ptr(),
-                 float(delta), int(l_max), iters.ctypes.data, hist.ctypes.data,
-                 tres.ctypes.data, status.ctypes.data, _native.stream_ptr())
+    if out_host is not None:
+        # stream each instance's solution to pinned host memory as soon as it stops
+        # iterating (copies enqueued on copy_stream)
+        if not out_host.is_pinned() or out_host.numel() < count * n ** 3:
+            raise ValueError("out_host must be a pinned buffer of count * n^3 doubles")
+        if copy_stream is None:
+            raise ValueError("streaming download needs a copy stream")
+        _native.call("rbws_mgcg_solve_to_host", ctx.handle, f.data_ptr(), f_stride,
+                     x.data_ptr(), float(delta), int(l_max), iters.ctypes.data,
+                     hist.ctypes.data, tres.ctypes.data, status.ctypes.data,
+                     _native.stream_ptr(), out_host.data_ptr(), n ** 3,
+                     int(copy_stream.cuda_stream))
+    else:
+        _native.call("rbws_mgcg_solve", ctx.handle, f.data_ptr(), f_stride, x.data_ptr(),
+                     float(delta), int(l_max), iters.ctypes.data, hist.ctypes.data,
+                     tres.ctypes.data, status.ctypes.data, _native.stream_ptr())
     wall = time.perf_counter() - t0
     if raise_on_breakdown and np.any(status & 1):
         bad = int(np.flatnonzero(status & 1)[0])

@@ -1,11 +1,11 @@
 """Host-to-host solving of a large parameter set (the reference's per-parameter
 loop, experiment.py:149-157, as one streamed call).
 
-Parameters are solved in device-resident sub-batches; while sub-batch c+1 is
-being solved on the compute stream, the solutions of sub-batch c are copied to
-pinned host memory on a side stream.  Two multigrid contexts and two solution
-buffers alternate, so the device->host transfer of all but the last
-sub-batch hides behind compute.
+Parameters are solved in device-resident sub-batches.  Each instance's solution
+is copied to pinned host memory on a side stream as soon as it converges
+(rbws_mgcg_solve_to_host), so downloads overlap the iterations of the
+instances still running and the solve of the next sub-batch.  Two multigrid
+contexts and two solution buffers alternate.
 """
 
 from __future__ import annotations
@@ -44,13 +44,18 @@ class HostPipeline:
     """
 
     def __init__(self, problem: ParametricProblem, method: MethodConfig, model=None,
-                 sub_batch: int = 512, nu: int = 1, tail: int | None = None):
+                 sub_batch: int = 512, nu: int = 1, tail: int | None = None,
+                 sizes: list[int] | None = None):
         import torch
         _native.require_cuda()
         if sub_batch < 1:
             raise ValueError("sub_batch must be positive")
         self.problem, self.method, self.model, self.sub = problem, method, model, sub_batch
         self.tail = max(1, sub_batch // 4) if tail is None else max(1, int(tail))
+        self.sizes = list(sizes) if sizes else None   # explicit sub-batch sizes (cycled)
+        if self.sizes:
+            sub_batch = max(sub_batch, max(self.sizes))
+            self.sub = sub_batch
         n = problem.n
         self.ctx = [MgContext(problem, sub_batch, nu=nu) for _ in range(2)]
         self.x = [torch.empty(padded_len(n, sub_batch), dtype=torch.float64, device="cuda")
@@ -64,6 +69,17 @@ class HostPipeline:
         self.solved = [torch.cuda.Event() for _ in range(2)]
         for ev in self.freed:
             ev.record()
+
+    def schedule(self, count: int) -> list[int]:
+        if not self.sizes:
+            return schedule(count, self.sub, self.tail)
+        out, rem, i = [], int(count), 0
+        while rem > 0:
+            take = min(rem, self.sizes[i % len(self.sizes)])
+            out.append(take)
+            rem -= take
+            i += 1
+        return out
 
     def solve(self, mus, out_host):
         import torch
@@ -85,19 +101,19 @@ class HostPipeline:
         import torch
         reports = []
         c0 = 0
-        for c, size in enumerate(schedule(len(mus), self.sub, self.tail)):
+        for c, size in enumerate(self.schedule(len(mus))):
             part = mus[c0:c0 + size]
             s = c % 2
             compute.wait_event(self.freed[s])     # buffer s no longer being copied out
             ctx = mg_context_for(self.problem, part, ctx=self.ctx[s])
+            m = len(part)
+            # each instance's solution streams to the host as soon as it converges,
+            # overlapping the iterations of the instances still running
             x, reps = rbi_pcg_solve(BatchOperator(ctx), self.f, self.method, mg_ctx=ctx,
-                                    l1roc_model=self.model, x0_out=self.x[s])
+                                    l1roc_model=self.model, x0_out=self.x[s],
+                                    out_host=out_host[c0 * n3:(c0 + m) * n3],
+                                    copy_stream=self.copy_stream)
             reports.append(reps)
-            self.solved[s].record(compute)
-            with torch.cuda.stream(self.copy_stream):
-                self.copy_stream.wait_event(self.solved[s])
-                m = len(part)
-                out_host[c0 * n3:(c0 + m) * n3].copy_(x[:m * n3], non_blocking=True)
-                self.freed[s].record(self.copy_stream)
+            self.freed[s].record(self.copy_stream)   # all downloads of buffer s enqueued
             c0 += size
         return SolveReports.concat(reports)

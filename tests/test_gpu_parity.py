@@ -363,3 +363,44 @@ def test_l1roc_online_matches_oracle_with_device_model():
     u4, _ = pkg.l1roc_online(sub, pkg.BatchOperator(ctx), prob.rhs())
     ur4, _, _ = so.l1roc_online(omodel.prefix(4), oprob.operator(test[0]), oprob.rhs())
     assert _rel(pkg.from_padded(u4, 32, len(test))[0], ur4) <= 1e-9
+
+
+def test_mgcg_streaming_download_matches_device():
+    """rbws_mgcg_solve_to_host: every instance's solution lands in pinned host memory
+    (downloaded as soon as it stops iterating) and equals the device result."""
+    pkg = _pkg()
+    prob, _, ospec = _pair((2, 2, 1), 32, 4)
+    mus = op.sample_mus(ospec, 9, seed=33)
+    ctx = pkg.mg_context_for(prob, mus)
+    n3 = 32 ** 3
+    host = torch.full((9 * n3,), float("nan"), dtype=torch.float64).pin_memory()
+    cs = torch.cuda.Stream()
+    x, reps = pkg.mgcg_solve(None, prob.rhs(), None, ctx, delta=1e-10, l_max=60,
+                             out_host=host, copy_stream=cs)
+    cs.synchronize()
+    torch.cuda.synchronize()
+    assert torch.equal(host, x[:9 * n3].cpu())
+    x2, reps2 = pkg.mgcg_solve(None, prob.rhs(), None, ctx, delta=1e-10, l_max=60)
+    assert [r.iterations for r in reps] == [r.iterations for r in reps2]
+    # l_max cap: nothing converges, everything is sent at the end
+    host.fill_(float("nan"))
+    x3, _ = pkg.mgcg_solve(None, prob.rhs(), None, ctx, delta=1e-30, l_max=2,
+                           out_host=host, copy_stream=cs)
+    cs.synchronize()
+    assert torch.equal(host, x3[:9 * n3].cpu())
+
+
+def test_host_pipeline_matches_device_solve():
+    pkg = _pkg()
+    prob, _, ospec = _pair((2, 2, 1), 32, 4)
+    mus = op.sample_mus(ospec, 11, seed=34)
+    ctx = pkg.mg_context_for(prob, mus)
+    cfg = pkg.MethodConfig("mgcg", delta=1e-10, l_max=60)
+    x, reps = pkg.rbi_pcg_solve(pkg.BatchOperator(ctx), prob.rhs(), cfg, mg_ctx=ctx)
+    n3 = 32 ** 3
+    host = torch.empty(11 * n3, dtype=torch.float64).pin_memory()
+    pipe = pkg.HostPipeline(prob, cfg, sub_batch=4, tail=2)
+    reps_p = pipe.solve(mus, host)
+    torch.cuda.synchronize()
+    assert [r.iterations for r in reps_p] == [r.iterations for r in reps]
+    assert _rel(host.numpy(), x[:11 * n3].cpu().numpy()) <= 1e-13
