@@ -36,7 +36,10 @@ struct FT {
 #ifndef RBWS_N512_NPT
 #define RBWS_N512_NPT 2
 #endif
-  static constexpr int NPT = N >= 512 ? RBWS_N512_NPT : ((RPP * 2 <= N) ? 2 : 1);
+#ifndef RBWS_SMALL_NPT
+#define RBWS_SMALL_NPT 2
+#endif
+  static constexpr int NPT = N >= 512 ? RBWS_N512_NPT : ((RPP * 2 <= N) ? RBWS_SMALL_NPT : 1);
   static constexpr int TY = RPP * NPT;
   static constexpr int THREADS = RPP * N;
   static constexpr int HSZ = (TY + 2) * N;  // doubles per staged array with halo rows
@@ -49,7 +52,7 @@ FineGeom fine_geom(int n, int batch, int nz) {
   if (rpp < 1) rpp = 1;
   if (rpp > n) rpp = n;
   g.rpp = rpp;
-  g.npt = n >= 512 ? RBWS_N512_NPT : ((rpp * 2 <= n) ? 2 : 1);
+  g.npt = n >= 512 ? RBWS_N512_NPT : ((rpp * 2 <= n) ? RBWS_SMALL_NPT : 1);
   g.ty = rpp * g.npt;
   g.threads = rpp * n;
   g.ytiles = n / g.ty;
@@ -134,7 +137,10 @@ struct FSmem {
 };
 
 template <int MODE, int N, bool DC>
-__global__ void __launch_bounds__(FT<N>::THREADS, FT<N>::THREADS <= 256 ? 2 : 1)
+#ifndef RBWS_MIN_CTAS
+#define RBWS_MIN_CTAS 2
+#endif
+__global__ void __launch_bounds__(FT<N>::THREADS, FT<N>::THREADS <= 256 ? RBWS_MIN_CTAS : 1)
 fine_kernel(FineArgs a) {
   using G = FT<N>;
   using L = SL<MODE, N, DC>;

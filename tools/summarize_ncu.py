@@ -25,10 +25,13 @@ def launch_list(path):
     rows = _rows(path)
     h = rows[0]
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     per = collections.OrderedDict()
     total = 0.0
     n = 0
     for r in rows[1:]:
+        if mi is not None and r[mi] != "gpu__time_duration.sum":
+            continue
         ns = float(r[vi].replace(",", ""))
         k = short(r[ki])
         t, c = per.get(k, (0.0, 0))
@@ -54,6 +57,9 @@ WANT = [
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "occupancy %"),
     ("launch__registers_per_thread", "regs"),
     ("lts__t_sector_hit_rate.pct", "L2 hit %"),
+    ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "fp64 pipe %"),
+    ("TPC.TriageCompute.sm__pipe_fp64_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+     "fp64 cycles %"),
 ]
 
 
