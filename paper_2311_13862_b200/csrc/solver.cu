@@ -56,11 +56,11 @@ __global__ void fetch_kernel(const unsigned char* __restrict__ src, unsigned cha
 }
 
 cudaError_t fetch_to_host(void* dst, const void* src, size_t bytes, cudaStream_t stream) {
-  static std::mutex mu;
-  static unsigned char* stage = nullptr;
-  static size_t cap = 0;
+  // per-thread staging: host threads driving solves on different streams never wait
+  // for each other's synchronisation
+  static thread_local unsigned char* stage = nullptr;
+  static thread_local size_t cap = 0;
   if (bytes == 0) return cudaSuccess;
-  std::lock_guard<std::mutex> guard(mu);
   if (bytes > cap) {
     if (stage) cudaFreeHost(stage);
     stage = nullptr;
