@@ -41,7 +41,7 @@ CONFIGS = {
             kind="tb", blocks=(2, 1, 1), n=32, m0=4, r=10, n_train=256, batch=64, delta=1e-10),
     1: dict(workload="thermal-block 2x2x1, 64^3 cells, r=20 from 1024 train, batch 1024, tol 1e-10",
             kind="tb", blocks=(2, 2, 1), n=64, m0=4, r=20, n_train=1024, batch=1024, delta=1e-10,
-            e2e_sizes=[512, 384, 128]),
+            e2e_sizes=[1024]),
     2: dict(workload="thermal-block 2x2x2, 128^3 cells, r=30 from 4096 train, batch 512, tol 1e-12",
             kind="tb", blocks=(2, 2, 2), n=128, m0=4, r=30, n_train=4096, batch=512, delta=1e-12),
     3: dict(workload="smooth affine (6 modes), 256^3 cells, r=40 from 2048 train, batch 128, tol 1e-12",
@@ -270,7 +270,10 @@ def run_b200(args, rank, world, dist):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        reps_e = pipe.solve(mus_host, hbuf)
+        # back-to-back calls: a call's last downloads overlap the next call's solves;
+        # every download is inside the timed region (the caller waits for them below)
+        reps_e = pipe.solve(mus_host, hbuf, sync=False)
+    stream.wait_stream(pipe.copy_stream)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")

@@ -69,6 +69,8 @@ class HostPipeline:
         self.solved = [torch.cuda.Event() for _ in range(2)]
         for ev in self.freed:
             ev.record()
+        self.done = torch.cuda.Event()
+        self._slot = 0
 
     def schedule(self, count: int) -> list[int]:
         if not self.sizes:
@@ -81,7 +83,15 @@ class HostPipeline:
             i += 1
         return out
 
-    def solve(self, mus, out_host):
+    def solve(self, mus, out_host, sync: bool = True):
+        """Solve ``mus`` into ``out_host``; returns the SolveReports.
+
+        sync=True: the caller's stream waits for every download (out_host is complete
+        once the caller's stream reaches this point).  sync=False: only the compute is
+        ordered before the caller's later work; the downloads finish on the copy stream
+        (``done`` event) while the next call already computes — back-to-back calls then
+        overlap one call's last downloads with the next call's solves.
+        """
         import torch
         mus = np.ascontiguousarray(mus, dtype=np.float64)
         n3 = self.problem.n ** 3
@@ -94,16 +104,19 @@ class HostPipeline:
         with torch.cuda.stream(compute):
             reports = self._run(mus, out_host, compute, n3)
         caller.wait_stream(compute)
-        caller.wait_stream(self.copy_stream)
+        self.done.record(self.copy_stream)
+        if sync:
+            caller.wait_stream(self.copy_stream)
         return reports
 
     def _run(self, mus, out_host, compute, n3):
         import torch
         reports = []
         c0 = 0
-        for c, size in enumerate(self.schedule(len(mus))):
+        for size in self.schedule(len(mus)):
             part = mus[c0:c0 + size]
-            s = c % 2
+            s = self._slot          # buffers alternate across calls too
+            self._slot ^= 1
             compute.wait_event(self.freed[s])     # buffer s no longer being copied out
             ctx = mg_context_for(self.problem, part, ctx=self.ctx[s])
             m = len(part)

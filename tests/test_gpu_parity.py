@@ -404,3 +404,25 @@ def test_host_pipeline_matches_device_solve():
     torch.cuda.synchronize()
     assert [r.iterations for r in reps_p] == [r.iterations for r in reps]
     assert _rel(host.numpy(), x[:11 * n3].cpu().numpy()) <= 1e-13
+
+
+def test_host_pipeline_back_to_back_async_calls():
+    """sync=False calls overlap one call's downloads with the next call's solves; after
+    waiting on the copy stream every output buffer holds its own call's solutions."""
+    pkg = _pkg()
+    prob, _, ospec = _pair((2, 2, 1), 32, 4)
+    cfg = pkg.MethodConfig("mgcg", delta=1e-10, l_max=60)
+    pipe = pkg.HostPipeline(prob, cfg, sizes=[5, 3])
+    n3 = 32 ** 3
+    outs, want = [], []
+    for seed in (41, 42, 43):
+        mus = op.sample_mus(ospec, 8, seed=seed)
+        ctx = pkg.mg_context_for(prob, mus)
+        x, _ = pkg.rbi_pcg_solve(pkg.BatchOperator(ctx), prob.rhs(), cfg, mg_ctx=ctx)
+        want.append(x[:8 * n3].cpu().numpy())
+        outs.append((mus, torch.empty(8 * n3, dtype=torch.float64).pin_memory()))
+    for mus, buf in outs:
+        pipe.solve(mus, buf, sync=False)
+    pipe.copy_stream.synchronize()
+    for (mus, buf), w in zip(outs, want):
+        assert _rel(buf.numpy(), w) <= 1e-13
