@@ -426,3 +426,23 @@ def test_host_pipeline_back_to_back_async_calls():
     pipe.copy_stream.synchronize()
     for (mus, buf), w in zip(outs, want):
         assert _rel(buf.numpy(), w) <= 1e-13
+
+
+def test_configs2_shape_128_matches_oracle():
+    """configs[2]-shaped problem (thermal 2x2x2, 128^3, tol 1e-12): batched and slab paths
+    against the oracle on one parameter (north_star tolerance: 1e-8 rel. L2, +-1 iteration)."""
+    pkg = _pkg()
+    prob, oprob, ospec = _pair((2, 2, 2), 128, 4)
+    mus = op.sample_mus(ospec, 3, seed=77)
+    ctx = pkg.mg_context_for(prob, mus)
+    x, reps = pkg.mgcg_solve(None, prob.rhs(), None, ctx, delta=1e-12, l_max=60)
+    assert all(r.converged for r in reps)
+    A, f = oprob.operator(mus[0]), oprob.rhs()
+    xr, rr = so.mgcg_solve(A, f, np.zeros_like(f), so.mg_context_for(oprob, mus[0]),
+                           delta=1e-12, l_max=60)
+    got = pkg.from_padded(x, 128, 3)[0]
+    assert abs(reps[0].iterations - rr.iterations) <= 1
+    assert _rel(got, xr) <= 1e-8
+    xs, rs = pkg.slab_mgcg_solve(prob, mus[:1], nslabs=4, delta=1e-12)
+    assert abs(rs.iterations - rr.iterations) <= 1
+    assert _rel(pkg.from_padded(xs, 128, 1)[0], xr) <= 1e-8
