@@ -42,23 +42,6 @@ struct Sep7 {
   const int* fz = nullptr;   // [n+1] plane k's diagonal equals plane k-1's (device, host-built)
 };
 
-// Per-instance symmetric 27-point stencil of a coarse level.
-// coef[(mu*14 + o)*n^3 + X]: o=0 diagonal, o=1..13 forward offsets; the
-// backward coefficient for -o at X is coef[o] at X - o.
-struct St27 {
-  int n;
-  const double* coef;
-};
-
-// forward offsets (dx,dy,dz) with (dz,dy,dx) lexicographically positive
-__host__ __device__ inline void fwd_offset(int o, int& dx, int& dy, int& dz) {
-  // o in 1..13
-  int t = o - 1;
-  if (t < 9) { dz = 1; dy = t / 3 - 1; dx = t % 3 - 1; }
-  else if (t < 12) { dz = 0; dy = 1; dx = t - 10; }
-  else { dz = 0; dy = 0; dx = 1; }
-}
-
 // Deterministic reduction of one double per thread over a (possibly 2D)
 // block.  Result valid in thread 0.  smem must hold >= 32 doubles.
 __device__ __forceinline__ double block_reduce_sum(double v, double* smem) {

@@ -271,7 +271,7 @@ Batch::~Batch() {
   cudaFree(theta);
   for (auto& l : lv) {
     cudaFree(l.b); cudaFree(l.e); cudaFree(l.t1); cudaFree(l.t2); cudaFree(l.t3);
-    cudaFree(l.zero); cudaFree(l.dinv); cudaFree(l.coef); cudaFree(l.u);
+    cudaFree(l.zero); cudaFree(l.dinv); cudaFree(l.u);
   }
   cudaFree(L0); cudaFree(d_status);
   cudaFree(r); cudaFree(p); cudaFree(p2); cudaFree(s); cudaFree(t_res);
@@ -478,15 +478,6 @@ int Batch::vcycle(int lvl, const double* bb, double* out, double* dot_partial,
   if (e == cudaSuccess) e = restrict_launch(n, count, l.t3, c.b, lc);
   if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
   if (vcycle(lvl - 1, c.b, c.e, nullptr, lc)) return 1;
-  if (nu == 0) {
-    // u = P e (u currently the zero vector): write into out
-    e = vec_copy(n, count, l.zero, (int64_t)n * n * n, out, lc);
-    if (e == cudaSuccess) e = prolong_launch(n, count, 0, c.e, out, nullptr, nullptr, 0.0, lc);
-    if (e == cudaSuccess && fine && dot_partial)
-      e = vec_dot(n, count, bb, (int64_t)n * n * n, out, (int64_t)n * n * n, dot_partial, lc);
-    if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
-    return 0;
-  }
   e = prolong_launch(n, count, 0, c.e, u, nullptr, nullptr, 0.0, lc);
   for (int s = 0; s < nu && e == cudaSuccess; ++s) {
     const bool last = (s == nu - 1);

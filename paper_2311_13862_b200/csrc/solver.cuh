@@ -52,7 +52,6 @@ struct LevelBuf {
   double* t3 = nullptr;    // scratch (nu != 1)
   double* zero = nullptr;  // zeros (nu != 1)
   double* dinv = nullptr;  // 1/diag per instance
-  double* coef = nullptr;  // (unused: coarse operators are matrix-free)
   double* u = nullptr;     // pre-scaled rhs w D^-1 b (coarse levels 1..L-2, nu=1)
 };
 

@@ -153,67 +153,6 @@ __global__ void __launch_bounds__(256) sep7_kernel(Sep7 op, int zc, int dot,
 }
 
 template <int Q>
-__global__ void __launch_bounds__(256) sep7_cg_kernel(Sep7 op, int zc,
-                                                      const double* __restrict__ p,
-                                                      double* __restrict__ x,
-                                                      double* __restrict__ r,
-                                                      const double* __restrict__ alpha,
-                                                      double* __restrict__ partial,
-                                                      const int* __restrict__ active) {
-  __shared__ double red[32];
-  const int n = op.n;
-  const int kc = blockIdx.z % zc, mu = blockIdx.z / zc;
-  if (active && !active[mu]) return;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = blockIdx.y * blockDim.y + threadIdx.y;
-  const bool valid = (i >= 1) && (j >= 1);
-  const int kz = n / zc;
-  const int kb = max(1, kc * kz), ke = min(n, (kc + 1) * kz);
-  const int64_t n2 = (int64_t)n * n;
-  const int64_t base = (int64_t)mu * n2 * n;
-  const double a = alpha[mu];
-  double acc = 0.0;
-  if (valid) {
-    ColConst<Q> cc;
-    cc.init(op, mu, i, j);
-    const int64_t col = base + i + (int64_t)n * j;
-    double um = __ldg(p + col + (int64_t)(kb - 1) * n2);
-    double uc = __ldg(p + col + (int64_t)kb * n2);
-    double wzm = cc.wz(kb - 1);
-    for (int k = kb; k < ke; ++k) {
-      const int64_t idx = col + (int64_t)k * n2;
-      const double up = __ldg(p + idx + n2);
-      const double ue = __ldg(p + idx + 1), uw = __ldg(p + idx - 1);
-      const double un = __ldg(p + idx + n), us = __ldg(p + idx - n);
-      double wxp, wxm, wyp, wym;
-      cc.wxy(k, wxp, wxm, wyp, wym);
-      const double wzp = cc.wz(k);
-      const double d = ((wxp + wxm) + (wyp + wym)) + (wzp + wzm);
-      double off = wxp * ue;
-      off = fma(wxm, uw, off);
-      off = fma(wyp, un, off);
-      off = fma(wym, us, off);
-      off = fma(wzp, up, off);
-      off = fma(wzm, um, off);
-      const double Ap = fma(d, uc, -off);
-      x[idx] = fma(a, uc, x[idx]);
-      const double rn = fma(-a, Ap, r[idx]);
-      r[idx] = rn;
-      acc = fma(rn, rn, acc);
-      um = uc;
-      uc = up;
-      wzm = wzp;
-    }
-  }
-  const double s = block_reduce_sum(acc, red);
-  if (threadIdx.x == 0 && threadIdx.y == 0) {
-    const int tile = (blockIdx.y * gridDim.x + blockIdx.x) * zc + kc;
-    const int tiles = gridDim.x * gridDim.y * zc;
-    partial[(int64_t)mu * tiles + tile] = s;
-  }
-}
-
-template <int Q>
 static cudaError_t sep7_launch_q(const Sep7& op, int batch, int mode, int dot, const double* x,
                                  const double* b, const double* dinv, double* y,
                                  double* partial, double omega, const LaunchCtx& lc) {
@@ -257,151 +196,6 @@ cudaError_t sep7_launch(const Sep7& op, int batch, int mode, int dot, const doub
 #define CALL(QQ) sep7_launch_q<QQ>(op, batch, mode, dot, x, b, dinv, y, partial, omega, lc)
   RBWS_Q_DISPATCH(op.Q, CALL)
 #undef CALL
-}
-
-template <int Q>
-static cudaError_t sep7_cg_q(const Sep7& op, int batch, const double* p, double* x, double* r,
-                             const double* alpha, double* partial, const LaunchCtx& lc) {
-  Sep7Geom g = sep7_geom(op.n, batch);
-  dim3 blk(g.tx, g.ty), grd(op.n / g.tx, op.n / g.ty, batch * g.zc);
-  count_launch();
-  sep7_cg_kernel<Q><<<grd, blk, 0, lc.stream>>>(op, g.zc, p, x, r, alpha, partial, lc.active);
-  return cudaGetLastError();
-}
-
-cudaError_t sep7_cg_update(const Sep7& op, int batch, const double* p, double* x, double* r,
-                           const double* alpha, double* partial, const LaunchCtx& lc) {
-#define CALL(QQ) sep7_cg_q<QQ>(op, batch, p, x, r, alpha, partial, lc)
-  RBWS_Q_DISPATCH(op.Q, CALL)
-#undef CALL
-}
-
-// ========================================================================
-// coarse levels: per-instance symmetric 27-point
-// ========================================================================
-
-__constant__ int c_off_dx[14], c_off_dy[14], c_off_dz[14];
-
-static bool g_offsets_ready = false;
-static cudaError_t ensure_offsets() {
-  if (g_offsets_ready) return cudaSuccess;
-  int dx[14] = {0}, dy[14] = {0}, dz[14] = {0};
-  for (int o = 1; o < 14; ++o) fwd_offset(o, dx[o], dy[o], dz[o]);
-  cudaError_t e = cudaMemcpyToSymbol(c_off_dx, dx, sizeof(dx));
-  if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_off_dy, dy, sizeof(dy));
-  if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_off_dz, dz, sizeof(dz));
-  if (e == cudaSuccess) g_offsets_ready = true;
-  return e;
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(256) st27_kernel(St27 op, const double* __restrict__ x,
-                                                   const double* __restrict__ b,
-                                                   const double* __restrict__ dinv,
-                                                   double* __restrict__ y,
-                                                   const int* __restrict__ active,
-                                                   double omega) {
-  const int n = op.n;
-  const int mu = blockIdx.y;
-  if (active && !active[mu]) return;
-  const int64_t n3 = (int64_t)n * n * n;
-  const int64_t X = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (X >= n3) return;
-  const int i = X % n, j = (X / n) % n, k = X / ((int64_t)n * n);
-  if (i == 0 || j == 0 || k == 0) return;
-  const int64_t base = (int64_t)mu * n3;
-  const double* C = op.coef + (int64_t)mu * 14 * n3;
-  auto ld = [&](int64_t idx) -> double {
-    if (MODE == MODE_PRE) return omega * __ldg(dinv + base + idx) * __ldg(b + base + idx);
-    return __ldg(x + base + idx);
-  };
-  const double c0 = __ldg(C + X);
-  double Au = c0 * ld(X);
-#pragma unroll
-  for (int o = 1; o < 14; ++o) {
-    const int64_t off = c_off_dx[o] + (int64_t)n * (c_off_dy[o] + (int64_t)n * c_off_dz[o]);
-    Au = fma(__ldg(C + o * n3 + X), ld(X + off), Au);
-    Au = fma(__ldg(C + o * n3 + X - off), ld(X - off), Au);
-  }
-  double out;
-  if (MODE == MODE_APPLY) out = Au;
-  else if (MODE == MODE_RESID || MODE == MODE_PRE) out = __ldg(b + base + X) - Au;
-  else if (MODE == MODE_JACOBI) out = ld(X) + omega * __ldg(dinv + base + X) * (__ldg(b + base + X) - Au);
-  else out = 1.0 / c0;
-  y[base + X] = out;
-}
-
-cudaError_t st27_launch(const St27& op, int batch, int mode, const double* x, const double* b,
-                        const double* dinv, double* y, double omega, const LaunchCtx& lc) {
-  cudaError_t e = ensure_offsets();
-  if (e != cudaSuccess) return e;
-  const int64_t n3 = (int64_t)op.n * op.n * op.n;
-  dim3 blk(256), grd((unsigned)((n3 + 255) / 256), batch);
-  count_launch();
-  switch (mode) {
-    case MODE_APPLY: st27_kernel<MODE_APPLY><<<grd, blk, 0, lc.stream>>>(op, x, b, dinv, y, lc.active, omega); break;
-    case MODE_RESID: st27_kernel<MODE_RESID><<<grd, blk, 0, lc.stream>>>(op, x, b, dinv, y, lc.active, omega); break;
-    case MODE_JACOBI: st27_kernel<MODE_JACOBI><<<grd, blk, 0, lc.stream>>>(op, x, b, dinv, y, lc.active, omega); break;
-    case MODE_PRE: st27_kernel<MODE_PRE><<<grd, blk, 0, lc.stream>>>(op, x, b, dinv, y, lc.active, omega); break;
-    default: return cudaErrorInvalidValue;
-  }
-  return cudaGetLastError();
-}
-
-// 1D factor entry T(i, i+o), o in {-1,0,1}; fac points at [2][n+1] (diag, upper)
-__device__ __forceinline__ double fac1(const double* f, int n1, int i, int o) {
-  if (o == 0) return __ldg(f + i);
-  if (o > 0) return __ldg(f + n1 + i);
-  return __ldg(f + n1 + i - 1);
-}
-
-__global__ void __launch_bounds__(256) st27_build_kernel(int n, int Q,
-                                                         const double* __restrict__ fac,
-                                                         const double* __restrict__ theta,
-                                                         double* __restrict__ coef,
-                                                         double* __restrict__ dinv) {
-  const int mu = blockIdx.y;
-  const int64_t n3 = (int64_t)n * n * n;
-  const int64_t X = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (X >= n3) return;
-  const int i = X % n, j = (X / n) % n, k = X / ((int64_t)n * n);
-  double* C = coef + (int64_t)mu * 14 * n3;
-  const bool ghost = (i == 0 || j == 0 || k == 0);
-  const int n1 = n + 1;
-  double c0 = 0.0;
-  for (int o = 0; o < 14; ++o) {
-    int dx = 0, dy = 0, dz = 0;
-    if (o > 0) { dx = c_off_dx[o]; dy = c_off_dy[o]; dz = c_off_dz[o]; }
-    double c = 0.0;
-    if (!ghost) {
-      for (int q = 0; q < Q; ++q) {
-        const double t = theta[mu * Q + q];
-        double s = 0.0;
-        for (int d = 0; d < 3; ++d) {
-          const double* f = fac + (size_t)((q * 3 + d) * 3) * 2 * n1;
-          const double fx = fac1(f + 0 * 2 * n1, n1, i, dx);
-          const double fy = fac1(f + 1 * 2 * n1, n1, j, dy);
-          const double fzv = fac1(f + 2 * 2 * n1, n1, k, dz);
-          s += fx * fy * fzv;
-        }
-        c = fma(t, s, c);
-      }
-    }
-    C[o * n3 + X] = c;
-    if (o == 0) c0 = c;
-  }
-  dinv[(int64_t)mu * n3 + X] = ghost ? 0.0 : 1.0 / c0;
-}
-
-cudaError_t st27_build(int n, int Q, const double* fac, const double* theta, int batch,
-                       double* coef, double* dinv, cudaStream_t stream) {
-  cudaError_t e = ensure_offsets();
-  if (e != cudaSuccess) return e;
-  const int64_t n3 = (int64_t)n * n * n;
-  dim3 blk(256), grd((unsigned)((n3 + 255) / 256), batch);
-  count_launch();
-  st27_build_kernel<<<grd, blk, 0, stream>>>(n, Q, fac, theta, coef, dinv);
-  return cudaGetLastError();
 }
 
 // ========================================================================
@@ -525,80 +319,6 @@ cudaError_t prolong_launch(int nf, int batch, int mode, const double* ec, double
 // coarsest level: dense Cholesky per instance
 // ========================================================================
 
-__global__ void coarse_factor_kernel(int n0, const double* __restrict__ coef,
-                                     double* __restrict__ Lout, int* __restrict__ status) {
-  extern __shared__ double A[];
-  const int m1 = n0 - 1, m = m1 * m1 * m1;
-  const int mu = blockIdx.x;
-  const int64_t n3 = (int64_t)n0 * n0 * n0;
-  const double* C = coef + (int64_t)mu * 14 * n3;
-  for (int t = threadIdx.x; t < m * m; t += blockDim.x) A[t] = 0.0;
-  __syncthreads();
-  for (int r = threadIdx.x; r < m; r += blockDim.x) {
-    const int i = r % m1 + 1, j = (r / m1) % m1 + 1, k = r / (m1 * m1) + 1;
-    const int64_t X = i + (int64_t)n0 * (j + (int64_t)n0 * k);
-    A[r * m + r] = C[X];
-    for (int o = 1; o < 14; ++o) {
-      int dx, dy, dz;
-      fwd_offset(o, dx, dy, dz);
-      // forward neighbour
-      int a = i + dx, bq = j + dy, c = k + dz;
-      if (a >= 1 && a <= m1 && bq >= 1 && bq <= m1 && c >= 1 && c <= m1) {
-        const int col = (a - 1) + m1 * ((bq - 1) + m1 * (c - 1));
-        A[r * m + col] = C[o * n3 + X];
-      }
-      a = i - dx; bq = j - dy; c = k - dz;
-      if (a >= 1 && a <= m1 && bq >= 1 && bq <= m1 && c >= 1 && c <= m1) {
-        const int col = (a - 1) + m1 * ((bq - 1) + m1 * (c - 1));
-        const int64_t Y = a + (int64_t)n0 * (bq + (int64_t)n0 * c);
-        A[r * m + col] = C[o * n3 + Y];
-      }
-    }
-  }
-  __syncthreads();
-  // right-looking Cholesky, lower triangle
-  __shared__ int bad;
-  if (threadIdx.x == 0) bad = 0;
-  __syncthreads();
-  for (int c = 0; c < m; ++c) {
-    if (threadIdx.x == 0) {
-      const double dd = A[c * m + c];
-      if (!(dd > 0.0)) bad = 1;
-      A[c * m + c] = sqrt(dd > 0.0 ? dd : 1.0);
-    }
-    __syncthreads();
-    const double piv = A[c * m + c];
-    for (int r = c + 1 + threadIdx.x; r < m; r += blockDim.x) A[r * m + c] /= piv;
-    __syncthreads();
-    for (int t = threadIdx.x; t < (m - c - 1) * (m - c - 1); t += blockDim.x) {
-      const int r = c + 1 + t / (m - c - 1), s = c + 1 + t % (m - c - 1);
-      if (s <= r) A[r * m + s] -= A[r * m + c] * A[s * m + c];
-    }
-    __syncthreads();
-  }
-  double* L = Lout + (int64_t)mu * m * m;
-  for (int t = threadIdx.x; t < m * m; t += blockDim.x) {
-    const int r = t / m, s = t % m;
-    L[t] = (s <= r) ? A[t] : 0.0;
-  }
-  if (threadIdx.x == 0 && status) status[mu] = bad;
-}
-
-cudaError_t coarse_factor(int n0, int batch, const double* coef, double* L, int* status,
-                          cudaStream_t stream) {
-  const int m1 = n0 - 1, m = m1 * m1 * m1;
-  const size_t smem = (size_t)m * m * sizeof(double);
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(coarse_factor_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  count_launch();
-  coarse_factor_kernel<<<batch, 128, smem, stream>>>(n0, coef, L, status);
-  return cudaGetLastError();
-}
-
 // one warp per instance: forward then backward substitution
 __global__ void coarse_solve_kernel(int n0, int batch, const double* __restrict__ Lall,
                                     const double* __restrict__ b, double* __restrict__ x,
@@ -708,51 +428,6 @@ cudaError_t vec_dot(int n, int batch, const double* x, int64_t x_stride, const d
   dim3 blk(256), grd(vec_tiles(n), batch);
   count_launch();
   dot_kernel<<<grd, blk, 0, lc.stream>>>(n3, x, x_stride, y, y_stride, partial, lc.active);
-  return cudaGetLastError();
-}
-
-__global__ void __launch_bounds__(256) xpby_kernel(int64_t n3, const double* __restrict__ x,
-                                                   const double* __restrict__ beta,
-                                                   double* __restrict__ y,
-                                                   const int* __restrict__ active) {
-  const int mu = blockIdx.y;
-  if (active && !active[mu]) return;
-  const double bt = beta ? beta[mu] : 0.0;
-  const int64_t base = (int64_t)mu * n3;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n3;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    y[base + idx] = fma(bt, y[base + idx], __ldg(x + base + idx));
-  }
-}
-
-cudaError_t vec_xpby(int n, int batch, const double* x, const double* beta, double* y,
-                     const LaunchCtx& lc) {
-  const int64_t n3 = (int64_t)n * n * n;
-  int gx = (int)((n3 + 1023) / 1024);
-  dim3 blk(256), grd(gx, batch);
-  count_launch();
-  xpby_kernel<<<grd, blk, 0, lc.stream>>>(n3, x, beta, y, lc.active);
-  return cudaGetLastError();
-}
-
-__global__ void __launch_bounds__(256) copy_kernel(int64_t n3, const double* __restrict__ x,
-                                                   int64_t xs, double* __restrict__ y,
-                                                   const int* __restrict__ active) {
-  const int mu = blockIdx.y;
-  if (active && !active[mu]) return;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n3;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    y[(int64_t)mu * n3 + idx] = __ldg(x + mu * xs + idx);
-  }
-}
-
-cudaError_t vec_copy(int n, int batch, const double* x, int64_t x_stride, double* y,
-                     const LaunchCtx& lc) {
-  const int64_t n3 = (int64_t)n * n * n;
-  int gx = (int)((n3 + 1023) / 1024);
-  dim3 blk(256), grd(gx, batch);
-  count_launch();
-  copy_kernel<<<grd, blk, 0, lc.stream>>>(n3, x, x_stride, y, lc.active);
   return cudaGetLastError();
 }
 

@@ -35,18 +35,6 @@ Sep7Geom sep7_geom(int n, int batch);
 cudaError_t sep7_launch(const Sep7& op, int batch, int mode, int dot, const double* x,
                         const double* b, const double* dinv, double* y, double* partial,
                         double omega, const LaunchCtx& lc);
-// x += alpha p ; r -= alpha A p ; partial = sum r^2
-cudaError_t sep7_cg_update(const Sep7& op, int batch, const double* p, double* x, double* r,
-                           const double* alpha, double* partial, const LaunchCtx& lc);
-
-// ---- coarse levels (per-instance 27-point) -------------------------------
-cudaError_t st27_launch(const St27& op, int batch, int mode, const double* x, const double* b,
-                        const double* dinv, double* y, double omega, const LaunchCtx& lc);
-
-// coefficients of a coarse level from its Kronecker 1D factors
-// fac[((t*3 + a)*2 + s)*(n+1) + i], t = q*3+d, s=0 diag / s=1 upper off-diagonal
-cudaError_t st27_build(int n, int Q, const double* fac, const double* theta, int batch,
-                       double* coef, double* dinv, cudaStream_t stream);
 
 // ---- transfers -----------------------------------------------------------
 // bc = P^T r  (coarse n_c = n_f/2); with dinv_c/uc also uc = omega dinv_c bc
@@ -58,8 +46,6 @@ cudaError_t prolong_launch(int nf, int batch, int mode, const double* ec, double
                            const double* b, const double* dinv, double omega, const LaunchCtx& lc);
 
 // ---- coarsest dense solve ------------------------------------------------
-cudaError_t coarse_factor(int n0, int batch, const double* coef, double* L, int* status,
-                          cudaStream_t stream);
 cudaError_t coarse_solve(int n0, int batch, const double* L, const double* b, double* x,
                          const LaunchCtx& lc);
 
@@ -74,11 +60,5 @@ cudaError_t vec_dot(int n, int batch, const double* x, int64_t x_stride, const d
 // partial[t] = sum x*y over `count` contiguous doubles, (count + 2047)/2048 tiles
 cudaError_t vec_dot_range(int64_t count, const double* x, const double* y, double* partial,
                           cudaStream_t stream);
-// y = a*x + beta[mu]*y   (beta may be null -> 0);  ghosts untouched (they are 0)
-cudaError_t vec_xpby(int n, int batch, const double* x, const double* beta, double* y,
-                     const LaunchCtx& lc);
-// y = x (instance-strided broadcast allowed: x_stride 0)
-cudaError_t vec_copy(int n, int batch, const double* x, int64_t x_stride, double* y,
-                     const LaunchCtx& lc);
 
 }  // namespace rbws
