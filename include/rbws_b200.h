@@ -80,6 +80,12 @@ int rbws_batch_destroy(rbws_batch* b);
  * instances whose coarsest operator failed to factor in *n_bad (host). */
 int rbws_batch_setup(rbws_batch* b, const double* theta, int count, int* n_bad, void* stream);
 
+/* PCG iterations after the first run as one CUDA graph with a device-side WHILE
+ * condition (no host synchronisation between iterations; cached per solve shape).
+ * Default on (environment RBWS_GRAPH=0 turns it off); not used while the event
+ * profiler or a streaming download is active. */
+int rbws_batch_set_graph(rbws_batch* b, int enable);
+
 /* y = A^level(mu) x for every instance (ParametricProblem.operator(mu, level) @ x,
  * grid.py:274-283).  x, y: (dev) padded vectors of that level. */
 int rbws_apply(rbws_batch* b, int level, const double* x, double* y, void* stream);

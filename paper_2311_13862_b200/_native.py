@@ -34,6 +34,7 @@ SIGNATURES = {
     "rbws_batch_create": [_pp, _vp, _c_int, _c_int, _c_double],
     "rbws_batch_destroy": [_vp],
     "rbws_batch_setup": [_vp, _vp, _c_int, _ip, _vp],
+    "rbws_batch_set_graph": [_vp, _c_int],
     "rbws_apply": [_vp, _c_int, _vp, _vp, _vp],
     "rbws_jacobi_sweep": [_vp, _c_int, _vp, _vp, _vp, _vp],
     "rbws_restrict": [_c_int, _c_int, _vp, _vp, _vp],

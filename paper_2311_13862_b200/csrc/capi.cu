@@ -91,6 +91,12 @@ int rbws_batch_destroy(rbws_batch* b) {
   return 0;
 }
 
+int rbws_batch_set_graph(rbws_batch* b, int enable) {
+  if (!b) RBWS_FAIL("null batch");
+  B(b)->use_graph = enable != 0;
+  return 0;
+}
+
 int rbws_batch_setup(rbws_batch* b, const double* theta, int count, int* n_bad, void* stream) {
   Batch* bb = B(b);
   if (rbws::batch_setup(bb, theta, count, S(stream))) return 1;

@@ -22,6 +22,7 @@ constexpr int kMaxTerms = 8;
 
 // process-wide count of kernel launches issued by this library
 void count_launch();
+void count_launches(int64_t k);
 int64_t launch_count();
 
 RBWS_HD int64_t vec_doubles(int n, int batch) {

@@ -86,6 +86,7 @@ cudaError_t fetch_to_host(void* dst, const void* src, size_t bytes, cudaStream_t
 
 static std::atomic<int64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void count_launches(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 template <class T>
@@ -281,6 +282,10 @@ Batch::~Batch() {
   cudaFree(partial); cudaFree(partial2); cudaFree(hist);
   for (cudaEvent_t e : ev) cudaEventDestroy(e);
   for (cudaEvent_t e : dl_ev) cudaEventDestroy(e);
+  if (gexec) cudaGraphExecDestroy(gexec);
+  if (graph) cudaGraphDestroy(graph);
+  if (gstream) cudaStreamDestroy(gstream);
+  for (cudaEvent_t e : gev) if (e) cudaEventDestroy(e);
 }
 
 Sep7 Batch::fine_op() const {
@@ -297,6 +302,10 @@ int batch_create(Batch** out, Hierarchy* h, int cap, int nu, double omega, int m
   if (nu == 0) RBWS_FAIL("nu = 0 (no smoothing) is not supported by the batched V-cycle");
   Batch* b = new Batch();
   b->h = h; b->cap = cap; b->nu = nu; b->omega = omega;
+  {
+    const char* g = getenv("RBWS_GRAPH");
+    b->use_graph = g ? atoi(g) != 0 : b->use_graph;
+  }
   const int L = h->levels;
   b->maxl = (maxl <= 0 || maxl > L) ? L : maxl;
   cudaError_t e = dalloc(&b->theta, (size_t)cap * h->Q);
@@ -675,6 +684,110 @@ static int stream_download(Batch* b, const double* x, const PcgOut& out, int cal
   return 0;
 }
 
+// device-side loop condition: keep iterating while any instance is active
+__global__ void pcg_cond_kernel(cudaGraphConditionalHandle h, const int* nactive) {
+  cudaGraphSetConditional(h, *nactive > 0 ? 1u : 0u);
+}
+
+// PCG iterations 1.. as one CUDA graph: a WHILE conditional node whose body (two
+// iterations, so the search-direction buffers alternate back) is captured from the same
+// launches the host loop issues; the condition is set on the device from the active
+// count, so no host synchronisation happens between iterations.
+static int pcg_graph_run(Batch* b, const Sep7& op, double* x, int tiles, double delta,
+                         int l_max, int hl, const LaunchCtx& act_in, cudaStream_t user) {
+  const int count = b->count, L = b->h->levels;
+  // the legacy default stream cannot be captured: capture and launch on a private stream
+  // ordered after / before the caller's
+  cudaStream_t stream = user;
+  if (user == nullptr || user == cudaStreamLegacy) {
+    if (!b->gstream) {
+      cudaError_t e0 = cudaStreamCreateWithFlags(&b->gstream, cudaStreamNonBlocking);
+      if (e0 == cudaSuccess) e0 = cudaEventCreateWithFlags(&b->gev[0], cudaEventDisableTiming);
+      if (e0 == cudaSuccess) e0 = cudaEventCreateWithFlags(&b->gev[1], cudaEventDisableTiming);
+      if (e0 != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e0));
+    }
+    stream = b->gstream;
+    cudaError_t e0 = cudaEventRecord(b->gev[0], user);
+    if (e0 == cudaSuccess) e0 = cudaStreamWaitEvent(stream, b->gev[0], 0);
+    if (e0 != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e0));
+  }
+  LaunchCtx act = act_in;
+  act.stream = stream;
+  const bool hit = b->gexec && b->gkey_x == x && b->gkey_count == count &&
+                   b->gkey_delta == delta && b->gkey_lmax == l_max && b->gkey_hl == hl &&
+                   b->gkey_active == act.active;
+  cudaError_t e = cudaSuccess;
+  if (!hit) {
+    if (b->gexec) cudaGraphExecDestroy(b->gexec);
+    if (b->graph) cudaGraphDestroy(b->graph);
+    b->gexec = nullptr;
+    b->graph = nullptr;
+    cudaGraph_t g;
+    e = cudaGraphCreate(&g, 0);
+    if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+    b->graph = g;
+    cudaGraphConditionalHandle hnd;
+    e = cudaGraphConditionalHandleCreate(&hnd, g, 1, cudaGraphCondAssignDefault);
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = hnd;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    if (e == cudaSuccess) e = cudaGraphAddNode(&node, g, nullptr, 0, &cp);
+    if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    const int64_t c0 = launch_count();
+    e = cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0,
+                                      cudaStreamCaptureModeRelaxed);
+    if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+    int rc = 0;
+    for (int half = 0; half < 2 && !rc && e == cudaSuccess; ++half) {
+      double* p_old = half ? b->p2 : b->p;
+      double* p_new = half ? b->p : b->p2;
+      e = fine_papply(op, count, b->s, p_old, b->beta, p_new, b->partial, act);
+      if (e != cudaSuccess) break;
+      count_launch();
+      pcg_alpha_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, tiles, b->rs,
+                                                             b->alpha, b->active, b->pstatus);
+      e = fine_cg_update(op, count, p_new, x, b->r, b->alpha, b->partial, act);
+      if (e == cudaSuccess) e = cudaMemsetAsync(b->nactive, 0, sizeof(int), stream);
+      if (e != cudaSuccess) break;
+      count_launch();
+      pcg_check_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, tiles, b->scale,
+                                                             delta, l_max, b->hist, hl, b->active,
+                                                             b->iters, b->nactive);
+      rc = b->vcycle(L - 1, b->r, b->s, b->partial, act);
+      if (rc) break;
+      count_launch();
+      pcg_beta_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, tiles, b->rs,
+                                                            b->beta, b->active);
+    }
+    if (!rc && e == cudaSuccess) {
+      count_launch();
+      pcg_cond_kernel<<<1, 1, 0, stream>>>(hnd, b->nactive);
+      e = cudaGetLastError();
+    }
+    cudaGraph_t captured = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(stream, &captured);
+    if (rc) return 1;
+    if (e == cudaSuccess) e = ec;
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&b->gexec, g, 0);
+    if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+    b->gbody_launches = launch_count() - c0;
+    count_launches(-b->gbody_launches);  // captured, not executed
+    b->gkey_x = x; b->gkey_count = count; b->gkey_delta = delta; b->gkey_lmax = l_max;
+    b->gkey_hl = hl; b->gkey_active = act.active;
+  }
+  e = cudaGraphLaunch(b->gexec, stream);
+  if (e == cudaSuccess && stream != user) {
+    e = cudaEventRecord(b->gev[1], stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(user, b->gev[1], 0);
+  }
+  if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+  return 0;
+}
+
 int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double delta, int l_max,
               const PcgOut& out, cudaStream_t stream) {
   if (!(delta > 0)) RBWS_FAIL("tolerance must be positive");
@@ -695,6 +808,7 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
   }
   const int hl = b->hist_len;
   const Sep7 op = b->fine_op();
+  bool graph_ran = false;
   const int tiles = fine_geom(n, count).tiles;
   LaunchCtx all{stream, nullptr};
   LaunchCtx act{stream, b->active};
@@ -730,6 +844,9 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
     double* p_new = b->p;
     const double* beta = nullptr;
     const bool pf = b->prof_on;
+    // the device-side loop has no per-iteration host readback: not with the event
+    // profiler or the streaming download, which act on the host between iterations
+    const bool use_graph = b->use_graph && !pf && !out.x_host;
     for (int k = 0; k < l_max; ++k) {
       int t0 = pf ? b->prof_begin(stream) : -1;
       e = fine_papply(op, count, b->s, p_old, beta, p_new, b->partial, act);
@@ -765,6 +882,11 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
       beta = b->beta;
       p_old = p_new;
       p_new = (p_new == b->p) ? b->p2 : b->p;
+      if (use_graph && k == 0 && k + 1 < l_max) {  // iterations 1.. on the device
+        if (pcg_graph_run(b, op, x, tiles, delta, l_max, hl, act, stream)) return 1;
+        graph_ran = true;
+        break;
+      }
     }
   }
   // the rest (last to converge, l_max reached, breakdown)
@@ -787,6 +909,13 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
   if (e == cudaSuccess && out.status)
     e = fetch_to_host(out.status, b->pstatus, sizeof(int) * count, stream);
   if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+  if (graph_ran) {  // launches replayed by the graph: body x replays
+    std::vector<int> it(count);
+    e = fetch_to_host(it.data(), b->iters, sizeof(int) * count, stream);
+    if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+    const int mx = *std::max_element(it.begin(), it.end());
+    count_launches((int64_t)std::max(1, mx / 2) * b->gbody_launches);
+  }
   if (b->prof_on) b->prof_flush();
   if (out.hist)
     for (int m = 0; m < count; ++m)

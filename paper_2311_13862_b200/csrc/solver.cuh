@@ -85,6 +85,17 @@ struct Batch {
   int* h_nactive = nullptr;         // pinned
   std::vector<int> h_active, h_sent;  // streaming download bookkeeping (host)
   std::vector<cudaEvent_t> dl_ev;     // compute-stream points the downloads wait for
+  // device-side PCG loop (iterations 1..) as a conditional CUDA graph, cached per solve shape
+  bool use_graph = true;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  const double* gkey_x = nullptr;
+  const int* gkey_active = nullptr;
+  int gkey_count = 0, gkey_lmax = 0, gkey_hl = 0;
+  double gkey_delta = 0.0;
+  int64_t gbody_launches = 0;
+  cudaStream_t gstream = nullptr;     // capture/launch stream when the caller's is the legacy one
+  cudaEvent_t gev[2] = {nullptr, nullptr};
   double* partial = nullptr;        // [cap][max tiles]
   double* partial2 = nullptr;
   double* hist = nullptr;           // [cap][hist_len]

@@ -446,3 +446,24 @@ def test_configs2_shape_128_matches_oracle():
     xs, rs = pkg.slab_mgcg_solve(prob, mus[:1], nslabs=4, delta=1e-12)
     assert abs(rs.iterations - rr.iterations) <= 1
     assert _rel(pkg.from_padded(xs, 128, 1)[0], xr) <= 1e-8
+
+
+def test_device_side_graph_loop_matches_host_loop():
+    """PCG iterations as a conditional CUDA graph (device-side WHILE) give bitwise the
+    host-driven loop's solutions, iteration counts and histories."""
+    pkg = _pkg()
+    from paper_2311_13862_b200 import _native
+    prob, _, ospec = _pair((2, 2, 1), 32, 4)
+    mus = op.sample_mus(ospec, 6, seed=51)
+    ctx = pkg.mg_context_for(prob, mus)
+    out = {}
+    for g in (0, 1, 1):   # the second graph run reuses the cached executable
+        _native.call("rbws_batch_set_graph", ctx.handle, g)
+        x, reps = pkg.mgcg_solve(None, prob.rhs(), None, ctx, delta=1e-11, l_max=60)
+        out.setdefault(g, []).append((x.clone(), [r.history for r in reps]))
+    x0, h0 = out[0][0]
+    for x1, h1 in out[1]:
+        assert torch.equal(x0, x1) and h0 == h1
+    # l_max cap inside the graph
+    x, reps = pkg.mgcg_solve(None, prob.rhs(), None, ctx, delta=1e-30, l_max=5)
+    assert all(r.iterations == 5 and not r.converged for r in reps)
