@@ -30,15 +30,15 @@ constexpr int kThreads = 256;  // threads per CTA (one per grid column of the ti
 // of the CTA, NPT rows per thread, TY = RPP*NPT rows per tile.  All shared-memory
 // and global offsets below are compile-time multiples of N, so a neighbour read
 // is one LDS with an immediate offset from a per-plane base register.
-template <int N>
-struct FT {
-  static constexpr int RPP = (kThreads / N) < 1 ? 1 : ((kThreads / N) < N ? kThreads / N : N);
 #ifndef RBWS_N512_NPT
 #define RBWS_N512_NPT 2
 #endif
 #ifndef RBWS_SMALL_NPT
 #define RBWS_SMALL_NPT 2
 #endif
+template <int N, int T = kThreads>
+struct FT {
+  static constexpr int RPP = (T / N) < 1 ? 1 : ((T / N) < N ? T / N : N);
   static constexpr int NPT = N >= 512 ? RBWS_N512_NPT : ((RPP * 2 <= N) ? RBWS_SMALL_NPT : 1);
   static constexpr int TY = RPP * NPT;
   static constexpr int THREADS = RPP * N;
@@ -46,9 +46,14 @@ struct FT {
   static constexpr int CSZ = TY * N;        // doubles per staged array, tile rows only
 };
 
-FineGeom fine_geom(int n, int batch, int nz) {
+// threads per CTA of a mode: the prolongation + post-smoothing kernel runs 512-thread
+// CTAs (16-row tiles) at N = 64: half the halo-row work per node, measured -5 %
+int fine_mode_threads(int mode, int n) { return (mode == 6 && n == 64) ? 512 : kThreads; }
+
+FineGeom fine_geom(int n, int batch, int nz, int threads) {
   FineGeom g;
-  int rpp = kThreads / n;
+  if (threads <= 0) threads = kThreads;
+  int rpp = threads / n;
   if (rpp < 1) rpp = 1;
   if (rpp > n) rpp = n;
   g.rpp = rpp;
@@ -99,6 +104,10 @@ enum FineMode : int {
 // tile, reloaded from the 1/diag vector only on planes where the diagonal changes along z
 // (thermal blocks: a few planes), instead of streaming 1/diag with every plane (8 bytes
 // per node less; bitwise the same values)
+// tile geometry of a mode (see fine_mode_threads)
+template <int MODE, int N>
+using FTM = FT<N, (MODE == FM_POSTP && N == 64) ? 512 : kThreads>;
+
 template <int MODE, int N, bool DC = false>
 struct SL {
   // PRE / PAPPLY stencil a derived vector (w dinv b, s + beta p_old): each staged
@@ -116,21 +125,22 @@ struct SL {
 
 // FM_POSTP stages, with every even fine plane p, coarse plane p/2 + 1 rows
 // [cj0, cj0 + CR) (cj0 = first coarse row the tile's rows j0-1 .. j0+TY touch)
-template <int N>
+template <int N, int TY_ = FT<N>::TY>
 struct FCoarse {
   static constexpr int NCC = N / 2;
-  static constexpr int CR = FT<N>::TY / 2 + 3;
+  static constexpr int CR = TY_ / 2 + 3;
   static constexpr int CSZ = CR * NCC;
 };
 
 template <int N, int MODE, bool DC = false>
 struct FSmem {
   using L = SL<MODE, N, DC>;
-  static constexpr int STAGE = L::NH * FT<N>::HSZ + L::NC * FT<N>::CSZ +
-                               (MODE == FM_POSTP ? FCoarse<N>::CSZ : 0);
+  using G = FTM<MODE, N>;
+  static constexpr int STAGE = L::NH * G::HSZ + L::NC * G::CSZ +
+                               (MODE == FM_POSTP ? FCoarse<N, G::TY>::CSZ : 0);
   // raw ring, transformed ring, cached w/diag tile (DC)
-  static constexpr int RING = L::S * STAGE + (L::XF ? L::U * FT<N>::HSZ : 0) +
-                              (DC ? FT<N>::HSZ : 0);
+  static constexpr int RING = L::S * STAGE + (L::XF ? L::U * G::HSZ : 0) +
+                              (DC ? G::HSZ : 0);
   static size_t bytes(int np, int Q) {
     return 64 + 4 * (kMaxKz + 4) + 8 * (((size_t)np * 3 * Q + 1) & ~(size_t)1) + 8 * (size_t)RING;
   }
@@ -140,9 +150,10 @@ template <int MODE, int N, bool DC>
 #ifndef RBWS_MIN_CTAS
 #define RBWS_MIN_CTAS 2
 #endif
-__global__ void __launch_bounds__(FT<N>::THREADS, FT<N>::THREADS <= 256 ? RBWS_MIN_CTAS : 1)
+__global__ void __launch_bounds__(FTM<MODE, N>::THREADS,
+                                  FTM<MODE, N>::THREADS <= 256 ? RBWS_MIN_CTAS : 1)
 fine_kernel(FineArgs a) {
-  using G = FT<N>;
+  using G = FTM<MODE, N>;
   using L = SL<MODE, N, DC>;
   constexpr bool XF = L::XF;
   constexpr int NH = L::NH, NC = L::NC, S = L::S, U = L::U;
@@ -200,14 +211,14 @@ fine_kernel(FineArgs a) {
   }
 
   const int skip = (j0 == 0) ? 1 : 0;  // row j0-1 does not exist for the first tile
-  constexpr int NCC = FCoarse<N>::NCC;
+  constexpr int NCC = FCoarse<N, TY>::NCC;
   const int cj0 = (j0 == 0) ? 0 : (j0 >> 1) - 1;  // first staged coarse row (FM_POSTP)
   auto issue = [&](int p) {
     const int sl = (p - p_first) % S;
     double* st = ring + sl * STAGE;
     const uint32_t hbytes = (uint32_t)((TY + 2 - skip) * N * 8);
     constexpr uint32_t cbytes = (uint32_t)(CSZ * 8);
-    constexpr uint32_t ebytes = (uint32_t)(FCoarse<N>::CSZ * 8);
+    constexpr uint32_t ebytes = (uint32_t)(FCoarse<N, TY>::CSZ * 8);
     // coarse plane p/2 + 1 (for the z march of P ec) with every even fine plane;
     // none past the last coarse plane (its ghost plane p/2 = n/2 is never advanced from)
     const bool stage_c = (MODE == FM_POSTP) && !(p & 1) && ((p >> 1) + 1 <= NCC);
@@ -517,7 +528,7 @@ fine_kernel(FineArgs a) {
 
 template <int MODE, int N, bool DC>
 static cudaError_t fine_launch_mnd(const FineArgs& a, int batch, cudaStream_t stream) {
-  using G = FT<N>;
+  using G = FTM<MODE, N>;
   if (a.g.threads != G::THREADS || a.g.ty != G::TY) return cudaErrorInvalidValue;
   const int np = a.g.kz + 2;
   const size_t smem = FSmem<N, MODE, DC>::bytes(np, a.op.Q);
@@ -559,7 +570,7 @@ static cudaError_t fine_launch_m(const FineArgs& a, int batch, cudaStream_t stre
 static cudaError_t fine_launch(int mode, FineArgs& a, int batch, cudaStream_t stream) {
   if (a.op.Q < 1 || a.op.Q > kMaxTerms) return cudaErrorInvalidValue;
   if (a.zhi <= 0) { a.zlo = 0; a.zhi = a.op.n; }
-  a.g = fine_geom(a.op.n, batch, a.zhi - a.zlo);
+  a.g = fine_geom(a.op.n, batch, a.zhi - a.zlo, fine_mode_threads(mode, a.op.n));
   switch (mode) {
     case FM_APPLY: return fine_launch_m<FM_APPLY>(a, batch, stream);
     case FM_RESID: return fine_launch_m<FM_RESID>(a, batch, stream);

@@ -16,7 +16,13 @@ struct FineGeom {
   int tiles;    // partial-sum slots per instance = ytiles * zc
 };
 // nz: planes per instance processed (0 = n; slabs pass their owned plane count)
-FineGeom fine_geom(int n, int batch, int nz = 0);
+FineGeom fine_geom(int n, int batch, int nz = 0, int threads = 0);
+// threads per CTA of fine kernel mode `mode` on an n-cell grid (geometry of its dot partials)
+int fine_mode_threads(int mode, int n);
+// partial-sum slots per instance of the prolongation + post-smoothing kernel (the V-cycle's dot)
+inline int fine_post_tiles(int n, int batch, int nz = 0) {
+  return fine_geom(n, batch, nz, fine_mode_threads(6, n)).tiles;
+}
 
 // y = A x (y may be null), partial (may be null) = x . A x
 cudaError_t fine_apply(const Sep7& op, int batch, const double* x, double* y, double* partial,

@@ -159,7 +159,7 @@ int Slab::vcycle(int l, int vb, int vout, bool dot, cudaStream_t st) {
     for (size_t i = 0; i < parts.size(); ++i) {
       const SlabPart& P = parts[i];
       RBWS_CK(fine_post_prolong(fop, 1, V(P, l, vb), V(P, l, SV_DINV), ec[i], V(P, l, vout),
-                                omega, dot ? partial + (int64_t)P.rank * tiles : nullptr,
+                                omega, dot ? partial + (int64_t)P.rank * vtiles : nullptr,
                                 lc(P, l, st, true)));
     }
   } else {
@@ -225,9 +225,11 @@ int slab_create(Slab** out, Hierarchy* h, int nslabs, int first, int nloc, Comm*
   }
   const int nz = n / nslabs;
   s->tiles = fine_geom(n, 1, nz).tiles;
+  s->vtiles = fine_post_tiles(n, 1, nz);
   s->ftiles = (int)(((int64_t)nz * n * n + 2047) / 2048);
   if (e == cudaSuccess) e = zalloc(&s->theta, kMaxTerms);
-  if (e == cudaSuccess) e = zalloc(&s->partial, (size_t)nslabs * s->tiles);
+  if (e == cudaSuccess)
+    e = zalloc(&s->partial, (size_t)nslabs * std::max(s->tiles, s->vtiles));
   if (e == cudaSuccess) e = zalloc(&s->partial2, (size_t)nslabs * s->ftiles);
   for (double** pp : {&s->rs, &s->alpha, &s->beta, &s->scale, &s->tres})
     if (e == cudaSuccess) e = zalloc(pp, 1);
@@ -324,7 +326,7 @@ int slab_solve(Slab* S, double delta, int l_max, int* iters, double* hist, doubl
   }
   const int hl = S->hist_len;
   const Sep7 op{n, h->Q, h->d_face, h->d_node, S->theta, h->fine_zchg, h->d_fzsame};
-  const int T = S->tiles;
+  const int T = S->tiles, VT = S->vtiles;  // VT: the V-cycle's (post-smoothing) dot slots
   auto part_of = [&](const SlabPart& P) { return S->partial + (int64_t)P.rank * T; };
   // ||f||^2 over the owned planes, r = f - A x0, |r|^2
   for (auto& P : S->parts)
@@ -344,8 +346,8 @@ int slab_solve(Slab* S, double delta, int l_max, int* iters, double* hist, doubl
   if (*S->h_nactive > 0) {
     if (S->xchg(l, SV_R, XCHG_BOTH, st)) return 1;
     if (S->vcycle(l, SV_R, SV_S, true, st)) return 1;
-    if (S->gather_partials(S->partial, T, st)) return 1;
-    RBWS_CK(pcg_rs(1, S->partial, R * T, S->rs, S->active, st));
+    if (S->gather_partials(S->partial, VT, st)) return 1;
+    RBWS_CK(pcg_rs(1, S->partial, R * VT, S->rs, S->active, st));
     int p_old = -1, p_new = SV_P;
     for (int k = 0; k < l_max; ++k) {
       if (S->xchg(l, SV_S, XCHG_BOTH, st)) return 1;
@@ -367,8 +369,8 @@ int slab_solve(Slab* S, double delta, int l_max, int* iters, double* hist, doubl
       if (*S->h_nactive == 0) break;
       if (S->xchg(l, SV_R, XCHG_BOTH, st)) return 1;
       if (S->vcycle(l, SV_R, SV_S, true, st)) return 1;
-      if (S->gather_partials(S->partial, T, st)) return 1;
-      RBWS_CK(pcg_beta(1, S->partial, R * T, S->rs, S->beta, S->active, st));
+      if (S->gather_partials(S->partial, VT, st)) return 1;
+      RBWS_CK(pcg_beta(1, S->partial, R * VT, S->rs, S->beta, S->active, st));
       p_old = p_new;
       p_new = (p_new == SV_P) ? SV_P2 : SV_P;
     }

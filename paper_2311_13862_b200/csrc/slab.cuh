@@ -43,7 +43,7 @@ struct Slab {
          *beta = nullptr, *scale = nullptr, *tres = nullptr, *hist = nullptr;
   int *active = nullptr, *iters = nullptr, *status = nullptr, *nactive = nullptr;
   int* h_nactive = nullptr;
-  int tiles = 0, ftiles = 0, hist_len = 0;
+  int tiles = 0, vtiles = 0, ftiles = 0, hist_len = 0;
   bool ready = false;
 
   ~Slab();

@@ -352,8 +352,9 @@ int batch_create(Batch** out, Hierarchy* h, int cap, int nu, double omega, int m
     for (int c = 2; c <= cap; c *= 2) t = std::max<int64_t>(t, sep7_geom(h->n, c).tiles);
     t = std::max<int64_t>(t, sep7_geom(h->n, cap).tiles);
     t = std::max<int64_t>(t, vec_tiles(h->n));
-    for (int c = 1; c <= cap; c *= 2) t = std::max<int64_t>(t, fine_geom(h->n, c).tiles);
-    t = std::max<int64_t>(t, fine_geom(h->n, cap).tiles);
+    for (int c = 1; c <= cap; c *= 2)
+      t = std::max<int64_t>(t, std::max(fine_geom(h->n, c).tiles, fine_post_tiles(h->n, c)));
+    t = std::max<int64_t>(t, std::max(fine_geom(h->n, cap).tiles, fine_post_tiles(h->n, cap)));
     b->partial_cap = t;
     e = dalloc(&b->partial, (size_t)cap * t);
     if (e == cudaSuccess) e = dalloc(&b->partial2, (size_t)cap * t);
@@ -693,8 +694,9 @@ __global__ void pcg_cond_kernel(cudaGraphConditionalHandle h, const int* nactive
 // iterations, so the search-direction buffers alternate back) is captured from the same
 // launches the host loop issues; the condition is set on the device from the active
 // count, so no host synchronisation happens between iterations.
-static int pcg_graph_run(Batch* b, const Sep7& op, double* x, int tiles, double delta,
-                         int l_max, int hl, const LaunchCtx& act_in, cudaStream_t user) {
+static int pcg_graph_run(Batch* b, const Sep7& op, double* x, int tiles, int vtiles,
+                         double delta, int l_max, int hl, const LaunchCtx& act_in,
+                         cudaStream_t user) {
   const int count = b->count, L = b->h->levels;
   // the legacy default stream cannot be captured: capture and launch on a private stream
   // ordered after / before the caller's
@@ -760,7 +762,7 @@ static int pcg_graph_run(Batch* b, const Sep7& op, double* x, int tiles, double 
       rc = b->vcycle(L - 1, b->r, b->s, b->partial, act);
       if (rc) break;
       count_launch();
-      pcg_beta_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, tiles, b->rs,
+      pcg_beta_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, vtiles, b->rs,
                                                             b->beta, b->active);
     }
     if (!rc && e == cudaSuccess) {
@@ -810,6 +812,8 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
   const Sep7 op = b->fine_op();
   bool graph_ran = false;
   const int tiles = fine_geom(n, count).tiles;
+  // the V-cycle's dot partials come from the post-smoothing kernel's geometry (nu = 1)
+  const int vtiles = (b->nu == 1) ? fine_post_tiles(n, count) : tiles;
   LaunchCtx all{stream, nullptr};
   LaunchCtx act{stream, b->active};
   const int fshared = (f_stride == 0);
@@ -837,7 +841,7 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
   if (*b->h_nactive > 0) {
     if (b->vcycle(L - 1, b->r, b->s, b->partial, act)) return 1;
     count_launch();
-    pcg_rs_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, tiles, b->rs, b->active);
+    pcg_rs_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, vtiles, b->rs, b->active);
     // search directions ping-pong between p and p2 (the p-update reads the old
     // direction with a halo, so it cannot be updated in place)
     double* p_old = nullptr;
@@ -876,14 +880,14 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
       if (b->vcycle(L - 1, b->r, b->s, b->partial, act)) return 1;
       if (pf) t0 = b->prof_begin(stream);
       count_launch();
-      pcg_beta_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, tiles, b->rs,
+      pcg_beta_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, vtiles, b->rs,
                                                             b->beta, b->active);
       if (pf) b->prof_end(PROF_SCALARS, t0, stream);
       beta = b->beta;
       p_old = p_new;
       p_new = (p_new == b->p) ? b->p2 : b->p;
       if (use_graph && k == 0 && k + 1 < l_max) {  // iterations 1.. on the device
-        if (pcg_graph_run(b, op, x, tiles, delta, l_max, hl, act, stream)) return 1;
+        if (pcg_graph_run(b, op, x, tiles, vtiles, delta, l_max, hl, act, stream)) return 1;
         graph_ran = true;
         break;
       }
