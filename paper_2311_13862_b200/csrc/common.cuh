@@ -41,6 +41,8 @@ struct Sep7 {
   const double* theta;
   int zchg = -1;             // planes where the diagonal changes along z (-1: unknown)
   const int* fz = nullptr;   // [n+1] plane k's diagonal equals plane k-1's (device, host-built)
+  const double* wface = nullptr;  // stored +x/+y/+z face weights (3 vectors), or null
+  int64_t wstride = 0;
 };
 
 // Deterministic reduction of one double per thread over a (possibly 2D)

@@ -132,6 +132,10 @@ struct FCoarse {
   static constexpr int CSZ = CR * NCC;
 };
 
+#ifndef RBWS_MIN_CTAS
+#define RBWS_MIN_CTAS 2
+#endif
+
 template <int N, int MODE, bool DC = false>
 struct FSmem {
   using L = SL<MODE, N, DC>;
@@ -146,10 +150,11 @@ struct FSmem {
   }
 };
 
-template <int MODE, int N, bool DC>
-#ifndef RBWS_MIN_CTAS
-#define RBWS_MIN_CTAS 2
-#endif
+// SCW ("stored coefficient weights"): the face weights come from per-instance arrays
+// (Sep7::wface, built at batch setup) instead of registers refreshed from the separable
+// tables — for coefficients whose z factors change on most planes, where the refresh
+// (5Q terms per node and plane) dominates; bitwise the same weights
+template <int MODE, int N, bool DC, bool SCW>
 __global__ void __launch_bounds__(FTM<MODE, N>::THREADS,
                                   FTM<MODE, N>::THREADS <= 256 ? RBWS_MIN_CTAS : 1)
 fine_kernel(FineArgs a) {
@@ -298,6 +303,7 @@ fine_kernel(FineArgs a) {
   };
 #pragma unroll
   for (int r = 0; r < NPT; ++r) {  // plane kb-1: its z face (kb-1, kb) is wzm of plane kb
+    if (SCW) break;
     weights(r, zf);
     wzm[r] = wzp[r];
   }
@@ -390,6 +396,7 @@ fine_kernel(FineArgs a) {
   int64_t gk = base + (int64_t)(j0 + rl0) * N + i + (int64_t)kb * N2;  // (i, j0+rl0, k)
   // face weights for plane k (refreshed only where the z factors change; CTA-uniform)
   auto refresh = [&](int k) {
+    if (SCW) return;
     if (k == kb || !repeats(k)) {
 #pragma unroll
       for (int r = 0; r < NPT; ++r) {
@@ -409,29 +416,56 @@ fine_kernel(FineArgs a) {
     }
   };
   // true when plane k keeps the current weights (no refresh work)
-  auto steady = [&](int k) { return k != kb && repeats(k) && !pend; };
+  auto steady = [&](int k) { return SCW || (k != kb && repeats(k) && !pend); };
+  // SCW: stored weights; wzs[r] = z-face weight below the current node (previous plane)
+  const double* WX = op.wface;
+  const double* WY = op.wface + op.wstride;
+  const double* WZ = op.wface + 2 * op.wstride;
+  double wzs[NPT];
+#pragma unroll
+  for (int r = 0; r < NPT; ++r)
+    wzs[r] = SCW ? __ldg(WZ + base + (int64_t)(j0 + rl0 + r * RPP) * N + i + (int64_t)(kb - 1) * N2)
+                 : 0.0;
   // the NPT nodes of one plane: vd / vc / vu = own-column input at k-1 / k / k+1, vb = own b
   auto node = [&](int k, int r, int64_t gk_, double ud, double uc, double uu, double vbr) {
     const double* P0 = (XF ? uring + (k - p_first) % U * HSZ : raw(k)) + hoff;
     const double* C0 = raw(k) + NH * HSZ + coff;
     const int o = r * RPP * N;  // compile-time after unrolling
     const double ue = P0[o + 1], uw = P0[o - 1], un = P0[o + N], us = P0[o - N];
-    // shallow FMA tree (a dependent chain of 6 would be latency bound)
-    const double offx = fma(wxm[r], uw, wxp[r] * ue);
-    const double offy = fma(wym[r], us, wyp[r] * un);
-    const double offz = fma(wzm[r], ud, wzp[r] * uu);
-    const double off = (offx + offy) + offz;
     const int64_t gidx = gk_ + o;
+    double xp, xm, yp, ym, zp, zm, dgr, wdr;
+    if constexpr (SCW) {
+      xp = __ldg(WX + gidx);
+      xm = __ldg(WX + gidx - 1);
+      yp = __ldg(WY + gidx);
+      ym = __ldg(WY + gidx - N);
+      zp = __ldg(WZ + gidx);
+      zm = wzs[r];
+      wzs[r] = zp;
+      dgr = ((xp + xm) + (yp + ym)) + (zp + zm);
+      // post-smoothing: w/diag from the staged 1/diag (no per-node division)
+      // (the raw ring slot of plane k may already be refilled: read 1/diag through L2)
+      wdr = (MODE == FM_POSTP) ? om * __ldg(a.h1 + gidx) : (MODE == FM_JACOBI ? om / dgr : 0.0);
+    } else {
+      xp = wxp[r]; xm = wxm[r]; yp = wyp[r]; ym = wym[r]; zp = wzp[r]; zm = wzm[r];
+      dgr = dg[r];
+      wdr = wdi[r];
+    }
+    // shallow FMA tree (a dependent chain of 6 would be latency bound)
+    const double offx = fma(xm, uw, xp * ue);
+    const double offy = fma(ym, us, yp * un);
+    const double offz = fma(zm, ud, zp * uu);
+    const double off = (offx + offy) + offz;
     if (MODE == FM_PRE) {
       // b - A (w D^-1 b) = (1 - w) b + off(w D^-1 b): the diagonal term is w b
       if (on[r]) a.out0[gidx] = fma(1.0 - om, vbr, off);
     } else if (MODE == FM_POSTP) {
-      const double Au = fma(dg[r], uc, -off);
-      const double y = fma(wdi[r], vbr - Au, uc);
+      const double Au = fma(dgr, uc, -off);
+      const double y = fma(wdr, vbr - Au, uc);
       if (on[r]) a.out0[gidx] = y;
       acc = on[r] ? fma(vbr, y, acc) : acc;
     } else {
-      const double Au = fma(dg[r], uc, -off);
+      const double Au = fma(dgr, uc, -off);
       if (MODE == FM_APPLY) {
         if (on[r] && a.out0) a.out0[gidx] = Au;
         acc = on[r] ? fma(uc, Au, acc) : acc;
@@ -441,7 +475,7 @@ fine_kernel(FineArgs a) {
         acc = on[r] ? fma(rv, rv, acc) : acc;
       } else if (MODE == FM_JACOBI) {
         const double bv = C0[o];
-        const double y = fma(wdi[r], bv - Au, uc);
+        const double y = fma(wdr, bv - Au, uc);
         if (on[r]) a.out0[gidx] = y;
         acc = on[r] ? fma(bv, y, acc) : acc;
       } else if (MODE == FM_CG) {
@@ -526,7 +560,7 @@ fine_kernel(FineArgs a) {
   }
 }
 
-template <int MODE, int N, bool DC>
+template <int MODE, int N, bool DC, bool SCW = false>
 static cudaError_t fine_launch_mnd(const FineArgs& a, int batch, cudaStream_t stream) {
   using G = FTM<MODE, N>;
   if (a.g.threads != G::THREADS || a.g.ty != G::TY) return cudaErrorInvalidValue;
@@ -535,19 +569,20 @@ static cudaError_t fine_launch_mnd(const FineArgs& a, int batch, cudaStream_t st
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   static size_t attr = 48 * 1024;
   if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(fine_kernel<MODE, N, DC>,
+    cudaError_t e = cudaFuncSetAttribute(fine_kernel<MODE, N, DC, SCW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = smem;
   }
   dim3 grd(1, a.g.ytiles, batch * a.g.zc);
   count_launch();
-  fine_kernel<MODE, N, DC><<<grd, G::THREADS, smem, stream>>>(a);
+  fine_kernel<MODE, N, DC, SCW><<<grd, G::THREADS, smem, stream>>>(a);
   return cudaGetLastError();
 }
 
 template <int MODE, int N>
 static cudaError_t fine_launch_mn(const FineArgs& a, int batch, cudaStream_t stream) {
+  if (a.op.wface) return fine_launch_mnd<MODE, N, false, true>(a, batch, stream);
   if constexpr (MODE == FM_PRE || MODE == FM_POSTP)
     if (a.dc) return fine_launch_mnd<MODE, N, true>(a, batch, stream);
   return fine_launch_mnd<MODE, N, false>(a, batch, stream);
@@ -581,6 +616,60 @@ static cudaError_t fine_launch(int mode, FineArgs& a, int batch, cudaStream_t st
     case FM_POSTP: return fine_launch_m<FM_POSTP>(a, batch, stream);
     default: return cudaErrorInvalidValue;
   }
+}
+
+// Stored face weights of every instance (batch setup of the SCW kernels): for node
+// (i, j, k) the weight of its +x, +y, +z face, with the same expression and summation
+// order as the kernels' register refresh (fine_kernel::weights), so both paths agree
+// bitwise.  Faces on the Dirichlet boundary planes (a coordinate 0) are included where a
+// kernel reads them as the -x / -y / -z face of an interior node.
+template <int Q>
+__global__ void __launch_bounds__(256) fine_faces_kernel(Sep7 op, int n, double* __restrict__ wx,
+                                                        double* __restrict__ wy,
+                                                        double* __restrict__ wz) {
+  const int n1 = n + 1;
+  const int64_t n2 = (int64_t)n * n, n3 = n2 * n;
+  const int mu = blockIdx.z;
+  const int64_t X = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (X >= n3) return;
+  const int i = X % n, j = (X / n) % n, k = (int)(X / n2);
+  const double* th = op.theta + (size_t)mu * Q;
+  double a0 = 0.0, a2 = 0.0, a4 = 0.0;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const double* F = op.face + (size_t)q * 3 * n;
+    const double* NF = op.node + (size_t)q * 9 * n1;
+    const double t = th[q];
+    const double zx = NF[(0 * 3 + 2) * n1 + k], zy = NF[(1 * 3 + 2) * n1 + k];
+    const double zz = (k < n) ? F[2 * n + k] : 0.0;
+    const double tx = t * NF[(0 * 3 + 1) * n1 + j] * zx;
+    const double tyv = t * NF[(1 * 3 + 0) * n1 + i] * zy;
+    const double tz = t * NF[(2 * 3 + 0) * n1 + i] * NF[(2 * 3 + 1) * n1 + j];
+    a0 = fma(F[0 * n + i], tx, a0);
+    a2 = fma(F[1 * n + j], tyv, a2);
+    a4 = fma(tz, zz, a4);
+  }
+  const int64_t o = (int64_t)mu * n3 + X;
+  wx[o] = (j >= 1 && k >= 1) ? a0 : 0.0;
+  wy[o] = (i >= 1 && k >= 1) ? a2 : 0.0;
+  wz[o] = (i >= 1 && j >= 1) ? a4 : 0.0;
+}
+
+cudaError_t fine_faces(const Sep7& op, int batch, double* wface, int64_t wstride,
+                       cudaStream_t stream) {
+  const int n = op.n;
+  const int64_t n3 = (int64_t)n * n * n;
+  dim3 grd((unsigned)((n3 + 255) / 256), 1, batch);
+  count_launch();
+#define RBWS_FQ(QQ) \
+  case QQ: fine_faces_kernel<QQ><<<grd, 256, 0, stream>>>(op, n, wface, wface + wstride, \
+                                                          wface + 2 * wstride); break;
+  switch (op.Q) {
+    RBWS_FQ(1) RBWS_FQ(2) RBWS_FQ(3) RBWS_FQ(4) RBWS_FQ(5) RBWS_FQ(6) RBWS_FQ(7) RBWS_FQ(8)
+    default: return cudaErrorInvalidValue;
+  }
+#undef RBWS_FQ
+  return cudaGetLastError();
 }
 
 // 1/diag of the finest operator for every instance (batch setup); weights are

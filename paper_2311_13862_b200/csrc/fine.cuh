@@ -45,6 +45,12 @@ cudaError_t fine_pre(const Sep7& op, int batch, const double* b, const double* d
 cudaError_t fine_post_prolong(const Sep7& op, int batch, const double* b, const double* dinv,
                               const double* ec, double* y, double omega, double* partial,
                               const LaunchCtx& lc);
+// stored face weights (+x, +y, +z face of every node) for the SCW kernels: wface holds three
+// padded batch vectors at stride wstride doubles
+cudaError_t fine_faces(const Sep7& op, int batch, double* wface, int64_t wstride,
+                       cudaStream_t stream);
+// planes with a new diagonal above which the stored-weight kernels are used
+constexpr int kFineStoredWeightsMinChanges = 17;
 // x += alpha p, r -= alpha A p, partial = |r|^2
 cudaError_t fine_cg_update(const Sep7& op, int batch, const double* p, double* x, double* r,
                            const double* alpha, double* partial, const LaunchCtx& lc);

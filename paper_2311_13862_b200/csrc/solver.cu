@@ -270,6 +270,7 @@ int hierarchy_create(Hierarchy** out, int n, int m0, int Q, const double* face,
 
 Batch::~Batch() {
   cudaFree(theta);
+  cudaFree(wface);
   for (auto& l : lv) {
     cudaFree(l.b); cudaFree(l.e); cudaFree(l.t1); cudaFree(l.t2); cudaFree(l.t3);
     cudaFree(l.zero); cudaFree(l.dinv); cudaFree(l.u);
@@ -293,6 +294,8 @@ Sep7 Batch::fine_op() const {
   op.n = h->n; op.Q = h->Q; op.face = h->d_face; op.node = h->d_node; op.theta = theta;
   op.zchg = h->fine_zchg;
   op.fz = h->d_fzsame;
+  op.wface = wface;
+  op.wstride = wstride;
   return op;
 }
 
@@ -336,6 +339,19 @@ int batch_create(Batch** out, Hierarchy* h, int cap, int nu, double omega, int m
   }
   const size_t VF = (size_t)vec_doubles(h->n, cap);
   if (e == cudaSuccess) e = dalloc(&b->d_status, cap);
+  // coefficients whose z factors change on most planes: stored face weights (SCW kernels);
+  // without the memory the register-refresh kernels run instead
+  const char* scw_env = getenv("RBWS_SCW");  // "0": keep the register-refresh kernels
+  const bool scw = !(scw_env && atoi(scw_env) == 0);
+  if (e == cudaSuccess && scw && b->maxl == L && h->fine_zchg >= kFineStoredWeightsMinChanges) {
+    b->wstride = (int64_t)VF;
+    if (dalloc(&b->wface, (size_t)3 * VF) != cudaSuccess) {
+      (void)cudaGetLastError();
+      b->wface = nullptr;
+    } else {
+      e = cudaMemset(b->wface, 0, sizeof(double) * 3 * VF);
+    }
+  }
   for (double** pp : {&b->r, &b->p, &b->p2, &b->s, &b->t_res}) {
     if (b->maxl < L) break;  // coarse levels only (slab path): no finest-level PCG vectors
     if (e == cudaSuccess) e = dalloc(pp, VF);
@@ -373,8 +389,9 @@ int batch_setup(Batch* b, const double* theta, int count, cudaStream_t stream) {
   if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
   const int L = h->levels;
   LaunchCtx lc{stream, nullptr};
-  // fine level 1/diag
+  // fine level 1/diag (and the stored face weights of the SCW kernels)
   if (b->maxl == L) e = fine_dinv(b->fine_op(), count, h->d_fzsame, b->lv[L - 1].dinv, stream);
+  if (e == cudaSuccess && b->wface) e = fine_faces(b->fine_op(), count, b->wface, b->wstride, stream);
   // coarse levels are matrix-free (Kronecker factors): only 1/diag is stored
   for (int l = 1; l < std::min(L - 1, b->maxl) && e == cudaSuccess; ++l)
     e = coarse_launch(4, h->coarse_op(l), b->theta, count,

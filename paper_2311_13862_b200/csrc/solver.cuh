@@ -75,6 +75,8 @@ struct Batch {
   int maxl = 0;                     // levels with buffers (< levels: coarse-only, slab path)
   double omega = 0.7;
   double* theta = nullptr;          // [cap][Q]
+  double* wface = nullptr;          // stored fine face weights [3][cap n^3 + 2n^2] (SCW kernels)
+  int64_t wstride = 0;
   std::vector<LevelBuf> lv;
   double* L0 = nullptr;             // coarsest Cholesky factors [cap][m][m]
   int* d_status = nullptr;          // coarse factor status per instance

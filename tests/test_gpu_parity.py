@@ -467,3 +467,23 @@ def test_device_side_graph_loop_matches_host_loop():
     # l_max cap inside the graph
     x, reps = pkg.mgcg_solve(None, prob.rhs(), None, ctx, delta=1e-30, l_max=5)
     assert all(r.iterations == 5 and not r.converged for r in reps)
+
+
+def test_stored_weight_kernels_match_register_kernels(monkeypatch):
+    """Coefficients whose z factors change on every plane use stored face weights (SCW);
+    they reproduce the register-refresh kernels (smooth affine coefficient)."""
+    pkg = _pkg()
+    prob, oprob, ospec = _pair("smooth", 32, 4)
+    mus = op.sample_mus(ospec, 3, seed=61)
+    out = []
+    for scw in ("1", "0"):
+        monkeypatch.setenv("RBWS_SCW", scw)
+        ctx = pkg.MgContext(prob, 3).setup(mus)
+        x, reps = pkg.mgcg_solve(None, prob.rhs(), None, ctx, delta=1e-12, l_max=60)
+        out.append((x.clone(), [r.history for r in reps]))
+        del ctx
+    # the post-smoothing takes w/diag from the 1/diag vector (one rounding apart)
+    assert _rel(out[0][0].cpu().numpy(), out[1][0].cpu().numpy()) <= 1e-12
+    for h0, h1 in zip(out[0][1], out[1][1]):
+        assert len(h0) == len(h1)
+        np.testing.assert_allclose(h0, h1, rtol=1e-9)
