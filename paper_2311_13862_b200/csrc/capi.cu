@@ -119,7 +119,7 @@ int rbws_apply(rbws_batch* b, int level, const double* x, double* y, void* strea
   if (level == h->levels - 1) {
     RBWS_CHECK(rbws::fine_apply(bb->fine_op(), bb->count, x, y, nullptr, lc));
   } else {
-    RBWS_CHECK(rbws::coarse_launch(0, h->coarse_op(level), bb->theta, bb->count, x, nullptr, y, 0.0, lc));
+    RBWS_CHECK(rbws::coarse_launch(0, bb->cop(level), bb->theta, bb->count, x, nullptr, y, 0.0, lc));
   }
   return 0;
 }
@@ -134,7 +134,7 @@ int rbws_jacobi_sweep(rbws_batch* b, int level, const double* x, const double* r
   if (level == h->levels - 1) {
     RBWS_CHECK(rbws::fine_jacobi(bb->fine_op(), bb->count, x, rhs, y, bb->omega, nullptr, lc));
   } else {
-    RBWS_CHECK(rbws::coarse_launch(2, h->coarse_op(level), bb->theta, bb->count, x, rhs, y, bb->omega, lc));
+    RBWS_CHECK(rbws::coarse_launch(2, bb->cop(level), bb->theta, bb->count, x, rhs, y, bb->omega, lc));
   }
   return 0;
 }
@@ -202,10 +202,10 @@ int rbws_level_kernel(rbws_batch* b, int level, int mode, const double* x, const
   } else if (mode == 3) {  // pre-smoothing residual = residual of u = w D^-1 rhs
     const int n = h->cells[level];
     RBWS_CHECK(rbws::vec_scale_dinv(n, bb->count, bb->omega, dinv, rhs, bb->lv[level].u, S(stream)));
-    RBWS_CHECK(rbws::coarse_launch(1, h->coarse_op(level), bb->theta,
+    RBWS_CHECK(rbws::coarse_launch(1, bb->cop(level), bb->theta,
                                    bb->count, bb->lv[level].u, rhs, y, bb->omega, lc));
   } else {
-    RBWS_CHECK(rbws::coarse_launch(mode, h->coarse_op(level), bb->theta, bb->count, x, rhs, y, bb->omega,
+    RBWS_CHECK(rbws::coarse_launch(mode, bb->cop(level), bb->theta, bb->count, x, rhs, y, bb->omega,
                                    lc));
   }
   return 0;

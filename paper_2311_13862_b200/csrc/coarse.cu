@@ -483,9 +483,122 @@ static cudaError_t coarse_launch_q(int mode, const CoarseArgs& a, int batch, cud
   }
 }
 
+// ---- stored 27-point coefficients (levels with many z-groups) ---------------------
+// The 13 forward offsets (dx, dy, dz), (dz, dy, dx) lexicographically positive; the
+// backward coefficient of node X for -o is the forward one of node X - o (symmetry).
+__device__ __forceinline__ void fwd_off(int o, int& dx, int& dy, int& dz) {
+  const int t = o - 1;
+  if (t < 9) { dz = 1; dy = t / 3 - 1; dx = t % 3 - 1; }
+  else if (t < 12) { dz = 0; dy = 1; dx = t - 10; }
+  else { dz = 0; dy = 0; dx = 1; }
+}
+
+__global__ void __launch_bounds__(256) coarse_build_kernel(int n, int Q,
+                                                           const double* __restrict__ fac,
+                                                           const double* __restrict__ theta,
+                                                           double* __restrict__ coef,
+                                                           double* __restrict__ dinv) {
+  const int mu = blockIdx.y;
+  const int64_t n3 = (int64_t)n * n * n;
+  const int64_t X = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (X >= n3) return;
+  const int i = X % n, j = (X / n) % n, k = (int)(X / ((int64_t)n * n));
+  double* C = coef + (int64_t)mu * 14 * n3;
+  const bool ghost = (i == 0 || j == 0 || k == 0);
+  const int n1 = n + 1;
+  double c0 = 0.0;
+  for (int o = 0; o < 14; ++o) {
+    int dx = 0, dy = 0, dz = 0;
+    if (o > 0) fwd_off(o, dx, dy, dz);
+    double c = 0.0;
+    if (!ghost) {
+      for (int q = 0; q < Q; ++q) {
+        double sum = 0.0;
+        for (int d = 0; d < 3; ++d) {
+          const double* f = fac + (size_t)((q * 3 + d) * 3) * 2 * n1;
+          sum += tri(f, n1, i, dx) * tri(f + 2 * n1, n1, j, dy) * tri(f + 4 * n1, n1, k, dz);
+        }
+        c = fma(theta[(int64_t)mu * Q + q], sum, c);
+      }
+    }
+    C[o * n3 + X] = c;
+    if (o == 0) c0 = c;
+  }
+  dinv[(int64_t)mu * n3 + X] = ghost ? 0.0 : 1.0 / c0;
+}
+
+cudaError_t coarse_build_coef(const CoarseOp& op, const double* theta, int batch, double* coef,
+                              double* dinv, cudaStream_t stream) {
+  const int64_t n3 = (int64_t)op.n * op.n * op.n;
+  dim3 grd((unsigned)((n3 + 255) / 256), batch);
+  count_launch();
+  coarse_build_kernel<<<grd, 256, 0, stream>>>(op.n, op.Q, op.fac, theta, coef, dinv);
+  return cudaGetLastError();
+}
+
+// one node per thread over the planes [zlo, zhi); coefficients streamed, neighbours
+// through L1/L2.  mode: 0 y = A x, 1 y = b - A x, 2 y = x + w (b - A x)/diag, 4 y = 1/diag
+template <int MODE>
+__global__ void __launch_bounds__(256) coarse_stored_kernel(int n, const double* __restrict__ coef,
+                                                            const double* __restrict__ x,
+                                                            const double* __restrict__ b,
+                                                            double* __restrict__ y,
+                                                            const int* __restrict__ active,
+                                                            double omega, int zlo, int zhi) {
+  const int mu = blockIdx.y;
+  if (active && !active[mu]) return;
+  const int64_t n2 = (int64_t)n * n, n3 = n2 * n;
+  const int64_t X = (int64_t)zlo * n2 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (X >= (int64_t)zhi * n2) return;
+  const int i = X % n, j = (X / n) % n, k = (int)(X / n2);
+  if (i == 0 || j == 0 || k == 0) return;
+  const double* C = coef + (int64_t)mu * 14 * n3;
+  const int64_t base = (int64_t)mu * n3;
+  const double c0 = __ldg(C + X);
+  if (MODE == 4) {
+    y[base + X] = 1.0 / c0;
+    return;
+  }
+  const double* xb = x + base;
+  const double xc = __ldg(xb + X);
+  double Au = c0 * xc;
+#pragma unroll
+  for (int o = 1; o < 14; ++o) {
+    int dx, dy, dz;
+    fwd_off(o, dx, dy, dz);
+    const int64_t off = dx + (int64_t)n * (dy + (int64_t)n * dz);
+    Au = fma(__ldg(C + o * n3 + X), __ldg(xb + X + off), Au);
+    Au = fma(__ldg(C + o * n3 + X - off), __ldg(xb + X - off), Au);
+  }
+  double out;
+  if (MODE == 0) out = Au;
+  else if (MODE == 1) out = __ldg(b + base + X) - Au;
+  else out = fma(omega / c0, __ldg(b + base + X) - Au, xc);
+  y[base + X] = out;
+}
+
+static cudaError_t coarse_stored_launch(int mode, const CoarseOp& op, int batch, const double* x,
+                                        const double* b, double* y, double omega,
+                                        const LaunchCtx& lc) {
+  const int n = op.n;
+  const int zlo = lc.zhi > 0 ? lc.zlo : 0, zhi = lc.zhi > 0 ? lc.zhi : n;
+  const int64_t cnt = (int64_t)(zhi - zlo) * n * n;
+  dim3 grd((unsigned)((cnt + 255) / 256), batch);
+  count_launch();
+  switch (mode) {
+    case 0: coarse_stored_kernel<0><<<grd, 256, 0, lc.stream>>>(n, op.coef, x, b, y, lc.active, omega, zlo, zhi); break;
+    case 1: coarse_stored_kernel<1><<<grd, 256, 0, lc.stream>>>(n, op.coef, x, b, y, lc.active, omega, zlo, zhi); break;
+    case 2: coarse_stored_kernel<2><<<grd, 256, 0, lc.stream>>>(n, op.coef, x, b, y, lc.active, omega, zlo, zhi); break;
+    case 4: coarse_stored_kernel<4><<<grd, 256, 0, lc.stream>>>(n, op.coef, x, b, y, lc.active, omega, zlo, zhi); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t coarse_launch(int mode, const CoarseOp& op, const double* theta, int batch,
                           const double* x, const double* b, double* y, double omega,
                           const LaunchCtx& lc) {
+  if (op.coef) return coarse_stored_launch(mode, op, batch, x, b, y, omega, lc);
   const int n = op.n;
   if (n < 2 || n > 256) return cudaErrorInvalidValue;
   CoarseArgs a{};

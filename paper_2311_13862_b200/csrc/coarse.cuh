@@ -19,12 +19,20 @@ struct CoarseOp {
   const double* fac = nullptr;
   const int* zsame = nullptr;
   const int* grp = nullptr;
+  // per-instance stored 27-point coefficients [batch][14][n^3] (diagonal, 13 forward
+  // offsets; symmetric), or null: matrix-free from the factors
+  const double* coef = nullptr;
 };
 
 // mode: 0 apply y=Ax | 1 resid y=b-Ax | 2 jacobi y=x+w(b-Ax)/diag | 4 dinv y=1/diag
 cudaError_t coarse_launch(int mode, const CoarseOp& op, const double* theta, int batch,
                           const double* x, const double* b, double* y, double omega,
                           const LaunchCtx& lc);
+// stored coefficients of a coarse level (and 1/diag) from its Kronecker factors, for levels
+// whose terms fall into more z-groups than the grouped kernel takes
+cudaError_t coarse_build_coef(const CoarseOp& op, const double* theta, int batch, double* coef,
+                              double* dinv, cudaStream_t stream);
+constexpr int kCoarseMaxGroups = 4;  // coarse_kron_kernel<G> instantiations
 // coarsest level: dense Galerkin operator from the factors + Cholesky per instance
 cudaError_t coarse_factor_kf(int n0, int Q, const double* fac, const double* theta, int batch,
                              double* L, int* status, cudaStream_t stream);

@@ -273,7 +273,7 @@ Batch::~Batch() {
   cudaFree(wface);
   for (auto& l : lv) {
     cudaFree(l.b); cudaFree(l.e); cudaFree(l.t1); cudaFree(l.t2); cudaFree(l.t3);
-    cudaFree(l.zero); cudaFree(l.dinv); cudaFree(l.u);
+    cudaFree(l.zero); cudaFree(l.dinv); cudaFree(l.u); cudaFree(l.coef);
   }
   cudaFree(L0); cudaFree(d_status);
   cudaFree(r); cudaFree(p); cudaFree(p2); cudaFree(s); cudaFree(t_res);
@@ -327,6 +327,15 @@ int batch_create(Batch** out, Hierarchy* h, int cap, int nu, double omega, int m
     zalloc(&lb.dinv, V);
     if (nu != 1) { zalloc(&lb.t2, V); zalloc(&lb.t3, V); zalloc(&lb.zero, V); }
     if (l >= 1 && l < L - 1) zalloc(&lb.u, V);
+    // levels whose terms fall into more z-groups than the grouped Kronecker kernel takes:
+    // stored per-instance coefficients (without the memory, the matrix-free 27-coefficient
+    // kernel runs instead)
+    if (e == cudaSuccess && l >= 1 && l < L - 1 && h->G[l] > kCoarseMaxGroups) {
+      if (dalloc(&lb.coef, (size_t)14 * cap * n3) != cudaSuccess) {
+        (void)cudaGetLastError();
+        lb.coef = nullptr;
+      }
+    }
     if (l < L - 1) {
       zalloc(&lb.b, V);
       zalloc(&lb.e, V);
@@ -394,7 +403,10 @@ int batch_setup(Batch* b, const double* theta, int count, cudaStream_t stream) {
   if (e == cudaSuccess && b->wface) e = fine_faces(b->fine_op(), count, b->wface, b->wstride, stream);
   // coarse levels are matrix-free (Kronecker factors): only 1/diag is stored
   for (int l = 1; l < std::min(L - 1, b->maxl) && e == cudaSuccess; ++l)
-    e = coarse_launch(4, h->coarse_op(l), b->theta, count,
+    e = b->lv[l].coef
+            ? coarse_build_coef(h->coarse_op(l), b->theta, count, b->lv[l].coef, b->lv[l].dinv,
+                                stream)
+            : coarse_launch(4, h->coarse_op(l), b->theta, count,
                       nullptr, nullptr, b->lv[l].dinv, 0.0, lc);
   if (e == cudaSuccess)
     e = coarse_factor_kf(h->m0, h->Q, h->d_fac[0], b->theta, count, b->L0, b->d_status, stream);
@@ -461,10 +473,10 @@ int Batch::vcycle(int lvl, const double* bb, double* out, double* dot_partial,
     }
     // coarse levels: the pre-smoothing residual is a residual of the pre-scaled rhs l.u
     if (mode == MODE_PRE)
-      return coarse_launch(1, h->coarse_op(lvl), theta, count, l.u, rhs, y,
+      return coarse_launch(1, cop(lvl), theta, count, l.u, rhs, y,
                            omega, lc);
     const int cm = (mode == MODE_JACOBI) ? 2 : (mode == MODE_RESID) ? 1 : 0;
-    return coarse_launch(cm, h->coarse_op(lvl), theta, count, x, rhs, y,
+    return coarse_launch(cm, cop(lvl), theta, count, x, rhs, y,
                          omega, lc);
   };
   const int fdot = (fine && dot_partial) ? DOT_BY : DOT_NONE;

@@ -52,6 +52,7 @@ struct LevelBuf {
   double* t3 = nullptr;    // scratch (nu != 1)
   double* zero = nullptr;  // zeros (nu != 1)
   double* dinv = nullptr;  // 1/diag per instance
+  double* coef = nullptr;  // stored 27-point coefficients [cap][14][n^3] (many z-groups)
   double* u = nullptr;     // pre-scaled rhs w D^-1 b (coarse levels 1..L-2, nu=1)
 };
 
@@ -118,6 +119,11 @@ struct Batch {
 
   ~Batch();
   Sep7 fine_op() const;
+  CoarseOp cop(int l) const {  // the level's operator with this batch's stored coefficients
+    CoarseOp o = h->coarse_op(l);
+    o.coef = lv[l].coef;
+    return o;
+  }
   int vcycle(int lvl, const double* b, double* out, double* dot_partial, const LaunchCtx& lc);
 };
 
