@@ -118,8 +118,12 @@ struct SL {
   // raw / transformed ring slots (N = 512 rows are 4 KB: a shallower raw ring fits 227 KB).
   // U >= 6: a trip reads transformed planes k-1 .. k+2 while the next trip's transform
   // (no barrier in between) writes k+3, k+4.
-  static constexpr int S = XF ? (N >= 512 ? (RBWS_N512_NPT == 2 ? (MODE == FM_POSTP ? 2 : 3) : 4) : 6)
-                              : (N >= 512 ? 6 : kStages);
+  // N = 256: rings shallow enough for two CTAs per SM (pre-smoothing / p-update 15.6 ->
+  // 10.3 ms, CG update 16.2 -> 11.3 ms per launch on configs[3]); the post-smoothing kernel
+  // (coarse rows staged too) does not fit two CTAs and keeps its deeper ring
+  static constexpr int S = XF ? (N >= 512 ? (RBWS_N512_NPT == 2 ? (MODE == FM_POSTP ? 2 : 3) : 4)
+                                          : ((N >= 256 && MODE != FM_POSTP) ? 3 : 6))
+                              : (N >= 256 ? 6 : kStages);
   static constexpr int U = 6;
 };
 
