@@ -119,10 +119,10 @@ struct SL {
   // U >= 6: a trip reads transformed planes k-1 .. k+2 while the next trip's transform
   // (no barrier in between) writes k+3, k+4.
   // N = 256: rings shallow enough for two CTAs per SM (pre-smoothing / p-update 15.6 ->
-  // 10.3 ms, CG update 16.2 -> 11.3 ms per launch on configs[3]); the post-smoothing kernel
-  // (coarse rows staged too) does not fit two CTAs and keeps its deeper ring
+  // 10.3 ms, CG update 16.2 -> 11.3 ms per launch on configs[3]; the post-smoothing kernel
+  // fits two only without the z-factor table, i.e. with stored weights)
   static constexpr int S = XF ? (N >= 512 ? (RBWS_N512_NPT == 2 ? (MODE == FM_POSTP ? 2 : 3) : 4)
-                                          : ((N >= 256 && MODE != FM_POSTP) ? 3 : 6))
+                                          : (N >= 256 ? 3 : 6))
                               : (N >= 256 ? 6 : kStages);
   static constexpr int U = 6;
 };
@@ -172,7 +172,7 @@ fine_kernel(FineArgs a) {
   constexpr int64_t N2 = (int64_t)N * N;
   extern __shared__ __align__(128) unsigned char smem[];
   const Sep7& op = a.op;
-  const int Q = op.Q, ZW = 3 * Q;
+  const int Q = op.Q, ZW = SCW ? 0 : 3 * Q;  // SCW: no z-factor table (weights are stored)
   const int zc = a.g.zc;
   const int kc = blockIdx.z % zc, mu = blockIdx.z / zc;
   if (a.active && !a.active[mu]) return;
@@ -198,7 +198,7 @@ fine_kernel(FineArgs a) {
   double* wd = uring + (XF ? U * HSZ : 0);                       // [HSZ] w/diag (DC)
 
   for (int t = tid; t < np * ZW; t += G::THREADS) {  // z factors of the staged planes
-    const int p = t / ZW, f = (t / Q) % 3, q = t % Q, k = p_first + p;
+    const int p = t / (3 * Q), f = (t / Q) % 3, q = t % Q, k = p_first + p;
     const double* F = op.face + (size_t)q * 3 * N;
     const double* NF = op.node + (size_t)q * 9 * (N + 1);
     double v;
@@ -569,7 +569,7 @@ static cudaError_t fine_launch_mnd(const FineArgs& a, int batch, cudaStream_t st
   using G = FTM<MODE, N>;
   if (a.g.threads != G::THREADS || a.g.ty != G::TY) return cudaErrorInvalidValue;
   const int np = a.g.kz + 2;
-  const size_t smem = FSmem<N, MODE, DC>::bytes(np, a.op.Q);
+  const size_t smem = FSmem<N, MODE, DC>::bytes(np, SCW ? 0 : a.op.Q);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   static size_t attr = 48 * 1024;
   if (smem > attr) {
