@@ -121,11 +121,15 @@ struct SL {
   // N = 256: rings shallow enough for two CTAs per SM (pre-smoothing / p-update 15.6 ->
   // 10.3 ms, CG update 16.2 -> 11.3 ms per launch on configs[3]; the post-smoothing kernel
   // fits two only without the z-factor table, i.e. with stored weights)
+#ifndef RBWS_N256_XF_S
+#define RBWS_N256_XF_S 3
+#endif
 #ifndef RBWS_N128_XF_S
 #define RBWS_N128_XF_S 4
 #endif
   static constexpr int S = XF ? (N >= 512 ? (RBWS_N512_NPT == 2 ? (MODE == FM_POSTP ? 2 : 3) : 4)
-                                          : (N >= 256 ? 3 : (N >= 128 ? RBWS_N128_XF_S : 6)))
+                                          : (N >= 256 ? (MODE == FM_POSTP ? 3 : RBWS_N256_XF_S)
+                                                      : (N >= 128 ? RBWS_N128_XF_S : 6)))
                               : (N >= 128 ? 6 : kStages);
   static constexpr int U = 6;
 };
