@@ -254,6 +254,7 @@ def run_b200(args, rank, world, dist):
     # ---- end to end through the public API with host buffers: host mu in, solutions
     # out to pinned host memory, sub-batches pipelined (paper_2311_13862_b200.pipeline)
     del state["x"]
+    scw = bool(_native.load().rbws_batch_stored_weights(ctx.handle))
     del ctx, xbuf
     torch.cuda.empty_cache()
     e2e_sub = min(batch, args.e2e_sub or cfg.get("e2e_sub", 512))
@@ -287,6 +288,8 @@ def run_b200(args, rank, world, dist):
     # ---- roofline of the dominant fine-level kernel class
     peak, peak_kind = peaks()
     nodes = (n - 1) ** 3
+    # stored face weights (SCW kernels): +24 B/node in every finest-level stencil sweep
+    class_bytes = {k: v + (24.0 if (scw and k != 3) else 0.0) for k, v in CLASS_BYTES.items()}
     table = {}
     for k in range(NC):
         if pcalls[k] == 0:
@@ -294,14 +297,14 @@ def run_b200(args, rank, world, dist):
         row = {"ms_total": round(float(pms[k]), 3), "launches": int(pcalls[k]),
                "ms_per_launch": round(float(pms[k]) / pcalls[k], 4),
                "share": round(float(pms[k]) / ms, 4)}
-        if k in CLASS_BYTES:
-            gbs = CLASS_BYTES[k] * nodes * punits[k] / (pms[k] / 1e3) / 1e9
+        if k in class_bytes:
+            gbs = class_bytes[k] * nodes * punits[k] / (pms[k] / 1e3) / 1e9
             row["achieved_gbs"] = round(gbs, 1)
         table[CLASS_NAMES[k]] = row
-    ran = [k for k in CLASS_BYTES if pcalls[k]]
+    ran = [k for k in class_bytes if pcalls[k]]
     if ran:
         dom = max(ran, key=lambda k: pms[k])
-        dom_bytes = CLASS_BYTES[dom] * nodes * punits[dom] / pcalls[dom]
+        dom_bytes = class_bytes[dom] * nodes * punits[dom] / pcalls[dom]
         dom_s = pms[dom] / pcalls[dom] / 1e3
         achieved = dom_bytes / dom_s / 1e9
         traffic, tsrc = _traffic(CLASS_NAMES[dom], dom_bytes, cfg)
@@ -309,7 +312,7 @@ def run_b200(args, rank, world, dist):
                     "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                     "traffic": traffic, "traffic_source": tsrc, "peak_source": peak_kind,
                     "bytes_per_launch": int(dom_bytes),
-                    "bytes_per_node": CLASS_BYTES[dom]}
+                    "bytes_per_node": class_bytes[dom], "stored_weights": scw}
     else:  # the warm start already met the tolerance: no PCG iteration ran
         roofline = {"bound": "hbm", "kernel": None, "achieved": None, "peak": peak,
                     "unit": "GB/s", "frac": None, "traffic": None, "peak_source": peak_kind}

@@ -85,6 +85,9 @@ int rbws_batch_setup(rbws_batch* b, const double* theta, int count, int* n_bad, 
  * Default on (environment RBWS_GRAPH=0 turns it off); not used while the event
  * profiler or a streaming download is active. */
 int rbws_batch_set_graph(rbws_batch* b, int enable);
+/* 1 if the finest-level kernels of this batch read stored face weights (coefficients
+ * whose z factors change on most planes; +24 B per node per stencil sweep), else 0 */
+int rbws_batch_stored_weights(const rbws_batch* b);
 
 /* y = A^level(mu) x for every instance (ParametricProblem.operator(mu, level) @ x,
  * grid.py:274-283).  x, y: (dev) padded vectors of that level. */
