@@ -48,7 +48,9 @@ struct FT {
 
 // threads per CTA of a mode: the prolongation + post-smoothing kernel runs 512-thread
 // CTAs (16-row tiles) at N = 64: half the halo-row work per node, measured -5 %
-int fine_mode_threads(int mode, int n) { return (mode == 6 && n == 64) ? 512 : kThreads; }
+int fine_mode_threads(int mode, int n) {
+  return (mode == 6 && (n == 64 || n == 128)) ? 512 : kThreads;
+}
 
 FineGeom fine_geom(int n, int batch, int nz, int threads) {
   FineGeom g;
@@ -106,7 +108,7 @@ enum FineMode : int {
 // per node less; bitwise the same values)
 // tile geometry of a mode (see fine_mode_threads)
 template <int MODE, int N>
-using FTM = FT<N, (MODE == FM_POSTP && N == 64) ? 512 : kThreads>;
+using FTM = FT<N, (MODE == FM_POSTP && (N == 64 || N == 128)) ? 512 : kThreads>;
 
 template <int MODE, int N, bool DC = false>
 struct SL {
