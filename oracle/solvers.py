@@ -42,6 +42,23 @@ def jacobi_sweep(A, diag, x, b, omega=JACOBI_OMEGA):
     return x + omega * (b - A @ x) / diag
 
 
+def gs_sweep(A, x, b, forward: bool = True):
+    """One in-place Gauss-Seidel sweep (reference _smoothers.pyx:14-28 csr_gauss_seidel,
+    kernels.py:124-134): x_i = (b_i - sum_{j != i} a_ij x_j) / a_ii row by row, rows in
+    ascending (forward) or descending (backward) order.  Vectorised as the triangular
+    solve of the reference's NumPy backend (_smoothers_np.py:35-42), which is the same
+    sequential update."""
+    from scipy.sparse.linalg import spsolve_triangular
+    A = sp.csr_matrix(A)
+    if forward:
+        x[:] = spsolve_triangular(sp.csr_matrix(sp.tril(A, k=0)),
+                                  b - sp.triu(A, k=1) @ x, lower=True)
+    else:
+        x[:] = spsolve_triangular(sp.csr_matrix(sp.triu(A, k=0)),
+                                  b - sp.tril(A, k=-1) @ x, lower=False)
+    return x
+
+
 @dataclass
 class OracleMgContext:
     """Per-parameter V-cycle data (multigrid.py:455-468, 493-507)."""
@@ -52,13 +69,15 @@ class OracleMgContext:
     nu: int
     coarse_factor: tuple
     omega: float = JACOBI_OMEGA
+    smoother: str = "jacobi"  # "jacobi" (isotropic default) or "gs" (multigrid.py:132-140)
 
     @property
     def levels(self):
         return len(self.operators)
 
 
-def mg_context_for(problem, mu, nu: int = 1, omega: float = JACOBI_OMEGA) -> OracleMgContext:
+def mg_context_for(problem, mu, nu: int = 1, omega: float = JACOBI_OMEGA,
+                   smoother: str = "jacobi") -> OracleMgContext:
     """Operators per level from the affine terms + Cholesky of level 0 (multigrid.py:530-541)."""
     if nu < 0:
         raise ValueError("smoothing count must be non-negative")
@@ -71,7 +90,9 @@ def mg_context_for(problem, mu, nu: int = 1, omega: float = JACOBI_OMEGA) -> Ora
     for d in diags[1:]:
         if np.any(d == 0.0):
             raise ValueError("zero diagonal entry; point smoothing undefined")
-    return OracleMgContext(ops, list(problem.prolongations), diags, nu, cf, omega)
+    if smoother not in ("jacobi", "gs"):
+        raise ValueError(f"unknown smoother kind {smoother!r}")
+    return OracleMgContext(ops, list(problem.prolongations), diags, nu, cf, omega, smoother)
 
 
 def mg_vcycle(b, ctx: OracleMgContext, level=None) -> np.ndarray:
@@ -84,13 +105,13 @@ def mg_vcycle(b, ctx: OracleMgContext, level=None) -> np.ndarray:
     A, d = ctx.operators[level], ctx.diags[level]
     P = ctx.prolongations[level - 1]
     u = np.zeros_like(b)
-    for _ in range(ctx.nu):
-        u = jacobi_sweep(A, d, u, b, ctx.omega)
+    for _ in range(ctx.nu):  # "gs": forward sweeps before, backward after (multigrid.py:138)
+        u = jacobi_sweep(A, d, u, b, ctx.omega) if ctx.smoother == "jacobi" else gs_sweep(A, u, b, True)
     r = b - A @ u
     e = mg_vcycle(P.T @ r, ctx, level - 1)
     u = u + P @ e
     for _ in range(ctx.nu):
-        u = jacobi_sweep(A, d, u, b, ctx.omega)
+        u = jacobi_sweep(A, d, u, b, ctx.omega) if ctx.smoother == "jacobi" else gs_sweep(A, u, b, False)
     return u
 
 

@@ -2,7 +2,8 @@
 
 Run in the build container (needs /root/reference; never on the GPU box):
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py          # golden_fd.npz
+    python tests/golden/make_golden.py --gs     # golden_gs.npz (Gauss-Seidel smoother)
 
 The reference (``/root/reference/pkg``) is copied to /tmp and its Cython
 smoother extension built in place (reference setup.py), so the reference's
@@ -197,5 +198,49 @@ def main():
     print(f"wrote {dest} ({dest.stat().st_size/1e6:.2f} MB, {len(out)} arrays)")
 
 
+def main_gs():
+    """Gauss-Seidel smoother goldens (smoother="gs": forward GS before, backward after the
+    coarse correction, multigrid.py:132-140) -> tests/golden/golden_gs.npz."""
+    rbws = _import_reference()
+    sys.path.insert(0, str(REPO))
+    from oracle import problems as op
+    from rbws.multigrid import mg_context_for, mg_vcycle, mgcg_solve
+
+    out = {}
+    tb4 = op.thermal_block((2, 2, 1))
+    prob16 = reference_problem(rbws, tb4, 16, m0=4)
+    mu = np.array([0.2, 3.0, 7.5, 0.9])
+    v = np.random.default_rng(5).standard_normal(prob16.n_free)
+    out["gs_vcycle_tb221_n16_mu"] = mu
+    out["gs_vcycle_tb221_n16_in"] = v
+    for nu in (1, 2):
+        ctx = mg_context_for(prob16, mu, nu=nu, smoother="gs")
+        out[f"gs_vcycle_tb221_n16_nu{nu}_out"] = mg_vcycle(v, ctx)
+    cases = [("tb221", tb4, 16, 2, 1e-10), ("smooth6", op.smooth_affine(6), 16, 2, 1e-12),
+             ("tb222", op.thermal_block((2, 2, 2)), 32, 1, 1e-10)]
+    for tag, spec, n, cnt, delta in cases:
+        p = reference_problem(rbws, spec, n, m0=4)
+        mus = op.sample_mus(spec, cnt, seed=300 + n)
+        xs, hists, its = [], [], []
+        for m in mus:
+            A, f = p.operator(m), p.rhs(m)
+            c = mg_context_for(p, m, smoother="gs")
+            x, rep = mgcg_solve(A, f, np.zeros_like(f), c, delta=delta, l_max=60, mu=m)
+            xs.append(x)
+            hists.append(np.pad(rep.history, (0, 61 - len(rep.history)), constant_values=np.nan))
+            its.append(rep.iterations)
+        out[f"gs_mgcg_{tag}_n{n}_mus"] = mus
+        out[f"gs_mgcg_{tag}_n{n}_x"] = np.array(xs)
+        out[f"gs_mgcg_{tag}_n{n}_hist"] = np.array(hists)
+        out[f"gs_mgcg_{tag}_n{n}_iters"] = np.array(its)
+        out[f"gs_mgcg_{tag}_n{n}_delta"] = np.array(delta)
+    dest = REPO / "tests/golden/golden_gs.npz"
+    np.savez_compressed(dest, **out)
+    print(f"wrote {dest} ({dest.stat().st_size/1e6:.2f} MB, {len(out)} arrays)")
+
+
 if __name__ == "__main__":
+    if "--gs" in sys.argv:
+        main_gs()
+        sys.exit(0)
     main()
