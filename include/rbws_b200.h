@@ -85,6 +85,12 @@ int rbws_batch_setup(rbws_batch* b, const double* theta, int count, int* n_bad, 
  * Default on (environment RBWS_GRAPH=0 turns it off); not used while the event
  * profiler or a streaming download is active. */
 int rbws_batch_set_graph(rbws_batch* b, int enable);
+/* Smoother of the V-cycle: 0 damped Jacobi (the reference default for isotropic problems,
+ * multigrid.py:183-188), 1 Gauss-Seidel (smoother="gs": nu forward lexicographic sweeps
+ * before and nu backward sweeps after the coarse correction, multigrid.py:132-140, sweep
+ * _smoothers.pyx:14-28).  Call before rbws_batch_setup; Gauss-Seidel allocates stored
+ * fine face weights and coarse coefficients (the hyperplane-ordered sweeps read them). */
+int rbws_batch_set_smoother(rbws_batch* b, int kind);
 /* 1 if the finest-level kernels of this batch read stored face weights (coefficients
  * whose z factors change on most planes; +24 B per node per stencil sweep), else 0 */
 int rbws_batch_stored_weights(const rbws_batch* b);

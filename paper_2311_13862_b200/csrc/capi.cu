@@ -91,6 +91,11 @@ int rbws_batch_destroy(rbws_batch* b) {
   return 0;
 }
 
+int rbws_batch_set_smoother(rbws_batch* b, int kind) {
+  if (!b) RBWS_FAIL("null batch");
+  return rbws::batch_set_smoother(B(b), kind);
+}
+
 int rbws_batch_stored_weights(const rbws_batch* b) {
   return reinterpret_cast<const Batch*>(b)->wface ? 1 : 0;
 }

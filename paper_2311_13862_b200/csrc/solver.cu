@@ -14,6 +14,7 @@
 
 #include "coarse.cuh"
 #include "fine.cuh"
+#include "gs.cuh"
 #include "solver.cuh"
 
 #include <algorithm>
@@ -389,6 +390,32 @@ int batch_create(Batch** out, Hierarchy* h, int cap, int nu, double omega, int m
   return 0;
 }
 
+int batch_set_smoother(Batch* b, int kind) {
+  if (kind != 0 && kind != 1) RBWS_FAIL("smoother kind must be 0 (jacobi) or 1 (gauss-seidel)");
+  Hierarchy* h = b->h;
+  const int L = h->levels;
+  if (kind == 1) {
+    if (b->maxl < L) RBWS_FAIL("Gauss-Seidel needs the finest level");
+    const size_t VF = (size_t)vec_doubles(h->n, b->cap);
+    cudaError_t e = cudaSuccess;
+    if (!b->wface) {
+      b->wstride = (int64_t)VF;
+      e = dalloc(&b->wface, 3 * VF);
+      if (e == cudaSuccess) e = cudaMemset(b->wface, 0, sizeof(double) * 3 * VF);
+    }
+    for (int l = 1; l < L - 1 && e == cudaSuccess; ++l) {
+      LevelBuf& lb = b->lv[l];
+      if (lb.coef) continue;
+      const size_t n3 = (size_t)lb.n * lb.n * lb.n;
+      e = dalloc(&lb.coef, (size_t)14 * b->cap * n3);
+    }
+    if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+  }
+  b->smoother = kind;
+  b->count = 0;  // set up again
+  return 0;
+}
+
 int batch_setup(Batch* b, const double* theta, int count, cudaStream_t stream) {
   if (count < 1 || count > b->cap) RBWS_FAIL("batch count outside [1, capacity]");
   Hierarchy* h = b->h;
@@ -481,6 +508,25 @@ int Batch::vcycle(int lvl, const double* bb, double* out, double* dot_partial,
   };
   const int fdot = (fine && dot_partial) ? DOT_BY : DOT_NONE;
   const bool pf = fine && prof_on;
+  if (smoother == 1) {  // Gauss-Seidel: forward sweeps from zero, backward after correction
+    const int64_t n3 = (int64_t)n * n * n;
+    auto gs = [&](bool fwd) -> cudaError_t {
+      return fine ? gs7_sweep(n, count, wface, wstride, bb, out, fwd, lc)
+                  : gs27_sweep(n, count, l.coef, bb, out, fwd, lc);
+    };
+    e = cudaMemsetAsync(out, 0, sizeof(double) * count * n3, lc.stream);
+    for (int s = 0; s < nu && e == cudaSuccess; ++s) e = gs(true);
+    if (e == cudaSuccess) e = op(MODE_RESID, DOT_NONE, out, bb, l.t1, nullptr);
+    if (e == cudaSuccess) e = restrict_launch(n, count, l.t1, c.b, lc);
+    if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+    if (vcycle(lvl - 1, c.b, c.e, nullptr, lc)) return 1;
+    e = prolong_launch(n, count, 0, c.e, out, nullptr, nullptr, 0.0, lc);
+    for (int s = 0; s < nu && e == cudaSuccess; ++s) e = gs(false);
+    if (e == cudaSuccess && fine && dot_partial)
+      e = vec_dot(n, count, bb, n3, out, n3, dot_partial, lc);
+    if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+    return 0;
+  }
   if (nu == 1) {
     int t0 = pf ? prof_begin(lc.stream) : -1;
     e = op(MODE_PRE, DOT_NONE, nullptr, bb, l.t1, nullptr);
@@ -842,7 +888,8 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
   bool graph_ran = false;
   const int tiles = fine_geom(n, count).tiles;
   // the V-cycle's dot partials come from the post-smoothing kernel's geometry (nu = 1)
-  const int vtiles = (b->nu == 1) ? fine_post_tiles(n, count) : tiles;
+  const int vtiles = (b->smoother == 1) ? vec_tiles(n)
+                     : ((b->nu == 1) ? fine_post_tiles(n, count) : tiles);
   LaunchCtx all{stream, nullptr};
   LaunchCtx act{stream, b->active};
   const int fshared = (f_stride == 0);

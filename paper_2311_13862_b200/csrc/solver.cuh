@@ -74,6 +74,7 @@ struct Batch {
   Hierarchy* h = nullptr;
   int cap = 0, count = 0, nu = 1;
   int maxl = 0;                     // levels with buffers (< levels: coarse-only, slab path)
+  int smoother = 0;                 // 0 damped Jacobi (isotropic default), 1 Gauss-Seidel ("gs")
   double omega = 0.7;
   double* theta = nullptr;          // [cap][Q]
   double* wface = nullptr;          // stored fine face weights [3][cap n^3 + 2n^2] (SCW kernels)
@@ -130,6 +131,9 @@ struct Batch {
 // maxl: allocate levels 0..maxl-1 only (0 = all; the slab path's replicated coarse levels)
 int batch_create(Batch** out, Hierarchy* h, int cap, int nu, double omega, int maxl = 0);
 int batch_setup(Batch* b, const double* theta, int count, cudaStream_t stream);
+// smoother kind (before batch_setup): 1 = Gauss-Seidel, which needs stored fine face weights
+// and stored coarse coefficients (allocated here)
+int batch_set_smoother(Batch* b, int kind);
 
 struct PcgOut {
   int* iters;          // host [count]

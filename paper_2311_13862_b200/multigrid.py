@@ -23,24 +23,31 @@ from .grid import BatchOperator, ParametricProblem, padded_len
 from .krylov import OperatorError, SolveReport, SolveReports
 
 JACOBI_OMEGA = 0.7
+# V-cycle smoothers (reference multigrid.py:132-150): damped Jacobi both sides, or forward
+# Gauss-Seidel before / backward after the coarse correction
+SMOOTHERS = ("jacobi", "gs")
 
 
 class MgContext:
     """Per-batch multigrid state (reference MgContext, multigrid.py:455-468)."""
 
     def __init__(self, problem: ParametricProblem, capacity: int, nu: int = 1,
-                 omega: float = JACOBI_OMEGA):
+                 omega: float = JACOBI_OMEGA, smoother: str = "jacobi"):
         if nu < 1:
             raise ValueError("the batched V-cycle needs nu >= 1 smoothing sweeps")
+        if smoother not in SMOOTHERS:
+            raise ValueError(f"unknown smoother kind {smoother!r}; choices: {SMOOTHERS}")
         self.problem = problem
         self.capacity = int(capacity)
         self.nu = nu
         self.omega = omega
-        self.smoother_kind = "jacobi"
+        self.smoother_kind = smoother
         b = ctypes.c_void_p()
         _native.call("rbws_batch_create", ctypes.byref(b), problem.handle, self.capacity, nu,
                      float(omega))
         self._b = b
+        if smoother == "gs":
+            _native.call("rbws_batch_set_smoother", b, 1)
         self.count = 0
         self.mus = None
         self.theta = None
@@ -83,11 +90,14 @@ def mg_context_for(problem: ParametricProblem, mus, nu: int = 1, smoother: str =
     ``mus``: one parameter or an array (count, p).  Pass an existing ``ctx``
     to reuse its device buffers for a new batch.
     """
-    if smoother not in ("auto", "jacobi"):
-        raise ValueError(f"smoother {smoother!r} is not on the B200 path (jacobi only)")
+    if smoother == "auto":  # isotropic problems: damped Jacobi (multigrid.py:183-188)
+        smoother = "jacobi"
+    if smoother not in SMOOTHERS:
+        raise ValueError(f"smoother {smoother!r} is not on the B200 path ({SMOOTHERS})")
     mus = problem.spec.check_mus(mus)
-    if ctx is None or ctx.capacity < len(mus) or ctx.nu != nu or ctx.problem is not problem:
-        ctx = MgContext(problem, len(mus), nu=nu)
+    if (ctx is None or ctx.capacity < len(mus) or ctx.nu != nu or ctx.problem is not problem
+            or ctx.smoother_kind != smoother):
+        ctx = MgContext(problem, len(mus), nu=nu, smoother=smoother)
     return ctx.setup(mus)
 
 
@@ -163,6 +173,6 @@ def mgcg_solve(A, f, x0, ctx: MgContext, delta: float = 1e-16, l_max: int = 40, 
         bad = int(np.flatnonzero(status & 1)[0])
         raise OperatorError(f"non-positive curvature for parameter #{bad}; operator not SPD")
     reports = SolveReports(method, iters, hist, tres, status, wall, delta, l_max, ctx.mus,
-                           {"batch": count, "batch_wall_time": wall, "smoother": "jacobi",
+                           {"batch": count, "batch_wall_time": wall, "smoother": ctx.smoother_kind,
                             "nu": ctx.nu})
     return x, reports
