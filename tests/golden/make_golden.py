@@ -4,6 +4,7 @@ Run in the build container (needs /root/reference; never on the GPU box):
 
     python tests/golden/make_golden.py          # golden_fd.npz
     python tests/golden/make_golden.py --gs     # golden_gs.npz (Gauss-Seidel smoother)
+    python tests/golden/make_golden.py --msrb   # golden_msrb.npz (rbi-msrbcg)
 
 The reference (``/root/reference/pkg``) is copied to /tmp and its Cython
 smoother extension built in place (reference setup.py), so the reference's
@@ -239,7 +240,51 @@ def main_gs():
     print(f"wrote {dest} ({dest.stat().st_size/1e6:.2f} MB, {len(out)} arrays)")
 
 
+def main_msrb():
+    """rbi-msrbcg goldens (msrb_train + MsrbPreconditioner through the reference's
+    rbi_pcg_solve) -> tests/golden/golden_msrb.npz."""
+    rbws = _import_reference()
+    sys.path.insert(0, str(REPO))
+    from oracle import problems as op
+    from rbws.hf import HighFidelitySolver
+    from rbws.msrb import msrb_train
+    from rbws.warmstart import MethodConfig, rbi_pcg_solve
+
+    out = {}
+    tb4 = op.thermal_block((2, 2, 1))
+    p = reference_problem(rbws, tb4, 16, m0=4)
+    train = op.sample_mus(tb4, 48, seed=11)
+    test = op.sample_mus(tb4, 3, seed=12)
+    N, K = 10, 8
+    hf = HighFidelitySolver(p, method="lu")
+    hier = msrb_train(list(train), N, K, hf, p.operator, p.rhs)
+    out["msrb_tb221_n16_train"] = train
+    out["msrb_tb221_n16_test"] = test
+    out["msrb_tb221_n16_NK"] = np.array([N, K])
+    out["msrb_tb221_n16_init"] = hier.init_basis.basis
+    out["msrb_tb221_n16_init_eig"] = hier.init_basis.eigenvalues
+    for k, W in enumerate(hier.bases):
+        out[f"msrb_tb221_n16_basis{k}"] = W
+    xs, its, hists = [], [], []
+    for m in test:
+        A, f = p.operator(m), p.rhs(m)
+        cfg = MethodConfig("rbi-msrbcg", delta=1e-10, l_max=60, N=N, K_max=K)
+        x, rep = rbi_pcg_solve(A, f, cfg, msrb_hier=hier, mu=m)
+        xs.append(x)
+        its.append(rep.iterations)
+        hists.append(np.pad(rep.history, (0, 61 - len(rep.history)), constant_values=np.nan))
+    out["msrb_tb221_n16_x"] = np.array(xs)
+    out["msrb_tb221_n16_iters"] = np.array(its)
+    out["msrb_tb221_n16_hist"] = np.array(hists)
+    dest = REPO / "tests/golden/golden_msrb.npz"
+    np.savez_compressed(dest, **out)
+    print(f"wrote {dest} ({dest.stat().st_size/1e6:.2f} MB, {len(out)} arrays)")
+
+
 if __name__ == "__main__":
+    if "--msrb" in sys.argv:
+        main_msrb()
+        sys.exit(0)
     if "--gs" in sys.argv:
         main_gs()
         sys.exit(0)
