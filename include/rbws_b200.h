@@ -91,6 +91,10 @@ int rbws_batch_set_graph(rbws_batch* b, int enable);
  * _smoothers.pyx:14-28).  Call before rbws_batch_setup; Gauss-Seidel allocates stored
  * fine face weights and coarse coefficients (the hyperplane-ordered sweeps read them). */
 int rbws_batch_set_smoother(rbws_batch* b, int kind);
+/* In-place Gauss-Seidel sweep(s) on `level` for every instance of a batch set up with
+ * smoother 1: kind 1 forward, 2 backward, 3 symmetric (forward then backward; the MSRB
+ * FINE_SMOOTH, reference msrb.py:19, kernels.py:97-101).  x, rhs: (dev) padded. */
+int rbws_smooth(rbws_batch* b, int level, int kind, double* x, const double* rhs, void* stream);
 /* 1 if the finest-level kernels of this batch read stored face weights (coefficients
  * whose z factors change on most planes; +24 B per node per stencil sweep), else 0 */
 int rbws_batch_stored_weights(const rbws_batch* b);

@@ -11,6 +11,7 @@ from .grid import (BatchOperator, ParametricProblem, from_padded, padded_len,
 from .hf import HighFidelitySolver
 from .krylov import OperatorError, SolveReport, pcg_solve
 from .multigrid import MgContext, mg_context_for, mg_vcycle, mgcg_solve
+from .msrb import MsrbHierarchy, PodBasis, msrb_train, pod_build, rbi_msrbcg_solve
 from .pipeline import HostPipeline
 from .problems import (ProblemSpec, get_problem, sample_mus, smooth_affine,
                        thermal_block)

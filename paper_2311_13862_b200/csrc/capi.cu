@@ -2,6 +2,7 @@
 #include "../../include/rbws_b200.h"
 #include "coarse.cuh"
 #include "fine.cuh"
+#include "gs.cuh"
 #include "l1roc.cuh"
 #include "slab.cuh"
 #include "solver.cuh"
@@ -94,6 +95,26 @@ int rbws_batch_destroy(rbws_batch* b) {
 int rbws_batch_set_smoother(rbws_batch* b, int kind) {
   if (!b) RBWS_FAIL("null batch");
   return rbws::batch_set_smoother(B(b), kind);
+}
+
+int rbws_smooth(rbws_batch* b, int level, int kind, double* x, const double* rhs, void* stream) {
+  Batch* bb = B(b);
+  Hierarchy* h = bb->h;
+  if (level < 1 || level >= h->levels) RBWS_FAIL("level must be in [1, levels)");
+  if (bb->count < 1) RBWS_FAIL("batch_setup must be called first");
+  if (kind != 1 && kind != 2 && kind != 3) RBWS_FAIL("kind: 1 forward, 2 backward, 3 symmetric GS");
+  const int n = h->cells[level];
+  rbws::LaunchCtx lc{S(stream), nullptr};
+  const bool fine = (level == h->levels - 1);
+  if (fine ? !bb->wface : !bb->lv[level].coef)
+    RBWS_FAIL("Gauss-Seidel sweeps need a batch with smoother = 1 (rbws_batch_set_smoother)");
+  for (int pass = 0; pass < 2; ++pass) {
+    const bool fwd = (pass == 0);
+    if ((fwd && kind == 2) || (!fwd && kind == 1)) continue;
+    RBWS_CHECK(fine ? rbws::gs7_sweep(n, bb->count, bb->wface, bb->wstride, rhs, x, fwd, lc)
+                    : rbws::gs27_sweep(n, bb->count, bb->lv[level].coef, rhs, x, fwd, lc));
+  }
+  return 0;
 }
 
 int rbws_batch_stored_weights(const rbws_batch* b) {

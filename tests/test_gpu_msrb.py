@@ -1,0 +1,76 @@
+"""rbi-msrbcg on the GPU (POD bases, iteration-indexed MSRB preconditioner) against the
+reference's own golden vectors (tests/golden/golden_msrb.npz)."""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+GOLDEN = Path(__file__).resolve().parent / "golden" / "golden_msrb.npz"
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import build
+    build.build(verbose=False)
+
+
+@pytest.fixture(scope="module")
+def gm():
+    return dict(np.load(GOLDEN))
+
+
+@pytest.fixture(scope="module")
+def trained(gm):
+    import paper_2311_13862_b200 as pkg
+    prob = pkg.ParametricProblem(pkg.thermal_block((2, 2, 1)), levels=3, m0=4)
+    N, K = (int(v) for v in gm["msrb_tb221_n16_NK"])
+    hf = pkg.HighFidelitySolver(prob, delta=1e-14, l_max=100)
+    hier = pkg.msrb_train(gm["msrb_tb221_n16_train"], N, K, hf, prob)
+    return pkg, prob, hier
+
+
+def _free(pkg, rows, n):
+    """(N, n^3) padded rows -> (M, N) free-DoF columns (reference ordering)."""
+    N = rows.shape[0]
+    buf = torch.zeros(pkg.padded_len(n, N), dtype=torch.float64, device="cuda")
+    buf[: N * n ** 3] = rows.reshape(-1)
+    return pkg.from_padded(buf, n, N).T
+
+
+def _span_err(A, B):
+    return np.linalg.norm(A - B @ (B.T @ A), 2)
+
+
+def test_msrb_bases_match_reference(gm, trained):
+    pkg, prob, hier = trained
+    np.testing.assert_allclose(hier.init_basis.eigenvalues[:10],
+                               gm["msrb_tb221_n16_init_eig"][:10], rtol=1e-8)
+    W0 = _free(pkg, hier.init_basis.basis, 16)
+    assert W0.shape == gm["msrb_tb221_n16_init"].shape
+    assert _span_err(W0, gm["msrb_tb221_n16_init"]) <= 1e-7
+    assert len(hier.bases) == int(gm["msrb_tb221_n16_NK"][1])
+    for k, W in enumerate(hier.bases):
+        assert _span_err(_free(pkg, W, 16), gm[f"msrb_tb221_n16_basis{k}"]) <= 1e-5, k
+
+
+def test_rbi_msrbcg_matches_reference(gm, trained):
+    pkg, prob, hier = trained
+    test = gm["msrb_tb221_n16_test"]
+    ctx = pkg.mg_context_for(prob, test)
+    N, K = (int(v) for v in gm["msrb_tb221_n16_NK"])
+    cfg = pkg.MethodConfig("rbi-msrbcg", delta=1e-10, l_max=60, N=N, K_max=K)
+    x, reps = pkg.rbi_pcg_solve(pkg.BatchOperator(ctx), prob.rhs(), cfg, mg_ctx=ctx,
+                                msrb_hier=hier)
+    got = pkg.from_padded(x, 16, len(test))
+    for m in range(len(test)):
+        assert abs(reps[m].iterations - int(gm["msrb_tb221_n16_iters"][m])) <= 1
+        h = gm["msrb_tb221_n16_hist"][m]
+        np.testing.assert_allclose(reps[m].history[:8], h[:8], rtol=1e-5)
+        ref = gm["msrb_tb221_n16_x"][m]
+        assert np.linalg.norm(got[m] - ref) <= 1e-5 * np.linalg.norm(ref)
+        assert reps[m].config["preconditioner"] == "msrb"
