@@ -407,6 +407,8 @@ def run_slab(args, rank, world, dist):
         c *= 2
     stream = torch.cuda.current_stream()
 
+    stored = torch.cuda.Event()  # e2e: the previous solution's download (x reusable after)
+
     def warm_start(mu):
         rb.mg_context_for(cprob, mu[None], ctx=cctx)
         u, _ = rb.l1roc_online(model, rb.BatchOperator(cctx), fc)
@@ -416,6 +418,7 @@ def run_slab(args, rank, world, dist):
             _native.call("rbws_prolong_add", 2 * c, 1, u.data_ptr(), buf.data_ptr(),
                          _native.stream_ptr())
             u, c = buf, 2 * c
+        torch.cuda.current_stream().wait_event(stored)
         solver.prolong_x(u)
 
     def step(mu):
@@ -461,10 +464,16 @@ def run_slab(args, rank, world, dist):
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    copy = torch.cuda.Stream()
     e0.record(stream)
     for s_ in range(args.steps):
         step(np.asarray(mus[args.warmup + s_]))
-        solver.store(hbuf, p0=k0)
+        # download this rank's planes on a side stream; the next step's setup and warm
+        # start overlap it and only the overwrite of x (prolong_x) waits for it
+        copy.wait_stream(stream)
+        solver.store(hbuf, p0=k0, stream=copy)
+        stored.record(copy)
+    stream.wait_stream(copy)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
