@@ -506,24 +506,41 @@ __global__ void __launch_bounds__(256) coarse_build_kernel(int n, int Q,
   double* C = coef + (int64_t)mu * 14 * n3;
   const bool ghost = (i == 0 || j == 0 || k == 0);
   const int n1 = n + 1;
-  double c0 = 0.0;
-  for (int o = 0; o < 14; ++o) {
-    int dx = 0, dy = 0, dz = 0;
-    if (o > 0) fwd_off(o, dx, dy, dz);
-    double c = 0.0;
-    if (!ghost) {
-      for (int q = 0; q < Q; ++q) {
-        double sum = 0.0;
-        for (int d = 0; d < 3; ++d) {
-          const double* f = fac + (size_t)((q * 3 + d) * 3) * 2 * n1;
-          sum += tri(f, n1, i, dx) * tri(f + 2 * n1, n1, j, dy) * tri(f + 4 * n1, n1, k, dz);
+  // per term: the 3x3x3 factor values of each part loaded once (9 loads per part),
+  // s[o] = sum_d fx fy fz, then c[o] += theta_q s[o] (the summation order of the
+  // per-offset formulation)
+  double c[14];
+#pragma unroll
+  for (int o = 0; o < 14; ++o) c[o] = 0.0;
+  if (!ghost) {
+    for (int q = 0; q < Q; ++q) {
+      double sq[14];
+#pragma unroll
+      for (int o = 0; o < 14; ++o) sq[o] = 0.0;
+      for (int d = 0; d < 3; ++d) {
+        const double* f = fac + (size_t)((q * 3 + d) * 3) * 2 * n1;
+        double fx[3], fy[3], fz[3];
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          fx[t] = tri(f, n1, i, t - 1);
+          fy[t] = tri(f + 2 * n1, n1, j, t - 1);
+          fz[t] = tri(f + 4 * n1, n1, k, t - 1);
         }
-        c = fma(theta[(int64_t)mu * Q + q], sum, c);
+#pragma unroll
+        for (int o = 0; o < 14; ++o) {
+          int dx = 0, dy = 0, dz = 0;
+          if (o > 0) fwd_off(o, dx, dy, dz);
+          sq[o] += fx[dx + 1] * fy[dy + 1] * fz[dz + 1];
+        }
       }
+      const double t = theta[(int64_t)mu * Q + q];
+#pragma unroll
+      for (int o = 0; o < 14; ++o) c[o] = fma(t, sq[o], c[o]);
     }
-    C[o * n3 + X] = c;
-    if (o == 0) c0 = c;
   }
+#pragma unroll
+  for (int o = 0; o < 14; ++o) C[o * n3 + X] = c[o];
+  const double c0 = c[0];
   dinv[(int64_t)mu * n3 + X] = ghost ? 0.0 : 1.0 / c0;
 }
 
