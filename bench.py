@@ -622,7 +622,7 @@ def run_reference(args, rank, world):
     train = op.sample_mus(ospec, cfg["n_train"], seed=1000)
     test = op.sample_mus(ospec, args.batch or cfg["batch"], seed=2000)
 
-    def hf(mu):  # reference HighFidelitySolver(method="mgcg") (hf.py:453-467)
+    def hf(mu):  # reference HighFidelitySolver(method="mgcg") (hf.py:40-57)
         A, f = oprob.operator(mu), oprob.rhs()
         x, _ = so.mgcg_solve(A, f, np.zeros_like(f), so.mg_context_for(oprob, mu), 1e-14, 100)
         return x

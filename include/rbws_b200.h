@@ -18,8 +18,8 @@
  *    A buffer for `count` instances holds count*n^3 + 2*n^2 doubles (the
  *    trailing ghost region absorbs diagonal stencil reads of the last instance).
  *    Interior ordering inside the padded block equals the reference's free-DoF
- *    ordering (lexicographic, x fastest; reference grid.py:29-34,
- *    problems.py:409-421).
+ *    ordering (lexicographic, x fastest; reference grid.py:1-5,
+ *    problems.py:63-75).
  *  - Separable operator tables of an n-cell finest grid with Q affine terms:
  *      face[(q*3+d)*n + i]           d-face factor between nodes i and i+1
  *      node[((q*3+d)*3+a)*(n+1)+j]   factor along axis a != d at node j
@@ -52,7 +52,7 @@ int rbws_fetch(void* dst_host, const void* src_device, int64_t bytes, void* stre
 
 /* ---- hierarchy: mu-independent part of ParametricProblem -------------------
  * Replaces ParametricProblem.__init__ hierarchy/coarsening
- * (reference grid.py:231-262) and build_hierarchy (grid.py:191-198): nested
+ * (reference grid.py:203-236) and build_hierarchy (grid.py:163-170): nested
  * grids m0*2^i cells, trilinear prolongation, termwise Galerkin coarsening
  * (carried out on the 1D Kronecker factors of every affine term).
  * face/node: (host) separable tables of the finest grid (see above). */
@@ -70,10 +70,10 @@ int rbws_kron_factors(int n, int m0, int nterms, const double* face, const doubl
                       int level, double* out, int64_t capacity);
 
 /* ---- batch: mg_context_for for a batch of parameters -----------------------
- * Replaces mg_context_for / _finish_context (multigrid.py:493-541): per-mu
+ * Replaces mg_context_for / _finish_context (multigrid.py:154-202): per-mu
  * operators on every level, Jacobi diagonals, Cholesky of the coarsest level.
  * nu: sweeps per side (>= 1), omega: Jacobi damping (reference 0.7,
- * multigrid.py:367). */
+ * multigrid.py:27). */
 int rbws_batch_create(rbws_batch** out, rbws_hierarchy* h, int capacity, int nu, double omega);
 int rbws_batch_destroy(rbws_batch* b);
 /* theta: (dev) [count][Q] affine weights theta_q(mu). Returns the number of
@@ -87,34 +87,34 @@ int rbws_batch_setup(rbws_batch* b, const double* theta, int count, int* n_bad, 
 int rbws_batch_set_graph(rbws_batch* b, int enable);
 /* Smoother of the V-cycle: 0 damped Jacobi (the reference default for isotropic problems,
  * multigrid.py:183-188), 1 Gauss-Seidel (smoother="gs": nu forward lexicographic sweeps
- * before and nu backward sweeps after the coarse correction, multigrid.py:132-140, sweep
+ * before and nu backward sweeps after the coarse correction, multigrid.py:132-152, sweep
  * _smoothers.pyx:14-28).  Call before rbws_batch_setup; Gauss-Seidel allocates stored
  * fine face weights and coarse coefficients (the hyperplane-ordered sweeps read them). */
 int rbws_batch_set_smoother(rbws_batch* b, int kind);
 /* In-place Gauss-Seidel sweep(s) on `level` for every instance of a batch set up with
  * smoother 1: kind 1 forward, 2 backward, 3 symmetric (forward then backward; the MSRB
- * FINE_SMOOTH, reference msrb.py:19, kernels.py:97-101).  x, rhs: (dev) padded. */
+ * FINE_SMOOTH, reference msrb.py:20, kernels.py:93-95).  x, rhs: (dev) padded. */
 int rbws_smooth(rbws_batch* b, int level, int kind, double* x, const double* rhs, void* stream);
 /* 1 if the finest-level kernels of this batch read stored face weights (coefficients
  * whose z factors change on most planes; +24 B per node per stencil sweep), else 0 */
 int rbws_batch_stored_weights(const rbws_batch* b);
 
 /* y = A^level(mu) x for every instance (ParametricProblem.operator(mu, level) @ x,
- * grid.py:274-283).  x, y: (dev) padded vectors of that level. */
+ * grid.py:246-255).  x, y: (dev) padded vectors of that level. */
 int rbws_apply(rbws_batch* b, int level, const double* x, double* y, void* stream);
 /* One damped-Jacobi sweep y = x + omega (rhs - A x)/diag on `level`
  * (replaces _smoothers.pyx:31 csr_jacobi via Smoother._jacobi, kernels.py:98-115). */
 int rbws_jacobi_sweep(rbws_batch* b, int level, const double* x, const double* rhs, double* y,
                       void* stream);
-/* bc = P^T rf (multigrid.py:559 `P.T @ r`); nf = fine cells. (dev) */
+/* bc = P^T rf (multigrid.py:220 `P.T @ r`); nf = fine cells. (dev) */
 int rbws_restrict(int nf, int count, const double* rf, double* bc, void* stream);
-/* u += P ec (multigrid.py:560 `u + P @ e`). (dev) */
+/* u += P ec (multigrid.py:221 `u + P @ e`). (dev) */
 int rbws_prolong_add(int nf, int count, const double* ec, double* u, void* stream);
-/* One V-cycle from zero on the finest level (mg_vcycle, multigrid.py:544-561). (dev) */
+/* One V-cycle from zero on the finest level (mg_vcycle, multigrid.py:205-222). (dev) */
 int rbws_vcycle(rbws_batch* b, const double* rhs, double* out, void* stream);
 
-/* Batched MGCG (pcg_solve with the V-cycle preconditioner, krylov.py:267-334,
- * multigrid.py:564-571).
+/* Batched MGCG (pcg_solve with the V-cycle preconditioner, krylov.py:42-109,
+ * multigrid.py:225-232).
  * f: (dev) rhs, per instance stride f_stride doubles (0 = shared by all).
  * x: (dev) in: initial guesses, out: solutions.
  * iters [count], hist [count][l_max+1] (NaN padded), true_res [count],
@@ -137,7 +137,7 @@ int rbws_mgcg_solve_to_host(rbws_batch* b, const double* f, int64_t f_stride, do
 
 /* One smoothing-level kernel on `level` (>= 1): mode 0 y = A x, 1 y = rhs - A x,
  * 2 y = x + omega (rhs - A x)/diag, 3 y = rhs - A (omega dinv rhs) (the nu=1
- * pre-smoothing residual, multigrid.py:557-558).  (dev) padded vectors. */
+ * pre-smoothing residual, multigrid.py:218-219).  (dev) padded vectors. */
 int rbws_level_kernel(rbws_batch* b, int level, int mode, const double* x, const double* rhs,
                       double* y, void* stream);
 /* Copy of the per-instance Jacobi inverse diagonals 1/diag(A^level(mu)) of a
@@ -186,8 +186,8 @@ int rbws_dense_solve(int m, const double* A, const double* b, double* x, int* st
                      void* stream);
 
 /* ---- slab-decomposed single instance (BASELINE configs[4]) ----------------
- * One large instance of pcg_solve + mg_vcycle (krylov.py:267-334,
- * multigrid.py:544-571) with every level cut into `nslabs` slabs of whole
+ * One large instance of pcg_solve + mg_vcycle (krylov.py:42-109,
+ * multigrid.py:205-232) with every level cut into `nslabs` slabs of whole
  * z-planes; slab r owns planes [r n_l/nslabs, (r+1) n_l/nslabs) of level l.
  * Coarse levels with fewer than 8 planes per slab are replicated.  Slabs in
  * one process exchange halo planes with device copies; across processes (one

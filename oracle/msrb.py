@@ -50,7 +50,7 @@ def rbm_pod_solve(A, b, W) -> np.ndarray:
 
 
 def sgs_sweep(A, b) -> np.ndarray:
-    """One symmetric Gauss-Seidel sweep from zero (FINE_SMOOTH, msrb.py:19, kernels.py:97-101)."""
+    """One symmetric Gauss-Seidel sweep from zero (FINE_SMOOTH, msrb.py:20, kernels.py:93-95)."""
     x = np.zeros(A.shape[0])
     gs_sweep(A, x, b, True)
     gs_sweep(A, x, b, False)
@@ -58,7 +58,7 @@ def sgs_sweep(A, b) -> np.ndarray:
 
 
 def msrb_apply(b, A, W) -> np.ndarray:
-    """One smoothing sweep plus the reduced correction of its residual (msrb.py:42-53)."""
+    """One smoothing sweep plus the reduced correction of its residual (msrb.py:40-50)."""
     u = sgs_sweep(A, b)
     if W.shape[1] == 0:
         return u
@@ -80,7 +80,7 @@ class MsrbHierarchy:
 
 def msrb_train(mus, N: int, K_max: int, hf_solver, operator, rhs) -> MsrbHierarchy:
     """Per-iteration error-snapshot bases from the simulated reduced-initialised,
-    MSRB-preconditioned CG over the training set (msrb.py:109-146)."""
+    MSRB-preconditioned CG over the training set (msrb.py:113-149)."""
     mus = [np.asarray(m, dtype=np.float64) for m in mus]
     init = pod_build([hf_solver(m) for m in mus], N)
     if K_max == 0:
@@ -94,7 +94,7 @@ def msrb_train(mus, N: int, K_max: int, hf_solver, operator, rhs) -> MsrbHierarc
     for _k in range(K_max):
         pod_k = pod_build([hf_solver(m, st["r"]) for m, st in zip(mus, states)], N)
         bases.append(pod_k.basis)
-        for (A, _f), st in zip(systems, states):   # _PcgState.advance (msrb.py:88-106)
+        for (A, _f), st in zip(systems, states):   # _PcgState.advance (msrb.py:88-110)
             s = msrb_apply(st["r"], A, pod_k.basis)
             rs_new = float(st["r"] @ s)
             st["p"] = s if st["p"] is None else s + (rs_new / st["rs"]) * st["p"]
@@ -108,7 +108,7 @@ def msrb_train(mus, N: int, K_max: int, hf_solver, operator, rhs) -> MsrbHierarc
 
 def rbi_msrbcg_solve(A, f, hier: MsrbHierarchy, delta=1e-10, l_max=40):
     """rbi-msrbcg: POD Galerkin initial guess, PCG with the iteration-indexed MSRB
-    preconditioner (warmstart.py:81-117, msrb.py:56-85)."""
+    preconditioner (warmstart.py:81-117, msrb.py:53-85)."""
     u0 = rbm_pod_solve(A, f, hier.init_basis.basis)
     return pcg_solve(A, f, u0, precond=lambda r, k: msrb_apply(r, A, hier.basis_for(k)),
                      delta=delta, l_max=l_max, method="rbi-msrbcg")

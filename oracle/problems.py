@@ -5,13 +5,13 @@ discretisations of -div(a(x; mu) grad u) = f on the unit cube with
 homogeneous Dirichlet data.  The reference package only ships trilinear-FEM
 assembly; its solver stack (Galerkin coarsening, smoothers, PCG, L1ROC) is
 discretisation-agnostic, so these operators are fed to it through the same
-``ParametricProblem`` interface (reference grid.py:222-318) and the golden
+``ParametricProblem`` interface (reference grid.py:193-290) and the golden
 script injects them into the reference unchanged.
 
 Discretisation (documented in DESIGN.md §2):
 
 * grid: n cells per axis, nodes (n+1)^3, free DoFs = interior nodes in
-  lexicographic x-fastest order (reference problems.py:409-421, grid.py:236-240);
+  lexicographic x-fastest order (reference problems.py:63-75, grid.py:205-210);
 * operator of affine term q: sum over grid edges of
   ``w_q(edge) * (u_X - u_Y)^2 / 2`` where the edge weight is ``h`` times the
   mean of the term's coefficient over the dual face (an h x h square centred at
@@ -34,7 +34,7 @@ import scipy.sparse as sp
 
 @dataclass(frozen=True)
 class FDProblemSpec:
-    """A parametrised FV diffusion problem (mirrors reference problems.py:372-399)."""
+    """A parametrised FV diffusion problem (mirrors reference problems.py:26-53)."""
 
     pid: str
     kind: str                      # "thermal-block" | "smooth-affine"
@@ -49,14 +49,14 @@ class FDProblemSpec:
         return self.p if self.kind == "thermal-block" else self.n_modes + 1
 
     def theta(self, mu) -> np.ndarray:
-        """Affine weights theta_q(mu) (reference problems.py:364-369 DiffusionTerm.theta)."""
+        """Affine weights theta_q(mu) (reference problems.py:18-23 DiffusionTerm.theta)."""
         mu = self.check_mu(mu)
         if self.kind == "thermal-block":
             return mu.copy()
         return np.concatenate([[1.0], mu])
 
     def check_mu(self, mu) -> np.ndarray:
-        """Shape/bounds validation, as reference problems.py:393-399."""
+        """Shape/bounds validation, as reference problems.py:47-53."""
         mu = np.asarray(mu, dtype=np.float64)
         if mu.shape != (self.p,):
             raise ValueError(f"{self.pid} expects {self.p}-dimensional parameters")
@@ -160,7 +160,7 @@ def assemble_term_full(spec: FDProblemSpec, n: int, q: int) -> sp.csr_matrix:
 
 
 def interior_mask(n: int) -> np.ndarray:
-    """Dirichlet mask on lexicographic nodes (reference problems.py:409-421)."""
+    """Dirichlet mask on lexicographic nodes (reference problems.py:63-75)."""
     K, J, I = _node_axes(n)
     on_b = (I == 0) | (I == n) | (J == 0) | (J == n) | (K == 0) | (K == n)
     return on_b.ravel()
@@ -179,7 +179,7 @@ def rhs_full(spec: FDProblemSpec, n: int) -> np.ndarray:
 
 
 def prolongation_full(nc: int) -> sp.csr_matrix:
-    """Trilinear interpolation nc -> 2nc cells on all nodes (reference grid.py:159-169)."""
+    """Trilinear interpolation nc -> 2nc cells on all nodes (reference grid.py:131-141)."""
     nf = 2 * nc
     r = np.arange(nf + 1)
     # fine node r sits on coarse r/2 (even) or between (r-1)/2 and (r+1)/2 (odd)
@@ -193,11 +193,11 @@ def prolongation_full(nc: int) -> sp.csr_matrix:
 
 
 class OracleProblem:
-    """Affine operator factory over a nested hierarchy (reference grid.py:222-318).
+    """Affine operator factory over a nested hierarchy (reference grid.py:193-290).
 
     Terms are assembled on the finest grid, restricted to free DoFs, and
     Galerkin-coarsened term by term; operator(mu, level) is the theta-weighted
-    sum accumulated in term order, exactly as grid.py:274-283.
+    sum accumulated in term order, exactly as grid.py:246-255.
     """
 
     def __init__(self, spec: FDProblemSpec, n: int, m0: int = 4):

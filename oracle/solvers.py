@@ -15,7 +15,7 @@ import numpy as np
 import scipy.linalg as sla
 import scipy.sparse as sp
 
-JACOBI_OMEGA = 0.7   # multigrid.py:367
+JACOBI_OMEGA = 0.7   # multigrid.py:27
 
 
 class OperatorError(Exception):
@@ -29,7 +29,7 @@ class DegenerateBasisError(Exception):
 # ----------------------------------------------------------------- grid / MG
 
 def galerkin(A_fine, P) -> sp.csr_matrix:
-    """P^T A P (grid.py:201-209)."""
+    """P^T A P (grid.py:173-182)."""
     A_fine = sp.csr_matrix(A_fine)
     P = sp.csr_matrix(P)
     if A_fine.shape[1] != P.shape[0]:
@@ -44,7 +44,7 @@ def jacobi_sweep(A, diag, x, b, omega=JACOBI_OMEGA):
 
 def gs_sweep(A, x, b, forward: bool = True):
     """One in-place Gauss-Seidel sweep (reference _smoothers.pyx:14-28 csr_gauss_seidel,
-    kernels.py:124-134): x_i = (b_i - sum_{j != i} a_ij x_j) / a_ii row by row, rows in
+    kernels.py:117-129): x_i = (b_i - sum_{j != i} a_ij x_j) / a_ii row by row, rows in
     ascending (forward) or descending (backward) order.  Vectorised as the triangular
     solve of the reference's NumPy backend (_smoothers_np.py:35-42), which is the same
     sequential update."""
@@ -61,7 +61,7 @@ def gs_sweep(A, x, b, forward: bool = True):
 
 @dataclass
 class OracleMgContext:
-    """Per-parameter V-cycle data (multigrid.py:455-468, 493-507)."""
+    """Per-parameter V-cycle data (multigrid.py:116-129, 154-168)."""
 
     operators: list
     prolongations: list
@@ -69,7 +69,7 @@ class OracleMgContext:
     nu: int
     coarse_factor: tuple
     omega: float = JACOBI_OMEGA
-    smoother: str = "jacobi"  # "jacobi" (isotropic default) or "gs" (multigrid.py:132-140)
+    smoother: str = "jacobi"  # "jacobi" (isotropic default) or "gs" (multigrid.py:132-152)
 
     @property
     def levels(self):
@@ -78,7 +78,7 @@ class OracleMgContext:
 
 def mg_context_for(problem, mu, nu: int = 1, omega: float = JACOBI_OMEGA,
                    smoother: str = "jacobi") -> OracleMgContext:
-    """Operators per level from the affine terms + Cholesky of level 0 (multigrid.py:530-541)."""
+    """Operators per level from the affine terms + Cholesky of level 0 (multigrid.py:191-202)."""
     if nu < 0:
         raise ValueError("smoothing count must be non-negative")
     ops = [problem.operator(mu, level=i) for i in range(problem.levels)]
@@ -96,7 +96,7 @@ def mg_context_for(problem, mu, nu: int = 1, omega: float = JACOBI_OMEGA,
 
 
 def mg_vcycle(b, ctx: OracleMgContext, level=None) -> np.ndarray:
-    """One V-cycle from zero (multigrid.py:544-561) with Jacobi pre/post sweeps."""
+    """One V-cycle from zero (multigrid.py:205-222) with Jacobi pre/post sweeps."""
     if level is None:
         level = ctx.levels - 1
     b = np.asarray(b, dtype=np.float64)
@@ -105,7 +105,7 @@ def mg_vcycle(b, ctx: OracleMgContext, level=None) -> np.ndarray:
     A, d = ctx.operators[level], ctx.diags[level]
     P = ctx.prolongations[level - 1]
     u = np.zeros_like(b)
-    for _ in range(ctx.nu):  # "gs": forward sweeps before, backward after (multigrid.py:138)
+    for _ in range(ctx.nu):  # "gs": forward sweeps before, backward after (multigrid.py:137-138)
         u = jacobi_sweep(A, d, u, b, ctx.omega) if ctx.smoother == "jacobi" else gs_sweep(A, u, b, True)
     r = b - A @ u
     e = mg_vcycle(P.T @ r, ctx, level - 1)
@@ -119,7 +119,7 @@ def mg_vcycle(b, ctx: OracleMgContext, level=None) -> np.ndarray:
 
 @dataclass
 class SolveReport:
-    """Convergence record (krylov.py:250-264)."""
+    """Convergence record (krylov.py:25-39)."""
 
     method: str
     iterations: int
@@ -135,7 +135,7 @@ class SolveReport:
 
 
 def pcg_solve(A, f, x0, precond=None, delta=1e-16, l_max=40, method="pcg", mu=None):
-    """Preconditioned CG, recurrence residual drives the loop (krylov.py:267-334)."""
+    """Preconditioned CG, recurrence residual drives the loop (krylov.py:42-109)."""
     if delta <= 0:
         raise ValueError("tolerance must be positive")
     if l_max < 0:
@@ -178,7 +178,7 @@ def pcg_solve(A, f, x0, precond=None, delta=1e-16, l_max=40, method="pcg", mu=No
 
 
 def mgcg_solve(A, f, x0, ctx, delta=1e-16, l_max=40, mu=None, method="mgcg"):
-    """PCG with one V-cycle per application (multigrid.py:564-571)."""
+    """PCG with one V-cycle per application (multigrid.py:225-232)."""
     return pcg_solve(A, f, x0, lambda r, k: mg_vcycle(r, ctx), delta, l_max, method, mu)
 
 
@@ -323,7 +323,7 @@ def l1roc_offline(mus, N, hf_solve, operator, operator_rows, rhs, seed=0, on_deg
 
 
 def rbi_mgcg_solve(problem, mu, model, delta=1e-10, l_max=40, nu=1):
-    """RBI-MGCG: L1ROC warm start then MGCG (warmstart.py:364-410, experiment.py:149-157)."""
+    """RBI-MGCG: L1ROC warm start then MGCG (warmstart.py:88-117, experiment.py:149-157)."""
     A, f = problem.operator(mu), problem.rhs(mu)
     ctx = mg_context_for(problem, mu, nu=nu)
     u0 = np.zeros_like(f) if model is None else l1roc_online(model, A, f)[0]
@@ -332,7 +332,7 @@ def rbi_mgcg_solve(problem, mu, model, delta=1e-10, l_max=40, nu=1):
 
 
 def lhs_sample(p, n, bounds, seed=0):
-    """Seeded Latin hypercube (sampling.py:478-497)."""
+    """Seeded Latin hypercube (sampling.py:8-27)."""
     if n < 1:
         raise ValueError("need at least one sample")
     bounds = np.asarray(bounds, dtype=np.float64)

@@ -1,5 +1,5 @@
 // Batched lexicographic Gauss-Seidel sweeps (reference smoother="gs": forward sweeps before
-// and backward sweeps after the coarse-grid correction, multigrid.py:132-140; the sweep is
+// and backward sweeps after the coarse-grid correction, multigrid.py:132-152; the sweep is
 // _smoothers.pyx:14-28 csr_gauss_seidel).
 //
 // A lexicographic sweep updates node X from the new values of its lower-index neighbours

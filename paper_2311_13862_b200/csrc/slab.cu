@@ -1,8 +1,8 @@
 // Slab-decomposed MGCG for one large instance (BASELINE configs[4]: 512^3,
 // slabs along z, one-plane halo exchange per stencil sweep).
 //
-// The reference solves one instance with pcg_solve + mg_vcycle (krylov.py:267-334,
-// multigrid.py:544-571); this is the same algorithm with the grid of every fine
+// The reference solves one instance with pcg_solve + mg_vcycle (krylov.py:42-109,
+// multigrid.py:205-232); this is the same algorithm with the grid of every fine
 // level cut into R slabs of whole z-planes.  Slab r owns the planes
 // [r n_l / R, (r+1) n_l / R) of level l and stores them with one halo plane on each
 // side in the padded layout, so the finest-level and coarse-level kernels run

@@ -1,10 +1,10 @@
 // Batched MGCG runtime (host C++ orchestrating the sm_100a kernels).
 //
 // Restates, batched over parameter instances:
-//   ParametricProblem hierarchy + termwise Galerkin coarsening  (reference grid.py:231-262)
-//   mg_context_for: per-mu operators on every level + Cholesky   (multigrid.py:530-541, 493-507)
-//   mg_vcycle with damped-Jacobi pre/post sweeps                  (multigrid.py:544-561, kernels.py:98-115)
-//   pcg_solve                                                      (krylov.py:267-334)
+//   ParametricProblem hierarchy + termwise Galerkin coarsening  (reference grid.py:203-236)
+//   mg_context_for: per-mu operators on every level + Cholesky   (multigrid.py:191-202, 154-168)
+//   mg_vcycle with damped-Jacobi pre/post sweeps                  (multigrid.py:205-222, kernels.py:98-115)
+//   pcg_solve                                                      (krylov.py:42-109)
 #include <atomic>
 #include <cmath>
 #include <cstdio>

@@ -1,7 +1,7 @@
 """Nested grids, padded device layout and the batched parametric operator.
 
 B200 counterpart of the reference ``grid.py`` (ParametricProblem,
-grid.py:222-318; build_hierarchy, grid.py:191-198).  The reference assembles
+grid.py:193-290; build_hierarchy, grid.py:163-170).  The reference assembles
 sparse matrices per term and Galerkin-coarsens them with scipy; here the
 mu-independent part (the hierarchy and the Kronecker factors of every term
 on every level) lives in the native ``rbws_hierarchy`` and per-parameter
@@ -62,7 +62,7 @@ def padded_to_interior_index(pidx, n: int) -> np.ndarray:
 class ParametricProblem:
     """Factory for batched A_h(mu), f_h(mu) and the multigrid hierarchy.
 
-    Signature mirrors the reference (grid.py:231): ``levels`` nested grids of
+    Signature mirrors the reference (grid.py:203): ``levels`` nested grids of
     ``m0 * 2**i`` cells.  Immutable after construction.
     """
 
@@ -129,7 +129,7 @@ class ParametricProblem:
         return torch.zeros(padded_len(n, count), dtype=torch.float64, device="cuda")
 
     def operator(self, mus, ctx=None):
-        """Batched operator A_h(mu) for the given parameters (grid.py:274-283)."""
+        """Batched operator A_h(mu) for the given parameters (grid.py:246-255)."""
         from .multigrid import mg_context_for
         if ctx is None:
             ctx = mg_context_for(self, mus)

@@ -1,8 +1,8 @@
-"""High-fidelity solves for snapshot generation (reference hf.py:422-470).
+"""High-fidelity solves for snapshot generation (reference hf.py:12-60).
 
 The reference factors A_h(mu) with SuperLU; on the B200 the high-fidelity
 solve is the batched MGCG driven to a tight tolerance (the reference's
-``method="mgcg"`` branch, hf.py:453-467, delta=1e-14, l_max=100).
+``method="mgcg"`` branch, hf.py:40-57, delta=1e-14, l_max=100).
 """
 
 from __future__ import annotations

@@ -1,6 +1,6 @@
 """Solve reports and errors of the batched Krylov path.
 
-Mirrors reference krylov.py:246-264 (OperatorError, SolveReport).  The
+Mirrors reference krylov.py:21-39 (OperatorError, SolveReport).  The
 batched PCG itself is native (rbws_mgcg_solve, csrc/solver.cu); the Python
 entry point is ``multigrid.mgcg_solve`` / ``krylov.pcg_solve``.
 """
@@ -19,7 +19,7 @@ class OperatorError(Exception):
 
 @dataclass
 class SolveReport:
-    """Convergence record of one iterative solve (krylov.py:250-264)."""
+    """Convergence record of one iterative solve (krylov.py:25-39)."""
 
     method: str
     iterations: int
@@ -107,7 +107,7 @@ class SolveReports(Sequence):
 
 def pcg_solve(A, f, x0, precond=None, delta: float = 1e-16, l_max: int = 40,
               method: str = "pcg", mu=None):
-    """Batched PCG (krylov.py:267-334) with the multigrid preconditioner.
+    """Batched PCG (krylov.py:42-109) with the multigrid preconditioner.
 
     ``precond`` must be the batch's MgContext (the B200 path fuses the
     preconditioner into the native PCG loop); A is the BatchOperator bound

@@ -16,7 +16,7 @@ error-snapshot POD space.  Batched over parameters:
 
 Semantics follow the reference: msrb_train simulates the reduced-initialised,
 MSRB-preconditioned CG over the training set, one iteration per basis index
-(msrb.py:109-146); the preconditioner for iteration k >= K_max reuses the last basis.
+(msrb.py:113-149); the preconditioner for iteration k >= K_max reuses the last basis.
 """
 
 from __future__ import annotations
@@ -106,7 +106,7 @@ class _Reduced:
 
 @dataclass
 class MsrbHierarchy:
-    """Initial POD space plus one error-snapshot basis per iteration index (msrb.py:22-39)."""
+    """Initial POD space plus one error-snapshot basis per iteration index (msrb.py:23-37)."""
 
     init_basis: PodBasis
     bases: tuple
@@ -157,7 +157,7 @@ def _apply_precond(ops, red: _Reduced | None, L, r):
 
 
 def msrb_train(mus, N: int, K_max: int, hf_solver, problem) -> MsrbHierarchy:
-    """Per-iteration error-snapshot bases (msrb.py:109-146); hf_solver: HighFidelitySolver."""
+    """Per-iteration error-snapshot bases (msrb.py:113-149); hf_solver: HighFidelitySolver."""
     import torch
     if K_max < 0:
         raise ValueError("K_max must be non-negative")
@@ -187,7 +187,7 @@ def msrb_train(mus, N: int, K_max: int, hf_solver, problem) -> MsrbHierarchy:
         spectra.append(pod_k.eigenvalues)
         red = _Reduced(problem, pod_k.basis)
         s = _apply_precond(ops, red, red.factor(theta) if red.N else None, r)
-        rs_new = (r * s).sum(1)                      # _PcgState.advance (msrb.py:88-106)
+        rs_new = (r * s).sum(1)                      # _PcgState.advance (msrb.py:88-110)
         p = s if p is None else s + (rs_new / rs)[:, None] * p
         rs = rs_new
         Ap = ops.apply(p)
@@ -200,8 +200,8 @@ def msrb_train(mus, N: int, K_max: int, hf_solver, problem) -> MsrbHierarchy:
 def rbi_msrbcg_solve(problem, mus, hier: MsrbHierarchy, f=None, delta: float = 1e-16,
                      l_max: int = 40, method: str = "rbi-msrbcg", ctx: MgContext | None = None):
     """Batched rbi-msrbcg: POD Galerkin initial guess (warmstart.py:81-84), then PCG
-    (krylov.py:42-93 semantics, per instance) with the MSRB preconditioner
-    (msrb.py:56-85).  Returns (x (count, n^3) padded rows, SolveReports)."""
+    (krylov.py:42-109 semantics, per instance) with the MSRB preconditioner
+    (msrb.py:53-85).  Returns (x (count, n^3) padded rows, SolveReports)."""
     import torch
     from .multigrid import mg_context_for
     mus = problem.spec.check_mus(mus)

@@ -1,14 +1,14 @@
 """Batched geometric multigrid and MGCG on the B200.
 
 B200 counterpart of reference multigrid.py:
-  * ``mg_context_for`` (multigrid.py:530-541) -> per-batch native context:
+  * ``mg_context_for`` (multigrid.py:191-202) -> per-batch native context:
     operators of every level for every mu (coarse levels as per-instance
     27-point stencils assembled from the Kronecker factors), Jacobi
     diagonals, Cholesky of the coarsest level;
-  * ``mg_vcycle`` (multigrid.py:544-561) -> one V-cycle for the whole batch;
-  * ``mgcg_solve`` (multigrid.py:564-571) -> native batched PCG.
+  * ``mg_vcycle`` (multigrid.py:205-222) -> one V-cycle for the whole batch;
+  * ``mgcg_solve`` (multigrid.py:225-232) -> native batched PCG.
 The smoother is the reference's isotropic default, damped Jacobi with
-omega = 0.7 (multigrid.py:366-367, 522-527).
+omega = 0.7 (multigrid.py:26-27, 183-188).
 """
 
 from __future__ import annotations
@@ -23,13 +23,13 @@ from .grid import BatchOperator, ParametricProblem, padded_len
 from .krylov import OperatorError, SolveReport, SolveReports
 
 JACOBI_OMEGA = 0.7
-# V-cycle smoothers (reference multigrid.py:132-150): damped Jacobi both sides, or forward
+# V-cycle smoothers (reference multigrid.py:132-152): damped Jacobi both sides, or forward
 # Gauss-Seidel before / backward after the coarse correction
 SMOOTHERS = ("jacobi", "gs")
 
 
 class MgContext:
-    """Per-batch multigrid state (reference MgContext, multigrid.py:455-468)."""
+    """Per-batch multigrid state (reference MgContext, multigrid.py:116-129)."""
 
     def __init__(self, problem: ParametricProblem, capacity: int, nu: int = 1,
                  omega: float = JACOBI_OMEGA, smoother: str = "jacobi"):
@@ -85,7 +85,7 @@ class MgContext:
 
 def mg_context_for(problem: ParametricProblem, mus, nu: int = 1, smoother: str = "auto",
                    ctx: MgContext | None = None) -> MgContext:
-    """Batched mg_context_for (multigrid.py:530-541).
+    """Batched mg_context_for (multigrid.py:191-202).
 
     ``mus``: one parameter or an array (count, p).  Pass an existing ``ctx``
     to reuse its device buffers for a new batch.
@@ -102,7 +102,7 @@ def mg_context_for(problem: ParametricProblem, mus, nu: int = 1, smoother: str =
 
 
 def mg_vcycle(b, ctx: MgContext, level=None):
-    """One V-cycle from zero for every instance of the batch (multigrid.py:544-561)."""
+    """One V-cycle from zero for every instance of the batch (multigrid.py:205-222)."""
     import torch
     if level is not None and level != ctx.levels - 1:
         raise ValueError("the batched V-cycle is entered on the finest level")
@@ -117,7 +117,7 @@ def mg_vcycle(b, ctx: MgContext, level=None):
 def mgcg_solve(A, f, x0, ctx: MgContext, delta: float = 1e-16, l_max: int = 40, mu=None,
                method: str = "mgcg", raise_on_breakdown: bool = True,
                overwrite_x0: bool = False, out_host=None, copy_stream=None):
-    """Batched MGCG (multigrid.py:564-571 -> krylov.py:267-334).
+    """Batched MGCG (multigrid.py:225-232 -> krylov.py:42-109).
 
     f: padded rhs, either one instance (shared) or a full batch; x0: padded
     batch of initial guesses (None = zeros), left untouched unless

@@ -1,6 +1,6 @@
 """Parametrised diffusion problems of the BASELINE configurations.
 
-Mirrors the reference's ``ProblemSpec`` (reference problems.py:372-421):
+Mirrors the reference's ``ProblemSpec`` (reference problems.py:26-75):
 a parameter box, affine diffusion terms ``K(x; mu) = sum_q theta_q(mu) k_q(x)``
 and a source.  Here every term is *separable along the grid axes*, which is
 what lets the B200 path keep the finest operator implicit: each term is
@@ -37,7 +37,7 @@ class ProblemSpec:
         return self.p if self.kind == "thermal-block" else self.n_modes + 1
 
     def check_mu(self, mu) -> np.ndarray:
-        """Validate one parameter (reference problems.py:393-399)."""
+        """Validate one parameter (reference problems.py:47-53)."""
         mu = np.asarray(mu, dtype=np.float64)
         if mu.shape != (self.p,):
             raise ValueError(f"{self.pid} expects {self.p}-dimensional parameters")
@@ -147,7 +147,7 @@ _REGISTRY = {
 
 
 def get_problem(pid: str) -> ProblemSpec:
-    """Registry lookup (reference problems.py:501-507)."""
+    """Registry lookup (reference problems.py:158-162)."""
     try:
         return _REGISTRY[pid]()
     except KeyError:

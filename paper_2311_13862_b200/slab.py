@@ -1,8 +1,8 @@
 """Slab-decomposed MGCG for one large instance (BASELINE configs[4]).
 
-The reference solves a single parameter with ``mgcg_solve`` (multigrid.py:564-571
--> krylov.py:267-334) on one CPU process.  ``SlabSolver`` runs the same
-preconditioned CG with the V-cycle of multigrid.py:544-561 on a grid cut into
+The reference solves a single parameter with ``mgcg_solve`` (multigrid.py:225-232
+-> krylov.py:42-109) on one CPU process.  ``SlabSolver`` runs the same
+preconditioned CG with the V-cycle of multigrid.py:205-222 on a grid cut into
 ``nslabs`` slabs of whole z-planes (C ABI ``rbws_slab_*``):
 
 * one process, ``nslabs`` slabs on its GPU (halo planes exchanged by device
@@ -104,7 +104,7 @@ class SlabSolver:
             _native._lib.rbws_slab_destroy(s)
 
     def setup(self, mu, stream=None):
-        """mg_context_for (multigrid.py:530-541) for one parameter."""
+        """mg_context_for (multigrid.py:191-202) for one parameter."""
         import torch
         mu = self.problem.spec.check_mus(mu)
         if len(mu) != 1:
@@ -142,7 +142,7 @@ class SlabSolver:
         _native.call("rbws_slab_prolong_x", self._s, ec.data_ptr(), _native.stream_ptr(stream))
 
     def solve(self, delta: float = 1e-10, l_max: int = 60, stream=None) -> SolveReport:
-        """PCG with the V-cycle preconditioner from the loaded x (krylov.py:267-334)."""
+        """PCG with the V-cycle preconditioner from the loaded x (krylov.py:42-109)."""
         if delta <= 0:
             raise ValueError("tolerance must be positive")
         if l_max < 0:

@@ -14,7 +14,7 @@ through the reference's own ``ProblemSpec``/``ParametricProblem`` API by
 substituting its two assembly hooks (``grid.assemble_stiffness_kernel`` and
 ``grid.assemble_load``) with the oracle's FV term matrices.  Everything after
 assembly — free-DoF slicing, prolongations, Galerkin coarsening
-(grid.py:231-262), ``mg_context_for``/``mg_vcycle``/``mgcg_solve``
+(grid.py:203-236), ``mg_context_for``/``mg_vcycle``/``mgcg_solve``
 (multigrid.py), ``pcg_solve`` (krylov.py), ``l1roc_offline``/``l1roc_online``
 (rb.py), ``HighFidelitySolver`` (hf.py) — is the unmodified reference code.
 
@@ -201,7 +201,7 @@ def main():
 
 def main_gs():
     """Gauss-Seidel smoother goldens (smoother="gs": forward GS before, backward after the
-    coarse correction, multigrid.py:132-140) -> tests/golden/golden_gs.npz."""
+    coarse correction, multigrid.py:132-152) -> tests/golden/golden_gs.npz."""
     rbws = _import_reference()
     sys.path.insert(0, str(REPO))
     from oracle import problems as op
