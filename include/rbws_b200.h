@@ -58,6 +58,22 @@ int rbws_fetch(void* dst_host, const void* src_device, int64_t bytes, void* stre
  * face/node: (host) separable tables of the finest grid (see above). */
 int rbws_hierarchy_create(rbws_hierarchy** out, int n, int m0, int nterms,
                           const double* face, const double* node);
+/* Assembled (FEM) problems — the reference's own ParametricProblem path: per-term
+ * stiffness assembled on the finest grid, restricted to free DoFs and Galerkin-coarsened
+ * term by term (grid.py:203-236); operator(mu, level) = sum_q theta_q A_q^level
+ * (grid.py:246-255).  coef: (host) levels 0..L-1 concatenated, level l =
+ * [nterms][14][n_l^3] symmetric 27-point coefficients in the padded layout (index 0 the
+ * diagonal, 1..13 the lexicographically positive offsets (dx,dy,dz): dz=1 rows
+ * 1 + 3(dy+1) + (dx+1), then (dx,1,0) at 11+dx, then (1,0,0) at 13), zero on ghosts.
+ * Every level runs the stored-coefficient kernels; batches, V-cycles and MGCG use the
+ * same entry points as separable problems (the rhs must be per instance). */
+int rbws_hierarchy_create_stored(rbws_hierarchy** out, int n, int m0, int nterms,
+                                 const double* coef);
+int rbws_hierarchy_is_stored(const rbws_hierarchy* h);
+/* y = A_q^level x for `count` padded vectors (one affine term, mu-independent): the
+ * per-term products of the L1ROC projection (rb.py:200-201) on stored problems. */
+int rbws_hierarchy_term_apply(const rbws_hierarchy* h, int level, int term, int count,
+                              const double* x, double* y, void* stream);
 int rbws_hierarchy_destroy(rbws_hierarchy* h);
 int rbws_hierarchy_levels(const rbws_hierarchy* h);
 int rbws_hierarchy_cells(const rbws_hierarchy* h, int level);

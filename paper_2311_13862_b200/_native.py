@@ -26,6 +26,9 @@ SIGNATURES = {
     "rbws_launch_count": [],
     "rbws_fetch": [_vp, _vp, _c_int64, _vp],
     "rbws_hierarchy_create": [_pp, _c_int, _c_int, _c_int, _vp, _vp],
+    "rbws_hierarchy_create_stored": [_pp, _c_int, _c_int, _c_int, _vp],
+    "rbws_hierarchy_is_stored": [_vp],
+    "rbws_hierarchy_term_apply": [_vp, _c_int, _c_int, _c_int, _vp, _vp, _vp],
     "rbws_hierarchy_destroy": [_vp],
     "rbws_hierarchy_levels": [_vp],
     "rbws_hierarchy_cells": [_vp, _c_int],

@@ -47,6 +47,35 @@ int rbws_hierarchy_create(rbws_hierarchy** out, int n, int m0, int nterms, const
   return 0;
 }
 
+int rbws_hierarchy_create_stored(rbws_hierarchy** out, int n, int m0, int nterms,
+                                 const double* coef) {
+  if (!out || !coef) RBWS_FAIL("null argument");
+  Hierarchy* h = nullptr;
+  if (rbws::hierarchy_create_stored(&h, n, m0, nterms, coef)) return 1;
+  *out = reinterpret_cast<rbws_hierarchy*>(h);
+  return 0;
+}
+
+int rbws_hierarchy_is_stored(const rbws_hierarchy* h) { return H(h)->stored ? 1 : 0; }
+
+int rbws_hierarchy_term_apply(const rbws_hierarchy* h, int level, int term, int count,
+                              const double* x, double* y, void* stream) {
+  const Hierarchy* hh = H(h);
+  if (!hh->stored) RBWS_FAIL("term products need a stored-coefficient hierarchy");
+  if (level < 0 || level >= hh->levels) RBWS_FAIL("level outside hierarchy");
+  if (term < 0 || term >= hh->Q) RBWS_FAIL("term outside [0, nterms)");
+  if (count < 1) RBWS_FAIL("count must be positive");
+  rbws::CoarseOp op;
+  op.n = hh->cells[level];
+  op.Q = hh->Q;
+  const int64_t n3 = (int64_t)op.n * op.n * op.n;
+  op.coef = hh->d_tcoef[level] + (int64_t)term * 14 * n3;
+  op.coef_shared = true;
+  rbws::LaunchCtx lc{S(stream), nullptr};
+  RBWS_CHECK(rbws::coarse_launch(0, op, nullptr, count, x, nullptr, y, 0.0, lc));
+  return 0;
+}
+
 int rbws_hierarchy_destroy(rbws_hierarchy* h) {
   delete H(h);
   return 0;
@@ -105,7 +134,7 @@ int rbws_smooth(rbws_batch* b, int level, int kind, double* x, const double* rhs
   if (kind != 1 && kind != 2 && kind != 3) RBWS_FAIL("kind: 1 forward, 2 backward, 3 symmetric GS");
   const int n = h->cells[level];
   rbws::LaunchCtx lc{S(stream), nullptr};
-  const bool fine = (level == h->levels - 1);
+  const bool fine = h->sep_fine(level);
   if (fine ? !bb->wface : !bb->lv[level].coef)
     RBWS_FAIL("Gauss-Seidel sweeps need a batch with smoother = 1 (rbws_batch_set_smoother)");
   for (int pass = 0; pass < 2; ++pass) {
@@ -146,7 +175,7 @@ int rbws_apply(rbws_batch* b, int level, const double* x, double* y, void* strea
   if (level < 0 || level >= h->levels) RBWS_FAIL("level outside hierarchy");
   if (bb->count < 1) RBWS_FAIL("batch_setup must be called first");
   rbws::LaunchCtx lc{S(stream), nullptr};
-  if (level == h->levels - 1) {
+  if (h->sep_fine(level)) {
     RBWS_CHECK(rbws::fine_apply(bb->fine_op(), bb->count, x, y, nullptr, lc));
   } else {
     RBWS_CHECK(rbws::coarse_launch(0, bb->cop(level), bb->theta, bb->count, x, nullptr, y, 0.0, lc));
@@ -161,7 +190,7 @@ int rbws_jacobi_sweep(rbws_batch* b, int level, const double* x, const double* r
   if (level < 1 || level >= h->levels) RBWS_FAIL("smoothing level must be in [1, levels)");
   if (bb->count < 1) RBWS_FAIL("batch_setup must be called first");
   rbws::LaunchCtx lc{S(stream), nullptr};
-  if (level == h->levels - 1) {
+  if (h->sep_fine(level)) {
     RBWS_CHECK(rbws::fine_jacobi(bb->fine_op(), bb->count, x, rhs, y, bb->omega, nullptr, lc));
   } else {
     RBWS_CHECK(rbws::coarse_launch(2, bb->cop(level), bb->theta, bb->count, x, rhs, y, bb->omega, lc));
@@ -221,7 +250,7 @@ int rbws_level_kernel(rbws_batch* b, int level, int mode, const double* x, const
   if (bb->count < 1) RBWS_FAIL("batch_setup must be called first");
   rbws::LaunchCtx lc{S(stream), nullptr};
   const double* dinv = bb->lv[level].dinv;
-  if (level == h->levels - 1) {
+  if (h->sep_fine(level)) {
     const rbws::Sep7 op = bb->fine_op();
     cudaError_t e;
     if (mode == 0) e = rbws::fine_apply(op, bb->count, x, y, nullptr, lc);
@@ -276,6 +305,7 @@ int rbws_batch_profile_read(rbws_batch* b, double* ms, int64_t* calls, int64_t* 
 
 int rbws_l1roc_project(rbws_hierarchy* h, const double* W, int64_t Wstride, int N,
                        const int64_t* rows, int M, double* Bq, void* stream) {
+  if (H(h)->stored) RBWS_FAIL("stored-coefficient problems project with rbws_hierarchy_term_apply");
   Hierarchy* hh = H(h);
   RBWS_CHECK(rbws::l1roc_project(hh->n, hh->Q, hh->d_face, hh->d_node, W, Wstride, N, rows, M, Bq,
                                  S(stream)));
@@ -329,6 +359,7 @@ int rbws_comm_unique_id(uint8_t* out128) {
 int rbws_slab_create(rbws_slab** out, rbws_hierarchy* h, int nslabs, int nlocal,
                      const uint8_t* nccl_id, int nprocs, int proc_rank, double omega) {
   if (!out || !h) RBWS_FAIL("null argument");
+  if (H(h)->stored) RBWS_FAIL("the slab path takes separable (Kronecker-factor) problems");
   rbws::Comm* comm = nullptr;
   if (nprocs < 1 || proc_rank < 0 || proc_rank >= nprocs) RBWS_FAIL("bad process count / rank");
   if (nprocs > 1 && !nccl_id) RBWS_FAIL("multi-process slabs need an NCCL id");

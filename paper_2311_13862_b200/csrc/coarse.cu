@@ -561,7 +561,8 @@ __global__ void __launch_bounds__(256) coarse_stored_kernel(int n, const double*
                                                             const double* __restrict__ b,
                                                             double* __restrict__ y,
                                                             const int* __restrict__ active,
-                                                            double omega, int zlo, int zhi) {
+                                                            double omega, int zlo, int zhi,
+                                                            int64_t cstride) {
   const int mu = blockIdx.y;
   if (active && !active[mu]) return;
   const int64_t n2 = (int64_t)n * n, n3 = n2 * n;
@@ -569,7 +570,7 @@ __global__ void __launch_bounds__(256) coarse_stored_kernel(int n, const double*
   if (X >= (int64_t)zhi * n2) return;
   const int i = X % n, j = (X / n) % n, k = (int)(X / n2);
   if (i == 0 || j == 0 || k == 0) return;
-  const double* C = coef + (int64_t)mu * 14 * n3;
+  const double* C = coef + (int64_t)mu * cstride;
   const int64_t base = (int64_t)mu * n3;
   const double c0 = __ldg(C + X);
   if (MODE == 4) {
@@ -601,12 +602,13 @@ static cudaError_t coarse_stored_launch(int mode, const CoarseOp& op, int batch,
   const int zlo = lc.zhi > 0 ? lc.zlo : 0, zhi = lc.zhi > 0 ? lc.zhi : n;
   const int64_t cnt = (int64_t)(zhi - zlo) * n * n;
   dim3 grd((unsigned)((cnt + 255) / 256), batch);
+  const int64_t cs = op.coef_shared ? 0 : (int64_t)14 * n * n * n;
   count_launch();
   switch (mode) {
-    case 0: coarse_stored_kernel<0><<<grd, 256, 0, lc.stream>>>(n, op.coef, x, b, y, lc.active, omega, zlo, zhi); break;
-    case 1: coarse_stored_kernel<1><<<grd, 256, 0, lc.stream>>>(n, op.coef, x, b, y, lc.active, omega, zlo, zhi); break;
-    case 2: coarse_stored_kernel<2><<<grd, 256, 0, lc.stream>>>(n, op.coef, x, b, y, lc.active, omega, zlo, zhi); break;
-    case 4: coarse_stored_kernel<4><<<grd, 256, 0, lc.stream>>>(n, op.coef, x, b, y, lc.active, omega, zlo, zhi); break;
+    case 0: coarse_stored_kernel<0><<<grd, 256, 0, lc.stream>>>(n, op.coef, x, b, y, lc.active, omega, zlo, zhi, cs); break;
+    case 1: coarse_stored_kernel<1><<<grd, 256, 0, lc.stream>>>(n, op.coef, x, b, y, lc.active, omega, zlo, zhi, cs); break;
+    case 2: coarse_stored_kernel<2><<<grd, 256, 0, lc.stream>>>(n, op.coef, x, b, y, lc.active, omega, zlo, zhi, cs); break;
+    case 4: coarse_stored_kernel<4><<<grd, 256, 0, lc.stream>>>(n, op.coef, x, b, y, lc.active, omega, zlo, zhi, cs); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -657,6 +659,35 @@ cudaError_t coarse_launch(int mode, const CoarseOp& op, const double* theta, int
 namespace rbws {
 
 // ---------------------------------------------------------------- coarsest level
+// right-looking Cholesky of the m x m matrix A (shared memory, lower triangle) by the whole
+// CTA; L (global) gets the factor, *status 1 if a pivot was not positive
+__device__ void chol_store(double* A, int m, double* L, int* status) {
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int c = 0; c < m; ++c) {
+    if (threadIdx.x == 0) {
+      const double dd = A[c * m + c];
+      if (!(dd > 0.0)) bad = 1;
+      A[c * m + c] = sqrt(dd > 0.0 ? dd : 1.0);
+    }
+    __syncthreads();
+    const double piv = A[c * m + c];
+    for (int r = c + 1 + threadIdx.x; r < m; r += blockDim.x) A[r * m + c] /= piv;
+    __syncthreads();
+    for (int t = threadIdx.x; t < (m - c - 1) * (m - c - 1); t += blockDim.x) {
+      const int r = c + 1 + t / (m - c - 1), s = c + 1 + t % (m - c - 1);
+      if (s <= r) A[r * m + s] -= A[r * m + c] * A[s * m + c];
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < m * m; t += blockDim.x) {
+    const int r = t / m, s = t % m;
+    L[t] = (s <= r) ? A[t] : 0.0;
+  }
+  if (threadIdx.x == 0 && status) *status = bad;
+}
+
 // Dense Galerkin operator of the coarsest level assembled from the Kronecker
 // factors, then Cholesky-factored in shared memory (one CTA per instance).
 __global__ void coarse_factor_kf_kernel(int n0, int Q, const double* __restrict__ fac,
@@ -682,31 +713,7 @@ __global__ void coarse_factor_kf_kernel(int n0, int Q, const double* __restrict_
     A[t] = v;
   }
   __syncthreads();
-  __shared__ int bad;
-  if (threadIdx.x == 0) bad = 0;
-  __syncthreads();
-  for (int c = 0; c < m; ++c) {  // right-looking Cholesky, lower triangle
-    if (threadIdx.x == 0) {
-      const double dd = A[c * m + c];
-      if (!(dd > 0.0)) bad = 1;
-      A[c * m + c] = sqrt(dd > 0.0 ? dd : 1.0);
-    }
-    __syncthreads();
-    const double piv = A[c * m + c];
-    for (int r = c + 1 + threadIdx.x; r < m; r += blockDim.x) A[r * m + c] /= piv;
-    __syncthreads();
-    for (int t = threadIdx.x; t < (m - c - 1) * (m - c - 1); t += blockDim.x) {
-      const int r = c + 1 + t / (m - c - 1), s = c + 1 + t % (m - c - 1);
-      if (s <= r) A[r * m + s] -= A[r * m + c] * A[s * m + c];
-    }
-    __syncthreads();
-  }
-  double* L = Lout + (int64_t)mu * m * m;
-  for (int t = threadIdx.x; t < m * m; t += blockDim.x) {
-    const int r = t / m, s = t % m;
-    L[t] = (s <= r) ? A[t] : 0.0;
-  }
-  if (threadIdx.x == 0 && status) status[mu] = bad;
+  chol_store(A, m, Lout + (int64_t)mu * m * m, status ? status + mu : nullptr);
 }
 
 cudaError_t coarse_factor_kf(int n0, int Q, const double* fac, const double* theta, int batch,
@@ -721,6 +728,102 @@ cudaError_t coarse_factor_kf(int n0, int Q, const double* fac, const double* the
   }
   count_launch();
   coarse_factor_kf_kernel<<<batch, 128, smem, stream>>>(n0, Q, fac, theta, L, status);
+  return cudaGetLastError();
+}
+
+}  // namespace rbws
+
+namespace rbws {
+
+// ---------------------------------------------------------------- stored-coefficient hierarchy
+// (assembled FEM problems): per-term coefficients are mu-independent, the per-instance
+// operator of a level is their theta-weighted sum in term order (reference grid.py:246-255)
+__global__ void __launch_bounds__(256) stored_combine_kernel(int n, int Q,
+                                                             const double* __restrict__ tcoef,
+                                                             const double* __restrict__ theta,
+                                                             double* __restrict__ coef,
+                                                             double* __restrict__ dinv) {
+  const int mu = blockIdx.y;
+  const int64_t n3 = (int64_t)n * n * n;
+  const int64_t X = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (X >= n3) return;
+  const double* th = theta + (int64_t)mu * Q;
+  double* C = coef + (int64_t)mu * 14 * n3;
+  double c0 = 0.0;
+#pragma unroll 2
+  for (int o = 0; o < 14; ++o) {
+    double v = th[0] * __ldg(tcoef + o * n3 + X);
+    for (int q = 1; q < Q; ++q) v = fma(th[q], __ldg(tcoef + ((int64_t)q * 14 + o) * n3 + X), v);
+    C[o * n3 + X] = v;
+    if (o == 0) c0 = v;
+  }
+  const int i = X % n, j = (X / n) % n, k = (int)(X / ((int64_t)n * n));
+  dinv[(int64_t)mu * n3 + X] = (i == 0 || j == 0 || k == 0) ? 0.0 : 1.0 / c0;
+}
+
+cudaError_t stored_combine(int n, int Q, const double* tcoef, const double* theta, int batch,
+                           double* coef, double* dinv, cudaStream_t stream) {
+  const int64_t n3 = (int64_t)n * n * n;
+  dim3 grd((unsigned)((n3 + 255) / 256), batch);
+  count_launch();
+  stored_combine_kernel<<<grd, 256, 0, stream>>>(n, Q, tcoef, theta, coef, dinv);
+  return cudaGetLastError();
+}
+
+__device__ __forceinline__ int fwd_index(int dx, int dy, int dz) {
+  // inverse of fwd_off for a lexicographically positive offset
+  if (dz == 1) return 1 + (dy + 1) * 3 + (dx + 1);
+  if (dy == 1) return 10 + (dx + 1);
+  return 13;
+}
+
+__global__ void coarse_factor_stored_kernel(int n0, int Q, const double* __restrict__ tcoef,
+                                            const double* __restrict__ theta,
+                                            double* __restrict__ Lout, int* __restrict__ status) {
+  extern __shared__ double A[];
+  const int m1 = n0 - 1, m = m1 * m1 * m1;
+  const int64_t n3 = (int64_t)n0 * n0 * n0;
+  const int mu = blockIdx.x;
+  const double* th = theta + (size_t)mu * Q;
+  for (int t = threadIdx.x; t < m * m; t += blockDim.x) {
+    const int r = t / m, cidx = t % m;
+    const int i = r % m1 + 1, j = (r / m1) % m1 + 1, k = r / (m1 * m1) + 1;
+    const int i2 = cidx % m1 + 1, j2 = (cidx / m1) % m1 + 1, k2 = cidx / (m1 * m1) + 1;
+    int ox = i2 - i, oy = j2 - j, oz = k2 - k;
+    double v = 0.0;
+    if (ox >= -1 && ox <= 1 && oy >= -1 && oy <= 1 && oz >= -1 && oz <= 1) {
+      // the coefficient is stored at the row whose offset to the other node is forward
+      int64_t X = i + (int64_t)n0 * (j + (int64_t)n0 * k);
+      int o = 0;
+      if (ox || oy || oz) {
+        const bool fwd = oz > 0 || (oz == 0 && (oy > 0 || (oy == 0 && ox > 0)));
+        if (!fwd) {
+          X = i2 + (int64_t)n0 * (j2 + (int64_t)n0 * k2);
+          ox = -ox; oy = -oy; oz = -oz;
+        }
+        o = fwd_index(ox, oy, oz);
+      }
+      v = th[0] * tcoef[o * n3 + X];
+      for (int q = 1; q < Q; ++q) v = fma(th[q], tcoef[((int64_t)q * 14 + o) * n3 + X], v);
+    }
+    A[t] = v;
+  }
+  __syncthreads();
+  chol_store(A, m, Lout + (int64_t)mu * m * m, status ? status + mu : nullptr);
+}
+
+cudaError_t coarse_factor_stored(int n0, int Q, const double* tcoef, const double* theta,
+                                 int batch, double* L, int* status, cudaStream_t stream) {
+  const int m1 = n0 - 1, m = m1 * m1 * m1;
+  const size_t smem = (size_t)m * m * sizeof(double);
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(coarse_factor_stored_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  count_launch();
+  coarse_factor_stored_kernel<<<batch, 128, smem, stream>>>(n0, Q, tcoef, theta, L, status);
   return cudaGetLastError();
 }
 

@@ -22,6 +22,7 @@ struct CoarseOp {
   // per-instance stored 27-point coefficients [batch][14][n^3] (diagonal, 13 forward
   // offsets; symmetric), or null: matrix-free from the factors
   const double* coef = nullptr;
+  bool coef_shared = false;  // coef is one coefficient set applied to every instance
 };
 
 // mode: 0 apply y=Ax | 1 resid y=b-Ax | 2 jacobi y=x+w(b-Ax)/diag | 4 dinv y=1/diag
@@ -32,6 +33,13 @@ cudaError_t coarse_launch(int mode, const CoarseOp& op, const double* theta, int
 // whose terms fall into more z-groups than the grouped kernel takes
 cudaError_t coarse_build_coef(const CoarseOp& op, const double* theta, int batch, double* coef,
                               double* dinv, cudaStream_t stream);
+// per-instance coefficients coef[mu] = sum_q theta_q tcoef[q] (and 1/diag) of a stored-coefficient
+// level; tcoef = [Q][14][n^3]
+cudaError_t stored_combine(int n, int Q, const double* tcoef, const double* theta, int batch,
+                           double* coef, double* dinv, cudaStream_t stream);
+// coarsest level of a stored-coefficient hierarchy: dense operator + Cholesky per instance
+cudaError_t coarse_factor_stored(int n0, int Q, const double* tcoef, const double* theta,
+                                 int batch, double* L, int* status, cudaStream_t stream);
 constexpr int kCoarseMaxGroups = 4;  // coarse_kron_kernel<G> instantiations
 // coarsest level: dense Galerkin operator from the factors + Cholesky per instance
 cudaError_t coarse_factor_kf(int n0, int Q, const double* fac, const double* theta, int batch,

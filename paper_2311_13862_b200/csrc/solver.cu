@@ -104,6 +104,7 @@ Hierarchy::~Hierarchy() {
   for (int* p : d_zsame) cudaFree(p);
   for (int* p : d_grp) cudaFree(p);
   cudaFree(d_fzsame);
+  for (double* p : d_tcoef) cudaFree(p);
 }
 
 // 1D Galerkin product P^T T P of a tridiagonal interior operator
@@ -267,6 +268,40 @@ int hierarchy_create(Hierarchy** out, int n, int m0, int Q, const double* face,
   return 0;
 }
 
+int hierarchy_create_stored(Hierarchy** out, int n, int m0, int Q, const double* coef) {
+  if (Q < 1) RBWS_FAIL("need at least one affine term");
+  if (m0 < 2) RBWS_FAIL("base grid needs at least 2 cells per dimension");
+  if ((m0 - 1) * (m0 - 1) * (m0 - 1) > 125) RBWS_FAIL("coarsest grid too large (m0 <= 6)");
+  if (n < 2 * m0 || n % m0) RBWS_FAIL("finest grid must be m0 * 2^J cells with J >= 1");
+  {
+    const int r = n / m0;
+    if (r & (r - 1)) RBWS_FAIL("finest grid must be m0 * 2^J cells");
+  }
+  Hierarchy* h = new Hierarchy();
+  h->n = n; h->m0 = m0; h->Q = Q; h->stored = true;
+  for (int c = m0; c <= n; c *= 2) h->cells.push_back(c);
+  h->levels = (int)h->cells.size();
+  const int L = h->levels;
+  h->d_fac.assign(L, nullptr);
+  h->d_zsame.assign(L, nullptr);
+  h->d_grp.assign(L, nullptr);
+  h->G.assign(L, 0);
+  h->h_fac.assign(L, {});
+  h->d_tcoef.assign(L, nullptr);
+  cudaError_t e = cudaSuccess;
+  size_t off = 0;
+  for (int l = 0; l < L && e == cudaSuccess; ++l) {
+    const size_t nl = h->cells[l], cnt = (size_t)Q * 14 * nl * nl * nl;
+    e = dalloc(&h->d_tcoef[l], cnt);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(h->d_tcoef[l], coef + off, sizeof(double) * cnt, cudaMemcpyHostToDevice);
+    off += cnt;
+  }
+  if (e != cudaSuccess) { delete h; RBWS_FAIL(cudaGetErrorString(e)); }
+  *out = h;
+  return 0;
+}
+
 // ------------------------------------------------------------ batch
 
 Batch::~Batch() {
@@ -327,11 +362,12 @@ int batch_create(Batch** out, Hierarchy* h, int cap, int nu, double omega, int m
     zalloc(&lb.t1, V);
     zalloc(&lb.dinv, V);
     if (nu != 1) { zalloc(&lb.t2, V); zalloc(&lb.t3, V); zalloc(&lb.zero, V); }
-    if (l >= 1 && l < L - 1) zalloc(&lb.u, V);
+    if (l >= 1 && (l < L - 1 || h->stored)) zalloc(&lb.u, V);
+    if (e == cudaSuccess && h->stored && l >= 1) e = dalloc(&lb.coef, (size_t)14 * cap * n3);
     // levels whose terms fall into more z-groups than the grouped Kronecker kernel takes:
     // stored per-instance coefficients (without the memory, the matrix-free 27-coefficient
     // kernel runs instead)
-    if (e == cudaSuccess && l >= 1 && l < L - 1 && h->G[l] > kCoarseMaxGroups) {
+    if (e == cudaSuccess && !h->stored && l >= 1 && l < L - 1 && h->G[l] > kCoarseMaxGroups) {
       if (dalloc(&lb.coef, (size_t)14 * cap * n3) != cudaSuccess) {
         (void)cudaGetLastError();
         lb.coef = nullptr;
@@ -425,6 +461,16 @@ int batch_setup(Batch* b, const double* theta, int count, cudaStream_t stream) {
   if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
   const int L = h->levels;
   LaunchCtx lc{stream, nullptr};
+  if (h->stored) {  // assembled problem: per-instance coefficients on every level, dense coarsest
+    for (int l = 1; l < b->maxl && e == cudaSuccess; ++l)
+      e = stored_combine(h->cells[l], h->Q, h->d_tcoef[l], b->theta, count, b->lv[l].coef,
+                         b->lv[l].dinv, stream);
+    if (e == cudaSuccess)
+      e = coarse_factor_stored(h->m0, h->Q, h->d_tcoef[0], b->theta, count, b->L0, b->d_status,
+                               stream);
+    if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+    return 0;
+  }
   // fine level 1/diag (and the stored face weights of the SCW kernels)
   if (b->maxl == L) e = fine_dinv(b->fine_op(), count, h->d_fzsame, b->lv[L - 1].dinv, stream);
   if (e == cudaSuccess && b->wface) e = fine_faces(b->fine_op(), count, b->wface, b->wstride, stream);
@@ -484,7 +530,9 @@ int Batch::vcycle(int lvl, const double* bb, double* out, double* dot_partial,
     if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
     return 0;
   }
-  const bool fine = (lvl == h->levels - 1);
+  const bool fine = h->sep_fine(lvl);
+  // top level of a stored-coefficient hierarchy: coarse-type kernels, the PCG dot separately
+  const bool stop = h->stored && lvl == h->levels - 1;
   LevelBuf& l = lv[lvl];
   LevelBuf& c = lv[lvl - 1];
   const int n = l.n;
@@ -522,14 +570,15 @@ int Batch::vcycle(int lvl, const double* bb, double* out, double* dot_partial,
     if (vcycle(lvl - 1, c.b, c.e, nullptr, lc)) return 1;
     e = prolong_launch(n, count, 0, c.e, out, nullptr, nullptr, 0.0, lc);
     for (int s = 0; s < nu && e == cudaSuccess; ++s) e = gs(false);
-    if (e == cudaSuccess && fine && dot_partial)
+    if (e == cudaSuccess && (fine || stop) && dot_partial)
       e = vec_dot(n, count, bb, n3, out, n3, dot_partial, lc);
     if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
     return 0;
   }
   if (nu == 1) {
     int t0 = pf ? prof_begin(lc.stream) : -1;
-    e = op(MODE_PRE, DOT_NONE, nullptr, bb, l.t1, nullptr);
+    if (stop) e = vec_scale_dinv(n, count, omega, l.dinv, bb, l.u, lc.stream);
+    if (e == cudaSuccess) e = op(MODE_PRE, DOT_NONE, nullptr, bb, l.t1, nullptr);
     if (pf) { prof_end(PROF_FINE_PRE, t0, lc.stream); t0 = prof_begin(lc.stream); }
     // the restriction also writes the next level's pre-scaled rhs u = w D^-1 b
     if (e == cudaSuccess)
@@ -546,6 +595,8 @@ int Batch::vcycle(int lvl, const double* bb, double* out, double* dot_partial,
     } else {
       e = prolong_launch(n, count, 2, c.e, l.t1, l.u, nullptr, omega, lc);
       if (e == cudaSuccess) e = op(MODE_JACOBI, fdot, l.t1, bb, out, dot_partial);
+      if (e == cudaSuccess && stop && dot_partial)
+        e = vec_dot(n, count, bb, (int64_t)n * n * n, out, (int64_t)n * n * n, dot_partial, lc);
     }
     if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
     return 0;
@@ -570,6 +621,8 @@ int Batch::vcycle(int lvl, const double* bb, double* out, double* dot_partial,
     e = op(MODE_JACOBI, last ? fdot : DOT_NONE, u, bb, dst, last ? dot_partial : nullptr);
     u = dst;
   }
+  if (e == cudaSuccess && stop && dot_partial)
+    e = vec_dot(n, count, bb, (int64_t)n * n * n, out, (int64_t)n * n * n, dot_partial, lc);
   if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
   return 0;
 }
@@ -865,6 +918,134 @@ static int pcg_graph_run(Batch* b, const Sep7& op, double* x, int tiles, int vti
   return 0;
 }
 
+// ------------------------------------------------------------ PCG on a stored-coefficient
+// hierarchy (assembled FEM problems): the reference loop (krylov.py:73-101) over generic
+// kernels — 27-point apply, elementwise updates, deterministic per-instance dot partials
+
+__global__ void __launch_bounds__(256) pcg_xpby_kernel(int64_t n3, const double* __restrict__ s,
+                                                       const double* __restrict__ beta,
+                                                       double* __restrict__ p,
+                                                       const int* __restrict__ active) {
+  const int mu = blockIdx.y;
+  if (!active[mu]) return;
+  const int64_t X = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (X >= n3) return;
+  const int64_t o = (int64_t)mu * n3 + X;
+  p[o] = beta ? fma(beta[mu], p[o], s[o]) : s[o];
+}
+
+__global__ void __launch_bounds__(256) pcg_update_kernel(int64_t n3, const double* __restrict__ p,
+                                                         const double* __restrict__ Ap,
+                                                         const double* __restrict__ alpha,
+                                                         double* __restrict__ x,
+                                                         double* __restrict__ r,
+                                                         const int* __restrict__ active) {
+  const int mu = blockIdx.y;
+  if (!active[mu]) return;
+  const int64_t X = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (X >= n3) return;
+  const int64_t o = (int64_t)mu * n3 + X;
+  const double a = alpha[mu];
+  x[o] = fma(a, p[o], x[o]);
+  r[o] = fma(-a, Ap[o], r[o]);
+}
+
+static int pcg_solve_stored(Batch* b, const double* f, int64_t f_stride, double* x, double delta,
+                            int l_max, const PcgOut& out, cudaStream_t stream) {
+  Hierarchy* h = b->h;
+  const int count = b->count, n = h->n, L = h->levels;
+  const int64_t n3 = (int64_t)n * n * n;
+  if (f_stride == 0 && count > 1)
+    RBWS_FAIL("stored-coefficient problems take one rhs per instance (f_stride = n^3)");
+  const int hl = b->hist_len;
+  const int tiles = vec_tiles(n);
+  const CoarseOp op = b->cop(L - 1);
+  LaunchCtx all{stream, nullptr};
+  LaunchCtx act{stream, b->active};
+  const dim3 vg((unsigned)((n3 + 255) / 256), count);
+  cudaError_t e = vec_dot(n, count, f, n3, f, n3, b->partial2, all);
+  if (e == cudaSuccess) e = coarse_launch(1, op, b->theta, count, x, f, b->r, 0.0, all);
+  if (e == cudaSuccess) e = vec_dot(n, count, b->r, n3, b->r, n3, b->partial, all);
+  if (e == cudaSuccess) e = cudaMemsetAsync(b->nactive, 0, sizeof(int), stream);
+  if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+  count_launch();
+  pcg_init_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial2, tiles, 0, b->partial,
+                                                        tiles, delta, l_max, b->scale, b->hist,
+                                                        hl, b->active, b->iters, b->pstatus,
+                                                        b->nactive);
+  e = fetch_to_host(b->h_nactive, b->nactive, sizeof(int), stream);
+  if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+  b->cur_active = *b->h_nactive;
+  int dl_call = 0;
+  if (out.x_host) {
+    b->h_active.assign(count, 1);
+    b->h_sent.assign(count, 0);
+    if (stream_download(b, x, out, dl_call++, false, stream)) return 1;
+  }
+  if (*b->h_nactive > 0) {
+    if (b->vcycle(L - 1, b->r, b->s, b->partial, act)) return 1;
+    count_launch();
+    pcg_rs_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, tiles, b->rs, b->active);
+    const double* beta = nullptr;
+    for (int k = 0; k < l_max; ++k) {
+      count_launch();
+      pcg_xpby_kernel<<<vg, 256, 0, stream>>>(n3, b->s, beta, b->p, b->active);
+      e = coarse_launch(0, op, b->theta, count, b->p, nullptr, b->t_res, 0.0, act);
+      if (e == cudaSuccess) e = vec_dot(n, count, b->p, n3, b->t_res, n3, b->partial, act);
+      if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+      count_launch();
+      pcg_alpha_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, tiles, b->rs,
+                                                             b->alpha, b->active, b->pstatus);
+      count_launch();
+      pcg_update_kernel<<<vg, 256, 0, stream>>>(n3, b->p, b->t_res, b->alpha, x, b->r, b->active);
+      e = vec_dot(n, count, b->r, n3, b->r, n3, b->partial, act);
+      if (e == cudaSuccess) e = cudaMemsetAsync(b->nactive, 0, sizeof(int), stream);
+      if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+      count_launch();
+      pcg_check_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, tiles, b->scale,
+                                                             delta, l_max, b->hist, hl, b->active,
+                                                             b->iters, b->nactive);
+      e = fetch_to_host(b->h_nactive, b->nactive, sizeof(int), stream);
+      if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+      if (*b->h_nactive == 0) break;
+      if (out.x_host && *b->h_nactive < b->cur_active &&
+          stream_download(b, x, out, dl_call++, false, stream))
+        return 1;
+      b->cur_active = *b->h_nactive;
+      if (b->vcycle(L - 1, b->r, b->s, b->partial, act)) return 1;
+      count_launch();
+      pcg_beta_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, tiles, b->rs,
+                                                            b->beta, b->active);
+      beta = b->beta;
+    }
+  }
+  if (out.x_host && stream_download(b, x, out, dl_call++, true, stream)) return 1;
+  e = coarse_launch(1, op, b->theta, count, x, f, b->t_res, 0.0, all);
+  if (e == cudaSuccess) e = vec_dot(n, count, b->t_res, n3, b->t_res, n3, b->partial, all);
+  if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+  double* d_true = b->beta;
+  count_launch();
+  pcg_true_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, tiles, b->scale, d_true);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+  std::vector<double> hh((size_t)count * hl);
+  e = fetch_to_host(hh.data(), b->hist, sizeof(double) * count * hl, stream);
+  if (e == cudaSuccess && out.iters) e = fetch_to_host(out.iters, b->iters, sizeof(int) * count, stream);
+  if (e == cudaSuccess && out.true_res)
+    e = fetch_to_host(out.true_res, d_true, sizeof(double) * count, stream);
+  if (e == cudaSuccess && out.status)
+    e = fetch_to_host(out.status, b->pstatus, sizeof(int) * count, stream);
+  if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+  const int hist_len = l_max + 1;
+  if (out.hist)
+    for (int m = 0; m < count; ++m)
+      memcpy(out.hist + (size_t)m * hist_len, hh.data() + (size_t)m * hl, sizeof(double) * hist_len);
+  if (out.status && out.true_res)
+    for (int m = 0; m < count; ++m)
+      if (!(out.status[m] & 1) && !(out.true_res[m] <= delta)) out.status[m] |= 2;
+  return 0;
+}
+
 int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double delta, int l_max,
               const PcgOut& out, cudaStream_t stream) {
   if (!(delta > 0)) RBWS_FAIL("tolerance must be positive");
@@ -884,6 +1065,7 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
     b->hist_len = hist_len;
   }
   const int hl = b->hist_len;
+  if (h->stored) return pcg_solve_stored(b, f, f_stride, x, delta, l_max, out, stream);
   const Sep7 op = b->fine_op();
   bool graph_ran = false;
   const int tiles = fine_geom(n, count).tiles;

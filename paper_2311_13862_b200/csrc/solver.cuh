@@ -28,8 +28,15 @@ struct Hierarchy {
   std::vector<int*> d_grp;          // per level [3Q]: z-group of every term
   std::vector<int> G;               // per level: number of z-groups
   std::vector<std::vector<double>> h_fac;
+  // stored-coefficient hierarchy (assembled FEM problems, rbws_hierarchy_create_stored): every
+  // level's operator is sum_q theta_q C_q with per-term symmetric 27-point coefficients
+  // d_tcoef[l] = [Q][14][n_l^3] (padded layout, zero on ghosts); no Kronecker factors
+  bool stored = false;
+  std::vector<double*> d_tcoef;
 
   ~Hierarchy();
+  // the finest level runs the separable 7-point kernels (fine.cu)
+  bool sep_fine(int l) const { return !stored && l == levels - 1; }
   CoarseOp coarse_op(int l) const {
     CoarseOp o;
     o.n = cells[l]; o.Q = Q; o.G = G[l];
@@ -42,6 +49,8 @@ int kron_factors(int n, int m0, int Q, const double* face, const double* node,
                  std::vector<int>& cells, std::vector<std::vector<double>>& fac);
 int hierarchy_create(Hierarchy** out, int n, int m0, int Q, const double* face,
                      const double* node);
+// coef: host, levels 0..L-1 concatenated, level l = [Q][14][n_l^3] (n_l = m0 2^l)
+int hierarchy_create_stored(Hierarchy** out, int n, int m0, int Q, const double* coef);
 
 struct LevelBuf {
   int n = 0;

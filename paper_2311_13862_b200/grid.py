@@ -66,6 +66,12 @@ class ParametricProblem:
     ``m0 * 2**i`` cells.  Immutable after construction.
     """
 
+    def __new__(cls, spec, levels: int = 3, m0: int = 2):
+        if getattr(spec, "kind", None) == "fem":  # assembled problems (fem.py)
+            from .fem import FemProblem
+            return FemProblem(spec, levels, m0)
+        return super().__new__(cls)
+
     def __init__(self, spec: ProblemSpec, levels: int = 3, m0: int = 2):
         if levels < 2:
             raise ValueError("need at least 2 levels for coarse-grid correction")

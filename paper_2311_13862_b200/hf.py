@@ -32,7 +32,7 @@ class HighFidelitySolver:
         mus = self.problem.spec.check_mus(mus)
         self._ctx = mg_context_for(self.problem, mus, nu=self.nu, smoother=self.smoother,
                                    ctx=self._ctx)
-        f = self.problem.rhs() if rhs is None else rhs
+        f = self.problem.rhs(mus) if rhs is None else rhs
         x, reps = mgcg_solve(None, f, None, self._ctx, delta=self.delta, l_max=self.l_max)
         self.last_reports = reps
         return x

@@ -131,7 +131,7 @@ def mgcg_solve(A, f, x0, ctx: MgContext, delta: float = 1e-16, l_max: int = 40, 
     prob = ctx.problem
     n, count = prob.n, ctx.count
     if f is None:
-        f = prob.rhs()
+        f = prob.rhs(ctx.mus)
     nb = padded_len(n, count)
     if f.numel() == padded_len(n, 1) and count > 1:
         f_stride = 0

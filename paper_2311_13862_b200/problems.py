@@ -146,7 +146,19 @@ _REGISTRY = {
 }
 
 
-def get_problem(pid: str) -> ProblemSpec:
+def _fem(name):
+    def make():
+        from . import fem
+        return getattr(fem, name)()
+    return make
+
+
+# the reference's own assembled (Q1 FEM) problems, problems.py:96-155
+_REGISTRY["example-1"] = _fem("example1")
+_REGISTRY["example-2"] = _fem("example2")
+
+
+def get_problem(pid: str):
     """Registry lookup (reference problems.py:158-162)."""
     try:
         return _REGISTRY[pid]()

@@ -5,6 +5,7 @@ Run in the build container (needs /root/reference; never on the GPU box):
     python tests/golden/make_golden.py          # golden_fd.npz
     python tests/golden/make_golden.py --gs     # golden_gs.npz (Gauss-Seidel smoother)
     python tests/golden/make_golden.py --msrb   # golden_msrb.npz (rbi-msrbcg)
+    python tests/golden/make_golden.py --fem    # golden_fem.npz (example-1, unmodified reference)
 
 The reference (``/root/reference/pkg``) is copied to /tmp and its Cython
 smoother extension built in place (reference setup.py), so the reference's
@@ -281,7 +282,85 @@ def main_msrb():
     print(f"wrote {dest} ({dest.stat().st_size/1e6:.2f} MB, {len(out)} arrays)")
 
 
+def main_fem():
+    """The reference's own assembled problem example-1 (Q1 FEM, Dirichlet, p = 2) through
+    its unmodified API -> tests/golden/golden_fem.npz: per-level operators (CSR) and
+    right-hand sides, a V-cycle, zero-init MGCG and L1ROC RBI-MGCG solves."""
+    rbws = _import_reference()
+    from rbws.grid import ParametricProblem
+    from rbws.hf import HighFidelitySolver
+    from rbws.multigrid import mg_context_for, mg_vcycle, mgcg_solve
+    from rbws.problems import get_problem
+    from rbws.rb import l1roc_offline
+    from rbws.sampling import lhs_sample
+    from rbws.warmstart import MethodConfig, rbi_pcg_solve
+
+    out = {}
+    spec = get_problem("example-1")
+    rng = np.random.default_rng(5)
+    mus = np.array([[0.3, 0.25], [1.7, 0.8], [1.0, 0.5], [0.05, 0.95]])
+    for tag, levels, m0 in (("n16m4", 3, 4), ("n16m2", 4, 2), ("n32m4", 4, 4)):
+        p = ParametricProblem(spec, levels=levels, m0=m0)
+        k = f"fem_{tag}"
+        out[f"{k}_mus"] = mus
+        mu = mus[0]
+        for lvl in range(p.mesh.levels):
+            A = p.operator(mu, level=lvl).tocsr()
+            if tag == "n32m4" and lvl == p.mesh.levels - 1:
+                v = rng.standard_normal(A.shape[0])
+                out[f"{k}_op{lvl}_v"] = v
+                out[f"{k}_op{lvl}_Av"] = A @ v
+                continue
+            A.sort_indices()
+            out[f"{k}_op{lvl}_data"] = A.data
+            out[f"{k}_op{lvl}_indices"] = A.indices.astype(np.int64)
+            out[f"{k}_op{lvl}_indptr"] = A.indptr.astype(np.int64)
+        out[f"{k}_rhs"] = np.array([p.rhs(m) for m in mus])
+        ctx = mg_context_for(p, mu)
+        b = rng.standard_normal(p.n_free)
+        out[f"{k}_vcyc_b"] = b
+        out[f"{k}_vcyc"] = mg_vcycle(b, ctx)
+        xs, its, hists = [], [], []
+        for m in mus:
+            A, f = p.operator(m), p.rhs(m)
+            x, rep = mgcg_solve(A, f, np.zeros_like(f), mg_context_for(p, m), delta=1e-10,
+                                l_max=60)
+            xs.append(x)
+            its.append(rep.iterations)
+            hists.append(np.pad(rep.history, (0, 61 - len(rep.history)), constant_values=np.nan))
+        out[f"{k}_mgcg_x"] = np.array(xs)
+        out[f"{k}_mgcg_iters"] = np.array(its)
+        out[f"{k}_mgcg_hist"] = np.array(hists)
+        if tag != "n16m4":
+            continue
+        # L1ROC greedy (reference default LU high fidelity) + RBI-MGCG warm-started solves
+        train = np.array(lhs_sample(spec.p, 24, spec.bounds, seed=3))
+        model = l1roc_offline(list(train), 6, HighFidelitySolver(p), p.operator,
+                              p.operator_rows, p.rhs, seed=0)
+        out[f"{k}_l1_train"] = train
+        out[f"{k}_l1_basis"] = model.basis
+        out[f"{k}_l1_transform"] = model.transform
+        out[f"{k}_l1_colloc"] = model.collocation
+        out[f"{k}_l1_chosen"] = model.chosen_mus
+        out[f"{k}_l1_hist"] = model.indicator_history
+        xs, its = [], []
+        for m in mus:
+            A, f = p.operator(m), p.rhs(m)
+            cfg = MethodConfig("rbi-mgcg", delta=1e-10, l_max=60, N=model.dim)
+            x, rep = rbi_pcg_solve(A, f, cfg, mg_ctx=mg_context_for(p, m), l1roc_model=model)
+            xs.append(x)
+            its.append(rep.iterations)
+        out[f"{k}_rbi_x"] = np.array(xs)
+        out[f"{k}_rbi_iters"] = np.array(its)
+    dest = REPO / "tests/golden/golden_fem.npz"
+    np.savez_compressed(dest, **out)
+    print(f"wrote {dest} ({dest.stat().st_size/1e6:.2f} MB, {len(out)} arrays)")
+
+
 if __name__ == "__main__":
+    if "--fem" in sys.argv:
+        main_fem()
+        sys.exit(0)
     if "--msrb" in sys.argv:
         main_msrb()
         sys.exit(0)

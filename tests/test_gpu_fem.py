@@ -1,0 +1,130 @@
+"""The reference's own assembled problem example-1 (Q1 FEM, mu-dependent Dirichlet data)
+on the CUDA path (stored-coefficient hierarchy, through the C ABI) vs the unmodified
+reference's goldens (tests/golden/golden_fem.npz) and the oracle."""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+G = np.load(Path(__file__).parent / "golden" / "golden_fem.npz")
+CASES = (("n16m4", 3, 4), ("n16m2", 4, 2), ("n32m4", 4, 4))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import build
+    build.build(verbose=False)
+
+
+def _pkg():
+    import paper_2311_13862_b200 as pkg
+    return pkg
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def _golden_op(k, lvl):
+    ip = G[f"{k}_op{lvl}_indptr"]
+    return sp.csr_matrix((G[f"{k}_op{lvl}_data"], G[f"{k}_op{lvl}_indices"], ip),
+                         shape=(len(ip) - 1,) * 2)
+
+
+@pytest.fixture(scope="module")
+def probs():
+    pkg = _pkg()
+    spec = pkg.get_problem("example-1")
+    return {t: pkg.ParametricProblem(spec, levels=l, m0=m) for t, l, m in CASES}
+
+
+@pytest.mark.parametrize("tag,levels,m0", CASES)
+def test_fem_operators_rhs_vcycle(probs, tag, levels, m0):
+    pkg = _pkg()
+    p, k = probs[tag], f"fem_{tag}"
+    assert type(p).__name__ == "FemProblem"
+    mus = G[f"{k}_mus"]
+    ctx = pkg.mg_context_for(p, mus)
+    A = pkg.BatchOperator(ctx)
+    rng = np.random.default_rng(1)
+    for lvl in range(levels):
+        n = p.cells[lvl]
+        v = rng.standard_normal((len(mus), (n - 1) ** 3))
+        y = pkg.from_padded(A.apply(pkg.to_padded(v, n), level=lvl), n, len(mus))
+        if f"{k}_op{lvl}_data" in G:
+            ref = _golden_op(k, lvl) @ v[0]
+            assert _rel(y[0], ref) <= 1e-13, lvl
+        else:
+            vb = _pad_batch(pkg, G[f"{k}_op{lvl}_v"], n, len(mus))
+            y0 = pkg.from_padded(A.apply(vb, level=lvl), n, len(mus))
+            assert _rel(y0[0], G[f"{k}_op{lvl}_Av"]) <= 1e-13
+        # every instance against its own host operator
+        for m in range(len(mus)):
+            assert _rel(y[m], p.operator_host(mus[m], lvl) @ v[m]) <= 1e-13
+    f = pkg.from_padded(p.rhs(mus), p.n, len(mus))
+    assert _rel(f, G[f"{k}_rhs"]) <= 1e-13
+    # one V-cycle (instance 0 = the golden's mu)
+    b = np.tile(G[f"{k}_vcyc_b"], (len(mus), 1))
+    out = pkg.from_padded(pkg.mg_vcycle(pkg.to_padded(b, p.n), ctx), p.n, len(mus))
+    assert _rel(out[0], G[f"{k}_vcyc"]) <= 1e-12
+
+
+def _pad_batch(pkg, v, n, count):
+    return pkg.to_padded(np.tile(v, (count, 1)), n)
+
+
+@pytest.mark.parametrize("tag,levels,m0", CASES)
+def test_fem_mgcg_matches_reference(probs, tag, levels, m0):
+    """Zero-init MGCG to 1e-10: solutions within 1e-8 relative L2 and iteration counts
+    within +-1 of the reference (north_star tolerance)."""
+    pkg = _pkg()
+    p, k = probs[tag], f"fem_{tag}"
+    mus = G[f"{k}_mus"]
+    ctx = pkg.mg_context_for(p, mus)
+    x, reps = pkg.mgcg_solve(None, None, None, ctx, delta=1e-10, l_max=60)
+    got = pkg.from_padded(x, p.n, len(mus))
+    for m in range(len(mus)):
+        assert _rel(got[m], G[f"{k}_mgcg_x"][m]) <= 1e-8
+        assert abs(reps[m].iterations - G[f"{k}_mgcg_iters"][m]) <= 1
+        assert reps[m].converged
+        hist = G[f"{k}_mgcg_hist"][m][: reps[m].iterations + 1]
+        assert np.allclose(reps[m].history[: len(hist)], hist, rtol=1e-6)
+
+
+def test_fem_term_apply_and_streaming(probs):
+    pkg = _pkg()
+    p = probs["n16m4"]
+    mus = G["fem_n16m4_mus"]
+    n = p.n
+    rng = np.random.default_rng(2)
+    v = rng.standard_normal((3, (n - 1) ** 3))
+    for q in range(p.spec.n_terms):
+        y = pkg.from_padded(p.term_apply(q, pkg.to_padded(v, n), 3), n, 3)
+        T = p.terms_by_level[-1][q]
+        for m in range(3):
+            assert _rel(y[m], T @ v[m]) <= 1e-13
+    # streaming download of converged instances == device solutions (bitwise)
+    ctx = pkg.mg_context_for(p, mus)
+    x, _ = pkg.mgcg_solve(None, None, None, ctx, delta=1e-10, l_max=60)
+    host = torch.zeros(len(mus) * n ** 3, dtype=torch.float64).pin_memory()
+    cs = torch.cuda.Stream()
+    x2, _ = pkg.mgcg_solve(None, None, None, ctx, delta=1e-10, l_max=60, out_host=host,
+                           copy_stream=cs)
+    cs.synchronize()
+    torch.cuda.synchronize()
+    assert torch.equal(host, x[: len(mus) * n ** 3].cpu())
+    assert torch.equal(x2, x)
+
+
+def test_fem_example2_is_refused():
+    pkg = _pkg()
+    with pytest.raises(NotImplementedError):
+        pkg.ParametricProblem(pkg.get_problem("example-2"), levels=3, m0=2)
