@@ -363,7 +363,7 @@ int batch_create(Batch** out, Hierarchy* h, int cap, int nu, double omega, int m
     zalloc(&lb.dinv, V);
     if (nu != 1) { zalloc(&lb.t2, V); zalloc(&lb.t3, V); zalloc(&lb.zero, V); }
     if (l >= 1 && (l < L - 1 || h->stored)) zalloc(&lb.u, V);
-    if (e == cudaSuccess && h->stored && l >= 1) e = dalloc(&lb.coef, (size_t)14 * cap * n3);
+    if (e == cudaSuccess && h->stored) e = dalloc(&lb.coef, (size_t)14 * cap * n3);
     // levels whose terms fall into more z-groups than the grouped Kronecker kernel takes:
     // stored per-instance coefficients (without the memory, the matrix-free 27-coefficient
     // kernel runs instead)
@@ -462,7 +462,7 @@ int batch_setup(Batch* b, const double* theta, int count, cudaStream_t stream) {
   const int L = h->levels;
   LaunchCtx lc{stream, nullptr};
   if (h->stored) {  // assembled problem: per-instance coefficients on every level, dense coarsest
-    for (int l = 1; l < b->maxl && e == cudaSuccess; ++l)
+    for (int l = 0; l < b->maxl && e == cudaSuccess; ++l)
       e = stored_combine(h->cells[l], h->Q, h->d_tcoef[l], b->theta, count, b->lv[l].coef,
                          b->lv[l].dinv, stream);
     if (e == cudaSuccess)
