@@ -347,6 +347,8 @@ class FemProblem:
     (grid.py:193-290): same constructor, per-term assembly + termwise Galerkin coarsening
     once, operators and right-hand sides per parameter batch on the device."""
 
+    stored = True  # stored-coefficient hierarchy: mu-dependent rhs, term products by apply
+
     def __init__(self, spec: FemProblemSpec, levels: int = 3, m0: int = 2):
         if levels < 2:
             raise ValueError("need at least 2 levels for coarse-grid correction")

@@ -92,9 +92,16 @@ class L1rocModel:
         rows = torch.as_tensor(interior_to_padded_index(self.collocation, n), device="cuda")
         M = len(self.collocation)
         Q = problem.spec.n_terms
-        Bq = torch.zeros(Q * M * N, dtype=torch.float64, device="cuda")
-        _native.call("rbws_l1roc_project", problem.handle, self.basis.data_ptr(), n ** 3, N,
-                     rows.data_ptr(), M, Bq.data_ptr(), _native.stream_ptr())
+        if getattr(problem, "stored", False):
+            # assembled problems: per-term products A_q W from the stored coefficients,
+            # then the collocation rows (the affine pieces of rb.py:200-201)
+            n3 = n ** 3
+            Bq = torch.stack([problem.term_apply(q, self.basis, N)[: N * n3].view(N, n3)[:, rows].T
+                              for q in range(Q)]).contiguous().view(-1)
+        else:
+            Bq = torch.zeros(Q * M * N, dtype=torch.float64, device="cuda")
+            _native.call("rbws_l1roc_project", problem.handle, self.basis.data_ptr(), n ** 3, N,
+                         rows.data_ptr(), M, Bq.data_ptr(), _native.stream_ptr())
         T = torch.as_tensor(self.transform, dtype=torch.float64, device="cuda").contiguous()
         self._cache[key] = (rows, Bq, T)
         return self._cache[key]
@@ -109,7 +116,7 @@ def _online_batch(model: L1rocModel, problem, theta, f, count):
         bs = f[rows].contiguous()
         bstride = 0
     else:
-        bs = torch.stack([f[m * n ** 3 + rows] for m in range(count)]).contiguous()
+        bs = f[: count * n ** 3].view(count, n ** 3)[:, rows].contiguous()
         bstride = M
     a = torch.empty(count * N, dtype=torch.float64, device="cuda")
     c = torch.empty(count * N, dtype=torch.float64, device="cuda")
@@ -220,7 +227,10 @@ def l1roc_offline(mus, N: int, hf_solve, problem: ParametricProblem, seed: int =
     n = problem.n
     n3 = n ** 3
     first = int(np.random.default_rng(seed).integers(n_train))
-    f = problem.rhs()
+    # one rhs for every training parameter (assembled problems: mu-dependent data) or a
+    # shared one
+    stored = getattr(problem, "stored", False)
+    f = problem.rhs(mus) if stored else problem.rhs()
     theta_train = problem.thetas(mus).contiguous()
     W = torch.zeros(padded_len(n, N), dtype=torch.float64, device="cuda")
     R = torch.zeros(padded_len(n, max(N - 1, 1)), dtype=torch.float64, device="cuda")
@@ -273,7 +283,8 @@ def l1roc_offline(mus, N: int, hf_solve, problem: ParametricProblem, seed: int =
         Au = torch.zeros_like(upick)
         _native.call("rbws_apply", ctx1.handle, problem.finest_level, upick.data_ptr(),
                      Au.data_ptr(), _native.stream_ptr())
-        r = f - Au
+        fp = f[pick * n3:(pick + 1) * n3 + 2 * n * n] if stored else f
+        r = fp - Au
         rstep = deim_extend(n, R if xr else None, xr, r, exclude=taken)
         R[len(xr) * n3:(len(xr) + 1) * n3] = rstep.column[:n3]
         xr.append(rstep.index)

@@ -29,6 +29,19 @@ def _pkg():
     return pkg
 
 
+def canonical_points(idx, n):
+    """example-1 is invariant under the y<->z swap and the point inversion through the cube
+    centre, so DEIM's |residual| maxima tie across each orbit and which member a solver
+    picks depends on the last bit of its arithmetic.  Map interior indices to the orbit's
+    smallest member (a tie-invariant view of the collocation set)."""
+    m = n - 1
+    idx = np.asarray(idx, dtype=np.int64)
+    i, j, k = idx % m, (idx // m) % m, idx // (m * m)
+    orbit = [(i, j, k), (i, k, j), (m - 1 - i, m - 1 - j, m - 1 - k),
+             (m - 1 - i, m - 1 - k, m - 1 - j)]
+    return np.sort(np.min([a + m * (b + m * c) for a, b, c in orbit], axis=0))
+
+
 def _rel(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
 
@@ -128,3 +141,31 @@ def test_fem_example2_is_refused():
     pkg = _pkg()
     with pytest.raises(NotImplementedError):
         pkg.ParametricProblem(pkg.get_problem("example-2"), levels=3, m0=2)
+
+
+def test_fem_l1roc_rbi_mgcg_matches_reference(probs):
+    """Greedy L1ROC on the device (MGCG high fidelity at 1e-14, the reference ran LU) and
+    RBI-MGCG on example-1 vs the unmodified reference: same chosen parameters, indicator
+    history and collocation orbits (ties across the problem's symmetry, canonical_points),
+    same basis span, warm-started solutions 1e-8 and iterations +-1."""
+    pkg = _pkg()
+    p, k = probs["n16m4"], "fem_n16m4"
+    train = G[f"{k}_l1_train"]
+    model = pkg.l1roc_offline(train, 6, pkg.HighFidelitySolver(p), p, seed=0)
+    assert np.array_equal(canonical_points(model.collocation, p.n),
+                          canonical_points(G[f"{k}_l1_colloc"], p.n))
+    assert np.allclose(model.chosen_mus, G[f"{k}_l1_chosen"])
+    assert np.allclose(model.indicator_history, G[f"{k}_l1_hist"], rtol=1e-6)
+    W = model.basis_numpy()
+    Wr = G[f"{k}_l1_basis"]
+    proj = W @ np.linalg.lstsq(W, Wr, rcond=None)[0]
+    assert np.linalg.norm(proj - Wr) <= 1e-8 * np.linalg.norm(Wr)
+    mus = G[f"{k}_mus"]
+    ctx = pkg.mg_context_for(p, mus)
+    cfg = pkg.MethodConfig("rbi-mgcg", delta=1e-10, l_max=60, N=model.dim)
+    x, reps = pkg.rbi_pcg_solve(pkg.BatchOperator(ctx), p.rhs(mus), cfg, mg_ctx=ctx,
+                                l1roc_model=model)
+    got = pkg.from_padded(x, p.n, len(mus))
+    for m in range(len(mus)):
+        assert _rel(got[m], G[f"{k}_rbi_x"][m]) <= 1e-8
+        assert abs(reps[m].iterations - G[f"{k}_rbi_iters"][m]) <= 1
