@@ -576,6 +576,175 @@ def cpu_baseline(cfg, model, test, gpu_iters, budget_s=15.0):
                       f"{match}/{done}"}
 
 
+# ---------------------------------------------------------------- assembled (FEM) problems
+
+FEM_WORKLOAD = ("example-1 (the reference's own Q1 FEM problem: oscillatory coefficient, "
+                "mu-dependent Dirichlet data), {n}^3 cells, m0=4, r={r} from {t} LHS train, "
+                "batch {b}, tol 1e-10")
+
+
+def run_fem(args, rank, world, dist):
+    """`--problem example-1`: RBI-MGCG on the reference's own assembled problem (stored
+    27-point coefficients on every level).  Step = mg_context_for + L1ROC warm start + MGCG
+    for the batch with the right-hand sides already assembled (the reference's t_on
+    protocol excludes operator and rhs assembly, experiment.py:31-33)."""
+    import torch
+
+    import build as _build
+    if rank == 0:
+        _build.build(verbose=False)
+    if dist is not None:
+        dist.barrier()
+    import paper_2311_13862_b200 as rb
+    from paper_2311_13862_b200 import _native
+
+    n, m0, r, n_train = args.fem_n, 4, args.fem_r, args.fem_train
+    batch = args.batch or 256
+    delta = 1e-10
+    spec = rb.get_problem(args.problem)
+    levels = rb.problems.levels_for(n, m0)
+    t0 = time.perf_counter()
+    prob = rb.ParametricProblem(spec, levels=levels, m0=m0)
+    t_setup = time.perf_counter() - t0
+    train = np.array(rb.problems.lhs_sample(spec.p, n_train, spec.bounds, seed=1000))
+    test = np.array(rb.problems.lhs_sample(spec.p, batch, spec.bounds, seed=2000 + rank))
+    t0 = time.perf_counter()
+    model = rb.l1roc_offline(train, r, rb.HighFidelitySolver(prob, delta=1e-14, l_max=100),
+                             prob, seed=0, on_degenerate="stop")
+    torch.cuda.synchronize()
+    t_off = time.perf_counter() - t0
+    F = prob.rhs(test)
+    ctx = rb.MgContext(prob, batch)
+    method = rb.MethodConfig("rbi-mgcg", delta=delta, l_max=L_MAX, N=model.dim)
+    xbuf = torch.empty(rb.padded_len(n, batch), dtype=torch.float64, device="cuda")
+    state = {}
+
+    def step(f):
+        rb.mg_context_for(prob, test, ctx=ctx)
+        x, reps = rb.rbi_pcg_solve(rb.BatchOperator(ctx), f, method, mg_ctx=ctx,
+                                   l1roc_model=model, x0_out=xbuf)
+        state["reps"] = reps
+        return x
+
+    for _ in range(args.warmup):
+        step(F)
+    torch.cuda.synchronize()
+    _, zreps = rb.mgcg_solve(None, F, None, ctx, delta=delta, l_max=L_MAX)
+    zero_iters = float(np.mean([z.iterations for z in zreps]))
+    stream = torch.cuda.current_stream()
+    lc0 = _native.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step(F)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = _native.launch_count() - lc0
+    ms = ev0.elapsed_time(ev1)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = world * batch * args.steps / (ms_max / 1e3)
+    reps = state["reps"]
+    iters = [q.iterations for q in reps]
+
+    # e2e: rhs batch from pinned host memory, solutions back to pinned host memory
+    fh = F.cpu().pin_memory()
+    xh = torch.empty(batch * n ** 3, dtype=torch.float64, pin_memory=True)
+    fd = torch.empty_like(F)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        fd.copy_(fh, non_blocking=True)
+        x = step(fd)
+        xh.copy_(x[: batch * n ** 3], non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = world * batch * args.steps / (float(e2e_ms.item()) / 1e3)
+
+    # roofline: the finest-level stored 27-point apply over the batch, timed alone
+    peak, peak_kind = peaks()
+    A = rb.BatchOperator(ctx)
+    xv = torch.randn(rb.padded_len(n, batch), dtype=torch.float64, device="cuda")
+    A.apply(xv)
+    reps_k = 20
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0.record(stream)
+    for _ in range(reps_k):
+        A.apply(xv)
+    k1.record(stream)
+    torch.cuda.synchronize()
+    k_ms = k0.elapsed_time(k1) / reps_k
+    bpn = float(getattr(prob, "apply_bytes_per_node", 128.0))
+    kbytes = bpn * (n - 1) ** 3 * batch
+    achieved = kbytes / (k_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "stored27_apply (finest level, batch)",
+                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_kind,
+                "bytes_per_launch": int(kbytes), "bytes_per_node": bpn,
+                "ms_per_launch": round(k_ms, 4)}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = fem_cpu_baseline(spec, n, m0, model, test, iters, budget_s=args.cpu_budget)
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "solves/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded LHS parameters, sampling.py:8-27; no dataset)",
+        "config": {"workload": FEM_WORKLOAD.format(n=n, r=r, t=n_train, b=batch),
+                   "batch_per_gpu": batch, "grid_cells": n, "levels": levels,
+                   "rb_dim": model.dim, "n_train": n_train, "tolerance": delta,
+                   "smoother": "jacobi(0.7), nu=1", "parallelism": f"parameter-sharded x{world}",
+                   "mean_iterations_warm": round(float(np.mean(iters)), 3),
+                   "max_iterations_warm": int(max(iters)),
+                   "mean_iterations_zero_init": round(zero_iters, 3),
+                   "all_converged": all(q.converged for q in reps),
+                   "t_setup_s": round(t_setup, 2), "t_offline_s": round(t_off, 2),
+                   "l2": "inputs larger than L2"},
+        "e2e": {"value": round(e2e_value, 2), "unit": "solves/s",
+                "h2d_bytes_per_step": int(F.numel() * 8),
+                "d2h_bytes_per_step": int(batch * n ** 3 * 8),
+                "api": "assembled rhs (pinned host) -> rbi_pcg_solve -> pinned host solutions"},
+        "gpu_launches": int(launches), "roofline": roofline, "clocks": clocks.summary(),
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def fem_cpu_baseline(spec, n, m0, model, test, gpu_iters, budget_s=15.0):
+    """Oracle RBI-MGCG on example-1 (single core) on a bounded sample."""
+    _single_thread_blas()
+    from oracle import fem as of
+    from oracle import solvers as so
+    t0 = time.perf_counter()
+    oprob = of.OracleFemProblem(of.Example1(), levels=int(np.log2(n // m0)) + 1, m0=m0)
+    t_build = time.perf_counter() - t0
+    omodel = so.OracleL1rocModel(model.basis_numpy(), model.transform, model.collocation,
+                                 model.solution_points, model.residual_points,
+                                 np.asarray(model.chosen if model.chosen is not None else []),
+                                 model.indicator_history, model.saturated)
+    done, match, t_solve = 0, 0, 0.0
+    for m, mu in enumerate(test):
+        t1 = time.perf_counter()
+        _, rep = so.rbi_mgcg_solve(oprob, mu, omodel, delta=1e-10, l_max=L_MAX)
+        t_solve += time.perf_counter() - t1
+        done += 1
+        match += int(abs(rep.iterations - gpu_iters[m]) <= 1)
+        if t_solve > budget_s:
+            break
+    return {"value": round(done / t_solve, 4), "unit": "solves/s", "cores": 1, "kind": "port",
+            "sample": f"{done} of the step's test parameters, oracle RBI-MGCG single-threaded; "
+                      f"assembly {t_build:.1f}s excluded; iterations within +-1 of the GPU: "
+                      f"{match}/{done}"}
+
+
 # ---------------------------------------------------------------- reference arm
 
 _W = {}
@@ -726,6 +895,11 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-per-core", type=int, default=2)
+    ap.add_argument("--problem", default="",
+                    help="reference problem id (example-1): RBI-MGCG on its assembled operator")
+    ap.add_argument("--fem-n", type=int, default=64)
+    ap.add_argument("--fem-r", type=int, default=10)
+    ap.add_argument("--fem-train", type=int, default=256)
     ap.add_argument("--slabs-per-gpu", type=int, default=1,
                     help="configs[4]: slabs per GPU (>1: in-process slabs exchanging by copies)")
     args = ap.parse_args()
@@ -743,7 +917,9 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    if CONFIGS[args.config].get("slab"):
+    if args.problem:
+        run_fem(args, rank, world, dist)
+    elif CONFIGS[args.config].get("slab"):
         run_slab(args, rank, world, dist)
     else:
         run_b200(args, rank, world, dist)

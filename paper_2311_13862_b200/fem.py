@@ -348,6 +348,9 @@ class FemProblem:
     once, operators and right-hand sides per parameter batch on the device."""
 
     stored = True  # stored-coefficient hierarchy: mu-dependent rhs, term products by apply
+    # algorithmic bytes per interior node and instance of one finest-level batched apply:
+    # 14 per-instance coefficients + x + y
+    apply_bytes_per_node = 128.0
 
     def __init__(self, spec: FemProblemSpec, levels: int = 3, m0: int = 2):
         if levels < 2:

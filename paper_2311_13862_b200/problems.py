@@ -177,6 +177,25 @@ def sample_mus(spec: ProblemSpec, count: int, seed: int) -> np.ndarray:
     return b[:, 0] + u * (b[:, 1] - b[:, 0])
 
 
+def lhs_sample(p: int, n: int, bounds, seed: int = 0) -> list:
+    """Seeded Latin hypercube over a box (the reference's sampling, sampling.py:8-27): one
+    point per stratum per axis, generator draws the in-stratum offsets then one permutation
+    per axis."""
+    if n < 1:
+        raise ValueError("need at least one sample")
+    b = np.asarray(bounds, dtype=np.float64)
+    if b.shape != (p, 2):
+        raise ValueError(f"bounds must be ({p}, 2), got {b.shape}")
+    if np.any(b[:, 1] <= b[:, 0]):
+        raise ValueError("degenerate bounds: need min < max per dimension")
+    g = np.random.default_rng(seed)
+    offsets = g.random((n, p))
+    strata = np.column_stack([g.permutation(n) for _ in range(p)])
+    u = (offsets + strata) / n
+    pts = b[:, 0] + u * (b[:, 1] - b[:, 0])
+    return [row.copy() for row in pts]
+
+
 def levels_for(n: int, m0: int) -> int:
     r = n // m0
     if n % m0 or r & (r - 1):
