@@ -680,7 +680,7 @@ def run_fem(args, rank, world, dist):
     k1.record(stream)
     torch.cuda.synchronize()
     k_ms = k0.elapsed_time(k1) / reps_k
-    bpn = float(getattr(prob, "apply_bytes_per_node", 128.0))
+    bpn = float(prob.apply_bytes_per_node(ctx))
     kbytes = bpn * (n - 1) ** 3 * batch
     achieved = kbytes / (k_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "kernel": "stored27_apply (finest level, batch)",

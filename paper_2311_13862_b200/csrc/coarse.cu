@@ -614,10 +614,139 @@ static cudaError_t coarse_stored_launch(int mode, const CoarseOp& op, int batch,
   return cudaGetLastError();
 }
 
+// ---- per-term coefficients shared by the batch (assembled problems, finest level) ----------
+// The batch's operators differ only in theta: a thread owns one node and IB instances, loads
+// each per-term coefficient once and combines it for all IB instances (the combination order
+// of stored_combine, the accumulation order of coarse_stored_kernel: bitwise the same
+// results).  Instance groups are the fastest grid dimension, so the CTAs resident at one time
+// work on the same nodes and the term coefficients are L2 hits after the first group: per
+// node and instance HBM sees only the vectors.
+template <int MODE, int Q, int IB>
+__global__ void __launch_bounds__(256) stored_shared_kernel(int n, int batch,
+                                                            const double* __restrict__ tc,
+                                                            const double* __restrict__ theta,
+                                                            const double* __restrict__ x,
+                                                            const double* __restrict__ b,
+                                                            double* __restrict__ y,
+                                                            const int* __restrict__ active,
+                                                            double omega, int zlo, int zhi) {
+  const int mu0 = blockIdx.x * IB;
+  const int64_t n2 = (int64_t)n * n, n3 = n2 * n;
+  const int64_t X = (int64_t)zlo * n2 + (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
+  if (X >= (int64_t)zhi * n2) return;
+  const int i = X % n, j = (X / n) % n, k = (int)(X / n2);
+  if (i == 0 || j == 0 || k == 0) return;
+  bool on[IB];
+  double th[IB][Q];
+  int nact = 0;
+#pragma unroll
+  for (int u = 0; u < IB; ++u) {
+    const int mu = mu0 + u;
+    on[u] = mu < batch && (!active || active[mu]);
+    nact += on[u] ? 1 : 0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) th[u][q] = on[u] ? __ldg(theta + (int64_t)mu * Q + q) : 0.0;
+  }
+  if (!nact) return;
+  auto comb = [&](const double* cq, int u) {  // sum_q theta_q c_q in stored_combine's order
+    double v = th[u][0] * cq[0];
+#pragma unroll
+    for (int q = 1; q < Q; ++q) v = fma(th[u][q], cq[q], v);
+    return v;
+  };
+  double cq[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) cq[q] = __ldg(tc + (int64_t)q * 14 * n3 + X);
+  double acc[IB], c0[IB], xc[IB];
+#pragma unroll
+  for (int u = 0; u < IB; ++u) {
+    c0[u] = comb(cq, u);
+    xc[u] = on[u] ? __ldg(x + (int64_t)(mu0 + u) * n3 + X) : 0.0;
+    acc[u] = c0[u] * xc[u];
+  }
+#pragma unroll
+  for (int o = 1; o < 14; ++o) {
+    int dx, dy, dz;
+    fwd_off(o, dx, dy, dz);
+    const int64_t off = dx + (int64_t)n * (dy + (int64_t)n * dz);
+    double cf[Q], cb[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      cf[q] = __ldg(tc + ((int64_t)q * 14 + o) * n3 + X);
+      cb[q] = __ldg(tc + ((int64_t)q * 14 + o) * n3 + X - off);
+    }
+#pragma unroll
+    for (int u = 0; u < IB; ++u) {
+      if (!on[u]) continue;
+      const double* xb = x + (int64_t)(mu0 + u) * n3;
+      acc[u] = fma(comb(cf, u), __ldg(xb + X + off), acc[u]);
+      acc[u] = fma(comb(cb, u), __ldg(xb + X - off), acc[u]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < IB; ++u) {
+    if (!on[u]) continue;
+    const int64_t o = (int64_t)(mu0 + u) * n3 + X;
+    double out;
+    if (MODE == 0) out = acc[u];
+    else if (MODE == 1) out = __ldg(b + o) - acc[u];
+    else out = fma(omega / c0[u], __ldg(b + o) - acc[u], xc[u]);
+    y[o] = out;
+  }
+}
+
+template <int Q, int IB>
+static cudaError_t stored_shared_launch_qi(int mode, const CoarseOp& op, const double* theta,
+                                           int batch, const double* x, const double* b,
+                                           double* y, double omega, const LaunchCtx& lc) {
+  const int n = op.n;
+  const int zlo = lc.zhi > 0 ? lc.zlo : 0, zhi = lc.zhi > 0 ? lc.zhi : n;
+  const int64_t cnt = (int64_t)(zhi - zlo) * n * n;
+  dim3 grd((unsigned)((batch + IB - 1) / IB), (unsigned)((cnt + 255) / 256));
+  count_launch();
+#define RBWS_SSK(M) stored_shared_kernel<M, Q, IB><<<grd, 256, 0, lc.stream>>>( \
+    n, batch, op.tcoef, theta, x, b, y, lc.active, omega, zlo, zhi)
+  switch (mode) {
+    case 0: RBWS_SSK(0); break;
+    case 1: RBWS_SSK(1); break;
+    case 2: RBWS_SSK(2); break;
+    default: return cudaErrorInvalidValue;
+  }
+#undef RBWS_SSK
+  return cudaGetLastError();
+}
+
+// instances per thread (RBWS_FEM_IB = 2 | 4 | 8 for A/B runs)
+template <int Q>
+static cudaError_t stored_shared_launch_q(int mode, const CoarseOp& op, const double* theta,
+                                          int batch, const double* x, const double* b, double* y,
+                                          double omega, const LaunchCtx& lc) {
+  static const int ib = [] {
+    const char* e = getenv("RBWS_FEM_IB");
+    return e ? atoi(e) : 4;
+  }();
+  if (ib == 2) return stored_shared_launch_qi<Q, 2>(mode, op, theta, batch, x, b, y, omega, lc);
+  if (ib == 8) return stored_shared_launch_qi<Q, 8>(mode, op, theta, batch, x, b, y, omega, lc);
+  return stored_shared_launch_qi<Q, 4>(mode, op, theta, batch, x, b, y, omega, lc);
+}
+
+static cudaError_t stored_shared_launch(int mode, const CoarseOp& op, const double* theta,
+                                        int batch, const double* x, const double* b, double* y,
+                                        double omega, const LaunchCtx& lc) {
+  switch (op.Q) {
+    case 1: return stored_shared_launch_q<1>(mode, op, theta, batch, x, b, y, omega, lc);
+    case 2: return stored_shared_launch_q<2>(mode, op, theta, batch, x, b, y, omega, lc);
+    case 3: return stored_shared_launch_q<3>(mode, op, theta, batch, x, b, y, omega, lc);
+    case 4: return stored_shared_launch_q<4>(mode, op, theta, batch, x, b, y, omega, lc);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 cudaError_t coarse_launch(int mode, const CoarseOp& op, const double* theta, int batch,
                           const double* x, const double* b, double* y, double omega,
                           const LaunchCtx& lc) {
   if (op.coef) return coarse_stored_launch(mode, op, batch, x, b, y, omega, lc);
+  if (op.tcoef) return stored_shared_launch(mode, op, theta, batch, x, b, y, omega, lc);
   const int n = op.n;
   if (n < 2 || n > 256) return cudaErrorInvalidValue;
   CoarseArgs a{};
@@ -748,13 +877,12 @@ __global__ void __launch_bounds__(256) stored_combine_kernel(int n, int Q,
   const int64_t X = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (X >= n3) return;
   const double* th = theta + (int64_t)mu * Q;
-  double* C = coef + (int64_t)mu * 14 * n3;
   double c0 = 0.0;
-#pragma unroll 2
-  for (int o = 0; o < 14; ++o) {
+  const int no = coef ? 14 : 1;
+  for (int o = 0; o < no; ++o) {
     double v = th[0] * __ldg(tcoef + o * n3 + X);
     for (int q = 1; q < Q; ++q) v = fma(th[q], __ldg(tcoef + ((int64_t)q * 14 + o) * n3 + X), v);
-    C[o * n3 + X] = v;
+    if (coef) coef[(int64_t)mu * 14 * n3 + o * n3 + X] = v;
     if (o == 0) c0 = v;
   }
   const int i = X % n, j = (X / n) % n, k = (int)(X / ((int64_t)n * n));

@@ -23,6 +23,9 @@ struct CoarseOp {
   // offsets; symmetric), or null: matrix-free from the factors
   const double* coef = nullptr;
   bool coef_shared = false;  // coef is one coefficient set applied to every instance
+  // stored-coefficient hierarchy without per-instance coefficients on this level: the
+  // per-term coefficients [Q][14][n^3], combined with theta on the fly (shared by the batch)
+  const double* tcoef = nullptr;
 };
 
 // mode: 0 apply y=Ax | 1 resid y=b-Ax | 2 jacobi y=x+w(b-Ax)/diag | 4 dinv y=1/diag
@@ -35,6 +38,7 @@ cudaError_t coarse_build_coef(const CoarseOp& op, const double* theta, int batch
                               double* dinv, cudaStream_t stream);
 // per-instance coefficients coef[mu] = sum_q theta_q tcoef[q] (and 1/diag) of a stored-coefficient
 // level; tcoef = [Q][14][n^3]
+// coef may be null: 1/diag only
 cudaError_t stored_combine(int n, int Q, const double* tcoef, const double* theta, int batch,
                            double* coef, double* dinv, cudaStream_t stream);
 // coarsest level of a stored-coefficient hierarchy: dense operator + Cholesky per instance

@@ -335,6 +335,11 @@ Sep7 Batch::fine_op() const {
   return op;
 }
 
+static bool fem_shared(const Hierarchy* h) {
+  static const char* env = getenv("RBWS_FEM_SHARED");
+  return h->Q <= 4 && !(env && atoi(env) == 0);
+}
+
 int batch_create(Batch** out, Hierarchy* h, int cap, int nu, double omega, int maxl) {
   if (cap < 1) RBWS_FAIL("batch capacity must be positive");
   if (nu < 0) RBWS_FAIL("smoothing count must be non-negative");
@@ -363,7 +368,11 @@ int batch_create(Batch** out, Hierarchy* h, int cap, int nu, double omega, int m
     zalloc(&lb.dinv, V);
     if (nu != 1) { zalloc(&lb.t2, V); zalloc(&lb.t3, V); zalloc(&lb.zero, V); }
     if (l >= 1 && (l < L - 1 || h->stored)) zalloc(&lb.u, V);
-    if (e == cudaSuccess && h->stored) e = dalloc(&lb.coef, (size_t)14 * cap * n3);
+    // stored-coefficient hierarchies: per-instance coefficients on the coarse levels; the
+    // finest level combines the batch-shared term coefficients on the fly (Q <= 4, unless
+    // RBWS_FEM_SHARED=0) and keeps no per-instance copy
+    if (e == cudaSuccess && h->stored && (l < L - 1 || !fem_shared(h)))
+      e = dalloc(&lb.coef, (size_t)14 * cap * n3);
     // levels whose terms fall into more z-groups than the grouped Kronecker kernel takes:
     // stored per-instance coefficients (without the memory, the matrix-free 27-coefficient
     // kernel runs instead)
@@ -434,12 +443,12 @@ int batch_set_smoother(Batch* b, int kind) {
     if (b->maxl < L) RBWS_FAIL("Gauss-Seidel needs the finest level");
     const size_t VF = (size_t)vec_doubles(h->n, b->cap);
     cudaError_t e = cudaSuccess;
-    if (!b->wface) {
+    if (!b->wface && !h->stored) {
       b->wstride = (int64_t)VF;
       e = dalloc(&b->wface, 3 * VF);
       if (e == cudaSuccess) e = cudaMemset(b->wface, 0, sizeof(double) * 3 * VF);
     }
-    for (int l = 1; l < L - 1 && e == cudaSuccess; ++l) {
+    for (int l = 1; l < (h->stored ? L : L - 1) && e == cudaSuccess; ++l) {
       LevelBuf& lb = b->lv[l];
       if (lb.coef) continue;
       const size_t n3 = (size_t)lb.n * lb.n * lb.n;
@@ -1054,7 +1063,6 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
   const int count = b->count;
   if (count < 1) RBWS_FAIL("batch_setup must be called before solving");
   const int n = h->n;
-  const int64_t n3 = (int64_t)n * n * n;
   const int L = h->levels;
   const int hist_len = l_max + 1;
   cudaError_t e = cudaSuccess;

@@ -41,6 +41,7 @@ struct Hierarchy {
     CoarseOp o;
     o.n = cells[l]; o.Q = Q; o.G = G[l];
     o.fac = d_fac[l]; o.zsame = d_zsame[l]; o.grp = d_grp[l];
+    if (stored) o.tcoef = d_tcoef[l];
     return o;
   }
 };

@@ -348,9 +348,16 @@ class FemProblem:
     once, operators and right-hand sides per parameter batch on the device."""
 
     stored = True  # stored-coefficient hierarchy: mu-dependent rhs, term products by apply
-    # algorithmic bytes per interior node and instance of one finest-level batched apply:
-    # 14 per-instance coefficients + x + y
-    apply_bytes_per_node = 128.0
+
+    def apply_bytes_per_node(self, ctx) -> float:
+        """Algorithmic bytes per interior node and instance of one finest-level batched
+        apply: x + y, plus one pass over the batch-shared term coefficients (14 Q doubles
+        per node) spread over the batch — or 14 per-instance coefficients when the batch
+        keeps its own copies (Q > 4 or RBWS_FEM_SHARED=0)."""
+        import os
+        q = self.spec.n_terms
+        shared = q <= 4 and os.environ.get("RBWS_FEM_SHARED", "1") != "0"
+        return 16.0 + (112.0 * q / ctx.count if shared else 112.0)
 
     def __init__(self, spec: FemProblemSpec, levels: int = 3, m0: int = 2):
         if levels < 2:
