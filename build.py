@@ -22,6 +22,8 @@ OUT = PKG / "_rbws_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CFLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
           "-Xcompiler", "-fPIC", "-Xptxas", "-O3"]
+# extra -D definitions for A/B builds of kernel variants (e.g. RBWS_EXTRA_DEFS="RBWS_X=1 RBWS_Y=2")
+CFLAGS += [f"-D{d}" for d in os.environ.get("RBWS_EXTRA_DEFS", "").split()]
 
 
 def sources():

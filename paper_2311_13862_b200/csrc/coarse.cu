@@ -621,8 +621,11 @@ static cudaError_t coarse_stored_launch(int mode, const CoarseOp& op, int batch,
 // results).  Instance groups are the fastest grid dimension, so the CTAs resident at one time
 // work on the same nodes and the term coefficients are L2 hits after the first group: per
 // node and instance HBM sees only the vectors.
+#ifndef RBWS_SHARED_MINB
+#define RBWS_SHARED_MINB 2
+#endif
 template <int MODE, int Q, int IB>
-__global__ void __launch_bounds__(256) stored_shared_kernel(int n, int batch,
+__global__ void __launch_bounds__(256, RBWS_SHARED_MINB) stored_shared_kernel(int n, int batch,
                                                             const double* __restrict__ tc,
                                                             const double* __restrict__ theta,
                                                             const double* __restrict__ x,

@@ -156,8 +156,15 @@ def _apply_precond(ops, red: _Reduced | None, L, r):
     return u + red.solve(L, r - ops.apply(u))
 
 
+def _separable_only(problem):
+    if getattr(problem, "stored", False):
+        raise NotImplementedError("rbi-msrbcg runs on the separable (Kronecker-factor) problems; "
+                                  "assembled problems take mgcg / rbi-mgcg")
+
+
 def msrb_train(mus, N: int, K_max: int, hf_solver, problem) -> MsrbHierarchy:
     """Per-iteration error-snapshot bases (msrb.py:113-149); hf_solver: HighFidelitySolver."""
+    _separable_only(problem)
     import torch
     if K_max < 0:
         raise ValueError("K_max must be non-negative")
@@ -202,6 +209,7 @@ def rbi_msrbcg_solve(problem, mus, hier: MsrbHierarchy, f=None, delta: float = 1
     """Batched rbi-msrbcg: POD Galerkin initial guess (warmstart.py:81-84), then PCG
     (krylov.py:42-109 semantics, per instance) with the MSRB preconditioner
     (msrb.py:53-85).  Returns (x (count, n^3) padded rows, SolveReports)."""
+    _separable_only(problem)
     import torch
     from .multigrid import mg_context_for
     mus = problem.spec.check_mus(mus)

@@ -48,6 +48,9 @@ class HostPipeline:
                  sizes: list[int] | None = None):
         import torch
         _native.require_cuda()
+        if getattr(problem, "stored", False):
+            raise NotImplementedError("HostPipeline streams one shared rhs; for assembled "
+                                      "problems call rbi_pcg_solve with problem.rhs(mus)")
         if sub_batch < 1:
             raise ValueError("sub_batch must be positive")
         self.problem, self.method, self.model, self.sub = problem, method, model, sub_batch

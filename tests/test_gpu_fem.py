@@ -169,3 +169,13 @@ def test_fem_l1roc_rbi_mgcg_matches_reference(probs):
     for m in range(len(mus)):
         assert _rel(got[m], G[f"{k}_rbi_x"][m]) <= 1e-8
         assert abs(reps[m].iterations - G[f"{k}_rbi_iters"][m]) <= 1
+
+
+def test_fem_unsupported_paths_fail_loudly(probs):
+    pkg = _pkg()
+    p = probs["n16m4"]
+    method = pkg.MethodConfig("rbi-mgcg", delta=1e-10, l_max=60, N=2)
+    with pytest.raises(NotImplementedError):
+        pkg.HostPipeline(p, method)
+    with pytest.raises(NotImplementedError):
+        pkg.msrb_train(G["fem_n16m4_mus"], 2, 1, None, p)
