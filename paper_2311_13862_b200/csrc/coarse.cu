@@ -624,6 +624,11 @@ static cudaError_t coarse_stored_launch(int mode, const CoarseOp& op, int batch,
 #ifndef RBWS_SHARED_MINB
 #define RBWS_SHARED_MINB 2
 #endif
+#ifndef RBWS_SHARED_UNROLL
+#define RBWS_SHARED_UNROLL 13
+#endif
+#define RBWS_PRAGMA(x) _Pragma(#x)
+#define RBWS_UNROLL(n) RBWS_PRAGMA(unroll n)
 template <int MODE, int Q, int IB>
 __global__ void __launch_bounds__(256, RBWS_SHARED_MINB) stored_shared_kernel(int n, int batch,
                                                             const double* __restrict__ tc,
@@ -667,7 +672,7 @@ __global__ void __launch_bounds__(256, RBWS_SHARED_MINB) stored_shared_kernel(in
     xc[u] = on[u] ? __ldg(x + (int64_t)(mu0 + u) * n3 + X) : 0.0;
     acc[u] = c0[u] * xc[u];
   }
-#pragma unroll
+  RBWS_UNROLL(RBWS_SHARED_UNROLL)
   for (int o = 1; o < 14; ++o) {
     int dx, dy, dz;
     fwd_off(o, dx, dy, dz);
