@@ -333,6 +333,16 @@ def main_fem():
         out[f"{k}_mgcg_hist"] = np.array(hists)
         if tag != "n16m4":
             continue
+        # Gauss-Seidel V-cycle smoother (forward before / backward after, multigrid.py:137-138)
+        xs, its = [], []
+        for m in mus:
+            A, f = p.operator(m), p.rhs(m)
+            x, rep = mgcg_solve(A, f, np.zeros_like(f), mg_context_for(p, m, smoother="gs"),
+                                delta=1e-10, l_max=60)
+            xs.append(x)
+            its.append(rep.iterations)
+        out[f"{k}_gs_x"] = np.array(xs)
+        out[f"{k}_gs_iters"] = np.array(its)
         # L1ROC greedy (reference default LU high fidelity) + RBI-MGCG warm-started solves
         train = np.array(lhs_sample(spec.p, 24, spec.bounds, seed=3))
         model = l1roc_offline(list(train), 6, HighFidelitySolver(p), p.operator,

@@ -179,3 +179,42 @@ def test_fem_unsupported_paths_fail_loudly(probs):
         pkg.HostPipeline(p, method)
     with pytest.raises(NotImplementedError):
         pkg.msrb_train(G["fem_n16m4_mus"], 2, 1, None, p)
+
+
+def test_fem_gs_smoother_matches_reference(probs):
+    """smoother="gs" (forward / backward Gauss-Seidel sweeps on the stored coefficients of
+    every level) on example-1 vs the unmodified reference."""
+    pkg = _pkg()
+    p, k = probs["n16m4"], "fem_n16m4"
+    mus = G[f"{k}_mus"]
+    ctx = pkg.mg_context_for(p, mus, smoother="gs")
+    x, reps = pkg.mgcg_solve(None, None, None, ctx, delta=1e-10, l_max=60)
+    got = pkg.from_padded(x, p.n, len(mus))
+    for m in range(len(mus)):
+        assert _rel(got[m], G[f"{k}_gs_x"][m]) <= 1e-8
+        assert abs(reps[m].iterations - G[f"{k}_gs_iters"][m]) <= 1
+
+
+def test_fem_full_size_properties():
+    """At the bench size (64^3, 64 instances): every instance converges with a true residual
+    <= tol, the V-cycle is linear and symmetric (b1 . M b2 == b2 . M b1), and repeated solves
+    are bitwise identical."""
+    pkg = _pkg()
+    spec = pkg.get_problem("example-1")
+    p = pkg.ParametricProblem(spec, levels=5, m0=4)
+    mus = np.array(pkg.problems.lhs_sample(spec.p, 64, spec.bounds, seed=9))
+    ctx = pkg.mg_context_for(p, mus)
+    x1, reps = pkg.mgcg_solve(None, None, None, ctx, delta=1e-10, l_max=60)
+    assert all(r.converged and r.true_residual <= 1e-10 for r in reps)
+    x2, _ = pkg.mgcg_solve(None, None, None, ctx, delta=1e-10, l_max=60)
+    assert torch.equal(x1, x2)
+    n, c = p.n, len(mus)
+    rng = np.random.default_rng(4)
+    b1 = rng.standard_normal((c, (n - 1) ** 3))
+    b2 = rng.standard_normal((c, (n - 1) ** 3))
+    M = lambda b: pkg.from_padded(pkg.mg_vcycle(pkg.to_padded(b, n), ctx), n, c)
+    m1, m2, m12 = M(b1), M(b2), M(2.0 * b1 + b2)
+    assert np.abs(m12 - (2.0 * m1 + m2)).max() <= 1e-11 * np.abs(m12).max()
+    s12 = np.einsum("ij,ij->i", b1, m2)
+    s21 = np.einsum("ij,ij->i", b2, m1)
+    assert np.all(np.abs(s12 - s21) <= 1e-11 * np.abs(s12))

@@ -129,3 +129,15 @@ def test_product_lhs_sample_matches_reference():
     spec_b = np.array([[0.0, 2.0], [0.0, 1.0]])
     got = np.array(lhs_sample(2, 24, spec_b, seed=3))
     assert np.array_equal(got, G["fem_n16m4_l1_train"])
+
+
+def test_oracle_gs_mgcg(oprobs):
+    """Gauss-Seidel smoother (smoother="gs") on example-1 matches the reference."""
+    p, k = oprobs["n16m4"], "fem_n16m4"
+    for m, mu in enumerate(G[f"{k}_mus"]):
+        A, f = p.operator(mu), p.rhs(mu)
+        x, rep = so.mgcg_solve(A, f, np.zeros_like(f), so.mg_context_for(p, mu, smoother="gs"),
+                               delta=1e-10, l_max=60)
+        assert rep.iterations == G[f"{k}_gs_iters"][m]
+        xr = G[f"{k}_gs_x"][m]
+        assert np.linalg.norm(x - xr) <= 1e-10 * np.linalg.norm(xr)
