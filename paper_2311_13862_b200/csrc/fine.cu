@@ -484,7 +484,7 @@ fine_kernel(FineArgs a) {
         acc = on[r] ? fma(uc, Au, acc) : acc;
       } else if (MODE == FM_RESID) {
         const double rv = C0[o] - Au;
-        if (on[r]) a.out0[gidx] = rv;
+        if (on[r] && a.out0) a.out0[gidx] = rv;  // null: the norm only (true residual)
         acc = on[r] ? fma(rv, rv, acc) : acc;
       } else if (MODE == FM_JACOBI) {
         const double bv = C0[o];

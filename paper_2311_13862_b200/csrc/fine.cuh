@@ -27,7 +27,8 @@ inline int fine_post_tiles(int n, int batch, int nz = 0) {
 // y = A x (y may be null), partial (may be null) = x . A x
 cudaError_t fine_apply(const Sep7& op, int batch, const double* x, double* y, double* partial,
                        const LaunchCtx& lc);
-// r = b - A x, partial = |r|^2 (b_shared: b is one instance used by every instance)
+// r = b - A x (r may be null: norm only), partial = |r|^2 (b_shared: b is one instance used
+// by every instance)
 cudaError_t fine_resid(const Sep7& op, int batch, const double* x, const double* b, double* r,
                        double* partial, const LaunchCtx& lc, bool b_shared = false);
 // dinv = 1/diag(A(mu)) (batch setup); zsame: per-plane "z factors unchanged" flags

@@ -189,6 +189,8 @@ __global__ void __launch_bounds__(256) expand_kernel(int64_t n3, const double* _
   double w[NB];
 #pragma unroll
   for (int c = 0; c < NB; ++c) w[c] = (c < N) ? __ldg(W + c * Wstride + X) : 0.0;
+  // four instances per trip: independent FMA chains and stores in flight
+#pragma unroll 4
   for (int mu = m0; mu < m1; ++mu) {
     const double2* am = reinterpret_cast<const double2*>(as + (mu - m0) * NB);
     double s0 = 0.0, s1 = 0.0;

@@ -1161,8 +1161,8 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
   }
   // the rest (last to converge, l_max reached, breakdown)
   if (out.x_host && stream_download(b, x, out, dl_call++, true, stream)) return 1;
-  // true residual ||f - A x|| / scale for every instance
-  if (e == cudaSuccess) e = fine_resid(op, count, x, f, b->t_res, b->partial, all, fshared);
+  // true residual ||f - A x|| / scale for every instance (the norm only: no vector written)
+  if (e == cudaSuccess) e = fine_resid(op, count, x, f, nullptr, b->partial, all, fshared);
   if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
   double* d_true = b->beta;  // reuse as scratch
   count_launch();
