@@ -778,6 +778,8 @@ def _ref_solve(mu):
 def run_reference(args, rank, world):
     if rank != 0:
         return
+    if args.problem:
+        return run_reference_fem(args, world)
     if CONFIGS[args.config].get("slab"):
         return run_reference_slab(args, world)
     import multiprocessing as mp
@@ -830,6 +832,81 @@ def run_reference(args, rank, world):
                          "sample": f"{sample} test parameters per step ({args.ref_per_core} per "
                                    f"core), oracle restatement of the reference RBI-MGCG "
                                    f"(scipy.sparse), process pool over all host cores"},
+        "e2e": {"value": round(value, 4), "unit": "solves/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _ref_fem_init(n, m0, model_state):
+    _single_thread_blas()
+    from oracle import fem as of
+    from oracle import solvers as so
+    _W["oprob"] = of.OracleFemProblem(of.Example1(), levels=int(np.log2(n // m0)) + 1, m0=m0)
+    _W["model"] = so.OracleL1rocModel(*model_state)
+
+
+def _ref_fem_solve(mu):
+    from oracle import solvers as so
+    _, rep = so.rbi_mgcg_solve(_W["oprob"], mu, _W["model"], delta=1e-10, l_max=L_MAX)
+    return rep.iterations
+
+
+def run_reference_fem(args, world):
+    """`--impl reference --problem example-1`: the oracle restatement of the reference's
+    RBI-MGCG on its own FEM problem, process pool over all host cores (rank 0 only)."""
+    import multiprocessing as mp
+    from oracle import fem as of
+    from oracle import solvers as so
+    if args.problem != "example-1":
+        raise SystemExit(f"no reference arm for problem {args.problem!r}")
+    n, m0 = args.fem_n, 4
+    spec = of.Example1()
+    oprob = of.OracleFemProblem(spec, levels=int(np.log2(n // m0)) + 1, m0=m0)
+    train = np.array(so.lhs_sample(spec.p, args.fem_train, spec.bounds, seed=1000))
+    test = np.array(so.lhs_sample(spec.p, args.batch or 256, spec.bounds, seed=2000))
+
+    def hf(mu):  # HighFidelitySolver(method="mgcg") semantics (hf.py:40-57)
+        A, f = oprob.operator(mu), oprob.rhs(mu)
+        x, _ = so.mgcg_solve(A, f, np.zeros_like(f), so.mg_context_for(oprob, mu), 1e-14, 100)
+        return x
+
+    t0 = time.perf_counter()
+    model = so.l1roc_offline(list(train), args.fem_r, hf, oprob.operator, oprob.operator_rows,
+                             oprob.rhs, seed=0, on_degenerate="stop")
+    t_off = time.perf_counter() - t0
+    state = (model.basis, model.transform, model.collocation, model.solution_points,
+             model.residual_points, model.chosen, model.indicator_history, model.saturated)
+    cores = os.cpu_count() or 1
+    sample = cores * max(1, args.ref_per_core)
+    with mp.get_context("fork").Pool(cores, initializer=_ref_fem_init,
+                                     initargs=(n, m0, state)) as pool:
+        k = 0
+        for _ in range(args.warmup):
+            pool.map(_ref_fem_solve, [test[(k + i) % len(test)] for i in range(cores)])
+            k += cores
+        t1 = time.perf_counter()
+        iters = []
+        for _ in range(args.steps):
+            iters += pool.map(_ref_fem_solve, [test[(k + i) % len(test)] for i in range(sample)])
+            k += sample
+        el = time.perf_counter() - t1
+    value = args.steps * sample / el
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": "solves/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(el / args.steps * 1e3, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded LHS parameters, sampling.py:8-27; no dataset)",
+        "impl": "reference",
+        "config": {"workload": FEM_WORKLOAD.format(n=n, r=args.fem_r, t=args.fem_train,
+                                                   b=args.batch or 256),
+                   "rb_dim": model.dim, "mean_iterations_warm": round(float(np.mean(iters)), 3),
+                   "t_offline_s": round(t_off, 1)},
+        "cpu_baseline": {"value": round(value, 4), "unit": "solves/s", "cores": cores,
+                         "kind": "port",
+                         "sample": f"{sample} test parameters per step ({args.ref_per_core} per "
+                                   f"core), oracle restatement of the reference RBI-MGCG on "
+                                   f"example-1 (scipy.sparse), process pool over all host cores"},
         "e2e": {"value": round(value, 4), "unit": "solves/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
