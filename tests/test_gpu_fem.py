@@ -218,3 +218,47 @@ def test_fem_full_size_properties():
     s12 = np.einsum("ij,ij->i", b1, m2)
     s21 = np.einsum("ij,ij->i", b2, m1)
     assert np.all(np.abs(s12 - s21) <= 1e-11 * np.abs(s12))
+
+
+class _HostView:
+    """The product's host-side operators through the oracle solver interface."""
+
+    def __init__(self, p):
+        self.p, self.prolongations, self.levels = p, p.prolongations, p.levels
+
+    def operator(self, mu, level=None):
+        return self.p.operator_host(mu, level)
+
+
+def _five_term_spec(pkg):
+    from paper_2311_13862_b200 import fem
+    def blk(k):
+        return lambda x, y, z: (((x * 5).astype(int) % 5) == k).astype(np.float64) + 0.1
+    return fem.FemProblemSpec(
+        pid="five-blocks", p=5, bounds=np.array([[0.5, 2.0]] * 5),
+        diffusion_terms=tuple(fem.DiffusionTerm((lambda q: (lambda mu: mu[q]))(q), blk(q))
+                              for q in range(5)),
+        source=lambda x, y, z, mu: np.ones(np.broadcast(x, y, z).shape),
+        dirichlet=lambda x, y, z, mu: x * mu[0], source_mu_dependent=False)
+
+
+@pytest.mark.parametrize("nu", [1, 2])
+def test_fem_five_terms_and_nu(nu):
+    """Q = 5 (> 4: the finest level keeps per-instance coefficients) and nu = 1, 2 against
+    the oracle solvers on the product's own host operators."""
+    from oracle import solvers as so
+    pkg = _pkg()
+    spec = _five_term_spec(pkg)
+    p = pkg.ParametricProblem(spec, levels=3, m0=4)
+    mus = np.array([[0.6, 1.9, 1.0, 0.7, 1.3], [1.5, 0.5, 0.9, 2.0, 1.1]])
+    ctx = pkg.mg_context_for(p, mus, nu=nu)
+    x, reps = pkg.mgcg_solve(None, None, None, ctx, delta=1e-10, l_max=60)
+    got = pkg.from_padded(x, p.n, len(mus))
+    f = p.rhs_host(mus)
+    hv = _HostView(p)
+    for m, mu in enumerate(mus):
+        A = p.operator_host(mu)
+        xr, rr = so.mgcg_solve(A, f[m], np.zeros_like(f[m]), so.mg_context_for(hv, mu, nu=nu),
+                               delta=1e-10, l_max=60)
+        assert _rel(got[m], xr) <= 1e-8
+        assert abs(reps[m].iterations - rr.iterations) <= 1
