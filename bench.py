@@ -63,6 +63,10 @@ CLASS_NAMES = ["fine_p_update_apply_dot", "fine_cg_update", "fine_pre_residual",
 #  p-update+apply: s, p_old -> p_new | cg: p, x, r -> x, r | pre: b, dinv -> r1
 #  restrict: r1 -> bc, uc (2/8) + dinv_c (1/8) | prolong+post (fused): b, dinv, e (1/8) -> s
 CLASS_BYTES = {0: 24.0, 1: 40.0, 2: 24.0, 3: 11.0, 4: 25.0, 5: 25.0, 6: 24.0}
+# fused pre-smoothing (b, dinv -> t, the x/z-restricted residual: 1/4) and its y pass
+# (t 1/4 -> bc, uc 2/8, dinv_c 1/8)
+FUSED_PRE_BYTES = 18.0
+FUSED_RESTRICT_Y_BYTES = 5.0
 
 
 def log(*a):
@@ -255,6 +259,7 @@ def run_b200(args, rank, world, dist):
     # out to pinned host memory, sub-batches pipelined (paper_2311_13862_b200.pipeline)
     del state["x"]
     scw = bool(_native.load().rbws_batch_stored_weights(ctx.handle))
+    fused = bool(_native.load().rbws_batch_fused_restrict(ctx.handle))
     del ctx, xbuf
     torch.cuda.empty_cache()
     e2e_sub = min(batch, args.e2e_sub or cfg.get("e2e_sub", 512))
@@ -290,6 +295,9 @@ def run_b200(args, rank, world, dist):
     nodes = (n - 1) ** 3
     # stored face weights (SCW kernels): +24 B/node in every finest-level stencil sweep
     class_bytes = {k: v + (24.0 if (scw and k != 3) else 0.0) for k, v in CLASS_BYTES.items()}
+    if fused:  # pre-smoothing + x/z restriction in one kernel: r1 never written
+        class_bytes[2] = FUSED_PRE_BYTES + (24.0 if scw else 0.0)
+        class_bytes[3] = FUSED_RESTRICT_Y_BYTES
     table = {}
     for k in range(NC):
         if pcalls[k] == 0:
@@ -312,7 +320,8 @@ def run_b200(args, rank, world, dist):
                     "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                     "traffic": traffic, "traffic_source": tsrc, "peak_source": peak_kind,
                     "bytes_per_launch": int(dom_bytes),
-                    "bytes_per_node": class_bytes[dom], "stored_weights": scw}
+                    "bytes_per_node": class_bytes[dom], "stored_weights": scw,
+                    "fused_pre_restrict": fused}
     else:  # the warm start already met the tolerance: no PCG iteration ran
         roofline = {"bound": "hbm", "kernel": None, "achieved": None, "peak": peak,
                     "unit": "GB/s", "frac": None, "traffic": None, "peak_source": peak_kind}

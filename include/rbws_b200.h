@@ -114,6 +114,9 @@ int rbws_smooth(rbws_batch* b, int level, int kind, double* x, const double* rhs
 /* 1 if the finest-level kernels of this batch read stored face weights (coefficients
  * whose z factors change on most planes; +24 B per node per stencil sweep), else 0 */
 int rbws_batch_stored_weights(const rbws_batch* b);
+/* 1 if the last V-cycle ran the finest pre-smoothing residual fused with the x/z passes of
+ * the restriction (r1 = b - A(w D^-1 b) never written; the measurement's byte counts) */
+int rbws_batch_fused_restrict(const rbws_batch* b);
 
 /* y = A^level(mu) x for every instance (ParametricProblem.operator(mu, level) @ x,
  * grid.py:246-255).  x, y: (dev) padded vectors of that level. */

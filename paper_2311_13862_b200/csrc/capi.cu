@@ -150,6 +150,10 @@ int rbws_batch_stored_weights(const rbws_batch* b) {
   return reinterpret_cast<const Batch*>(b)->wface ? 1 : 0;
 }
 
+int rbws_batch_fused_restrict(const rbws_batch* b) {
+  return reinterpret_cast<const Batch*>(b)->fused_used ? 1 : 0;
+}
+
 int rbws_batch_set_graph(rbws_batch* b, int enable) {
   if (!b) RBWS_FAIL("null batch");
   B(b)->use_graph = enable != 0;

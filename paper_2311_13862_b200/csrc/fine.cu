@@ -100,6 +100,8 @@ enum FineMode : int {
   FM_CG = 4,      // h0 = p, c0 = x, c1 = r  x += a p, r -= a A p (in place), dot |r|^2
   FM_PAPPLY = 5,  // h0 = s, h1 = p_old      out0 = p = s + b p_old, dot p.Ap
   FM_POSTP = 6,   // h0 = b, h1 = dinv, ec   u = w dinv b + P ec; out0 = u + w (b - A u)/d, dot b.out
+  FM_PREX = 7,    // h0 = b, h1 = dinv       r1 = b - A (w dinv b), restricted along x and z in the
+                  //                         CTA: out0 = t[K][j][I] (n/2 x n x n/2 per instance)
 };
 
 // DC ("diagonal cached"): PRE / POSTP keep w/diag of the staged rows in a shared-memory
@@ -114,7 +116,8 @@ template <int MODE, int N, bool DC = false>
 struct SL {
   // PRE / PAPPLY stencil a derived vector (w dinv b, s + beta p_old): each staged
   // plane is transformed once into a second ring, so neighbours cost one LDS
-  static constexpr bool XF = (MODE == FM_PRE || MODE == FM_PAPPLY || MODE == FM_POSTP);
+  static constexpr bool XF = (MODE == FM_PRE || MODE == FM_PREX || MODE == FM_PAPPLY ||
+                              MODE == FM_POSTP);
   static constexpr int NH = XF ? 2 : 1;  // DC: h1 (1/diag) staged only on reload planes
   static constexpr int NC = (MODE == FM_CG) ? 2 : ((MODE == FM_RESID || MODE == FM_JACOBI) ? 1 : 0);
   // raw / transformed ring slots (N = 512 rows are 4 KB: a shallower raw ring fits 227 KB).
@@ -157,7 +160,7 @@ struct FSmem {
                                (MODE == FM_POSTP ? FCoarse<N, G::TY>::CSZ : 0);
   // raw ring, transformed ring, cached w/diag tile (DC)
   static constexpr int RING = L::S * STAGE + (L::XF ? L::U * G::HSZ : 0) +
-                              (DC ? G::HSZ : 0);
+                              (DC ? G::HSZ : 0) + (MODE == FM_PREX ? 4 * G::CSZ : 0);
   static size_t bytes(int np, int Q) {
     return 64 + 4 * (kMaxKz + 4) + 8 * (((size_t)np * 3 * Q + 1) & ~(size_t)1) + 8 * (size_t)RING;
   }
@@ -205,6 +208,7 @@ fine_kernel(FineArgs a) {
   double* ring = zf + ((np * ZW + 1) & ~1);                      // [S][STAGE]
   double* uring = ring + S * STAGE;                              // [U][HSZ] (XF)
   double* wd = uring + (XF ? U * HSZ : 0);                       // [HSZ] w/diag (DC)
+  double* rbuf = wd + (DC ? HSZ : 0);  // FM_PREX: r1 of [2 trips][2 planes][TY rows][N]
 
   for (int t = tid; t < np * ZW; t += G::THREADS) {  // z factors of the staged planes
     const int p = t / (3 * Q), f = (t / Q) % 3, q = t % Q, k = p_first + p;
@@ -362,7 +366,7 @@ fine_kernel(FineArgs a) {
       const int e = trow_e(t);
       double v;
       if (DC && reload) wd[e] = om * R[HSZ + e];  // staged with this plane
-      if (MODE == FM_PRE) {
+      if (MODE == FM_PRE || MODE == FM_PREX) {
         v = (DC ? wd[e] : om * R[HSZ + e]) * R[e];  // w dinv b
       } else if (MODE == FM_PAPPLY) {
         v = fma(sc, R[HSZ + e], R[e]);  // s + beta p_old
@@ -472,6 +476,9 @@ fine_kernel(FineArgs a) {
     if (MODE == FM_PRE) {
       // b - A (w D^-1 b) = (1 - w) b + off(w D^-1 b): the diagonal term is w b
       if (on[r]) a.out0[gidx] = fma(1.0 - om, vbr, off);
+    } else if (MODE == FM_PREX) {  // to the CTA's r1 buffer (ghost nodes: 0)
+      const int t = k - kb;
+      rbuf[(((t >> 1) & 1) * 2 + (t & 1)) * CSZ + coff + o] = on[r] ? fma(1.0 - om, vbr, off) : 0.0;
     } else if (MODE == FM_POSTP) {
       const double Au = fma(dgr, uc, -off);
       const double y = fma(wdr, vbr - Au, uc);
@@ -512,6 +519,30 @@ fine_kernel(FineArgs a) {
     gk += N2;
   };
 
+  // FM_PREX epilogue: thread (I, orow) restricts row j0+orow of plane kk along x
+  // (0.5 r(2I-1) + r(2I) + 0.5 r(2I+1), the order of restrict_kernel) and accumulates the
+  // z weights 0.5 / 1 / 0.5 of coarse plane K in a register; a completed coarse plane goes
+  // to t[K][j][I].  Needs the whole z-range of the instance in one CTA (zc == 1).
+  constexpr int NCX = N / 2;
+  const int xI = tid % NCX, xrow = tid / NCX;
+  const bool xon = (MODE == FM_PREX) && xrow < TY && xI >= 1;
+  double xacc = 0.0;
+  double* tout = a.out0 + (int64_t)mu * NCX * N * NCX + (int64_t)(j0 + xrow) * NCX + xI;
+  auto xz = [&](int kk) {
+    if (!xon) return;
+    const int t = kk - kb;
+    const double* R1 = rbuf + (((t >> 1) & 1) * 2 + (t & 1)) * CSZ + xrow * N + 2 * xI;
+    const double v = 0.5 * (R1[-1] + R1[1]) + R1[0];
+    if (kk & 1) {  // 2K+1: closes coarse plane K, opens K+1
+      xacc += 0.5 * v;
+      const int K = (kk - 1) >> 1;
+      if (K >= 1) tout[(int64_t)K * N * NCX] = xacc;
+      xacc = 0.5 * v;
+    } else {
+      xacc += v;
+    }
+  };
+
   // two planes per trip with statically rotating register roles: one CTA barrier
   // and two TMA issues amortised over two nodes per row
   for (int k0 = kb; k0 < ke; k0 += 2) {
@@ -528,6 +559,10 @@ fine_kernel(FineArgs a) {
       if (tid == 0) {
         if (k0 + 1 + S <= p_last) issue(k0 + 1 + S);
         if (k0 + 2 + S <= p_last) issue(k0 + 2 + S);
+      }
+      if (MODE == FM_PREX && k0 > kb) {  // the previous trip's r1 planes are complete
+        xz(k0 - 2);
+        xz(k0 - 1);
       }
     } else {
       wait(k0 + 1);
@@ -566,6 +601,12 @@ fine_kernel(FineArgs a) {
       }
     }
   }
+  if (MODE == FM_PREX) {  // the last trip's planes
+    __syncthreads();
+    const int kl = kb + (((ke - kb) - 1) & ~1);
+    xz(kl);
+    if (kl + 1 < ke) xz(kl + 1);
+  }
   if (a.dot != DOT_NONE) {
     __shared__ double red[32];
     const double s = block_reduce_sum(acc, red);
@@ -596,7 +637,7 @@ static cudaError_t fine_launch_mnd(const FineArgs& a, int batch, cudaStream_t st
 template <int MODE, int N>
 static cudaError_t fine_launch_mn(const FineArgs& a, int batch, cudaStream_t stream) {
   if (a.op.wface) return fine_launch_mnd<MODE, N, false, true>(a, batch, stream);
-  if constexpr (MODE == FM_PRE || MODE == FM_POSTP)
+  if constexpr (MODE == FM_PRE || MODE == FM_PREX || MODE == FM_POSTP)
     if (a.dc) return fine_launch_mnd<MODE, N, true>(a, batch, stream);
   return fine_launch_mnd<MODE, N, false>(a, batch, stream);
 }
@@ -624,6 +665,7 @@ static cudaError_t fine_launch(int mode, FineArgs& a, int batch, cudaStream_t st
     case FM_RESID: return fine_launch_m<FM_RESID>(a, batch, stream);
     case FM_JACOBI: return fine_launch_m<FM_JACOBI>(a, batch, stream);
     case FM_PRE: return fine_launch_m<FM_PRE>(a, batch, stream);
+    case FM_PREX: return fine_launch_m<FM_PREX>(a, batch, stream);
     case FM_CG: return fine_launch_m<FM_CG>(a, batch, stream);
     case FM_PAPPLY: return fine_launch_m<FM_PAPPLY>(a, batch, stream);
     case FM_POSTP: return fine_launch_m<FM_POSTP>(a, batch, stream);
@@ -790,6 +832,21 @@ cudaError_t fine_pre(const Sep7& op, int batch, const double* b, const double* d
   a.h1 = dinv;
   a.out0 = r1;
   return fine_launch(FM_PRE, a, batch, lc.stream);
+}
+
+bool fine_pre_xz_ok(int n, int batch, const LaunchCtx& lc) {
+  if (lc.zhi > 0 && (lc.zlo != 0 || lc.zhi != n)) return false;  // z-ranges (slabs): no
+  return fine_geom(n, batch, n, fine_mode_threads(FM_PREX, n)).zc == 1;
+}
+
+cudaError_t fine_pre_xz(const Sep7& op, int batch, const double* b, const double* dinv,
+                        double* t, double omega, const LaunchCtx& lc) {
+  if (!fine_pre_xz_ok(op.n, batch, lc)) return cudaErrorInvalidValue;
+  FineArgs a = base_args(op, DOT_NONE, nullptr, lc, omega);
+  a.h0 = b;
+  a.h1 = dinv;
+  a.out0 = t;
+  return fine_launch(FM_PREX, a, batch, lc.stream);
 }
 
 cudaError_t fine_post_prolong(const Sep7& op, int batch, const double* b, const double* dinv,

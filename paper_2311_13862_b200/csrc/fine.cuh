@@ -40,6 +40,13 @@ cudaError_t fine_jacobi(const Sep7& op, int batch, const double* x, const double
 // r1 = b - A (omega dinv b)
 cudaError_t fine_pre(const Sep7& op, int batch, const double* b, const double* dinv, double* r1,
                      double omega, const LaunchCtx& lc);
+// pre-smoothing residual fused with the x and z passes of the restriction:
+// t[K][j][I] (n/2 x n x n/2 per instance) = sum over fine planes 2K-1..2K+1 and columns
+// 2I-1..2I+1 (weights 0.5 / 1 / 0.5) of r1 = b - A (omega dinv b) on fine row j; the y pass is
+// restrict_y_launch.  Only when one CTA holds an instance's whole z-range (fine_pre_xz_ok).
+bool fine_pre_xz_ok(int n, int batch, const LaunchCtx& lc);
+cudaError_t fine_pre_xz(const Sep7& op, int batch, const double* b, const double* dinv,
+                        double* t, double omega, const LaunchCtx& lc);
 // fused prolongation + post-smoothing of the nu=1 V-cycle:
 // u = w dinv b + P ec (ec: coarse correction, n/2 cells), y = u + w (b - A u)/diag,
 // partial (may be null) = b . y

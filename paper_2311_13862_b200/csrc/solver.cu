@@ -349,6 +349,8 @@ int batch_create(Batch** out, Hierarchy* h, int cap, int nu, double omega, int m
   {
     const char* g = getenv("RBWS_GRAPH");
     b->use_graph = g ? atoi(g) != 0 : b->use_graph;
+    const char* fr = getenv("RBWS_FUSED_RESTRICT");  // "0": separate pre-smoothing + restriction
+    b->fuse_restrict = fr ? atoi(fr) != 0 : true;
   }
   const int L = h->levels;
   b->maxl = (maxl <= 0 || maxl > L) ? L : maxl;
@@ -586,13 +588,20 @@ int Batch::vcycle(int lvl, const double* bb, double* out, double* dot_partial,
   }
   if (nu == 1) {
     int t0 = pf ? prof_begin(lc.stream) : -1;
+    // finest level, whole instances per CTA: the pre-smoothing kernel also runs the x and z
+    // passes of the restriction (r1 never reaches HBM), a light kernel the y pass
+    const bool fused = fine && fuse_restrict && lvl - 1 >= 1 && fine_pre_xz_ok(n, count, lc);
+    fused_used = fused;
     if (stop) e = vec_scale_dinv(n, count, omega, l.dinv, bb, l.u, lc.stream);
-    if (e == cudaSuccess) e = op(MODE_PRE, DOT_NONE, nullptr, bb, l.t1, nullptr);
+    if (e == cudaSuccess)
+      e = fused ? fine_pre_xz(fine_op(), count, bb, l.dinv, l.t1, omega, lc)
+                : op(MODE_PRE, DOT_NONE, nullptr, bb, l.t1, nullptr);
     if (pf) { prof_end(PROF_FINE_PRE, t0, lc.stream); t0 = prof_begin(lc.stream); }
     // the restriction also writes the next level's pre-scaled rhs u = w D^-1 b
     if (e == cudaSuccess)
-      e = (lvl - 1 >= 1) ? restrict_launch(n, count, l.t1, c.b, lc, c.dinv, c.u, omega)
-                         : restrict_launch(n, count, l.t1, c.b, lc);
+      e = fused ? restrict_y_launch(n, count, l.t1, c.b, lc, c.dinv, c.u, omega)
+          : (lvl - 1 >= 1) ? restrict_launch(n, count, l.t1, c.b, lc, c.dinv, c.u, omega)
+                           : restrict_launch(n, count, l.t1, c.b, lc);
     if (pf) { prof_end(PROF_FINE_RESTRICT, t0, lc.stream); t0 = prof_begin(lc.stream); }
     if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
     if (vcycle(lvl - 1, c.b, c.e, nullptr, lc)) return 1;

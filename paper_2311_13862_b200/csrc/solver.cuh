@@ -85,6 +85,8 @@ struct Batch {
   int cap = 0, count = 0, nu = 1;
   int maxl = 0;                     // levels with buffers (< levels: coarse-only, slab path)
   int smoother = 0;                 // 0 damped Jacobi (isotropic default), 1 Gauss-Seidel ("gs")
+  bool fuse_restrict = true;        // finest pre-smoothing + x/z restriction in one kernel
+  bool fused_used = false;          // the last V-cycle took the fused path
   double omega = 0.7;
   double* theta = nullptr;          // [cap][Q]
   double* wface = nullptr;          // stored fine face weights [3][cap n^3 + 2n^2] (SCW kernels)

@@ -248,6 +248,41 @@ cudaError_t restrict_launch(int nf, int batch, const double* rf, double* bc, con
   return cudaGetLastError();
 }
 
+// y pass of the restriction whose x and z passes ran inside the pre-smoothing kernel
+// (fine_pre_xz): bc(I,J,K) = 0.5 t(K,2J-1,I) + t(K,2J,I) + 0.5 t(K,2J+1,I), t = n/2 x n x n/2
+// per instance; with dinv_c/uc also uc = omega dinv_c bc
+__global__ void __launch_bounds__(256) restrict_y_kernel(int nf, const double* __restrict__ t,
+                                                         double* __restrict__ bc,
+                                                         const int* __restrict__ active,
+                                                         const double* __restrict__ dinv_c,
+                                                         double* __restrict__ uc, double omega) {
+  const int nc = nf / 2;
+  const int mu = blockIdx.y;
+  if (active && !active[mu]) return;
+  const int64_t nc3 = (int64_t)nc * nc * nc;
+  const int64_t X = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // coarse node
+  if (X >= nc3) return;
+  const int I = X % nc, J = (X / nc) % nc, K = X / ((int64_t)nc * nc);
+  if (I == 0 || J == 0 || K == 0) return;
+  const double* tk = t + (int64_t)mu * nc * nf * nc + (int64_t)K * nf * nc + I;
+  double acc = 0.0;
+  acc += 0.5 * __ldg(tk + (int64_t)(2 * J - 1) * nc);
+  acc += __ldg(tk + (int64_t)(2 * J) * nc);
+  acc += 0.5 * __ldg(tk + (int64_t)(2 * J + 1) * nc);
+  const int64_t o = (int64_t)mu * nc3 + X;
+  bc[o] = acc;
+  if (uc) uc[o] = omega * __ldg(dinv_c + o) * acc;
+}
+
+cudaError_t restrict_y_launch(int nf, int batch, const double* t, double* bc, const LaunchCtx& lc,
+                              const double* dinv_c, double* uc, double omega) {
+  const int64_t nc3 = (int64_t)(nf / 2) * (nf / 2) * (nf / 2);
+  dim3 grd((unsigned)((nc3 + 255) / 256), batch);
+  count_launch();
+  restrict_y_kernel<<<grd, 256, 0, lc.stream>>>(nf, t, bc, lc.active, dinv_c, uc, omega);
+  return cudaGetLastError();
+}
+
 // z-marching trilinear prolongation: one thread per fine column (i, j); the
 // xy-interpolated coarse values of the two bracketing coarse planes are kept in
 // registers, so each fine node costs one coarse gather per two fine planes.

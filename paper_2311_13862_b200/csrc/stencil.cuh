@@ -41,6 +41,10 @@ cudaError_t sep7_launch(const Sep7& op, int batch, int mode, int dot, const doub
 cudaError_t restrict_launch(int nf, int batch, const double* rf, double* bc, const LaunchCtx& lc,
                             const double* dinv_c = nullptr, double* uc = nullptr,
                             double omega = 0.0);
+// y pass of a restriction whose x / z passes ran in fine_pre_xz (t: n/2 x n x n/2 per instance)
+cudaError_t restrict_y_launch(int nf, int batch, const double* t, double* bc, const LaunchCtx& lc,
+                              const double* dinv_c = nullptr, double* uc = nullptr,
+                              double omega = 0.0);
 // mode 0: u += P e ;  mode 1: u = omega dinv b + P e ;  mode 2: u = b + P e
 cudaError_t prolong_launch(int nf, int batch, int mode, const double* ec, double* u,
                            const double* b, const double* dinv, double omega, const LaunchCtx& lc);
