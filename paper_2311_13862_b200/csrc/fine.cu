@@ -193,7 +193,10 @@ fine_kernel(FineArgs a) {
   const int tid = threadIdx.x;
   const int64_t base = (int64_t)mu * N2 * N;
   const int kz = a.g.kz;
-  const int kb = max(1, a.zlo + kc * kz), ke = min(min(N, a.zhi), a.zlo + (kc + 1) * kz);
+  const int kb0 = max(1, a.zlo + kc * kz), ke = min(min(N, a.zhi), a.zlo + (kc + 1) * kz);
+  // FM_PREX on a z-chunk starting at an even plane 2K: coarse plane K also needs fine plane
+  // 2K-1, so the chunk recomputes it (output planes from kb0 - 1; nothing is written for it)
+  const int kb = (MODE == FM_PREX && kb0 > 1) ? kb0 - 1 : kb0;
   if (kb >= ke) {  // empty chunk (never for the geometries fine_geom builds)
     if (a.dot != DOT_NONE && tid == 0) a.partial[(int64_t)mu * a.g.tiles + yt * zc + kc] = 0.0;
     return;
@@ -275,7 +278,7 @@ fine_kernel(FineArgs a) {
   const bool zlast = (np > 64) ? zsame[64] != 0 : false;  // kz = 64: plane p_first + 64 = ke - 1
   auto repeats = [&](int k) -> bool {  // CTA-uniform
     const int t = k - p_first;
-    return t < 64 ? ((zmask >> t) & 1) != 0 : zlast;
+    return t < 64 ? ((zmask >> t) & 1) != 0 : (MODE == FM_PREX ? zsame[t] != 0 : zlast);
   };
 
   // ---- this thread's column i and rows j = j0 + rl0 + r*RPP
@@ -533,10 +536,10 @@ fine_kernel(FineArgs a) {
     const int t = kk - kb;
     const double* R1 = rbuf + (((t >> 1) & 1) * 2 + (t & 1)) * CSZ + xrow * N + 2 * xI;
     const double v = 0.5 * (R1[-1] + R1[1]) + R1[0];
-    if (kk & 1) {  // 2K+1: closes coarse plane K, opens K+1
+    if (kk & 1) {  // 2K+1: closes coarse plane K (if 2K-1 was in this chunk), opens K+1
       xacc += 0.5 * v;
       const int K = (kk - 1) >> 1;
-      if (K >= 1) tout[(int64_t)K * N * NCX] = xacc;
+      if (K >= 1 && kk >= kb + 2) tout[(int64_t)K * N * NCX] = xacc;
       xacc = 0.5 * v;
     } else {
       xacc += v;
@@ -618,7 +621,7 @@ template <int MODE, int N, bool DC, bool SCW = false>
 static cudaError_t fine_launch_mnd(const FineArgs& a, int batch, cudaStream_t stream) {
   using G = FTM<MODE, N>;
   if (a.g.threads != G::THREADS || a.g.ty != G::TY) return cudaErrorInvalidValue;
-  const int np = a.g.kz + 2;
+  const int np = a.g.kz + (MODE == FM_PREX ? 3 : 2);  // FM_PREX: one recomputed plane
   const size_t smem = FSmem<N, MODE, DC>::bytes(np, SCW ? 0 : a.op.Q);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   static size_t attr = 48 * 1024;
@@ -836,7 +839,11 @@ cudaError_t fine_pre(const Sep7& op, int batch, const double* b, const double* d
 
 bool fine_pre_xz_ok(int n, int batch, const LaunchCtx& lc) {
   if (lc.zhi > 0 && (lc.zlo != 0 || lc.zhi != n)) return false;  // z-ranges (slabs): no
-  return fine_geom(n, batch, n, fine_mode_threads(FM_PREX, n)).zc == 1;
+  // N = 128: the r1 double buffer (16 KB) costs the second CTA per SM; measured on configs[2]
+  // (pre + restriction 7.4 -> 10.4 ms per V-cycle), so the separate kernels stay there
+  if (n == 128) return false;
+  // z-chunks must start on even planes (a chunk then recomputes the odd plane below it)
+  return (fine_geom(n, batch, n, fine_mode_threads(FM_PREX, n)).kz & 1) == 0;
 }
 
 cudaError_t fine_pre_xz(const Sep7& op, int batch, const double* b, const double* dinv,
