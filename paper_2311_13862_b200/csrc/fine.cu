@@ -134,7 +134,8 @@ struct SL {
 #endif
   static constexpr int S = XF ? (N >= 512 ? (RBWS_N512_NPT == 2 ? (MODE == FM_POSTP ? 2 : 3) : 4)
                                           : (N >= 256 ? (MODE == FM_POSTP ? 3 : RBWS_N256_XF_S)
-                                                      : (N >= 128 ? RBWS_N128_XF_S : 6)))
+                                                      : (N >= 128 ? (MODE == FM_PREX ? 3 : RBWS_N128_XF_S)
+                                                                  : 6)))
                               : (N >= 128 ? 6 : kStages);
   static constexpr int U = 6;
 };
@@ -839,9 +840,14 @@ cudaError_t fine_pre(const Sep7& op, int batch, const double* b, const double* d
 
 bool fine_pre_xz_ok(int n, int batch, const LaunchCtx& lc) {
   if (lc.zhi > 0 && (lc.zlo != 0 || lc.zhi != n)) return false;  // z-ranges (slabs): no
-  // N = 128: the r1 double buffer (16 KB) costs the second CTA per SM; measured on configs[2]
-  // (pre + restriction 7.4 -> 10.4 ms per V-cycle), so the separate kernels stay there
-  if (n == 128) return false;
+  static const bool n128 = [] {  // A/B: RBWS_FUSED_N128=0 keeps the separate kernels
+    const char* e = getenv("RBWS_FUSED_N128");
+    return !(e && atoi(e) == 0);
+  }();
+  // N = 128: the r1 double buffer (16 KB) on top of the 4-slot ring cost the second CTA per
+  // SM (configs[2]: pre + restriction 7.4 -> 10.4 ms per V-cycle); FM_PREX runs a 3-slot ring
+  // there: 7.37 -> 7.27 ms, 792 -> 813 solves/s (A/B, two runs each)
+  if (n == 128 && !n128) return false;
   // z-chunks must start on even planes (a chunk then recomputes the odd plane below it)
   return (fine_geom(n, batch, n, fine_mode_threads(FM_PREX, n)).kz & 1) == 0;
 }
