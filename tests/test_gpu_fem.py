@@ -262,3 +262,24 @@ def test_fem_five_terms_and_nu(nu):
                                delta=1e-10, l_max=60)
         assert _rel(got[m], xr) <= 1e-8
         assert abs(reps[m].iterations - rr.iterations) <= 1
+
+
+def test_fem_pcg_edge_cases(probs):
+    """The stored-coefficient PCG on the reference's edge cases (krylov.py:42-109): l_max = 0,
+    an exact initial guess, a zero right-hand side (absolute norms)."""
+    pkg = _pkg()
+    p = probs["n16m4"]
+    mus = G["fem_n16m4_mus"]
+    c = len(mus)
+    ctx = pkg.mg_context_for(p, mus)
+    f = p.rhs(mus)
+    x, reps = pkg.mgcg_solve(None, f, None, ctx, delta=1e-10, l_max=0)
+    assert all(r.iterations == 0 and len(r.history) == 1 and not r.converged for r in reps)
+    assert float(x.abs().max()) == 0.0
+    xs, _ = pkg.mgcg_solve(None, f, None, ctx, delta=1e-13, l_max=60)
+    _, reps2 = pkg.mgcg_solve(None, f, xs, ctx, delta=1e-10, l_max=60)
+    assert all(r.iterations == 0 and r.converged for r in reps2)
+    z = torch.zeros_like(f)
+    xz, reps3 = pkg.mgcg_solve(None, z, None, ctx, delta=1e-10, l_max=60)
+    assert all(r.iterations == 0 and r.converged and r.absolute_norms for r in reps3)
+    assert float(xz.abs().max()) == 0.0
