@@ -17,7 +17,8 @@ does it, so it is independent of the product's stencil-direct assembly
   (grid.py:266-284).
 
 Pinned against tests/golden/golden_fem.npz (the unmodified reference run on
-``example-1``, tests/golden/make_golden.py --fem).
+``example-1``, tests/golden/make_golden.py --fem) and golden_fem2.npz
+(``example-2``: zero-flux face, anisotropy, plane smoothers; ``--fem2``).
 """
 
 from __future__ import annotations
@@ -149,6 +150,42 @@ class Example1:
         return mu
 
 
+# ------------------------------------------------------------------ example-2 (problems.py:113-152)
+
+def _indicator(y_lo, y_hi, z_lo, z_hi):
+    """Block indicator of the y/z quadrant (problems.py:116-122)."""
+    def kernel(x, y, z):
+        return (((y >= y_lo) & (y < y_hi)) & ((z >= z_lo) & (z < z_hi))).astype(np.float64)
+    return kernel
+
+
+class Example2:
+    """Mixed problem: zero-flux face x = 1, anisotropic diag(1, 1, 1e-2) piecewise-constant
+    coefficient on four y/z quadrants, mu-dependent Gaussian source (problems.py:135-152)."""
+
+    pid = "example-2"
+    p = 7
+    bounds = np.array([[0.1, 1.0]] * 3 + [[0.4, 0.6]] * 3 + [[0.25, 0.5]])
+    neumann_face_x1 = True
+    aniso = ((1.0, 1.0, 1.0e-2),) * 4
+
+    def kernels(self):
+        return (_indicator(0.0, 0.5, 0.0, 0.5), _indicator(0.0, 0.5, 0.5, 1.01),
+                _indicator(0.5, 1.01, 0.0, 0.5), _indicator(0.5, 1.01, 0.5, 1.01))
+
+    def theta(self, mu):
+        return np.array([mu[0], mu[1], mu[2], 1.0])
+
+    def source(self, x, y, z, mu):
+        r2 = (x - mu[3]) ** 2 + (y - mu[4]) ** 2 + (z - mu[5]) ** 2
+        return mu[6] + np.exp(-r2 / mu[6]) / mu[6]
+
+    def dirichlet(self, x, y, z, mu):
+        return np.zeros(np.broadcast(x, y, z).shape)
+
+    check_mu = Example1.check_mu
+
+
 class OracleFemProblem:
     """Reference ParametricProblem restated for assembled problems (grid.py:193-290)."""
 
@@ -172,7 +209,10 @@ class OracleFemProblem:
             P = self.prolongations[i]
             self.terms_by_level[i] = [(P.T @ (T @ P)).tocsr() for T in self.terms_by_level[i + 1]]
         self.terms_ff = self.terms_by_level[-1]
-        self._load = load(n, spec.source, None)   # example-1: mu-independent source
+        # example-1's source is mu-independent (assembled once, grid.py:270-275)
+        self._load = None if spec.neumann_face_x1 else load(n, spec.source, None)
+        # z-layer of every free DoF per level (plane smoothers, multigrid.py:197-201)
+        self.layers_by_level = [f // (c + 1) ** 2 for f, c in zip(self.free_by_level, self.cells)]
 
     @property
     def levels(self):
@@ -199,7 +239,8 @@ class OracleFemProblem:
     def rhs(self, mu):
         mu = self.spec.check_mu(mu)
         n = self.n
-        f = self._load[self.free_by_level[-1]].copy()
+        ld = self._load if self._load is not None else load(n, self.spec.source, mu)
+        f = ld[self.free_by_level[-1]].copy()
         t = np.linspace(0.0, 1.0, n + 1)
         Z, Y, X = np.meshgrid(t, t, t, indexing="ij")
         d = self.dir_by_level[-1]

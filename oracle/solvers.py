@@ -16,6 +16,7 @@ import scipy.linalg as sla
 import scipy.sparse as sp
 
 JACOBI_OMEGA = 0.7   # multigrid.py:27
+PLANE_OMEGA = 0.6    # multigrid.py:29 (damped plane-Jacobi of the anisotropic problem)
 
 
 class OperatorError(Exception):
@@ -59,6 +60,64 @@ def gs_sweep(A, x, b, forward: bool = True):
     return x
 
 
+class PlaneSmoother:
+    """z-plane block smoother (multigrid.py:48-110): plane blocks A[plane, plane] solved
+    exactly (here: dense Cholesky of each block, the reference uses sparse LU — the same
+    solve up to rounding), neighbour couplings only to the adjacent layers.  omega = 1:
+    block Gauss-Seidel, ascending planes before / descending after the coarse correction
+    ("plane-z"); omega < 1: damped block Jacobi x += omega A_pp^-1 (b - A x)_p
+    ("plane-jacobi")."""
+
+    def __init__(self, A, layers, omega: float = 1.0):
+        A = sp.csr_matrix(A)
+        layers = np.asarray(layers)
+        if len(layers) != A.shape[0]:
+            raise ValueError("layer map does not match operator size")
+        self.A, self.omega = A, float(omega)
+        self.planes = [np.flatnonzero(layers == z) for z in np.unique(layers)]
+        self.factors, self.nbrs = [], []
+        for p, idx in enumerate(self.planes):
+            try:
+                self.factors.append(sla.cho_factor(A[idx][:, idx].toarray()))
+            except sla.LinAlgError as exc:
+                raise OperatorError(f"plane block not SPD: {exc}") from exc
+            prv = A[idx][:, self.planes[p - 1]].tocsr() if p > 0 else None
+            nxt = A[idx][:, self.planes[p + 1]].tocsr() if p + 1 < len(self.planes) else None
+            self.nbrs.append((prv, nxt))
+
+    def _gs(self, x, b, order):
+        for p in order:
+            idx = self.planes[p]
+            rhs = b[idx].copy()
+            prv, nxt = self.nbrs[p]
+            if prv is not None:
+                rhs -= prv @ x[self.planes[p - 1]]
+            if nxt is not None:
+                rhs -= nxt @ x[self.planes[p + 1]]
+            x[idx] = sla.cho_solve(self.factors[p], rhs)
+        return x
+
+    def _jacobi(self, x, b):
+        r = b - self.A @ x
+        for p, idx in enumerate(self.planes):
+            x[idx] += self.omega * sla.cho_solve(self.factors[p], r[idx])
+        return x
+
+    def sweep(self, u, b, nu, forward: bool):
+        x = np.array(u, dtype=np.float64, copy=True)
+        order = range(len(self.planes)) if forward else range(len(self.planes) - 1, -1, -1)
+        for _ in range(nu):
+            x = self._gs(x, b, order) if self.omega == 1.0 else self._jacobi(x, b)
+        return x
+
+
+def default_smoother(problem) -> str:
+    """Plane smoothing when any term is anisotropic, damped Jacobi otherwise
+    (multigrid.py:183-188)."""
+    aniso = getattr(problem.spec, "aniso", ())
+    return "plane-jacobi" if any(len(set(a)) > 1 for a in aniso) else "jacobi"
+
+
 @dataclass
 class OracleMgContext:
     """Per-parameter V-cycle data (multigrid.py:116-129, 154-168)."""
@@ -70,6 +129,7 @@ class OracleMgContext:
     coarse_factor: tuple
     omega: float = JACOBI_OMEGA
     smoother: str = "jacobi"  # "jacobi" (isotropic default) or "gs" (multigrid.py:132-152)
+    planes: list | None = None  # PlaneSmoother per level ("plane-z" / "plane-jacobi")
 
     @property
     def levels(self):
@@ -86,7 +146,17 @@ def mg_context_for(problem, mu, nu: int = 1, omega: float = JACOBI_OMEGA,
         cf = sla.cho_factor(ops[0].toarray())
     except sla.LinAlgError as exc:
         raise OperatorError(f"coarsest operator not SPD: {exc}") from exc
+    if smoother == "auto":
+        smoother = default_smoother(problem)
     diags = [A.diagonal().copy() for A in ops]
+    if smoother in ("plane-z", "plane-jacobi"):
+        layers = getattr(problem, "layers_by_level", None)
+        if layers is None:
+            raise ValueError("plane smoothing needs per-level layer maps")
+        w = 1.0 if smoother == "plane-z" else PLANE_OMEGA
+        planes = [None] + [PlaneSmoother(ops[i], layers[i], w) for i in range(1, len(ops))]
+        return OracleMgContext(ops, list(problem.prolongations), diags, nu, cf, w, smoother,
+                               planes)
     for d in diags[1:]:
         if np.any(d == 0.0):
             raise ValueError("zero diagonal entry; point smoothing undefined")
@@ -104,6 +174,11 @@ def mg_vcycle(b, ctx: OracleMgContext, level=None) -> np.ndarray:
         return sla.cho_solve(ctx.coarse_factor, b)
     A, d = ctx.operators[level], ctx.diags[level]
     P = ctx.prolongations[level - 1]
+    if ctx.planes is not None:  # plane smoothers (multigrid.py:97-110, 219-222)
+        sm = ctx.planes[level]
+        u = sm.sweep(np.zeros_like(b), b, ctx.nu, True)
+        e = mg_vcycle(P.T @ (b - A @ u), ctx, level - 1)
+        return sm.sweep(u + P @ e, b, ctx.nu, False)
     u = np.zeros_like(b)
     for _ in range(ctx.nu):  # "gs": forward sweeps before, backward after (multigrid.py:137-138)
         u = jacobi_sweep(A, d, u, b, ctx.omega) if ctx.smoother == "jacobi" else gs_sweep(A, u, b, True)

@@ -6,6 +6,7 @@ Run in the build container (needs /root/reference; never on the GPU box):
     python tests/golden/make_golden.py --gs     # golden_gs.npz (Gauss-Seidel smoother)
     python tests/golden/make_golden.py --msrb   # golden_msrb.npz (rbi-msrbcg)
     python tests/golden/make_golden.py --fem    # golden_fem.npz (example-1, unmodified reference)
+    python tests/golden/make_golden.py --fem2   # golden_fem2.npz (example-2, unmodified reference)
 
 The reference (``/root/reference/pkg``) is copied to /tmp and its Cython
 smoother extension built in place (reference setup.py), so the reference's
@@ -367,7 +368,62 @@ def main_fem():
     print(f"wrote {dest} ({dest.stat().st_size/1e6:.2f} MB, {len(out)} arrays)")
 
 
+def main_fem2():
+    """The reference's example-2 (zero-flux face x = 1, anisotropic piecewise-constant
+    coefficient, mu-dependent source, plane smoothers) through its unmodified API ->
+    tests/golden/golden_fem2.npz: per-level operators, right-hand sides, V-cycles with
+    the plane-Jacobi (default) and plane-z smoothers, zero-init MGCG solves."""
+    rbws = _import_reference()
+    from rbws.grid import ParametricProblem
+    from rbws.multigrid import mg_context_for, mg_vcycle, mgcg_solve
+    from rbws.problems import get_problem
+
+    out = {}
+    spec = get_problem("example-2")
+    rng = np.random.default_rng(7)
+    mus = np.array([[0.1, 1.0, 0.5, 0.4, 0.6, 0.5, 0.25],
+                    [0.9, 0.2, 0.3, 0.55, 0.45, 0.42, 0.5],
+                    [0.5, 0.5, 1.0, 0.6, 0.4, 0.6, 0.33]])
+    for tag, levels, m0 in (("n8m2", 3, 2), ("n16m4", 3, 4)):
+        p = ParametricProblem(spec, levels=levels, m0=m0)
+        k = f"fem2_{tag}"
+        out[f"{k}_mus"] = mus
+        out[f"{k}_free"] = p.free_by_level[-1].astype(np.int64)
+        for lvl in range(p.mesh.levels):
+            A = p.operator(mus[0], level=lvl).tocsr()
+            A.sort_indices()
+            out[f"{k}_op{lvl}_data"] = A.data
+            out[f"{k}_op{lvl}_indices"] = A.indices.astype(np.int64)
+            out[f"{k}_op{lvl}_indptr"] = A.indptr.astype(np.int64)
+        out[f"{k}_rhs"] = np.array([p.rhs(m) for m in mus])
+        b = rng.standard_normal(p.n_free)
+        out[f"{k}_vcyc_b"] = b
+        for sm in ("plane-jacobi", "plane-z", "jacobi"):
+            ctx = mg_context_for(p, mus[0], smoother=sm if sm != "plane-jacobi" else "auto")
+            assert ctx.smoother_kind == sm
+            key = sm.replace("-", "")
+            out[f"{k}_vcyc_{key}"] = mg_vcycle(b, ctx)
+            xs, its, hists = [], [], []
+            for m in mus:
+                A, f = p.operator(m), p.rhs(m)
+                x, rep = mgcg_solve(A, f, np.zeros_like(f),
+                                    mg_context_for(p, m, smoother=sm), delta=1e-10, l_max=80)
+                xs.append(x)
+                its.append(rep.iterations)
+                hists.append(np.pad(rep.history, (0, 81 - len(rep.history)),
+                                    constant_values=np.nan))
+            out[f"{k}_{key}_x"] = np.array(xs)
+            out[f"{k}_{key}_iters"] = np.array(its)
+            out[f"{k}_{key}_hist"] = np.array(hists)
+    dest = REPO / "tests/golden/golden_fem2.npz"
+    np.savez_compressed(dest, **out)
+    print(f"wrote {dest} ({dest.stat().st_size/1e6:.2f} MB, {len(out)} arrays)")
+
+
 if __name__ == "__main__":
+    if "--fem2" in sys.argv:
+        main_fem2()
+        sys.exit(0)
     if "--fem" in sys.argv:
         main_fem()
         sys.exit(0)
