@@ -241,6 +241,39 @@ int rbws_slab_prolong_x(rbws_slab* s, const double* ec, void* stream);
 int rbws_slab_solve(rbws_slab* s, double delta, int l_max, int* iters, double* hist,
                     double* true_res, int* status, void* stream);
 
+/* ---- full-node ("FN") layout: assembled problems with free boundary nodes ----
+ * (reference example-2, problems.py:135-152: zero-flux face x = 1).  One instance
+ * = all (c+1)^3 nodes of a level (x fastest), Dirichlet nodes held at zero.  coef /
+ * coefA: 27-point full-node coefficients [27][(c+1)^3], A[X, X+o] with
+ * o = (dx+1) + 3(dy+1) + 9(dz+1); per term (coef, batch-shared) or per instance
+ * (coefA).  All pointers device, streams cudaStream_t. */
+/* coefA[i] = sum_q theta[i][q] coef[q] — ParametricProblem.operator, grid.py:246-255 */
+int rbws_fn_combine(int count, int nterms, int c, const double* theta, const double* coef,
+                    double* coefA, void* stream);
+/* mode 0: y = A x; mode 1: y = b - A x — A @ x in multigrid.py:218, kernels.py:98-115 */
+int rbws_fn_apply(int count, int c, const double* coefA, const double* x, const double* b,
+                  double* y, int mode, void* stream);
+/* doubles of the band factors: planar = 1 z-plane blocks (PlaneSmootherPair,
+ * multigrid.py:56-77: splu of A[plane, plane]), planar = 0 the whole level (coarsest
+ * factor, multigrid.py:154-168: cho_factor) */
+int64_t rbws_fn_band_doubles(int count, int c, int planar);
+/* build + banded Cholesky of every block (info[sys] = first bad pivot + 1, or 0) */
+int rbws_fn_band_factor(int count, int c, int planar, const double* coefA, double* band,
+                        int* info, void* stream);
+/* block solves of r (overwritten): mode 0 x = A_blk^-1 r, mode 1 x += omega A_blk^-1 r
+ * (plane-Jacobi sweep, multigrid.py:91-95; cho_solve, multigrid.py:216) */
+int rbws_fn_band_solve(int count, int c, int planar, const double* band, double* r, double* x,
+                       double omega, int mode, void* stream);
+/* b = P^T r (cc coarse cells; zero on coarse Dirichlet nodes) — grid.py:131-141 */
+int rbws_fn_restrict(int count, int cc, const double* r_fine, double* b_coarse,
+                     const unsigned char* coarse_mask, void* stream);
+/* u += P e on fine free nodes — multigrid.py:220 */
+int rbws_fn_prolong_add(int count, int cc, const double* e_coarse, double* u_fine,
+                        const unsigned char* fine_mask, void* stream);
+/* x += omega r / diag(A) on free nodes — damped point Jacobi, kernels.py:98-115 */
+int rbws_fn_point_jacobi(int count, int c, const double* coefA, const double* r, double* x,
+                         double omega, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -69,8 +69,18 @@ SIGNATURES = {
     "rbws_slab_store": [_vp, _c_int, _vp, _c_int64, _c_int, _vp],
     "rbws_slab_prolong_x": [_vp, _vp, _vp],
     "rbws_slab_solve": [_vp, _c_double, _c_int, _ip, _vp, _vp, _ip, _vp],
+    # full-node layout (csrc/planes.cu)
+    "rbws_fn_combine": [_c_int, _c_int, _c_int, _vp, _vp, _vp, _vp],
+    "rbws_fn_apply": [_c_int, _c_int, _vp, _vp, _vp, _vp, _c_int, _vp],
+    "rbws_fn_band_doubles": [_c_int, _c_int, _c_int],
+    "rbws_fn_band_factor": [_c_int, _c_int, _c_int, _vp, _vp, _vp, _vp],
+    "rbws_fn_band_solve": [_c_int, _c_int, _c_int, _vp, _vp, _vp, _c_double, _c_int, _vp],
+    "rbws_fn_restrict": [_c_int, _c_int, _vp, _vp, _vp, _vp],
+    "rbws_fn_prolong_add": [_c_int, _c_int, _vp, _vp, _vp, _vp],
+    "rbws_fn_point_jacobi": [_c_int, _c_int, _vp, _vp, _vp, _c_double, _vp],
 }
-_RESTYPES = {"rbws_last_error": ctypes.c_char_p, "rbws_launch_count": ctypes.c_int64}
+_RESTYPES = {"rbws_last_error": ctypes.c_char_p, "rbws_launch_count": ctypes.c_int64,
+             "rbws_fn_band_doubles": ctypes.c_int64}
 
 
 def launch_count() -> int:
