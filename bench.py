@@ -727,6 +727,169 @@ def run_fem(args, rank, world, dist):
         print(json.dumps(line), flush=True)
 
 
+FEM2_WORKLOAD = ("example-2 (the reference's mixed problem: zero-flux face x=1, anisotropic "
+                 "quadrant coefficient, mu-dependent source), {n}^3 cells, m0=4, zero-init MGCG "
+                 "with the plane-Jacobi smoother (reference default), batch {b}, tol 1e-10")
+
+
+def run_fem2(args, rank, world, dist):
+    """`--problem example-2`: HighFidelitySolver(method="mgcg") semantics (hf.py:40-57) on
+    the reference's example-2 in the full-node layout (csrc/planes.cu).  Step =
+    mg_context_for (theta-combined coefficients, banded Cholesky of every z-plane block and
+    of the coarsest level) + zero-init MGCG to 1e-10 for the batch, right-hand sides
+    resident (assembly excluded, experiment.py:31-33)."""
+    import torch
+
+    import build as _build
+    if rank == 0:
+        _build.build(verbose=False)
+    if dist is not None:
+        dist.barrier()
+    from paper_2311_13862_b200 import _native, fem
+    from paper_2311_13862_b200.fem_fn import FnFemProblem, _ptr, mg_context_for, mgcg_solve
+    from paper_2311_13862_b200.problems import levels_for, lhs_sample
+
+    n, m0 = args.fem_n, 4
+    batch = args.batch or 64
+    delta = 1e-10
+    spec = fem.example2()
+    levels = levels_for(n, m0)
+    t0 = time.perf_counter()
+    prob = FnFemProblem(spec, levels=levels, m0=m0)
+    t_setup = time.perf_counter() - t0
+    test = np.array(lhs_sample(spec.p, batch, spec.bounds, seed=2000 + rank))
+    F = prob.rhs(test)
+    state = {}
+
+    def step(f):
+        ctx = mg_context_for(prob, test)
+        x, reps = mgcg_solve(ctx, f, delta=delta, l_max=L_MAX)
+        state["reps"], state["ctx"] = reps, ctx
+        return x
+
+    for _ in range(args.warmup):
+        step(F)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    lc0 = _native.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step(F)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = _native.launch_count() - lc0
+    ms = ev0.elapsed_time(ev1)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = world * batch * args.steps / (ms_max / 1e3)
+    reps = state["reps"]
+    iters = [int(i) for i in reps.iterations]
+
+    # e2e: rhs batch from pinned host memory, free-DoF solutions back to pinned host memory
+    fh = F.cpu().pin_memory()
+    xh = torch.empty_like(fh).pin_memory()
+    fd = torch.empty_like(F)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        fd.copy_(fh, non_blocking=True)
+        x = step(fd)
+        xh.copy_(x, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = world * batch * args.steps / (float(e2e_ms.item()) / 1e3)
+
+    # roofline: the finest-level plane-block solve (one warp per plane system), timed alone;
+    # algorithmic bytes = the band factors (M (w+1) doubles per plane) + r read/write + x r/w
+    peak, peak_kind = peaks()
+    ctx = state["ctx"]
+    c = n
+    M, w = (c + 1) ** 2, c + 2
+    nsys = batch * (c + 1)
+    kbytes = nsys * M * (w + 1) * 8 + 4 * batch * (c + 1) ** 3 * 8
+    r = torch.randn(batch, (c + 1) ** 3, dtype=torch.float64, device="cuda")
+    xk = torch.zeros_like(r)
+    st = _native.stream_ptr()
+
+    def solve_once():
+        _native.call("rbws_fn_band_solve", batch, c, 1, _ptr(ctx.bands[-1]), _ptr(r), _ptr(xk),
+                     0.6, 1, st)
+
+    solve_once()
+    reps_k = 10
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0.record(stream)
+    for _ in range(reps_k):
+        solve_once()
+    k1.record(stream)
+    torch.cuda.synchronize()
+    k_ms = k0.elapsed_time(k1) / reps_k
+    achieved = kbytes / (k_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "band_solve_kernel (finest z-plane blocks, batch)",
+                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_kind,
+                "bytes_per_launch": int(kbytes), "ms_per_launch": round(k_ms, 4)}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = fem2_cpu_baseline(n, m0, test, iters, budget_s=args.cpu_budget)
+    line = {
+        "metric": "zero-init MGCG solves/s to 1e-10 rel. residual (example-2, plane-Jacobi)",
+        "value": round(value, 2), "unit": "solves/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded LHS parameters, sampling.py:8-27; no dataset)",
+        "config": {"workload": FEM2_WORKLOAD.format(n=n, b=batch),
+                   "batch_per_gpu": batch, "grid_cells": n, "levels": levels,
+                   "tolerance": delta, "smoother": "plane-jacobi(0.6), nu=1",
+                   "layout": "full-node (c+1)^3 per instance", "parallelism": f"parameter-sharded x{world}",
+                   "mean_iterations": round(float(np.mean(iters)), 3), "max_iterations": int(max(iters)),
+                   "all_converged": bool(np.all(reps.converged)),
+                   "t_setup_s": round(t_setup, 2), "l2": "inputs larger than L2"},
+        "e2e": {"value": round(e2e_value, 2), "unit": "solves/s",
+                "h2d_bytes_per_step": int(F.numel() * 8), "d2h_bytes_per_step": int(F.numel() * 8),
+                "api": "assembled rhs (pinned host) -> fem_fn.mgcg_solve -> pinned host solutions"},
+        "gpu_launches": int(launches), "roofline": roofline, "clocks": clocks.summary(),
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def fem2_cpu_baseline(n, m0, test, gpu_iters, budget_s=15.0):
+    """Oracle zero-init MGCG (plane-Jacobi, splu plane factors as the reference) on
+    example-2, single core, on a bounded sample of the batch's parameters."""
+    from oracle import fem as of
+    from oracle import solvers as so
+    from paper_2311_13862_b200.problems import levels_for
+    t0 = time.perf_counter()
+    op = of.OracleFemProblem(of.Example2(), levels=levels_for(n, m0), m0=m0)
+    t_asm = time.perf_counter() - t0
+    done, agree, t_solve = 0, 0, 0.0
+    for i, mu in enumerate(test):
+        t1 = time.perf_counter()
+        A, f = op.operator(mu), op.rhs(mu)
+        _, rep = so.mgcg_solve(A, f, np.zeros_like(f), so.mg_context_for(op, mu, smoother="auto"),
+                               delta=1e-10, l_max=L_MAX)
+        t_solve += time.perf_counter() - t1
+        done += 1
+        agree += int(rep.iterations == gpu_iters[i])
+        if t_solve > budget_s:
+            break
+    return {"value": round(done / t_solve, 4), "unit": "solves/s", "cores": 1, "kind": "port",
+            "sample": f"{done} of the step's parameters, oracle MGCG (operator + rhs + "
+                      f"mg_context_for incl. splu plane factors + MGCG) single-threaded; "
+                      f"assembly {t_asm:.1f}s excluded; iteration counts equal to the GPU: "
+                      f"{agree}/{done}"}
+
+
 def fem_cpu_baseline(spec, n, m0, model, test, gpu_iters, budget_s=15.0):
     """Oracle RBI-MGCG on example-1 (single core) on a bounded sample."""
     _single_thread_blas()
@@ -982,7 +1145,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-per-core", type=int, default=2)
     ap.add_argument("--problem", default="",
-                    help="reference problem id (example-1): RBI-MGCG on its assembled operator")
+                    help="reference problem id: example-1 (RBI-MGCG on its assembled operator) or "
+                         "example-2 (zero-init plane-Jacobi MGCG, full-node layout)")
     ap.add_argument("--fem-n", type=int, default=64)
     ap.add_argument("--fem-r", type=int, default=10)
     ap.add_argument("--fem-train", type=int, default=256)
@@ -1003,7 +1167,9 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    if args.problem:
+    if args.problem == "example-2":
+        run_fem2(args, rank, world, dist)
+    elif args.problem:
         run_fem(args, rank, world, dist)
     elif CONFIGS[args.config].get("slab"):
         run_slab(args, rank, world, dist)

@@ -14,6 +14,7 @@ from typing import Callable, Sequence
 import numpy as np
 import scipy.linalg as sla
 import scipy.sparse as sp
+import scipy.sparse.linalg as spla
 
 JACOBI_OMEGA = 0.7   # multigrid.py:27
 PLANE_OMEGA = 0.6    # multigrid.py:29 (damped plane-Jacobi of the anisotropic problem)
@@ -62,8 +63,7 @@ def gs_sweep(A, x, b, forward: bool = True):
 
 class PlaneSmoother:
     """z-plane block smoother (multigrid.py:48-110): plane blocks A[plane, plane] solved
-    exactly (here: dense Cholesky of each block, the reference uses sparse LU — the same
-    solve up to rounding), neighbour couplings only to the adjacent layers.  omega = 1:
+    exactly by sparse LU (scipy splu, as the reference), neighbour couplings only to the adjacent layers.  omega = 1:
     block Gauss-Seidel, ascending planes before / descending after the coarse correction
     ("plane-z"); omega < 1: damped block Jacobi x += omega A_pp^-1 (b - A x)_p
     ("plane-jacobi")."""
@@ -78,9 +78,9 @@ class PlaneSmoother:
         self.factors, self.nbrs = [], []
         for p, idx in enumerate(self.planes):
             try:
-                self.factors.append(sla.cho_factor(A[idx][:, idx].toarray()))
-            except sla.LinAlgError as exc:
-                raise OperatorError(f"plane block not SPD: {exc}") from exc
+                self.factors.append(spla.splu(A[idx][:, idx].tocsc()))
+            except RuntimeError as exc:
+                raise OperatorError(f"plane block singular: {exc}") from exc
             prv = A[idx][:, self.planes[p - 1]].tocsr() if p > 0 else None
             nxt = A[idx][:, self.planes[p + 1]].tocsr() if p + 1 < len(self.planes) else None
             self.nbrs.append((prv, nxt))
@@ -94,13 +94,13 @@ class PlaneSmoother:
                 rhs -= prv @ x[self.planes[p - 1]]
             if nxt is not None:
                 rhs -= nxt @ x[self.planes[p + 1]]
-            x[idx] = sla.cho_solve(self.factors[p], rhs)
+            x[idx] = self.factors[p].solve(rhs)
         return x
 
     def _jacobi(self, x, b):
         r = b - self.A @ x
         for p, idx in enumerate(self.planes):
-            x[idx] += self.omega * sla.cho_solve(self.factors[p], r[idx])
+            x[idx] += self.omega * self.factors[p].solve(r[idx])
         return x
 
     def sweep(self, u, b, nu, forward: bool):
