@@ -832,7 +832,7 @@ def run_fem2(args, rank, world, dist):
     torch.cuda.synchronize()
     k_ms = k0.elapsed_time(k1) / reps_k
     achieved = kbytes / (k_ms / 1e3) / 1e9
-    roofline = {"bound": "hbm", "kernel": "band_solve_kernel (finest z-plane blocks, batch)",
+    roofline = {"bound": "hbm", "kernel": "band_solve_sub_kernel (finest z-plane blocks, batch)",
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_kind,
                 "bytes_per_launch": int(kbytes), "ms_per_launch": round(k_ms, 4)}

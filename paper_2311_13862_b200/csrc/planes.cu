@@ -14,9 +14,14 @@
 #include "common.cuh"
 
 #include <cuda_runtime.h>
+#include <cstdlib>
+#include <type_traits>
 
 namespace rbws {
 namespace {
+
+// band row stride: w+1 entries padded to whole 32-byte sectors
+__host__ __device__ __forceinline__ int band_ws(int w) { return (w + 1 + 3) & ~3; }
 
 __device__ __forceinline__ void o27_split(int o, int& dx, int& dy, int& dz) {
   dx = o % 3 - 1;
@@ -65,7 +70,7 @@ __global__ void fn_apply_kernel(int count, int c, const double* __restrict__ coe
 
 // lower band of the plane blocks (planar = 1: systems = instances x planes, M = (c+1)^2,
 // w = c+2) or of the whole level (planar = 0: M = (c+1)^3, w = (c+1)^2 + c + 2):
-// band[(s*M + r)*(w+1) + d] = A[r, r-d]; Dirichlet rows -> identity rows
+// band[(s*M + r)*ws + d] = A[r, r-d] (ws = band_ws(w)); Dirichlet rows -> identity rows
 __global__ void fn_band_build_kernel(int count, int c, int planar, const double* __restrict__ coefA,
                                      double* __restrict__ band) {
   const int c1 = c + 1;
@@ -78,8 +83,9 @@ __global__ void fn_band_build_kernel(int count, int c, int planar, const double*
   const int ix = (int)(X % c1), iy = (int)((X / c1) % c1), iz = (int)(X / ((int64_t)c1 * c1));
   const int64_t s = planar ? (int64_t)i * c1 + iz : i;
   const int64_t r = planar ? X - (int64_t)iz * c1 * c1 : X;
-  double* row = band + (s * M + r) * (w + 1);
-  for (int d = 0; d <= w; ++d) row[d] = 0.0;
+  const int ws = band_ws(w);
+  double* row = band + (s * M + r) * ws;
+  for (int d = 0; d < ws; ++d) row[d] = 0.0;
   const double* ca = coefA + (int64_t)i * 27 * nodes + X;
   const double dg = ca[13 * nodes];
   if (dg == 0.0) {  // Dirichlet node: decoupled identity row
@@ -103,29 +109,30 @@ __global__ void band_factor_kernel(int64_t nsys, int64_t M, int w, double* __res
                                    int* __restrict__ info) {
   const int64_t s = blockIdx.x;
   if (s >= nsys) return;
-  double* B = band + s * M * (w + 1);
+  const int ws = band_ws(w);
+  double* B = band + s * M * ws;
   __shared__ double piv;
   __shared__ int bad;
   if (threadIdx.x == 0) bad = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int64_t j = 0; j < M; ++j) {
     if (threadIdx.x == 0) {
-      const double a = B[j * (w + 1)];
+      const double a = B[j * ws];
       if (!(a > 0.0) && !bad) bad = (int)(j + 1);
       piv = a > 0.0 ? sqrt(a) : 1.0;
-      B[j * (w + 1)] = piv;
+      B[j * ws] = piv;
     }
     __syncthreads();
     const double p = piv;
     for (int t = 1 + threadIdx.x; t <= w; t += blockDim.x)
-      if (j + t < M) B[(j + t) * (w + 1) + t] /= p;
+      if (j + t < M) B[(j + t) * ws + t] /= p;
     __syncthreads();
     // A[j+a][j+b] -= L[j+a][j] L[j+b][j], 1 <= b <= a <= w
     for (int a = 1 + warp; a <= w; a += nw) {
       if (j + a >= M) break;
-      const double la = B[(j + a) * (w + 1) + a];
+      const double la = B[(j + a) * ws + a];
       for (int bb = 1 + lane; bb <= a; bb += 32)
-        B[(j + a) * (w + 1) + (a - bb)] -= la * B[(j + bb) * (w + 1) + bb];
+        B[(j + a) * ws + (a - bb)] -= la * B[(j + bb) * ws + bb];
     }
     __syncthreads();
   }
@@ -149,11 +156,12 @@ __global__ void band_solve_kernel(int64_t nsys, int64_t M, int w, int ring,
   if (s >= nsys) return;
   double* zr = sring + warp * ring;
   const int rm = ring - 1;
-  const double* Ls = L + s * M * (w + 1);
+  const int ws = band_ws(w);
+  const double* Ls = L + s * M * ws;
   double* rs = r + s * M;
   double* xs = x + s * M;
   for (int64_t i = 0; i < M; ++i) {
-    const double* li = Ls + i * (w + 1);
+    const double* li = Ls + i * ws;
     double acc = 0.0;
     for (int d = 1 + lane; d <= w; d += 32)
       if (i - d >= 0) acc += li[d] * zr[(i - d) & rm];
@@ -169,15 +177,133 @@ __global__ void band_solve_kernel(int64_t nsys, int64_t M, int w, int ring,
   for (int64_t i = M - 1; i >= 0; --i) {
     double acc = 0.0;
     for (int d = 1 + lane; d <= w; d += 32)
-      if (i + d < M) acc += Ls[(i + d) * (w + 1) + d] * zr[(i + d) & rm];
+      if (i + d < M) acc += Ls[(i + d) * ws + d] * zr[(i + d) & rm];
     acc = warp_sum(acc);
-    const double z = (rs[i] - acc) / Ls[i * (w + 1)];
+    const double z = (rs[i] - acc) / Ls[i * ws];
     __syncwarp();
     if (lane == 0) {
       zr[i & rm] = z;
       xs[i] = mode == 0 ? z : xs[i] + omega * z;
     }
     __syncwarp();
+  }
+}
+
+// Sub-warp variant: LPS lanes per system (32/LPS systems per warp); lane j of a system
+// holds band entries d = j + LPS k (k < KPS) of a row.  The M-step chains are latency
+// bound and the row work is tiny (w FMAs), so nothing on the chain touches memory: the
+// window of the last w solution values lives in registers (slot d of the window on the
+// lane owning d) and moves one slot per step by shuffles, and the rows of the next PF
+// steps are loaded into registers ahead of the chain.  (A shared-memory window needs a
+// __syncwarp per step, whose memory-ordering semantics make every step wait for the
+// prefetch loads in flight: measured 1.4-1.9 us per step.)
+// Forward: row form, y_i = (r_i - sum_d L[i][i-d] y_{i-d}) / L_ii (log2(LPS)-level
+// reduction).  Backward: column form on ROWS of L (no strided column reads, no
+// reduction): z_i = p_0 / L_ii, p_d -= L[i][i-d] z_i, then the window shifts and entry
+// i-1-w enters it with its forward value.
+template <int LPS, int KPS, int PF>
+__global__ void __launch_bounds__(128) band_solve_sub_kernel(int64_t nsys, int64_t M, int w,
+                                                             const double* __restrict__ L,
+                                                             double* __restrict__ r,
+                                                             double* __restrict__ x, double omega,
+                                                             int mode) {
+  constexpr int SPW = 32 / LPS;  // systems per warp
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane / LPS, j = lane % LPS;
+  const int64_t s = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * SPW + g;
+  if (s >= nsys) return;  // whole groups only (a group = one system)
+  const unsigned gmask = (LPS == 32) ? 0xffffffffu : (((1u << LPS) - 1u) << (g * LPS));
+  const int W1 = band_ws(w);
+  const int jw = w % LPS, kw = w / LPS;  // owner of d = w
+  const double* Ls = L + s * M * W1;
+  double* rs = r + s * M;
+  double* xs = x + s * M;
+  double buf[PF][KPS], ga[PF], gb[PF];
+  double win[KPS];
+#pragma unroll
+  for (int k = 0; k < KPS; ++k) win[k] = 0.0;
+  auto load_row = [&](int64_t i, int u, bool fwd) {
+    const bool ok = i >= 0 && i < M;
+#pragma unroll
+    for (int k = 0; k < KPS; ++k) {
+      const int d = j + LPS * k;
+      buf[u][k] = (ok && d <= w) ? __ldcs(Ls + i * W1 + d) : 0.0;
+    }
+    if (fwd) {
+      ga[u] = (ok && j == 0) ? rs[i] : 0.0;
+    } else {  // y_{i-1-w}: enters the window after step i
+      ga[u] = (ok && j == jw && i - 1 - w >= 0) ? rs[i - 1 - w] : 0.0;
+      gb[u] = (ok && j == 0 && mode == 1) ? xs[i] : 0.0;
+    }
+  };
+  // ---- forward: L y = r; window slot d holds y_{i-d} (d >= 1)
+#pragma unroll
+  for (int u = 0; u < PF; ++u) load_row(u, u, true);
+  for (int64_t i0 = 0; i0 < M; i0 += PF) {
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const int64_t i = i0 + u;
+      if (i < M) {
+        double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < KPS; ++k) {
+          if (k & 1) acc1 = fma(buf[u][k], win[k], acc1);  // slot 0 and slots past w hold 0
+          else acc0 = fma(j == 0 && k == 0 ? 0.0 : buf[u][k], win[k], acc0);
+        }
+        double acc = acc0 + acc1;
+#pragma unroll
+        for (int o = LPS / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(gmask, acc, o, LPS);
+        const double y = (__shfl_sync(gmask, ga[u], 0, LPS) - acc) / __shfl_sync(gmask, buf[u][0], 0, LPS);
+        if (j == 0) rs[i] = y;
+        // shift: slot d+1 <- slot d, slot 1 <- y_i; slots past w drop out (zeroed)
+        double nw[KPS];
+#pragma unroll
+        for (int k = 0; k < KPS; ++k) {
+          const double up = __shfl_up_sync(gmask, win[k], 1, LPS);
+          const double wrap = __shfl_sync(gmask, k > 0 ? win[k - 1] : y, LPS - 1, LPS);
+          nw[k] = (j == 0) ? (k == 0 ? 0.0 : wrap) : up;
+        }
+        // lane 1 (or lane 0's next slot when LPS == 1) receives y_i into slot 1
+#pragma unroll
+        for (int k = 0; k < KPS; ++k) {
+          const int d = j + LPS * k;
+          win[k] = (d == 1) ? y : (d > w ? 0.0 : nw[k]);
+        }
+      }
+      load_row(i + PF, u, true);
+    }
+  }
+  __syncwarp(gmask);  // the forward values in rs are read back by other lanes below
+  // ---- backward: L^T z = y; window slot d holds the pending value of entry i-d
+#pragma unroll
+  for (int k = 0; k < KPS; ++k) {
+    const int d = j + LPS * k;
+    win[k] = (d <= w && M - 1 - d >= 0) ? rs[M - 1 - d] : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < PF; ++u) load_row(M - 1 - u, u, false);
+  for (int64_t i0 = M - 1; i0 >= 0; i0 -= PF) {
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const int64_t i = i0 - u;
+      if (i >= 0) {
+        const double z = __shfl_sync(gmask, win[0], 0, LPS) / __shfl_sync(gmask, buf[u][0], 0, LPS);
+        if (j == 0) xs[i] = mode == 0 ? z : gb[u] + omega * z;
+#pragma unroll
+        for (int k = 0; k < KPS; ++k) win[k] = fma(-buf[u][k], z, win[k]);  // (slot 0 unused after)
+        // shift: slot d <- slot d+1; slot w <- y_{i-1-w}
+        double nw[KPS];
+#pragma unroll
+        for (int k = 0; k < KPS; ++k) {
+          const double dn = __shfl_down_sync(gmask, win[k], 1, LPS);
+          const double wrap = __shfl_sync(gmask, k + 1 < KPS ? win[k + 1] : 0.0, 0, LPS);
+          nw[k] = (j == LPS - 1) ? wrap : dn;
+        }
+#pragma unroll
+        for (int k = 0; k < KPS; ++k) win[k] = (j == jw && k == kw) ? ga[u] : nw[k];
+      }
+      load_row(i - PF, u, false);
+    }
   }
 }
 
@@ -298,7 +424,7 @@ int64_t rbws_fn_band_doubles(int count, int c, int planar) {
   const int64_t c1 = c + 1;
   const int64_t nsys = planar ? count * c1 : count;
   const int64_t M = planar ? c1 * c1 : c1 * c1 * c1;
-  return nsys * M * (band_w(c, planar) + 1);
+  return nsys * M * band_ws(band_w(c, planar));
 }
 
 int rbws_fn_band_factor(int count, int c, int planar, const double* coefA, double* band,
@@ -327,6 +453,29 @@ int rbws_fn_band_solve(int count, int c, int planar, const double* band, double*
   while (ring < w + 1) ring *= 2;
   const int warps = 4;
   const size_t smem = (size_t)warps * ring * sizeof(double);
+  // sub-warp systems (LPS lanes each); RBWS_BAND_SOLVE_SIMPLE=1 for the warp-per-system
+  // kernel (A/B)
+  auto sub = [&](auto lps_c, auto kps_c) -> int {
+    constexpr int LPS = decltype(lps_c)::value, KPS = decltype(kps_c)::value;
+    constexpr int SPW = 32 / LPS;
+    const int64_t warps_needed = (nsys + SPW - 1) / SPW;
+    const unsigned nb = (unsigned)((warps_needed + 3) / 4);
+    band_solve_sub_kernel<LPS, KPS, 4><<<nb, 128, 0, St(stream)>>>(nsys, M, w, band, r, x, omega,
+                                                                    mode);
+    FN_LAUNCHED();
+    return 0;
+  };
+  // lanes per system: RBWS_BAND_LPS (8 / 16 / 32) for A/B
+  static const int lps = getenv("RBWS_BAND_LPS") ? atoi(getenv("RBWS_BAND_LPS")) : 16;
+  using std::integral_constant;
+#define RBWS_SUB(L_, K_) \
+  if (lps == L_ && w + 1 <= L_ * K_) return sub(integral_constant<int, L_>{}, integral_constant<int, K_>{});
+  if (!getenv("RBWS_BAND_SOLVE_SIMPLE")) {
+    RBWS_SUB(8, 1) RBWS_SUB(8, 2) RBWS_SUB(8, 3) RBWS_SUB(8, 5) RBWS_SUB(8, 9) RBWS_SUB(8, 17)
+    RBWS_SUB(16, 1) RBWS_SUB(16, 2) RBWS_SUB(16, 3) RBWS_SUB(16, 5) RBWS_SUB(16, 9)
+    RBWS_SUB(32, 1) RBWS_SUB(32, 2) RBWS_SUB(32, 3) RBWS_SUB(32, 5) RBWS_SUB(32, 9)
+  }
+#undef RBWS_SUB
   if (smem > 48 * 1024) {
     RBWS_CUDA_CHECK(cudaFuncSetAttribute(band_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
