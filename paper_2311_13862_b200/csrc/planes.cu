@@ -104,7 +104,8 @@ __global__ void fn_band_build_kernel(int count, int c, int planar, const double*
 }
 
 // banded Cholesky in place, one CTA per system (right-looking, column j's trailing
-// (w x w) triangle updated in parallel); info[s] = 0 or the first non-positive pivot + 1
+// (w x w) triangle updated in parallel); the diagonal slot of row j ends as 1 / L_jj;
+// info[s] = 0 or the first non-positive pivot + 1
 __global__ void band_factor_kernel(int64_t nsys, int64_t M, int w, double* __restrict__ band,
                                    int* __restrict__ info) {
   const int64_t s = blockIdx.x;
@@ -126,6 +127,8 @@ __global__ void band_factor_kernel(int64_t nsys, int64_t M, int w, double* __res
     const double p = piv;
     for (int t = 1 + threadIdx.x; t <= w; t += blockDim.x)
       if (j + t < M) B[(j + t) * ws + t] /= p;
+    // the diagonal slot keeps 1 / L_jj: the solves multiply (no division on their chains)
+    if (threadIdx.x == 0) B[j * ws] = 1.0 / p;
     __syncthreads();
     // A[j+a][j+b] -= L[j+a][j] L[j+b][j], 1 <= b <= a <= w
     for (int a = 1 + warp; a <= w; a += nw) {
@@ -166,7 +169,7 @@ __global__ void band_solve_kernel(int64_t nsys, int64_t M, int w, int ring,
     for (int d = 1 + lane; d <= w; d += 32)
       if (i - d >= 0) acc += li[d] * zr[(i - d) & rm];
     acc = warp_sum(acc);
-    const double y = (rs[i] - acc) / li[0];
+    const double y = (rs[i] - acc) * li[0];
     __syncwarp();
     if (lane == 0) {
       zr[i & rm] = y;
@@ -179,7 +182,7 @@ __global__ void band_solve_kernel(int64_t nsys, int64_t M, int w, int ring,
     for (int d = 1 + lane; d <= w; d += 32)
       if (i + d < M) acc += Ls[(i + d) * ws + d] * zr[(i + d) & rm];
     acc = warp_sum(acc);
-    const double z = (rs[i] - acc) / Ls[i * ws];
+    const double z = (rs[i] - acc) * Ls[i * ws];
     __syncwarp();
     if (lane == 0) {
       zr[i & rm] = z;
@@ -253,7 +256,7 @@ __global__ void __launch_bounds__(128) band_solve_sub_kernel(int64_t nsys, int64
         double acc = acc0 + acc1;
 #pragma unroll
         for (int o = LPS / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(gmask, acc, o, LPS);
-        const double y = (__shfl_sync(gmask, ga[u], 0, LPS) - acc) / __shfl_sync(gmask, buf[u][0], 0, LPS);
+        const double y = (__shfl_sync(gmask, ga[u], 0, LPS) - acc) * __shfl_sync(gmask, buf[u][0], 0, LPS);
         if (j == 0) rs[i] = y;
         // shift: slot d+1 <- slot d, slot 1 <- y_i; slots past w drop out (zeroed)
         double nw[KPS];
@@ -287,7 +290,7 @@ __global__ void __launch_bounds__(128) band_solve_sub_kernel(int64_t nsys, int64
     for (int u = 0; u < PF; ++u) {
       const int64_t i = i0 - u;
       if (i >= 0) {
-        const double z = __shfl_sync(gmask, win[0], 0, LPS) / __shfl_sync(gmask, buf[u][0], 0, LPS);
+        const double z = __shfl_sync(gmask, win[0], 0, LPS) * __shfl_sync(gmask, buf[u][0], 0, LPS);
         if (j == 0) xs[i] = mode == 0 ? z : gb[u] + omega * z;
 #pragma unroll
         for (int k = 0; k < KPS; ++k) win[k] = fma(-buf[u][k], z, win[k]);  // (slot 0 unused after)
