@@ -18,8 +18,9 @@ Galerkin triple products go through scipy.
 
 Scope: Dirichlet problems (free DoFs = interior nodes, the padded layout of
 the separable path).  ``example-2``'s zero-flux face keeps boundary nodes free
-and its default smoother is the plane-block Jacobi of multigrid.py:48-110;
-neither is on the B200 path yet (NotImplementedError).
+and its default smoother is the plane-block Jacobi of multigrid.py:48-110: it
+runs on the full-node path (``fem_fn.py``), to which ``ParametricProblem``
+dispatches; ``FemProblem`` itself refuses it (NotImplementedError).
 """
 
 from __future__ import annotations

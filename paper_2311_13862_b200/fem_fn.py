@@ -140,6 +140,14 @@ class FnFemProblem:
     def levels(self) -> int:
         return len(self.cells)
 
+    @property
+    def handle(self):
+        """No native hierarchy: the padded-layout entry points (batches, RBI warm starts,
+        L1ROC, HostPipeline) do not take full-node problems yet."""
+        raise NotImplementedError(
+            f"{self.spec.pid}: only mg_context_for / mg_vcycle / mgcg_solve are on the "
+            "full-node B200 path (RBI-MGCG on it is a next step, DESIGN.md §5d)")
+
     def nodes(self, level=None) -> int:
         c = self.cells[-1 if level is None else level]
         return (c + 1) ** 3

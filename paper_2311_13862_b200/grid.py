@@ -68,6 +68,9 @@ class ParametricProblem:
 
     def __new__(cls, spec, levels: int = 3, m0: int = 2):
         if getattr(spec, "kind", None) == "fem":  # assembled problems (fem.py)
+            if spec.neumann_face_x1:  # free boundary nodes: full-node layout (fem_fn.py)
+                from .fem_fn import FnFemProblem
+                return FnFemProblem(spec, levels, m0)
             from .fem import FemProblem
             return FemProblem(spec, levels, m0)
         return super().__new__(cls)

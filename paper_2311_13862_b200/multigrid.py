@@ -104,6 +104,9 @@ def mg_context_for(problem: ParametricProblem, mus, nu: int = 1, smoother: str =
 def mg_vcycle(b, ctx: MgContext, level=None):
     """One V-cycle from zero for every instance of the batch (multigrid.py:205-222)."""
     import torch
+    from .fem_fn import FnMgContext
+    if isinstance(ctx, FnMgContext):
+        return ctx.vcycle(b, level)
     if level is not None and level != ctx.levels - 1:
         raise ValueError("the batched V-cycle is entered on the finest level")
     n = ctx.problem.n
@@ -122,8 +125,13 @@ def mgcg_solve(A, f, x0, ctx: MgContext, delta: float = 1e-16, l_max: int = 40, 
     f: padded rhs, either one instance (shared) or a full batch; x0: padded
     batch of initial guesses (None = zeros), left untouched unless
     ``overwrite_x0`` (then the solve runs in x0's storage).  Returns (x, [SolveReport]).
+    Full-node contexts (example-2): f / x0 are (count, (n+1)^3) full-node batches.
     """
     import torch
+    from .fem_fn import FnMgContext
+    if isinstance(ctx, FnMgContext):
+        from . import fem_fn
+        return fem_fn.mgcg_solve(ctx, f, x0, delta=delta, l_max=l_max, method=method)
     if delta <= 0:
         raise ValueError("tolerance must be positive")
     if l_max < 0:

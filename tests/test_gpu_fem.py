@@ -137,10 +137,19 @@ def test_fem_term_apply_and_streaming(probs):
     assert torch.equal(x2, x)
 
 
-def test_fem_example2_is_refused():
+def test_fem_example2_goes_to_the_full_node_path():
+    """The padded stored-coefficient path refuses free boundary nodes; the factory sends
+    example-2 to the full-node path (fem_fn.py, tests/test_gpu_fem_fn.py), whose
+    unsupported calls (RBI warm starts, native batches) fail loudly."""
     pkg = _pkg()
+    from paper_2311_13862_b200.fem import FemProblem
+    from paper_2311_13862_b200.fem_fn import FnFemProblem
     with pytest.raises(NotImplementedError):
-        pkg.ParametricProblem(pkg.get_problem("example-2"), levels=3, m0=2)
+        FemProblem(pkg.get_problem("example-2"), levels=3, m0=2)
+    p = pkg.ParametricProblem(pkg.get_problem("example-2"), levels=3, m0=2)
+    assert isinstance(p, FnFemProblem)
+    with pytest.raises(NotImplementedError):
+        p.handle
 
 
 def test_fem_l1roc_rbi_mgcg_matches_reference(probs):

@@ -167,3 +167,20 @@ def test_larger_grid_against_oracle():
                                 delta=1e-10, l_max=80)
         assert reps.iterations[i] == rep.iterations
         assert _rel(xs[i], xo) <= 1e-9
+
+
+def test_reference_api_dispatch():
+    """A reference user's calls (ParametricProblem / mg_context_for / mgcg_solve) reach the
+    full-node path for example-2 and give the reference's iteration counts."""
+    import paper_2311_13862_b200 as rb
+    from paper_2311_13862_b200.fem_fn import FnFemProblem
+    k = "fem2_n16m4"
+    prob = rb.ParametricProblem(rb.get_problem("example-2"), levels=3, m0=4)
+    assert isinstance(prob, FnFemProblem)
+    mus = G[f"{k}_mus"]
+    ctx = rb.mg_context_for(prob, mus)
+    assert ctx.smoother == "plane-jacobi"
+    x, reps = rb.mgcg_solve(None, prob.rhs(mus), None, ctx, delta=1e-10, l_max=80)
+    np.testing.assert_array_equal([r.iterations for r in reps], G[f"{k}_planejacobi_iters"])
+    v = prob.from_full(rb.mg_vcycle(prob.to_full(G[f"{k}_vcyc_b"][None].repeat(3, 0)), ctx))
+    assert _rel(v[0], G[f"{k}_vcyc_planejacobi"]) <= 1e-12
