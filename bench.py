@@ -806,14 +806,16 @@ def run_fem2(args, rank, world, dist):
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_value = world * batch * args.steps / (float(e2e_ms.item()) / 1e3)
 
-    # roofline: the finest-level plane-block solve (one warp per plane system), timed alone;
-    # algorithmic bytes = the band factors (M (w+1) doubles per plane) + r read/write + x r/w
+    # roofline: the finest-level plane-block solve (16 lanes per plane system), timed alone;
+    # algorithmic bytes = the band factors (M (w+1) doubles per plane) read by BOTH the
+    # forward and the backward substitution (a 2.3 MB factor per plane does not stay on
+    # chip between the passes) + r read/write/read-back + x read/write
     peak, peak_kind = peaks()
     ctx = state["ctx"]
     c = n
     M, w = (c + 1) ** 2, c + 2
     nsys = batch * (c + 1)
-    kbytes = nsys * M * (w + 1) * 8 + 4 * batch * (c + 1) ** 3 * 8
+    kbytes = 2 * nsys * M * (w + 1) * 8 + 5 * batch * (c + 1) ** 3 * 8
     r = torch.randn(batch, (c + 1) ** 3, dtype=torch.float64, device="cuda")
     xk = torch.zeros_like(r)
     st = _native.stream_ptr()
@@ -832,9 +834,14 @@ def run_fem2(args, rank, world, dist):
     torch.cuda.synchronize()
     k_ms = k0.elapsed_time(k1) / reps_k
     achieved = kbytes / (k_ms / 1e3) / 1e9
+    # DRAM bytes of one such launch from the ncu --set full capture (64^3, 64 instances)
+    traffic = 19_569_175_000 + 241_493_248 if (n, batch) == (64, 64) else None
     roofline = {"bound": "hbm", "kernel": "band_solve_sub_kernel (finest z-plane blocks, batch)",
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_kind,
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "traffic_source": "profiles/r01i_example2.md (ncu --set full, one finest sweep, "
+                                  "64^3 x 64; dram/algorithmic = 1.01)",
+                "peak_source": peak_kind,
                 "bytes_per_launch": int(kbytes), "ms_per_launch": round(k_ms, 4)}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -142,6 +142,62 @@ __global__ void band_factor_kernel(int64_t nsys, int64_t M, int w, double* __res
   if (threadIdx.x == 0) info[s] = bad;
 }
 
+// The same factorization with the active (w+1)-row window in shared memory (row r in
+// slot r mod (w+1)): the per-step read-modify-write of the trailing triangle stays on
+// chip (in global memory every step wrote ~w^2/2 doubles through to L2); row j leaves
+// for HBM when final, row j+w+1 enters from the assembled band just before its first
+// update.
+__global__ void __launch_bounds__(256) band_factor_smem_kernel(int64_t nsys, int64_t M, int w,
+                                                               double* __restrict__ band,
+                                                               int* __restrict__ info) {
+  extern __shared__ double wnd[];
+  const int64_t s = blockIdx.x;
+  if (s >= nsys) return;
+  const int ws = band_ws(w), W1 = w + 1;
+  double* B = band + s * M * ws;
+  __shared__ double piv;
+  __shared__ int bad;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) bad = 0;
+  for (int t = threadIdx.x; t < W1 * ws; t += blockDim.x) {
+    const int row = t / ws;
+    wnd[t] = row < M ? B[(int64_t)row * ws + t % ws] : 0.0;
+  }
+  __syncthreads();
+  int jm = 0;  // j mod (w+1): rows j..j+w live in slots jm, jm+1, ... (wrapping)
+  auto rowp = [&](int x) {  // row j + x, 0 <= x <= w
+    const int t = jm + x;
+    return wnd + (t >= W1 ? t - W1 : t) * ws;
+  };
+  for (int64_t j = 0; j < M; ++j) {
+    double* rj = rowp(0);
+    if (threadIdx.x == 0) {
+      const double a = rj[0];
+      if (!(a > 0.0) && !bad) bad = (int)(j + 1);
+      piv = a > 0.0 ? sqrt(a) : 1.0;
+    }
+    __syncthreads();
+    const double p = piv;
+    for (int t = 1 + threadIdx.x; t <= w; t += blockDim.x)
+      if (j + t < M) rowp(t)[t] /= p;
+    __syncthreads();
+    for (int a = 1 + warp; a <= w; a += nw) {
+      if (j + a >= M) break;
+      double* ra = rowp(a);
+      const double la = ra[a];
+      for (int bb = 1 + lane; bb <= a; bb += 32) ra[a - bb] -= la * rowp(bb)[bb];
+    }
+    // row j is final: out to HBM (diagonal slot = 1 / L_jj), row j+w+1 in
+    for (int t = threadIdx.x; t < ws; t += blockDim.x) B[j * ws + t] = t == 0 ? 1.0 / p : rj[t];
+    __syncthreads();
+    if (j + W1 < M)
+      for (int t = threadIdx.x; t < ws; t += blockDim.x) rj[t] = B[(j + W1) * ws + t];
+    jm = (jm + 1 == W1) ? 0 : jm + 1;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) info[s] = bad;
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -439,7 +495,19 @@ int rbws_fn_band_factor(int count, int c, int planar, const double* coefA, doubl
   const int64_t M = planar ? c1 * c1 : nodes;
   fn_band_build_kernel<<<grid_of(nodes, count), 256, 0, St(stream)>>>(count, c, planar, coefA, band);
   FN_LAUNCHED();
-  band_factor_kernel<<<(unsigned)nsys, 256, 0, St(stream)>>>(nsys, M, band_w(c, planar), band, info);
+  const int w = band_w(c, planar);
+  const size_t wsm = (size_t)(w + 1) * band_ws(w) * sizeof(double);
+  if (wsm <= 200 * 1024 && !getenv("RBWS_BAND_FACTOR_GLOBAL")) {
+    static size_t attr = 48 * 1024;
+    if (wsm > attr) {
+      RBWS_CUDA_CHECK(cudaFuncSetAttribute(band_factor_smem_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+      attr = wsm;
+    }
+    band_factor_smem_kernel<<<(unsigned)nsys, 256, wsm, St(stream)>>>(nsys, M, w, band, info);
+  } else {
+    band_factor_kernel<<<(unsigned)nsys, 256, 0, St(stream)>>>(nsys, M, w, band, info);
+  }
   FN_LAUNCHED();
   return 0;
 }

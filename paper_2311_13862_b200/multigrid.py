@@ -88,8 +88,14 @@ def mg_context_for(problem: ParametricProblem, mus, nu: int = 1, smoother: str =
     """Batched mg_context_for (multigrid.py:191-202).
 
     ``mus``: one parameter or an array (count, p).  Pass an existing ``ctx``
-    to reuse its device buffers for a new batch.
+    to reuse its device buffers for a new batch.  Problems with free boundary nodes
+    (example-2) get a full-node context (fem_fn.py; smoothers "auto" = plane-Jacobi,
+    "plane-jacobi", "jacobi").
     """
+    from .fem_fn import FnFemProblem
+    if isinstance(problem, FnFemProblem):
+        from . import fem_fn
+        return fem_fn.mg_context_for(problem, mus, nu=nu, smoother=smoother)
     if smoother == "auto":  # isotropic problems: damped Jacobi (multigrid.py:183-188)
         smoother = "jacobi"
     if smoother not in SMOOTHERS:
