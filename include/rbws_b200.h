@@ -253,6 +253,10 @@ int rbws_fn_combine(int count, int nterms, int c, const double* theta, const dou
 /* mode 0: y = A x; mode 1: y = b - A x — A @ x in multigrid.py:218, kernels.py:98-115 */
 int rbws_fn_apply(int count, int c, const double* coefA, const double* x, const double* b,
                   double* y, int mode, void* stream);
+/* the same from the batch-shared per-term coef [Q][27][(c+1)^3] and theta [count][Q]
+ * (no per-instance copy; bitwise rbws_fn_apply's result) */
+int rbws_fn_apply_shared(int count, int nterms, int c, const double* theta, const double* coef,
+                         const double* x, const double* b, double* y, int mode, void* stream);
 /* doubles of the band factors: planar = 1 z-plane blocks (PlaneSmootherPair,
  * multigrid.py:56-77: splu of A[plane, plane]), planar = 0 the whole level (coarsest
  * factor, multigrid.py:154-168: cho_factor) */

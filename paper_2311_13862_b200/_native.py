@@ -72,6 +72,7 @@ SIGNATURES = {
     # full-node layout (csrc/planes.cu)
     "rbws_fn_combine": [_c_int, _c_int, _c_int, _vp, _vp, _vp, _vp],
     "rbws_fn_apply": [_c_int, _c_int, _vp, _vp, _vp, _vp, _c_int, _vp],
+    "rbws_fn_apply_shared": [_c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _c_int, _vp],
     "rbws_fn_band_doubles": [_c_int, _c_int, _c_int],
     "rbws_fn_band_factor": [_c_int, _c_int, _c_int, _vp, _vp, _vp, _vp],
     "rbws_fn_band_solve": [_c_int, _c_int, _c_int, _vp, _vp, _vp, _c_double, _c_int, _vp],

@@ -68,6 +68,65 @@ __global__ void fn_apply_kernel(int count, int c, const double* __restrict__ coe
   y[g] = mode == 0 ? s : __dsub_rn(b[g], s);
 }
 
+// The same apply from the batch-shared per-term coefficients (no per-instance copy):
+// each thread serves node X for IPT instances, combining theta_q coef_q[o][X] on the fly
+// in the combine kernel's order and rounding, so the result is bitwise fn_apply_kernel's.
+// Instance groups are the fastest grid dimension: the CTAs resident together work on the
+// same nodes and the term coefficients come from L2.
+template <int IPT>
+__global__ void __launch_bounds__(256) fn_apply_shared_kernel(int count, int Q, int c,
+                                                              const double* __restrict__ theta,
+                                                              const double* __restrict__ coef,
+                                                              const double* __restrict__ x,
+                                                              const double* __restrict__ b,
+                                                              double* __restrict__ y, int mode) {
+  const int c1 = c + 1;
+  const int64_t nodes = (int64_t)c1 * c1 * c1;
+  const int groups = (count + IPT - 1) / IPT;
+  const int grp = blockIdx.x % groups;
+  const int64_t X = (int64_t)(blockIdx.x / groups) * blockDim.x + threadIdx.x;
+  if (X >= nodes) return;
+  const int i0 = grp * IPT;
+  const int ix = (int)(X % c1), iy = (int)((X / c1) % c1), iz = (int)(X / ((int64_t)c1 * c1));
+  double th[IPT][kMaxTerms];
+#pragma unroll
+  for (int u = 0; u < IPT; ++u)
+#pragma unroll
+    for (int q = 0; q < kMaxTerms; ++q)
+      th[u][q] = (q < Q && i0 + u < count) ? theta[(i0 + u) * Q + q] : 0.0;
+  double sacc[IPT];
+#pragma unroll
+  for (int u = 0; u < IPT; ++u) sacc[u] = 0.0;
+  const int64_t per = 27 * nodes;
+#pragma unroll 3
+  for (int o = 0; o < 27; ++o) {
+    int dx, dy, dz;
+    o27_split(o, dx, dy, dz);
+    const int jx = ix + dx, jy = iy + dy, jz = iz + dz;
+    if (jx < 0 || jx > c || jy < 0 || jy > c || jz < 0 || jz > c) continue;
+    const int64_t off = X + dx + (int64_t)c1 * (dy + (int64_t)c1 * dz);
+    double cq[kMaxTerms];
+#pragma unroll
+    for (int q = 0; q < kMaxTerms; ++q) cq[q] = q < Q ? coef[q * per + o * nodes + X] : 0.0;
+#pragma unroll
+    for (int u = 0; u < IPT; ++u) {
+      if (i0 + u >= count) break;
+      double a = __dmul_rn(th[u][0], cq[0]);
+#pragma unroll
+      for (int q = 1; q < kMaxTerms; ++q)
+        if (q < Q) a = __dadd_rn(a, __dmul_rn(th[u][q], cq[q]));
+      if (a != 0.0)
+        sacc[u] = __dadd_rn(sacc[u], __dmul_rn(a, x[(int64_t)(i0 + u) * nodes + off]));
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < IPT; ++u) {
+    if (i0 + u >= count) break;
+    const int64_t g = (int64_t)(i0 + u) * nodes + X;
+    y[g] = mode == 0 ? sacc[u] : __dsub_rn(b[g], sacc[u]);
+  }
+}
+
 // lower band of the plane blocks (planar = 1: systems = instances x planes, M = (c+1)^2,
 // w = c+2) or of the whole level (planar = 0: M = (c+1)^3, w = (c+1)^2 + c + 2):
 // band[(s*M + r)*ws + d] = A[r, r-d] (ws = band_ws(w)); Dirichlet rows -> identity rows
@@ -475,6 +534,21 @@ int rbws_fn_apply(int count, int c, const double* coefA, const double* x, const 
     return rbws_set_error("rbws_fn_apply: bad argument", __FILE__, __LINE__);
   const int64_t nodes = (int64_t)(c + 1) * (c + 1) * (c + 1);
   fn_apply_kernel<<<grid_of(nodes, count), 256, 0, St(stream)>>>(count, c, coefA, x, b, y, mode);
+  FN_LAUNCHED();
+  return 0;
+}
+
+int rbws_fn_apply_shared(int count, int nterms, int c, const double* theta, const double* coef,
+                         const double* x, const double* b, double* y, int mode, void* stream) {
+  if (count <= 0 || nterms <= 0 || nterms > kMaxTerms || c < 1 || !theta || !coef || !x || !y ||
+      (mode == 1 && !b) || mode < 0 || mode > 1)
+    return rbws_set_error("rbws_fn_apply_shared: bad argument", __FILE__, __LINE__);
+  const int64_t nodes = (int64_t)(c + 1) * (c + 1) * (c + 1);
+  constexpr int IPT = 4;
+  const int64_t groups = (count + IPT - 1) / IPT;
+  const int64_t blocks = ((nodes + 255) / 256) * groups;
+  fn_apply_shared_kernel<IPT><<<(unsigned)blocks, 256, 0, St(stream)>>>(count, nterms, c, theta, coef,
+                                                                      x, b, y, mode);
   FN_LAUNCHED();
   return 0;
 }

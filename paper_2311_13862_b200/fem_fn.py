@@ -222,6 +222,11 @@ class FnMgContext:
         self.mus = mus
         theta = torch.as_tensor(problem.spec.thetas(mus), dtype=torch.float64, device="cuda")
         Q = theta.shape[1]
+        self.theta = theta
+        import os
+        # batch-shared finest apply: bitwise equal but measured slower at 64^3 x 64
+        # (139.6 vs 158.2 solves/s, profiles/r01i_example2.md) -> opt-in RBWS_FN_SHARED=1
+        self.shared_finest = Q <= 8 and os.environ.get("RBWS_FN_SHARED", "0") == "1"
         st = _native.stream_ptr()
         self.coefA, self.bands = [], []
         bad = []
@@ -256,9 +261,17 @@ class FnMgContext:
         import torch
         level = self.levels - 1 if level is None else level
         y = torch.empty_like(x) if out is None else out
-        _native.call("rbws_fn_apply", self.count, self.problem.cells[level],
-                     _ptr(self.coefA[level]), _ptr(x), _ptr(b) if b is not None else None,
-                     _ptr(y), 0 if b is None else 1, _native.stream_ptr())
+        bp = _ptr(b) if b is not None else None
+        mode = 0 if b is None else 1
+        if level == self.levels - 1 and self.shared_finest:
+            # finest level: batch-shared term coefficients combined on the fly (bitwise the
+            # per-instance apply; 16 B/node + the shared terms instead of 232 B/node)
+            _native.call("rbws_fn_apply_shared", self.count, self.theta.shape[1],
+                         self.problem.cells[level], _ptr(self.theta), _ptr(self.problem._coef[level]),
+                         _ptr(x), bp, _ptr(y), mode, _native.stream_ptr())
+        else:
+            _native.call("rbws_fn_apply", self.count, self.problem.cells[level],
+                         _ptr(self.coefA[level]), _ptr(x), bp, _ptr(y), mode, _native.stream_ptr())
         return y
 
     def _smooth(self, level, u, b):

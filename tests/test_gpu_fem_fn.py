@@ -184,3 +184,28 @@ def test_reference_api_dispatch():
     np.testing.assert_array_equal([r.iterations for r in reps], G[f"{k}_planejacobi_iters"])
     v = prob.from_full(rb.mg_vcycle(prob.to_full(G[f"{k}_vcyc_b"][None].repeat(3, 0)), ctx))
     assert _rel(v[0], G[f"{k}_vcyc_planejacobi"]) <= 1e-12
+
+
+def test_shared_apply_is_bitwise_the_per_instance_apply(case):
+    """rbws_fn_apply_shared (batch-shared term coefficients combined on the fly, the finest
+    level's apply) equals rbws_fn_apply over the combined per-instance coefficients bit for
+    bit, for a batch size that is not a multiple of the 4 instances per thread."""
+    from paper_2311_13862_b200 import _native
+    from paper_2311_13862_b200.fem_fn import _ptr, mg_context_for
+    k, p = case
+    b = p.spec.bounds
+    rng = np.random.default_rng(4)
+    mus = b[:, 0] + rng.random((7, 7)) * (b[:, 1] - b[:, 0])
+    ctx = mg_context_for(p, mus, smoother="jacobi")
+    lvl = p.levels - 1
+    x = p.to_full(rng.standard_normal((7, p.n_free)))
+    f = p.to_full(rng.standard_normal((7, p.n_free)))
+    st = _native.stream_ptr()
+    for mode, bb in ((0, None), (1, f)):
+        y1, y2 = torch.empty_like(x), torch.empty_like(x)
+        _native.call("rbws_fn_apply", 7, p.n, _ptr(ctx.coefA[lvl]), _ptr(x),
+                     _ptr(bb) if bb is not None else None, _ptr(y1), mode, st)
+        _native.call("rbws_fn_apply_shared", 7, ctx.theta.shape[1], p.n, _ptr(ctx.theta),
+                     _ptr(p._coef[lvl]), _ptr(x), _ptr(bb) if bb is not None else None, _ptr(y2),
+                     mode, st)
+        assert torch.equal(y1, y2)
