@@ -268,6 +268,12 @@ int rbws_fn_band_factor(int count, int c, int planar, const double* coefA, doubl
  * (plane-Jacobi sweep, multigrid.py:91-95; cho_solve, multigrid.py:216) */
 int rbws_fn_band_solve(int count, int c, int planar, const double* band, double* r, double* x,
                        double omega, int mode, void* stream);
+/* one block Gauss-Seidel sweep over the z-planes of x (ascending if forward, else
+ * descending): x_p = A_pp^-1 (b_p - A[p,p-1] x_{p-1} - A[p,p+1] x_{p+1}) with the plane
+ * factors of rbws_fn_band_factor(planar = 1); scratch >= count (c+1)^2 doubles —
+ * PlaneSmootherPair._sweep (multigrid.py:79-89), smoother "plane-z" */
+int rbws_fn_plane_gs_sweep(int count, int c, const double* coefA, const double* band,
+                           const double* b, double* x, double* scratch, int forward, void* stream);
 /* b = P^T r (cc coarse cells; zero on coarse Dirichlet nodes) — grid.py:131-141 */
 int rbws_fn_restrict(int count, int cc, const double* r_fine, double* b_coarse,
                      const unsigned char* coarse_mask, void* stream);

@@ -127,6 +127,37 @@ __global__ void __launch_bounds__(256) fn_apply_shared_kernel(int count, int Q, 
   }
 }
 
+// block Gauss-Seidel right-hand side of z-plane p (multigrid.py:79-89):
+// out[i][r] = (b - A[p, p-1] x_{p-1}) - A[p, p+1] x_{p+1} at node r of the plane
+__global__ void fn_plane_rhs_kernel(int count, int c, int p, const double* __restrict__ coefA,
+                                    const double* __restrict__ x, const double* __restrict__ b,
+                                    double* __restrict__ out) {
+  const int c1 = c + 1;
+  const int64_t nodes = (int64_t)c1 * c1 * c1, M = (int64_t)c1 * c1;
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (r >= M) return;
+  const int64_t X = p * M + r;
+  const int ix = (int)(r % c1), iy = (int)(r / c1);
+  const double* ca = coefA + (int64_t)i * 27 * nodes + X;
+  const double* xi = x + (int64_t)i * nodes;
+  double sp = 0.0, sn = 0.0;
+#pragma unroll
+  for (int o = 0; o < 27; ++o) {
+    int dx, dy, dz;
+    o27_split(o, dx, dy, dz);
+    if (dz == 0) continue;
+    const int jx = ix + dx, jy = iy + dy, jz = p + dz;
+    if (jx < 0 || jx > c || jy < 0 || jy > c || jz < 0 || jz > c) continue;
+    const double a = ca[o * nodes];
+    if (a == 0.0) continue;
+    const double t = __dmul_rn(a, xi[X + dx + (int64_t)c1 * (dy + (int64_t)c1 * dz)]);
+    if (dz < 0) sp = __dadd_rn(sp, t);
+    else sn = __dadd_rn(sn, t);
+  }
+  out[(int64_t)i * M + r] = __dsub_rn(__dsub_rn(b[(int64_t)i * nodes + X], sp), sn);
+}
+
 // lower band of the plane blocks (planar = 1: systems = instances x planes, M = (c+1)^2,
 // w = c+2) or of the whole level (planar = 0: M = (c+1)^3, w = (c+1)^2 + c + 2):
 // band[(s*M + r)*ws + d] = A[r, r-d] (ws = band_ws(w)); Dirichlet rows -> identity rows
@@ -322,9 +353,10 @@ __global__ void band_solve_kernel(int64_t nsys, int64_t M, int w, int ring,
 template <int LPS, int KPS, int PF>
 __global__ void __launch_bounds__(128) band_solve_sub_kernel(int64_t nsys, int64_t M, int w,
                                                              const double* __restrict__ L,
-                                                             double* __restrict__ r,
-                                                             double* __restrict__ x, double omega,
-                                                             int mode) {
+                                                             int64_t lstride,
+                                                             double* __restrict__ r, int64_t rstride,
+                                                             double* __restrict__ x, int64_t xstride,
+                                                             double omega, int mode) {
   constexpr int SPW = 32 / LPS;  // systems per warp
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane / LPS, j = lane % LPS;
@@ -333,9 +365,9 @@ __global__ void __launch_bounds__(128) band_solve_sub_kernel(int64_t nsys, int64
   const unsigned gmask = (LPS == 32) ? 0xffffffffu : (((1u << LPS) - 1u) << (g * LPS));
   const int W1 = band_ws(w);
   const int jw = w % LPS, kw = w / LPS;  // owner of d = w
-  const double* Ls = L + s * M * W1;
-  double* rs = r + s * M;
-  double* xs = x + s * M;
+  const double* Ls = L + s * lstride;  // system strides (contiguous: M W1, M, M)
+  double* rs = r + s * rstride;
+  double* xs = x + s * xstride;
   double buf[PF][KPS], ga[PF], gb[PF];
   double win[KPS];
 #pragma unroll
@@ -586,27 +618,18 @@ int rbws_fn_band_factor(int count, int c, int planar, const double* coefA, doubl
   return 0;
 }
 
-int rbws_fn_band_solve(int count, int c, int planar, const double* band, double* r, double* x,
-                       double omega, int mode, void* stream) {
-  if (count <= 0 || c < 1 || !band || !r || !x || mode < 0 || mode > 1)
-    return rbws_set_error("rbws_fn_band_solve: bad argument", __FILE__, __LINE__);
-  const int64_t c1 = c + 1;
-  const int64_t nsys = planar ? count * c1 : count;
-  const int64_t M = planar ? c1 * c1 : c1 * c1 * c1;
-  const int w = band_w(c, planar);
-  int ring = 32;
-  while (ring < w + 1) ring *= 2;
-  const int warps = 4;
-  const size_t smem = (size_t)warps * ring * sizeof(double);
+static int band_solve_launch(int64_t nsys, int64_t M, int w, const double* band, int64_t lstride,
+                             double* r, int64_t rstride, double* x, int64_t xstride, double omega,
+                             int mode, cudaStream_t stream, bool allow_simple) {
   // sub-warp systems (LPS lanes each); RBWS_BAND_SOLVE_SIMPLE=1 for the warp-per-system
-  // kernel (A/B)
+  // kernel (A/B, contiguous systems only)
   auto sub = [&](auto lps_c, auto kps_c) -> int {
     constexpr int LPS = decltype(lps_c)::value, KPS = decltype(kps_c)::value;
     constexpr int SPW = 32 / LPS;
     const int64_t warps_needed = (nsys + SPW - 1) / SPW;
     const unsigned nb = (unsigned)((warps_needed + 3) / 4);
-    band_solve_sub_kernel<LPS, KPS, 4><<<nb, 128, 0, St(stream)>>>(nsys, M, w, band, r, x, omega,
-                                                                    mode);
+    band_solve_sub_kernel<LPS, KPS, 4><<<nb, 128, 0, stream>>>(nsys, M, w, band, lstride, r, rstride,
+                                                               x, xstride, omega, mode);
     FN_LAUNCHED();
     return 0;
   };
@@ -615,19 +638,56 @@ int rbws_fn_band_solve(int count, int c, int planar, const double* band, double*
   using std::integral_constant;
 #define RBWS_SUB(L_, K_) \
   if (lps == L_ && w + 1 <= L_ * K_) return sub(integral_constant<int, L_>{}, integral_constant<int, K_>{});
-  if (!getenv("RBWS_BAND_SOLVE_SIMPLE")) {
+  if (!(allow_simple && getenv("RBWS_BAND_SOLVE_SIMPLE"))) {
     RBWS_SUB(8, 1) RBWS_SUB(8, 2) RBWS_SUB(8, 3) RBWS_SUB(8, 5) RBWS_SUB(8, 9) RBWS_SUB(8, 17)
     RBWS_SUB(16, 1) RBWS_SUB(16, 2) RBWS_SUB(16, 3) RBWS_SUB(16, 5) RBWS_SUB(16, 9)
     RBWS_SUB(32, 1) RBWS_SUB(32, 2) RBWS_SUB(32, 3) RBWS_SUB(32, 5) RBWS_SUB(32, 9)
   }
 #undef RBWS_SUB
+  if (!allow_simple)
+    return rbws_set_error("band solve: bandwidth beyond the sub-warp kernels", __FILE__, __LINE__);
+  int ring = 32;
+  while (ring < w + 1) ring *= 2;
+  const int warps = 4;
+  const size_t smem = (size_t)warps * ring * sizeof(double);
   if (smem > 48 * 1024) {
     RBWS_CUDA_CHECK(cudaFuncSetAttribute(band_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
   }
-  band_solve_kernel<<<(unsigned)((nsys + warps - 1) / warps), warps * 32, smem, St(stream)>>>(
+  band_solve_kernel<<<(unsigned)((nsys + warps - 1) / warps), warps * 32, smem, stream>>>(
       nsys, M, w, ring, band, r, x, omega, mode);
   FN_LAUNCHED();
+  return 0;
+}
+
+int rbws_fn_band_solve(int count, int c, int planar, const double* band, double* r, double* x,
+                       double omega, int mode, void* stream) {
+  if (count <= 0 || c < 1 || !band || !r || !x || mode < 0 || mode > 1)
+    return rbws_set_error("rbws_fn_band_solve: bad argument", __FILE__, __LINE__);
+  const int64_t c1 = c + 1;
+  const int64_t nsys = planar ? count * c1 : count;
+  const int64_t M = planar ? c1 * c1 : c1 * c1 * c1;
+  const int w = band_w(c, planar);
+  return band_solve_launch(nsys, M, w, band, M * band_ws(w), r, M, x, M, omega, mode, St(stream),
+                           true);
+}
+
+int rbws_fn_plane_gs_sweep(int count, int c, const double* coefA, const double* band,
+                           const double* b, double* x, double* scratch, int forward, void* stream) {
+  if (count <= 0 || c < 1 || !coefA || !band || !b || !x || !scratch)
+    return rbws_set_error("rbws_fn_plane_gs_sweep: bad argument", __FILE__, __LINE__);
+  const int64_t c1 = c + 1, M = c1 * c1;
+  const int w = band_w(c, 1);
+  const int64_t lsz = M * band_ws(w);
+  for (int q = 0; q <= c; ++q) {
+    const int p = forward ? q : c - q;
+    fn_plane_rhs_kernel<<<grid_of(M, count), 256, 0, St(stream)>>>(count, c, p, coefA, x, b, scratch);
+    FN_LAUNCHED();
+    // x_p = A_pp^-1 rhs for every instance: systems (i, p) at strides (c+1) planes
+    if (band_solve_launch(count, M, w, band + p * lsz, c1 * lsz, scratch, M, x + p * M, c1 * M, 1.0,
+                          0, St(stream), false))
+      return 1;
+  }
   return 0;
 }
 

@@ -16,7 +16,9 @@ all (c+1)^3 nodes per instance with Dirichlet nodes held at zero
   SPD systems, factored by banded Cholesky;
 * ``mg_vcycle`` (multigrid.py:205-222) and the batched PCG ``mgcg_solve``
   (krylov.py:42-109) over those kernels.  Smoothers: ``"plane-jacobi"`` (the
-  reference default for anisotropic terms, omega 0.6) and ``"jacobi"`` (omega 0.7).
+  reference default for anisotropic terms, omega 0.6), ``"plane-z"`` (block
+  Gauss-Seidel over the planes, ascending before / descending after the coarse
+  correction; a parity path: 2 launches per plane) and ``"jacobi"`` (omega 0.7).
 """
 
 from __future__ import annotations
@@ -213,10 +215,10 @@ class FnMgContext:
         if smoother == "auto":  # multigrid.py:183-188
             aniso = any(len(set(t.aniso)) > 1 for t in problem.spec.diffusion_terms)
             smoother = "plane-jacobi" if aniso else "jacobi"
-        if smoother not in ("plane-jacobi", "jacobi"):
+        if smoother not in ("plane-jacobi", "plane-z", "jacobi"):
             raise ValueError(f"smoother {smoother!r} is not on the full-node B200 path")
         self.problem, self.nu, self.smoother = problem, nu, smoother
-        self.omega = PLANE_OMEGA if smoother == "plane-jacobi" else JACOBI_OMEGA
+        self.omega = {"plane-jacobi": PLANE_OMEGA, "plane-z": 1.0}.get(smoother, JACOBI_OMEGA)
         mus = problem.spec.check_mus(mus)
         self.count = count = len(mus)
         self.mus = mus
@@ -235,7 +237,7 @@ class FnMgContext:
             _native.call("rbws_fn_combine", count, Q, c, _ptr(theta), _ptr(problem._coef[l]),
                          _ptr(ca), st)
             self.coefA.append(ca)
-            planar = 0 if l == 0 else (1 if smoother == "plane-jacobi" else -1)
+            planar = 0 if l == 0 else (1 if smoother.startswith("plane") else -1)
             if planar < 0:
                 self.bands.append(None)
                 continue
@@ -274,9 +276,17 @@ class FnMgContext:
                          _ptr(self.coefA[level]), _ptr(x), bp, _ptr(y), mode, _native.stream_ptr())
         return y
 
-    def _smooth(self, level, u, b):
+    def _smooth(self, level, u, b, forward=True):
         c = self.problem.cells[level]
         st = _native.stream_ptr()
+        if self.smoother == "plane-z":  # ascending pre / descending post (multigrid.py:97-110)
+            import torch
+            scratch = torch.empty(self.count * (c + 1) ** 2, dtype=torch.float64, device="cuda")
+            for _ in range(self.nu):
+                _native.call("rbws_fn_plane_gs_sweep", self.count, c, _ptr(self.coefA[level]),
+                             _ptr(self.bands[level]), _ptr(b), _ptr(u), _ptr(scratch),
+                             1 if forward else 0, st)
+            return u
         for _ in range(self.nu):
             r = self.apply(u, level, b)
             if self.smoother == "plane-jacobi":  # multigrid.py:91-95
@@ -308,7 +318,7 @@ class FnMgContext:
         e = self.vcycle(bc, level - 1)
         _native.call("rbws_fn_prolong_add", self.count, cc, _ptr(e), _ptr(u),
                      _ptr(p._mask_dev[level]), st)
-        return self._smooth(level, u, b)
+        return self._smooth(level, u, b, forward=False)
 
 
 def mg_context_for(problem: FnFemProblem, mus, nu: int = 1, smoother: str = "auto"):

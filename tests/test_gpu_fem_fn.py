@@ -14,7 +14,7 @@ torch = pytest.importorskip("torch")
 
 G = np.load(Path(__file__).parent / "golden" / "golden_fem2.npz")
 CASES = (("n8m2", 3, 2), ("n16m4", 3, 4))
-SMOOTHERS = (("planejacobi", "auto"), ("jacobi", "jacobi"))
+SMOOTHERS = (("planejacobi", "auto"), ("planez", "plane-z"), ("jacobi", "jacobi"))
 
 
 @pytest.fixture(scope="module", autouse=True)
