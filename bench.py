@@ -1031,12 +1031,74 @@ def _ref_fem_solve(mu):
     return rep.iterations
 
 
+def _ref_fem2_init(n, m0):
+    _single_thread_blas()
+    from oracle import fem as of
+    _W["oprob"] = of.OracleFemProblem(of.Example2(), levels=int(np.log2(n // m0)) + 1, m0=m0)
+
+
+def _ref_fem2_solve(mu):
+    from oracle import solvers as so
+    op = _W["oprob"]
+    A, f = op.operator(mu), op.rhs(mu)
+    _, rep = so.mgcg_solve(A, f, np.zeros_like(f), so.mg_context_for(op, mu, smoother="auto"),
+                           delta=1e-10, l_max=L_MAX)
+    return rep.iterations
+
+
+def run_reference_fem2(args, world):
+    """`--impl reference --problem example-2`: the oracle restatement of the reference's
+    zero-init plane-Jacobi MGCG (mg_context_for incl. splu plane factors + MGCG per
+    parameter, as HighFidelitySolver(method="mgcg")), process pool over all host cores."""
+    import multiprocessing as mp
+    from oracle import fem as of
+    from oracle import solvers as so
+    n, m0 = args.fem_n, 4
+    spec = of.Example2()
+    test = np.array(so.lhs_sample(spec.p, args.batch or 64, spec.bounds, seed=2000))
+    cores = os.cpu_count() or 1
+    sample = cores * max(1, args.ref_per_core)
+    with mp.get_context("fork").Pool(cores, initializer=_ref_fem2_init, initargs=(n, m0)) as pool:
+        k = 0
+        for _ in range(args.warmup):
+            pool.map(_ref_fem2_solve, [test[(k + i) % len(test)] for i in range(cores)])
+            k += cores
+        t1 = time.perf_counter()
+        iters = []
+        for _ in range(args.steps):
+            iters += pool.map(_ref_fem2_solve, [test[(k + i) % len(test)] for i in range(sample)])
+            k += sample
+        el = time.perf_counter() - t1
+    value = args.steps * sample / el
+    line = {
+        "metric": "zero-init MGCG solves/s to 1e-10 rel. residual (example-2, plane-Jacobi)",
+        "value": round(value, 4), "unit": "solves/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(el / args.steps * 1e3, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded LHS parameters, sampling.py:8-27; no dataset)",
+        "impl": "reference",
+        "config": {"workload": FEM2_WORKLOAD.format(n=n, b=args.batch or 64),
+                   "mean_iterations": round(float(np.mean(iters)), 3)},
+        "cpu_baseline": {"value": round(value, 4), "unit": "solves/s", "cores": cores,
+                         "kind": "port",
+                         "sample": f"{sample} test parameters per step ({args.ref_per_core} per "
+                                   f"core), oracle restatement of the reference MGCG with the "
+                                   f"plane-Jacobi smoother on example-2 (scipy.sparse, splu "
+                                   f"plane factors), process pool over all host cores"},
+        "e2e": {"value": round(value, 4), "unit": "solves/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_reference_fem(args, world):
     """`--impl reference --problem example-1`: the oracle restatement of the reference's
     RBI-MGCG on its own FEM problem, process pool over all host cores (rank 0 only)."""
     import multiprocessing as mp
     from oracle import fem as of
     from oracle import solvers as so
+    if args.problem == "example-2":
+        return run_reference_fem2(args, world)
     if args.problem != "example-1":
         raise SystemExit(f"no reference arm for problem {args.problem!r}")
     n, m0 = args.fem_n, 4
