@@ -209,3 +209,28 @@ def test_shared_apply_is_bitwise_the_per_instance_apply(case):
                      _ptr(p._coef[lvl]), _ptr(x), _ptr(bb) if bb is not None else None, _ptr(y2),
                      mode, st)
         assert torch.equal(y1, y2)
+
+
+def test_mgcg_edge_cases(case):
+    """krylov.py:49-67 semantics on the full-node path: l_max = 0 returns x0 with the true
+    residual, a zero right-hand side switches to absolute norms and needs no iteration, an
+    exact initial guess stops at k = 0, and non-positive tolerances / negative l_max raise."""
+    from paper_2311_13862_b200.fem_fn import mg_context_for, mgcg_solve
+    k, p = case
+    mus = G[f"{k}_mus"]
+    ctx = mg_context_for(p, mus)
+    f = p.rhs(mus)
+    x, reps = mgcg_solve(ctx, f, delta=1e-10, l_max=0)
+    assert all(r.iterations == 0 for r in reps) and torch.all(x == 0)
+    assert all(abs(r.true_residual - 1.0) < 1e-12 for r in reps)
+    z = torch.zeros_like(f)
+    x, reps = mgcg_solve(ctx, z, delta=1e-10, l_max=10)
+    assert all(r.iterations == 0 and r.absolute_norms and r.converged for r in reps)
+    xs, _ = mgcg_solve(ctx, f, delta=1e-12, l_max=80)
+    x, reps = mgcg_solve(ctx, f, x0=xs, delta=1e-6, l_max=80)
+    assert all(r.iterations == 0 for r in reps)
+    assert torch.equal(x, xs)
+    with pytest.raises(ValueError):
+        mgcg_solve(ctx, f, delta=0.0)
+    with pytest.raises(ValueError):
+        mgcg_solve(ctx, f, l_max=-1)
