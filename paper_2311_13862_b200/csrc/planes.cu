@@ -237,15 +237,16 @@ __global__ void band_factor_kernel(int64_t nsys, int64_t M, int w, double* __res
 // chip (in global memory every step wrote ~w^2/2 doubles through to L2); row j leaves
 // for HBM when final, row j+w+1 enters from the assembled band just before its first
 // update.
+constexpr int kFacK = 5;  // shared-window factorization: bandwidths w < 32 kFacK
+
 __global__ void __launch_bounds__(256) band_factor_smem_kernel(int64_t nsys, int64_t M, int w,
                                                                double* __restrict__ band,
                                                                int* __restrict__ info) {
   extern __shared__ double wnd[];
   const int64_t s = blockIdx.x;
   if (s >= nsys) return;
-  const int ws = band_ws(w), W1 = w + 1;
+  const int ws = band_ws(w), W1 = w + 1, NS = w + 2;  // one spare slot: see below
   double* B = band + s * M * ws;
-  __shared__ double piv;
   __shared__ int bad;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if (threadIdx.x == 0) bad = 0;
@@ -254,35 +255,45 @@ __global__ void __launch_bounds__(256) band_factor_smem_kernel(int64_t nsys, int
     wnd[t] = row < M ? B[(int64_t)row * ws + t % ws] : 0.0;
   }
   __syncthreads();
-  int jm = 0;  // j mod (w+1): rows j..j+w live in slots jm, jm+1, ... (wrapping)
-  auto rowp = [&](int x) {  // row j + x, 0 <= x <= w
+  // rows j..j+w live in slots jm.. (mod w+2); the spare slot (that of row j-1, already
+  // written out) receives row j+w+1 while step j updates, so a step needs two barriers
+  int jm = 0;
+  auto rowp = [&](int x) {  // row j + x, 0 <= x <= w+1
     const int t = jm + x;
-    return wnd + (t >= W1 ? t - W1 : t) * ws;
+    return wnd + (t >= NS ? t - NS : t) * ws;
   };
   for (int64_t j = 0; j < M; ++j) {
     double* rj = rowp(0);
-    if (threadIdx.x == 0) {
-      const double a = rj[0];
-      if (!(a > 0.0) && !bad) bad = (int)(j + 1);
-      piv = a > 0.0 ? sqrt(a) : 1.0;
-    }
-    __syncthreads();
-    const double p = piv;
+    const double a0 = rj[0];  // every thread derives the pivot itself (no broadcast barrier)
+    const double p = a0 > 0.0 ? sqrt(a0) : 1.0;
+    if (threadIdx.x == 0 && !(a0 > 0.0) && !bad) bad = (int)(j + 1);
     for (int t = 1 + threadIdx.x; t <= w; t += blockDim.x)
       if (j + t < M) rowp(t)[t] /= p;
     __syncthreads();
+    // column j (L[j+bb][j], bb = lane + 1 + 32k) in registers: the same for every row
+    double colv[kFacK];
+#pragma unroll
+    for (int k = 0; k < kFacK; ++k) {
+      const int bb = lane + 1 + 32 * k;
+      colv[k] = (bb <= w && j + bb < M) ? rowp(bb)[bb] : 0.0;
+    }
     for (int a = 1 + warp; a <= w; a += nw) {
       if (j + a >= M) break;
       double* ra = rowp(a);
       const double la = ra[a];
-      for (int bb = 1 + lane; bb <= a; bb += 32) ra[a - bb] -= la * rowp(bb)[bb];
+#pragma unroll
+      for (int k = 0; k < kFacK; ++k) {
+        const int bb = lane + 1 + 32 * k;
+        if (bb <= a) ra[a - bb] -= la * colv[k];
+      }
     }
-    // row j is final: out to HBM (diagonal slot = 1 / L_jj), row j+w+1 in
+    // row j is final: out to HBM (diagonal slot = 1 / L_jj); row j+w+1 into the spare slot
     for (int t = threadIdx.x; t < ws; t += blockDim.x) B[j * ws + t] = t == 0 ? 1.0 / p : rj[t];
-    __syncthreads();
-    if (j + W1 < M)
-      for (int t = threadIdx.x; t < ws; t += blockDim.x) rj[t] = B[(j + W1) * ws + t];
-    jm = (jm + 1 == W1) ? 0 : jm + 1;
+    if (j + W1 < M) {
+      double* rn = rowp(W1);
+      for (int t = threadIdx.x; t < ws; t += blockDim.x) rn[t] = B[(j + W1) * ws + t];
+    }
+    jm = (jm + 1 == NS) ? 0 : jm + 1;
     __syncthreads();
   }
   if (threadIdx.x == 0) info[s] = bad;
@@ -602,8 +613,8 @@ int rbws_fn_band_factor(int count, int c, int planar, const double* coefA, doubl
   fn_band_build_kernel<<<grid_of(nodes, count), 256, 0, St(stream)>>>(count, c, planar, coefA, band);
   FN_LAUNCHED();
   const int w = band_w(c, planar);
-  const size_t wsm = (size_t)(w + 1) * band_ws(w) * sizeof(double);
-  if (wsm <= 200 * 1024 && !getenv("RBWS_BAND_FACTOR_GLOBAL")) {
+  const size_t wsm = (size_t)(w + 2) * band_ws(w) * sizeof(double);
+  if (wsm <= 200 * 1024 && w < 32 * kFacK && !getenv("RBWS_BAND_FACTOR_GLOBAL")) {
     static size_t attr = 48 * 1024;
     if (wsm > attr) {
       RBWS_CUDA_CHECK(cudaFuncSetAttribute(band_factor_smem_kernel,
