@@ -101,6 +101,11 @@ int rbws_batch_setup(rbws_batch* b, const double* theta, int count, int* n_bad, 
  * Default on (environment RBWS_GRAPH=0 turns it off); not used while the event
  * profiler or a streaming download is active. */
 int rbws_batch_set_graph(rbws_batch* b, int enable);
+/* Process-wide kernel-variant override for tests and A/B runs (no reference counterpart).
+ * which 0 = "DC" finest pre/post-smoothing kernels (w/diag cached in shared memory, 1/diag
+ * rows staged only on planes where the diagonal changes): value -1 auto (N >= 256),
+ * 0 never, 1 whenever the diagonal changes on few planes (any N). */
+int rbws_set_kernel_variant(int which, int value);
 /* Smoother of the V-cycle: 0 damped Jacobi (the reference default for isotropic problems,
  * multigrid.py:183-188), 1 Gauss-Seidel (smoother="gs": nu forward lexicographic sweeps
  * before and nu backward sweeps after the coarse correction, multigrid.py:132-152, sweep

@@ -38,6 +38,7 @@ SIGNATURES = {
     "rbws_batch_destroy": [_vp],
     "rbws_batch_setup": [_vp, _vp, _c_int, _ip, _vp],
     "rbws_batch_set_graph": [_vp, _c_int],
+    "rbws_set_kernel_variant": [_c_int, _c_int],
     "rbws_batch_set_smoother": [_vp, _c_int],
     "rbws_smooth": [_vp, _c_int, _c_int, _vp, _vp, _vp],
     "rbws_batch_stored_weights": [_vp],

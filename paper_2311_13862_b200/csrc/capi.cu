@@ -156,8 +156,17 @@ int rbws_batch_fused_restrict(const rbws_batch* b) {
 
 int rbws_batch_set_graph(rbws_batch* b, int enable) {
   if (!b) RBWS_FAIL("null batch");
+  if (!enable) B(b)->drop_graph();
   B(b)->use_graph = enable != 0;
   return 0;
+}
+
+int rbws_set_kernel_variant(int which, int value) {
+  if (which == 0) {
+    if (rbws::fine_set_dc(value)) RBWS_FAIL("DC variant must be -1 (auto), 0 or 1");
+    return 0;
+  }
+  RBWS_FAIL("unknown kernel variant");
 }
 
 int rbws_batch_setup(rbws_batch* b, const double* theta, int count, int* n_bad, void* stream) {

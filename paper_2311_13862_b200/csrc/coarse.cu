@@ -426,12 +426,9 @@ static cudaError_t coarse_kron_launch_m(CoarseArgs a, int batch, cudaStream_t st
   if (np > kCMaxPlanes) return cudaErrorInvalidValue;
   const size_t smem = 64 + 4 * kCMaxPlanes + 8 * (((size_t)np * G * 3 + 1) & ~(size_t)1) +
                       (size_t)kCStages * (NH * ((a.g.ty + 2) * a.n + 2) + NC * a.g.ty * a.n) * 8;
-  static size_t attr = 48 * 1024;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(coarse_kron_kernel<G, MODE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = smem_attr((const void*)coarse_kron_kernel<G, MODE>, smem);
     if (e != cudaSuccess) return e;
-    attr = smem;
   }
   dim3 grd(1, a.g.ytiles, batch * a.g.zc);
   count_launch();
@@ -459,12 +456,9 @@ static cudaError_t coarse_launch_m(CoarseArgs a, int batch, cudaStream_t stream)
   if (a.g.kz + 2 > kCMaxPlanes) return cudaErrorInvalidValue;
   const size_t smem = 64 + 4 * kCMaxPlanes + 64 +
                       (size_t)kCStages * (NH * ((a.g.ty + 2) * a.n + 2) + NC * a.g.ty * a.n) * 8;
-  static size_t attr = 48 * 1024;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(coarse_kernel<Q, MODE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = smem_attr((const void*)coarse_kernel<Q, MODE>, smem);
     if (e != cudaSuccess) return e;
-    attr = smem;
   }
   dim3 grd(1, a.g.ytiles, batch * a.g.zc);
   count_launch();

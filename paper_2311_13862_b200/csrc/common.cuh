@@ -24,6 +24,9 @@ constexpr int kMaxTerms = 8;
 void count_launch();
 void count_launches(int64_t k);
 int64_t launch_count();
+// raise fn's dynamic shared-memory limit to `bytes` on the current device (cached per
+// kernel and device, thread-safe; no-op at or below the 48 KB default)
+cudaError_t smem_attr(const void* fn, size_t bytes);
 
 RBWS_HD int64_t vec_doubles(int n, int batch) {
   return (int64_t)batch * n * n * n + 2 * (int64_t)n * n;

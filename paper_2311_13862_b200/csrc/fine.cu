@@ -16,6 +16,7 @@
 // plane's; for piecewise-constant (thermal-block) coefficients they almost
 // always do, so the six face weights and the diagonal stay cached in
 // registers and a node costs only the 7-point update.
+#include <atomic>
 #include "fine.cuh"
 #include "tma.cuh"
 
@@ -24,6 +25,16 @@ namespace rbws {
 constexpr int kStages = 8;  // ring slots (power of two)
 constexpr int kMaxKz = 64;  // planes per z-chunk (bounds the z-factor table)
 constexpr int kMaxDiagChanges = 16;  // DC kernels when the diagonal changes on <= 16 planes
+
+// test/A-B override of the DC choice (rbws_set_kernel_variant): -1 auto, 0 never, 1 whenever
+// the diagonal changes on few enough planes (any N)
+static std::atomic<int> g_force_dc{-1};
+int fine_set_dc(int v) {
+  if (v < -1 || v > 1) return 1;
+  g_force_dc.store(v);
+  return 0;
+}
+int fine_variant() { return g_force_dc.load(); }
 constexpr int kThreads = 256;  // threads per CTA (one per grid column of the tile; N = 512: 512)
 
 // Compile-time tile geometry for a grid with N cells per axis: RPP rows per pass
@@ -625,12 +636,9 @@ static cudaError_t fine_launch_mnd(const FineArgs& a, int batch, cudaStream_t st
   const int np = a.g.kz + (MODE == FM_PREX ? 3 : 2);  // FM_PREX: one recomputed plane
   const size_t smem = FSmem<N, MODE, DC>::bytes(np, SCW ? 0 : a.op.Q);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  static size_t attr = 48 * 1024;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(fine_kernel<MODE, N, DC, SCW>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = smem_attr((const void*)fine_kernel<MODE, N, DC, SCW>, smem);
     if (e != cudaSuccess) return e;
-    attr = smem;
   }
   dim3 grd(1, a.g.ytiles, batch * a.g.zc);
   count_launch();
@@ -798,7 +806,9 @@ static FineArgs base_args(const Sep7& op, int dot, double* partial, const Launch
   // few planes where the diagonal changes along z: cache w/diag instead of reading dinv.
   // Measured: at N <= 128 (two 256-thread CTAs per SM) the transformed-input kernels are
   // issue-bound and the saved 8 B/node buy nothing; at N = 512 (one CTA per SM) they do.
-  a.dc = (op.fz && op.n >= 256 && op.zchg >= 0 && op.zchg <= kMaxDiagChanges) ? 1 : 0;
+  const int force = g_force_dc.load(std::memory_order_relaxed);
+  const bool few = op.fz && op.zchg >= 0 && op.zchg <= kMaxDiagChanges;
+  a.dc = (few && (force < 0 ? op.n >= 256 : force == 1)) ? 1 : 0;
   return a;
 }
 

@@ -5,6 +5,10 @@
 
 namespace rbws {
 
+// override of the DC kernel choice (-1 auto: N >= 256; 0 never; 1 whenever applicable)
+int fine_set_dc(int v);
+int fine_variant();  // current override (part of the cached PCG graph's key)
+
 struct FineGeom {
   int threads;  // threads per CTA (rows-per-pass x n)
   int rpp;      // grid rows covered per pass of the CTA

@@ -615,12 +615,7 @@ int rbws_fn_band_factor(int count, int c, int planar, const double* coefA, doubl
   const int w = band_w(c, planar);
   const size_t wsm = (size_t)(w + 2) * band_ws(w) * sizeof(double);
   if (wsm <= 200 * 1024 && w < 32 * kFacK && !getenv("RBWS_BAND_FACTOR_GLOBAL")) {
-    static size_t attr = 48 * 1024;
-    if (wsm > attr) {
-      RBWS_CUDA_CHECK(cudaFuncSetAttribute(band_factor_smem_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
-      attr = wsm;
-    }
+    RBWS_CUDA_CHECK(rbws::smem_attr((const void*)band_factor_smem_kernel, wsm));
     band_factor_smem_kernel<<<(unsigned)nsys, 256, wsm, St(stream)>>>(nsys, M, w, band, info);
   } else {
     band_factor_kernel<<<(unsigned)nsys, 256, 0, St(stream)>>>(nsys, M, w, band, info);

@@ -6,6 +6,7 @@
 //   mg_vcycle with damped-Jacobi pre/post sweeps                  (multigrid.py:205-222, kernels.py:98-115)
 //   pcg_solve                                                      (krylov.py:42-109)
 #include <atomic>
+#include <map>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -89,6 +90,23 @@ static std::atomic<int64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 void count_launches(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+// the dynamic shared-memory limit is a per-device kernel attribute: remember the largest
+// value set for every (kernel, device) pair, under a lock (several host threads may launch)
+cudaError_t smem_attr(const void* fn, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> set;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = set[{fn, dev}];
+  if (bytes <= cur) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
 
 template <class T>
 static cudaError_t dalloc(T** p, size_t count) {
@@ -437,6 +455,15 @@ int batch_create(Batch** out, Hierarchy* h, int cap, int nu, double omega, int m
   return 0;
 }
 
+void Batch::drop_graph() {
+  if (gexec) cudaGraphExecDestroy(gexec);
+  if (graph) cudaGraphDestroy(graph);
+  gexec = nullptr;
+  graph = nullptr;
+  gkey_x = nullptr;
+  gkey_active = nullptr;
+}
+
 int batch_set_smoother(Batch* b, int kind) {
   if (kind != 0 && kind != 1) RBWS_FAIL("smoother kind must be 0 (jacobi) or 1 (gauss-seidel)");
   Hierarchy* h = b->h;
@@ -458,6 +485,7 @@ int batch_set_smoother(Batch* b, int kind) {
     }
     if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
   }
+  if (kind != b->smoother) b->drop_graph();  // the captured V-cycle used the old smoother
   b->smoother = kind;
   b->count = 0;  // set up again
   return 0;
@@ -863,13 +891,12 @@ static int pcg_graph_run(Batch* b, const Sep7& op, double* x, int tiles, int vti
   act.stream = stream;
   const bool hit = b->gexec && b->gkey_x == x && b->gkey_count == count &&
                    b->gkey_delta == delta && b->gkey_lmax == l_max && b->gkey_hl == hl &&
-                   b->gkey_active == act.active;
+                   b->gkey_active == act.active && b->gkey_smoother == b->smoother &&
+                   b->gkey_fused == (int)b->fuse_restrict && b->gkey_wface == b->wface &&
+                   b->gkey_variant == fine_variant();
   cudaError_t e = cudaSuccess;
   if (!hit) {
-    if (b->gexec) cudaGraphExecDestroy(b->gexec);
-    if (b->graph) cudaGraphDestroy(b->graph);
-    b->gexec = nullptr;
-    b->graph = nullptr;
+    b->drop_graph();
     cudaGraph_t g;
     e = cudaGraphCreate(&g, 0);
     if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
@@ -925,7 +952,9 @@ static int pcg_graph_run(Batch* b, const Sep7& op, double* x, int tiles, int vti
     b->gbody_launches = launch_count() - c0;
     count_launches(-b->gbody_launches);  // captured, not executed
     b->gkey_x = x; b->gkey_count = count; b->gkey_delta = delta; b->gkey_lmax = l_max;
-    b->gkey_hl = hl; b->gkey_active = act.active;
+    b->gkey_hl = hl; b->gkey_active = act.active; b->gkey_smoother = b->smoother;
+    b->gkey_fused = (int)b->fuse_restrict; b->gkey_wface = b->wface;
+    b->gkey_variant = fine_variant();
   }
   e = cudaGraphLaunch(b->gexec, stream);
   if (e == cudaSuccess && stream != user) {

@@ -107,8 +107,11 @@ struct Batch {
   cudaGraphExec_t gexec = nullptr;
   const double* gkey_x = nullptr;
   const int* gkey_active = nullptr;
-  int gkey_count = 0, gkey_lmax = 0, gkey_hl = 0;
+  int gkey_count = 0, gkey_lmax = 0, gkey_hl = 0, gkey_smoother = -1, gkey_fused = -1,
+      gkey_variant = -2;
+  const double* gkey_wface = nullptr;
   double gkey_delta = 0.0;
+  void drop_graph();                // invalidate the cached executable (smoother/graph changes)
   int64_t gbody_launches = 0;
   cudaStream_t gstream = nullptr;     // capture/launch stream when the caller's is the legacy one
   cudaEvent_t gev[2] = {nullptr, nullptr};

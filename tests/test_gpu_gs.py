@@ -81,3 +81,21 @@ def test_gs_batch_matches_oracle_and_rejects_unknown():
         assert _rel(got[m], xr) <= 1e-8
     with pytest.raises(ValueError):
         pkg.mg_context_for(prob, mus, smoother="plane-jacobi")
+
+
+def test_smoother_switch_rebuilds_cached_graph():
+    """Switching a solved batch from Jacobi to Gauss-Seidel must not replay the cached
+    Jacobi PCG graph: the solve equals a fresh Gauss-Seidel context's, bit for bit."""
+    pkg = _pkg()
+    from paper_2311_13862_b200 import _native
+    prob = pkg.ParametricProblem(pkg.thermal_block((2, 2, 1)), levels=3, m0=4)
+    mus = op.sample_mus(op.thermal_block((2, 2, 1)), 4, seed=21)
+    ctx = pkg.mg_context_for(prob, mus)
+    pkg.mgcg_solve(None, prob.rhs(), None, ctx, delta=1e-10, l_max=60)  # caches the graph
+    _native.call("rbws_batch_set_smoother", ctx.handle, 1)
+    ctx.setup(mus)
+    x, reps = pkg.mgcg_solve(None, prob.rhs(), None, ctx, delta=1e-10, l_max=60)
+    fresh = pkg.mg_context_for(prob, mus, smoother="gs")
+    xr, rr = pkg.mgcg_solve(None, prob.rhs(), None, fresh, delta=1e-10, l_max=60)
+    assert [r.iterations for r in reps] == [r.iterations for r in rr]
+    assert torch.equal(x, xr)
