@@ -43,7 +43,8 @@ CONFIGS = {
             kind="tb", blocks=(2, 2, 1), n=64, m0=4, r=20, n_train=1024, batch=1024, delta=1e-10,
             e2e_sizes=[1024]),
     2: dict(workload="thermal-block 2x2x2, 128^3 cells, r=30 from 4096 train, batch 512, tol 1e-12",
-            kind="tb", blocks=(2, 2, 2), n=128, m0=4, r=30, n_train=4096, batch=512, delta=1e-12),
+            kind="tb", blocks=(2, 2, 2), n=128, m0=4, r=30, n_train=4096, batch=512, delta=1e-12,
+            scaling="strong"),
     3: dict(workload="smooth affine (6 modes), 256^3 cells, r=40 from 2048 train, batch 128, tol 1e-12",
             kind="smooth", blocks=None, n=256, m0=4, r=40, n_train=2048, batch=128, delta=1e-12,
             chunk=64, e2e_sub=32),
@@ -162,6 +163,22 @@ def _traffic(kernel, bytes_per_launch, cfg):
     return int(ratio * bytes_per_launch), f"{cap['source']}; dram/algorithmic = {ratio:.3f}"
 
 
+def rank_shard(args, cfg, rank, world, sampler):
+    """This rank's test parameters.  weak: every rank solves its own batch of the config's
+    size (seed 2000 + rank), whole-job units = world x batch; strong: one global batch
+    (seed 2000) split into contiguous shards (dist.shard_parameters), units = the batch."""
+    from paper_2311_13862_b200 import dist as rdist
+    batch = args.batch or cfg["batch"]
+    scaling = args.scaling or cfg.get("scaling", "weak")
+    if scaling == "strong":
+        mus = rdist.shard_parameters(sampler(batch, 2000), rank, world)
+        lo, hi = rdist.shard_bounds(batch, rank, world)
+        return {"mus": mus, "local": len(mus), "total": batch, "scaling": "strong",
+                "desc": f"global batch {batch} sharded: rank {rank} of {world} owns [{lo}, {hi})"}
+    return {"mus": sampler(batch, 2000 + rank), "local": batch, "total": world * batch,
+            "scaling": "weak", "desc": f"{batch} parameters per rank (seed 2000 + rank)"}
+
+
 def run_b200(args, rank, world, dist):
     import torch
 
@@ -172,16 +189,17 @@ def run_b200(args, rank, world, dist):
         dist.barrier()
     import paper_2311_13862_b200 as rb
     from paper_2311_13862_b200 import _native
+    from paper_2311_13862_b200 import dist as rdist
 
     cfg = CONFIGS[args.config]
     n, m0 = cfg["n"], cfg["m0"]
-    batch = args.batch or cfg["batch"]
     delta = cfg["delta"]
     spec = make_spec(cfg, rb)
     levels = rb.problems.levels_for(n, m0)
     prob = rb.ParametricProblem(spec, levels=levels, m0=m0)
     train = rb.sample_mus(spec, cfg["n_train"], seed=1000)
-    test = rb.sample_mus(spec, batch, seed=2000 + rank)
+    shard = rank_shard(args, cfg, rank, world, lambda c, s: rb.sample_mus(spec, c, seed=s))
+    test, batch = shard["mus"], shard["local"]
 
     t0 = time.perf_counter()
     hf = rb.HighFidelitySolver(prob, delta=1e-14, l_max=100)
@@ -217,11 +235,11 @@ def run_b200(args, rank, world, dist):
     _, zreps = rb.mgcg_solve(None, f, None, ctx, delta=delta, l_max=L_MAX)  # last sub-batch
     zero_iters = float(np.mean([r.iterations for r in zreps]))
 
-    # ---- timed region (device-resident inputs)
+    # ---- timed region (device-resident inputs; the default device-side graph PCG loop,
+    # no per-kernel events)
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    _native.call("rbws_batch_profile", ctx.handle, 1)
     lc0 = _native.launch_count()
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -235,6 +253,28 @@ def run_b200(args, rank, world, dist):
         torch.cuda.nvtx.range_pop()
     launches = _native.launch_count() - lc0
     ms = ev0.elapsed_time(ev1)
+    ms_max = rdist.max_over_ranks(ms, device="cuda")
+    ms_step = ms_max / args.steps
+    value = shard["total"] * args.steps / (ms_max / 1e3)
+    reps = [r for batch_reps in state["reps"] for r in batch_reps]
+    all_reps = rdist.gather_reports(reps)            # every rank's reports, global order
+    iters = [r[0] if isinstance(r, tuple) else r.iterations for r in all_reps]
+    worst_res = max(r[1] if isinstance(r, tuple) else r.true_residual for r in all_reps)
+    converged = all(r[2] if isinstance(r, tuple) else r.converged for r in all_reps)
+    my_iters = [r.iterations for r in reps]
+
+    # ---- per-kernel-class breakdown (roofline): the same K steps once more with the CUDA
+    # event profiler on (host-driven PCG loop, an event pair per kernel class); not the
+    # timed region above, whose number it does not touch
+    torch.cuda.synchronize()
+    _native.call("rbws_batch_profile", ctx.handle, 1)
+    pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pe0.record(stream)
+    for _ in range(args.steps):
+        step()
+    pe1.record(stream)
+    torch.cuda.synchronize()
+    ms_prof = pe0.elapsed_time(pe1)
     NC = len(CLASS_NAMES)
     pms = np.zeros(NC)
     pcalls = np.zeros(NC, dtype=np.int64)
@@ -242,18 +282,6 @@ def run_b200(args, rank, world, dist):
     _native.call("rbws_batch_profile_read", ctx.handle, pms.ctypes.data, pcalls.ctypes.data,
                  punits.ctypes.data, NC)
     _native.call("rbws_batch_profile", ctx.handle, 0)
-    if dist is not None:
-        dist.barrier()
-    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if dist is not None:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
-    ms_step = ms_max / args.steps
-    value = world * batch * args.steps / (ms_max / 1e3)
-    reps = [r for batch_reps in state["reps"] for r in batch_reps]
-    iters = [r.iterations for r in reps]
-    worst_res = max(r.true_residual for r in reps)
-    converged = all(r.converged for r in reps)
 
     # ---- end to end through the public API with host buffers: host mu in, solutions
     # out to pinned host memory, sub-batches pipelined (paper_2311_13862_b200.pipeline)
@@ -264,7 +292,7 @@ def run_b200(args, rank, world, dist):
     torch.cuda.empty_cache()
     e2e_sub = min(batch, args.e2e_sub or cfg.get("e2e_sub", 512))
     sizes = [int(v) for v in args.e2e_sizes.split(",")] if args.e2e_sizes else \
-        cfg.get("e2e_sizes")
+        (cfg.get("e2e_sizes") if batch == cfg["batch"] else None)
     pipe = rb.HostPipeline(prob, method, model, sub_batch=e2e_sub,
                            tail=args.e2e_tail or None, sizes=sizes)
     hbuf = torch.empty(batch * n ** 3, dtype=torch.float64, pin_memory=True)
@@ -282,13 +310,12 @@ def run_b200(args, rank, world, dist):
     stream.wait_stream(pipe.copy_stream)
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
-    if dist is not None:
-        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-    e2e_value = world * batch * args.steps / (float(e2e_ms.item()) / 1e3)
-    e2e_iters_ok = all(a.iterations == b.iterations for a, b in zip(reps_e, reps))
-    h2d = batch * spec.n_terms * 8
-    d2h = batch * n ** 3 * 8 + batch * (L_MAX + 1) * 8 + batch * (4 + 8 + 4)
+    e2e_ms = rdist.max_over_ranks(e0.elapsed_time(e1), device="cuda")
+    e2e_value = shard["total"] * args.steps / (e2e_ms / 1e3)
+    e2e_iters_ok = all(a.iterations == b for a, b in zip(reps_e, my_iters))
+    tb = shard["total"]  # whole job: every rank's copies
+    h2d = tb * spec.n_terms * 8
+    d2h = tb * n ** 3 * 8 + tb * (L_MAX + 1) * 8 + tb * (4 + 8 + 4)
 
     # ---- roofline of the dominant fine-level kernel class
     peak, peak_kind = peaks()
@@ -304,7 +331,7 @@ def run_b200(args, rank, world, dist):
             continue
         row = {"ms_total": round(float(pms[k]), 3), "launches": int(pcalls[k]),
                "ms_per_launch": round(float(pms[k]) / pcalls[k], 4),
-               "share": round(float(pms[k]) / ms, 4)}
+               "share": round(float(pms[k]) / ms_prof, 4)}
         if k in class_bytes:
             gbs = class_bytes[k] * nodes * punits[k] / (pms[k] / 1e3) / 1e9
             row["achieved_gbs"] = round(gbs, 1)
@@ -329,14 +356,17 @@ def run_b200(args, rank, world, dist):
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(cfg, model, test, iters, budget_s=args.cpu_budget)
+        cpu = cpu_baseline(cfg, model, test, my_iters, budget_s=args.cpu_budget)
+    fracs = rdist.gather_values(roofline.get("frac"))
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "solves/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": shard["scaling"], "vs_baseline": None,
+        "dtype": "f64",
         "data": "synthetic (seeded log-uniform parameters; no dataset)",
-        "config": {"workload": cfg["workload"], "batch_per_gpu": batch, "sub_batch": chunk,
+        "config": {"workload": cfg["workload"], "batch_per_gpu": batch,
+                   "global_batch": shard["total"], "sharding": shard["desc"], "sub_batch": chunk,
                    "grid_cells": n,
                    "levels": levels, "rb_dim": model.dim, "n_train": cfg["n_train"],
                    "tolerance": delta, "smoother": "jacobi(0.7), nu=1",
@@ -354,6 +384,11 @@ def run_b200(args, rank, world, dist):
                 "iterations_match_device_run": bool(e2e_iters_ok)},
         "gpu_launches": int(launches),
         "roofline": roofline,
+        "roofline_pass": ("per-class CUDA events over a second run of the same K steps "
+                          "(host-driven PCG loop); the timed region runs the device-side "
+                          f"graph loop: {ms_prof / args.steps:.3f} ms/step profiled vs "
+                          f"{ms / args.steps:.3f} timed on rank {rank}"),
+        "roofline_frac_per_rank": fracs,
         "kernels": table,
         "clocks": clocks.summary(),
     }
@@ -1195,6 +1230,65 @@ def run_reference_slab(args, world):
     print(json.dumps(line), flush=True)
 
 
+def run_dry(args, rank, world, dist):
+    """--dry-run: the multi-rank flow of run_b200 (sharding, barrier-bracketed timed
+    region, max over ranks, report gathering, one JSON line from rank 0) on CPU with gloo
+    and a host stand-in for the solve (iterations = global parameter index), so the rank
+    orchestration is testable without GPUs (tests/test_bench_ranks_gloo.py)."""
+    from paper_2311_13862_b200 import dist as rdist
+    from paper_2311_13862_b200.krylov import SolveReport
+    from paper_2311_13862_b200.problems import sample_mus, thermal_block
+    cfg = CONFIGS[args.config]
+    spec = thermal_block(cfg["blocks"] or (2, 2, 1))
+    shard = rank_shard(args, cfg, rank, world, lambda c, s: sample_mus(spec, c, seed=s))
+    if shard["scaling"] == "strong":
+        lo, _ = rdist.shard_bounds(shard["total"], rank, world)
+    else:
+        lo = rank * shard["local"]
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        reps = [SolveReport("rbi-mgcg", lo + i, [1.0], True, 1e-11, 0.0, 1e-10, L_MAX)
+                for i in range(shard["local"])]
+        time.sleep(0.01 * (1 + rank))
+    ms = (time.perf_counter() - t0) * 1e3
+    ms_max = rdist.max_over_ranks(ms)
+    merged = rdist.gather_reports(reps)
+    mus_all = rdist.gather_values(shard["mus"].tolist())
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": round(shard["total"] * args.steps / (ms_max / 1e3), 2),
+            "unit": "solves/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_max / args.steps, 3), "higher_is_better": True,
+            "scaling": shard["scaling"], "dry_run": True,
+            "config": {"workload": cfg["workload"], "global_batch": shard["total"],
+                       "batch_per_gpu": shard["local"], "sharding": shard["desc"]},
+            "report_order": [m[0] for m in merged],
+            "mus_by_rank": mus_all}), flush=True)
+
+
+def _spawn_ranks(n):
+    """`bench.py --gpus N` without a launcher: start N copies of this command as ranks
+    0..N-1 (RANK/LOCAL_RANK/WORLD_SIZE, rendezvous on 127.0.0.1), the way
+    torch.distributed.run would; rank 0's stdout carries the JSON line."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__), *sys.argv[1:]],
+                                      env=env, stdout=None if r == 0 else subprocess.DEVNULL))
+    rc = 0
+    for p in procs:
+        rc = max(rc, p.wait())
+    return rc
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -1219,18 +1313,35 @@ def main():
     ap.add_argument("--fem-n", type=int, default=64)
     ap.add_argument("--fem-r", type=int, default=10)
     ap.add_argument("--fem-train", type=int, default=256)
+    ap.add_argument("--scaling", default="", choices=["", "weak", "strong"],
+                    help="weak: a full batch per GPU (default); strong: one global batch "
+                         "sharded by parameter across the GPUs (configs[2]'s default)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU/gloo run of the multi-rank orchestration with a stand-in solve")
     ap.add_argument("--slabs-per-gpu", type=int, default=1,
                     help="configs[4]: slabs per GPU (>1: in-process slabs exchanging by copies)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         log("note: fewer than 3 warm-up steps requested")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl != "reference":
+        sys.exit(_spawn_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     dist = None
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        run_reference(args, rank, max(world, args.gpus))
+        return
+    if args.dry_run:
+        if world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("gloo")
+        run_dry(args, rank, world, dist)
+        if dist is not None:
+            dist.destroy_process_group()
         return
     import torch
+    if args.gpus > 1 and torch.cuda.device_count() < world:
+        raise SystemExit(f"--gpus {args.gpus}: only {torch.cuda.device_count()} CUDA devices")
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:

@@ -17,6 +17,8 @@
 // always do, so the six face weights and the diagonal stay cached in
 // registers and a node costs only the 7-point update.
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include "fine.cuh"
 #include "tma.cuh"
 
@@ -632,18 +634,29 @@ fine_kernel(FineArgs a) {
 template <int MODE, int N, bool DC, bool SCW = false>
 static cudaError_t fine_launch_mnd(const FineArgs& a, int batch, cudaStream_t stream) {
   using G = FTM<MODE, N>;
-  if (a.g.threads != G::THREADS || a.g.ty != G::TY) return cudaErrorInvalidValue;
   const int np = a.g.kz + (MODE == FM_PREX ? 3 : 2);  // FM_PREX: one recomputed plane
   const size_t smem = FSmem<N, MODE, DC>::bytes(np, SCW ? 0 : a.op.Q);
-  if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  {
-    cudaError_t e = smem_attr((const void*)fine_kernel<MODE, N, DC, SCW>, smem);
-    if (e != cudaSuccess) return e;
+  cudaError_t e0 = cudaSuccess;
+  if (a.g.threads != G::THREADS || a.g.ty != G::TY || smem > 227 * 1024)
+    e0 = cudaErrorInvalidValue;
+  else
+    e0 = smem_attr((const void*)fine_kernel<MODE, N, DC, SCW>, smem);
+  if (e0 != cudaSuccess) {
+    fprintf(stderr, "[rbws] fine_kernel<%d,%d,%d,%d> not launched: threads %d/%d ty %d/%d kz %d "
+            "smem %zu: %s\n", MODE, N, (int)DC, (int)SCW, a.g.threads, G::THREADS, a.g.ty, G::TY,
+            a.g.kz, smem, cudaGetErrorString(e0));
+    return e0;
   }
   dim3 grd(1, a.g.ytiles, batch * a.g.zc);
   count_launch();
   fine_kernel<MODE, N, DC, SCW><<<grd, G::THREADS, smem, stream>>>(a);
-  return cudaGetLastError();
+  const cudaError_t e = cudaGetLastError();
+  static const bool dbg = getenv("RBWS_DEBUG_LAUNCH") != nullptr;
+  if (dbg || e != cudaSuccess)
+    fprintf(stderr, "[rbws] fine_kernel<%d,%d,%d,%d> grid (1,%d,%d) block %d smem %zu: %s\n",
+            MODE, N, (int)DC, (int)SCW, a.g.ytiles, batch * a.g.zc, G::THREADS, smem,
+            cudaGetErrorString(e));
+  return e;
 }
 
 template <int MODE, int N>
@@ -848,7 +861,13 @@ cudaError_t fine_pre(const Sep7& op, int batch, const double* b, const double* d
   return fine_launch(FM_PRE, a, batch, lc.stream);
 }
 
-bool fine_pre_xz_ok(int n, int batch, const LaunchCtx& lc) {
+template <int N>
+static size_t prex_smem(bool dc, int np, int Q) {
+  return dc ? FSmem<N, FM_PREX, true>::bytes(np, Q) : FSmem<N, FM_PREX, false>::bytes(np, Q);
+}
+
+bool fine_pre_xz_ok(const Sep7& op, int batch, const LaunchCtx& lc) {
+  const int n = op.n;
   if (lc.zhi > 0 && (lc.zlo != 0 || lc.zhi != n)) return false;  // z-ranges (slabs): no
   static const bool n128 = [] {  // A/B: RBWS_FUSED_N128=0 keeps the separate kernels
     const char* e = getenv("RBWS_FUSED_N128");
@@ -859,12 +878,29 @@ bool fine_pre_xz_ok(int n, int batch, const LaunchCtx& lc) {
   // there: 7.37 -> 7.27 ms, 792 -> 813 solves/s (A/B, two runs each)
   if (n == 128 && !n128) return false;
   // z-chunks must start on even planes (a chunk then recomputes the odd plane below it)
-  return (fine_geom(n, batch, n, fine_mode_threads(FM_PREX, n)).kz & 1) == 0;
+  const FineGeom g = fine_geom(n, batch, n, fine_mode_threads(FM_PREX, n));
+  if (g.kz & 1) return false;
+  // the z-factor table grows with the chunk's planes: at N = 512 with a short batch (long
+  // chunks) it no longer fits next to the ring -> separate pre-smoothing + restriction
+  const int Q = op.wface ? 0 : op.Q, np = g.kz + 3;
+  const bool dc = base_args(op, DOT_NONE, nullptr, lc, 0.0).dc != 0;
+  size_t smem = 0;
+  switch (n) {
+    case 8: smem = prex_smem<8>(dc, np, Q); break;
+    case 16: smem = prex_smem<16>(dc, np, Q); break;
+    case 32: smem = prex_smem<32>(dc, np, Q); break;
+    case 64: smem = prex_smem<64>(dc, np, Q); break;
+    case 128: smem = prex_smem<128>(dc, np, Q); break;
+    case 256: smem = prex_smem<256>(dc, np, Q); break;
+    case 512: smem = prex_smem<512>(dc, np, Q); break;
+    default: return false;
+  }
+  return smem <= 227 * 1024;
 }
 
 cudaError_t fine_pre_xz(const Sep7& op, int batch, const double* b, const double* dinv,
                         double* t, double omega, const LaunchCtx& lc) {
-  if (!fine_pre_xz_ok(op.n, batch, lc)) return cudaErrorInvalidValue;
+  if (!fine_pre_xz_ok(op, batch, lc)) return cudaErrorInvalidValue;
   FineArgs a = base_args(op, DOT_NONE, nullptr, lc, omega);
   a.h0 = b;
   a.h1 = dinv;

@@ -48,7 +48,7 @@ cudaError_t fine_pre(const Sep7& op, int batch, const double* b, const double* d
 // t[K][j][I] (n/2 x n x n/2 per instance) = sum over fine planes 2K-1..2K+1 and columns
 // 2I-1..2I+1 (weights 0.5 / 1 / 0.5) of r1 = b - A (omega dinv b) on fine row j; the y pass is
 // restrict_y_launch.  Only when one CTA holds an instance's whole z-range (fine_pre_xz_ok).
-bool fine_pre_xz_ok(int n, int batch, const LaunchCtx& lc);
+bool fine_pre_xz_ok(const Sep7& op, int batch, const LaunchCtx& lc);
 cudaError_t fine_pre_xz(const Sep7& op, int batch, const double* b, const double* dinv,
                         double* t, double omega, const LaunchCtx& lc);
 // fused prolongation + post-smoothing of the nu=1 V-cycle:

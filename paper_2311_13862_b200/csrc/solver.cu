@@ -618,7 +618,7 @@ int Batch::vcycle(int lvl, const double* bb, double* out, double* dot_partial,
     int t0 = pf ? prof_begin(lc.stream) : -1;
     // finest level, whole instances per CTA: the pre-smoothing kernel also runs the x and z
     // passes of the restriction (r1 never reaches HBM), a light kernel the y pass
-    const bool fused = fine && fuse_restrict && lvl - 1 >= 1 && fine_pre_xz_ok(n, count, lc);
+    const bool fused = fine && fuse_restrict && lvl - 1 >= 1 && fine_pre_xz_ok(fine_op(), count, lc);
     if (fine) fused_used = fused;  // (the coarse levels of the recursion leave it alone)
     if (stop) e = vec_scale_dinv(n, count, omega, l.dinv, bb, l.u, lc.stream);
     if (e == cudaSuccess)

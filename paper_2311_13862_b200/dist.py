@@ -3,7 +3,9 @@
 Parameter instances are independent, so a batch is split across ranks with no
 collective on the data path.  The only communication is
 host-side bookkeeping: gathering iteration counts / residuals for reporting
-and the max-over-ranks timing reduction done by bench.py.
+and the max-over-ranks timing reduction.  bench.py's rank flow (``rank_shard``,
+the timed region, the reports) goes through these helpers, and
+tests/test_bench_ranks_gloo.py runs that flow with two gloo ranks on CPU.
 """
 
 from __future__ import annotations
@@ -40,6 +42,16 @@ def gather_reports(reports, group=None) -> list:
     for part in out:
         merged.extend(part)
     return merged
+
+
+def gather_values(value, group=None) -> list:
+    """Every rank's (small, picklable) value in rank order; [value] without a process group."""
+    import torch.distributed as dist
+    if not dist.is_available() or not dist.is_initialized():
+        return [value]
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, value, group=group)
+    return out
 
 
 def max_over_ranks(value: float, device=None) -> float:
