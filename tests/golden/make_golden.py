@@ -7,6 +7,8 @@ Run in the build container (needs /root/reference; never on the GPU box):
     python tests/golden/make_golden.py --msrb   # golden_msrb.npz (rbi-msrbcg)
     python tests/golden/make_golden.py --fem    # golden_fem.npz (example-1, unmodified reference)
     python tests/golden/make_golden.py --fem2   # golden_fem2.npz (example-2, unmodified reference)
+    python tests/golden/make_golden.py --experiment  # golden_experiment.npz (run_experiment loop)
+    python tests/golden/make_golden.py --signatures  # ref_signatures.json (public API)
 
 The reference (``/root/reference/pkg``) is copied to /tmp and its Cython
 smoother extension built in place (reference setup.py), so the reference's
@@ -420,7 +422,100 @@ def main_fem2():
     print(f"wrote {dest} ({dest.stat().st_size/1e6:.2f} MB, {len(out)} arrays)")
 
 
+EXPERIMENTS = {
+    # tag: (problem, levels, m0, n_train, n_test, rb_dims, deltas)
+    "ex1": ("example-1", 3, 4, 16, 3, (4, 6), (1e-10, 1e-12)),
+    "ex2": ("example-2", 3, 4, 12, 3, (4,), (1e-10,)),
+}
+
+
+def main_experiment():
+    """The reference's own experiment driver, unmodified (experiment.py:108-172: LHS train /
+    test sets, the LU-backed L1ROC greedy, per-parameter mg_context_for + rbi_pcg_solve for
+    mgcg and rbi-mgcg) -> tests/golden/golden_experiment.npz.  The loop's calls are recorded
+    through wrappers around the names it imports (training / test sets, the trained model,
+    every solve's solution and report); nothing inside the loop is changed.  The compat layer
+    (paper_2311_13862_b200/compat.py) replays the same loop on the GPU against these."""
+    rbws = _import_reference()
+    import rbws.experiment as ex
+
+    out = {}
+    for tag, (pid, levels, m0, n_train, n_test, dims, deltas) in EXPERIMENTS.items():
+        rec = {"lhs": [], "model": None, "solves": []}
+        orig_lhs, orig_off, orig_rbi = ex.lhs_sample, ex.l1roc_offline, ex.rbi_pcg_solve
+
+        def lhs(*a, **k):
+            pts = orig_lhs(*a, **k)
+            rec["lhs"].append(np.array(pts))
+            return pts
+
+        def off(*a, **k):
+            rec["model"] = orig_off(*a, **k)
+            return rec["model"]
+
+        def rbi(A, f, mcfg, **k):
+            x, rep = orig_rbi(A, f, mcfg, **k)
+            rec["solves"].append((mcfg.method, mcfg.N, mcfg.delta, x, rep))
+            return x, rep
+
+        ex.lhs_sample, ex.l1roc_offline, ex.rbi_pcg_solve = lhs, off, rbi
+        try:
+            cfg = ex.ExperimentConfig(problem=pid, levels=levels, m0=m0, n_train=n_train,
+                                      n_test=n_test, seed=0, methods=("mgcg", "rbi-mgcg"),
+                                      rb_dims=dims, deltas=deltas, l_max=60)
+            ex.run_experiment(cfg)
+        finally:
+            ex.lhs_sample, ex.l1roc_offline, ex.rbi_pcg_solve = orig_lhs, orig_off, orig_rbi
+        k = f"exp_{tag}"
+        out[f"{k}_train"], out[f"{k}_test"] = rec["lhs"]
+        m = rec["model"]
+        out[f"{k}_colloc"] = m.collocation
+        out[f"{k}_chosen"] = m.chosen_mus
+        out[f"{k}_hist"] = m.indicator_history
+        out[f"{k}_basis"] = m.basis
+        keys = []
+        for i, (method, N, delta, x, rep) in enumerate(rec["solves"]):
+            keys.append(f"{method}|{N}|{delta!r}")
+            out[f"{k}_x{i}"] = x
+            out[f"{k}_it{i}"] = np.array(rep.iterations)
+            out[f"{k}_h{i}"] = np.array(rep.history)
+        out[f"{k}_keys"] = np.array(keys)
+    dest = REPO / "tests/golden/golden_experiment.npz"
+    np.savez_compressed(dest, **out)
+    print(f"wrote {dest} ({dest.stat().st_size/1e6:.2f} MB, {len(out)} arrays)")
+
+
+SIGNATURE_NAMES = ["ParametricProblem", "mg_context_for", "mg_vcycle", "mgcg_solve", "pcg_solve",
+                   "cg_solve", "rbi_pcg_solve", "make_initial_guess", "initial_residual",
+                   "MethodConfig", "l1roc_offline", "l1roc_online", "HighFidelitySolver",
+                   "msrb_train", "lhs_sample", "get_problem"]
+
+
+def main_signatures():
+    """Parameter names / defaults of the reference's public solver API ->
+    tests/golden/ref_signatures.json (the compat layer's signature pin)."""
+    import inspect
+    import json
+    rbws = _import_reference()
+    out = {}
+    for name in SIGNATURE_NAMES:
+        obj = getattr(rbws, name)
+        if inspect.isclass(obj):
+            obj = obj.__init__
+        out[name] = [[p.name, None if p.default is inspect._empty else repr(p.default)]
+                     for p in inspect.signature(obj).parameters.values() if p.name != "self"]
+    dest = REPO / "tests/golden/ref_signatures.json"
+    dest.write_text(json.dumps(out, indent=1))
+    print(f"wrote {dest}")
+
+
 if __name__ == "__main__":
+    if "--signatures" in sys.argv:
+        main_signatures()
+        sys.exit(0)
+    if "--experiment" in sys.argv:
+        main_experiment()
+        sys.exit(0)
     if "--fem2" in sys.argv:
         main_fem2()
         sys.exit(0)
