@@ -204,6 +204,12 @@ int rbws_expand(int n, int count, const double* W, int64_t Wstride, int N, const
 int rbws_deim_step(int n, const double* W, int64_t Wstride, int N, const double* c,
                    const double* v, const uint8_t* excluded, double* col, int64_t* out_idx,
                    double* out_vals, void* stream);
+/* The same DEIM step on full-node vectors ((side)^3 nodes per instance, fem_fn layout of
+ * problems with free boundary nodes, example-2): every node is admissible (Dirichlet nodes
+ * hold zeros; the free x = 1 face keeps its edge nodes, problems.py:63-75). */
+int rbws_deim_step_fn(int side, const double* W, int64_t Wstride, int N, const double* c,
+                      const double* v, const uint8_t* excluded, double* col, int64_t* out_idx,
+                      double* out_vals, void* stream);
 /* Small dense solve A x = b (partial pivoting) on the device, A (dev) [m][m]
  * row-major, b/x (dev) [m] (np.linalg.solve in rb.py:113). */
 int rbws_dense_solve(int m, const double* A, const double* b, double* x, int* status,

@@ -13,7 +13,7 @@ from .krylov import OperatorError, SolveReport, pcg_solve
 from .multigrid import MgContext, mg_context_for, mg_vcycle, mgcg_solve
 from .msrb import MsrbHierarchy, PodBasis, msrb_train, pod_build, rbi_msrbcg_solve
 from .pipeline import HostPipeline
-from .problems import (ProblemSpec, get_problem, sample_mus, smooth_affine,
+from .problems import (ProblemSpec, get_problem, lhs_sample, sample_mus, smooth_affine,
                        thermal_block)
 from .slab import SlabSolver, slab_mgcg_solve, slab_partition
 from .rb import (DegenerateBasisError, L1rocModel, deim_extend, l1_indicator,

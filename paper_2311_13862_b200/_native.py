@@ -60,6 +60,7 @@ SIGNATURES = {
                           _vp, _vp, _vp, _vp],
     "rbws_expand": [_c_int, _c_int, _vp, _c_int64, _c_int, _vp, _vp, _vp],
     "rbws_deim_step": [_c_int, _vp, _c_int64, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "rbws_deim_step_fn": [_c_int, _vp, _c_int64, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "rbws_dense_solve": [_c_int, _vp, _vp, _vp, _vp, _vp],
     "rbws_comm_unique_id": [_vp],
     "rbws_slab_create": [_pp, _vp, _c_int, _c_int, _vp, _c_int, _c_int, _c_double],

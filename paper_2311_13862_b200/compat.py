@@ -565,7 +565,7 @@ def rbi_pcg_solve(A, f, cfg: MethodConfig, mg_ctx: MgContext | None = None,
         if cfg.initializer == "l1roc" and l1roc_model is None:
             raise ValueError(f"{cfg.method} requires a trained over-collocation model")
         p = mg_ctx.problem
-        if residual_log is None and _same_operator(A, mg_ctx) and not p._fn:
+        if residual_log is None and _same_operator(A, mg_ctx):
             t0 = time.perf_counter()
             model = None if l1roc_model is None else l1roc_model.native
             x, reps = _ws.rbi_pcg_solve(_grid.BatchOperator(mg_ctx.native), p.to_device(f),

@@ -353,6 +353,18 @@ int rbws_deim_step(int n, const double* W, int64_t Wstride, int N, const double*
   return 0;
 }
 
+int rbws_deim_step_fn(int side, const double* W, int64_t Wstride, int N, const double* c,
+                      const double* v, const uint8_t* excluded, double* col, int64_t* out_idx,
+                      double* out_vals, void* stream) {
+  void* scratch = nullptr;
+  RBWS_CHECK(cudaMallocAsync(&scratch, rbws::deim_scratch_bytes(side), S(stream)));
+  cudaError_t e = rbws::deim_step(side, W, Wstride, N, c, v, excluded, col, out_idx, out_vals,
+                                  scratch, S(stream), false);
+  cudaFreeAsync(scratch, S(stream));
+  RBWS_CHECK(e);
+  return 0;
+}
+
 int rbws_dense_solve(int m, const double* A, const double* b, double* x, int* status,
                      void* stream) {
   if (m < 1) RBWS_FAIL("empty system");

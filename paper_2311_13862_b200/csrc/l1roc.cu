@@ -238,7 +238,8 @@ __device__ __forceinline__ ArgMax better(ArgMax a, ArgMax b) {
   return a;
 }
 
-__global__ void __launch_bounds__(256) deim_rho_kernel(int n, const double* __restrict__ W,
+__global__ void __launch_bounds__(256) deim_rho_kernel(int n, int ghosts,
+                                                       const double* __restrict__ W,
                                                        int64_t Wstride, int N,
                                                        const double* __restrict__ c,
                                                        const double* __restrict__ v,
@@ -256,7 +257,9 @@ __global__ void __launch_bounds__(256) deim_rho_kernel(int n, const double* __re
     const int i = X % n, j = (X / n) % n, k = X / ((int64_t)n * n);
     double r = v[X];
     for (int q = 0; q < N; ++q) r -= W[q * Wstride + X] * c[q];
-    const bool interior = i && j && k;
+    // padded layout: entries with a zero coordinate are ghosts; full-node layout (ghosts = 0):
+    // every node is admissible (Dirichlet nodes hold zeros, free x = 1 face edges included)
+    const bool interior = !ghosts || (i && j && k);
     if (!interior) r = 0.0;
     rho[X] = r;
     if (interior) {
@@ -327,13 +330,14 @@ __global__ void __launch_bounds__(256) scale_kernel(int64_t n3, double* __restri
 
 cudaError_t deim_step(int n, const double* W, int64_t Wstride, int N, const double* c,
                       const double* v, const uint8_t* excl, double* col, int64_t* out_idx,
-                      double* out_vals, void* scratch, cudaStream_t stream) {
+                      double* out_vals, void* scratch, cudaStream_t stream, bool ghosts) {
   const int64_t n3 = (int64_t)n * n * n;
   const int nb = (int)((n3 + 255) / 256);
   ArgMax* pa = (ArgMax*)scratch;
   double* pm = (double*)(pa + nb);
   count_launch();
-  deim_rho_kernel<<<nb, 256, 0, stream>>>(n, W, Wstride, N, c, v, excl, col, pa, pm);
+  deim_rho_kernel<<<nb, 256, 0, stream>>>(n, ghosts ? 1 : 0, W, Wstride, N, c, v, excl, col,
+                                          pa, pm);
   count_launch();
   deim_final_kernel<<<1, 256, 0, stream>>>(nb, pa, pm, col, out_idx, out_vals);
   count_launch();

@@ -16,7 +16,7 @@ cudaError_t expand(int n, int count, const double* W, int64_t Wstride, int N, co
 size_t deim_scratch_bytes(int n);
 cudaError_t deim_step(int n, const double* W, int64_t Wstride, int N, const double* c,
                       const double* v, const uint8_t* excl, double* col, int64_t* out_idx,
-                      double* out_vals, void* scratch, cudaStream_t stream);
+                      double* out_vals, void* scratch, cudaStream_t stream, bool ghosts = true);
 cudaError_t dense_solve(int m, const double* A, const double* b, double* x, int* status,
                         cudaStream_t stream);
 

@@ -144,11 +144,15 @@ class FnFemProblem:
 
     @property
     def handle(self):
-        """No native hierarchy: the padded-layout entry points (batches, RBI warm starts,
-        L1ROC, HostPipeline) do not take full-node problems yet."""
+        """No native hierarchy object: full-node problems run through FnMgContext (fem_fn),
+        not the padded-layout batch entry points (rbws_batch_*)."""
         raise NotImplementedError(
-            f"{self.spec.pid}: only mg_context_for / mg_vcycle / mgcg_solve are on the "
-            "full-node B200 path (RBI-MGCG on it is a next step, DESIGN.md §5d)")
+            f"{self.spec.pid}: full-node problems have no padded-layout hierarchy handle; "
+            "use mg_context_for / mgcg_solve / rbi_pcg_solve / l1roc_* (fem_fn contexts)")
+
+    def thetas(self, mus):
+        import torch
+        return torch.as_tensor(self.spec.thetas(mus), dtype=torch.float64, device="cuda")
 
     def nodes(self, level=None) -> int:
         c = self.cells[-1 if level is None else level]

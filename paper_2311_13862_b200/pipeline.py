@@ -38,19 +38,20 @@ def schedule(count: int, sub_batch: int, tail: int) -> list[int]:
 class HostPipeline:
     """Solve ``mus`` (host array) into a pinned host buffer, sub-batch by sub-batch.
 
-    ``out_host``: pinned float64 tensor with at least ``len(mus) * n**3``
-    elements; instance m's padded solution (n^3 doubles) lands at
-    ``out_host[m*n^3 : (m+1)*n^3]``.
+    ``out_host``: pinned float64 tensor with at least ``len(mus) * stride``
+    elements; instance m's solution lands at ``out_host[m*stride : (m+1)*stride]`` in the
+    problem's device layout: the padded n^3 block or, for problems with free
+    boundary nodes (example-2), the (c+1)^3 full-node block (``stride`` attribute).
+    Assembled problems (example-1, example-2) have parameter-dependent right-hand sides:
+    each sub-batch's f(mu) is assembled on the host and uploaded inside the call.
     """
 
     def __init__(self, problem: ParametricProblem, method: MethodConfig, model=None,
                  sub_batch: int = 512, nu: int = 1, tail: int | None = None,
                  sizes: list[int] | None = None):
         import torch
+        from .fem_fn import FnFemProblem
         _native.require_cuda()
-        if getattr(problem, "stored", False):
-            raise NotImplementedError("HostPipeline streams one shared rhs; for assembled "
-                                      "problems call rbi_pcg_solve with problem.rhs(mus)")
         if sub_batch < 1:
             raise ValueError("sub_batch must be positive")
         self.problem, self.method, self.model, self.sub = problem, method, model, sub_batch
@@ -60,10 +61,19 @@ class HostPipeline:
             sub_batch = max(sub_batch, max(self.sizes))
             self.sub = sub_batch
         n = problem.n
-        self.ctx = [MgContext(problem, sub_batch, nu=nu) for _ in range(2)]
-        self.x = [torch.empty(padded_len(n, sub_batch), dtype=torch.float64, device="cuda")
-                  for _ in range(2)]
-        self.f = problem.rhs()
+        self.nu = nu
+        self.full_node = isinstance(problem, FnFemProblem)
+        self.per_mu_rhs = self.full_node or getattr(problem, "stored", False)
+        self.stride = problem.nodes() if self.full_node else n ** 3
+        if self.full_node:  # FnMgContext is built per sub-batch (operators + plane factors)
+            self.ctx = [None, None]
+            self.x = [None, None]
+            self.f = None
+        else:
+            self.ctx = [MgContext(problem, sub_batch, nu=nu) for _ in range(2)]
+            self.x = [torch.empty(padded_len(n, sub_batch), dtype=torch.float64, device="cuda")
+                      for _ in range(2)]
+            self.f = None if self.per_mu_rhs else problem.rhs()
         # both streams are side streams: the legacy default stream would serialise
         # with the copies
         self.compute_stream = torch.cuda.Stream()
@@ -97,9 +107,9 @@ class HostPipeline:
         """
         import torch
         mus = np.ascontiguousarray(mus, dtype=np.float64)
-        n3 = self.problem.n ** 3
+        n3 = self.stride
         if out_host.numel() < len(mus) * n3 or not out_host.is_pinned():
-            raise ValueError("out_host must be a pinned buffer of len(mus) * n^3 doubles")
+            raise ValueError("out_host must be a pinned buffer of len(mus) * stride doubles")
         caller = torch.cuda.current_stream()
         compute = self.compute_stream
         compute.wait_stream(caller)
@@ -121,11 +131,27 @@ class HostPipeline:
             s = self._slot          # buffers alternate across calls too
             self._slot ^= 1
             compute.wait_event(self.freed[s])     # buffer s no longer being copied out
-            ctx = mg_context_for(self.problem, part, ctx=self.ctx[s])
             m = len(part)
+            if self.full_node:
+                ctx = mg_context_for(self.problem, part, nu=self.nu)
+                f = self.problem.rhs(part)
+                x, reps = rbi_pcg_solve(BatchOperator(ctx), f, self.method, mg_ctx=ctx,
+                                        l1roc_model=self.model)
+                self.x[s] = x                        # kept alive until its copy is done
+                done = torch.cuda.Event()
+                done.record(compute)
+                self.copy_stream.wait_event(done)
+                with torch.cuda.stream(self.copy_stream):
+                    out_host[c0 * n3:(c0 + m) * n3].copy_(x.reshape(-1), non_blocking=True)
+                reports.append(reps)
+                self.freed[s].record(self.copy_stream)
+                c0 += size
+                continue
+            ctx = mg_context_for(self.problem, part, ctx=self.ctx[s])
+            f = self.problem.rhs(part) if self.per_mu_rhs else self.f
             # each instance's solution streams to the host as soon as it converges,
             # overlapping the iterations of the instances still running
-            x, reps = rbi_pcg_solve(BatchOperator(ctx), self.f, self.method, mg_ctx=ctx,
+            x, reps = rbi_pcg_solve(BatchOperator(ctx), f, self.method, mg_ctx=ctx,
                                     l1roc_model=self.model, x0_out=self.x[s],
                                     out_host=out_host[c0 * n3:(c0 + m) * n3],
                                     copy_stream=self.copy_stream)

@@ -28,6 +28,67 @@ class DegenerateBasisError(Exception):
     """A snapshot or reduced operator was numerically dependent/singular."""
 
 
+# ----------------------------------------------------------------- vector layouts
+
+class PaddedLayout:
+    """Interior (Dirichlet) problems: n^3 padded block per instance (grid.py layout)."""
+
+    full_node = False
+
+    def __init__(self, n: int):
+        self.side = n
+        self.S = n ** 3
+
+    def to_storage(self, idx) -> np.ndarray:
+        return interior_to_padded_index(idx, self.side)
+
+    def from_storage(self, p) -> np.ndarray:
+        return padded_to_interior_index(p, self.side)
+
+    def free_view(self, t, count: int):
+        n = self.side
+        return t[: count * self.S].view(count, n, n, n)[:, 1:, 1:, 1:].reshape(count, -1)
+
+
+class FullNodeLayout:
+    """Problems with free boundary nodes (example-2): all (c+1)^3 nodes per instance,
+    Dirichlet nodes held at zero (fem_fn.py); free DoFs are the nodes ``free`` in order."""
+
+    full_node = True
+
+    def __init__(self, side: int, free: np.ndarray):
+        self.side = side
+        self.S = side ** 3
+        self.free = np.asarray(free, dtype=np.int64)
+
+    def to_storage(self, idx) -> np.ndarray:
+        return self.free[np.asarray(idx, dtype=np.int64)]
+
+    def from_storage(self, p) -> np.ndarray:
+        p = np.asarray(p, dtype=np.int64)
+        i = np.searchsorted(self.free, p)
+        if np.any(i >= len(self.free)) or np.any(self.free[np.minimum(i, len(self.free) - 1)] != p):
+            raise ValueError("storage index is not a free node")
+        return i
+
+    def free_view(self, t, count: int):
+        import torch
+        fr = torch.as_tensor(self.free, device=t.device)
+        return t[: count * self.S].view(count, self.S)[:, fr]
+
+
+def layout_of(problem):
+    from .fem_fn import FnFemProblem
+    if isinstance(problem, FnFemProblem):
+        return FullNodeLayout(problem.cells[-1] + 1, problem.free_by_level[-1])
+    return PaddedLayout(problem.n)
+
+
+def _vec(lay, count: int):
+    import torch
+    return torch.zeros(count * lay.S + 2 * lay.side ** 2, dtype=torch.float64, device="cuda")
+
+
 def l1_indicator(c) -> float:
     """l1 norm of snapshot coordinates (rb.py:129-131)."""
     return float(np.sum(np.abs(np.asarray(c))))
@@ -52,7 +113,12 @@ class L1rocModel:
     indicator_history: np.ndarray
     saturated: bool = False
     chosen: np.ndarray | None = None
+    layout: object = None            # FullNodeLayout for full-node problems (None: padded)
     _cache: dict = field(default_factory=dict, repr=False)
+
+    @property
+    def lay(self):
+        return self.layout if self.layout is not None else PaddedLayout(self.n)
 
     @property
     def dim(self) -> int:
@@ -64,21 +130,18 @@ class L1rocModel:
 
     def basis_numpy(self) -> np.ndarray:
         """(n_free, N) basis in the reference's free-DoF ordering."""
-        n, N = self.n, self.dim
-        blk = self.basis[: N * n ** 3].view(N, n, n, n)[:, 1:, 1:, 1:]
-        return blk.reshape(N, -1).T.cpu().numpy()
+        return self.lay.free_view(self.basis, self.dim).T.cpu().numpy()
 
     def prefix(self, N: int) -> "L1rocModel":
         if not 1 <= N <= self.dim:
             raise ValueError(f"prefix dimension {N} outside [1, {self.dim}]")
-        n = self.n
-        import torch
-        b = torch.zeros(padded_len(n, N), dtype=torch.float64, device="cuda")
-        b[: N * n ** 3] = self.basis[: N * n ** 3]
-        return L1rocModel(n, b, self.transform[:N, :N].copy(), self.collocation[: 2 * N - 1],
+        lay = self.lay
+        b = _vec(lay, N)
+        b[: N * lay.S] = self.basis[: N * lay.S]
+        return L1rocModel(self.n, b, self.transform[:N, :N].copy(), self.collocation[: 2 * N - 1],
                           self.solution_points[:N], self.residual_points[: N - 1],
                           self.chosen_mus[:N], self.indicator_history[:N], self.saturated,
-                          None if self.chosen is None else self.chosen[:N])
+                          None if self.chosen is None else self.chosen[:N], self.layout)
 
     # ---- device-side pieces of the online stage
     def _device(self, problem: ParametricProblem):
@@ -87,12 +150,28 @@ class L1rocModel:
         if key in self._cache:
             return self._cache[key]
         n, N = self.n, self.dim
-        if problem.n != n:
+        lay = self.lay
+        if layout_of(problem).side != n:
             raise ValueError("model and problem grids differ")
-        rows = torch.as_tensor(interior_to_padded_index(self.collocation, n), device="cuda")
+        rows = torch.as_tensor(lay.to_storage(self.collocation), device="cuda")
         M = len(self.collocation)
         Q = problem.spec.n_terms
-        if getattr(problem, "stored", False):
+        if lay.full_node:
+            # full-node problems: A_q W from the batch-shared term coefficients with a unit
+            # theta row per term (rbws_fn_apply_shared), then the collocation rows
+            S, c = lay.S, problem.cells[-1]
+            W = self.basis[: N * S].contiguous()
+            parts = []
+            for q in range(Q):
+                th = torch.zeros(N, Q, dtype=torch.float64, device="cuda")
+                th[:, q] = 1.0
+                y = torch.empty(N * S, dtype=torch.float64, device="cuda")
+                _native.call("rbws_fn_apply_shared", N, Q, c, th.data_ptr(),
+                             problem._coef[-1].data_ptr(), W.data_ptr(), None, y.data_ptr(), 0,
+                             _native.stream_ptr())
+                parts.append(y.view(N, S)[:, rows].T)
+            Bq = torch.stack(parts).contiguous().view(-1)
+        elif getattr(problem, "stored", False):
             # assembled problems: per-term products A_q W from the stored coefficients,
             # then the collocation rows (the affine pieces of rb.py:200-201)
             n3 = n ** 3
@@ -111,12 +190,13 @@ def _online_batch(model: L1rocModel, problem, theta, f, count):
     """a, c, ind, status (device) for a batch; f padded rhs (shared or batch)."""
     import torch
     rows, Bq, T = model._device(problem)
-    n, N, M = model.n, model.dim, len(model.collocation)
-    if f.numel() == padded_len(n, 1):
+    N, M, S = model.dim, len(model.collocation), model.lay.S
+    f = f.reshape(-1)
+    if f.numel() < count * S:  # one rhs shared by the batch
         bs = f[rows].contiguous()
         bstride = 0
     else:
-        bs = f[: count * n ** 3].view(count, n ** 3)[:, rows].contiguous()
+        bs = f[: count * S].view(count, S)[:, rows].contiguous()
         bstride = M
     a = torch.empty(count * N, dtype=torch.float64, device="cuda")
     c = torch.empty(count * N, dtype=torch.float64, device="cuda")
@@ -141,12 +221,14 @@ def l1roc_online(model: L1rocModel, A, b, out=None, coords: bool = True):
     ctx = A.ctx
     problem, count = ctx.problem, ctx.count
     a, c, _, st = _online_batch(model, problem, ctx.theta, b, count)
-    n = model.n
-    x = out if out is not None else torch.empty(padded_len(n, count), dtype=torch.float64,
-                                                device="cuda")
-    _native.call("rbws_expand", n, count, model.basis.data_ptr(), n ** 3, model.dim,
+    lay = model.lay
+    n, S = lay.side, lay.S
+    x = out if out is not None else _vec(lay, count)
+    _native.call("rbws_expand", n, count, model.basis.data_ptr(), S, model.dim,
                  a.data_ptr(), x.data_ptr(), _native.stream_ptr())
-    x[count * n ** 3:] = 0.0
+    x[count * S:] = 0.0
+    if lay.full_node:  # full-node batches are (count, nodes) tensors (fem_fn.py)
+        x = x[: count * S].view(count, S)
     # one host sync, after the expansion is queued (x is discarded if the check fails)
     if np.any(_native.fetch(st) != 0):
         raise DegenerateBasisError("sub-sampled reduced system is rank deficient")
@@ -170,11 +252,13 @@ def deim_extend(n: int, W, X, v, exclude=None) -> DeimStep:
     v: padded single vector.  Returns the normalised column and new index.
     """
     import torch
+    lay = n if hasattr(n, "side") else PaddedLayout(n)
+    n, n3 = lay.side, lay.S
+    v = v.reshape(-1)
     X = list(X)
     N = len(X)
-    n3 = n ** 3
     if N:
-        pX = torch.as_tensor(interior_to_padded_index(X, n), device="cuda")
+        pX = torch.as_tensor(lay.to_storage(X), device="cuda")
         Wm = W[: N * n3].view(N, n3)
         Aint = Wm[:, pX].T.contiguous()          # (N, N): W[X, :]
         bint = v[pX].contiguous()
@@ -188,13 +272,14 @@ def deim_extend(n: int, W, X, v, exclude=None) -> DeimStep:
     else:
         cvec = torch.zeros(1, dtype=torch.float64, device="cuda")
         wptr = v.data_ptr()
-    excl = torch.zeros(padded_len(n, 1), dtype=torch.uint8, device="cuda")
+    excl = torch.zeros(n3 + 2 * n * n, dtype=torch.uint8, device="cuda")
     if exclude:
-        excl[torch.as_tensor(interior_to_padded_index(sorted(exclude), n), device="cuda")] = 1
-    col = torch.zeros(padded_len(n, 1), dtype=torch.float64, device="cuda")
+        excl[torch.as_tensor(lay.to_storage(sorted(exclude)), device="cuda")] = 1
+    col = torch.zeros(n3 + 2 * n * n, dtype=torch.float64, device="cuda")
     idx = torch.zeros(1, dtype=torch.int64, device="cuda")
     vals = torch.zeros(3, dtype=torch.float64, device="cuda")
-    _native.call("rbws_deim_step", n, wptr, n3, N, cvec.data_ptr(), v.data_ptr(), excl.data_ptr(),
+    _native.call("rbws_deim_step_fn" if lay.full_node else "rbws_deim_step", n, wptr, n3, N,
+                 cvec.data_ptr(), v.data_ptr(), excl.data_ptr(),
                  col.data_ptr(), idx.data_ptr(), vals.data_ptr(), _native.stream_ptr())
     pv, maxv, maxrho = (float(t) for t in vals.cpu())
     if maxrho <= 1e-14 * max(maxv, 1e-300):
@@ -202,7 +287,7 @@ def deim_extend(n: int, W, X, v, exclude=None) -> DeimStep:
     pidx = int(idx.item())
     if pidx < 0 or pv == 0.0:
         raise DegenerateBasisError("residual vanishes at all admissible points")
-    index = int(padded_to_interior_index(pidx, n))
+    index = int(lay.from_storage(pidx))
     return DeimStep(col, index, cvec[:N].cpu().numpy() if N else np.zeros(0), pv)
 
 
@@ -224,18 +309,19 @@ def l1roc_offline(mus, N: int, hf_solve, problem: ParametricProblem, seed: int =
     n_train = len(mus)
     if not 1 <= N <= n_train:
         raise ValueError("need 1 <= N <= number of training parameters")
-    n = problem.n
-    n3 = n ** 3
+    lay = layout_of(problem)
+    n, n3 = lay.side, lay.S
     first = int(np.random.default_rng(seed).integers(n_train))
     # one rhs for every training parameter (assembled problems: mu-dependent data) or a
     # shared one
-    stored = getattr(problem, "stored", False)
-    f = problem.rhs(mus) if stored else problem.rhs()
+    per_mu = getattr(problem, "stored", False) or lay.full_node
+    f = problem.rhs(mus).reshape(-1) if per_mu else problem.rhs()
     theta_train = problem.thetas(mus).contiguous()
-    W = torch.zeros(padded_len(n, N), dtype=torch.float64, device="cuda")
-    R = torch.zeros(padded_len(n, max(N - 1, 1)), dtype=torch.float64, device="cuda")
+    W = _vec(lay, N)
+    R = _vec(lay, max(N - 1, 1))
+    model_layout = lay if lay.full_node else None
 
-    step = deim_extend(n, None, [], hf_solve(mus[first]))
+    step = deim_extend(lay, None, [], hf_solve(mus[first]))
     W[:n3] = step.column[:n3]
     T = np.array([[step.pivot]])
     xs, xr, xi = [step.index], [], [step.index]
@@ -246,7 +332,8 @@ def l1roc_offline(mus, N: int, hf_solve, problem: ParametricProblem, seed: int =
     for nn in range(2, N + 1):
         taken = set(xs) | set(xr)
         cur = L1rocModel(n, W, T, np.asarray(xi, np.int64), np.asarray(xs, np.int64),
-                         np.asarray(xr, np.int64), mus[chosen], np.asarray(hist))
+                         np.asarray(xr, np.int64), mus[chosen], np.asarray(hist),
+                         layout=model_layout)
         a, c, ind, st = _online_batch(cur, problem, theta_train, f, n_train)
         if bool((st != 0).any()):
             raise DegenerateBasisError("sub-sampled reduced system is rank deficient")
@@ -262,7 +349,7 @@ def l1roc_offline(mus, N: int, hf_solve, problem: ParametricProblem, seed: int =
         u = hf_solve(mus[pick])
         m = nn - 1  # current basis width
         try:
-            step = deim_extend(n, W, xs, u, exclude=taken)
+            step = deim_extend(lay, W, xs, u, exclude=taken)
         except DegenerateBasisError:
             if on_degenerate != "stop":
                 raise
@@ -274,24 +361,31 @@ def l1roc_offline(mus, N: int, hf_solve, problem: ParametricProblem, seed: int =
         W[m * n3:(m + 1) * n3] = step.column[:n3]
         xs.append(step.index)
         # residual snapshot r = f - A(mu_pick) (W[:, :m] a_pick)
-        ctx1 = mg_context_for(problem, mus[pick][None], ctx=ctx1)
-        upick = torch.zeros(padded_len(n, 1), dtype=torch.float64, device="cuda")
+        upick = _vec(lay, 1)
         apick = a[pick * m:(pick + 1) * m].contiguous()
         _native.call("rbws_expand", n, 1, W.data_ptr(), n3, m, apick.data_ptr(),
                      upick.data_ptr(), _native.stream_ptr())
         upick[n3:] = 0.0
-        Au = torch.zeros_like(upick)
-        _native.call("rbws_apply", ctx1.handle, problem.finest_level, upick.data_ptr(),
-                     Au.data_ptr(), _native.stream_ptr())
-        fp = f[pick * n3:(pick + 1) * n3 + 2 * n * n] if stored else f
+        if lay.full_node:  # point-Jacobi context: operators only, no plane factorizations
+            from .fem_fn import FnMgContext
+            ctx1 = FnMgContext(problem, mus[pick][None], smoother="jacobi")
+            Au = torch.zeros_like(upick)
+            Au[:n3] = ctx1.apply(upick[:n3].view(1, n3)).view(-1)
+        else:
+            ctx1 = mg_context_for(problem, mus[pick][None], ctx=ctx1)
+            Au = torch.zeros_like(upick)
+            _native.call("rbws_apply", ctx1.handle, problem.finest_level, upick.data_ptr(),
+                         Au.data_ptr(), _native.stream_ptr())
+        fp = torch.zeros_like(upick)
+        fp[:n3] = f[pick * n3:(pick + 1) * n3] if per_mu else f[:n3]
         r = fp - Au
-        rstep = deim_extend(n, R if xr else None, xr, r, exclude=taken)
+        rstep = deim_extend(lay, R if xr else None, xr, r, exclude=taken)
         R[len(xr) * n3:(len(xr) + 1) * n3] = rstep.column[:n3]
         xr.append(rstep.index)
         xi.extend([step.index, rstep.index])
     Nf = len(xs)
-    Wf = torch.zeros(padded_len(n, Nf), dtype=torch.float64, device="cuda")
+    Wf = _vec(lay, Nf)
     Wf[: Nf * n3] = W[: Nf * n3]
     return L1rocModel(n, Wf, T, np.asarray(xi, np.int64), np.asarray(xs, np.int64),
                       np.asarray(xr, np.int64), mus[chosen], np.asarray(hist), saturated,
-                      np.asarray(chosen, np.int64))
+                      np.asarray(chosen, np.int64), model_layout)

@@ -65,7 +65,7 @@ def run_experiment_calls(rb, pid, levels, m0, n_train, n_test, dims, deltas, see
 
 @pytest.mark.parametrize("tag,pid,levels,m0,n_train,n_test,dims,deltas,methods", [
     ("ex1", "example-1", 3, 4, 16, 3, (4, 6), (1e-10, 1e-12), ("mgcg", "rbi-mgcg")),
-    ("ex2", "example-2", 3, 4, 12, 3, (4,), (1e-10,), ("mgcg",)),
+    ("ex2", "example-2", 3, 4, 12, 3, (4,), (1e-10,), ("mgcg", "rbi-mgcg")),
 ])
 def test_experiment_loop_matches_reference(tag, pid, levels, m0, n_train, n_test, dims, deltas,
                                            methods):

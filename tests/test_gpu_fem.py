@@ -139,8 +139,8 @@ def test_fem_term_apply_and_streaming(probs):
 
 def test_fem_example2_goes_to_the_full_node_path():
     """The padded stored-coefficient path refuses free boundary nodes; the factory sends
-    example-2 to the full-node path (fem_fn.py, tests/test_gpu_fem_fn.py), whose
-    unsupported calls (RBI warm starts, native batches) fail loudly."""
+    example-2 to the full-node path (fem_fn.py, tests/test_gpu_fem_fn.py), which has no
+    padded-layout hierarchy handle (asking for one fails loudly)."""
     pkg = _pkg()
     from paper_2311_13862_b200.fem import FemProblem
     from paper_2311_13862_b200.fem_fn import FnFemProblem
@@ -183,9 +183,6 @@ def test_fem_l1roc_rbi_mgcg_matches_reference(probs):
 def test_fem_unsupported_paths_fail_loudly(probs):
     pkg = _pkg()
     p = probs["n16m4"]
-    method = pkg.MethodConfig("rbi-mgcg", delta=1e-10, l_max=60, N=2)
-    with pytest.raises(NotImplementedError):
-        pkg.HostPipeline(p, method)
     with pytest.raises(NotImplementedError):
         pkg.msrb_train(G["fem_n16m4_mus"], 2, 1, None, p)
 
