@@ -762,8 +762,17 @@ def run_fem(args, rank, world, dist):
         print(json.dumps(line), flush=True)
 
 
+def _fem2_desc(args):
+    if args.fem2_method == "mgcg":
+        return "zero-init MGCG"
+    return f"RBI-MGCG (L1ROC r={args.fem_r} from {args.fem_train} LHS training parameters)"
+
+
+FEM2_METRIC = {
+    "rbi-mgcg": "warm-started MGCG solves/s to 1e-10 rel. residual (example-2, plane-Jacobi)",
+    "mgcg": "zero-init MGCG solves/s to 1e-10 rel. residual (example-2, plane-Jacobi)"}
 FEM2_WORKLOAD = ("example-2 (the reference's mixed problem: zero-flux face x=1, anisotropic "
-                 "quadrant coefficient, mu-dependent source), {n}^3 cells, m0=4, zero-init MGCG "
+                 "quadrant coefficient, mu-dependent source), {n}^3 cells, m0=4, {m} "
                  "with the plane-Jacobi smoother (reference default), batch {b}, tol 1e-10")
 
 
@@ -780,6 +789,7 @@ def run_fem2(args, rank, world, dist):
         _build.build(verbose=False)
     if dist is not None:
         dist.barrier()
+    import paper_2311_13862_b200 as rb
     from paper_2311_13862_b200 import _native, fem
     from paper_2311_13862_b200.fem_fn import FnFemProblem, _ptr, mg_context_for, mgcg_solve
     from paper_2311_13862_b200.problems import levels_for, lhs_sample
@@ -795,10 +805,23 @@ def run_fem2(args, rank, world, dist):
     test = np.array(lhs_sample(spec.p, batch, spec.bounds, seed=2000 + rank))
     F = prob.rhs(test)
     state = {}
+    rbi = args.fem2_method == "rbi-mgcg"
+    model, t_off = None, 0.0
+    if rbi:  # the reference's rbi-mgcg on Ex.2: L1ROC greedy from an LHS training set
+        train = np.array(lhs_sample(spec.p, args.fem_train, spec.bounds, seed=1000))
+        t0 = time.perf_counter()
+        hf = rb.HighFidelitySolver(prob, delta=1e-14, l_max=100)
+        model = rb.l1roc_offline(train, args.fem_r, hf, prob, seed=0, on_degenerate="stop")
+        torch.cuda.synchronize()
+        t_off = time.perf_counter() - t0
+        log(f"[rank {rank}] example-2 greedy: N={model.dim} in {t_off:.2f}s")
+    cfg = rb.MethodConfig(args.fem2_method, delta=delta, l_max=L_MAX,
+                          N=model.dim if model is not None else 0)
 
     def step(f):
         ctx = mg_context_for(prob, test)
-        x, reps = mgcg_solve(ctx, f, delta=delta, l_max=L_MAX)
+        x, reps = rb.rbi_pcg_solve(rb.BatchOperator(ctx), f, cfg, mg_ctx=ctx,
+                                   l1roc_model=model)
         state["reps"], state["ctx"] = reps, ctx
         return x
 
@@ -823,6 +846,8 @@ def run_fem2(args, rank, world, dist):
     value = world * batch * args.steps / (ms_max / 1e3)
     reps = state["reps"]
     iters = [int(i) for i in reps.iterations]
+    _, zreps = mgcg_solve(state["ctx"], F, delta=delta, l_max=L_MAX)  # untimed reference
+    zero_iters = float(np.mean(zreps.iterations))
 
     # e2e: rhs batch from pinned host memory, free-DoF solutions back to pinned host memory
     fh = F.cpu().pin_memory()
@@ -880,23 +905,28 @@ def run_fem2(args, rank, world, dist):
                 "bytes_per_launch": int(kbytes), "ms_per_launch": round(k_ms, 4)}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = fem2_cpu_baseline(n, m0, test, iters, budget_s=args.cpu_budget)
+        cpu = fem2_cpu_baseline(n, m0, test, iters, budget_s=args.cpu_budget, model=model)
     line = {
-        "metric": "zero-init MGCG solves/s to 1e-10 rel. residual (example-2, plane-Jacobi)",
+        "metric": FEM2_METRIC[args.fem2_method],
         "value": round(value, 2), "unit": "solves/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded LHS parameters, sampling.py:8-27; no dataset)",
-        "config": {"workload": FEM2_WORKLOAD.format(n=n, b=batch),
+        "config": {"workload": FEM2_WORKLOAD.format(n=n, b=batch, m=_fem2_desc(args)),
                    "batch_per_gpu": batch, "grid_cells": n, "levels": levels,
                    "tolerance": delta, "smoother": "plane-jacobi(0.6), nu=1",
                    "layout": "full-node (c+1)^3 per instance", "parallelism": f"parameter-sharded x{world}",
+                   "method": args.fem2_method,
+                   "rb_dim": model.dim if model is not None else 0,
+                   "n_train": args.fem_train if rbi else 0, "t_offline_s": round(t_off, 2),
                    "mean_iterations": round(float(np.mean(iters)), 3), "max_iterations": int(max(iters)),
+                   "mean_iterations_zero_init": round(zero_iters, 3),
                    "all_converged": bool(np.all(reps.converged)),
                    "t_setup_s": round(t_setup, 2), "l2": "inputs larger than L2"},
         "e2e": {"value": round(e2e_value, 2), "unit": "solves/s",
                 "h2d_bytes_per_step": int(F.numel() * 8), "d2h_bytes_per_step": int(F.numel() * 8),
-                "api": "assembled rhs (pinned host) -> fem_fn.mgcg_solve -> pinned host solutions"},
+                "api": "assembled rhs (pinned host) -> rbi_pcg_solve (full-node batch) -> "
+                       "pinned host solutions"},
         "gpu_launches": int(launches), "roofline": roofline, "clocks": clocks.summary(),
     }
     if cpu is not None:
@@ -905,31 +935,35 @@ def run_fem2(args, rank, world, dist):
         print(json.dumps(line), flush=True)
 
 
-def fem2_cpu_baseline(n, m0, test, gpu_iters, budget_s=15.0):
-    """Oracle zero-init MGCG (plane-Jacobi, splu plane factors as the reference) on
-    example-2, single core, on a bounded sample of the batch's parameters."""
+def fem2_cpu_baseline(n, m0, test, gpu_iters, budget_s=15.0, model=None):
+    """Oracle MGCG (plane-Jacobi, splu plane factors as the reference; with ``model`` the
+    L1ROC warm start on the GPU-trained model first) on example-2, single core, on a bounded
+    sample of the batch's parameters."""
     from oracle import fem as of
     from oracle import solvers as so
     from paper_2311_13862_b200.problems import levels_for
     t0 = time.perf_counter()
     op = of.OracleFemProblem(of.Example2(), levels=levels_for(n, m0), m0=m0)
     t_asm = time.perf_counter() - t0
+    omodel = None if model is None else so.OracleL1rocModel(
+        model.basis_numpy(), model.transform, model.collocation, model.solution_points,
+        model.residual_points, np.asarray(model.chosen if model.chosen is not None else []),
+        model.indicator_history, model.saturated)
     done, agree, t_solve = 0, 0, 0.0
     for i, mu in enumerate(test):
         t1 = time.perf_counter()
-        A, f = op.operator(mu), op.rhs(mu)
-        _, rep = so.mgcg_solve(A, f, np.zeros_like(f), so.mg_context_for(op, mu, smoother="auto"),
-                               delta=1e-10, l_max=L_MAX)
+        _, rep = so.rbi_mgcg_solve(op, mu, omodel, delta=1e-10, l_max=L_MAX, smoother="auto")
         t_solve += time.perf_counter() - t1
         done += 1
-        agree += int(rep.iterations == gpu_iters[i])
+        agree += int(abs(rep.iterations - gpu_iters[i]) <= (1 if omodel is not None else 0))
         if t_solve > budget_s:
             break
     return {"value": round(done / t_solve, 4), "unit": "solves/s", "cores": 1, "kind": "port",
-            "sample": f"{done} of the step's parameters, oracle MGCG (operator + rhs + "
-                      f"mg_context_for incl. splu plane factors + MGCG) single-threaded; "
-                      f"assembly {t_asm:.1f}s excluded; iteration counts equal to the GPU: "
-                      f"{agree}/{done}"}
+            "sample": f"{done} of the step's parameters, oracle "
+                      f"{'RBI-MGCG (L1ROC warm start on the GPU-trained model) ' if omodel is not None else 'MGCG '}"
+                      f"(operator + rhs + mg_context_for incl. splu plane factors + MGCG) "
+                      f"single-threaded; assembly {t_asm:.1f}s excluded; iteration counts "
+                      f"agreeing with the GPU: {agree}/{done}"}
 
 
 def fem_cpu_baseline(spec, n, m0, model, test, gpu_iters, budget_s=15.0):
@@ -1066,18 +1100,18 @@ def _ref_fem_solve(mu):
     return rep.iterations
 
 
-def _ref_fem2_init(n, m0):
+def _ref_fem2_init(n, m0, model_state=None):
     _single_thread_blas()
     from oracle import fem as of
+    from oracle import solvers as so
     _W["oprob"] = of.OracleFemProblem(of.Example2(), levels=int(np.log2(n // m0)) + 1, m0=m0)
+    _W["model"] = None if model_state is None else so.OracleL1rocModel(*model_state)
 
 
 def _ref_fem2_solve(mu):
     from oracle import solvers as so
-    op = _W["oprob"]
-    A, f = op.operator(mu), op.rhs(mu)
-    _, rep = so.mgcg_solve(A, f, np.zeros_like(f), so.mg_context_for(op, mu, smoother="auto"),
-                           delta=1e-10, l_max=L_MAX)
+    _, rep = so.rbi_mgcg_solve(_W["oprob"], mu, _W["model"], delta=1e-10, l_max=L_MAX,
+                               smoother="auto")
     return rep.iterations
 
 
@@ -1093,7 +1127,25 @@ def run_reference_fem2(args, world):
     test = np.array(so.lhs_sample(spec.p, args.batch or 64, spec.bounds, seed=2000))
     cores = os.cpu_count() or 1
     sample = cores * max(1, args.ref_per_core)
-    with mp.get_context("fork").Pool(cores, initializer=_ref_fem2_init, initargs=(n, m0)) as pool:
+    state, t_off = None, 0.0
+    if args.fem2_method == "rbi-mgcg":  # the oracle greedy (HighFidelitySolver "mgcg")
+        oprob = of.OracleFemProblem(spec, levels=int(np.log2(n // m0)) + 1, m0=m0)
+        train = np.array(so.lhs_sample(spec.p, args.fem_train, spec.bounds, seed=1000))
+
+        def hf(mu):
+            A, f = oprob.operator(mu), oprob.rhs(mu)
+            x, _ = so.mgcg_solve(A, f, np.zeros_like(f),
+                                 so.mg_context_for(oprob, mu, smoother="auto"), 1e-14, 100)
+            return x
+
+        t0 = time.perf_counter()
+        model = so.l1roc_offline(list(train), args.fem_r, hf, oprob.operator,
+                                 oprob.operator_rows, oprob.rhs, seed=0, on_degenerate="stop")
+        t_off = time.perf_counter() - t0
+        state = (model.basis, model.transform, model.collocation, model.solution_points,
+                 model.residual_points, model.chosen, model.indicator_history, model.saturated)
+    with mp.get_context("fork").Pool(cores, initializer=_ref_fem2_init,
+                                     initargs=(n, m0, state)) as pool:
         k = 0
         for _ in range(args.warmup):
             pool.map(_ref_fem2_solve, [test[(k + i) % len(test)] for i in range(cores)])
@@ -1106,20 +1158,22 @@ def run_reference_fem2(args, world):
         el = time.perf_counter() - t1
     value = args.steps * sample / el
     line = {
-        "metric": "zero-init MGCG solves/s to 1e-10 rel. residual (example-2, plane-Jacobi)",
+        "metric": FEM2_METRIC[args.fem2_method],
         "value": round(value, 4), "unit": "solves/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(el / args.steps * 1e3, 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded LHS parameters, sampling.py:8-27; no dataset)",
         "impl": "reference",
-        "config": {"workload": FEM2_WORKLOAD.format(n=n, b=args.batch or 64),
+        "config": {"workload": FEM2_WORKLOAD.format(n=n, b=args.batch or 64, m=_fem2_desc(args)),
+                   "method": args.fem2_method, "t_offline_s": round(t_off, 1),
                    "mean_iterations": round(float(np.mean(iters)), 3)},
         "cpu_baseline": {"value": round(value, 4), "unit": "solves/s", "cores": cores,
                          "kind": "port",
                          "sample": f"{sample} test parameters per step ({args.ref_per_core} per "
-                                   f"core), oracle restatement of the reference MGCG with the "
-                                   f"plane-Jacobi smoother on example-2 (scipy.sparse, splu "
-                                   f"plane factors), process pool over all host cores"},
+                                   f"core), oracle restatement of the reference "
+                                   f"{args.fem2_method} with the plane-Jacobi smoother on "
+                                   f"example-2 (scipy.sparse, splu plane factors), process "
+                                   f"pool over all host cores"},
         "e2e": {"value": round(value, 4), "unit": "solves/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -1311,6 +1365,8 @@ def main():
                     help="reference problem id: example-1 (RBI-MGCG on its assembled operator) or "
                          "example-2 (zero-init plane-Jacobi MGCG, full-node layout)")
     ap.add_argument("--fem-n", type=int, default=64)
+    ap.add_argument("--fem2-method", default="rbi-mgcg", choices=["rbi-mgcg", "mgcg"],
+                    help="example-2: warm-started (L1ROC) or zero-init MGCG")
     ap.add_argument("--fem-r", type=int, default=10)
     ap.add_argument("--fem-train", type=int, default=256)
     ap.add_argument("--scaling", default="", choices=["", "weak", "strong"],

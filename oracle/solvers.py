@@ -397,10 +397,10 @@ def l1roc_offline(mus, N, hf_solve, operator, operator_rows, rhs, seed=0, on_deg
                             np.asarray(hist), saturated)
 
 
-def rbi_mgcg_solve(problem, mu, model, delta=1e-10, l_max=40, nu=1):
+def rbi_mgcg_solve(problem, mu, model, delta=1e-10, l_max=40, nu=1, smoother="jacobi"):
     """RBI-MGCG: L1ROC warm start then MGCG (warmstart.py:88-117, experiment.py:149-157)."""
     A, f = problem.operator(mu), problem.rhs(mu)
-    ctx = mg_context_for(problem, mu, nu=nu)
+    ctx = mg_context_for(problem, mu, nu=nu, smoother=smoother)
     u0 = np.zeros_like(f) if model is None else l1roc_online(model, A, f)[0]
     return mgcg_solve(A, f, u0, ctx, delta, l_max, mu,
                       "mgcg" if model is None else "rbi-mgcg")
