@@ -30,7 +30,10 @@ constexpr int kMaxDiagChanges = 16;  // DC kernels when the diagonal changes on 
 
 // test/A-B override of the DC choice (rbws_set_kernel_variant): -1 auto, 0 never, 1 whenever
 // the diagonal changes on few enough planes (any N)
-static std::atomic<int> g_force_dc{-1};
+static std::atomic<int> g_force_dc{[] {
+  const char* e = getenv("RBWS_DC");  // A/B runs: "0" never, "1" whenever applicable
+  return e ? atoi(e) : -1;
+}()};
 int fine_set_dc(int v) {
   if (v < -1 || v > 1) return 1;
   g_force_dc.store(v);
@@ -62,6 +65,10 @@ struct FT {
 // threads per CTA of a mode: the prolongation + post-smoothing kernel runs 512-thread
 // CTAs (16-row tiles) at N = 64: half the halo-row work per node, measured -5 %
 int fine_mode_threads(int mode, int n) {
+#ifndef RBWS_PREX_512
+#define RBWS_PREX_512 0
+#endif
+  if (RBWS_PREX_512 && mode == 7 && n == 64) return 512;
   return (mode == 6 && (n == 64 || n == 128)) ? 512 : kThreads;
 }
 
@@ -123,7 +130,8 @@ enum FineMode : int {
 // per node less; bitwise the same values)
 // tile geometry of a mode (see fine_mode_threads)
 template <int MODE, int N>
-using FTM = FT<N, (MODE == FM_POSTP && (N == 64 || N == 128)) ? 512 : kThreads>;
+using FTM = FT<N, ((MODE == FM_POSTP && (N == 64 || N == 128)) ||
+                   (RBWS_PREX_512 && MODE == FM_PREX && N == 64)) ? 512 : kThreads>;
 
 template <int MODE, int N, bool DC = false>
 struct SL {
