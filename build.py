@@ -17,8 +17,10 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 PKG = ROOT / "paper_2311_13862_b200"
 CSRC = PKG / "csrc"
-OBJ = ROOT / "build" / "obj"
-OUT = PKG / "_rbws_b200.so"
+# RBWS_OBJ_DIR / RBWS_OUT: a variant build (A/B experiments, tools/ab_libs.sh) in its own
+# object directory, so the default objects are never mixed with variant ones
+OBJ = Path(os.environ["RBWS_OBJ_DIR"]) if os.environ.get("RBWS_OBJ_DIR") else ROOT / "build" / "obj"
+OUT = Path(os.environ["RBWS_OUT"]) if os.environ.get("RBWS_OUT") else PKG / "_rbws_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CFLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
           "-Xcompiler", "-fPIC", "-Xptxas", "-O3"]

@@ -748,7 +748,12 @@ cudaError_t coarse_launch(int mode, const CoarseOp& op, const double* theta, int
                           const double* x, const double* b, double* y, double omega,
                           const LaunchCtx& lc) {
   if (op.coef) return coarse_stored_launch(mode, op, batch, x, b, y, omega, lc);
-  if (op.tcoef) return stored_shared_launch(mode, op, theta, batch, x, b, y, omega, lc);
+  if (op.tcoef) {
+    if (mode <= 2 && stored_zm_ok(op.n, op.Q, lc))
+      return stored_zm_launch(mode, op.n, op.Q, op.tcoef, theta, op.dinv, batch, x, b, y, omega,
+                              lc);
+    return stored_shared_launch(mode, op, theta, batch, x, b, y, omega, lc);
+  }
   const int n = op.n;
   if (n < 2 || n > 256) return cudaErrorInvalidValue;
   CoarseArgs a{};

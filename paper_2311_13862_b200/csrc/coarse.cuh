@@ -26,6 +26,8 @@ struct CoarseOp {
   // stored-coefficient hierarchy without per-instance coefficients on this level: the
   // per-term coefficients [Q][14][n^3], combined with theta on the fly (shared by the batch)
   const double* tcoef = nullptr;
+  // 1/diag of this level per instance (padded batch), or null (then diag is combined on the fly)
+  const double* dinv = nullptr;
 };
 
 // mode: 0 apply y=Ax | 1 resid y=b-Ax | 2 jacobi y=x+w(b-Ax)/diag | 4 dinv y=1/diag
@@ -44,6 +46,13 @@ cudaError_t stored_combine(int n, int Q, const double* tcoef, const double* thet
 // coarsest level of a stored-coefficient hierarchy: dense operator + Cholesky per instance
 cudaError_t coarse_factor_stored(int n0, int Q, const double* tcoef, const double* theta,
                                  int batch, double* L, int* status, cudaStream_t stream);
+// finest level of a stored-coefficient hierarchy with batch-shared per-term coefficients:
+// z-marching kernel with TMA-staged planes (stored.cu); ok for n in {16,32,64,128}, Q <= 4,
+// whole instances (no slab z-ranges)
+bool stored_zm_ok(int n, int Q, const LaunchCtx& lc);
+cudaError_t stored_zm_launch(int mode, int n, int Q, const double* tcoef, const double* theta,
+                             const double* dinv, int batch, const double* x, const double* b, double* y,
+                             double omega, const LaunchCtx& lc);
 constexpr int kCoarseMaxGroups = 4;  // coarse_kron_kernel<G> instantiations
 // coarsest level: dense Galerkin operator from the factors + Cholesky per instance
 cudaError_t coarse_factor_kf(int n0, int Q, const double* fac, const double* theta, int batch,

@@ -138,6 +138,7 @@ struct Batch {
   CoarseOp cop(int l) const {  // the level's operator with this batch's stored coefficients
     CoarseOp o = h->coarse_op(l);
     o.coef = lv[l].coef;
+    o.dinv = lv[l].dinv;
     return o;
   }
   int vcycle(int lvl, const double* b, double* out, double* dot_partial, const LaunchCtx& lc);
