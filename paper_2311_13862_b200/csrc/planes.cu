@@ -299,6 +299,170 @@ __global__ void __launch_bounds__(256) band_factor_smem_kernel(int64_t nsys, int
   if (threadIdx.x == 0) info[s] = bad;
 }
 
+// Blocked (panel) variant: NB columns per step.  The window holds rows j .. j+w+NB-1 (row r
+// in slot r mod (w+NB)).  Per panel: (1) the NB x NB diagonal block is factored by one warp
+// (lane r = row j+r, columns broadcast by shuffles), (2) the w trailing rows' panel entries
+// are solved against it (one thread per row, L_D entries broadcast from shared memory),
+// (3) the trailing w x w triangle takes the rank-NB update as 4 x 4 register tiles (SYRK),
+// (4) the panel rows leave for HBM (diagonal slot = 1 / L_jj) and the next NB band rows
+// enter.  Four barriers per NB rows instead of two per row; the same arithmetic as the
+// right-looking kernels up to the order of the trailing sums.
+#ifndef RBWS_BF_TPB
+#define RBWS_BF_TPB 128
+#endif
+template <int NB>
+__global__ void __launch_bounds__(RBWS_BF_TPB, 4) band_factor_blk_kernel(int64_t nsys, int64_t M, int w,
+                                                             double* __restrict__ band,
+                                                             int* __restrict__ info) {
+  extern __shared__ double wnd[];
+  const int64_t s = blockIdx.x;
+  if (s >= nsys) return;
+  const int ws = band_ws(w), R = w + NB;
+  double* B = band + s * M * ws;
+  __shared__ int bad;
+  __shared__ double dinvp[NB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) bad = 0;
+  auto row = [&](int64_t r) -> double* { return wnd + (int)(r % R) * ws; };
+  for (int t = tid; t < R * ws; t += blockDim.x) {
+    const int r = t / ws;
+    wnd[t] = r < M ? B[(int64_t)r * ws + t % ws] : 0.0;
+  }
+  __syncthreads();
+  const int TA = (w + 3) / 4, ntiles = TA * (TA + 1) / 2;
+  for (int64_t j = 0; j < M; j += NB) {
+    const int nbe = (int)(M - j < NB ? M - j : NB);
+    // (1) diagonal block
+    if (warp == 0) {
+      double a[NB];
+      double* rr = row(j + (lane < nbe ? lane : 0));
+#pragma unroll
+      for (int c = 0; c < NB; ++c) a[c] = (lane < nbe && c <= lane && lane - c <= w) ? rr[lane - c] : 0.0;
+#pragma unroll
+      for (int c = 0; c < NB; ++c) {
+        if (c < nbe) {
+          const double pv = __shfl_sync(0xffffffffu, a[c], c);
+          const bool ok = pv > 0.0;
+          if (lane == 0 && !ok && !bad) bad = (int)(j + c + 1);
+          // 1/sqrt by the hardware estimate + two Newton steps (no DSQRT / DDIV sequence on
+          // the panel's critical path), L = pv / sqrt(pv)
+          const double q = ok ? pv : 1.0;
+          double inv = rsqrt(q);
+          inv = inv * fma(-0.5 * q, inv * inv, 1.5);
+          inv = inv * fma(-0.5 * q, inv * inv, 1.5);
+          const double L = q * inv;
+          if (lane == c) {
+            a[c] = L;
+            dinvp[c] = inv;
+          } else if (lane > c) {
+            a[c] *= inv;
+          }
+#pragma unroll
+          for (int c2 = c + 1; c2 < NB; ++c2) {
+            const double l2 = __shfl_sync(0xffffffffu, a[c], c2);
+            if (lane >= c2 && c2 < nbe) a[c2] = fma(-a[c], l2, a[c2]);
+          }
+        }
+      }
+      if (lane < nbe) {
+#pragma unroll
+        for (int c = 0; c < NB; ++c)
+          if (c <= lane && lane - c <= w) rr[lane - c] = a[c];
+      }
+    }
+    __syncthreads();
+    // (2) panel entries of the trailing rows
+    const int64_t t0 = j + nbe;
+    for (int tr = tid; tr < w && t0 + tr < M; tr += blockDim.x) {
+      const int64_t rr = t0 + tr;
+      double* rw = row(rr);
+      double x[NB];
+#pragma unroll
+      for (int c = 0; c < NB; ++c) {
+        const int64_t d = rr - j - c;
+        x[c] = (c < nbe && d <= w) ? rw[d] : 0.0;
+      }
+      // column-oriented: x_c is final after its scaling, then eliminated from the later
+      // columns (16 short steps instead of one 120-FMA dependent chain)
+#pragma unroll
+      for (int c = 0; c < NB; ++c) {
+        if (c < nbe) {
+          x[c] *= dinvp[c];
+#pragma unroll
+          for (int c2 = c + 1; c2 < NB; ++c2)
+            if (c2 < nbe && c2 - c <= w) x[c2] = fma(-x[c], row(j + c2)[c2 - c], x[c2]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NB; ++c) {
+        const int64_t d = rr - j - c;
+        if (c < nbe && d <= w) rw[d] = x[c];
+      }
+    }
+    __syncthreads();
+    // (3) trailing update A[t0+a][t0+b] -= sum_c L[t0+a][j+c] L[t0+b][j+c], b <= a < w
+    for (int tt = tid; tt < ntiles; tt += blockDim.x) {
+      int ta = 0;
+      while ((ta + 1) * (ta + 2) / 2 <= tt) ++ta;
+      const int tb = tt - ta * (ta + 1) / 2;
+      double acc[4][4];
+      const double* ra[4];
+      const double* cb[4];
+      int64_t da[4], db[4];
+      bool oka[4], okb[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t rr = t0 + ta * 4 + u, cc = t0 + tb * 4 + u;
+        oka[u] = ta * 4 + u < w && rr < M;
+        okb[u] = tb * 4 + u < w && cc < M;
+        ra[u] = row(oka[u] ? rr : t0);
+        cb[u] = row(okb[u] ? cc : t0);
+        da[u] = rr - j;
+        db[u] = cc - j;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+      }
+      for (int c = 0; c < nbe; ++c) {
+        double pa[4], pb[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          pa[u] = (oka[u] && da[u] - c <= w) ? ra[u][da[u] - c] : 0.0;
+          pb[u] = (okb[u] && db[u] - c <= w) ? cb[u][db[u] - c] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v] = fma(pa[u], pb[v], acc[u][v]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int a = ta * 4 + u;
+        const int64_t rr = t0 + a;
+        if (a >= w || rr >= M) continue;
+        double* rw = row(rr);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int b = tb * 4 + v;
+          if (b <= a) rw[a - b] -= acc[u][v];
+        }
+      }
+    }
+    __syncthreads();
+    // (4) panel rows out (diagonal slot 1 / L_jj), next band rows in
+    for (int t = tid; t < nbe * ws; t += blockDim.x) {
+      const int c = t / ws, d = t % ws;
+      B[(j + c) * ws + d] = d == 0 ? dinvp[c] : row(j + c)[d];
+    }
+    __syncthreads();
+    for (int t = tid; t < nbe * ws; t += blockDim.x) {
+      const int64_t r = j + R + t / ws;
+      row(r)[t % ws] = r < M ? B[r * ws + t % ws] : 0.0;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) info[s] = bad;
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -614,7 +778,17 @@ int rbws_fn_band_factor(int count, int c, int planar, const double* coefA, doubl
   FN_LAUNCHED();
   const int w = band_w(c, planar);
   const size_t wsm = (size_t)(w + 2) * band_ws(w) * sizeof(double);
-  if (wsm <= 200 * 1024 && w < 32 * kFacK && !getenv("RBWS_BAND_FACTOR_GLOBAL")) {
+  static const int blk = [] {  // A/B: RBWS_BAND_FACTOR_BLK=0 keeps the row-by-row kernel
+    const char* e = getenv("RBWS_BAND_FACTOR_BLK");
+    return e ? atoi(e) : 1;
+  }();
+  constexpr int kNB = 16;
+  const size_t bsm = (size_t)(w + kNB) * band_ws(w) * sizeof(double);
+  if (blk && w < 256 && bsm <= 200 * 1024) {
+    RBWS_CUDA_CHECK(rbws::smem_attr((const void*)band_factor_blk_kernel<kNB>, bsm));
+    band_factor_blk_kernel<kNB><<<(unsigned)nsys, RBWS_BF_TPB, bsm, St(stream)>>>(nsys, M, w, band,
+                                                                                 info);
+  } else if (wsm <= 200 * 1024 && w < 32 * kFacK && !getenv("RBWS_BAND_FACTOR_GLOBAL")) {
     RBWS_CUDA_CHECK(rbws::smem_attr((const void*)band_factor_smem_kernel, wsm));
     band_factor_smem_kernel<<<(unsigned)nsys, 256, wsm, St(stream)>>>(nsys, M, w, band, info);
   } else {
