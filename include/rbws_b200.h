@@ -193,6 +193,13 @@ int rbws_l1roc_project(rbws_hierarchy* h, const double* W, int64_t Wstride, int 
 int rbws_l1roc_online(int count, int Q, int M, int N, const double* theta, const double* Bq,
                       const double* bs, int64_t bs_stride, const double* T, double* a,
                       double* c, double* ind, int* status, void* stream);
+/* out[m][a] = W[a] . v[m] for m < count, a < N: the basis projections W^T v of the
+ * multispace preconditioner's Galerkin correction and the POD initial guess (reference
+ * msrb.py:53-85, rb.py:71-83; `b @ W.T`).  W: (dev) N vectors of n3 doubles at stride
+ * Wstride, v: (dev) count vectors at stride vstride, out: (dev) [count][N].  Deterministic
+ * (fixed-order partial sums). */
+int rbws_basis_dot(int64_t n3, int count, const double* W, int64_t Wstride, int N,
+                   const double* v, int64_t vstride, double* out, void* stream);
 /* x[mu] = W a[mu] (rb.py:205 `model.basis @ a`), (dev) padded output. */
 int rbws_expand(int n, int count, const double* W, int64_t Wstride, int N, const double* a,
                 double* x, void* stream);

@@ -58,6 +58,7 @@ SIGNATURES = {
     "rbws_l1roc_project": [_vp, _vp, _c_int64, _c_int, _vp, _c_int, _vp, _vp],
     "rbws_l1roc_online": [_c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _c_int64, _vp, _vp,
                           _vp, _vp, _vp, _vp],
+    "rbws_basis_dot": [_c_int64, _c_int, _vp, _c_int64, _c_int, _vp, _c_int64, _vp, _vp],
     "rbws_expand": [_c_int, _c_int, _vp, _c_int64, _c_int, _vp, _vp, _vp],
     "rbws_deim_step": [_c_int, _vp, _c_int64, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "rbws_deim_step_fn": [_c_int, _vp, _c_int64, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp],

@@ -334,6 +334,18 @@ int rbws_l1roc_online(int count, int Q, int M, int N, const double* theta, const
   return 0;
 }
 
+int rbws_basis_dot(int64_t n3, int count, const double* W, int64_t Wstride, int N,
+                   const double* v, int64_t vstride, double* out, void* stream) {
+  if (N < 1 || count < 1 || n3 < 1) RBWS_FAIL("empty projection");
+  void* scratch = nullptr;
+  RBWS_CHECK(cudaMallocAsync(&scratch, rbws::basis_dot_scratch(n3, count, N), S(stream)));
+  cudaError_t e = rbws::basis_dot(n3, count, W, Wstride, N, v, vstride, out,
+                                  static_cast<double*>(scratch), S(stream));
+  cudaFreeAsync(scratch, S(stream));
+  RBWS_CHECK(e);
+  return 0;
+}
+
 int rbws_expand(int n, int count, const double* W, int64_t Wstride, int N, const double* a,
                 double* x, void* stream) {
   if (N < 1) RBWS_FAIL("empty basis");

@@ -226,6 +226,94 @@ cudaError_t expand(int n, int count, const double* W, int64_t Wstride, int N, co
   return cudaErrorInvalidValue;
 }
 
+// ---------------------------------------------------------------- basis projection
+// out[m][a] = sum_x W[a][x] v[m][x]: the W^T v of the multispace preconditioner's Galerkin
+// correction (reference msrb.py:53-85, rb.py:71-83).  Tall-skinny and memory-bound: a CTA
+// takes a chunk of x for IB instances and NB basis vectors (IB x NB accumulators per
+// thread); instance groups are the fastest grid dimension, so the basis chunk is an L2 hit
+// for every group after the first and HBM sees v and W once.  Per-CTA sums go to fixed
+// slots and are added in a fixed order (deterministic).
+#ifndef RBWS_DOT_EPT
+#define RBWS_DOT_EPT 32
+#endif
+constexpr int kDotIB = 4, kDotNB = 8, kDotEPT = RBWS_DOT_EPT;
+__global__ void __launch_bounds__(256) basis_dot_kernel(int64_t n3, int count,
+                                                        const double* __restrict__ W,
+                                                        int64_t Wstride, int N,
+                                                        const double* __restrict__ v,
+                                                        int64_t vstride,
+                                                        double* __restrict__ part) {
+  const int m0 = blockIdx.x * kDotIB, xc = blockIdx.y, a0 = blockIdx.z * kDotNB;
+  const int64_t x0 = (int64_t)xc * 256 * kDotEPT;
+  double acc[kDotIB][kDotNB];
+#pragma unroll
+  for (int u = 0; u < kDotIB; ++u)
+#pragma unroll
+    for (int a = 0; a < kDotNB; ++a) acc[u][a] = 0.0;
+#pragma unroll
+  for (int e = 0; e < kDotEPT; ++e) {
+    const int64_t x = x0 + e * 256 + threadIdx.x;
+    if (x >= n3) break;
+    double wv[kDotNB], vv[kDotIB];
+#pragma unroll
+    for (int a = 0; a < kDotNB; ++a) wv[a] = (a0 + a < N) ? __ldg(W + (int64_t)(a0 + a) * Wstride + x) : 0.0;
+#pragma unroll
+    for (int u = 0; u < kDotIB; ++u) vv[u] = (m0 + u < count) ? __ldg(v + (int64_t)(m0 + u) * vstride + x) : 0.0;
+#pragma unroll
+    for (int u = 0; u < kDotIB; ++u)
+#pragma unroll
+      for (int a = 0; a < kDotNB; ++a) acc[u][a] = fma(wv[a], vv[u], acc[u][a]);
+  }
+  __shared__ double red[8][kDotIB * kDotNB];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int u = 0; u < kDotIB; ++u)
+#pragma unroll
+    for (int a = 0; a < kDotNB; ++a) {
+      double s = acc[u][a];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+      if (lane == 0) red[warp][u * kDotNB + a] = s;
+    }
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t < kDotIB * kDotNB) {
+    double s = 0.0;
+    for (int w8 = 0; w8 < 8; ++w8) s += red[w8][t];
+    const int u = t / kDotNB, a = t % kDotNB;
+    if (m0 + u < count && a0 + a < N)
+      part[((int64_t)(m0 + u) * N + a0 + a) * gridDim.y + xc] = s;
+  }
+}
+
+__global__ void basis_dot_final_kernel(int total, int nchunks, const double* __restrict__ part,
+                                       double* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  double s = 0.0;
+  for (int c = 0; c < nchunks; ++c) s += part[(int64_t)t * nchunks + c];
+  out[t] = s;
+}
+
+size_t basis_dot_scratch(int64_t n3, int count, int N) {
+  const int64_t chunks = (n3 + 256 * kDotEPT - 1) / (256 * kDotEPT);
+  return (size_t)count * N * chunks * sizeof(double);
+}
+
+cudaError_t basis_dot(int64_t n3, int count, const double* W, int64_t Wstride, int N,
+                      const double* v, int64_t vstride, double* out, double* scratch,
+                      cudaStream_t stream) {
+  const int64_t chunks = (n3 + 256 * kDotEPT - 1) / (256 * kDotEPT);
+  dim3 grd((unsigned)((count + kDotIB - 1) / kDotIB), (unsigned)chunks,
+           (unsigned)((N + kDotNB - 1) / kDotNB));
+  count_launch();
+  basis_dot_kernel<<<grd, 256, 0, stream>>>(n3, count, W, Wstride, N, v, vstride, scratch);
+  const int total = count * N;
+  count_launch();
+  basis_dot_final_kernel<<<(total + 127) / 128, 128, 0, stream>>>(total, (int)chunks, scratch, out);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- DEIM step
 struct ArgMax {
   double v;

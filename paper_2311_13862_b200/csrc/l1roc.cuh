@@ -13,6 +13,11 @@ cudaError_t l1roc_online(int count, int Q, int M, int N, const double* theta, co
                          double* c, double* ind, int* status, cudaStream_t stream);
 cudaError_t expand(int n, int count, const double* W, int64_t Wstride, int N, const double* a,
                    double* x, cudaStream_t stream);
+// out[m][a] = W[a] . v[m] (count x N, dev), per-chunk partials in scratch
+size_t basis_dot_scratch(int64_t n3, int count, int N);
+cudaError_t basis_dot(int64_t n3, int count, const double* W, int64_t Wstride, int N,
+                      const double* v, int64_t vstride, double* out, double* scratch,
+                      cudaStream_t stream);
 size_t deim_scratch_bytes(int n);
 cudaError_t deim_step(int n, const double* W, int64_t Wstride, int N, const double* c,
                       const double* v, const uint8_t* excl, double* col, int64_t* out_idx,

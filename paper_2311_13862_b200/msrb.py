@@ -72,7 +72,7 @@ class _Reduced:
     def __init__(self, problem, W):
         import torch
         n, N, Q = problem.n, int(W.shape[0]), problem.spec.n_terms
-        self.W, self.N = W, N
+        self.W, self.N, self.n = W, N, n
         if N == 0:
             self.red = None
             return
@@ -98,10 +98,22 @@ class _Reduced:
         return L
 
     def solve(self, L, b):
-        """W (A_N)^{-1} W^T b for every instance row of b (count, n^3)."""
+        """W (A_N)^{-1} W^T b for every instance row of b (count, n^3): the projections
+        W^T b (rbws_basis_dot) and the expansion W t (rbws_expand) are the library's
+        memory-bound kernels; the N x N Cholesky solves are per-instance torch calls."""
         import torch
-        t = torch.cholesky_solve((b @ self.W.T).unsqueeze(-1), L).squeeze(-1)
-        return t @ self.W
+        count, n3 = b.shape
+        N = self.N
+        Wc = self.W.contiguous()
+        t = torch.empty(count, N, dtype=torch.float64, device="cuda")
+        st = _native.stream_ptr()
+        _native.call("rbws_basis_dot", n3, count, Wc.data_ptr(), Wc.stride(0), N, b.data_ptr(),
+                     b.stride(0), t.data_ptr(), st)
+        t = torch.cholesky_solve(t.unsqueeze(-1), L).squeeze(-1).contiguous()
+        out = torch.empty(count * n3 + 2 * self.n * self.n, dtype=torch.float64, device="cuda")
+        _native.call("rbws_expand", self.n, count, Wc.data_ptr(), Wc.stride(0), N, t.data_ptr(),
+                     out.data_ptr(), st)
+        return out[: count * n3].view(count, n3)
 
 
 @dataclass
@@ -238,8 +250,8 @@ def rbi_msrbcg_solve(problem, mus, hier: MsrbHierarchy, f=None, delta: float = 1
     scale = torch.where(absolute, torch.ones_like(fn), fn)
     r = f - ops.apply(x)
     rel = torch.linalg.vector_norm(r, dim=1) / scale
-    hist = [rel.cpu().numpy()]
-    iters = np.zeros(cnt, dtype=np.int32)
+    hist = [rel]  # device tensors, copied to the host once at the end
+    iters_d = torch.zeros(cnt, dtype=torch.int32, device="cuda")
     active = (rel > delta) if l_max > 0 else torch.zeros_like(rel, dtype=torch.bool)
     status = np.zeros(cnt, dtype=np.int32)
     if bool(active.any()):
@@ -259,11 +271,8 @@ def rbi_msrbcg_solve(problem, mus, hier: MsrbHierarchy, f=None, delta: float = 1
             r = r - alpha[:, None] * Ap
             k += 1
             rel_k = torch.linalg.vector_norm(r, dim=1) / scale
-            act_h = active.cpu().numpy()
-            iters[act_h] = k
-            h = np.full(cnt, np.nan)
-            h[act_h] = rel_k.cpu().numpy()[act_h]
-            hist.append(h)
+            iters_d = torch.where(active, torch.full_like(iters_d, k), iters_d)
+            hist.append(torch.where(active, rel_k, torch.full_like(rel_k, float("nan"))))
             active = active & (rel_k > delta)
             if not bool(active.any()) or k >= l_max:
                 break
@@ -274,9 +283,10 @@ def rbi_msrbcg_solve(problem, mus, hier: MsrbHierarchy, f=None, delta: float = 1
             rs = rs_new
     tres = (torch.linalg.vector_norm(f - ops.apply(x), dim=1) / scale).cpu().numpy()
     status |= np.where(absolute.cpu().numpy(), 4, 0).astype(np.int32)
+    iters = iters_d.cpu().numpy()
     H = np.full((cnt, l_max + 1), np.nan)
-    for j, h in enumerate(hist):
-        H[:, j] = h
+    Hd = torch.stack(hist, 1).cpu().numpy()
+    H[:, : Hd.shape[1]] = Hd
     reps = SolveReports(method, iters, H, tres, status, time.perf_counter() - t0, delta, l_max,
                         mus, {"batch": cnt, "smoother": "gauss-seidel-symmetric",
                               "K_max": hier.K_max, "N": hier.N})

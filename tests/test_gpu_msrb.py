@@ -74,3 +74,23 @@ def test_rbi_msrbcg_matches_reference(gm, trained):
         ref = gm["msrb_tb221_n16_x"][m]
         assert np.linalg.norm(got[m] - ref) <= 1e-5 * np.linalg.norm(ref)
         assert reps[m].config["preconditioner"] == "msrb"
+
+
+def test_basis_dot_kernel_matches_matmul():
+    """rbws_basis_dot (W^T v of the MSRB correction) against a plain fp64 torch matmul,
+    shared (stride 0) and per-instance right-hand sides, N above one 8-vector chunk."""
+    from paper_2311_13862_b200 import _native
+    g = torch.Generator(device="cuda").manual_seed(3)
+    n3, count, N = 33 * 33 * 33 + 17, 13, 11
+    W = torch.randn(N, n3, generator=g, device="cuda", dtype=torch.float64)
+    v = torch.randn(count, n3, generator=g, device="cuda", dtype=torch.float64)
+    for vv, stride in ((v, n3), (v[:1].expand(count, n3), 0)):
+        out = torch.empty(count, N, dtype=torch.float64, device="cuda")
+        _native.call("rbws_basis_dot", n3, count, W.data_ptr(), n3, N, vv.data_ptr(), stride,
+                     out.data_ptr(), 0)
+        ref = vv @ W.T
+        assert torch.allclose(out, ref, rtol=1e-12, atol=1e-10)
+        out2 = torch.empty_like(out)
+        _native.call("rbws_basis_dot", n3, count, W.data_ptr(), n3, N, vv.data_ptr(), stride,
+                     out2.data_ptr(), 0)
+        assert torch.equal(out, out2)  # fixed-order partial sums
