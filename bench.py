@@ -38,16 +38,17 @@ METRIC = "warm-started MGCG solves/s to 1e-10 rel. residual; stencil HBM GB/s vs
 # BASELINE.json configs (index = position in "configs")
 CONFIGS = {
     0: dict(workload="thermal-block 2x1x1, 32^3 cells, r=10 from 256 train, batch 64, tol 1e-10",
-            kind="tb", blocks=(2, 1, 1), n=32, m0=4, r=10, n_train=256, batch=64, delta=1e-10),
+            kind="tb", blocks=(2, 1, 1), n=32, m0=4, r=10, n_train=256, batch=64, delta=1e-10,
+            degenerate="stop"),
     1: dict(workload="thermal-block 2x2x1, 64^3 cells, r=20 from 1024 train, batch 1024, tol 1e-10",
             kind="tb", blocks=(2, 2, 1), n=64, m0=4, r=20, n_train=1024, batch=1024, delta=1e-10,
             e2e_sizes=[1024]),
     2: dict(workload="thermal-block 2x2x2, 128^3 cells, r=30 from 4096 train, batch 512, tol 1e-12",
             kind="tb", blocks=(2, 2, 2), n=128, m0=4, r=30, n_train=4096, batch=512, delta=1e-12,
-            scaling="strong"),
+            scaling="strong", degenerate="stop"),
     3: dict(workload="smooth affine (6 modes), 256^3 cells, r=40 from 2048 train, batch 128, tol 1e-12",
             kind="smooth", blocks=None, n=256, m0=4, r=40, n_train=2048, batch=128, delta=1e-12,
-            chunk=64, e2e_sub=32),
+            chunk=64, e2e_sub=32, degenerate="stop"),
     4: dict(workload="thermal-block 2x2x2, 512^3 cells, one instance slab-decomposed along z "
                      "(one slab per GPU); RB warm start r=30 from 4096 train at 128^3, prolonged; "
                      "tol 1e-10",
@@ -203,7 +204,11 @@ def run_b200(args, rank, world, dist):
 
     t0 = time.perf_counter()
     hf = rb.HighFidelitySolver(prob, delta=1e-14, l_max=100)
-    model = rb.l1roc_offline(train, cfg["r"], hf, prob, seed=0, on_degenerate="stop")
+    # the reference raises on a snapshot numerically inside the basis (rb.py:116-117); the
+    # configs whose greedy reaches that (degenerate="stop") end it there instead, flagged as
+    # saturated in the model (configs[1] keeps the reference behaviour)
+    model = rb.l1roc_offline(train, cfg["r"], hf, prob, seed=0,
+                             on_degenerate=cfg.get("degenerate", "raise"))
     torch.cuda.synchronize()
     t_off = time.perf_counter() - t0
     log(f"[rank {rank}] offline greedy: N={model.dim} saturated={model.saturated} "
@@ -1048,7 +1053,7 @@ def run_reference(args, rank, world):
 
     t0 = time.perf_counter()
     model = so.l1roc_offline(list(train), cfg["r"], hf, oprob.operator, oprob.operator_rows,
-                             oprob.rhs, seed=0, on_degenerate="stop")
+                             oprob.rhs, seed=0, on_degenerate=cfg.get("degenerate", "raise"))
     t_off = time.perf_counter() - t0
     log(f"[reference] offline greedy N={model.dim} in {t_off:.1f}s")
     state = (model.basis, model.transform, model.collocation, model.solution_points,
@@ -1346,7 +1351,7 @@ def _spawn_ranks(n):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", type=int, default=1)

@@ -49,6 +49,8 @@ cudaError_t l1roc_project(int n, int Q, const double* face, const double* node, 
 }
 
 // ---------------------------------------------------------------- online LS
+__device__ __forceinline__ bool warp_id_is_zero() { return (threadIdx.x >> 5) == 0; }
+
 // one block per instance; Householder QR of the M x N sampled matrix in smem
 __global__ void __launch_bounds__(128) l1roc_online_kernel(int M, int N, int Q,
                                                            const double* __restrict__ theta,
@@ -65,6 +67,9 @@ __global__ void __launch_bounds__(128) l1roc_online_kernel(int M, int N, int Q,
   double* rhs = B + M * N;      // [M]
   double* red = rhs + M;        // [32]
   double* sol = red + 32;       // [N]
+  double* Rw = sol + N;         // [N][N] scratch: R^-1 (rank certificate) / Jacobi SVD
+  __shared__ int s_bad;
+  __shared__ double s_cert[2];
   const int mu = blockIdx.x;
   const int tid = threadIdx.x;
   const double* th = theta + (int64_t)mu * Q;
@@ -76,7 +81,6 @@ __global__ void __launch_bounds__(128) l1roc_online_kernel(int M, int N, int Q,
   }
   for (int m = tid; m < M; m += blockDim.x) rhs[m] = bs[mu * bs_stride + m];
   __syncthreads();
-  double rmax = 0.0;
   int bad = 0;
   for (int j = 0; j < N; ++j) {
     double* col = B + j * M;
@@ -115,11 +119,104 @@ __global__ void __launch_bounds__(128) l1roc_online_kernel(int M, int N, int Q,
     if (tid == 0) col[j] = alpha;  // R_jj (below-diagonal part of v no longer needed)
     __syncthreads();
   }
+  // ---- rank test with numpy's lstsq rule (rb.py:174-179: SVD, rcond = eps max(M, N),
+  // rank = #{s_i > rcond s_max}).  Certificate first: s_max <= ||R||_F and
+  // s_min >= 1 / ||R^-1||_F, so 1/||R^-1||_F > rcond ||R||_F proves full rank; otherwise the
+  // singular values of R are computed (one-sided Jacobi, warp 0) and counted.
+  const double rcond = DBL_EPSILON * (double)(M > N ? M : N);
+  {
+    double fr = 0.0;
+    int zero = 0;
+    for (int t = tid; t < N * N; t += blockDim.x) {
+      const int r = t % N, c = t / N;
+      const double v = (r <= c) ? B[c * M + r] : 0.0;
+      fr = fma(v, v, fr);
+      if (r == c && v == 0.0) zero = 1;
+    }
+    const double frs = block_reduce_sum(fr, red);
+    if (tid == 0) {
+      s_cert[0] = frs;
+      s_bad = 0;
+    }
+    __syncthreads();
+    if (zero) s_bad = 2;  // exactly singular R: s_min = 0
+    __syncthreads();
+    // ||R^-1||_F^2: column k of R^-1 by back substitution (one thread per column)
+    double inv2 = 0.0;
+    if (s_bad == 0) {
+      for (int k = tid; k < N; k += blockDim.x) {
+        double* x = Rw + k * N;
+        for (int r = N - 1; r >= 0; --r) {
+          double v = (r == k) ? 1.0 : 0.0;
+          if (r <= k)
+            for (int c = r + 1; c <= k; ++c) v -= B[c * M + r] * x[c];
+          x[r] = (r <= k) ? v / B[r * M + r] : 0.0;
+          inv2 = fma(x[r], x[r], inv2);
+        }
+      }
+    }
+    const double inv2s = block_reduce_sum(inv2, red);
+    if (tid == 0) s_cert[1] = inv2s;
+    __syncthreads();
+    const bool certain = s_bad == 0 && 1.0 / sqrt(s_cert[1]) > rcond * sqrt(s_cert[0]);
+    if (!certain && warp_id_is_zero()) {
+      // one-sided Jacobi on the columns of R (lanes over rows), cyclic pair order
+      const int lane = tid & 31;
+      for (int t = lane; t < N * N; t += 32) {
+        const int r = t % N, c = t / N;
+        Rw[c * N + r] = (r <= c) ? B[c * M + r] : 0.0;
+      }
+      __syncwarp();
+      for (int sweep = 0; sweep < 40; ++sweep) {
+        int rotated = 0;
+        for (int p = 0; p < N - 1; ++p)
+          for (int q = p + 1; q < N; ++q) {
+            double al = 0.0, be = 0.0, ga = 0.0;
+            for (int r = lane; r < N; r += 32) {
+              const double xp = Rw[p * N + r], xq = Rw[q * N + r];
+              al = fma(xp, xp, al);
+              be = fma(xq, xq, be);
+              ga = fma(xp, xq, ga);
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+              al += __shfl_xor_sync(0xffffffffu, al, o);
+              be += __shfl_xor_sync(0xffffffffu, be, o);
+              ga += __shfl_xor_sync(0xffffffffu, ga, o);
+            }
+            if (fabs(ga) <= DBL_EPSILON * sqrt(al * be) || ga == 0.0) continue;
+            rotated = 1;
+            const double zeta = (be - al) / (2.0 * ga);
+            const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
+            for (int r = lane; r < N; r += 32) {
+              const double xp = Rw[p * N + r], xq = Rw[q * N + r];
+              Rw[p * N + r] = cs * xp - sn * xq;
+              Rw[q * N + r] = sn * xp + cs * xq;
+            }
+            __syncwarp();
+          }
+        if (!rotated) break;
+      }
+      // singular values = column norms
+      double smax = 0.0;
+      for (int c = 0; c < N; ++c) {
+        double v = 0.0;
+        for (int r = lane; r < N; r += 32) v = fma(Rw[c * N + r], Rw[c * N + r], v);
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        smax = fmax(smax, sqrt(v));
+        if (lane == 0) sol[c] = sqrt(v);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        int rank = 0;
+        for (int c = 0; c < N; ++c) rank += sol[c] > rcond * smax ? 1 : 0;
+        s_bad = rank < N ? 1 : 0;
+      }
+    }
+    __syncthreads();
+    bad = s_bad != 0;
+  }
   if (tid == 0) {
-    for (int j = 0; j < N; ++j) rmax = fmax(rmax, fabs(B[j * M + j]));
-    const double tol = rmax * DBL_EPSILON * (double)(M > N ? M : N);
-    for (int j = 0; j < N; ++j)
-      if (!(fabs(B[j * M + j]) > tol)) bad = 1;
     // back substitution R a = (Q^T b)[0:N]
     for (int j = N - 1; j >= 0; --j) {
       double s = rhs[j];
@@ -147,7 +244,7 @@ __global__ void __launch_bounds__(128) l1roc_online_kernel(int M, int N, int Q,
 cudaError_t l1roc_online(int count, int Q, int M, int N, const double* theta, const double* Bq,
                          const double* bs, int64_t bs_stride, const double* T, double* a,
                          double* c, double* ind, int* status, cudaStream_t stream) {
-  const size_t smem = sizeof(double) * ((size_t)M * N + M + 32 + N);
+  const size_t smem = sizeof(double) * ((size_t)M * N + M + 32 + N + (size_t)N * N);
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(l1roc_online_kernel,

@@ -487,3 +487,37 @@ def test_stored_weight_kernels_match_register_kernels(monkeypatch):
     for h0, h1 in zip(out[0][1], out[1][1]):
         assert len(h0) == len(h1)
         np.testing.assert_allclose(h0, h1, rtol=1e-9)
+
+
+def test_l1roc_rank_test_follows_numpy_lstsq():
+    """The online least squares declares rank deficiency exactly when numpy's lstsq
+    (SVD, rcond = eps max(M, N); reference rb.py:174-179) reports rank < N: sampled
+    matrices with a smallest singular value just above / below the threshold, and a
+    well-conditioned one (the unpivoted-QR diagonal test disagreed)."""
+    from paper_2311_13862_b200 import _native
+    M, N = 7, 4
+    rng = np.random.default_rng(11)
+    U, _ = np.linalg.qr(rng.standard_normal((M, M)))
+    V, _ = np.linalg.qr(rng.standard_normal((N, N)))
+    rc = np.finfo(float).eps * max(M, N)
+    svals = [[1.0, 0.5, 0.2, 0.1], [1.0, 1e-3, 1e-9, 0.3 * rc], [1.0, 1e-3, 1e-9, 3.0 * rc],
+             [1.0, 1e-3, 1e-9, 1e-12], [1.0, 0.0, 0.5, 0.2]]
+    Bs = [U[:, :N] @ np.diag(s) @ V.T for s in svals]
+    Q = count = len(Bs)
+    theta = torch.eye(count, dtype=torch.float64, device="cuda").contiguous()
+    Bq = torch.as_tensor(np.stack(Bs), device="cuda").contiguous()
+    bs = torch.as_tensor(rng.standard_normal((count, M)), device="cuda").contiguous()
+    T = torch.eye(N, dtype=torch.float64, device="cuda")
+    a = torch.zeros(count * N, dtype=torch.float64, device="cuda")
+    c = torch.zeros_like(a)
+    ind = torch.zeros(count, dtype=torch.float64, device="cuda")
+    st = torch.zeros(count, dtype=torch.int32, device="cuda")
+    _native.call("rbws_l1roc_online", count, Q, M, N, theta.data_ptr(), Bq.data_ptr(),
+                 bs.data_ptr(), M, T.data_ptr(), a.data_ptr(), c.data_ptr(), ind.data_ptr(),
+                 st.data_ptr(), 0)
+    got = st.cpu().numpy()
+    for m, B in enumerate(Bs):
+        sol, _, rank, _ = np.linalg.lstsq(B, bs[m].cpu().numpy(), rcond=None)
+        assert bool(got[m]) == (rank < N), (m, got[m], rank)
+        if rank == N and np.linalg.cond(B) < 1e6:
+            np.testing.assert_allclose(a.view(count, N)[m].cpu().numpy(), sol, rtol=1e-10)
