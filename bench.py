@@ -340,6 +340,15 @@ def run_b200(args, rank, world, dist):
         if k in class_bytes:
             gbs = class_bytes[k] * nodes * punits[k] / (pms[k] / 1e3) / 1e9
             row["achieved_gbs"] = round(gbs, 1)
+        elif CLASS_NAMES[k] == "coarse_levels":
+            # algorithmic bytes of one V-cycle's coarse levels per instance: 76 B per node
+            # of every smoothed coarse level (pre-smoothing residual 24, restriction 11,
+            # prolongation 17, post-smoothing 24) + the coarsest Cholesky solve
+            m0 = prob.cells[0]
+            cb = sum(76.0 * (c - 1) ** 3 for c in prob.cells[1:-1]) + \
+                8.0 * ((m0 - 1) ** 6 + 2 * (m0 - 1) ** 3)
+            row["achieved_gbs"] = round(cb * punits[k] / (pms[k] / 1e3) / 1e9, 1)
+            row["bytes_per_instance"] = cb
         table[CLASS_NAMES[k]] = row
     ran = [k for k in class_bytes if pcalls[k]]
     if ran:
