@@ -286,6 +286,15 @@ int rbws_fn_band_factor(int count, int c, int planar, const double* coefA, doubl
  * (plane-Jacobi sweep, multigrid.py:91-95; cho_solve, multigrid.py:216) */
 int rbws_fn_band_solve(int count, int c, int planar, const double* band, double* r, double* x,
                        double omega, int mode, void* stream);
+/* The band factor transposed (bandT[i][d] = L[i+d][i], the columns of L as rows), for the
+ * scatter-form forward substitution of rbws_fn_band_solve_t; same size as the band. */
+int rbws_fn_band_transpose(int count, int c, int planar, const double* band, double* bandT,
+                           void* stream);
+/* rbws_fn_band_solve with both substitutions in scatter form (rows of bandT forward, rows of
+ * band backward), one warp per system, rows owned round-robin by the lanes: no dot-product
+ * reduction on the dependency chain.  Same arguments and results (up to rounding). */
+int rbws_fn_band_solve_t(int count, int c, int planar, const double* band, const double* bandT,
+                         double* r, double* x, double omega, int mode, void* stream);
 /* one block Gauss-Seidel sweep over the z-planes of x (ascending if forward, else
  * descending): x_p = A_pp^-1 (b_p - A[p,p-1] x_{p-1} - A[p,p+1] x_{p+1}) with the plane
  * factors of rbws_fn_band_factor(planar = 1); scratch >= count (c+1)^2 doubles —

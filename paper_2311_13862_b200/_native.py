@@ -79,6 +79,8 @@ SIGNATURES = {
     "rbws_fn_band_doubles": [_c_int, _c_int, _c_int],
     "rbws_fn_band_factor": [_c_int, _c_int, _c_int, _vp, _vp, _vp, _vp],
     "rbws_fn_band_solve": [_c_int, _c_int, _c_int, _vp, _vp, _vp, _c_double, _c_int, _vp],
+    "rbws_fn_band_transpose": [_c_int, _c_int, _c_int, _vp, _vp, _vp],
+    "rbws_fn_band_solve_t": [_c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _c_double, _c_int, _vp],
     "rbws_fn_plane_gs_sweep": [_c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _c_int, _vp],
     "rbws_fn_restrict": [_c_int, _c_int, _vp, _vp, _vp, _vp],
     "rbws_fn_prolong_add": [_c_int, _c_int, _vp, _vp, _vp, _vp],

@@ -632,6 +632,136 @@ __global__ void __launch_bounds__(128) band_solve_sub_kernel(int64_t nsys, int64
   }
 }
 
+// The band factor transposed: U[i][d] = L[i+d][i] (= band[(i+d) ws + d]), U[i][0] = 1 / L_ii.
+// Row i of U is column i of L, i.e. what the forward substitution scatters once y_i is known.
+__global__ void band_transpose_kernel(int64_t nsys, int64_t M, int w, const double* __restrict__ band,
+                                      double* __restrict__ bandT) {
+  const int ws = band_ws(w);
+  const int64_t s = blockIdx.y;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (i, d) of the output
+  if (s >= nsys || t >= M * ws) return;
+  const int64_t i = t / ws;
+  const int d = (int)(t % ws);
+  const double* B = band + s * M * ws;
+  bandT[s * M * ws + t] = (d <= w && i + d < M) ? B[(i + d) * ws + d] : 0.0;
+}
+
+// L L^T z = r per system with one warp and no reductions on the dependency chain.  Both
+// substitutions run in scatter form: when y_i (forward, rows of U = L^T) or x_i (backward,
+// rows of L) is final, the pending values of the w rows it couples to are updated at once.
+// Rows are owned round-robin (row t by lane t mod 32, slot = 32-row group, SL slots cover the
+// w + 32 rows in flight), so the next row's owner is the next lane and the chain per row is
+// one multiply, one shuffle broadcast and one FMA (no shifting window, no dot-product
+// reduction); the row loads are coalesced and independent of the chain.
+// mode 0: x = z; mode 1: x += omega z.  r is overwritten with the forward result.
+template <int SL>
+__global__ void __launch_bounds__(128) band_solve_rot_kernel(int64_t nsys, int64_t M, int w,
+                                                             const double* __restrict__ L,
+                                                             const double* __restrict__ U,
+                                                             int64_t lstride,
+                                                             double* __restrict__ r, int64_t rstride,
+                                                             double* __restrict__ x, int64_t xstride,
+                                                             double omega, int mode) {
+#ifndef RBWS_ROT_PF
+#define RBWS_ROT_PF 8
+#endif
+  constexpr int PF = RBWS_ROT_PF;  // rows loaded ahead of the chain (registers: PF x SL)
+  const int lane = threadIdx.x & 31;
+  const int64_t s = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= nsys) return;
+  const int ws = band_ws(w);
+  const double* Ls = L + s * lstride;
+  const double* Us = U + s * lstride;
+  double* rs = r + s * rstride;
+  double* xs = x + s * xstride;
+  const int64_t G = (M + 31) / 32;
+  double p[SL];
+  double buf[PF][SL];
+  // row i's entries for this lane's slots: forward d = 32 m + lane - (i mod 32) of U row i,
+  // backward d = 32 m + (i mod 32) - lane of L row i
+  auto load_fwd = [&](int64_t i, double* b) {
+    const int o = (int)(i & 31);
+#pragma unroll
+    for (int m = 0; m < SL; ++m) {
+      const int d = 32 * m + lane - o;
+      b[m] = (i < M && d >= 0 && d <= w) ? __ldcs(Us + i * ws + d) : 0.0;
+    }
+  };
+  auto load_bwd = [&](int64_t i, double* b) {
+    const int o = (int)(i & 31);
+#pragma unroll
+    for (int m = 0; m < SL; ++m) {
+      const int d = 32 * m + o - lane;
+      b[m] = (i >= 0 && i < M && d >= 0 && d <= w) ? __ldcs(Ls + i * ws + d) : 0.0;
+    }
+  };
+  // ---- forward L y = r (scatter with the rows of U); slot m <-> row 32 (q + m) + lane
+#pragma unroll
+  for (int m = 0; m < SL; ++m) {
+    const int64_t t = 32 * m + lane;
+    p[m] = t < M ? rs[t] : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < PF; ++u) load_fwd(u, buf[u]);
+  for (int64_t q = 0; q < G; ++q) {
+#pragma unroll
+    for (int o0 = 0; o0 < 32; o0 += PF) {
+#pragma unroll
+      for (int u = 0; u < PF; ++u) {
+        const int o = o0 + u;
+        const int64_t i = 32 * q + o;
+        if (i < M) {
+          const double z = __shfl_sync(0xffffffffu, p[0] * buf[u][0], o);  // lane o: row i
+          if (lane == o) rs[i] = z;
+#pragma unroll
+          for (int m = 0; m < SL; ++m) {
+            const int d = 32 * m + lane - o;
+            if (d >= 1 && d <= w) p[m] = fma(-buf[u][m], z, p[m]);
+          }
+        }
+        load_fwd(i + PF, buf[u]);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m + 1 < SL; ++m) p[m] = p[m + 1];
+    const int64_t t = 32 * (q + SL) + lane;
+    p[SL - 1] = t < M ? rs[t] : 0.0;
+  }
+  __syncwarp();
+  // ---- backward L^T x = y (scatter with the rows of L); slot m <-> row 32 (q - m) + lane
+#pragma unroll
+  for (int m = 0; m < SL; ++m) {
+    const int64_t t = 32 * (G - 1 - m) + lane;
+    p[m] = (t >= 0 && t < M) ? rs[t] : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < PF; ++u) load_bwd(32 * G - 1 - u, buf[u]);
+  for (int64_t q = G - 1; q >= 0; --q) {
+#pragma unroll
+    for (int o0 = 31; o0 >= 0; o0 -= PF) {
+#pragma unroll
+      for (int u = 0; u < PF; ++u) {
+        const int o = o0 - u;
+        const int64_t i = 32 * q + o;
+        if (i < M) {
+          const double z = __shfl_sync(0xffffffffu, p[0] * buf[u][0], o);
+          if (lane == o) xs[i] = mode == 0 ? z : fma(omega, z, xs[i]);
+#pragma unroll
+          for (int m = 0; m < SL; ++m) {
+            const int d = 32 * m + o - lane;
+            if (d >= 1 && d <= w) p[m] = fma(-buf[u][m], z, p[m]);
+          }
+        }
+        load_bwd(i - PF, buf[u]);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m + 1 < SL; ++m) p[m] = p[m + 1];
+    const int64_t t = 32 * (q - SL) + lane;
+    p[SL - 1] = t >= 0 ? rs[t] : 0.0;
+  }
+}
+
 // b[I] = sum_a w(a) r[2I + a] over the 27 fine neighbours (ascending fine index: the
 // reference's P^T r), zero on coarse Dirichlet nodes (cmask)
 __global__ void fn_restrict_kernel(int count, int cc, const double* __restrict__ r,
@@ -850,6 +980,46 @@ int rbws_fn_band_solve(int count, int c, int planar, const double* band, double*
   const int w = band_w(c, planar);
   return band_solve_launch(nsys, M, w, band, M * band_ws(w), r, M, x, M, omega, mode, St(stream),
                            true);
+}
+
+int rbws_fn_band_transpose(int count, int c, int planar, const double* band, double* bandT,
+                           void* stream) {
+  if (count <= 0 || c < 1 || !band || !bandT)
+    return rbws_set_error("rbws_fn_band_transpose: bad argument", __FILE__, __LINE__);
+  const int64_t c1 = c + 1;
+  const int64_t nsys = planar ? count * c1 : count;
+  const int64_t M = planar ? c1 * c1 : c1 * c1 * c1;
+  const int w = band_w(c, planar);
+  const int64_t tot = M * band_ws(w);
+  dim3 grd((unsigned)((tot + 255) / 256), (unsigned)nsys);
+  band_transpose_kernel<<<grd, 256, 0, St(stream)>>>(nsys, M, w, band, bandT);
+  FN_LAUNCHED();
+  return 0;
+}
+
+int rbws_fn_band_solve_t(int count, int c, int planar, const double* band, const double* bandT,
+                         double* r, double* x, double omega, int mode, void* stream) {
+  if (count <= 0 || c < 1 || !band || !bandT || !r || !x || mode < 0 || mode > 1)
+    return rbws_set_error("rbws_fn_band_solve_t: bad argument", __FILE__, __LINE__);
+  const int64_t c1 = c + 1;
+  const int64_t nsys = planar ? count * c1 : count;
+  const int64_t M = planar ? c1 * c1 : c1 * c1 * c1;
+  const int w = band_w(c, planar);
+  const int sl = (w + 32 + 31) / 32;  // slots: w + 32 rows in flight
+  const unsigned nb = (unsigned)((nsys + 3) / 4);
+  const int64_t ls = M * band_ws(w);
+#define RBWS_ROT(SL_)                                                                       \
+  case SL_:                                                                                 \
+    band_solve_rot_kernel<SL_><<<nb, 128, 0, St(stream)>>>(nsys, M, w, band, bandT, ls, r, M, \
+                                                           x, M, omega, mode);              \
+    break;
+  switch (sl) {
+    RBWS_ROT(2) RBWS_ROT(3) RBWS_ROT(4) RBWS_ROT(5) RBWS_ROT(6)
+    default: return rbws_set_error("rbws_fn_band_solve_t: bandwidth beyond the kernels", __FILE__, __LINE__);
+  }
+#undef RBWS_ROT
+  FN_LAUNCHED();
+  return 0;
 }
 
 int rbws_fn_plane_gs_sweep(int count, int c, const double* coefA, const double* band,

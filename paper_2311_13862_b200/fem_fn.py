@@ -234,7 +234,12 @@ class FnMgContext:
         # (139.6 vs 158.2 solves/s, profiles/r01i_example2.md) -> opt-in RBWS_FN_SHARED=1
         self.shared_finest = Q <= 8 and os.environ.get("RBWS_FN_SHARED", "0") == "1"
         st = _native.stream_ptr()
-        self.coefA, self.bands = [], []
+        self.coefA, self.bands, self.bandsT = [], [], []
+        # scatter-form plane solves on the transposed factors (rbws_fn_band_solve_t): opt-in,
+        # RBWS_BAND_SOLVE_T=1 — measured slower than the gather-form kernel at 64^3 x 64
+        # (MGCG 352-423 vs 287 ms, profiles/r02_example2.md)
+        self.scatter = os.environ.get("RBWS_BAND_SOLVE_T", "0") == "1" and \
+            smoother == "plane-jacobi"
         bad = []
         for l, c in enumerate(problem.cells):
             ca = torch.empty(count * 27 * problem.nodes(l), dtype=torch.float64, device="cuda")
@@ -244,6 +249,7 @@ class FnMgContext:
             planar = 0 if l == 0 else (1 if smoother.startswith("plane") else -1)
             if planar < 0:
                 self.bands.append(None)
+                self.bandsT.append(None)
                 continue
             nb = _native.load().rbws_fn_band_doubles(count, c, planar)
             band = torch.empty(nb, dtype=torch.float64, device="cuda")
@@ -252,6 +258,12 @@ class FnMgContext:
             _native.call("rbws_fn_band_factor", count, c, planar, _ptr(ca), _ptr(band),
                          _ptr(info), st)
             self.bands.append(band)
+            bandT = None
+            if self.scatter and planar == 1:
+                bandT = torch.empty_like(band)
+                _native.call("rbws_fn_band_transpose", count, c, planar, _ptr(band),
+                             _ptr(bandT), st)
+            self.bandsT.append(bandT)
             bad.append((l, info))
         for l, info in bad:
             if int(info.max()) > 0:
@@ -294,8 +306,13 @@ class FnMgContext:
         for _ in range(self.nu):
             r = self.apply(u, level, b)
             if self.smoother == "plane-jacobi":  # multigrid.py:91-95
-                _native.call("rbws_fn_band_solve", self.count, c, 1, _ptr(self.bands[level]),
-                             _ptr(r), _ptr(u), self.omega, 1, st)
+                if self.bandsT[level] is not None:
+                    _native.call("rbws_fn_band_solve_t", self.count, c, 1,
+                                 _ptr(self.bands[level]), _ptr(self.bandsT[level]), _ptr(r),
+                                 _ptr(u), self.omega, 1, st)
+                else:
+                    _native.call("rbws_fn_band_solve", self.count, c, 1, _ptr(self.bands[level]),
+                                 _ptr(r), _ptr(u), self.omega, 1, st)
             else:
                 _native.call("rbws_fn_point_jacobi", self.count, c, _ptr(self.coefA[level]),
                              _ptr(r), _ptr(u), self.omega, st)

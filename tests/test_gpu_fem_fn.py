@@ -130,21 +130,34 @@ def test_plane_blocks_solved_exactly(case):
     from paper_2311_13862_b200.fem_fn import _ptr, mg_context_for
     k, p = case
     mu = G[f"{k}_mus"][1]
-    ctx = mg_context_for(p, mu[None], smoother="plane-jacobi")
+    import os
+    os.environ["RBWS_BAND_SOLVE_T"] = "1"  # also build the transposed factors (opt-in path)
+    try:
+        ctx = mg_context_for(p, mu[None], smoother="plane-jacobi")
+    finally:
+        os.environ.pop("RBWS_BAND_SOLVE_T", None)
     A = p.operator_host(mu).toarray()
     rng = np.random.default_rng(3)
     b = rng.standard_normal((1, p.n_free))
     r = p.to_full(b)
-    x = torch.zeros_like(r)
-    _native.call("rbws_fn_band_solve", 1, p.n, 1, _ptr(ctx.bands[-1]), _ptr(r), _ptr(x), 1.0,
-                 1, _native.stream_ptr())
-    got = p.from_full(x)[0]
     layers = p.free_by_level[-1] // (p.n + 1) ** 2
     ref = np.zeros(p.n_free)
     for z in np.unique(layers):
         idx = np.flatnonzero(layers == z)
         ref[idx] = np.linalg.solve(A[np.ix_(idx, idx)], b[0, idx])
-    assert _rel(got, ref) <= 1e-12
+    # gather-form kernel and the scatter-form kernel on the transposed factor
+    for kind in ("gather", "scatter"):
+        r = p.to_full(b)
+        x = torch.zeros_like(r)
+        if kind == "gather":
+            _native.call("rbws_fn_band_solve", 1, p.n, 1, _ptr(ctx.bands[-1]), _ptr(r), _ptr(x),
+                         1.0, 1, _native.stream_ptr())
+        else:
+            assert ctx.bandsT[-1] is not None
+            _native.call("rbws_fn_band_solve_t", 1, p.n, 1, _ptr(ctx.bands[-1]),
+                         _ptr(ctx.bandsT[-1]), _ptr(r), _ptr(x), 1.0, 1, _native.stream_ptr())
+        got = p.from_full(x)[0]
+        assert _rel(got, ref) <= 1e-12, kind
 
 
 def test_larger_grid_against_oracle():
