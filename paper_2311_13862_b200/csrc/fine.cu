@@ -39,7 +39,18 @@ int fine_set_dc(int v) {
   g_force_dc.store(v);
   return 0;
 }
-int fine_variant() { return g_force_dc.load(); }
+// SW ("scaled weights") pre-smoothing kernels: -1 auto (whenever the diagonal changes on few
+// planes and the weights are not stored), 0 never, 1 = auto
+static std::atomic<int> g_force_sw{[] {
+  const char* e = getenv("RBWS_PRE_SW");
+  return e ? atoi(e) : -1;
+}()};
+int fine_set_sw(int v) {
+  if (v < -1 || v > 1) return 1;
+  g_force_sw.store(v);
+  return 0;
+}
+int fine_variant() { return (g_force_dc.load() + 1) + 4 * (g_force_sw.load() + 1); }
 constexpr int kThreads = 256;  // threads per CTA (one per grid column of the tile; N = 512: 512)
 
 // Compile-time tile geometry for a grid with N cells per axis: RPP rows per pass
@@ -108,6 +119,7 @@ struct FineArgs {
   double omega;
   int zlo, zhi;   // output planes [zlo, zhi) (global plane indices, virtual base pointers)
   int dc;         // PRE / POSTP: w/diag from the cached shared-memory tile (h1 unused)
+  int sw;         // PRE / PREX: scaled weights on the raw b (h1 read on rebuild planes only)
   int c0_shared;  // c0 is one instance shared by the whole batch (e.g. the rhs f)
   const double* ec;  // FM_POSTP: coarse-grid correction (n/2 cells, padded batch layout)
 };
@@ -133,12 +145,16 @@ template <int MODE, int N>
 using FTM = FT<N, ((MODE == FM_POSTP && (N == 64 || N == 128)) ||
                    (RBWS_PREX_512 && MODE == FM_PREX && N == 64)) ? 512 : kThreads>;
 
-template <int MODE, int N, bool DC = false>
+// SW ("scaled weights", FM_PRE / FM_PREX): the stencil of u = w D^-1 b is taken on the raw b
+// with the face weights pre-multiplied by the neighbours' w/diag, cached in registers and
+// rebuilt only on planes around a change of the z factors (1/diag read through L2 there):
+// no transformed ring, no 1/diag stream
+template <int MODE, int N, bool DC = false, bool SW = false>
 struct SL {
   // PRE / PAPPLY stencil a derived vector (w dinv b, s + beta p_old): each staged
   // plane is transformed once into a second ring, so neighbours cost one LDS
-  static constexpr bool XF = (MODE == FM_PRE || MODE == FM_PREX || MODE == FM_PAPPLY ||
-                              MODE == FM_POSTP);
+  static constexpr bool XF = !SW && (MODE == FM_PRE || MODE == FM_PREX || MODE == FM_PAPPLY ||
+                                     MODE == FM_POSTP);
   static constexpr int NH = XF ? 2 : 1;  // DC: h1 (1/diag) staged only on reload planes
   static constexpr int NC = (MODE == FM_CG) ? 2 : ((MODE == FM_RESID || MODE == FM_JACOBI) ? 1 : 0);
   // raw / transformed ring slots (N = 512 rows are 4 KB: a shallower raw ring fits 227 KB).
@@ -174,9 +190,9 @@ struct FCoarse {
 #define RBWS_MIN_CTAS 2
 #endif
 
-template <int N, int MODE, bool DC = false>
+template <int N, int MODE, bool DC = false, bool SW = false>
 struct FSmem {
-  using L = SL<MODE, N, DC>;
+  using L = SL<MODE, N, DC, SW>;
   using G = FTM<MODE, N>;
   static constexpr int STAGE = L::NH * G::HSZ + L::NC * G::CSZ +
                                (MODE == FM_POSTP ? FCoarse<N, G::TY>::CSZ : 0);
@@ -184,7 +200,8 @@ struct FSmem {
   static constexpr int RING = L::S * STAGE + (L::XF ? L::U * G::HSZ : 0) +
                               (DC ? G::HSZ : 0) + (MODE == FM_PREX ? 4 * G::CSZ : 0);
   static size_t bytes(int np, int Q) {
-    return 64 + 4 * (kMaxKz + 4) + 8 * (((size_t)np * 3 * Q + 1) & ~(size_t)1) + 8 * (size_t)RING;
+    return 64 + 4 * (kMaxKz + 4) + (SW ? 16 : 0) + 8 * (((size_t)np * 3 * Q + 1) & ~(size_t)1) +
+           8 * (size_t)RING;
   }
 };
 
@@ -192,17 +209,24 @@ struct FSmem {
 // (Sep7::wface, built at batch setup) instead of registers refreshed from the separable
 // tables — for coefficients whose z factors change on most planes, where the refresh
 // (5Q terms per node and plane) dominates; bitwise the same weights
-template <int MODE, int N, bool DC, bool SCW>
+// SW kernels at N <= 128: 80 registers without spills, three CTAs per SM (pre-smoothing
+// 0.86 -> 0.81 ms per full configs[1] launch)
+#ifndef RBWS_SW_MIN_CTAS
+#define RBWS_SW_MIN_CTAS 3
+#endif
+template <int MODE, int N, bool DC, bool SCW, bool SW = false>
 __global__ void __launch_bounds__(FTM<MODE, N>::THREADS,
-                                  FTM<MODE, N>::THREADS <= 256 ? RBWS_MIN_CTAS : 1)
+                                  FTM<MODE, N>::THREADS <= 256
+                                      ? ((SW && N <= 128) ? RBWS_SW_MIN_CTAS : RBWS_MIN_CTAS) : 1)
 fine_kernel(FineArgs a) {
+  static_assert(!SW || ((MODE == FM_PRE || MODE == FM_PREX) && !DC && !SCW), "SW: PRE / PREX only");
   using G = FTM<MODE, N>;
-  using L = SL<MODE, N, DC>;
+  using L = SL<MODE, N, DC, SW>;
   constexpr bool XF = L::XF;
   constexpr int NH = L::NH, NC = L::NC, S = L::S, U = L::U;
   constexpr int NPT = G::NPT, RPP = G::RPP, TY = G::TY;
   constexpr int HSZ = G::HSZ, CSZ = G::CSZ;
-  constexpr int STAGE = FSmem<N, MODE, DC>::STAGE;  // doubles per raw ring slot
+  constexpr int STAGE = FSmem<N, MODE, DC, SW>::STAGE;  // doubles per raw ring slot
   constexpr int64_t N2 = (int64_t)N * N;
   extern __shared__ __align__(128) unsigned char smem[];
   const Sep7& op = a.op;
@@ -229,7 +253,8 @@ fine_kernel(FineArgs a) {
   // ---- shared memory carve-up (offsets multiples of 16 bytes)
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);            // [S]
   int* zsame = reinterpret_cast<int*>(smem + 64);                // [kMaxKz + 2]
-  double* zf = reinterpret_cast<double*>(smem + 64 + 4 * (kMaxKz + 4));  // [np][3Q]
+  uint32_t* swbits = reinterpret_cast<uint32_t*>(smem + 64 + 4 * (kMaxKz + 4));  // [4] (SW)
+  double* zf = reinterpret_cast<double*>(smem + 64 + 4 * (kMaxKz + 4) + (SW ? 16 : 0));  // [np][3Q]
   double* ring = zf + ((np * ZW + 1) & ~1);                      // [S][STAGE]
   double* uring = ring + S * STAGE;                              // [U][HSZ] (XF)
   double* wd = uring + (XF ? U * HSZ : 0);                       // [HSZ] w/diag (DC)
@@ -249,6 +274,12 @@ fine_kernel(FineArgs a) {
 #pragma unroll
     for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
     mbar_fence_init();
+  }
+  if (SW && tid < 64) {  // plane flags of the staged planes, 32 per word
+    const int m = p_first + tid;
+    const bool f = tid < np && (m <= 1 || m >= N || __ldg(op.fz + m) != 0);
+    const uint32_t bits = __ballot_sync(0xffffffffu, f);
+    if ((tid & 31) == 0) swbits[tid >> 5] = bits;
   }
   __syncthreads();
   for (int p = 1 + tid; p < np; p += G::THREADS) {  // plane p repeats plane p-1's z factors?
@@ -302,6 +333,20 @@ fine_kernel(FineArgs a) {
     const int t = k - p_first;
     return t < 64 ? ((zmask >> t) & 1) != 0 : (MODE == FM_PREX ? zsame[t] != 0 : zlast);
   };
+  // SW: plane k keeps plane k-1's scaled weights when the planes k-1, k, k+1 all repeat their
+  // predecessor's face weights and diagonal (host-built flags op.fz; the Dirichlet planes 0
+  // and n multiply zeros of b, so they never force a rebuild); bit t = plane p_first + t
+  uint64_t smask = 0;
+  auto fzx = [&](int m) -> bool { return m <= 1 || m >= N || __ldg(op.fz + m) != 0; };
+  if (SW) {
+    const uint64_t fm = ((uint64_t)swbits[1] << 32) | swbits[0];  // bit t: fzx(p_first + t)
+    smask = (fm << 1) & fm & (fm >> 1);
+  }
+  auto steady_sw = [&](int k) -> bool {  // CTA-uniform
+    const int t = k - p_first;
+    if (t < 63) return ((smask >> t) & 1) != 0;
+    return fzx(k - 1) && fzx(k) && fzx(k + 1);
+  };
 
   // ---- this thread's column i and rows j = j0 + rl0 + r*RPP
   const int i = tid % N;
@@ -343,9 +388,34 @@ fine_kernel(FineArgs a) {
     dg[r] = ((wxp[r] + wxm[r]) + (wyp[r] + wym[r])) + (wzp[r] + wzm[r]);
     wdi[r] = om / dg[r];  // cached damping / diagonal (no per-node division)
   };
+  // SW: face weights of node (i, j, k) times w/diag of the neighbour across the face (a.h1 =
+  // 1/diag, read through L2 on the few planes where the weights are rebuilt)
+  auto scaled = [&](int r, int k, int64_t gidx) {
+    weights(r, zf + (k - p_first) * ZW);  // wxp, wxm, wyp, wym, wzp of plane k
+    double zm = 0.0;                      // z face (k-1, k): the z weight of plane k-1
+    const int j = j0 + rl0 + r * RPP;
+    if (i >= 1 && j >= 1) {
+      const double* zk = zf + (k - 1 - p_first) * ZW;
+#pragma unroll 2
+      for (int q = 0; q < Q; ++q) {
+        const double* NF = op.node + (size_t)q * 9 * (N + 1);
+        const double tz = th[q] * __ldg(NF + (2 * 3 + 0) * (N + 1) + i) * __ldg(NF + (2 * 3 + 1) * (N + 1) + j);
+        zm = fma(tz, zk[2 * Q + q], zm);
+      }
+    }
+    const double* D = a.h1 + gidx;
+    wxp[r] *= om * __ldg(D + 1);
+    wxm[r] *= om * __ldg(D - 1);
+    wyp[r] *= om * __ldg(D + N);
+    wym[r] *= om * __ldg(D - N);
+    // (planes 0 and n hold zeros of b: their factor only has to be the one a steady plane
+    // above / below would use)
+    wzp[r] *= om * __ldg(k + 1 < N ? D + N2 : D);
+    wzm[r] = zm * (om * __ldg(k > 1 ? D - N2 : D));
+  };
 #pragma unroll
   for (int r = 0; r < NPT; ++r) {  // plane kb-1: its z face (kb-1, kb) is wzm of plane kb
-    if (SCW) break;
+    if (SCW || SW) break;
     weights(r, zf);
     wzm[r] = wzp[r];
   }
@@ -439,6 +509,13 @@ fine_kernel(FineArgs a) {
   // face weights for plane k (refreshed only where the z factors change; CTA-uniform)
   auto refresh = [&](int k) {
     if (SCW) return;
+    if constexpr (SW) {
+      if (k == kb || !steady_sw(k)) {
+#pragma unroll
+        for (int r = 0; r < NPT; ++r) scaled(r, k, gk + r * RPP * N);
+      }
+      return;
+    }
     if (k == kb || !repeats(k)) {
 #pragma unroll
       for (int r = 0; r < NPT; ++r) {
@@ -469,11 +546,19 @@ fine_kernel(FineArgs a) {
     wzs[r] = SCW ? __ldg(WZ + base + (int64_t)(j0 + rl0 + r * RPP) * N + i + (int64_t)(kb - 1) * N2)
                  : 0.0;
   // the NPT nodes of one plane: vd / vc / vu = own-column input at k-1 / k / k+1, vb = own b
-  auto node = [&](int k, int r, int64_t gk_, double ud, double uc, double uu, double vbr) {
-    const double* P0 = (XF ? uring + (k - p_first) % U * HSZ : raw(k)) + hoff;
+  // the four in-plane neighbours of row r's node on plane k (shared memory)
+  auto nbrs = [&](int k, int r, double* nb) {
+    const double* P0 = (XF ? uring + (k - p_first) % U * HSZ : raw(k)) + hoff + r * RPP * N;
+    nb[0] = P0[1];
+    nb[1] = P0[-1];
+    nb[2] = P0[N];
+    nb[3] = P0[-N];
+  };
+  auto node = [&](int k, int r, int64_t gk_, double ud, double uc, double uu, double vbr,
+                  const double* nb) {
     const double* C0 = raw(k) + NH * HSZ + coff;
     const int o = r * RPP * N;  // compile-time after unrolling
-    const double ue = P0[o + 1], uw = P0[o - 1], un = P0[o + N], us = P0[o - N];
+    const double ue = nb[0], uw = nb[1], un = nb[2], us = nb[3];
     const int64_t gidx = gk_ + o;
     double xp, xm, yp, ym, zp, zm, dgr, wdr;
     if constexpr (SCW) {
@@ -494,6 +579,8 @@ fine_kernel(FineArgs a) {
       wdr = wdi[r];
     }
     // shallow FMA tree (a dependent chain of 6 would be latency bound)
+    // (SW: the weights are scaled by the neighbours' w/diag and the input is b itself)
+    if (SW) vbr = uc;
     const double offx = fma(xm, uw, xp * ue);
     const double offy = fma(ym, us, yp * un);
     const double offz = fma(zm, ud, zp * uu);
@@ -540,7 +627,11 @@ fine_kernel(FineArgs a) {
   auto step = [&](int k, const double* vd, const double* vc, const double* vu, const double* vb) {
     refresh(k);
 #pragma unroll
-    for (int r = 0; r < NPT; ++r) node(k, r, gk, vd[r], vc[r], vu[r], vb[r]);
+    for (int r = 0; r < NPT; ++r) {
+      double nb[4];
+      nbrs(k, r, nb);
+      node(k, r, gk, vd[r], vc[r], vu[r], vb[r], nb);
+    }
     gk += N2;
   };
 
@@ -553,11 +644,13 @@ fine_kernel(FineArgs a) {
   const bool xon = (MODE == FM_PREX) && xrow < TY && xI >= 1;
   double xacc = 0.0;
   double* tout = a.out0 + (int64_t)mu * NCX * N * NCX + (int64_t)(j0 + xrow) * NCX + xI;
-  auto xz = [&](int kk) {
-    if (!xon) return;
+  auto xload = [&](int kk) -> double {  // x-restricted r1 of plane kk at (xI, xrow)
     const int t = kk - kb;
     const double* R1 = rbuf + (((t >> 1) & 1) * 2 + (t & 1)) * CSZ + xrow * N + 2 * xI;
-    const double v = 0.5 * (R1[-1] + R1[1]) + R1[0];
+    return 0.5 * (R1[-1] + R1[1]) + R1[0];
+  };
+  auto xz = [&](int kk, double v) {
+    if (!xon) return;
     if (kk & 1) {  // 2K+1: closes coarse plane K (if 2K-1 was in this chunk), opens K+1
       xacc += 0.5 * v;
       const int K = (kk - 1) >> 1;
@@ -585,9 +678,10 @@ fine_kernel(FineArgs a) {
         if (k0 + 1 + S <= p_last) issue(k0 + 1 + S);
         if (k0 + 2 + S <= p_last) issue(k0 + 2 + S);
       }
-      if (MODE == FM_PREX && k0 > kb) {  // the previous trip's r1 planes are complete
-        xz(k0 - 2);
-        xz(k0 - 1);
+      if (MODE == FM_PREX && k0 > kb && xon) {  // the previous trip's r1 planes are complete
+        const double v0 = xload(k0 - 2), v1 = xload(k0 - 1);
+        xz(k0 - 2, v0);
+        xz(k0 - 1, v1);
       }
     } else {
       wait(k0 + 1);
@@ -599,13 +693,28 @@ fine_kernel(FineArgs a) {
         for (int r = 0; r < NPT; ++r) u1[r] = raw(k0 + 2)[hoff + r * RPP * N];
       }
     }
-    if (two && steady(k0) && repeats(k0 + 1)) {
+    if (two && (SW ? (k0 != kb && steady_sw(k0) && steady_sw(k0 + 1))
+                   : (steady(k0) && repeats(k0 + 1)))) {
       // common case: both planes keep the weights; one straight-line block of 2*NPT
       // independent nodes (latency hiding by ILP)
+      // (all neighbour loads first: FM_PREX stores r1 to shared memory, which the compiler
+      // must otherwise keep ordered with the next node's loads)
+      // (measured: FM_PREX 1.35 -> 1.29 ms, SW 1.23 -> 0.87 ms; the other modes store to
+      // global memory and lose 2-8 % to the longer live ranges, so they keep node order)
+      double nb[2 * NPT][4];
+      if (MODE == FM_PREX) {
+#pragma unroll
+        for (int r = 0; r < NPT; ++r) {
+          nbrs(k0, r, nb[2 * r]);
+          nbrs(k0 + 1, r, nb[2 * r + 1]);
+        }
+      }
 #pragma unroll
       for (int r = 0; r < NPT; ++r) {
-        node(k0, r, gk, xd[r], xc[r], u0[r], bcv[r]);
-        node(k0 + 1, r, gk + N2, xc[r], u0[r], u1[r], b0[r]);
+        if (MODE != FM_PREX) nbrs(k0, r, nb[2 * r]);
+        node(k0, r, gk, xd[r], xc[r], u0[r], bcv[r], nb[2 * r]);
+        if (MODE != FM_PREX) nbrs(k0 + 1, r, nb[2 * r + 1]);
+        node(k0 + 1, r, gk + N2, xc[r], u0[r], u1[r], b0[r], nb[2 * r + 1]);
       }
       gk += 2 * N2;
     } else {
@@ -624,13 +733,20 @@ fine_kernel(FineArgs a) {
         if (k0 - 1 + S <= p_last) issue(k0 - 1 + S);
         if (k0 + S <= p_last) issue(k0 + S);
       }
+      if (MODE == FM_PREX && xon) {  // SW: this trip's r1 planes are complete (barrier above)
+        const double v0 = xload(k0), v1 = two ? xload(k0 + 1) : 0.0;
+        xz(k0, v0);
+        if (two) xz(k0 + 1, v1);
+      }
     }
   }
-  if (MODE == FM_PREX) {  // the last trip's planes
+  if (MODE == FM_PREX && XF) {  // the last trip's planes
     __syncthreads();
     const int kl = kb + (((ke - kb) - 1) & ~1);
-    xz(kl);
-    if (kl + 1 < ke) xz(kl + 1);
+    if (xon) {
+      xz(kl, xload(kl));
+      if (kl + 1 < ke) xz(kl + 1, xload(kl + 1));
+    }
   }
   if (a.dot != DOT_NONE) {
     __shared__ double red[32];
@@ -639,25 +755,25 @@ fine_kernel(FineArgs a) {
   }
 }
 
-template <int MODE, int N, bool DC, bool SCW = false>
+template <int MODE, int N, bool DC, bool SCW = false, bool SW = false>
 static cudaError_t fine_launch_mnd(const FineArgs& a, int batch, cudaStream_t stream) {
   using G = FTM<MODE, N>;
   const int np = a.g.kz + (MODE == FM_PREX ? 3 : 2);  // FM_PREX: one recomputed plane
-  const size_t smem = FSmem<N, MODE, DC>::bytes(np, SCW ? 0 : a.op.Q);
+  const size_t smem = FSmem<N, MODE, DC, SW>::bytes(np, SCW ? 0 : a.op.Q);
   cudaError_t e0 = cudaSuccess;
   if (a.g.threads != G::THREADS || a.g.ty != G::TY || smem > 227 * 1024)
     e0 = cudaErrorInvalidValue;
   else
-    e0 = smem_attr((const void*)fine_kernel<MODE, N, DC, SCW>, smem);
+    e0 = smem_attr((const void*)fine_kernel<MODE, N, DC, SCW, SW>, smem);
   if (e0 != cudaSuccess) {
-    fprintf(stderr, "[rbws] fine_kernel<%d,%d,%d,%d> not launched: threads %d/%d ty %d/%d kz %d "
-            "smem %zu: %s\n", MODE, N, (int)DC, (int)SCW, a.g.threads, G::THREADS, a.g.ty, G::TY,
+    fprintf(stderr, "[rbws] fine_kernel<%d,%d,%d,%d,%d> not launched: threads %d/%d ty %d/%d kz %d "
+            "smem %zu: %s\n", MODE, N, (int)DC, (int)SCW, (int)SW, a.g.threads, G::THREADS, a.g.ty, G::TY,
             a.g.kz, smem, cudaGetErrorString(e0));
     return e0;
   }
   dim3 grd(1, a.g.ytiles, batch * a.g.zc);
   count_launch();
-  fine_kernel<MODE, N, DC, SCW><<<grd, G::THREADS, smem, stream>>>(a);
+  fine_kernel<MODE, N, DC, SCW, SW><<<grd, G::THREADS, smem, stream>>>(a);
   const cudaError_t e = cudaGetLastError();
   static const bool dbg = getenv("RBWS_DEBUG_LAUNCH") != nullptr;
   if (dbg || e != cudaSuccess)
@@ -670,6 +786,8 @@ static cudaError_t fine_launch_mnd(const FineArgs& a, int batch, cudaStream_t st
 template <int MODE, int N>
 static cudaError_t fine_launch_mn(const FineArgs& a, int batch, cudaStream_t stream) {
   if (a.op.wface) return fine_launch_mnd<MODE, N, false, true>(a, batch, stream);
+  if constexpr (MODE == FM_PRE || MODE == FM_PREX)
+    if (a.sw) return fine_launch_mnd<MODE, N, false, false, true>(a, batch, stream);
   if constexpr (MODE == FM_PRE || MODE == FM_PREX || MODE == FM_POSTP)
     if (a.dc) return fine_launch_mnd<MODE, N, true>(a, batch, stream);
   return fine_launch_mnd<MODE, N, false>(a, batch, stream);
@@ -830,6 +948,7 @@ static FineArgs base_args(const Sep7& op, int dot, double* partial, const Launch
   const int force = g_force_dc.load(std::memory_order_relaxed);
   const bool few = op.fz && op.zchg >= 0 && op.zchg <= kMaxDiagChanges;
   a.dc = (few && (force < 0 ? op.n >= 256 : force == 1)) ? 1 : 0;
+  a.sw = (few && !op.wface && g_force_sw.load(std::memory_order_relaxed) != 0) ? 1 : 0;
   return a;
 }
 
@@ -870,7 +989,8 @@ cudaError_t fine_pre(const Sep7& op, int batch, const double* b, const double* d
 }
 
 template <int N>
-static size_t prex_smem(bool dc, int np, int Q) {
+static size_t prex_smem(bool dc, bool sw, int np, int Q) {
+  if (sw) return FSmem<N, FM_PREX, false, true>::bytes(np, Q);
   return dc ? FSmem<N, FM_PREX, true>::bytes(np, Q) : FSmem<N, FM_PREX, false>::bytes(np, Q);
 }
 
@@ -891,16 +1011,17 @@ bool fine_pre_xz_ok(const Sep7& op, int batch, const LaunchCtx& lc) {
   // the z-factor table grows with the chunk's planes: at N = 512 with a short batch (long
   // chunks) it no longer fits next to the ring -> separate pre-smoothing + restriction
   const int Q = op.wface ? 0 : op.Q, np = g.kz + 3;
-  const bool dc = base_args(op, DOT_NONE, nullptr, lc, 0.0).dc != 0;
+  const FineArgs ba = base_args(op, DOT_NONE, nullptr, lc, 0.0);
+  const bool dc = ba.dc != 0, sw = ba.sw != 0;
   size_t smem = 0;
   switch (n) {
-    case 8: smem = prex_smem<8>(dc, np, Q); break;
-    case 16: smem = prex_smem<16>(dc, np, Q); break;
-    case 32: smem = prex_smem<32>(dc, np, Q); break;
-    case 64: smem = prex_smem<64>(dc, np, Q); break;
-    case 128: smem = prex_smem<128>(dc, np, Q); break;
-    case 256: smem = prex_smem<256>(dc, np, Q); break;
-    case 512: smem = prex_smem<512>(dc, np, Q); break;
+    case 8: smem = prex_smem<8>(dc, sw, np, Q); break;
+    case 16: smem = prex_smem<16>(dc, sw, np, Q); break;
+    case 32: smem = prex_smem<32>(dc, sw, np, Q); break;
+    case 64: smem = prex_smem<64>(dc, sw, np, Q); break;
+    case 128: smem = prex_smem<128>(dc, sw, np, Q); break;
+    case 256: smem = prex_smem<256>(dc, sw, np, Q); break;
+    case 512: smem = prex_smem<512>(dc, sw, np, Q); break;
     default: return false;
   }
   return smem <= 227 * 1024;

@@ -7,6 +7,8 @@ namespace rbws {
 
 // override of the DC kernel choice (-1 auto: N >= 256; 0 never; 1 whenever applicable)
 int fine_set_dc(int v);
+// override of the scaled-weights pre-smoothing kernels (-1 / 1 auto, 0 never)
+int fine_set_sw(int v);
 int fine_variant();  // current override (part of the cached PCG graph's key)
 
 struct FineGeom {

@@ -231,6 +231,28 @@ def test_dc_variant_matches_default(n, case, force):
     _compare_runs(var, base, 1e-13)
 
 
+@pytest.mark.parametrize("n,case", [(16, (2, 1, 1)), (64, (2, 2, 1)), (64, (2, 2, 2)),
+                                    (128, (2, 2, 2)), (256, (2, 2, 2))])
+def test_sw_variant_matches_transformed(n, case):
+    """The scaled-weights pre-smoothing kernels (face weights x the neighbours' w/diag on the
+    raw b, default for piecewise-constant coefficients) against the transformed-ring kernels
+    (u = w D^-1 b staged, rbws_set_kernel_variant(1, 0)): V-cycle, solutions, iterations."""
+    pkg = _pkg()
+    from paper_2311_13862_b200 import _native
+    spec, ospec = _specs(case)
+    prob = pkg.ParametricProblem(spec, levels=pkg.problems.levels_for(n, 4), m0=4)
+    mus = op.sample_mus(ospec, 3 if n < 256 else 1, seed=57)
+    delta = 1e-10
+    try:
+        _native.call("rbws_set_kernel_variant", 1, 0)
+        base = _vcycle_and_solve(prob, mus, delta, n)
+        _native.call("rbws_set_kernel_variant", 1, -1)
+        var = _vcycle_and_solve(prob, mus, delta, n)
+    finally:
+        _native.call("rbws_set_kernel_variant", 1, -1)
+    _compare_runs(var, base, 1e-13)
+
+
 @pytest.mark.parametrize("n,count", [(256, 2), (512, 1)])
 def test_fused_restrict_matches_separate_large(monkeypatch, n, count):
     """Pre-smoothing fused with the x/z restriction vs the separate kernels (N = 256, 512)."""
