@@ -293,6 +293,7 @@ def run_b200(args, rank, world, dist):
     del state["x"]
     scw = bool(_native.load().rbws_batch_stored_weights(ctx.handle))
     fused = bool(_native.load().rbws_batch_fused_restrict(ctx.handle))
+    pre_sw = bool(_native.load().rbws_batch_pre_scaled(ctx.handle))
     del ctx, xbuf
     torch.cuda.empty_cache()
     e2e_sub = min(batch, args.e2e_sub or cfg.get("e2e_sub", 512))
@@ -330,6 +331,11 @@ def run_b200(args, rank, world, dist):
     if fused:  # pre-smoothing + x/z restriction in one kernel: r1 never written
         class_bytes[2] = FUSED_PRE_BYTES + (24.0 if scw else 0.0)
         class_bytes[3] = FUSED_RESTRICT_Y_BYTES
+    # scaled-weights pre-smoothing kernels: the 1/diag vector is not streamed (-8 B/node); the
+    # bytes of the operation as the reference states it (b, D^-1 in) are reported next to it
+    op_bytes = dict(class_bytes)
+    if pre_sw:
+        class_bytes[2] -= 8.0
     table = {}
     for k in range(NC):
         if pcalls[k] == 0:
@@ -340,6 +346,10 @@ def run_b200(args, rank, world, dist):
         if k in class_bytes:
             gbs = class_bytes[k] * nodes * punits[k] / (pms[k] / 1e3) / 1e9
             row["achieved_gbs"] = round(gbs, 1)
+            row["bytes_per_node"] = class_bytes[k]
+            if op_bytes[k] != class_bytes[k]:
+                row["op_bytes_per_node"] = op_bytes[k]
+                row["op_gbs"] = round(gbs * op_bytes[k] / class_bytes[k], 1)
         elif CLASS_NAMES[k] == "coarse_levels":
             # algorithmic bytes of one V-cycle's coarse levels per instance: 76 B per node
             # of every smoothed coarse level (pre-smoothing residual 24, restriction 11,
@@ -362,7 +372,7 @@ def run_b200(args, rank, world, dist):
                     "traffic": traffic, "traffic_source": tsrc, "peak_source": peak_kind,
                     "bytes_per_launch": int(dom_bytes),
                     "bytes_per_node": class_bytes[dom], "stored_weights": scw,
-                    "fused_pre_restrict": fused}
+                    "fused_pre_restrict": fused, "scaled_weights_pre": pre_sw}
     else:  # the warm start already met the tolerance: no PCG iteration ran
         roofline = {"bound": "hbm", "kernel": None, "achieved": None, "peak": peak,
                     "unit": "GB/s", "frac": None, "traffic": None, "peak_source": peak_kind}

@@ -104,7 +104,10 @@ int rbws_batch_set_graph(rbws_batch* b, int enable);
 /* Process-wide kernel-variant override for tests and A/B runs (no reference counterpart).
  * which 0 = "DC" finest pre/post-smoothing kernels (w/diag cached in shared memory, 1/diag
  * rows staged only on planes where the diagonal changes): value -1 auto (N >= 256),
- * 0 never, 1 whenever the diagonal changes on few planes (any N). */
+ * 0 never, 1 whenever the diagonal changes on few planes (any N).
+ * which 1 = "SW" scaled-weights pre-smoothing kernels: -1 / 1 auto (whenever the diagonal
+ * changes on few planes and the face weights are not stored), 0 never (the transformed-ring
+ * kernels that stage u = omega D^-1 b). */
 int rbws_set_kernel_variant(int which, int value);
 /* Smoother of the V-cycle: 0 damped Jacobi (the reference default for isotropic problems,
  * multigrid.py:183-188), 1 Gauss-Seidel (smoother="gs": nu forward lexicographic sweeps
@@ -122,6 +125,10 @@ int rbws_batch_stored_weights(const rbws_batch* b);
 /* 1 if the last V-cycle ran the finest pre-smoothing residual fused with the x/z passes of
  * the restriction (r1 = b - A(w D^-1 b) never written; the measurement's byte counts) */
 int rbws_batch_fused_restrict(const rbws_batch* b);
+/* 1 if the last V-cycle's finest pre-smoothing residual ran the scaled-weights kernels
+ * (face weights pre-multiplied by the neighbours' omega/diag in registers, stencil taken on
+ * the raw b: the 1/diag vector is not streamed; piecewise-constant coefficients), else 0 */
+int rbws_batch_pre_scaled(const rbws_batch* b);
 
 /* y = A^level(mu) x for every instance (ParametricProblem.operator(mu, level) @ x,
  * grid.py:246-255).  x, y: (dev) padded vectors of that level. */

@@ -455,28 +455,43 @@ fine_kernel(FineArgs a) {
     const double* R = raw(p);
     double* T = uring + (p - p_first) % U * HSZ;
     const bool adv = (MODE == FM_POSTP) && p != p_first && !(p & 1);
+    // three passes (coarse-plane advance, raw loads, stores): the compiler keeps shared-memory
+    // loads behind earlier shared-memory stores, so row by row every row would wait for the
+    // previous row's whole load -> FMA -> store chain
+    if (adv) {
+#pragma unroll
+      for (int t = 0; t < NPT + 2; ++t) {
+        if (!trow_on(t)) continue;
+        cv0[t] = cv1[t];
+        cv1[t] = vxy(R + NH * HSZ, cj0, trow_j(t));
+      }
+    }
+    double rb[NPT + 2], rd[NPT + 2];
+#pragma unroll
+    for (int t = 0; t < NPT + 2; ++t) {
+      if (!trow_on(t)) continue;
+      const int e = trow_e(t);
+      rb[t] = R[e];
+      rd[t] = (DC && !reload) ? wd[e] : R[HSZ + e];
+    }
 #pragma unroll
     for (int t = 0; t < NPT + 2; ++t) {
       if (!trow_on(t)) continue;
       const int e = trow_e(t);
       double v;
-      if (DC && reload) wd[e] = om * R[HSZ + e];  // staged with this plane
+      if (DC && reload) wd[e] = rd[t] = om * rd[t];  // staged with this plane
       if (MODE == FM_PRE || MODE == FM_PREX) {
-        v = (DC ? wd[e] : om * R[HSZ + e]) * R[e];  // w dinv b
+        v = (DC ? rd[t] : om * rd[t]) * rb[t];  // w dinv b
       } else if (MODE == FM_PAPPLY) {
-        v = fma(sc, R[HSZ + e], R[e]);  // s + beta p_old
+        v = fma(sc, rd[t], rb[t]);  // s + beta p_old
       } else {  // FM_POSTP: w dinv b + P ec
-        if (adv) {
-          cv0[t] = cv1[t];
-          cv1[t] = vxy(R + NH * HSZ, cj0, trow_j(t));
-        }
         const double pe = (p & 1) ? 0.5 * (cv0[t] + cv1[t]) : cv0[t];
-        v = fma(DC ? wd[e] : om * R[HSZ + e], R[e], pe);
+        v = fma(DC ? rd[t] : om * rd[t], rb[t], pe);
       }
       T[e] = v;
       if (t < NPT) {
         xo[t] = v;
-        bo[t] = R[e];
+        bo[t] = rb[t];
       }
     }
   };
@@ -992,6 +1007,10 @@ template <int N>
 static size_t prex_smem(bool dc, bool sw, int np, int Q) {
   if (sw) return FSmem<N, FM_PREX, false, true>::bytes(np, Q);
   return dc ? FSmem<N, FM_PREX, true>::bytes(np, Q) : FSmem<N, FM_PREX, false>::bytes(np, Q);
+}
+
+bool fine_pre_scaled(const Sep7& op) {
+  return base_args(op, DOT_NONE, nullptr, LaunchCtx{}, 0.0).sw != 0;
 }
 
 bool fine_pre_xz_ok(const Sep7& op, int batch, const LaunchCtx& lc) {

@@ -51,6 +51,9 @@ cudaError_t fine_pre(const Sep7& op, int batch, const double* b, const double* d
 // 2I-1..2I+1 (weights 0.5 / 1 / 0.5) of r1 = b - A (omega dinv b) on fine row j; the y pass is
 // restrict_y_launch.  Only when one CTA holds an instance's whole z-range (fine_pre_xz_ok).
 bool fine_pre_xz_ok(const Sep7& op, int batch, const LaunchCtx& lc);
+// true when fine_pre / fine_pre_xz run the scaled-weights kernels on this operator (no 1/diag
+// stream: the measurement's byte counts)
+bool fine_pre_scaled(const Sep7& op);
 cudaError_t fine_pre_xz(const Sep7& op, int batch, const double* b, const double* dinv,
                         double* t, double omega, const LaunchCtx& lc);
 // fused prolongation + post-smoothing of the nu=1 V-cycle:

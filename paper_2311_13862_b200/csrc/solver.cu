@@ -619,7 +619,10 @@ int Batch::vcycle(int lvl, const double* bb, double* out, double* dot_partial,
     // finest level, whole instances per CTA: the pre-smoothing kernel also runs the x and z
     // passes of the restriction (r1 never reaches HBM), a light kernel the y pass
     const bool fused = fine && fuse_restrict && lvl - 1 >= 1 && fine_pre_xz_ok(fine_op(), count, lc);
-    if (fine) fused_used = fused;  // (the coarse levels of the recursion leave it alone)
+    if (fine) {  // (the coarse levels of the recursion leave these alone)
+      fused_used = fused;
+      sw_used = fine_pre_scaled(fine_op());
+    }
     if (stop) e = vec_scale_dinv(n, count, omega, l.dinv, bb, l.u, lc.stream);
     if (e == cudaSuccess)
       e = fused ? fine_pre_xz(fine_op(), count, bb, l.dinv, l.t1, omega, lc)

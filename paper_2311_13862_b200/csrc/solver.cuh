@@ -87,6 +87,7 @@ struct Batch {
   int smoother = 0;                 // 0 damped Jacobi (isotropic default), 1 Gauss-Seidel ("gs")
   bool fuse_restrict = true;        // finest pre-smoothing + x/z restriction in one kernel
   bool fused_used = false;          // the last V-cycle took the fused path
+  bool sw_used = false;             // ... with the scaled-weights pre-smoothing kernels
   double omega = 0.7;
   double* theta = nullptr;          // [cap][Q]
   double* wface = nullptr;          // stored fine face weights [3][cap n^3 + 2n^2] (SCW kernels)
