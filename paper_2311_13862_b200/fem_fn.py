@@ -292,7 +292,9 @@ class FnMgContext:
                          _ptr(self.coefA[level]), _ptr(x), bp, _ptr(y), mode, _native.stream_ptr())
         return y
 
-    def _smooth(self, level, u, b, forward=True):
+    def _smooth(self, level, u, b, forward=True, from_zero=False):
+        """nu sweeps on `level`; from_zero: u is the zero vector (the pre-smoothing of a V-cycle),
+        so the first sweep's residual b - A u is b itself (bitwise) and no apply is launched."""
         c = self.problem.cells[level]
         st = _native.stream_ptr()
         if self.smoother == "plane-z":  # ascending pre / descending post (multigrid.py:97-110)
@@ -303,8 +305,8 @@ class FnMgContext:
                              _ptr(self.bands[level]), _ptr(b), _ptr(u), _ptr(scratch),
                              1 if forward else 0, st)
             return u
-        for _ in range(self.nu):
-            r = self.apply(u, level, b)
+        for s in range(self.nu):
+            r = b.clone() if (from_zero and s == 0) else self.apply(u, level, b)
             if self.smoother == "plane-jacobi":  # multigrid.py:91-95
                 if self.bandsT[level] is not None:
                     _native.call("rbws_fn_band_solve_t", self.count, c, 1,
@@ -330,7 +332,7 @@ class FnMgContext:
             _native.call("rbws_fn_band_solve", self.count, p.cells[0], 0, _ptr(self.bands[0]),
                          _ptr(r), _ptr(x), 1.0, 0, st)
             return x
-        u = self._smooth(level, torch.zeros_like(b), b)
+        u = self._smooth(level, torch.zeros_like(b), b, from_zero=True)
         r = self.apply(u, level, b)
         cc = p.cells[level - 1]
         bc = torch.empty(self.count, p.nodes(level - 1), dtype=torch.float64, device="cuda")
