@@ -155,6 +155,19 @@ int rbws_mgcg_solve(rbws_batch* b, const double* f, int64_t f_stride, double* x,
                     int l_max, int* iters, double* hist, double* true_res, int* status,
                     void* stream);
 
+/* Batched PCG with the iteration-indexed multispace reduced-basis preconditioner
+ * (msrbcg_solve, msrb.py:152-170, as called by rbi_pcg_solve, warmstart.py:103-104): from the
+ * loaded x (the POD Galerkin initial guess), iteration k is preconditioned by one symmetric
+ * Gauss-Seidel sweep from zero plus the Galerkin correction of its residual in basis
+ * min(k, nbases - 1) (MsrbPreconditioner.__call__, msrb.py:77-85).  The batch must be set up
+ * with smoother = 1.  Host arrays of nbases entries: W[k] (dev) N[k] <= 64 padded basis
+ * vectors at stride Wstride[k]; chol[k] (dev) [count][N[k]][N[k]] lower Cholesky factors of
+ * W_k^T A(mu) W_k (cho_factor, msrb.py:72).  Outputs as rbws_mgcg_solve. */
+int rbws_msrbcg_solve(rbws_batch* b, const double* f, int64_t f_stride, double* x, double delta,
+                      int l_max, int nbases, const double* const* W, const int64_t* Wstride,
+                      const int* N, const double* const* chol, int* iters, double* hist,
+                      double* true_res, int* status, void* stream);
+
 /* rbws_mgcg_solve that also streams the solutions to host memory: instance m's
  * padded solution (n^3 doubles) is copied to x_host + m*host_stride (pinned host,
  * host_stride >= n^3) on copy_stream as soon as m stops iterating (converged,

@@ -50,6 +50,8 @@ SIGNATURES = {
     "rbws_prolong_add": [_c_int, _c_int, _vp, _vp, _vp],
     "rbws_vcycle": [_vp, _vp, _vp, _vp],
     "rbws_mgcg_solve": [_vp, _vp, _c_int64, _vp, _c_double, _c_int, _vp, _vp, _vp, _vp, _vp],
+    "rbws_msrbcg_solve": [_vp, _vp, _c_int64, _vp, _c_double, _c_int, _c_int, _vp, _vp, _vp, _vp,
+                          _vp, _vp, _vp, _vp, _vp],
     "rbws_mgcg_solve_to_host": [_vp, _vp, _c_int64, _vp, _c_double, _c_int, _vp, _vp, _vp, _vp,
                                 _vp, _vp, _c_int64, _vp],
     "rbws_batch_dinv": [_vp, _c_int, _vp, _vp],

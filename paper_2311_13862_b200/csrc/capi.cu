@@ -247,6 +247,17 @@ int rbws_mgcg_solve(rbws_batch* b, const double* f, int64_t f_stride, double* x,
   return rbws::pcg_solve(B(b), f, f_stride, x, delta, l_max, o, S(stream));
 }
 
+int rbws_msrbcg_solve(rbws_batch* b, const double* f, int64_t f_stride, double* x, double delta,
+                      int l_max, int nbases, const double* const* W, const int64_t* Wstride,
+                      const int* N, const double* const* chol, int* iters, double* hist,
+                      double* true_res, int* status, void* stream) {
+  if (!b || !f || !x) RBWS_FAIL("null argument");
+  if (nbases > 0 && (!W || !Wstride || !N || !chol)) RBWS_FAIL("null basis arrays");
+  rbws::PcgOut o{iters, hist, true_res, status};
+  return rbws::msrbcg_solve(B(b), f, f_stride, x, delta, l_max, nbases, W, Wstride, N, chol, o,
+                            S(stream));
+}
+
 int rbws_mgcg_solve_to_host(rbws_batch* b, const double* f, int64_t f_stride, double* x,
                             double delta, int l_max, int* iters, double* hist, double* true_res,
                             int* status, void* stream, double* x_host, int64_t host_stride,

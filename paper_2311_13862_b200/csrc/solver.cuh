@@ -183,5 +183,11 @@ cudaError_t pcg_true(int count, const double* prr, int tiles, const double* scal
 
 int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double delta, int l_max,
               const PcgOut& out, cudaStream_t stream);
+// PCG with the iteration-indexed multispace reduced-basis preconditioner (msrb.cu): basis
+// min(k, nbases-1) serves iteration k; W[k]: N[k] padded vectors at stride Wstride[k],
+// chol[k]: [count][N[k]][N[k]] lower Cholesky factors of W_k^T A(mu) W_k (all device)
+int msrbcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double delta, int l_max,
+                 int nbases, const double* const* W, const int64_t* Wstride, const int* N,
+                 const double* const* chol, const PcgOut& out, cudaStream_t stream);
 
 }  // namespace rbws

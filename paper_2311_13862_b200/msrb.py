@@ -13,6 +13,11 @@ error-snapshot POD space.  Batched over parameters:
   matrix is sum_q theta_q W^T A_q W and its Cholesky factor is batched.
 * Sweeps and residuals are the native kernels (rbws_smooth symmetric Gauss-Seidel,
   rbws_level_kernel residual, rbws_apply).
+* The online solve is ONE native call (rbws_msrbcg_solve, csrc/msrb.cu): the PCG loop with
+  the iteration-indexed preconditioner, per-instance scalars and the active set on the
+  device; this module only sets up the bases' reduced factors.
+* Problems: the separable (Kronecker-factor) BASELINE problems and the reference's assembled
+  Dirichlet problem example-1 (stored-coefficient hierarchy, per-parameter right-hand sides).
 
 Semantics follow the reference: msrb_train simulates the reduced-initialised,
 MSRB-preconditioned CG over the training set, one iteration per basis index
@@ -80,11 +85,17 @@ class _Reduced:
         rows = torch.as_tensor(interior_to_padded_index(np.arange(m ** 3), n), device="cuda")
         Wp = torch.zeros(padded_len(n, N), dtype=torch.float64, device="cuda")
         Wp[: N * n ** 3] = W.reshape(-1)
-        Bq = torch.zeros(Q * m ** 3 * N, dtype=torch.float64, device="cuda")
-        _native.call("rbws_l1roc_project", problem.handle, Wp.data_ptr(), n ** 3, N,
-                     rows.data_ptr(), m ** 3, Bq.data_ptr(), _native.stream_ptr())
         Wr = W[:, rows]                                     # (N, M)
-        self.red = torch.einsum("am,qmb->qab", Wr, Bq.view(Q, m ** 3, N)).contiguous()
+        if getattr(problem, "stored", False):
+            # assembled problems: A_q W from the stored per-term coefficients
+            AW = torch.stack([problem.term_apply(q, Wp, N)[: N * n ** 3].view(N, n ** 3)[:, rows]
+                              for q in range(Q)])           # (Q, N, M), row b = A_q w_b
+            self.red = torch.einsum("am,qbm->qab", Wr, AW).contiguous()
+        else:
+            Bq = torch.zeros(Q * m ** 3 * N, dtype=torch.float64, device="cuda")
+            _native.call("rbws_l1roc_project", problem.handle, Wp.data_ptr(), n ** 3, N,
+                         rows.data_ptr(), m ** 3, Bq.data_ptr(), _native.stream_ptr())
+            self.red = torch.einsum("am,qmb->qab", Wr, Bq.view(Q, m ** 3, N)).contiguous()
 
     def factor(self, theta):
         """Cholesky factors of sum_q theta_q W^T A_q W for a batch (count, Q)."""
@@ -168,15 +179,31 @@ def _apply_precond(ops, red: _Reduced | None, L, r):
     return u + red.solve(L, r - ops.apply(u))
 
 
-def _separable_only(problem):
-    if getattr(problem, "stored", False):
-        raise NotImplementedError("rbi-msrbcg runs on the separable (Kronecker-factor) problems; "
-                                  "assembled problems take mgcg / rbi-mgcg")
+def _padded_only(problem):
+    """rbi-msrbcg runs on the padded interior layout: the separable BASELINE problems and
+    assembled Dirichlet problems (example-1).  Full-node problems (example-2: free boundary
+    nodes) have no Gauss-Seidel sweep on that layout."""
+    if hasattr(problem, "masks"):
+        raise NotImplementedError(f"{problem.spec.pid}: rbi-msrbcg needs the symmetric "
+                                  "Gauss-Seidel sweep, which the full-node layout does not have; "
+                                  "use mgcg / rbi-mgcg")
+
+
+def _rhs_rows(problem, mus, f=None):
+    """(count, n^3) right-hand sides: per parameter for assembled problems (lifted Dirichlet
+    data, grid.py:266-284), one shared vector expanded for the separable ones."""
+    cnt, n3 = len(mus), problem.n ** 3
+    if f is None:
+        f = problem.rhs(mus) if getattr(problem, "stored", False) else problem.rhs()
+    f = f.reshape(-1)
+    if f.numel() >= cnt * n3 and (cnt > 1 or getattr(problem, "stored", False)):
+        return f[: cnt * n3].view(cnt, n3)
+    return f[:n3].view(1, n3).expand(cnt, n3)
 
 
 def msrb_train(mus, N: int, K_max: int, hf_solver, problem) -> MsrbHierarchy:
     """Per-iteration error-snapshot bases (msrb.py:113-149); hf_solver: HighFidelitySolver."""
-    _separable_only(problem)
+    _padded_only(problem)
     import torch
     if K_max < 0:
         raise ValueError("K_max must be non-negative")
@@ -190,10 +217,10 @@ def msrb_train(mus, N: int, K_max: int, hf_solver, problem) -> MsrbHierarchy:
     ctx = mg_context_for(problem, mus, smoother="gs")
     ops = _BatchOps(ctx)
     theta = ctx.theta
-    f = problem.rhs()[:n3].view(1, n3).expand(cnt, n3)
+    f = _rhs_rows(problem, mus)
     red0 = _Reduced(problem, init.basis)
-    x = red0.solve(red0.factor(theta), f) if red0.N else torch.zeros(cnt, n3, dtype=torch.float64,
-                                                                       device="cuda")
+    x = red0.solve(red0.factor(theta), f.contiguous()) if red0.N else \
+        torch.zeros(cnt, n3, dtype=torch.float64, device="cuda")
     r = f - ops.apply(x)
     p, rs = None, None
     bases, spectra = [], []
@@ -220,76 +247,59 @@ def rbi_msrbcg_solve(problem, mus, hier: MsrbHierarchy, f=None, delta: float = 1
                      l_max: int = 40, method: str = "rbi-msrbcg", ctx: MgContext | None = None):
     """Batched rbi-msrbcg: POD Galerkin initial guess (warmstart.py:81-84), then PCG
     (krylov.py:42-109 semantics, per instance) with the MSRB preconditioner
-    (msrb.py:53-85).  Returns (x (count, n^3) padded rows, SolveReports)."""
-    _separable_only(problem)
+    (msrb.py:53-85) as one native call (rbws_msrbcg_solve).  Returns (x padded device
+    vector, SolveReports)."""
+    _padded_only(problem)
+    import ctypes
+
     import torch
     from .multigrid import mg_context_for
+    if delta <= 0:
+        raise ValueError("tolerance must be positive")
+    if l_max < 0:
+        raise ValueError("l_max must be non-negative")
     mus = problem.spec.check_mus(mus)
-    cnt, n3 = len(mus), problem.n ** 3
+    cnt, n, n3 = len(mus), problem.n, problem.n ** 3
     if ctx is None or ctx.smoother_kind != "gs" or ctx.count != cnt:
         ctx = mg_context_for(problem, mus, smoother="gs", ctx=ctx)
-    ops = _BatchOps(ctx)
     theta = ctx.theta
-    f = (problem.rhs() if f is None else f)[:n3].view(1, n3).expand(cnt, n3)
+    frows = _rhs_rows(problem, mus, f)
+    shared = frows.stride(0) == 0
+    fbuf = torch.zeros(padded_len(n, 1 if shared else cnt), dtype=torch.float64, device="cuda")
+    fbuf[: (1 if shared else cnt) * n3] = (frows[0] if shared else frows).reshape(-1)
     t0 = time.perf_counter()
-    red_cache = {}
-
-    def reduced(k):
-        W = hier.basis_for(k)
-        key = -1 if W is None else min(k, len(hier.bases) - 1)
-        if key not in red_cache:
-            red = None if W is None else _Reduced(problem, W)
-            red_cache[key] = (red, red.factor(theta) if red is not None and red.N else None)
-        return red_cache[key]
-
+    # the POD Galerkin initial guess and the reduced factors of every iteration's basis
     red0 = _Reduced(problem, hier.init_basis.basis)
-    x = red0.solve(red0.factor(theta), f) if red0.N else torch.zeros(cnt, n3, dtype=torch.float64,
-                                                                       device="cuda")
-    fn = torch.linalg.vector_norm(f, dim=1)
-    absolute = (fn == 0)
-    scale = torch.where(absolute, torch.ones_like(fn), fn)
-    r = f - ops.apply(x)
-    rel = torch.linalg.vector_norm(r, dim=1) / scale
-    hist = [rel]  # device tensors, copied to the host once at the end
-    iters_d = torch.zeros(cnt, dtype=torch.int32, device="cuda")
-    active = (rel > delta) if l_max > 0 else torch.zeros_like(rel, dtype=torch.bool)
+    xp = torch.zeros(padded_len(n, cnt), dtype=torch.float64, device="cuda")
+    if red0.N:
+        xp[: cnt * n3] = red0.solve(red0.factor(theta), frows.contiguous()).reshape(-1)
+    keep, Ws, strides, Ns, chols = [], [], [], [], []
+    for W in hier.bases:
+        Wc = W.contiguous()
+        red = _Reduced(problem, Wc)
+        Lk = red.factor(theta).contiguous() if red.N else None
+        keep.append((Wc, Lk))
+        Ws.append(Wc.data_ptr() if red.N else 0)
+        strides.append(Wc.stride(0) if red.N else 0)
+        Ns.append(red.N)
+        chols.append(Lk.data_ptr() if red.N else 0)
+    nb = len(Ws)
+    Wa = (ctypes.c_void_p * max(nb, 1))(*Ws)
+    Sa = (ctypes.c_int64 * max(nb, 1))(*strides)
+    Na = (ctypes.c_int * max(nb, 1))(*Ns)
+    Ca = (ctypes.c_void_p * max(nb, 1))(*chols)
+    iters = np.zeros(cnt, dtype=np.int32)
+    hist = np.zeros((cnt, l_max + 1))
+    tres = np.zeros(cnt)
     status = np.zeros(cnt, dtype=np.int32)
-    if bool(active.any()):
-        red, L = reduced(0)
-        s = _apply_precond(ops, red, L, r)
-        p = s
-        rs = (r * s).sum(1)
-        k = 0
-        while k < l_max and bool(active.any()):
-            Ap = ops.apply(p)
-            pAp = (p * Ap).sum(1)
-            bad = active & ~(pAp > 0)
-            if bool(bad.any()):
-                raise OperatorError("non-positive curvature p.A.p; operator not SPD")
-            alpha = torch.where(active, rs / pAp, torch.zeros_like(rs))
-            x = x + alpha[:, None] * p
-            r = r - alpha[:, None] * Ap
-            k += 1
-            rel_k = torch.linalg.vector_norm(r, dim=1) / scale
-            iters_d = torch.where(active, torch.full_like(iters_d, k), iters_d)
-            hist.append(torch.where(active, rel_k, torch.full_like(rel_k, float("nan"))))
-            active = active & (rel_k > delta)
-            if not bool(active.any()) or k >= l_max:
-                break
-            red, L = reduced(k)
-            s = _apply_precond(ops, red, L, r)
-            rs_new = (r * s).sum(1)
-            p = s + (rs_new / rs)[:, None] * p
-            rs = rs_new
-    tres = (torch.linalg.vector_norm(f - ops.apply(x), dim=1) / scale).cpu().numpy()
-    status |= np.where(absolute.cpu().numpy(), 4, 0).astype(np.int32)
-    iters = iters_d.cpu().numpy()
-    H = np.full((cnt, l_max + 1), np.nan)
-    Hd = torch.stack(hist, 1).cpu().numpy()
-    H[:, : Hd.shape[1]] = Hd
-    reps = SolveReports(method, iters, H, tres, status, time.perf_counter() - t0, delta, l_max,
+    _native.call("rbws_msrbcg_solve", ctx.handle, fbuf.data_ptr(), 0 if shared else n3,
+                 xp.data_ptr(), float(delta), int(l_max), nb, Wa, Sa, Na, Ca, iters.ctypes.data,
+                 hist.ctypes.data, tres.ctypes.data, status.ctypes.data, _native.stream_ptr())
+    torch.cuda.current_stream().synchronize()
+    del keep
+    if np.any(status & 1):
+        raise OperatorError("non-positive curvature p.A.p; operator not SPD")
+    reps = SolveReports(method, iters, hist, tres, status, time.perf_counter() - t0, delta, l_max,
                         mus, {"batch": cnt, "smoother": "gauss-seidel-symmetric",
                               "K_max": hier.K_max, "N": hier.N})
-    xp = torch.zeros(padded_len(problem.n, cnt), dtype=torch.float64, device="cuda")
-    xp[: cnt * n3] = x.reshape(-1)
     return xp, reps

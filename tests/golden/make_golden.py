@@ -5,6 +5,7 @@ Run in the build container (needs /root/reference; never on the GPU box):
     python tests/golden/make_golden.py          # golden_fd.npz
     python tests/golden/make_golden.py --gs     # golden_gs.npz (Gauss-Seidel smoother)
     python tests/golden/make_golden.py --msrb   # golden_msrb.npz (rbi-msrbcg)
+    python tests/golden/make_golden.py --msrb-fem  # golden_msrb_fem.npz (rbi-msrbcg, example-1)
     python tests/golden/make_golden.py --fem    # golden_fem.npz (example-1, unmodified reference)
     python tests/golden/make_golden.py --fem2   # golden_fem2.npz (example-2, unmodified reference)
     python tests/golden/make_golden.py --experiment  # golden_experiment.npz (run_experiment loop)
@@ -285,6 +286,50 @@ def main_msrb():
     print(f"wrote {dest} ({dest.stat().st_size/1e6:.2f} MB, {len(out)} arrays)")
 
 
+def main_msrb_fem():
+    """rbi-msrbcg on the reference's own assembled problem example-1 (unmodified reference,
+    no hooks: per-parameter right-hand sides with lifted Dirichlet data) ->
+    tests/golden/golden_msrb_fem.npz."""
+    rbws = _import_reference()
+    from rbws.grid import ParametricProblem
+    from rbws.hf import HighFidelitySolver
+    from rbws.msrb import msrb_train
+    from rbws.problems import get_problem
+    from rbws.sampling import lhs_sample
+    from rbws.warmstart import MethodConfig, rbi_pcg_solve
+
+    out = {}
+    spec = get_problem("example-1")
+    p = ParametricProblem(spec, levels=3, m0=4)
+    train = lhs_sample(spec.p, 24, spec.bounds, seed=21)
+    test = lhs_sample(spec.p, 3, spec.bounds, seed=22)
+    N, K = 6, 4
+    hf = HighFidelitySolver(p, method="lu")
+    hier = msrb_train(list(train), N, K, hf, p.operator, p.rhs)
+    k0 = "msrb_ex1_n16"
+    out[f"{k0}_train"] = np.asarray(train)
+    out[f"{k0}_test"] = np.asarray(test)
+    out[f"{k0}_NK"] = np.array([N, K])
+    out[f"{k0}_init"] = hier.init_basis.basis
+    out[f"{k0}_init_eig"] = hier.init_basis.eigenvalues
+    for k, W in enumerate(hier.bases):
+        out[f"{k0}_basis{k}"] = W
+    xs, its, hists = [], [], []
+    for m in test:
+        A, f = p.operator(m), p.rhs(m)
+        cfg = MethodConfig("rbi-msrbcg", delta=1e-10, l_max=60, N=N, K_max=K)
+        x, rep = rbi_pcg_solve(A, f, cfg, msrb_hier=hier, mu=m)
+        xs.append(x)
+        its.append(rep.iterations)
+        hists.append(np.pad(rep.history, (0, 61 - len(rep.history)), constant_values=np.nan))
+    out[f"{k0}_x"] = np.array(xs)
+    out[f"{k0}_iters"] = np.array(its)
+    out[f"{k0}_hist"] = np.array(hists)
+    dest = REPO / "tests/golden/golden_msrb_fem.npz"
+    np.savez_compressed(dest, **out)
+    print(f"wrote {dest} ({dest.stat().st_size/1e6:.2f} MB, {len(out)} arrays)", its)
+
+
 def main_fem():
     """The reference's own assembled problem example-1 (Q1 FEM, Dirichlet, p = 2) through
     its unmodified API -> tests/golden/golden_fem.npz: per-level operators (CSR) and
@@ -521,6 +566,9 @@ if __name__ == "__main__":
         sys.exit(0)
     if "--fem" in sys.argv:
         main_fem()
+        sys.exit(0)
+    if "--msrb-fem" in sys.argv:
+        main_msrb_fem()
         sys.exit(0)
     if "--msrb" in sys.argv:
         main_msrb()

@@ -94,3 +94,64 @@ def test_basis_dot_kernel_matches_matmul():
         _native.call("rbws_basis_dot", n3, count, W.data_ptr(), n3, N, vv.data_ptr(), stride,
                      out2.data_ptr(), 0)
         assert torch.equal(out, out2)  # fixed-order partial sums
+
+
+# ---- rbi-msrbcg on the reference's assembled problem example-1 (stored-coefficient hierarchy,
+# per-parameter right-hand sides): goldens from the unmodified reference,
+# make_golden.py --msrb-fem
+GOLDEN_FEM = Path(__file__).resolve().parent / "golden" / "golden_msrb_fem.npz"
+
+
+@pytest.fixture(scope="module")
+def trained_fem():
+    import paper_2311_13862_b200 as pkg
+    g = dict(np.load(GOLDEN_FEM))
+    prob = pkg.ParametricProblem(pkg.get_problem("example-1"), levels=3, m0=4)
+    N, K = (int(v) for v in g["msrb_ex1_n16_NK"])
+    hf = pkg.HighFidelitySolver(prob, delta=1e-14, l_max=100)
+    hier = pkg.msrb_train(g["msrb_ex1_n16_train"], N, K, hf, prob)
+    return pkg, prob, hier, g
+
+
+def test_msrb_example1_bases_match_reference(trained_fem):
+    pkg, prob, hier, g = trained_fem
+    np.testing.assert_allclose(hier.init_basis.eigenvalues[:6], g["msrb_ex1_n16_init_eig"][:6],
+                               rtol=1e-8)
+    assert _span_err(_free(pkg, hier.init_basis.basis, 16), g["msrb_ex1_n16_init"]) <= 1e-7
+    assert len(hier.bases) == int(g["msrb_ex1_n16_NK"][1])
+    for k, W in enumerate(hier.bases):
+        assert _span_err(_free(pkg, W, 16), g[f"msrb_ex1_n16_basis{k}"]) <= 1e-5, k
+
+
+def test_rbi_msrbcg_example1_matches_reference(trained_fem):
+    pkg, prob, hier, g = trained_fem
+    test = g["msrb_ex1_n16_test"]
+    ctx = pkg.mg_context_for(prob, test)
+    N, K = (int(v) for v in g["msrb_ex1_n16_NK"])
+    cfg = pkg.MethodConfig("rbi-msrbcg", delta=1e-10, l_max=60, N=N, K_max=K)
+    x, reps = pkg.rbi_pcg_solve(pkg.BatchOperator(ctx), prob.rhs(test), cfg, mg_ctx=ctx,
+                                msrb_hier=hier)
+    got = pkg.from_padded(x, 16, len(test))
+    for m in range(len(test)):
+        assert abs(reps[m].iterations - int(g["msrb_ex1_n16_iters"][m])) <= 1
+        np.testing.assert_allclose(reps[m].history[:8], g["msrb_ex1_n16_hist"][m][:8], rtol=1e-5)
+        ref = g["msrb_ex1_n16_x"][m]
+        assert np.linalg.norm(got[m] - ref) <= 1e-8 * np.linalg.norm(ref)
+        assert reps[m].converged
+
+
+def test_msrbcg_native_edge_cases(trained):
+    """The native loop's argument checks and degenerate runs: l_max = 0 (initial guess only),
+    no bases (sweep-only preconditioner), a converged initial guess."""
+    pkg, prob, hier = trained
+    from paper_2311_13862_b200.msrb import MsrbHierarchy, rbi_msrbcg_solve
+    mus = pkg.sample_mus(prob.spec, 2, seed=4)
+    x0, r0 = rbi_msrbcg_solve(prob, mus, hier, delta=1e-10, l_max=0)
+    assert all(r.iterations == 0 for r in r0)
+    bare = MsrbHierarchy(hier.init_basis, (), hier.N, 0)
+    x1, r1 = rbi_msrbcg_solve(prob, mus, bare, delta=1e-6, l_max=200)
+    assert all(r.converged for r in r1)
+    x2, r2 = rbi_msrbcg_solve(prob, mus, hier, delta=1e-6, l_max=200)
+    assert all(r.converged for r in r2)
+    with pytest.raises(ValueError):
+        rbi_msrbcg_solve(prob, mus, hier, delta=0.0)
