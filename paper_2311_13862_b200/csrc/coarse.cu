@@ -24,9 +24,15 @@ namespace rbws {
 constexpr int kCStages = 8;
 constexpr int kCMaxPlanes = 260;  // z-factor flag table bound (planes per z-chunk + 2)
 
+// threads per CTA of the coarse-level kernels: 128 on grids up to 32 cells (four CTAs per SM
+// hide the per-CTA weight set-up and the short z march better: coarse levels of configs[1]
+// 0.91 -> 0.86 ms per V-cycle; 64 and 512 threads measured slower), 256 above
+#ifndef RBWS_COARSE_SMALL_THREADS
+#define RBWS_COARSE_SMALL_THREADS 128
+#endif
 CoarseGeom coarse_geom(int n, int batch, int nz) {
   CoarseGeom g;
-  int ty = 256 / n;
+  int ty = (n <= 32 ? RBWS_COARSE_SMALL_THREADS : 256) / n;
   if (ty < 1) ty = 1;
   if (ty > n) ty = n;
   g.ty = ty;

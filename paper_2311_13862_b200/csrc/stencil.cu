@@ -251,33 +251,45 @@ cudaError_t restrict_launch(int nf, int batch, const double* rf, double* bc, con
 // y pass of the restriction whose x and z passes ran inside the pre-smoothing kernel
 // (fine_pre_xz): bc(I,J,K) = 0.5 t(K,2J-1,I) + t(K,2J,I) + 0.5 t(K,2J+1,I), t = n/2 x n x n/2
 // per instance; with dinv_c/uc also uc = omega dinv_c bc
+// (two coarse nodes I, I+1 per thread, 16-byte loads and stores; the ghost column I = 0 gets
+// explicit zeros)
 __global__ void __launch_bounds__(256) restrict_y_kernel(int nf, const double* __restrict__ t,
                                                          double* __restrict__ bc,
                                                          const int* __restrict__ active,
                                                          const double* __restrict__ dinv_c,
                                                          double* __restrict__ uc, double omega) {
-  const int nc = nf / 2;
+  const int nc = nf / 2, nh = nc / 2;
   const int mu = blockIdx.y;
   if (active && !active[mu]) return;
   const int64_t nc3 = (int64_t)nc * nc * nc;
-  const int64_t X = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // coarse node
-  if (X >= nc3) return;
-  const int I = X % nc, J = (X / nc) % nc, K = X / ((int64_t)nc * nc);
-  if (I == 0 || J == 0 || K == 0) return;
+  const int64_t P = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // pair of coarse nodes
+  if (P >= nc3 / 2) return;
+  const int I = 2 * (int)(P % nh), J = (int)((P / nh) % nc), K = (int)(P / ((int64_t)nh * nc));
+  if (J == 0 || K == 0) return;
   const double* tk = t + (int64_t)mu * nc * nf * nc + (int64_t)K * nf * nc + I;
-  double acc = 0.0;
-  acc += 0.5 * __ldg(tk + (int64_t)(2 * J - 1) * nc);
-  acc += __ldg(tk + (int64_t)(2 * J) * nc);
-  acc += 0.5 * __ldg(tk + (int64_t)(2 * J + 1) * nc);
-  const int64_t o = (int64_t)mu * nc3 + X;
-  bc[o] = acc;
-  if (uc) uc[o] = omega * __ldg(dinv_c + o) * acc;
+  const double2 a = __ldg(reinterpret_cast<const double2*>(tk + (int64_t)(2 * J - 1) * nc));
+  const double2 c = __ldg(reinterpret_cast<const double2*>(tk + (int64_t)(2 * J) * nc));
+  const double2 d = __ldg(reinterpret_cast<const double2*>(tk + (int64_t)(2 * J + 1) * nc));
+  double2 acc;
+  acc.x = 0.0; acc.x += 0.5 * a.x; acc.x += c.x; acc.x += 0.5 * d.x;
+  acc.y = 0.0; acc.y += 0.5 * a.y; acc.y += c.y; acc.y += 0.5 * d.y;
+  if (I == 0) acc.x = 0.0;
+  const int64_t o = (int64_t)mu * nc3 + 2 * P;
+  *reinterpret_cast<double2*>(bc + o) = acc;
+  if (uc) {
+    const double2 di = __ldg(reinterpret_cast<const double2*>(dinv_c + o));
+    double2 u;
+    u.x = omega * di.x * acc.x;
+    u.y = omega * di.y * acc.y;
+    if (I == 0) u.x = 0.0;
+    *reinterpret_cast<double2*>(uc + o) = u;
+  }
 }
 
 cudaError_t restrict_y_launch(int nf, int batch, const double* t, double* bc, const LaunchCtx& lc,
                               const double* dinv_c, double* uc, double omega) {
   const int64_t nc3 = (int64_t)(nf / 2) * (nf / 2) * (nf / 2);
-  dim3 grd((unsigned)((nc3 + 255) / 256), batch);
+  dim3 grd((unsigned)((nc3 / 2 + 255) / 256), batch);
   count_launch();
   restrict_y_kernel<<<grd, 256, 0, lc.stream>>>(nf, t, bc, lc.active, dinv_c, uc, omega);
   return cudaGetLastError();
