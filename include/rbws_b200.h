@@ -107,7 +107,11 @@ int rbws_batch_set_graph(rbws_batch* b, int enable);
  * 0 never, 1 whenever the diagonal changes on few planes (any N).
  * which 1 = "SW" scaled-weights pre-smoothing kernels: -1 / 1 auto (whenever the diagonal
  * changes on few planes and the face weights are not stored), 0 never (the transformed-ring
- * kernels that stage u = omega D^-1 b). */
+ * kernels that stage u = omega D^-1 b).
+ * which 2 = fused coarse tail (every level with at most 16 cells per axis and the coarsest
+ * solve in one kernel per instance, vectors in shared memory; bitwise the per-level kernels):
+ * 1 on where it applies, -1 / 0 the per-level kernels (default: measured neutral on the
+ * headline). */
 int rbws_set_kernel_variant(int which, int value);
 /* Smoother of the V-cycle: 0 damped Jacobi (the reference default for isotropic problems,
  * multigrid.py:183-188), 1 Gauss-Seidel (smoother="gs": nu forward lexicographic sweeps

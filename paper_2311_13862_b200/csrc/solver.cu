@@ -560,12 +560,63 @@ void Batch::prof_flush() {
   ev_used = 0;
 }
 
+// The fused coarse tail (tail.cu) is opt-in (rbws_set_kernel_variant(2, 1) or RBWS_TAIL=1):
+// bitwise the per-level kernels, 13 -> 5 launches per V-cycle below the 32^3 level, but on
+// configs[1] its one CTA per instance (phases separated by CTA barriers, 16 warps per SM) takes
+// 0.29 ms per full batch against 0.23 ms for the per-level kernels, and the step is unchanged
+// (13.9-14.0k solves/s either way; it wins only on short batches)
+static std::atomic<int> g_tail{[] {
+  const char* e = getenv("RBWS_TAIL");
+  return (e && atoi(e) == 1) ? 1 : 0;
+}()};
+int solver_set_tail(int v) {
+  if (v < -1 || v > 1) return 1;
+  g_tail.store(v == 1 ? 1 : 0);
+  return 0;
+}
+static int variant_key() { return fine_variant() + 64 * g_tail.load(); }
+
+// the fused coarse tail (tail.cu) serves level lvl and everything below it?
+bool Batch::tail_level(int lvl, const LaunchCtx& lc) const {
+  if (!g_tail.load(std::memory_order_relaxed) || h->stored || smoother != 0 || nu != 1)
+    return false;
+  if (lvl < 1 || lvl >= h->levels - 1 || lvl > kTailMaxLevels || lc.zhi > 0) return false;
+  if (h->cells[lvl] > 16 || (lvl + 1 < h->levels - 1 && h->cells[lvl + 1] <= 16)) return false;
+  TailArgs t;
+  t.LT = lvl;
+  for (int l = 0; l <= lvl; ++l) {
+    t.n[l] = h->cells[l];
+    if (l >= 1 && (h->G[l] != h->G[lvl] || lv[l].coef || !lv[l].u)) return false;
+  }
+  return coarse_tail_fits(t, h->G[lvl]);
+}
+
 // one V-cycle for A^lvl out = b from zero, per active instance
 int Batch::vcycle(int lvl, const double* bb, double* out, double* dot_partial,
                   const LaunchCtx& lc) {
   cudaError_t e = cudaSuccess;
   if (lvl == 0) {
     e = coarse_solve(h->m0, count, L0, bb, out, lc);
+    if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+    return 0;
+  }
+  if (tail_level(lvl, lc)) {  // levels <= 16 cells and the coarsest solve in one kernel
+    TailArgs t;
+    t.LT = lvl;
+    t.Q = h->Q;
+    for (int l = 0; l <= lvl; ++l) {
+      t.n[l] = h->cells[l];
+      t.fac[l] = h->d_fac[l];
+      t.grp[l] = h->d_grp[l];
+    }
+    t.theta = theta;
+    t.b = bb;
+    t.u = lv[lvl].u;
+    t.e = out;
+    t.L0 = L0;
+    t.active = lc.active;
+    t.omega = omega;
+    e = coarse_tail_launch(t, h->G[lvl], count, lc.stream);
     if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
     return 0;
   }
@@ -896,7 +947,7 @@ static int pcg_graph_run(Batch* b, const Sep7& op, double* x, int tiles, int vti
                    b->gkey_delta == delta && b->gkey_lmax == l_max && b->gkey_hl == hl &&
                    b->gkey_active == act.active && b->gkey_smoother == b->smoother &&
                    b->gkey_fused == (int)b->fuse_restrict && b->gkey_wface == b->wface &&
-                   b->gkey_variant == fine_variant();
+                   b->gkey_variant == variant_key();
   cudaError_t e = cudaSuccess;
   if (!hit) {
     b->drop_graph();
@@ -957,7 +1008,7 @@ static int pcg_graph_run(Batch* b, const Sep7& op, double* x, int tiles, int vti
     b->gkey_x = x; b->gkey_count = count; b->gkey_delta = delta; b->gkey_lmax = l_max;
     b->gkey_hl = hl; b->gkey_active = act.active; b->gkey_smoother = b->smoother;
     b->gkey_fused = (int)b->fuse_restrict; b->gkey_wface = b->wface;
-    b->gkey_variant = fine_variant();
+    b->gkey_variant = variant_key();
   }
   e = cudaGraphLaunch(b->gexec, stream);
   if (e == cudaSuccess && stream != user) {

@@ -9,6 +9,7 @@
 
 #include "coarse.cuh"
 #include "stencil.cuh"
+#include "tail.cuh"
 
 namespace rbws {
 
@@ -143,6 +144,7 @@ struct Batch {
     return o;
   }
   int vcycle(int lvl, const double* b, double* out, double* dot_partial, const LaunchCtx& lc);
+  bool tail_level(int lvl, const LaunchCtx& lc) const;  // fused coarse tail (tail.cu)
 };
 
 // maxl: allocate levels 0..maxl-1 only (0 = all; the slab path's replicated coarse levels)
@@ -181,6 +183,7 @@ cudaError_t pcg_beta(int count, const double* prs, int tiles, double* rs, double
 cudaError_t pcg_true(int count, const double* prr, int tiles, const double* scale, double* out,
                      cudaStream_t s);
 
+int solver_set_tail(int v);  // fused coarse tail: 0 off, else on (process-wide, tests / A-B)
 int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double delta, int l_max,
               const PcgOut& out, cudaStream_t stream);
 // PCG with the iteration-indexed multispace reduced-basis preconditioner (msrb.cu): basis

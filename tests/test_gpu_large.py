@@ -253,6 +253,30 @@ def test_sw_variant_matches_transformed(n, case):
     _compare_runs(var, base, 1e-13)
 
 
+@pytest.mark.parametrize("n,case,m0", [(16, (2, 1, 1), 4), (32, (2, 2, 1), 4), (64, (2, 2, 1), 4),
+                                       (64, (2, 2, 2), 4), (32, (2, 2, 2), 2), (128, (2, 2, 2), 4)])
+def test_coarse_tail_matches_per_level_kernels(n, case, m0):
+    """The opt-in fused coarse tail (levels <= 16 cells + the coarsest solve in one kernel,
+    vectors in shared memory; rbws_set_kernel_variant(2, 1)) against the per-level kernels:
+    every sum is taken in the same order, so V-cycles and solves agree to rounding (observed
+    bitwise)."""
+    pkg = _pkg()
+    from paper_2311_13862_b200 import _native
+    spec, ospec = _specs(case)
+    prob = pkg.ParametricProblem(spec, levels=pkg.problems.levels_for(n, m0), m0=m0)
+    mus = op.sample_mus(ospec, 5, seed=58)
+    delta = 1e-10
+    try:
+        _native.call("rbws_set_kernel_variant", 2, 0)
+        base = _vcycle_and_solve(prob, mus, delta, n)
+        _native.call("rbws_set_kernel_variant", 2, 1)
+        var = _vcycle_and_solve(prob, mus, delta, n)
+    finally:
+        _native.call("rbws_set_kernel_variant", 2, -1)
+    _compare_runs(var, base, 1e-13)
+    print("tail vs per-level: max |dv| =", float((var[0] - base[0]).abs().max()))
+
+
 @pytest.mark.parametrize("n,count", [(256, 2), (512, 1)])
 def test_fused_restrict_matches_separate_large(monkeypatch, n, count):
     """Pre-smoothing fused with the x/z restriction vs the separate kernels (N = 256, 512)."""
