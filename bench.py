@@ -151,9 +151,9 @@ def make_ospec(cfg):
 
 def _traffic(kernel, bytes_per_launch, cfg):
     """DRAM bytes per launch for the dominant kernel from the committed ncu capture
-    (profiles/r01_traffic.json, configs[1]); scaled to this run's average launch by the
+    (profiles/r02_traffic.json, configs[1]); scaled to this run's average launch by the
     captured traffic/algorithmic ratio. None for workloads that were not captured."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_traffic.json")
     if cfg["workload"] != CONFIGS[1]["workload"] or not os.path.exists(path):
         return None, None
     with open(path) as fh:
