@@ -169,11 +169,15 @@ struct SL {
 #ifndef RBWS_N128_XF_S
 #define RBWS_N128_XF_S 4
 #endif
+// raw ring slots of the scaled-weights kernels at N = 128 (4: three CTAs per SM fit)
+#ifndef RBWS_N128_SW_S
+#define RBWS_N128_SW_S 6
+#endif
   static constexpr int S = XF ? (N >= 512 ? (RBWS_N512_NPT == 2 ? (MODE == FM_POSTP ? 2 : 3) : 4)
                                           : (N >= 256 ? (MODE == FM_POSTP ? 3 : RBWS_N256_XF_S)
                                                       : (N >= 128 ? (MODE == FM_PREX ? 3 : RBWS_N128_XF_S)
                                                                   : 6)))
-                              : (N >= 128 ? 6 : kStages);
+                              : (N >= 128 ? ((SW && N == 128) ? RBWS_N128_SW_S : 6) : kStages);
   static constexpr int U = 6;
 };
 
