@@ -316,6 +316,7 @@ cudaError_t expand(int n, int count, const double* W, int64_t Wstride, int N, co
   const int64_t n3 = (int64_t)n * n * n;
   if (N <= 8) return expand_nb<8>(n3, count, W, Wstride, N, a, x, stream);
   if (N <= 16) return expand_nb<16>(n3, count, W, Wstride, N, a, x, stream);
+  if (N <= 20) return expand_nb<20>(n3, count, W, Wstride, N, a, x, stream);
   if (N <= 24) return expand_nb<24>(n3, count, W, Wstride, N, a, x, stream);
   if (N <= 32) return expand_nb<32>(n3, count, W, Wstride, N, a, x, stream);
   if (N <= 48) return expand_nb<48>(n3, count, W, Wstride, N, a, x, stream);

@@ -298,6 +298,8 @@ cudaError_t restrict_y_launch(int nf, int batch, const double* t, double* bc, co
 // z-marching trilinear prolongation: one thread per fine column (i, j); the
 // xy-interpolated coarse values of the two bracketing coarse planes are kept in
 // registers, so each fine node costs one coarse gather per two fine planes.
+// (a thread owns the fine column pair (2 ip, 2 ip + 1) of row j: both columns interpolate from
+// the same coarse entries, 16-byte loads / stores; the ghost column i = 0 receives P e = 0)
 __global__ void __launch_bounds__(512) prolong_kernel(int nf, int mode, int ty, int zc,
                                                       const double* __restrict__ ec,
                                                       double* __restrict__ u,
@@ -309,48 +311,74 @@ __global__ void __launch_bounds__(512) prolong_kernel(int nf, int mode, int ty, 
   const int nc = nf / 2;
   const int mu = blockIdx.z / zc, kc = blockIdx.z % zc;
   if (active && !active[mu]) return;
-  const int i = threadIdx.x % nf;
-  const int j = blockIdx.y * ty + threadIdx.x / nf;
-  if (i == 0 || j == 0) return;
+  const int ip = threadIdx.x % nc;
+  const int j = blockIdx.y * ty + threadIdx.x / nc;
+  if (j == 0) return;
   const int64_t nf2 = (int64_t)nf * nf, nc2 = (int64_t)nc * nc;
-  const double* e = ec + (int64_t)mu * nc2 * nc + (i >> 1) + (int64_t)nc * (j >> 1);
-  const bool oi = i & 1, oj = j & 1;
-  auto vxy = [&](int K) -> double {  // coarse plane K interpolated to (i, j)
+  const double* e = ec + (int64_t)mu * nc2 * nc + ip + (int64_t)nc * (j >> 1);
+  const bool oj = j & 1;
+  // coarse plane K interpolated to (2 ip, j) and (2 ip + 1, j)
+  auto vxy = [&](int K, double& ve, double& vo) {
     const double* q = e + nc2 * K;
-    double r0 = oi ? 0.5 * (__ldg(q) + __ldg(q + 1)) : __ldg(q);
-    if (!oj) return r0;
-    const double* q1 = q + nc;
-    const double r1 = oi ? 0.5 * (__ldg(q1) + __ldg(q1 + 1)) : __ldg(q1);
-    return 0.5 * (r0 + r1);
+    const double q0 = __ldg(q), q1 = __ldg(q + 1);
+    const double r0e = q0, r0o = 0.5 * (q0 + q1);
+    if (!oj) {
+      ve = r0e;
+      vo = r0o;
+      return;
+    }
+    const double p0 = __ldg(q + nc), p1 = __ldg(q + nc + 1);
+    ve = 0.5 * (r0e + p0);
+    vo = 0.5 * (r0o + 0.5 * (p0 + p1));
   };
   const int kz = (zhi - zlo + zc - 1) / zc;
   const int kb = max(1, zlo + kc * kz), ke = min(min(nf, zhi), zlo + (kc + 1) * kz);
   if (kb >= ke) return;
   int Kc = kb >> 1;
-  double v0 = vxy(Kc), v1 = vxy(Kc + 1);
-  const int64_t col = (int64_t)mu * nf2 * nf + i + (int64_t)nf * j;
+  double e0, o0, e1, o1;
+  vxy(Kc, e0, o0);
+  vxy(Kc + 1, e1, o1);
+  const int64_t col = (int64_t)mu * nf2 * nf + 2 * ip + (int64_t)nf * j;
   for (int k = kb; k < ke; ++k) {
     const int K = k >> 1;
     if (K != Kc) {  // advance one coarse plane
-      v0 = v1;
-      v1 = vxy(K + 1);
+      e0 = e1;
+      o0 = o1;
+      vxy(K + 1, e1, o1);
       Kc = K;
     }
-    const double pe = (k & 1) ? 0.5 * (v0 + v1) : v0;
+    const double pe = (k & 1) ? 0.5 * (e0 + e1) : e0;
+    const double po = (k & 1) ? 0.5 * (o0 + o1) : o0;
     const int64_t idx = col + (int64_t)k * nf2;
-    if (mode == 0) u[idx] += pe;
-    else if (mode == 2) u[idx] = __ldg(b + idx) + pe;  // b holds the pre-scaled rhs w D^-1 b
-    else u[idx] = fma(omega * __ldg(dinv + idx), __ldg(b + idx), pe);
+    double2* up = reinterpret_cast<double2*>(u + idx);
+    double2 v;
+    if (mode == 0) {
+      v = *up;
+      v.x += pe;
+      v.y += po;
+    } else if (mode == 2) {  // b holds the pre-scaled rhs w D^-1 b
+      const double2 bv = __ldg(reinterpret_cast<const double2*>(b + idx));
+      v.x = bv.x + pe;
+      v.y = bv.y + po;
+    } else {
+      const double2 bv = __ldg(reinterpret_cast<const double2*>(b + idx));
+      const double2 dv = __ldg(reinterpret_cast<const double2*>(dinv + idx));
+      v.x = fma(omega * dv.x, bv.x, pe);
+      v.y = fma(omega * dv.y, bv.y, po);
+    }
+    *up = v;
   }
 }
 
 cudaError_t prolong_launch(int nf, int batch, int mode, const double* ec, double* u,
                            const double* b, const double* dinv, double omega,
                            const LaunchCtx& lc) {
-  int ty = 256 / nf;
+  const int nc = nf / 2;
+  int ty = 256 / nc;
   if (ty < 1) ty = 1;
   if (ty > nf) ty = nf;
-  const int threads = ty * nf;
+  while (nf % ty) --ty;
+  const int threads = ty * nc;
   const int zlo = lc.zhi > 0 ? lc.zlo : 0, zhi = lc.zhi > 0 ? lc.zhi : nf;
   int zc = 1;
   while ((int64_t)(nf / ty) * batch * zc < 4 * 148 && (zhi - zlo) / (zc * 2) >= 4) zc *= 2;

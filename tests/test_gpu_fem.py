@@ -181,10 +181,14 @@ def test_fem_l1roc_rbi_mgcg_matches_reference(probs):
 
 
 def test_fem_unsupported_paths_fail_loudly(probs):
+    """rbi-msrbcg runs on example-1 (tests/test_gpu_msrb.py); the full-node layout of example-2
+    has no Gauss-Seidel sweep, so the multispace method is refused there with a clear error."""
     pkg = _pkg()
-    p = probs["n16m4"]
+    spec2 = pkg.get_problem("example-2")
+    p2 = pkg.ParametricProblem(spec2, levels=2, m0=4)
+    mus = np.array(pkg.problems.lhs_sample(spec2.p, 2, spec2.bounds, seed=1))
     with pytest.raises(NotImplementedError):
-        pkg.msrb_train(G["fem_n16m4_mus"], 2, 1, None, p)
+        pkg.msrb_train(mus, 2, 1, None, p2)
 
 
 def test_fem_gs_smoother_matches_reference(probs):
