@@ -111,7 +111,11 @@ int rbws_batch_set_graph(rbws_batch* b, int enable);
  * which 2 = fused coarse tail (every level with at most 16 cells per axis and the coarsest
  * solve in one kernel per instance, vectors in shared memory; bitwise the per-level kernels):
  * 1 on where it applies, -1 / 0 the per-level kernels (default: measured neutral on the
- * headline). */
+ * headline).
+ * which 3 = p-update kernel that forms the neighbours' p = s + beta p_old where they are read
+ * (no transformed ring, three CTAs per SM; bitwise the transformed-ring kernel): 1 on
+ * (N <= 128, weights not stored), -1 / 0 the transformed-ring kernel (default: measured
+ * slower). */
 int rbws_set_kernel_variant(int which, int value);
 /* Smoother of the V-cycle: 0 damped Jacobi (the reference default for isotropic problems,
  * multigrid.py:183-188), 1 Gauss-Seidel (smoother="gs": nu forward lexicographic sweeps

@@ -50,7 +50,24 @@ int fine_set_sw(int v) {
   g_force_sw.store(v);
   return 0;
 }
-int fine_variant() { return (g_force_dc.load() + 1) + 4 * (g_force_sw.load() + 1); }
+// p-update kernel without the transformed ring (the neighbours' p = s + beta p_old formed
+// where they are read; 80 registers, three CTAs per SM; bitwise the transformed-ring kernel):
+// opt-in (RBWS_PAPPLY_DIRECT=1 / rbws_set_kernel_variant(3, 1)) — measured slower on configs[1],
+// 1.12 -> 1.17 ms per full launch (1.24 ms at two CTAs per SM): unlike the pre-smoothing it
+// saves no HBM stream, and the 8 neighbour loads + 4 FMAs per node cost more than the
+// transformed ring's store + barrier coupling
+static std::atomic<int> g_direct_papply{[] {
+  const char* e = getenv("RBWS_PAPPLY_DIRECT");
+  return (e && atoi(e) == 1) ? 1 : 0;
+}()};
+int fine_set_direct(int v) {
+  if (v < -1 || v > 1) return 1;
+  g_direct_papply.store(v == 1 ? 1 : 0);
+  return 0;
+}
+int fine_variant() {
+  return (g_force_dc.load() + 1) + 4 * (g_force_sw.load() + 1) + 16 * g_direct_papply.load();
+}
 constexpr int kThreads = 256;  // threads per CTA (one per grid column of the tile; N = 512: 512)
 
 // Compile-time tile geometry for a grid with N cells per axis: RPP rows per pass
@@ -155,7 +172,10 @@ struct SL {
   // plane is transformed once into a second ring, so neighbours cost one LDS
   static constexpr bool XF = !SW && (MODE == FM_PRE || MODE == FM_PREX || MODE == FM_PAPPLY ||
                                      MODE == FM_POSTP);
-  static constexpr int NH = XF ? 2 : 1;  // DC: h1 (1/diag) staged only on reload planes
+  // SW on FM_PAPPLY ("direct"): no transformed ring either; the neighbours' p = s + beta p_old
+  // are formed from the two staged arrays where they are read
+  static constexpr bool DIRECT = SW && MODE == FM_PAPPLY;
+  static constexpr int NH = (XF || DIRECT) ? 2 : 1;  // DC: h1 (1/diag) staged only on reload planes
   static constexpr int NC = (MODE == FM_CG) ? 2 : ((MODE == FM_RESID || MODE == FM_JACOBI) ? 1 : 0);
   // raw / transformed ring slots (N = 512 rows are 4 KB: a shallower raw ring fits 227 KB).
   // U >= 6: a trip reads transformed planes k-1 .. k+2 while the next trip's transform
@@ -177,7 +197,8 @@ struct SL {
                                           : (N >= 256 ? (MODE == FM_POSTP ? 3 : RBWS_N256_XF_S)
                                                       : (N >= 128 ? (MODE == FM_PREX ? 3 : RBWS_N128_XF_S)
                                                                   : 6)))
-                              : (N >= 128 ? ((SW && N == 128) ? RBWS_N128_SW_S : 6) : kStages);
+                              : (N >= 128 ? ((SW && N == 128) ? RBWS_N128_SW_S : 6)
+                                          : (DIRECT ? 6 : kStages));
   static constexpr int U = 6;
 };
 
@@ -223,7 +244,10 @@ __global__ void __launch_bounds__(FTM<MODE, N>::THREADS,
                                   FTM<MODE, N>::THREADS <= 256
                                       ? ((SW && N <= 128) ? RBWS_SW_MIN_CTAS : RBWS_MIN_CTAS) : 1)
 fine_kernel(FineArgs a) {
-  static_assert(!SW || ((MODE == FM_PRE || MODE == FM_PREX) && !DC && !SCW), "SW: PRE / PREX only");
+  static_assert(!SW || ((MODE == FM_PRE || MODE == FM_PREX || MODE == FM_PAPPLY) && !DC && !SCW),
+                "SW: PRE / PREX (scaled weights) and PAPPLY (direct neighbours) only");
+  constexpr bool SCALED = SW && (MODE == FM_PRE || MODE == FM_PREX);
+  constexpr bool DIRECT = SW && MODE == FM_PAPPLY;
   using G = FTM<MODE, N>;
   using L = SL<MODE, N, DC, SW>;
   constexpr bool XF = L::XF;
@@ -279,7 +303,7 @@ fine_kernel(FineArgs a) {
     for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
     mbar_fence_init();
   }
-  if (SW && tid < 64) {  // plane flags of the staged planes, 32 per word
+  if (SCALED && tid < 64) {  // plane flags of the staged planes, 32 per word
     const int m = p_first + tid;
     const bool f = tid < np && (m <= 1 || m >= N || __ldg(op.fz + m) != 0);
     const uint32_t bits = __ballot_sync(0xffffffffu, f);
@@ -342,7 +366,7 @@ fine_kernel(FineArgs a) {
   // and n multiply zeros of b, so they never force a rebuild); bit t = plane p_first + t
   uint64_t smask = 0;
   auto fzx = [&](int m) -> bool { return m <= 1 || m >= N || __ldg(op.fz + m) != 0; };
-  if (SW) {
+  if (SCALED) {
     const uint64_t fm = ((uint64_t)swbits[1] << 32) | swbits[0];  // bit t: fzx(p_first + t)
     smask = (fm << 1) & fm & (fm >> 1);
   }
@@ -419,7 +443,7 @@ fine_kernel(FineArgs a) {
   };
 #pragma unroll
   for (int r = 0; r < NPT; ++r) {  // plane kb-1: its z face (kb-1, kb) is wzm of plane kb
-    if (SCW || SW) break;
+    if (SCW || SCALED) break;
     weights(r, zf);
     wzm[r] = wzp[r];
   }
@@ -500,6 +524,12 @@ fine_kernel(FineArgs a) {
     }
   };
 
+  // own-column stencil input of row r on staged plane p (non-transformed modes; DIRECT:
+  // p = s + beta p_old formed here)
+  auto own = [&](int p, int r) -> double {
+    const double* R = raw(p) + hoff + r * RPP * N;
+    return DIRECT ? fma(sc, R[HSZ], R[0]) : R[0];
+  };
   // Own-column values march in registers: xd = u(k-1), xc = u(k); only the four
   // in-plane neighbours are read from shared memory.
   double xd[NPT], xc[NPT], bcv[NPT];
@@ -518,8 +548,8 @@ fine_kernel(FineArgs a) {
     wait(p_first + 1);
 #pragma unroll
     for (int r = 0; r < NPT; ++r) {
-      xd[r] = raw(p_first)[hoff + r * RPP * N];
-      xc[r] = raw(p_first + 1)[hoff + r * RPP * N];
+      xd[r] = own(p_first, r);
+      xc[r] = own(p_first + 1, r);
     }
   }
 
@@ -528,7 +558,7 @@ fine_kernel(FineArgs a) {
   // face weights for plane k (refreshed only where the z factors change; CTA-uniform)
   auto refresh = [&](int k) {
     if (SCW) return;
-    if constexpr (SW) {
+    if constexpr (SCALED) {
       if (k == kb || !steady_sw(k)) {
 #pragma unroll
         for (int r = 0; r < NPT; ++r) scaled(r, k, gk + r * RPP * N);
@@ -568,6 +598,13 @@ fine_kernel(FineArgs a) {
   // the four in-plane neighbours of row r's node on plane k (shared memory)
   auto nbrs = [&](int k, int r, double* nb) {
     const double* P0 = (XF ? uring + (k - p_first) % U * HSZ : raw(k)) + hoff + r * RPP * N;
+    if (DIRECT) {  // s + beta p_old of the neighbours
+      nb[0] = fma(sc, P0[HSZ + 1], P0[1]);
+      nb[1] = fma(sc, P0[HSZ - 1], P0[-1]);
+      nb[2] = fma(sc, P0[HSZ + N], P0[N]);
+      nb[3] = fma(sc, P0[HSZ - N], P0[-N]);
+      return;
+    }
     nb[0] = P0[1];
     nb[1] = P0[-1];
     nb[2] = P0[N];
@@ -599,7 +636,7 @@ fine_kernel(FineArgs a) {
     }
     // shallow FMA tree (a dependent chain of 6 would be latency bound)
     // (SW: the weights are scaled by the neighbours' w/diag and the input is b itself)
-    if (SW) vbr = uc;
+    if (SCALED) vbr = uc;
     const double offx = fma(xm, uw, xp * ue);
     const double offy = fma(ym, us, yp * un);
     const double offz = fma(zm, ud, zp * uu);
@@ -705,14 +742,14 @@ fine_kernel(FineArgs a) {
     } else {
       wait(k0 + 1);
 #pragma unroll
-      for (int r = 0; r < NPT; ++r) u0[r] = raw(k0 + 1)[hoff + r * RPP * N];
+      for (int r = 0; r < NPT; ++r) u0[r] = own(k0 + 1, r);
       if (two) {
         wait(k0 + 2);
 #pragma unroll
-        for (int r = 0; r < NPT; ++r) u1[r] = raw(k0 + 2)[hoff + r * RPP * N];
+        for (int r = 0; r < NPT; ++r) u1[r] = own(k0 + 2, r);
       }
     }
-    if (two && (SW ? (k0 != kb && steady_sw(k0) && steady_sw(k0 + 1))
+    if (two && (SCALED ? (k0 != kb && steady_sw(k0) && steady_sw(k0 + 1))
                    : (steady(k0) && repeats(k0 + 1)))) {
       // common case: both planes keep the weights; one straight-line block of 2*NPT
       // independent nodes (latency hiding by ILP)
@@ -807,6 +844,9 @@ static cudaError_t fine_launch_mn(const FineArgs& a, int batch, cudaStream_t str
   if (a.op.wface) return fine_launch_mnd<MODE, N, false, true>(a, batch, stream);
   if constexpr (MODE == FM_PRE || MODE == FM_PREX)
     if (a.sw) return fine_launch_mnd<MODE, N, false, false, true>(a, batch, stream);
+  if constexpr (MODE == FM_PAPPLY)
+    if (g_direct_papply.load(std::memory_order_relaxed) && N <= 128)
+      return fine_launch_mnd<MODE, N, false, false, true>(a, batch, stream);
   if constexpr (MODE == FM_PRE || MODE == FM_PREX || MODE == FM_POSTP)
     if (a.dc) return fine_launch_mnd<MODE, N, true>(a, batch, stream);
   return fine_launch_mnd<MODE, N, false>(a, batch, stream);

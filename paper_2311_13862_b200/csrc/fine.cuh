@@ -9,6 +9,8 @@ namespace rbws {
 int fine_set_dc(int v);
 // override of the scaled-weights pre-smoothing kernels (-1 / 1 auto, 0 never)
 int fine_set_sw(int v);
+// p-update kernel without the transformed ring (-1 / 1 on, 0 off)
+int fine_set_direct(int v);
 int fine_variant();  // current override (part of the cached PCG graph's key)
 
 struct FineGeom {

@@ -574,7 +574,7 @@ int solver_set_tail(int v) {
   g_tail.store(v == 1 ? 1 : 0);
   return 0;
 }
-static int variant_key() { return fine_variant() + 64 * g_tail.load(); }
+static int variant_key() { return fine_variant() + 1024 * g_tail.load(); }
 
 // the fused coarse tail (tail.cu) serves level lvl and everything below it?
 bool Batch::tail_level(int lvl, const LaunchCtx& lc) const {
@@ -873,17 +873,25 @@ cudaError_t pcg_true(int count, const double* prr, int tiles, const double* scal
 // Streaming download: copy the solutions of instances that stopped iterating since the
 // last call (all remaining ones when `all`) to the host on out.copy_stream, after the
 // compute stream reaches this point.  Consecutive instances go in one copy.
-static int stream_download(Batch* b, const double* x, const PcgOut& out, int call, bool all,
-                           cudaStream_t stream) {
+// Two phases, so that the host does not hold back the next iteration's launches while it
+// enqueues up to `count` copies (3-5 us of host time each): dl_mark reads the active flags,
+// claims the finished instances and records the compute-stream event their x is final at;
+// dl_flush enqueues the claimed copies behind that event.  The PCG loops call dl_mark where an
+// iteration's active count is known and dl_flush after the next iteration's kernels are
+// launched (x of a stopped instance is never written again).
+static int dl_mark(Batch* b, const PcgOut& out, int call, bool all, cudaStream_t stream) {
   if (!out.x_host) return 0;
   const int count = b->count;
-  const int64_t n3 = (int64_t)b->h->n * b->h->n * b->h->n;
   if (!all) {
     cudaError_t e = fetch_to_host(b->h_active.data(), b->active, sizeof(int) * count, stream);
     if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
   }
   bool any = false;
-  for (int m = 0; m < count && !any; ++m) any = !b->h_sent[m] && (all || !b->h_active[m]);
+  for (int m = 0; m < count; ++m)
+    if (!b->h_sent[m] && (all || !b->h_active[m])) {
+      b->h_sent[m] = 2;  // claimed, copy not enqueued yet
+      any = true;
+    }
   if (!any) return 0;
   while ((size_t)call >= b->dl_ev.size()) {
     cudaEvent_t ev;
@@ -891,17 +899,25 @@ static int stream_download(Batch* b, const double* x, const PcgOut& out, int cal
     if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
     b->dl_ev.push_back(ev);
   }
-  cudaEvent_t ev = b->dl_ev[call];
-  cudaError_t e = cudaEventRecord(ev, stream);
+  cudaError_t e = cudaEventRecord(b->dl_ev[call], stream);
   if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
-  e = cudaStreamWaitEvent(out.copy_stream, ev, 0);
-  if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+  b->dl_pending.push_back(call);
+  return 0;
+}
+
+static int dl_flush(Batch* b, const double* x, const PcgOut& out) {
+  if (!out.x_host || b->dl_pending.empty()) return 0;
+  const int count = b->count;
+  const int64_t n3 = (int64_t)b->h->n * b->h->n * b->h->n;
+  cudaError_t e = cudaSuccess;
+  // the claimed instances' x became final no later than the last recorded event
+  e = cudaStreamWaitEvent(out.copy_stream, b->dl_ev[b->dl_pending.back()], 0);
+  b->dl_pending.clear();
   int m = 0;
   while (m < count && e == cudaSuccess) {
-    if (b->h_sent[m] || !(all || !b->h_active[m])) { ++m; continue; }
+    if (b->h_sent[m] != 2) { ++m; continue; }
     int m1 = m;
-    while (m1 < count && !b->h_sent[m1] && (all || !b->h_active[m1]) &&
-           (out.host_stride == n3 || m1 == m)) {
+    while (m1 < count && b->h_sent[m1] == 2 && (out.host_stride == n3 || m1 == m)) {
       b->h_sent[m1] = 1;
       ++m1;
     }
@@ -911,6 +927,13 @@ static int stream_download(Batch* b, const double* x, const PcgOut& out, int cal
   }
   if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
   return 0;
+}
+
+// mark + flush in one step (the end of a solve, instances converged at x0)
+static int stream_download(Batch* b, const double* x, const PcgOut& out, int call, bool all,
+                           cudaStream_t stream) {
+  if (dl_mark(b, out, call, all, stream)) return 1;
+  return dl_flush(b, x, out);
 }
 
 // device-side loop condition: keep iterating while any instance is active
@@ -1106,11 +1129,12 @@ static int pcg_solve_stored(Batch* b, const double* f, int64_t f_stride, double*
       pcg_check_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, tiles, b->scale,
                                                              delta, l_max, b->hist, hl, b->active,
                                                              b->iters, b->nactive);
+      if (dl_flush(b, x, out)) return 1;  // (behind this iteration's launches)
       e = fetch_to_host(b->h_nactive, b->nactive, sizeof(int), stream);
       if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
       if (*b->h_nactive == 0) break;
       if (out.x_host && *b->h_nactive < b->cur_active &&
-          stream_download(b, x, out, dl_call++, false, stream))
+          dl_mark(b, out, dl_call++, false, stream))
         return 1;
       b->cur_active = *b->h_nactive;
       if (b->vcycle(L - 1, b->r, b->s, b->partial, act)) return 1;
@@ -1227,12 +1251,14 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
                                                              delta, l_max, b->hist, hl, b->active,
                                                              b->iters, b->nactive);
       if (pf) b->prof_end(PROF_SCALARS, t0, stream);
+      if (dl_flush(b, x, out)) return 1;  // (behind this iteration's launches)
       e = fetch_to_host(b->h_nactive, b->nactive, sizeof(int), stream);
       if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
       if (*b->h_nactive == 0) break;
-      // instances that stopped this iteration: their x is final, start the download
+      // instances that stopped this iteration: their x is final; claim them now, enqueue
+      // the copies once the next iteration's kernels are launched
       if (out.x_host && *b->h_nactive < b->cur_active &&
-          stream_download(b, x, out, dl_call++, false, stream))
+          dl_mark(b, out, dl_call++, false, stream))
         return 1;
       b->cur_active = *b->h_nactive;
       if (b->vcycle(L - 1, b->r, b->s, b->partial, act)) return 1;

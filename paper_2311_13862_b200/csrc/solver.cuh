@@ -103,6 +103,7 @@ struct Batch {
   int* h_nactive = nullptr;         // pinned
   std::vector<int> h_active, h_sent;  // streaming download bookkeeping (host)
   std::vector<cudaEvent_t> dl_ev;     // compute-stream points the downloads wait for
+  std::vector<int> dl_pending;        // marked download calls whose copies are not enqueued yet
   // device-side PCG loop (iterations 1..) as a conditional CUDA graph, cached per solve shape
   bool use_graph = true;
   cudaGraph_t graph = nullptr;

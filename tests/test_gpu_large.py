@@ -253,6 +253,29 @@ def test_sw_variant_matches_transformed(n, case):
     _compare_runs(var, base, 1e-13)
 
 
+@pytest.mark.parametrize("n,case", [(16, (2, 1, 1)), (64, (2, 2, 1)), (64, "smooth"),
+                                    (128, (2, 2, 2))])
+def test_direct_p_update_matches_transformed(n, case):
+    """The opt-in p-update kernel that forms the neighbours' p = s + beta p_old where it reads
+    them (no transformed ring; rbws_set_kernel_variant(3, 1)) against the default
+    transformed-ring kernel: same sums in the same order (observed bitwise)."""
+    pkg = _pkg()
+    from paper_2311_13862_b200 import _native
+    spec, ospec = _specs(case)
+    prob = pkg.ParametricProblem(spec, levels=pkg.problems.levels_for(n, 4), m0=4)
+    mus = op.sample_mus(ospec, 3, seed=59)
+    delta = 1e-10
+    try:
+        _native.call("rbws_set_kernel_variant", 3, 0)
+        base = _vcycle_and_solve(prob, mus, delta, n)
+        _native.call("rbws_set_kernel_variant", 3, 1)
+        var = _vcycle_and_solve(prob, mus, delta, n)
+    finally:
+        _native.call("rbws_set_kernel_variant", 3, -1)
+    _compare_runs(var, base, 1e-13)
+    print("direct vs transformed p-update: max |dx| =", float((var[1] - base[1]).abs().max()))
+
+
 @pytest.mark.parametrize("n,case,m0", [(16, (2, 1, 1), 4), (32, (2, 2, 1), 4), (64, (2, 2, 1), 4),
                                        (64, (2, 2, 2), 4), (32, (2, 2, 2), 2), (128, (2, 2, 2), 4)])
 def test_coarse_tail_matches_per_level_kernels(n, case, m0):
