@@ -189,6 +189,10 @@ struct SL {
 #ifndef RBWS_N128_XF_S
 #define RBWS_N128_XF_S 4
 #endif
+// residual kernel (initial and true residual of every solve) at N <= 64: CTAs per SM
+#ifndef RBWS_RESID_CTAS
+#define RBWS_RESID_CTAS 2
+#endif
 // raw ring slots of the scaled-weights kernels at N = 128 (4: three CTAs per SM fit)
 #ifndef RBWS_N128_SW_S
 #define RBWS_N128_SW_S 6
@@ -198,7 +202,8 @@ struct SL {
                                                       : (N >= 128 ? (MODE == FM_PREX ? 3 : RBWS_N128_XF_S)
                                                                   : 6)))
                               : (N >= 128 ? ((SW && N == 128) ? RBWS_N128_SW_S : 6)
-                                          : (DIRECT ? 6 : kStages));
+                                          : ((DIRECT || (RBWS_RESID_CTAS == 3 && MODE == FM_RESID))
+                                                 ? 6 : kStages));
   static constexpr int U = 6;
 };
 
@@ -242,7 +247,10 @@ struct FSmem {
 template <int MODE, int N, bool DC, bool SCW, bool SW = false>
 __global__ void __launch_bounds__(FTM<MODE, N>::THREADS,
                                   FTM<MODE, N>::THREADS <= 256
-                                      ? ((SW && N <= 128) ? RBWS_SW_MIN_CTAS : RBWS_MIN_CTAS) : 1)
+                                      ? ((SW && N <= 128) ? RBWS_SW_MIN_CTAS
+                                         : ((MODE == FM_RESID && N <= 64 && !SCW) ? RBWS_RESID_CTAS
+                                                                                   : RBWS_MIN_CTAS))
+                                      : 1)
 fine_kernel(FineArgs a) {
   static_assert(!SW || ((MODE == FM_PRE || MODE == FM_PREX || MODE == FM_PAPPLY) && !DC && !SCW),
                 "SW: PRE / PREX (scaled weights) and PAPPLY (direct neighbours) only");
