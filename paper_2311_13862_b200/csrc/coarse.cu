@@ -245,14 +245,20 @@ __global__ void __launch_bounds__(256) coarse_kernel(CoarseArgs a) {
 // s_g of planes k-1, k, k+1 march in registers; Z_g(k, .) is a CTA-uniform table.
 // For thermal blocks G = 2 (4 with a z split): ~12G FMAs and 9 LDS per node and
 // about a third of the 27-coefficient kernel's registers (two CTAs per SM).
-template <int G, int MODE>
+// NT > 0: the grid size (and with it the tile rows, every shared-memory offset and row stride)
+// is a compile-time constant — the generic kernel spends ~40 % of its instructions on index
+// arithmetic (ncu: 149 instructions per node at 32^3, issue-bound); NT = 0: any grid.
+__host__ __device__ constexpr int coarse_ty(int n) {
+  return (n <= 32 ? RBWS_COARSE_SMALL_THREADS : 256) / n;
+}
+template <int G, int MODE, int NT = 0>
 __global__ void __launch_bounds__(256, 2) coarse_kron_kernel(CoarseArgs a) {
   constexpr int NH = (MODE == CM_DINV) ? 0 : 1;
   constexpr int NC = (MODE == CM_RESID || MODE == CM_JACOBI) ? 1 : 0;
   constexpr int S = kCStages;
   extern __shared__ __align__(128) unsigned char smem[];
-  const int n = a.n, n1 = n + 1, Q = a.Q;
-  const int ty = a.g.ty, zc = a.g.zc;
+  const int n = NT > 0 ? NT : a.n, n1 = n + 1, Q = a.Q;
+  const int ty = NT > 0 ? coarse_ty(NT > 0 ? NT : 1) : a.g.ty, zc = a.g.zc;
   const int kc = blockIdx.z % zc, mu = blockIdx.z / zc;
   if (a.active && !a.active[mu]) return;
   const int j0 = blockIdx.y * ty;
@@ -432,14 +438,22 @@ static cudaError_t coarse_kron_launch_m(CoarseArgs a, int batch, cudaStream_t st
   if (np > kCMaxPlanes) return cudaErrorInvalidValue;
   const size_t smem = 64 + 4 * kCMaxPlanes + 8 * (((size_t)np * G * 3 + 1) & ~(size_t)1) +
                       (size_t)kCStages * (NH * ((a.g.ty + 2) * a.n + 2) + NC * a.g.ty * a.n) * 8;
-  {
-    cudaError_t e = smem_attr((const void*)coarse_kron_kernel<G, MODE>, smem);
-    if (e != cudaSuccess) return e;
-  }
   dim3 grd(1, a.g.ytiles, batch * a.g.zc);
-  count_launch();
-  coarse_kron_kernel<G, MODE><<<grd, a.g.threads, smem, stream>>>(a);
-  return cudaGetLastError();
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t e = smem_attr((const void*)kern, smem);
+    if (e != cudaSuccess) return e;
+    count_launch();
+    kern<<<grd, a.g.threads, smem, stream>>>(a);
+    return cudaGetLastError();
+  };
+  // compile-time grid size for the sizes of the BASELINE hierarchies (RESID / JACOBI: the
+  // V-cycle's kernels)
+  if (MODE == CM_RESID || MODE == CM_JACOBI) {
+    if (a.n == 16 && a.g.ty == coarse_ty(16)) return go(coarse_kron_kernel<G, MODE, 16>);
+    if (a.n == 32 && a.g.ty == coarse_ty(32)) return go(coarse_kron_kernel<G, MODE, 32>);
+    if (a.n == 64 && a.g.ty == coarse_ty(64)) return go(coarse_kron_kernel<G, MODE, 64>);
+  }
+  return go(coarse_kron_kernel<G, MODE, 0>);
 }
 
 template <int G>
