@@ -208,3 +208,30 @@ def test_errors_follow_reference():
         rb.pcg_solve(A, f, np.zeros_like(f), delta=0.0)
     with pytest.raises(ValueError):
         rb.HighFidelitySolver(prob, method="qr")
+
+
+@pytest.mark.parametrize("tag", ["tb221", "ex1"])
+def test_rbi_msrbcg_reference_signature_matches_golden(tag):
+    """The reference's third method through its own call sequence (make_golden.py --msrb /
+    --msrb-fem: msrb_train(train, N, K, hf, p.operator, p.rhs), then per test parameter
+    rbi_pcg_solve(A, f, cfg, msrb_hier=hier, mu=mu)) on the compat module: the FV thermal block
+    and the reference's own assembled problem example-1."""
+    rb = _rb()
+    if tag == "tb221":
+        g, k = dict(np.load(GOLDEN / "golden_msrb.npz")), "msrb_tb221_n16"
+        prob = _fd(rb, (2, 2, 1), 16)
+    else:
+        g, k = dict(np.load(GOLDEN / "golden_msrb_fem.npz")), "msrb_ex1_n16"
+        prob = rb.ParametricProblem(rb.get_problem("example-1"), levels=3, m0=4)
+    N, K = (int(v) for v in g[f"{k}_NK"])
+    hf = rb.HighFidelitySolver(prob, method="lu")
+    hier = rb.msrb_train(list(g[f"{k}_train"]), N, K, hf, prob.operator, prob.rhs)
+    cfg = rb.MethodConfig("rbi-msrbcg", delta=1e-10, l_max=60, N=N, K_max=K)
+    for m, mu in enumerate(g[f"{k}_test"]):
+        A, f = prob.operator(mu), prob.rhs(mu)
+        x, rep = rb.rbi_pcg_solve(A, f, cfg, msrb_hier=hier, mu=mu)
+        assert abs(rep.iterations - int(g[f"{k}_iters"][m])) <= 1
+        assert _rel(x, g[f"{k}_x"][m]) <= (1e-8 if tag == "ex1" else 1e-5)
+        assert rep.config["preconditioner"] == "msrb"
+        # (the thermal-block run stops at l_max in the reference as well: same count)
+        assert rep.converged == (int(g[f"{k}_iters"][m]) < 60)
