@@ -189,6 +189,10 @@ struct SL {
 #ifndef RBWS_N128_XF_S
 #define RBWS_N128_XF_S 4
 #endif
+// raw ring slots of the 512-thread post-smoothing kernel at N = 128 (one CTA per SM)
+#ifndef RBWS_N128_POSTP_S
+#define RBWS_N128_POSTP_S 4
+#endif
 // residual kernel (initial and true residual of every solve) at N <= 64: CTAs per SM
 #ifndef RBWS_RESID_CTAS
 #define RBWS_RESID_CTAS 2
@@ -199,7 +203,7 @@ struct SL {
 #endif
   static constexpr int S = XF ? (N >= 512 ? (RBWS_N512_NPT == 2 ? (MODE == FM_POSTP ? 2 : 3) : 4)
                                           : (N >= 256 ? (MODE == FM_POSTP ? 3 : RBWS_N256_XF_S)
-                                                      : (N >= 128 ? (MODE == FM_PREX ? 3 : RBWS_N128_XF_S)
+                                                      : (N >= 128 ? (MODE == FM_PREX ? 3 : (MODE == FM_POSTP ? RBWS_N128_POSTP_S : RBWS_N128_XF_S))
                                                                   : 6)))
                               : (N >= 128 ? ((SW && N == 128) ? RBWS_N128_SW_S : 6)
                                           : ((DIRECT || (RBWS_RESID_CTAS == 3 && MODE == FM_RESID))
