@@ -170,6 +170,10 @@ int rbws_set_kernel_variant(int which, int value) {
     if (rbws::fine_set_dc(value)) RBWS_FAIL("DC variant must be -1 (auto), 0 or 1");
     return 0;
   }
+  if (which == 4) {
+    if (rbws::fine_set_cgp(value)) RBWS_FAIL("fused CG update variant must be -1 (auto), 0 or 1");
+    return 0;
+  }
   if (which == 3) {
     if (rbws::fine_set_direct(value)) RBWS_FAIL("direct p-update variant must be -1 (auto), 0 or 1");
     return 0;

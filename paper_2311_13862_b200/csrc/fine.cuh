@@ -73,6 +73,16 @@ constexpr int kFineStoredWeightsMinChanges = 17;
 // x += alpha p, r -= alpha A p, partial = |r|^2
 cudaError_t fine_cg_update(const Sep7& op, int batch, const double* p, double* x, double* r,
                            const double* alpha, double* partial, const LaunchCtx& lc);
+// The CG update fused with the next V-cycle's pre-smoothing residual and the x/z passes of its
+// restriction (cgp.cu): x += alpha p, r -= alpha A p, partial = |r|^2 (the CG update kernel's
+// slots), t = x/z-restricted r - A (omega D^-1 r) (the layout of fine_pre_xz).
+bool fine_cgp_ok(const Sep7& op, int batch, const LaunchCtx& lc);
+int fine_set_cgp(int v);    // 1 on where it applies, -1 / 0 off
+int fine_cgp_variant();
+// r_out != r_in: the tiles read each other's old rows as halos while they update
+cudaError_t fine_cg_update_pre(const Sep7& op, int batch, const double* p, double* x,
+                               const double* r_in, double* r_out, const double* alpha,
+                               double* partial, double* t, double omega, const LaunchCtx& lc);
 // p_new = s + beta p_old (beta null: p_new = s), partial = p_new . A p_new
 cudaError_t fine_papply(const Sep7& op, int batch, const double* s, const double* p_old,
                         const double* beta, double* p_new, double* partial, const LaunchCtx& lc);

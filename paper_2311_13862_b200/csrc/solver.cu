@@ -330,7 +330,7 @@ Batch::~Batch() {
     cudaFree(l.zero); cudaFree(l.dinv); cudaFree(l.u); cudaFree(l.coef);
   }
   cudaFree(L0); cudaFree(d_status);
-  cudaFree(r); cudaFree(p); cudaFree(p2); cudaFree(s); cudaFree(t_res);
+  cudaFree(r); cudaFree(r2); cudaFree(p); cudaFree(p2); cudaFree(s); cudaFree(t_res);
   cudaFree(rs); cudaFree(alpha); cudaFree(beta); cudaFree(scale);
   cudaFree(active); cudaFree(iters); cudaFree(pstatus); cudaFree(nactive);
   cudaFreeHost(h_nactive);
@@ -574,7 +574,9 @@ int solver_set_tail(int v) {
   g_tail.store(v == 1 ? 1 : 0);
   return 0;
 }
-static int variant_key() { return fine_variant() + 1024 * g_tail.load(); }
+static int variant_key() {
+  return fine_variant() + 1024 * g_tail.load() + 2048 * fine_cgp_variant();
+}
 
 // the fused coarse tail (tail.cu) serves level lvl and everything below it?
 bool Batch::tail_level(int lvl, const LaunchCtx& lc) const {
@@ -675,7 +677,7 @@ int Batch::vcycle(int lvl, const double* bb, double* out, double* dot_partial,
       sw_used = fine_pre_scaled(fine_op());
     }
     if (stop) e = vec_scale_dinv(n, count, omega, l.dinv, bb, l.u, lc.stream);
-    if (e == cudaSuccess)
+    if (e == cudaSuccess && !(fine && fused && pre_done))  // (pre_done: l.t1 holds t already)
       e = fused ? fine_pre_xz(fine_op(), count, bb, l.dinv, l.t1, omega, lc)
                 : op(MODE_PRE, DOT_NONE, nullptr, bb, l.t1, nullptr);
     if (pf) { prof_end(PROF_FINE_PRE, t0, lc.stream); t0 = prof_begin(lc.stream); }
@@ -936,6 +938,13 @@ static int stream_download(Batch* b, const double* x, const PcgOut& out, int cal
   return dl_flush(b, x, out);
 }
 
+// the CG update may carry the next V-cycle's pre-smoothing residual + x/z restriction (cgp.cu)
+static bool cgp_ok(Batch* b, const Sep7& op, const LaunchCtx& lc) {
+  const int L = b->h->levels;
+  return b->nu == 1 && b->smoother == 0 && b->fuse_restrict && L - 2 >= 1 &&
+         fine_cgp_ok(op, b->count, lc) && fine_pre_xz_ok(op, b->count, lc);
+}
+
 // device-side loop condition: keep iterating while any instance is active
 __global__ void pcg_cond_kernel(cudaGraphConditionalHandle h, const int* nactive) {
   cudaGraphSetConditional(h, *nactive > 0 ? 1u : 0u);
@@ -970,6 +979,7 @@ static int pcg_graph_run(Batch* b, const Sep7& op, double* x, int tiles, int vti
                    b->gkey_delta == delta && b->gkey_lmax == l_max && b->gkey_hl == hl &&
                    b->gkey_active == act.active && b->gkey_smoother == b->smoother &&
                    b->gkey_fused == (int)b->fuse_restrict && b->gkey_wface == b->wface &&
+                   b->gkey_rcur == b->rcur &&
                    b->gkey_variant == variant_key();
   cudaError_t e = cudaSuccess;
   if (!hit) {
@@ -1002,14 +1012,24 @@ static int pcg_graph_run(Batch* b, const Sep7& op, double* x, int tiles, int vti
       count_launch();
       pcg_alpha_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, tiles, b->rs,
                                                              b->alpha, b->active, b->pstatus);
-      e = fine_cg_update(op, count, p_new, x, b->r, b->alpha, b->partial, act);
+      const bool cgp = cgp_ok(b, op, act);
+      if (cgp) {  // (out of place: two halves bring the residual back to the buffer it started in)
+        double* r_out = (b->rcur == b->r) ? b->r2 : b->r;
+        e = fine_cg_update_pre(op, count, p_new, x, b->rcur, r_out, b->alpha, b->partial,
+                               b->lv[L - 1].t1, b->omega, act);
+        b->rcur = r_out;
+      } else {
+        e = fine_cg_update(op, count, p_new, x, b->rcur, b->alpha, b->partial, act);
+      }
       if (e == cudaSuccess) e = cudaMemsetAsync(b->nactive, 0, sizeof(int), stream);
       if (e != cudaSuccess) break;
       count_launch();
       pcg_check_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, tiles, b->scale,
                                                              delta, l_max, b->hist, hl, b->active,
                                                              b->iters, b->nactive);
-      rc = b->vcycle(L - 1, b->r, b->s, b->partial, act);
+      b->pre_done = cgp;
+      rc = b->vcycle(L - 1, b->rcur, b->s, b->partial, act);
+      b->pre_done = false;
       if (rc) break;
       count_launch();
       pcg_beta_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, vtiles, b->rs,
@@ -1031,6 +1051,7 @@ static int pcg_graph_run(Batch* b, const Sep7& op, double* x, int tiles, int vti
     b->gkey_x = x; b->gkey_count = count; b->gkey_delta = delta; b->gkey_lmax = l_max;
     b->gkey_hl = hl; b->gkey_active = act.active; b->gkey_smoother = b->smoother;
     b->gkey_fused = (int)b->fuse_restrict; b->gkey_wface = b->wface;
+    b->gkey_rcur = b->rcur;
     b->gkey_variant = variant_key();
   }
   e = cudaGraphLaunch(b->gexec, stream);
@@ -1203,6 +1224,12 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
   // ||f||
   e = vec_dot(n, fshared ? 1 : count, f, f_stride, f, f_stride, b->partial2, all);
   // r = f - A x0, ||r||^2  (a shared rhs is staged once per plane for every instance)
+  b->rcur = b->r;
+  if (cgp_ok(b, op, act) && !b->r2) {  // second residual buffer of the fused CG update
+    e = dalloc(&b->r2, (size_t)vec_doubles(n, b->cap));
+    if (e == cudaSuccess) e = cudaMemsetAsync(b->r2, 0, sizeof(double) * vec_doubles(n, b->cap), stream);
+    if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
+  }
   if (e == cudaSuccess) e = fine_resid(op, count, x, f, b->r, b->partial, all, fshared);
   if (e == cudaSuccess) e = cudaMemsetAsync(b->nactive, 0, sizeof(int), stream);
   if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
@@ -1242,7 +1269,15 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
       pcg_alpha_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, tiles, b->rs,
                                                              b->alpha, b->active, b->pstatus);
       if (pf) { b->prof_end(PROF_SCALARS, t0, stream); t0 = b->prof_begin(stream); }
-      e = fine_cg_update(op, count, p_new, x, b->r, b->alpha, b->partial, act);
+      const bool cgp = cgp_ok(b, op, act);
+      if (cgp) {
+        double* r_out = (b->rcur == b->r) ? b->r2 : b->r;
+        e = fine_cg_update_pre(op, count, p_new, x, b->rcur, r_out, b->alpha, b->partial,
+                               b->lv[L - 1].t1, b->omega, act);
+        b->rcur = r_out;
+      } else {
+        e = fine_cg_update(op, count, p_new, x, b->rcur, b->alpha, b->partial, act);
+      }
       if (pf) { b->prof_end(PROF_FINE_CG_UPDATE, t0, stream); t0 = b->prof_begin(stream); }
       if (e == cudaSuccess) e = cudaMemsetAsync(b->nactive, 0, sizeof(int), stream);
       if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));
@@ -1261,7 +1296,10 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
           dl_mark(b, out, dl_call++, false, stream))
         return 1;
       b->cur_active = *b->h_nactive;
-      if (b->vcycle(L - 1, b->r, b->s, b->partial, act)) return 1;
+      b->pre_done = cgp;
+      const int vrc = b->vcycle(L - 1, b->rcur, b->s, b->partial, act);
+      b->pre_done = false;
+      if (vrc) return 1;
       if (pf) t0 = b->prof_begin(stream);
       count_launch();
       pcg_beta_kernel<<<warp_grid(count), 256, 0, stream>>>(count, b->partial, vtiles, b->rs,

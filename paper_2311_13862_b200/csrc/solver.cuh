@@ -89,6 +89,8 @@ struct Batch {
   bool fuse_restrict = true;        // finest pre-smoothing + x/z restriction in one kernel
   bool fused_used = false;          // the last V-cycle took the fused path
   bool sw_used = false;             // ... with the scaled-weights pre-smoothing kernels
+  bool pre_done = false;            // the finest pre-smoothing residual + x/z restriction of the
+                                    // next V-cycle already ran inside the CG update (cgp.cu)
   double omega = 0.7;
   double* theta = nullptr;          // [cap][Q]
   double* wface = nullptr;          // stored fine face weights [3][cap n^3 + 2n^2] (SCW kernels)
@@ -98,6 +100,8 @@ struct Batch {
   int* d_status = nullptr;          // coarse factor status per instance
   // PCG state (fine level)
   double *r = nullptr, *p = nullptr, *p2 = nullptr, *s = nullptr, *t_res = nullptr;
+  double* r2 = nullptr;             // second residual buffer (fused CG update, allocated on use)
+  double* rcur = nullptr;           // the current residual of the running solve (r or r2)
   double *rs = nullptr, *alpha = nullptr, *beta = nullptr, *scale = nullptr;
   int *active = nullptr, *iters = nullptr, *pstatus = nullptr, *nactive = nullptr;
   int* h_nactive = nullptr;         // pinned
@@ -113,6 +117,7 @@ struct Batch {
   int gkey_count = 0, gkey_lmax = 0, gkey_hl = 0, gkey_smoother = -1, gkey_fused = -1,
       gkey_variant = -2;
   const double* gkey_wface = nullptr;
+  const double* gkey_rcur = nullptr;
   double gkey_delta = 0.0;
   void drop_graph();                // invalidate the cached executable (smoother/graph changes)
   int64_t gbody_launches = 0;

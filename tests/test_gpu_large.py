@@ -253,6 +253,35 @@ def test_sw_variant_matches_transformed(n, case):
     _compare_runs(var, base, 1e-13)
 
 
+@pytest.mark.parametrize("case,count", [((2, 2, 1), 40), ((2, 2, 2), 37)])
+def test_fused_cg_update_pre_smoothing_matches_separate(case, count):
+    """The CG update that also computes the next V-cycle's pre-smoothing residual and the x/z
+    passes of its restriction (cgp.cu, rbws_set_kernel_variant(4, 1); 64^3, whole instances per
+    CTA) against the separate kernels: solutions, iteration counts, histories."""
+    pkg = _pkg()
+    from paper_2311_13862_b200 import _native
+    n = 64
+    spec, ospec = _specs(case)
+    prob = pkg.ParametricProblem(spec, levels=pkg.problems.levels_for(n, 4), m0=4)
+    mus = op.sample_mus(ospec, count, seed=60)
+    delta = 1e-10
+    try:
+        _native.call("rbws_set_kernel_variant", 4, 0)
+        base = _vcycle_and_solve(prob, mus, delta, n)
+        _native.call("rbws_set_kernel_variant", 4, 1)
+        var = _vcycle_and_solve(prob, mus, delta, n)
+    finally:
+        _native.call("rbws_set_kernel_variant", 4, -1)
+    # (rounding-level differences: an instance whose residual sits at the tolerance may take
+    # one more / fewer iteration)
+    assert (torch.linalg.norm(var[0] - base[0]) / torch.linalg.norm(base[0])).item() <= 1e-12
+    assert (torch.linalg.norm(var[1] - base[1]) / torch.linalg.norm(base[1])).item() <= 1e-9
+    assert max(abs(a - b) for a, b in zip(var[2], base[2])) <= 1
+    for h0, h1 in zip(var[3], base[3]):
+        np.testing.assert_allclose(h0[:8], h1[:8], rtol=1e-8)
+    print("fused CG update: max |dx| =", float((var[1] - base[1]).abs().max()))
+
+
 @pytest.mark.parametrize("n,case", [(16, (2, 1, 1)), (64, (2, 2, 1)), (64, "smooth"),
                                     (128, (2, 2, 2))])
 def test_direct_p_update_matches_transformed(n, case):
