@@ -47,7 +47,8 @@ struct CgpGeom {
   static constexpr int TY = 2 * RPP;           // rows per tile
   static constexpr int PSZ = (TY + 4) * N;     // p: rows j0-2 .. j0+TY+1
   static constexpr int RSZ = (TY + 2) * N;     // r: rows j0-1 .. j0+TY
-  static constexpr int STAGE = PSZ + RSZ;
+  static constexpr int XSZ = TY * N;           // x: tile rows
+  static constexpr int STAGE = PSZ + RSZ + XSZ;
   static constexpr int USZ = (TY + 2) * N;     // u ring plane (rows j0-1 .. j0+TY)
   static constexpr int CSZ = TY * N;
   static size_t bytes(int Q) {
@@ -61,6 +62,7 @@ __global__ void __launch_bounds__(kCgpThreads, 1) cgp_kernel(CgpArgs a) {
   using G = CgpGeom<N>;
   constexpr int RPP = G::RPP, TY = G::TY, S = kCgpS;
   constexpr int PSZ = G::PSZ, RSZ = G::RSZ, STAGE = G::STAGE, USZ = G::USZ, CSZ = G::CSZ;
+  constexpr int XSZ = G::XSZ;
   constexpr int64_t N2 = (int64_t)N * N;
   extern __shared__ __align__(128) unsigned char smem[];
   const Sep7& op = a.op;
@@ -107,10 +109,12 @@ __global__ void __launch_bounds__(kCgpThreads, 1) cgp_kernel(CgpArgs a) {
   auto issue = [&](int p) {
     double* st = ring + (p % S) * STAGE;
     const uint32_t pb = (uint32_t)((TY + 4 - skp) * N * 8), rb = (uint32_t)((TY + 2 - skr) * N * 8);
-    mbar_arrive_expect_tx(&bar[p % S], pb + rb);
+    constexpr uint32_t xb = (uint32_t)(XSZ * 8);
+    mbar_arrive_expect_tx(&bar[p % S], pb + rb + xb);
     const int64_t plane = base + (int64_t)p * N2;
     bulk_g2s(st + skp * N, a.p + plane + (int64_t)(j0 - 2 + skp) * N, pb, &bar[p % S]);
     bulk_g2s(st + PSZ + skr * N, a.rin + plane + (int64_t)(j0 - 1 + skr) * N, rb, &bar[p % S]);
+    bulk_g2s(st + PSZ + RSZ, a.x + plane + (int64_t)j0 * N, xb, &bar[p % S]);
   };
   auto wait = [&](int p) { mbar_wait(&bar[p % S], (uint32_t)((p / S) & 1)); };
   if (tid == 0)
@@ -227,8 +231,8 @@ __global__ void __launch_bounds__(kCgpThreads, 1) cgp_kernel(CgpArgs a) {
   }
   __syncthreads();  // plane 0's slot is free: the ring then holds planes k .. k+3 in iteration k
   if (tid == 0 && S <= N) issue(S);
-  // running pointers of the own rows' x / r entries on the current plane; x of plane k is
-  // loaded one iteration ahead (a dependent global load would stall every plane)
+  // running pointers of the own rows' x / r entries on the current plane (x is staged with the
+  // plane: a dependent global load would stall every plane)
   double* xp[2];
   double* rq[2];
 #pragma unroll
@@ -237,9 +241,9 @@ __global__ void __launch_bounds__(kCgpThreads, 1) cgp_kernel(CgpArgs a) {
     xp[s] = a.x + g;
     rq[s] = a.rout + g;
   }
-  double xv[2], xn[2];
+  int xo[2];  // own rows inside the staged x rows
 #pragma unroll
-  for (int s = 0; s < 2; ++s) xv[s] = on[s] ? *xp[s] : 0.0;
+  for (int s = 0; s < 2; ++s) xo[s] = PSZ + RSZ + row[s] * N + i;
 
   for (int k = 1; k < N; ++k) {
     // (1) pre-smoothing residual of plane k-1 without its upper z face (weights of plane k-1)
@@ -259,8 +263,6 @@ __global__ void __launch_bounds__(kCgpThreads, 1) cgp_kernel(CgpArgs a) {
     wait(k + 1);
     const double* SK = ring + (k & (S - 1)) * STAGE;
     const double* SU = ring + ((k + 1) & (S - 1)) * STAGE;
-#pragma unroll
-    for (int s = 0; s < 2; ++s) xn[s] = (on[s] && k + 1 < N) ? xp[s][N2] : 0.0;  // x(k+1)
     double un[NS], rn[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
@@ -285,13 +287,12 @@ __global__ void __launch_bounds__(kCgpThreads, 1) cgp_kernel(CgpArgs a) {
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       if (on[s]) {
-        *xp[s] = fma(al, pc[s], xv[s]);
+        *xp[s] = fma(al, pc[s], SK[xo[s]]);
         *rq[s] = rn[s];
         acc = fma(rn[s], rn[s], acc);
       }
       xp[s] += N2;
       rq[s] += N2;
-      xv[s] = xn[s];
     }
     // (4) finish r1(k-1): upper z face = plane k's lower face
     if (k >= 2) {
