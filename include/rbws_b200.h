@@ -115,7 +115,10 @@ int rbws_batch_set_graph(rbws_batch* b, int enable);
  * which 3 = p-update kernel that forms the neighbours' p = s + beta p_old where they are read
  * (no transformed ring, three CTAs per SM; bitwise the transformed-ring kernel): 1 on
  * (N <= 128, weights not stored), -1 / 0 the transformed-ring kernel (default: measured
- * slower). */
+ * slower).
+ * which 4 = CG update fused with the next V-cycle's pre-smoothing residual and the x/z passes
+ * of its restriction (cgp.cu; 64^3 grids, whole instances per CTA, Jacobi nu = 1): -1 / 1 on
+ * where it applies, 0 the separate kernels. */
 int rbws_set_kernel_variant(int which, int value);
 /* Smoother of the V-cycle: 0 damped Jacobi (the reference default for isotropic problems,
  * multigrid.py:183-188), 1 Gauss-Seidel (smoother="gs": nu forward lexicographic sweeps

@@ -23,8 +23,14 @@ namespace rbws {
 
 namespace {
 
-constexpr int kCgpThreads = 512;
-constexpr int kCgpS = 4;  // ring slots (planes of p and r in flight)
+#ifndef RBWS_CGP_THREADS
+#define RBWS_CGP_THREADS 512
+#endif
+constexpr int kCgpThreads = RBWS_CGP_THREADS;
+#ifndef RBWS_CGP_S
+#define RBWS_CGP_S 4
+#endif
+constexpr int kCgpS = RBWS_CGP_S;  // ring slots (planes of p, r and x in flight)
 
 struct CgpArgs {
   Sep7 op;
@@ -58,7 +64,7 @@ struct CgpGeom {
 };
 
 template <int N>
-__global__ void __launch_bounds__(kCgpThreads, 1) cgp_kernel(CgpArgs a) {
+__global__ void __launch_bounds__(kCgpThreads, kCgpThreads <= 256 ? 2 : 1) cgp_kernel(CgpArgs a) {
   using G = CgpGeom<N>;
   constexpr int RPP = G::RPP, TY = G::TY, S = kCgpS;
   constexpr int PSZ = G::PSZ, RSZ = G::RSZ, STAGE = G::STAGE, USZ = G::USZ, CSZ = G::CSZ;
@@ -261,8 +267,8 @@ __global__ void __launch_bounds__(kCgpThreads, 1) cgp_kernel(CgpArgs a) {
     refresh(k);
     // (3) CG update on plane k (own rows + halo row), u(k) = w D^-1 r_new
     wait(k + 1);
-    const double* SK = ring + (k & (S - 1)) * STAGE;
-    const double* SU = ring + ((k + 1) & (S - 1)) * STAGE;
+    const double* SK = ring + (k % S) * STAGE;
+    const double* SU = ring + ((k + 1) % S) * STAGE;
     double un[NS], rn[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
@@ -342,14 +348,15 @@ __global__ void __launch_bounds__(kCgpThreads, 1) cgp_kernel(CgpArgs a) {
 
 }  // namespace
 
-// rbws_set_kernel_variant(4, .) / RBWS_CGP: 1 on where it applies, 0 the separate kernels
+// rbws_set_kernel_variant(4, .) / RBWS_CGP: on where it applies (default), 0 = the separate
+// CG update and pre-smoothing kernels
 static std::atomic<int> g_cgp{[] {
   const char* e = getenv("RBWS_CGP");
-  return (e && atoi(e) == 1) ? 1 : 0;
+  return (e && atoi(e) == 0) ? 0 : 1;
 }()};
 int fine_set_cgp(int v) {
   if (v < -1 || v > 1) return 1;
-  g_cgp.store(v == 1 ? 1 : 0);
+  g_cgp.store(v == 0 ? 0 : 1);
   return 0;
 }
 int fine_cgp_variant() { return g_cgp.load(); }

@@ -256,8 +256,9 @@ def test_sw_variant_matches_transformed(n, case):
 @pytest.mark.parametrize("case,count", [((2, 2, 1), 40), ((2, 2, 2), 37)])
 def test_fused_cg_update_pre_smoothing_matches_separate(case, count):
     """The CG update that also computes the next V-cycle's pre-smoothing residual and the x/z
-    passes of its restriction (cgp.cu, rbws_set_kernel_variant(4, 1); 64^3, whole instances per
-    CTA) against the separate kernels: solutions, iteration counts, histories."""
+    passes of its restriction (cgp.cu, the default at 64^3 with whole instances per CTA) against
+    the separate kernels (rbws_set_kernel_variant(4, 0)): solutions, iteration counts,
+    histories."""
     pkg = _pkg()
     from paper_2311_13862_b200 import _native
     n = 64
@@ -268,7 +269,7 @@ def test_fused_cg_update_pre_smoothing_matches_separate(case, count):
     try:
         _native.call("rbws_set_kernel_variant", 4, 0)
         base = _vcycle_and_solve(prob, mus, delta, n)
-        _native.call("rbws_set_kernel_variant", 4, 1)
+        _native.call("rbws_set_kernel_variant", 4, -1)
         var = _vcycle_and_solve(prob, mus, delta, n)
     finally:
         _native.call("rbws_set_kernel_variant", 4, -1)
