@@ -59,7 +59,7 @@ struct CgpGeom {
   static constexpr int CSZ = TY * N;
   static size_t bytes(int Q) {
     return 64 + 8 * (size_t)(((N + 1) * 3 * Q + 1) & ~1) +
-           8 * ((size_t)kCgpS * STAGE + 2 * USZ + 2 * CSZ + 2) + 16;
+           8 * ((size_t)kCgpS * STAGE + 2 * USZ + 2 * CSZ + 2) + 16 + 4 * (size_t)(N + 4);
   }
 };
 
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kCgpThreads, kCgpThreads <= 256 ? 2 : 1) cgp_k
   double* uring = ring + S * STAGE;                     // [2][USZ]
   double* rbuf = uring + 2 * USZ;                       // [2][CSZ]
   uint32_t* zbits = reinterpret_cast<uint32_t*>(rbuf + 2 * CSZ + 2);  // [2] plane k repeats k-1
-  static_assert(N <= 64, "the z-repeat mask holds 64 planes");
+  int* zs = reinterpret_cast<int*>(zbits + 4);                          // [N + 1] (N > 64)
 
   for (int t = tid; t < (N + 1) * ZW; t += kCgpThreads) {  // z factors of planes 0 .. N
     const int k = t / (3 * Q), f = (t / Q) % 3, q = t % Q;
@@ -108,6 +108,12 @@ __global__ void __launch_bounds__(kCgpThreads, kCgpThreads <= 256 ? 2 : 1) cgp_k
     const uint32_t bits = __ballot_sync(0xffffffffu, sm);
     if ((tid & 31) == 0) zbits[tid >> 5] = bits;
   }
+  if (N > 64)
+    for (int k = tid; k <= N; k += kCgpThreads) {
+      bool sm = k >= 2 && k < N;
+      for (int t = 0; t < ZW && sm; ++t) sm = (zf[k * ZW + t] == zf[(k - 1) * ZW + t]);
+      zs[k] = sm ? 1 : 0;
+    }
   __syncthreads();
   const uint64_t zmask = ((uint64_t)zbits[1] << 32) | zbits[0];
   // staged rows below 0 do not exist for the first tile
@@ -175,7 +181,9 @@ __global__ void __launch_bounds__(kCgpThreads, kCgpThreads <= 256 ? 2 : 1) cgp_k
     wzm[s] = wzp[s];
   }
   bool pend = false;
-  auto same = [&](int k) -> bool { return ((zmask >> k) & 1) != 0; };  // CTA-uniform
+  auto same = [&](int k) -> bool {  // CTA-uniform
+    return N <= 64 ? ((zmask >> k) & 1) != 0 : zs[k] != 0;
+  };
   auto refresh = [&](int k) {  // fine_kernel::refresh
     if (k == 1 || !same(k)) {
 #pragma unroll
@@ -361,14 +369,31 @@ int fine_set_cgp(int v) {
 }
 int fine_cgp_variant() { return g_cgp.load(); }
 
+template <int N>
+static bool cgp_fits(const Sep7& op, int batch) {
+  const FineGeom g = fine_geom(op.n, batch);  // the CG update kernel's partial slots
+  if (g.tiles % (N / CgpGeom<N>::TY)) return false;
+  // whole z-range per CTA: enough CTAs to fill the GPU
+  if ((int64_t)batch * (N / CgpGeom<N>::TY) < 148) return false;
+  return CgpGeom<N>::bytes(op.Q) <= 227 * 1024;
+}
+
 bool fine_cgp_ok(const Sep7& op, int batch, const LaunchCtx& lc) {
   if (!g_cgp.load(std::memory_order_relaxed) || op.wface || lc.zhi > 0) return false;
-  if (op.n != 64) return false;
-  const FineGeom g = fine_geom(op.n, batch);  // the CG update kernel's partial slots
-  if (g.zc != 1 || g.tiles % (op.n / CgpGeom<64>::TY)) return false;
-  // whole z-range per CTA: enough CTAs to fill the GPU
-  if ((int64_t)batch * (op.n / CgpGeom<64>::TY) < 148) return false;
-  return CgpGeom<64>::bytes(op.Q) <= 227 * 1024;
+  if (op.n == 64) return cgp_fits<64>(op, batch);
+  if (op.n == 128) return cgp_fits<128>(op, batch);
+  return false;
+}
+
+template <int N>
+static cudaError_t cgp_launch(const CgpArgs& a, int batch, cudaStream_t stream) {
+  const size_t smem = CgpGeom<N>::bytes(a.op.Q);
+  cudaError_t e = smem_attr((const void*)cgp_kernel<N>, smem);
+  if (e != cudaSuccess) return e;
+  dim3 grd(1, N / CgpGeom<N>::TY, batch);
+  count_launch();
+  cgp_kernel<N><<<grd, kCgpThreads, smem, stream>>>(a);
+  return cudaGetLastError();
 }
 
 cudaError_t fine_cg_update_pre(const Sep7& op, int batch, const double* p, double* x,
@@ -388,13 +413,7 @@ cudaError_t fine_cg_update_pre(const Sep7& op, int batch, const double* p, doubl
   a.tiles = fine_geom(op.n, batch).tiles;
   a.active = lc.active;
   a.omega = omega;
-  const size_t smem = CgpGeom<64>::bytes(op.Q);
-  cudaError_t e = smem_attr((const void*)cgp_kernel<64>, smem);
-  if (e != cudaSuccess) return e;
-  dim3 grd(1, 64 / CgpGeom<64>::TY, batch);
-  count_launch();
-  cgp_kernel<64><<<grd, kCgpThreads, smem, lc.stream>>>(a);
-  return cudaGetLastError();
+  return op.n == 64 ? cgp_launch<64>(a, batch, lc.stream) : cgp_launch<128>(a, batch, lc.stream);
 }
 
 }  // namespace rbws

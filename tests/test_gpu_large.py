@@ -253,15 +253,15 @@ def test_sw_variant_matches_transformed(n, case):
     _compare_runs(var, base, 1e-13)
 
 
-@pytest.mark.parametrize("case,count", [((2, 2, 1), 40), ((2, 2, 2), 37)])
-def test_fused_cg_update_pre_smoothing_matches_separate(case, count):
+@pytest.mark.parametrize("n,case,count", [(64, (2, 2, 1), 40), (64, (2, 2, 2), 37),
+                                          (128, (2, 2, 2), 10)])
+def test_fused_cg_update_pre_smoothing_matches_separate(n, case, count):
     """The CG update that also computes the next V-cycle's pre-smoothing residual and the x/z
     passes of its restriction (cgp.cu, the default at 64^3 with whole instances per CTA) against
     the separate kernels (rbws_set_kernel_variant(4, 0)): solutions, iteration counts,
     histories."""
     pkg = _pkg()
     from paper_2311_13862_b200 import _native
-    n = 64
     spec, ospec = _specs(case)
     prob = pkg.ParametricProblem(spec, levels=pkg.problems.levels_for(n, 4), m0=4)
     mus = op.sample_mus(ospec, count, seed=60)
