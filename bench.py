@@ -294,6 +294,7 @@ def run_b200(args, rank, world, dist):
     scw = bool(_native.load().rbws_batch_stored_weights(ctx.handle))
     fused = bool(_native.load().rbws_batch_fused_restrict(ctx.handle))
     pre_sw = bool(_native.load().rbws_batch_pre_scaled(ctx.handle))
+    cg_fused = bool(_native.load().rbws_batch_cg_fused(ctx.handle))
     del ctx, xbuf
     torch.cuda.empty_cache()
     e2e_sub = min(batch, args.e2e_sub or cfg.get("e2e_sub", 512))
@@ -336,6 +337,11 @@ def run_b200(args, rank, world, dist):
     op_bytes = dict(class_bytes)
     if pre_sw:
         class_bytes[2] -= 8.0
+    # CG update fused with the next V-cycle's pre-smoothing residual + x/z restriction
+    # (p, x, r -> x, r, t 1/4): the pre-smoothing class then only holds each solve's first V-cycle
+    if cg_fused:
+        class_bytes[1] = 42.0 + (24.0 if scw else 0.0)
+        op_bytes[1] = 42.0 + (24.0 if scw else 0.0)
     table = {}
     for k in range(NC):
         if pcalls[k] == 0:
@@ -372,7 +378,8 @@ def run_b200(args, rank, world, dist):
                     "traffic": traffic, "traffic_source": tsrc, "peak_source": peak_kind,
                     "bytes_per_launch": int(dom_bytes),
                     "bytes_per_node": class_bytes[dom], "stored_weights": scw,
-                    "fused_pre_restrict": fused, "scaled_weights_pre": pre_sw}
+                    "fused_pre_restrict": fused, "scaled_weights_pre": pre_sw,
+                    "cg_update_fused_with_pre_smoothing": cg_fused}
     else:  # the warm start already met the tolerance: no PCG iteration ran
         roofline = {"bound": "hbm", "kernel": None, "achieved": None, "peak": peak,
                     "unit": "GB/s", "frac": None, "traffic": None, "peak_source": peak_kind}

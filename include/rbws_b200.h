@@ -140,6 +140,10 @@ int rbws_batch_fused_restrict(const rbws_batch* b);
  * (face weights pre-multiplied by the neighbours' omega/diag in registers, stencil taken on
  * the raw b: the 1/diag vector is not streamed; piecewise-constant coefficients), else 0 */
 int rbws_batch_pre_scaled(const rbws_batch* b);
+/* 1 if the last solve's CG update (x += alpha p, r -= alpha A p, krylov.py:89-92) also computed
+ * the next V-cycle's pre-smoothing residual and the x/z passes of its restriction in the same
+ * pass (r never re-read: 42 instead of 40 + 10 B per node; the measurement's byte counts) */
+int rbws_batch_cg_fused(const rbws_batch* b);
 
 /* y = A^level(mu) x for every instance (ParametricProblem.operator(mu, level) @ x,
  * grid.py:246-255).  x, y: (dev) padded vectors of that level. */

@@ -44,6 +44,7 @@ SIGNATURES = {
     "rbws_batch_stored_weights": [_vp],
     "rbws_batch_fused_restrict": [_vp],
     "rbws_batch_pre_scaled": [_vp],
+    "rbws_batch_cg_fused": [_vp],
     "rbws_apply": [_vp, _c_int, _vp, _vp, _vp],
     "rbws_jacobi_sweep": [_vp, _c_int, _vp, _vp, _vp, _vp],
     "rbws_restrict": [_c_int, _c_int, _vp, _vp, _vp],

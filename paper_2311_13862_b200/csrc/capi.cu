@@ -158,6 +158,10 @@ int rbws_batch_pre_scaled(const rbws_batch* b) {
   return reinterpret_cast<const Batch*>(b)->sw_used ? 1 : 0;
 }
 
+int rbws_batch_cg_fused(const rbws_batch* b) {
+  return reinterpret_cast<const Batch*>(b)->cgp_used ? 1 : 0;
+}
+
 int rbws_batch_set_graph(rbws_batch* b, int enable) {
   if (!b) RBWS_FAIL("null batch");
   if (!enable) B(b)->drop_graph();

@@ -680,7 +680,11 @@ int Batch::vcycle(int lvl, const double* bb, double* out, double* dot_partial,
     if (e == cudaSuccess && !(fine && fused && pre_done))  // (pre_done: l.t1 holds t already)
       e = fused ? fine_pre_xz(fine_op(), count, bb, l.dinv, l.t1, omega, lc)
                 : op(MODE_PRE, DOT_NONE, nullptr, bb, l.t1, nullptr);
-    if (pf) { prof_end(PROF_FINE_PRE, t0, lc.stream); t0 = prof_begin(lc.stream); }
+    // (pre_done: nothing was launched for the pre-smoothing class)
+    if (pf && !(fine && fused && pre_done)) {
+      prof_end(PROF_FINE_PRE, t0, lc.stream);
+      t0 = prof_begin(lc.stream);
+    }
     // the restriction also writes the next level's pre-scaled rhs u = w D^-1 b
     if (e == cudaSuccess)
       e = fused ? restrict_y_launch(n, count, l.t1, c.b, lc, c.dinv, c.u, omega)
@@ -1225,7 +1229,8 @@ int pcg_solve(Batch* b, const double* f, int64_t f_stride, double* x, double del
   e = vec_dot(n, fshared ? 1 : count, f, f_stride, f, f_stride, b->partial2, all);
   // r = f - A x0, ||r||^2  (a shared rhs is staged once per plane for every instance)
   b->rcur = b->r;
-  if (cgp_ok(b, op, act) && !b->r2) {  // second residual buffer of the fused CG update
+  b->cgp_used = cgp_ok(b, op, act);
+  if (b->cgp_used && !b->r2) {  // second residual buffer of the fused CG update
     e = dalloc(&b->r2, (size_t)vec_doubles(n, b->cap));
     if (e == cudaSuccess) e = cudaMemsetAsync(b->r2, 0, sizeof(double) * vec_doubles(n, b->cap), stream);
     if (e != cudaSuccess) RBWS_FAIL(cudaGetErrorString(e));

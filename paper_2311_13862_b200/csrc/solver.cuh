@@ -89,6 +89,7 @@ struct Batch {
   bool fuse_restrict = true;        // finest pre-smoothing + x/z restriction in one kernel
   bool fused_used = false;          // the last V-cycle took the fused path
   bool sw_used = false;             // ... with the scaled-weights pre-smoothing kernels
+  bool cgp_used = false;            // the last solve ran the fused CG update (cgp.cu)
   bool pre_done = false;            // the finest pre-smoothing residual + x/z restriction of the
                                     // next V-cycle already ran inside the CG update (cgp.cu)
   double omega = 0.7;
