@@ -47,7 +47,8 @@ print(open(sys.argv[2]).read())
 if len(sys.argv) > 3:
     # full-batch launches (the longest of each fine kernel) against their algorithmic bytes
     nodes, inst = 63 ** 3, 1024
-    classes = {"fine_cg_update": ("fine_kernel<4, 64", 40.0), "fine_p_update_apply_dot": ("fine_kernel<5, 64", 24.0),
+    classes = {"fine_cg_update": ("cgp_kernel<64>", 42.0), "fine_cg_update_separate": ("fine_kernel<4, 64", 40.0),
+               "fine_p_update_apply_dot": ("fine_kernel<5, 64", 24.0),
                "fine_prolong_post_smooth": ("fine_kernel<6, 64", 25.0),
                "fine_pre_residual": ("fine_kernel<7, 64", 10.0), "fine_resid": ("fine_kernel<1, 64", 16.0)}
     out = {"source": f"{sys.argv[1]}: ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
