@@ -31,6 +31,10 @@ constexpr int kCgpThreads = RBWS_CGP_THREADS;
 #define RBWS_CGP_S 4
 #endif
 constexpr int kCgpS = RBWS_CGP_S;  // ring slots (planes of p, r and x in flight)
+#ifndef RBWS_CGP_UNROLL
+#define RBWS_CGP_UNROLL 1
+#endif
+constexpr int kCgpUnroll = RBWS_CGP_UNROLL;  // planes per unrolled trip of the main loop
 
 struct CgpArgs {
   Sep7 op;
@@ -259,6 +263,7 @@ __global__ void __launch_bounds__(kCgpThreads, kCgpThreads <= 256 ? 2 : 1) cgp_k
 #pragma unroll
   for (int s = 0; s < 2; ++s) xo[s] = PSZ + RSZ + row[s] * N + i;
 
+#pragma unroll kCgpUnroll
   for (int k = 1; k < N; ++k) {
     // (1) pre-smoothing residual of plane k-1 without its upper z face (weights of plane k-1)
     if (k >= 2) {
