@@ -283,6 +283,30 @@ def test_fused_cg_update_pre_smoothing_matches_separate(n, case, count):
     print("fused CG update: max |dx| =", float((var[1] - base[1]).abs().max()))
 
 
+@pytest.mark.parametrize("count", [37, 150])
+def test_fused_cg_update_is_repeatable(count):
+    """The fused CG update reads its neighbours' halo rows of r while they update theirs (out of
+    place) and hands planes between warps through shared memory: repeated solves of the same
+    batch must agree bitwise (a race would show up as run-to-run differences)."""
+    pkg = _pkg()
+    from paper_2311_13862_b200 import _native
+    n = 64
+    spec, ospec = _specs((2, 2, 1))
+    prob = pkg.ParametricProblem(spec, levels=pkg.problems.levels_for(n, 4), m0=4)
+    mus = op.sample_mus(ospec, count, seed=61)
+    ctx = pkg.mg_context_for(prob, mus)
+    runs = []
+    for _ in range(3):
+        x, reps = pkg.mgcg_solve(None, prob.rhs(), None, ctx, delta=1e-10, l_max=60)
+        assert _native.load().rbws_batch_cg_fused(ctx.handle) == 1
+        runs.append((x.clone(), [r.iterations for r in reps], np.array([r.history for r in reps], dtype=object)))
+    for x, it, _ in runs[1:]:
+        assert torch.equal(x, runs[0][0])
+        assert it == runs[0][1]
+    del ctx, runs
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("n,case", [(16, (2, 1, 1)), (64, (2, 2, 1)), (64, "smooth"),
                                     (128, (2, 2, 2))])
 def test_direct_p_update_matches_transformed(n, case):
