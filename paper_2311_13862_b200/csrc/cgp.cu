@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(kCgpThreads, kCgpThreads <= 256 ? 2 : 1) cgp_k
   const int j0 = yt * TY, tid = threadIdx.x;
   const int64_t base = (int64_t)mu * N2 * N;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  static_assert(kCgpS <= 8, "the ring barriers occupy the first 64 bytes");
   double* zf = reinterpret_cast<double*>(smem + 64);   // [N + 1][3Q]
   double* ring = zf + (((N + 1) * ZW + 1) & ~1);        // [S][STAGE]
   double* uring = ring + S * STAGE;                     // [2][USZ]
@@ -263,26 +264,10 @@ __global__ void __launch_bounds__(kCgpThreads, kCgpThreads <= 256 ? 2 : 1) cgp_k
 #pragma unroll
   for (int s = 0; s < 2; ++s) xo[s] = PSZ + RSZ + row[s] * N + i;
 
-#pragma unroll kCgpUnroll
-  for (int k = 1; k < N; ++k) {
-    // (1) pre-smoothing residual of plane k-1 without its upper z face (weights of plane k-1)
-    if (k >= 2) {
-      const double* U = uring + ((k - 1) & 1) * USZ;
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const double* P = U + ro[s];
-        const double offx = fma(wxm[s], P[-1], wxp[s] * P[1]);
-        const double offy = fma(wym[s], P[-N], wyp[s] * P[N]);
-        part[s] = fma(1.0 - om, rp[s], (offx + offy) + wzm[s] * ud[s]);
-      }
-    }
-    // (2) weights of plane k
-    refresh(k);
-    // (3) CG update on plane k (own rows + halo row), u(k) = w D^-1 r_new
-    wait(k + 1);
+  // one plane of the CG update (math only): r_new and u = w D^-1 r_new of every slot
+  auto cgmath = [&](int k, double* un, double* rn) {
     const double* SK = ring + (k % S) * STAGE;
     const double* SU = ring + ((k + 1) % S) * STAGE;
-    double un[NS], rn[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       if (s == 2 && !has3) continue;
@@ -297,6 +282,21 @@ __global__ void __launch_bounds__(kCgpThreads, kCgpThreads <= 256 ? 2 : 1) cgp_k
       rn[s] = on[s] ? fma(-al, Au, SK[PSZ + ro[s]]) : 0.0;
       un[s] = on[s] ? wdi[s] * rn[s] : 0.0;
     }
+  };
+  // pre-smoothing residual of plane k-1 without its upper z face (weights of plane k-1)
+  auto prepart = [&](int k) {
+    const double* U = uring + ((k - 1) & 1) * USZ;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const double* P = U + ro[s];
+      const double offx = fma(wxm[s], P[-1], wxp[s] * P[1]);
+      const double offy = fma(wym[s], P[-N], wyp[s] * P[N]);
+      part[s] = fma(1.0 - om, rp[s], (offx + offy) + wzm[s] * ud[s]);
+    }
+  };
+  // results of plane k: u ring, x, r, and r1(k-1) finished with plane k's lower z face
+  auto stores = [&](int k, const double* un, const double* rn) {
+    const double* SK = ring + (k % S) * STAGE;
     double* UK = uring + (k & 1) * USZ;
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
@@ -313,16 +313,13 @@ __global__ void __launch_bounds__(kCgpThreads, kCgpThreads <= 256 ? 2 : 1) cgp_k
       xp[s] += N2;
       rq[s] += N2;
     }
-    // (4) finish r1(k-1): upper z face = plane k's lower face
     if (k >= 2) {
 #pragma unroll
       for (int s = 0; s < 2; ++s)
         rbuf[((k - 1) & 1) * CSZ + row[s] * N + i] = on[s] ? fma(wzm[s], un[s], part[s]) : 0.0;
     }
-    __syncthreads();  // u(k), r1(k-1) visible; plane k's ring slot is free
-    if (tid == 0 && k + S <= N) issue(k + S);
-    // (5) x/z restriction of r1(k-1)
-    if (k >= 2) xz(k - 1);
+  };
+  auto rotate = [&](const double* un, const double* rn) {
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       pd[s] = pc[s];
@@ -334,20 +331,28 @@ __global__ void __launch_bounds__(kCgpThreads, kCgpThreads <= 256 ? 2 : 1) cgp_k
       uc[s] = un[s];
       rp[s] = rn[s];
     }
+  };
+  // (a split arrive / wait CTA barrier that lets the CG math of steady planes run ahead of the
+  // wait measured slower: 2.26 vs 2.04 ms, profiles/r02g_cgp.md)
+#pragma unroll kCgpUnroll
+  for (int k = 1; k < N; ++k) {
+    if (k >= 2) prepart(k);
+    refresh(k);
+    wait(k + 1);
+    double un[NS], rn[NS];
+    cgmath(k, un, rn);
+    stores(k, un, rn);
+    __syncthreads();  // u(k), r1(k-1) visible; plane k's ring slot is free
+    if (tid == 0 && k + S <= N) issue(k + S);
+    if (k >= 2) xz(k - 1);
+    rotate(un, rn);
   }
-  {  // drain: r1(N-1) (u(N) = 0), with the weights of plane N-1
-    const double* U = uring + ((N - 1) & 1) * USZ;
+  prepart(N);  // drain: r1(N-1) (u(N) = 0), with the weights of plane N-1
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const double* P = U + ro[s];
-      const double offx = fma(wxm[s], P[-1], wxp[s] * P[1]);
-      const double offy = fma(wym[s], P[-N], wyp[s] * P[N]);
-      const double v = fma(1.0 - om, rp[s], (offx + offy) + wzm[s] * ud[s]);
-      rbuf[((N - 1) & 1) * CSZ + row[s] * N + i] = on[s] ? v : 0.0;
-    }
-    __syncthreads();
-    xz(N - 1);
-  }
+  for (int s = 0; s < 2; ++s)
+    rbuf[((N - 1) & 1) * CSZ + row[s] * N + i] = on[s] ? part[s] : 0.0;
+  __syncthreads();
+  xz(N - 1);
   __shared__ double red[32];
   const double sred = block_reduce_sum(acc, red);
   if (tid == 0) {
